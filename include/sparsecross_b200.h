@@ -1,0 +1,170 @@
+/*
+ * sparsecross_b200.h -- C ABI of the B200 (sm_100a) sparse cross-encoder hot path.
+ *
+ * Drop-in boundary for the asymmetric windowed self-attention of
+ * arXiv 2312.17649 and the backward-free encoder loop around it.  The
+ * reference (`sparsecross` 0.1.0, pure Python/numpy) has no FFI; each entry
+ * point below replaces the Python function cited beside it
+ * (R/ = /root/reference/pkg/src/sparsecross/).
+ *
+ * Conventions
+ *   - All data pointers are caller-owned DEVICE memory; nothing allocates.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *     every call is stream-ordered and asynchronous.
+ *   - Return 0 (SC_OK) on success; on failure a non-zero SC_ERR_* code and a
+ *     thread-local message readable through sc_last_error().  The Python
+ *     facade maps SC_ERR_INVALID / SC_ERR_NO_VALID_ROW to the reference's
+ *     ValueError subclasses (AttentionError, BandShapeError, EncoderError).
+ *   - Reentrant: concurrent calls on shared read-only inputs are safe.
+ *
+ * Packed varlen layout (new; the reference batches one partition only,
+ * R/encoder.py:461-468):
+ *   cu_seqlens[nseq+1]  int32 prefix of sequence lengths (token rows)
+ *   qgroup_len[nseq]    int32 query-group length m+1 of each sequence
+ *                       (query tokens + its [SEP]); cls group is 1 row,
+ *                       doc group = s - 1 - qgroup_len (R/encoder.py:58-94,
+ *                       R/encoder.py:154-177 span convention)
+ *
+ * Attention pattern = `links[9]`, int32, row-major [src][tgt] over groups
+ * (0 cls, 1 query, 2 doc): SC_LINK_NONE, SC_LINK_FULL or a window w >= 0
+ * (R/attention.py:55-157; FULL = math.inf at R/attention.py:40).
+ */
+#ifndef SPARSECROSS_B200_H
+#define SPARSECROSS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SC_API __attribute__((visibility("default")))
+#else
+#define SC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SC_OK 0
+#define SC_ERR_INVALID 1        /* bad shape/window/pattern argument            */
+#define SC_ERR_CUDA 2           /* CUDA runtime/launch failure                  */
+#define SC_ERR_UNSUPPORTED 3    /* valid request this build does not implement  */
+#define SC_ERR_NO_VALID_ROW 4   /* a row has zero valid keys (R/attention.py:250-251) */
+
+#define SC_LINK_NONE (-2)
+#define SC_LINK_FULL (-1)
+
+#define SC_DTYPE_F32 0
+#define SC_DTYPE_BF16 1
+
+#define SC_PAD_EXCLUDE 0        /* R/attention.py:8-12   */
+#define SC_PAD_ZERO_LOGIT 1     /* R/attention.py:13-16  */
+
+#define SC_ATTN_AUTO 0          /* pick the fastest kernel for the pattern      */
+#define SC_ATTN_GENERIC 1       /* warp-per-row CUDA-core kernel (any pattern)  */
+#define SC_ATTN_BAND_MMA 2      /* tiled band kernel (finite doc window)        */
+
+SC_API const char* sc_last_error(void);
+SC_API int sc_version(void);
+
+/* ---- K1: device index / mask construction ------------------------------ */
+
+/* Per-token sequence id, group id (0/1/2), group-relative index and position
+ * (token index within its sequence), plus a per-sequence prefix of doc-row
+ * tiles of `tile_rows` rows (seq_tile_base[nseq+1]) used by the band kernel
+ * scheduler.  Replaces SubsequencePartition/_split_groups/_locate
+ * (R/encoder.py:58-94, :299-303; R/reference.py:22-27).  qds_every > 0 also
+ * fills tok_flags bit0 for QDS global doc tokens (R/encoder.py:180-193) and
+ * their CSR lists glob_cu[nseq+1]/glob_pos (doc-relative); pass NULLs when 0.
+ * glob_pos must hold at least total_tokens entries. */
+SC_API int sc_index_build(const int32_t* cu_seqlens, const int32_t* qgroup_len, int32_t nseq,
+                   int32_t total_tokens, int32_t tile_rows, int32_t qds_every,
+                   int32_t* tok_seq, int32_t* tok_group, int32_t* tok_rel, int32_t* tok_pos,
+                   int32_t* seq_tile_base, uint8_t* tok_flags, int32_t* glob_cu,
+                   int32_t* glob_pos, void* stream);
+
+/* Dense (s x s) attendability bitmap of sequence `seq` (uint8, 1 = may attend),
+ * exactly the attention kernels' predicate.  Replaces pattern_mask
+ * (R/reference.py:30-57); debug/parity export.  seq_len must equal the
+ * sequence's length (the caller sizes mask_out = seq_len^2 bytes). */
+SC_API int sc_mask_export(const int32_t* cu_seqlens, const int32_t* qgroup_len, int32_t nseq,
+                   int32_t seq, int32_t seq_len, const int32_t* links, const uint8_t* tok_flags,
+                   uint8_t* mask_out, void* stream);
+
+/* Band validity (rows x (2w+1), uint8) -- R/band.py:48-52. */
+SC_API int sc_band_validity(int32_t rows, int32_t window, int32_t target_len, uint8_t* out, void* stream);
+
+/* ---- L1 band kernels ---------------------------------------------------- */
+
+/* out[b, i, j] = q[b, i, :] . k[b, i+j-w, :], 0 where out of range.
+ * q: [batch, s, d], k: [batch, t, d], out: [batch, s, 2w+1] (row-major,
+ * contiguous), all of `dtype`.  Replaces band_scores / band_qk
+ * (R/band.py:154-194, :290-303). */
+SC_API int sc_band_scores(const void* q, const void* k, void* out, int64_t batch, int32_t s,
+                   int32_t t, int32_t d, int32_t window, int32_t dtype, void* stream);
+
+/* out[b, i, :] = sum_j p[b, i, j] v[b, i+j-w, :]; invalid slots never read.
+ * Replaces band_apply / band_pv (R/band.py:197-236, :306-313). */
+SC_API int sc_band_apply(const void* p, const void* v, void* out, int64_t batch, int32_t s,
+                  int32_t t, int32_t d, int32_t window, int32_t dtype, void* stream);
+
+/* ---- K2/K3: fused asymmetric windowed attention ------------------------- */
+
+/* Workspace for sc_attn_fwd (split-softmax partials of full-attention rows). */
+SC_API size_t sc_attn_workspace_bytes(int32_t nseq, int32_t total_tokens, int32_t heads,
+                               int32_t head_dim, int32_t tile_rows);
+
+/* Attention of every token row of a packed batch under one pattern:
+ * all three groups (cls, query, doc) of every sequence in one call.
+ * q/k/v: row r, head h at base + r*row_stride + h*head_dim (elements of
+ * `dtype`); typical packed QKV [T][3][H][d]: k = q + H*d, v = q + 2*H*d,
+ * row_stride = 3*H*d.  out: [T][H][d] with out_row_stride.  scale divides
+ * the logits (sqrt(d) in the encoder, R/encoder.py:329).  tok_* /
+ * seq_tile_base come from sc_index_build with the same tile_rows.
+ * status (optional, device int32) gets bit0 set if a row had zero valid keys.
+ * Replaces group_attention x3 (R/attention.py:416-473), apply_pattern
+ * (:510-537), attend_segments (:290-345), masked_segment_softmax (:228-257)
+ * and the band kernels underneath (R/band.py:154-236). */
+SC_API int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t row_stride,
+                void* out, int64_t out_row_stride,
+                const int32_t* cu_seqlens, const int32_t* qgroup_len, int32_t nseq,
+                int32_t total_tokens, int32_t heads, int32_t head_dim,
+                const int32_t* links, int32_t padding, float scale, int32_t dtype,
+                const int32_t* tok_seq, const int32_t* seq_tile_base, int32_t tile_rows,
+                const uint8_t* tok_flags, const int32_t* glob_cu, const int32_t* glob_pos,
+                int32_t algo, void* workspace, size_t workspace_bytes, int32_t* status,
+                void* stream);
+
+/* ---- Encoder-loop kernels (R/encoder.py:306-371, :475-509) -------------- */
+
+/* x[t] = tok_emb[ids[t]] + pos_emb[tok_pos[t]] (R/encoder.py:483); fp32 out,
+ * optional bf16 copy (xh may be NULL).  emb tables are fp32 [*, hidden]. */
+SC_API int sc_embed(const int32_t* ids, const int32_t* tok_pos, const float* tok_emb,
+             const float* pos_emb, float* x, void* xh, int32_t total_tokens, int32_t hidden,
+             void* stream);
+
+/* x_out = LN(resid + y (+ bias)) * gamma + beta, eps 1e-12, biased variance
+ * (R/encoder.py:267-273 after the residuals at :346 and :353).  resid/x_out
+ * fp32 (may alias); y of y_dtype; bias may be NULL; out_h (bf16) may be NULL. */
+SC_API int sc_residual_layernorm(const float* resid, const void* y, int32_t y_dtype,
+                          const float* bias, const float* gamma, const float* beta,
+                          float* x_out, void* out_h, int32_t rows, int32_t hidden,
+                          void* stream);
+
+/* In-place exact-erf GELU with optional bias (R/encoder.py:258-259). */
+SC_API int sc_bias_gelu(void* x, const float* bias, int32_t dtype, int64_t rows, int32_t cols,
+                 void* stream);
+
+/* score[j] = x[cu_seqlens[j]] . head_w + head_b (R/encoder.py:506). */
+SC_API int sc_cls_score(const float* x, const int32_t* cu_seqlens, int32_t nseq, int32_t hidden,
+                 const float* head_w, float head_b, float* scores, void* stream);
+
+/* Count of rows with a non-finite value in x[rows][cols] (fp32) accumulated
+ * into *count (device int32); the encoder raises NonFiniteActivationError
+ * when non-zero (R/encoder.py:356-357). */
+SC_API int sc_count_nonfinite(const float* x, int64_t n, int32_t* count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSECROSS_B200_H */

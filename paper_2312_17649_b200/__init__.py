@@ -1,0 +1,43 @@
+"""B200-native hot path of the sparse cross-encoder (arXiv 2312.17649).
+
+Drop-in for the reference package's attention module and encoder forward
+(``sparsecross.attention`` / ``sparsecross.encoder``): same names, argument
+meaning and error classes, computed by sm_100a CUDA kernels behind the C ABI
+in ``include/sparsecross_b200.h``.  No CPU fallback exists.
+"""
+
+from .attention import (
+    FULL,
+    GROUPS,
+    PADDING_MODES,
+    AttentionError,
+    AttentionPattern,
+    apply_pattern,
+    attend_packed,
+    full_pattern,
+    group_attention,
+    longformer_pattern,
+    make_pattern,
+    qds_pattern,
+    sparse_pattern,
+)
+from .band import BandShapeError, band_apply, band_pv, band_qk, band_scores, band_validity
+from .encoder import (
+    CrossEncoder,
+    EncoderConfig,
+    EncoderError,
+    NonFiniteActivationError,
+    PackedBatch,
+    SubsequencePartition,
+    TokenSequence,
+    assemble_input,
+    encoder_forward,
+    init_weights,
+    interpolate_positions,
+    qds_global_positions,
+    relevance_score,
+    resolve_pattern,
+)
+from .layout import PackedLayout
+
+__version__ = "0.1.0"

@@ -1,0 +1,290 @@
+"""Attention patterns and the fused windowed cross-attention on B200.
+
+Mirrors the reference module ``sparsecross.attention`` (R/attention.py):
+the same pattern objects, names, error class and argument meaning, with the
+computation done by the sm_100a kernels behind ``sc_attn_fwd``.
+
+* ``AttentionPattern`` / ``make_pattern`` / ``*_pattern`` -- R/attention.py:55-157
+* ``attend_packed``  -- NEW packed varlen entry point used by the encoder:
+  all groups of all sequences of a packed batch in one kernel call.
+* ``group_attention`` / ``apply_pattern`` / ``windowed_cross_attention`` /
+  ``full_attention`` -- compatibility shims with the reference signatures
+  (R/attention.py:276-287, :381-400, :416-473, :510-537); inputs may be torch
+  CUDA tensors or numpy arrays (uploaded; returned as numpy).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .layout import PackedLayout
+
+FULL = math.inf                                  # R/attention.py:40
+GROUPS = ("cls", "query", "doc")                 # R/attention.py:42
+PADDING_MODES = ("exclude", "zero-logit")        # R/attention.py:44
+
+
+class AttentionError(ValueError):
+    """Malformed segment tuples, rows without valid targets, or bad patterns (R/attention.py:47-48)."""
+
+
+def is_full(window) -> bool:
+    return window == FULL
+
+
+@dataclass(frozen=True)
+class AttentionPattern:
+    """Per-group targets: source group -> ((target group, window), ...) (R/attention.py:55-89)."""
+
+    name: str
+    targets: dict
+    global_positions: tuple = ()
+
+    def __post_init__(self):
+        for source, tlist in self.targets.items():
+            if source not in GROUPS:
+                raise AttentionError(f"unknown source group {source!r}")
+            seen = [t for t, _ in tlist]
+            if len(set(seen)) != len(seen):
+                raise AttentionError(f"duplicate target group for source {source!r}")
+            for target, window in tlist:
+                if target not in GROUPS:
+                    raise AttentionError(f"unknown target group {target!r}")
+                if not is_full(window) and (int(window) != window or window < 0):
+                    raise AttentionError(f"bad window {window!r} for {source}->{target}")
+        if any(p < 0 for p in self.global_positions):
+            raise AttentionError("global positions must be non-negative")
+        if self.global_positions and self.name != "qds":
+            raise AttentionError("global positions are only meaningful for the qds pattern")
+
+    def targets_of(self, source: str):
+        try:
+            return self.targets[source]
+        except KeyError:
+            raise AttentionError(f"pattern {self.name!r} has no targets for group {source!r}")
+
+    def links(self) -> np.ndarray:
+        """int32[9] link table [src][tgt]: -2 none, -1 full, else the window (sc_attn_fwd ABI)."""
+        out = np.full(9, _lib.LINK_NONE, dtype=np.int32)
+        for si, src in enumerate(GROUPS):
+            for tgt, w in self.targets.get(src, ()):
+                out[si * 3 + GROUPS.index(tgt)] = _lib.LINK_FULL if is_full(w) else int(w)
+        return out
+
+
+_EVERY = (("cls", FULL), ("query", FULL), ("doc", FULL))
+
+
+def full_pattern() -> AttentionPattern:
+    return AttentionPattern("full", {g: _EVERY for g in GROUPS})
+
+
+def longformer_pattern(window) -> AttentionPattern:
+    return AttentionPattern("longformer", {"cls": _EVERY, "query": _EVERY,
+                                           "doc": (("cls", FULL), ("query", FULL), ("doc", window))})
+
+
+def qds_pattern(window, global_positions=()) -> AttentionPattern:
+    return AttentionPattern("qds", {"cls": _EVERY, "query": _EVERY,
+                                    "doc": (("cls", FULL), ("query", FULL), ("doc", window))},
+                            global_positions=tuple(int(p) for p in global_positions))
+
+
+def sparse_pattern(window) -> AttentionPattern:
+    """Asymmetric pattern of Eqs. 1-3: query tokens attend only to query tokens."""
+    return AttentionPattern("sparse", {"cls": _EVERY, "query": (("query", FULL),),
+                                       "doc": (("cls", FULL), ("query", FULL), ("doc", window))})
+
+
+PATTERN_FACTORIES = {
+    "full": lambda window, globals_=(): full_pattern(),
+    "longformer": lambda window, globals_=(): longformer_pattern(window),
+    "qds": lambda window, globals_=(): qds_pattern(window, globals_),
+    "sparse": lambda window, globals_=(): sparse_pattern(window),
+}
+
+
+def make_pattern(name: str, window, global_positions=()) -> AttentionPattern:
+    try:
+        factory = PATTERN_FACTORIES[name]
+    except KeyError:
+        raise AttentionError(f"unknown pattern {name!r}; expected one of {sorted(PATTERN_FACTORIES)}")
+    return factory(window, global_positions)
+
+
+# ---------------------------------------------------------------------------
+# Host-side validation (no device sync): rows with zero valid keys raise like
+# masked_segment_softmax does (R/attention.py:250-251).
+# ---------------------------------------------------------------------------
+
+def check_rows_have_keys(pattern: AttentionPattern, group_lens: np.ndarray, padding: str,
+                         has_globals: bool = False) -> None:
+    """group_lens: int array (nseq, 3).  Raises AttentionError if any row has no valid key."""
+    for si, src in enumerate(GROUPS):
+        tl = pattern.targets.get(src, ())
+        if not tl:
+            raise AttentionError(f"pattern {pattern.name!r} has no targets for group {src!r}")
+        if any(is_full(w) for _, w in tl):
+            continue
+        if padding == "zero-logit" or (has_globals and src == "doc"):
+            continue
+        # Windowed only: row i has a key iff i < len_t + w for some target.
+        reach = np.max(np.stack([group_lens[:, GROUPS.index(t)] + int(w) for t, w in tl]), axis=0)
+        if np.any(group_lens[:, si] > reach):
+            raise AttentionError("a row has zero valid entries across all segments")
+
+
+# ---------------------------------------------------------------------------
+# Packed varlen entry point.
+# ---------------------------------------------------------------------------
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return _lib.DTYPE_F32
+    if t.dtype == torch.bfloat16:
+        return _lib.DTYPE_BF16
+    raise AttentionError(f"unsupported dtype {t.dtype}; expected float32 or bfloat16")
+
+
+def attend_packed(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: PackedLayout,
+                  pattern: AttentionPattern, heads: int, scale: float | None = None,
+                  padding: str = "exclude", out: torch.Tensor | None = None,
+                  algo: str = "auto", check: bool = True) -> torch.Tensor:
+    """Pattern attention over every row of a packed batch (all groups, all sequences).
+
+    q/k/v: [T, >=heads*d] views sharing a row stride (e.g. the thirds of a
+    packed QKV projection [T, 3*heads*d]).  Returns out [T, heads*d].
+    """
+    if padding not in PADDING_MODES:
+        raise AttentionError(f"unknown padding mode {padding!r}")
+    T = layout.total_tokens
+    if q.dim() != 2 or q.shape[0] != T:
+        raise AttentionError(f"q must be [T={T}, heads*d], got {tuple(q.shape)}")
+    hd = q.shape[1]
+    if hd % heads:
+        raise AttentionError("q width not divisible by heads")
+    d = hd // heads
+    if not (q.stride(1) == k.stride(1) == v.stride(1) == 1) or not (q.stride(0) == k.stride(0) == v.stride(0)):
+        raise AttentionError("q/k/v must share a row stride with unit column stride")
+    if scale is None:
+        scale = math.sqrt(d)
+    if scale <= 0:
+        raise AttentionError(f"scale must be positive, got {scale}")
+    qds = pattern.name == "qds" and layout.tok_flags is not None
+    if pattern.global_positions and not qds:
+        raise AttentionError("QDS globals need a layout built with qds globals")
+    if check:
+        check_rows_have_keys(pattern, layout.group_lens_host, padding, qds)
+    dt = _dtype_code(q)
+    if out is None:
+        out = torch.empty((T, hd), dtype=q.dtype, device=q.device)
+    algo_code = {"auto": _lib.ALGO_AUTO, "generic": _lib.ALGO_GENERIC, "band": _lib.ALGO_BAND_MMA}[algo]
+    ws = layout.attn_workspace(heads, d)
+    links = pattern.links()
+    _lib.call(
+        "sc_attn_fwd",
+        q.data_ptr(), k.data_ptr(), v.data_ptr(), q.stride(0), out.data_ptr(), out.stride(0),
+        layout.cu_seqlens.data_ptr(), layout.qgroup_len.data_ptr(), layout.nseq, T, heads, d,
+        links.ctypes.data, _lib.PAD_EXCLUDE if padding == "exclude" else _lib.PAD_ZERO_LOGIT,
+        float(scale), dt, layout.tok_seq.data_ptr(), layout.seq_tile_base.data_ptr(), layout.tile_rows,
+        _lib.ptr(layout.tok_flags) if qds else None, _lib.ptr(layout.glob_cu) if qds else None,
+        _lib.ptr(layout.glob_pos) if qds else None, algo_code,
+        _lib.ptr(ws), 0 if ws is None else ws.numel(), None, _lib.stream_handle(),
+        exc=AttentionError,
+    )
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Reference-signature compatibility shims (one partition shared by all leading dims).
+# ---------------------------------------------------------------------------
+
+def _to_device(x):
+    if isinstance(x, torch.Tensor):
+        return x, False
+    arr = np.asarray(x)
+    return torch.from_numpy(np.ascontiguousarray(arr)).cuda(), True
+
+
+def _compute_dtype(t: torch.Tensor):
+    return t if t.dtype in (torch.float32, torch.bfloat16) else t.float()
+
+
+def _run_groups(qkv: dict, pattern: AttentionPattern, scale: float, padding: str):
+    """Pack the three groups of (Q, K, V) views, run the kernel, return per-group outputs."""
+    for g in GROUPS:
+        if g not in qkv:
+            raise AttentionError(f"pattern references absent group {g!r}")
+    mats, was_np, orig_dtype = [], False, None
+    for g in GROUPS:
+        trip = []
+        for x in qkv[g]:
+            t, from_np = _to_device(x)
+            was_np |= from_np
+            orig_dtype = orig_dtype or t.dtype
+            trip.append(t)
+        mats.append(trip)
+    lead = mats[0][0].shape[:-2]
+    d = mats[0][0].shape[-1]
+    lens = [m[0].shape[-2] for m in mats]
+    for g, m in zip(GROUPS, mats):
+        for t in m:
+            if t.shape[:-2] != lead or t.shape[-1] != d:
+                raise AttentionError(f"incompatible shapes in group {g!r}")
+        if m[1].shape[-2] != m[2].shape[-2] or m[0].shape[-2] != m[1].shape[-2]:
+            raise AttentionError("key/value row counts differ")
+    if lens[0] != 1:
+        raise AttentionError("the cls group must have exactly one row")
+    H = int(np.prod(lead)) if len(lead) else 1
+    s = sum(lens)
+    cat = []
+    for which in range(3):
+        x = torch.cat([_compute_dtype(m[which]) for m in mats], dim=-2)   # (*lead, s, d)
+        x = x.reshape(H, s, d).permute(1, 0, 2).contiguous().reshape(s, H * d)
+        cat.append(x)
+    dtype = cat[0].dtype
+    cat = [c.to(dtype) for c in cat]
+    layout = PackedLayout.from_lengths([s], [lens[1]], device=cat[0].device,
+                                       qds_positions=[pattern.global_positions] if pattern.global_positions else None)
+    if pattern.global_positions and max(pattern.global_positions) >= lens[2]:
+        raise AttentionError("global positions outside the document group")
+    out = attend_packed(cat[0], cat[1], cat[2], layout, pattern, H, scale, padding)
+    out = out.reshape(s, H, d).permute(1, 0, 2).reshape(*lead, s, d) if len(lead) else out.reshape(s, d)
+    outs, lo = [], 0
+    for n in lens:
+        o = out[..., lo:lo + n, :]
+        if was_np:
+            o = o.float().cpu().numpy().astype(np.dtype(str(orig_dtype).replace("torch.", "")), copy=False)
+        outs.append(o)
+        lo += n
+    return outs
+
+
+def group_attention(qkv: dict, source: str, pattern: AttentionPattern, scale: float,
+                    padding: str = "exclude"):
+    """Output of one source group under a pattern (R/attention.py:416-473)."""
+    if source not in GROUPS:
+        raise AttentionError(f"unknown source group {source!r}")
+    pattern.targets_of(source)
+    return _run_groups(qkv, pattern, scale, padding)[GROUPS.index(source)]
+
+
+def apply_pattern(partition, qkv: dict, pattern: AttentionPattern, scale: float | None = None,
+                  padding: str = "exclude"):
+    """(O_cls, O_query, O_doc) for all groups (R/attention.py:510-537)."""
+    for g in GROUPS:
+        if g not in qkv:
+            raise AttentionError(f"missing Q/K/V for group {g!r}")
+    if partition is not None:
+        for g in GROUPS:
+            if qkv[g][0].shape[-2] != partition.group_len(g):
+                raise AttentionError(f"group {g!r} queries have {qkv[g][0].shape[-2]} rows, "
+                                     f"partition says {partition.group_len(g)}")
+    if scale is None:
+        scale = math.sqrt(qkv["cls"][0].shape[-1])
+    return tuple(_run_groups(qkv, pattern, scale, padding))

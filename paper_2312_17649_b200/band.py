@@ -1,0 +1,94 @@
+"""Band-matrix kernels ⊡_w / ⊙_w on device (R/band.py).
+
+Band storage is (rows, 2w+1): slot j of row i addresses target row i+j-w and
+is valid iff 0 <= i+j-w < target_len (R/band.py:48-52).  These wrap the
+standalone ``sc_band_scores`` / ``sc_band_apply`` kernels; the encoder never
+materialises bands (the fused attention kernels fold them into the softmax).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+class BandShapeError(ValueError):
+    """Band/dense operands have inconsistent shapes (R/band.py:31-32)."""
+
+
+def _check_window(window) -> int:
+    if not isinstance(window, (int, np.integer)) or window < 0:
+        raise BandShapeError(f"window must be a non-negative integer, got {window!r}")
+    return int(window)
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return _lib.DTYPE_F32
+    if t.dtype == torch.bfloat16:
+        return _lib.DTYPE_BF16
+    raise BandShapeError(f"unsupported dtype {t.dtype}")
+
+
+def band_validity(seq_len: int, window: int, target_len: int, device="cuda") -> torch.Tensor:
+    """Bool (seq_len, 2w+1) validity mask computed on device (R/band.py:48-52)."""
+    w = _check_window(window)
+    out = torch.empty((seq_len, 2 * w + 1), dtype=torch.uint8, device=device)
+    _lib.call("sc_band_validity", seq_len, w, target_len, out.data_ptr(), _lib.stream_handle(),
+              exc=BandShapeError)
+    return out.bool()
+
+
+def _flatten(a: torch.Tensor, b: torch.Tensor):
+    lead = torch.broadcast_shapes(a.shape[:-2], b.shape[:-2])
+    a = a.expand(*lead, *a.shape[-2:]).reshape(-1, *a.shape[-2:]).contiguous()
+    b = b.expand(*lead, *b.shape[-2:]).reshape(-1, *b.shape[-2:]).contiguous()
+    return lead, a, b
+
+
+def band_scores(q: torch.Tensor, k: torch.Tensor, window: int) -> torch.Tensor:
+    """out[..., i, j] = q[..., i, :] . k[..., i+j-w, :]; 0 out of range (R/band.py:154-177)."""
+    w = _check_window(window)
+    if q.shape[-1] != k.shape[-1]:
+        raise BandShapeError(f"feature dims differ: q has {q.shape[-1]}, k has {k.shape[-1]}")
+    if q.dtype != k.dtype:
+        raise BandShapeError("q and k dtypes differ")
+    lead, qf, kf = _flatten(q, k)
+    B, s, d = qf.shape
+    t = kf.shape[1]
+    out = torch.empty((B, s, 2 * w + 1), dtype=q.dtype, device=q.device)
+    _lib.call("sc_band_scores", qf.data_ptr(), kf.data_ptr(), out.data_ptr(), B, s, t, d, w, _dt(qf),
+              _lib.stream_handle(), exc=BandShapeError)
+    return out.reshape(*lead, s, 2 * w + 1)
+
+
+def band_apply(p: torch.Tensor, v: torch.Tensor, window: int) -> torch.Tensor:
+    """out[..., i, :] = sum_j p[..., i, j] v[..., i+j-w, :]; invalid slots ignored (R/band.py:197-218)."""
+    w = _check_window(window)
+    if p.shape[-1] != 2 * w + 1:
+        raise BandShapeError(f"band width {p.shape[-1]} inconsistent with window {w}")
+    if p.dtype != v.dtype:
+        raise BandShapeError("p and v dtypes differ")
+    lead, pf, vf = _flatten(p, v)
+    B, s, _ = pf.shape
+    t, d = vf.shape[1], vf.shape[2]
+    out = torch.empty((B, s, d), dtype=v.dtype, device=v.device)
+    _lib.call("sc_band_apply", pf.data_ptr(), vf.data_ptr(), out.data_ptr(), B, s, t, d, w, _dt(pf),
+              _lib.stream_handle(), exc=BandShapeError)
+    return out.reshape(*lead, s, d)
+
+
+def band_qk(q: torch.Tensor, k: torch.Tensor, window: int) -> torch.Tensor:
+    """2-D windowed query-key product (R/band.py:290-303); returns the (s, 2w+1) band data."""
+    if q.dim() != 2 or k.dim() != 2:
+        raise BandShapeError("Q and K must be 2-D")
+    return band_scores(q, k, window)
+
+
+def band_pv(p: torch.Tensor, v: torch.Tensor, window: int) -> torch.Tensor:
+    """2-D band-probability-value product (R/band.py:306-313)."""
+    if p.dim() != 2 or v.dim() != 2:
+        raise BandShapeError("P and V must be 2-D")
+    return band_apply(p, v, window)

@@ -1,0 +1,47 @@
+// sc_attn_fwd: argument validation and kernel dispatch for the fused
+// asymmetric windowed attention (R/attention.py:416-537).
+#include "attn.cuh"
+
+using namespace sc;
+
+extern "C" size_t sc_attn_workspace_bytes(int32_t nseq, int32_t total_tokens, int32_t heads,
+                                          int32_t head_dim, int32_t tile_rows) {
+  return band_workspace_bytes(nseq, total_tokens, heads, head_dim, tile_rows);
+}
+
+extern "C" int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t row_stride,
+                           void* out, int64_t out_row_stride, const int32_t* cu_seqlens,
+                           const int32_t* qgroup_len, int32_t nseq, int32_t total_tokens,
+                           int32_t heads, int32_t head_dim, const int32_t* links, int32_t padding,
+                           float scale, int32_t dtype, const int32_t* tok_seq,
+                           const int32_t* seq_tile_base, int32_t tile_rows,
+                           const uint8_t* tok_flags, const int32_t* glob_cu,
+                           const int32_t* glob_pos, int32_t algo, void* workspace,
+                           size_t workspace_bytes, int32_t* status, void* stream) {
+  AttnArgs a;
+  SC_CHECK_ARG(load_links(links, &a.links), "sc_attn_fwd: bad links");
+  SC_CHECK_ARG(q && k && v && out && cu_seqlens && qgroup_len, "sc_attn_fwd: null pointer");
+  SC_CHECK_ARG(nseq >= 1 && total_tokens >= 3 * nseq, "sc_attn_fwd: bad nseq/total_tokens");
+  SC_CHECK_ARG(heads >= 1 && head_dim >= 1 && head_dim <= 128, "sc_attn_fwd: head_dim must be in [1,128]");
+  SC_CHECK_ARG(row_stride >= (int64_t)heads * head_dim && out_row_stride >= (int64_t)heads * head_dim,
+               "sc_attn_fwd: row strides smaller than heads*head_dim");
+  SC_CHECK_ARG(padding == SC_PAD_EXCLUDE || padding == SC_PAD_ZERO_LOGIT, "unknown padding mode %d", padding);
+  SC_CHECK_ARG(scale > 0.f, "scale must be positive, got %g", (double)scale);
+  SC_CHECK_ARG(dtype == SC_DTYPE_F32 || dtype == SC_DTYPE_BF16, "sc_attn_fwd: bad dtype %d", dtype);
+  SC_CHECK_ARG((glob_cu == nullptr) == (glob_pos == nullptr), "sc_attn_fwd: glob_cu/glob_pos must be both set or both NULL");
+  SC_CHECK_ARG(glob_cu == nullptr || tok_flags != nullptr, "sc_attn_fwd: QDS globals need tok_flags");
+  a.q = q; a.k = k; a.v = v; a.ld = row_stride; a.out = out; a.ld_out = out_row_stride;
+  a.cu = cu_seqlens; a.qlen = qgroup_len; a.nseq = nseq; a.T = total_tokens; a.H = heads;
+  a.d = head_dim; a.padding = padding; a.scale = scale; a.flags = tok_flags; a.glob_cu = glob_cu;
+  a.glob_pos = glob_pos; a.status = status; a.row_begin = 0; a.row_end = total_tokens;
+  a.only_group = -1;
+  cudaStream_t st = (cudaStream_t)stream;
+  SC_CHECK_ARG(algo == SC_ATTN_AUTO || algo == SC_ATTN_GENERIC || algo == SC_ATTN_BAND_MMA,
+               "sc_attn_fwd: bad algo %d", algo);
+  if (algo != SC_ATTN_GENERIC) {
+    int rc = launch_attn_band(a, dtype, tok_seq, seq_tile_base, tile_rows, workspace,
+                              workspace_bytes, st);
+    if (rc != SC_ERR_UNSUPPORTED || algo == SC_ATTN_BAND_MMA) return rc;
+  }
+  return launch_attn_generic(a, dtype, st);
+}

@@ -1,0 +1,256 @@
+// Encoder-loop kernels around the attention (R/encoder.py:306-371, :475-509):
+// embedding gather + per-sequence positions, residual + LayerNorm (eps 1e-12),
+// bias + exact-erf GELU, [CLS] relevance head, non-finite detection.
+#include "common.cuh"
+
+namespace sc {
+
+constexpr float kLnEps = 1e-12f;  // R/encoder.py:41
+
+// Grid-stride launch size: enough CTAs for `per_sm` waves of 256 threads over 148 SMs.
+static inline unsigned grid_cap(int64_t n, int per_sm) {
+  int64_t b = (n + 255) / 256, cap = 148LL * per_sm;
+  return (unsigned)(b < cap ? b : cap);
+}
+
+__global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __restrict__ pos,
+                             const float* __restrict__ tok, const float* __restrict__ pe,
+                             float* __restrict__ x, __nv_bfloat16* __restrict__ xh, int T, int h) {
+  int r = blockIdx.x;
+  if (r >= T) return;
+  const float* a = tok + (int64_t)__ldg(ids + r) * h;
+  const float* b = pe + (int64_t)__ldg(pos + r) * h;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) {
+    float v = __ldg(a + c) + __ldg(b + c);
+    x[(int64_t)r * h + c] = v;
+    if (xh) xh[(int64_t)r * h + c] = __float2bfloat16_rn(v);
+  }
+}
+
+// One warp per row, row cached in registers (h <= 32 * kPer).
+template <typename Y, int kPer>
+__global__ void residual_ln_kernel(const float* __restrict__ resid, const Y* __restrict__ y,
+                                   const float* __restrict__ bias, const float* __restrict__ gamma,
+                                   const float* __restrict__ beta, float* __restrict__ out,
+                                   __nv_bfloat16* __restrict__ out_h, int rows, int h) {
+  int lane = threadIdx.x & 31;
+  int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const float* rr = resid + (int64_t)r * h;
+  const Y* yr = y + (int64_t)r * h;
+  float v[kPer];
+  float sum = 0.f;
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    int c = lane + 32 * e;
+    v[e] = 0.f;
+    if (c < h) {
+      float t = to_f32(yr[c]);
+      if (bias) t += __ldg(bias + c);
+      v[e] = rr[c] + t;
+      sum += v[e];
+    }
+  }
+  float mu = warp_sum(sum) / (float)h;
+  float sq = 0.f;
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    int c = lane + 32 * e;
+    if (c < h) {
+      v[e] -= mu;
+      sq = fmaf(v[e], v[e], sq);
+    }
+  }
+  float var = warp_sum(sq) / (float)h;
+  float inv = 1.f / sqrtf(var + kLnEps);
+  float* orow = out + (int64_t)r * h;
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    int c = lane + 32 * e;
+    if (c < h) {
+      float o = __ldg(gamma + c) * (v[e] * inv) + __ldg(beta + c);
+      orow[c] = o;
+      if (out_h) out_h[(int64_t)r * h + c] = __float2bfloat16_rn(o);
+    }
+  }
+}
+
+// Large-h fallback: block per row, three passes through L1/L2.
+template <typename Y>
+__global__ void residual_ln_big_kernel(const float* __restrict__ resid, const Y* __restrict__ y,
+                                       const float* __restrict__ bias, const float* __restrict__ gamma,
+                                       const float* __restrict__ beta, float* __restrict__ out,
+                                       __nv_bfloat16* __restrict__ out_h, int rows, int h) {
+  __shared__ float red[32];
+  int r = blockIdx.x;
+  const float* rr = resid + (int64_t)r * h;
+  const Y* yr = y + (int64_t)r * h;
+  auto val = [&](int c) { return rr[c] + to_f32(yr[c]) + (bias ? bias[c] : 0.f); };
+  auto block_sum = [&](float s) {
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    __syncthreads();
+    return t;
+  };
+  float s = 0.f;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) s += val(c);
+  float mu = block_sum(s) / (float)h;
+  float q = 0.f;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) { float t = val(c) - mu; q = fmaf(t, t, q); }
+  float inv = 1.f / sqrtf(block_sum(q) / (float)h + kLnEps);
+  __syncthreads();
+  for (int c = threadIdx.x; c < h; c += blockDim.x) {
+    float o = gamma[c] * ((val(c) - mu) * inv) + beta[c];
+    out[(int64_t)r * h + c] = o;
+    if (out_h) out_h[(int64_t)r * h + c] = __float2bfloat16_rn(o);
+  }
+}
+
+__device__ __forceinline__ float gelu_erf(float x) {
+  return 0.5f * x * (1.f + erff(x * 0.70710678118654752440f));
+}
+
+template <typename T>
+__global__ void bias_gelu_kernel(T* __restrict__ x, const float* __restrict__ bias, int64_t n,
+                                 int cols) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float v = to_f32(x[i]);
+    if (bias) v += __ldg(bias + (int)(i % cols));
+    x[i] = from_f32<T>(gelu_erf(v));
+  }
+}
+
+// bf16, 8 elements per thread, cols % 8 == 0.
+__global__ void bias_gelu_bf16x8_kernel(__nv_bfloat16* __restrict__ x, const float* __restrict__ bias,
+                                        int64_t n8, int cols) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  uint4* xv = reinterpret_cast<uint4*>(x);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride) {
+    uint4 u = xv[i];
+    __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&u);
+    int c0 = (int)((i * 8) % cols);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = __bfloat1622float2(b[e]);
+      if (bias) { f.x += __ldg(bias + c0 + 2 * e); f.y += __ldg(bias + c0 + 2 * e + 1); }
+      b[e] = __floats2bfloat162_rn(gelu_erf(f.x), gelu_erf(f.y));
+    }
+    xv[i] = u;
+  }
+}
+
+__global__ void cls_score_kernel(const float* __restrict__ x, const int32_t* __restrict__ cu, int nseq,
+                                 int h, const float* __restrict__ w, float b, float* __restrict__ out) {
+  int lane = threadIdx.x & 31;
+  int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= nseq) return;
+  const float* xr = x + (int64_t)cu[j] * h;
+  float s = 0.f;
+  for (int c = lane; c < h; c += 32) s = fmaf(xr[c], w[c], s);
+  s = warp_sum(s);
+  if (lane == 0) out[j] = s + b;
+}
+
+__global__ void nonfinite_kernel(const float* __restrict__ x, int64_t n, int32_t* __restrict__ count) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    bad |= !isfinite(x[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicAdd(count, 1);
+}
+
+template <typename Y>
+int launch_ln(const float* resid, const void* y, const float* bias, const float* gamma,
+              const float* beta, float* out, void* out_h, int rows, int h, cudaStream_t st) {
+  const Y* yy = static_cast<const Y*>(y);
+  __nv_bfloat16* oh = static_cast<__nv_bfloat16*>(out_h);
+  unsigned blocks = (unsigned)((rows + 7) / 8);
+  int per = (h + 31) / 32;
+  if (per <= 1) residual_ln_kernel<Y, 1><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  else if (per <= 4) residual_ln_kernel<Y, 4><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  else if (per <= 8) residual_ln_kernel<Y, 8><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  else if (per <= 24) residual_ln_kernel<Y, 24><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  else if (per <= 32) residual_ln_kernel<Y, 32><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  else residual_ln_big_kernel<Y><<<rows, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  SC_CHECK_LAUNCH("residual_ln_kernel");
+  return SC_OK;
+}
+
+}  // namespace sc
+
+using namespace sc;
+
+extern "C" int sc_embed(const int32_t* ids, const int32_t* tok_pos, const float* tok_emb,
+                        const float* pos_emb, float* x, void* xh, int32_t total_tokens,
+                        int32_t hidden, void* stream) {
+  SC_CHECK_ARG(ids && tok_pos && tok_emb && pos_emb && x, "sc_embed: null pointer");
+  SC_CHECK_ARG(total_tokens >= 0 && hidden >= 1, "sc_embed: bad shape");
+  if (total_tokens == 0) return SC_OK;
+  int threads = hidden >= 256 ? 256 : 32 * ((hidden + 31) / 32);
+  embed_kernel<<<total_tokens, threads, 0, (cudaStream_t)stream>>>(
+      ids, tok_pos, tok_emb, pos_emb, x, (__nv_bfloat16*)xh, total_tokens, hidden);
+  SC_CHECK_LAUNCH("embed_kernel");
+  return SC_OK;
+}
+
+extern "C" int sc_residual_layernorm(const float* resid, const void* y, int32_t y_dtype,
+                                     const float* bias, const float* gamma, const float* beta,
+                                     float* x_out, void* out_h, int32_t rows, int32_t hidden,
+                                     void* stream) {
+  SC_CHECK_ARG(resid && y && gamma && beta && x_out, "sc_residual_layernorm: null pointer");
+  SC_CHECK_ARG(rows >= 0 && hidden >= 1, "sc_residual_layernorm: bad shape");
+  if (rows == 0) return SC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (y_dtype == SC_DTYPE_F32) return launch_ln<float>(resid, y, bias, gamma, beta, x_out, out_h, rows, hidden, st);
+  if (y_dtype == SC_DTYPE_BF16) return launch_ln<__nv_bfloat16>(resid, y, bias, gamma, beta, x_out, out_h, rows, hidden, st);
+  set_error("sc_residual_layernorm: bad dtype %d", y_dtype);
+  return SC_ERR_INVALID;
+}
+
+extern "C" int sc_bias_gelu(void* x, const float* bias, int32_t dtype, int64_t rows, int32_t cols,
+                            void* stream) {
+  SC_CHECK_ARG(x && rows >= 0 && cols >= 1, "sc_bias_gelu: bad arguments");
+  int64_t n = rows * cols;
+  if (n == 0) return SC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SC_DTYPE_BF16 && cols % 8 == 0 && ((uintptr_t)x & 15) == 0) {
+    int64_t n8 = n / 8;
+    unsigned blocks = grid_cap(n8, 16);
+    bias_gelu_bf16x8_kernel<<<blocks, 256, 0, st>>>((__nv_bfloat16*)x, bias, n8, cols);
+  } else if (dtype == SC_DTYPE_BF16) {
+    unsigned blocks = grid_cap(n, 16);
+    bias_gelu_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((__nv_bfloat16*)x, bias, n, cols);
+  } else if (dtype == SC_DTYPE_F32) {
+    unsigned blocks = grid_cap(n, 16);
+    bias_gelu_kernel<float><<<blocks, 256, 0, st>>>((float*)x, bias, n, cols);
+  } else {
+    set_error("sc_bias_gelu: bad dtype %d", dtype);
+    return SC_ERR_INVALID;
+  }
+  SC_CHECK_LAUNCH("bias_gelu_kernel");
+  return SC_OK;
+}
+
+extern "C" int sc_cls_score(const float* x, const int32_t* cu_seqlens, int32_t nseq, int32_t hidden,
+                            const float* head_w, float head_b, float* scores, void* stream) {
+  SC_CHECK_ARG(x && cu_seqlens && head_w && scores && nseq >= 0 && hidden >= 1,
+               "sc_cls_score: bad arguments");
+  if (nseq == 0) return SC_OK;
+  cls_score_kernel<<<(nseq + 7) / 8, 256, 0, (cudaStream_t)stream>>>(x, cu_seqlens, nseq, hidden,
+                                                                      head_w, head_b, scores);
+  SC_CHECK_LAUNCH("cls_score_kernel");
+  return SC_OK;
+}
+
+extern "C" int sc_count_nonfinite(const float* x, int64_t n, int32_t* count, void* stream) {
+  SC_CHECK_ARG(x && count && n >= 0, "sc_count_nonfinite: bad arguments");
+  if (n == 0) return SC_OK;
+  unsigned blocks = grid_cap(n, 8);
+  nonfinite_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(x, n, count);
+  SC_CHECK_LAUNCH("nonfinite_kernel");
+  return SC_OK;
+}

@@ -1,0 +1,464 @@
+"""Backward-free cross-encoder inference on B200 (R/encoder.py).
+
+Same public surface as the reference encoder -- ``EncoderConfig``,
+``SubsequencePartition``, ``TokenSequence``, ``assemble_input``,
+``init_weights``, ``CrossEncoder.forward/score/score_pair`` -- plus a packed
+varlen path (``PackedBatch``, ``CrossEncoder.score_packed``) that scores
+many (query, document) pairs of different lengths in one pass.
+
+Per layer (post-LN BERT, R/encoder.py:306-371):
+    qkv = x @ [Wq|Wk|Wv] + b          cuBLAS (bf16, or fp32 with TF32 off)
+    o   = attention(qkv)              sc_attn_fwd (sm_100a kernels)
+    x1  = LN(x + o @ Wo + bo)         cuBLAS + sc_residual_layernorm
+    f   = gelu_erf(x1 @ W1 + b1)      cuBLAS + sc_bias_gelu
+    x   = LN(x1 + f @ W2 + b2)        cuBLAS + sc_residual_layernorm
+The residual stream stays fp32 in both precisions; bf16 mode feeds bf16
+copies to the GEMMs and the attention.
+"""
+
+from __future__ import annotations
+
+import math
+from contextlib import contextmanager
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from . import _lib
+from .attention import FULL, GROUPS, AttentionError, attend_packed, is_full, make_pattern
+from .layout import PackedLayout
+from .tokenizer import CLS_ID, NUM_SPECIAL_TOKENS, SEP_ID
+
+LAYER_NORM_EPS = 1e-12                         # R/encoder.py:41
+PRECISIONS = ("bf16", "f32", "f64")            # f64 configs compute in fp32 on the GPU
+
+
+class EncoderError(ValueError):
+    """Malformed configs, partitions, or inputs (R/encoder.py:46-47)."""
+
+
+class NonFiniteActivationError(FloatingPointError):
+    """A layer produced NaN or infinite activations (R/encoder.py:50-55)."""
+
+    def __init__(self, layer: int):
+        super().__init__(f"non-finite activations in layer {layer}")
+        self.layer = layer
+
+
+@dataclass(frozen=True)
+class SubsequencePartition:
+    """Half-open spans of the cls / query / doc groups (R/encoder.py:58-94)."""
+
+    cls_span: tuple
+    query_span: tuple
+    doc_span: tuple
+
+    def __post_init__(self):
+        if tuple(self.cls_span) != (0, 1):
+            raise EncoderError(f"cls span must be (0, 1), got {self.cls_span}")
+        prev = 0
+        for name, (a, b) in zip(GROUPS, (self.cls_span, self.query_span, self.doc_span)):
+            if a != prev or b <= a:
+                raise EncoderError(f"{name} span {a, b} must be nonempty and contiguous")
+            prev = b
+
+    @property
+    def seq_len(self) -> int:
+        return self.doc_span[1]
+
+    def span(self, group: str):
+        try:
+            return {"cls": self.cls_span, "query": self.query_span, "doc": self.doc_span}[group]
+        except KeyError:
+            raise EncoderError(f"unknown group {group!r}")
+
+    def group_len(self, group: str) -> int:
+        a, b = self.span(group)
+        return b - a
+
+
+@dataclass(frozen=True)
+class TokenSequence:
+    ids: np.ndarray
+    partition: SubsequencePartition
+
+    def __post_init__(self):
+        object.__setattr__(self, "ids", np.asarray(self.ids, dtype=np.int64))
+        if self.ids.ndim != 1 or self.ids.shape[0] != self.partition.seq_len:
+            raise EncoderError("token ids inconsistent with partition")
+
+
+@dataclass(frozen=True)
+class EncoderConfig:
+    """Architecture + pattern settings (R/encoder.py:108-151); precision adds 'bf16'."""
+
+    layers: int
+    embed_dim: int
+    heads: int
+    ff_dim: int
+    max_positions: int
+    vocab_size: int
+    pattern: str = "sparse"
+    window: float = 4
+    qds_global_every: int = 30
+    precision: str = "bf16"
+    padding: str = "exclude"
+
+    def __post_init__(self):
+        if self.layers < 0 or self.embed_dim < 1 or self.heads < 1 or self.ff_dim < 1:
+            raise EncoderError("layers/embed_dim/heads/ff_dim out of range")
+        if self.embed_dim % self.heads != 0:
+            raise EncoderError(f"embed_dim {self.embed_dim} not divisible by heads {self.heads}")
+        if self.precision not in PRECISIONS:
+            raise EncoderError(f"precision must be one of {sorted(PRECISIONS)}")
+        if not is_full(self.window) and (int(self.window) != self.window or self.window < 0):
+            raise EncoderError(f"bad window {self.window!r}")
+        if self.head_dim > 128:
+            raise EncoderError("head_dim > 128 is not supported by the attention kernels")
+        make_pattern(self.pattern, self.window)
+
+    @property
+    def head_dim(self) -> int:
+        return self.embed_dim // self.heads
+
+    @property
+    def torch_dtype(self):
+        return torch.bfloat16 if self.precision == "bf16" else torch.float32
+
+    def with_pattern(self, pattern: str, window=None) -> "EncoderConfig":
+        return replace(self, pattern=pattern, window=self.window if window is None else window)
+
+
+def assemble_input(query_ids, doc_ids, max_positions: int | None = None) -> TokenSequence:
+    """[CLS] q [SEP] d [SEP]; the doc tail is truncated, the query never (R/encoder.py:154-177)."""
+    q = [int(t) for t in query_ids]
+    d = [int(t) for t in doc_ids]
+    m = len(q)
+    if m < 1:
+        raise EncoderError("query must contain at least one token")
+    if max_positions is not None:
+        if m + 3 > max_positions:
+            raise EncoderError(f"query of {m} tokens cannot fit in {max_positions} positions")
+        d = d[: max_positions - m - 3]
+    n = len(d)
+    ids = np.asarray([CLS_ID] + q + [SEP_ID] + d + [SEP_ID], dtype=np.int64)
+    return TokenSequence(ids, SubsequencePartition((0, 1), (1, m + 2), (m + 2, m + n + 3)))
+
+
+def qds_global_positions(doc_token_count: int, every: int = 30) -> tuple:
+    """Every ``every``-th document token is global (R/encoder.py:180-184)."""
+    if every < 1:
+        raise EncoderError("global spacing must be >= 1")
+    return tuple(range(every - 1, doc_token_count, every))
+
+
+def resolve_pattern(config: EncoderConfig, partition: SubsequencePartition):
+    """Concrete pattern for one input (R/encoder.py:187-193)."""
+    g = ()
+    if config.pattern == "qds":
+        g = qds_global_positions(partition.group_len("doc") - 1, config.qds_global_every)
+    return make_pattern(config.pattern, config.window, g)
+
+
+def interpolate_positions(pos_embeddings: np.ndarray, new_max: int) -> np.ndarray:
+    """Linear resample of positional embeddings (R/encoder.py:196-210)."""
+    pos = np.asarray(pos_embeddings)
+    old = pos.shape[0]
+    if new_max < 2 or old < 2:
+        raise EncoderError("positional interpolation requires at least 2 rows")
+    x = np.arange(new_max) * (old - 1) / (new_max - 1)
+    lo = np.floor(x).astype(np.intp)
+    hi = np.minimum(lo + 1, old - 1)
+    fr = (x - lo).astype(pos.dtype)[:, None]
+    return (1 - fr) * pos[lo] + fr * pos[hi]
+
+
+def init_weights(config: EncoderConfig, seed: int = 0) -> dict:
+    """Seeded U(+-1/sqrt(fan_in)) weights with the reference's draw order (R/encoder.py:217-247).
+
+    Generated in float64 by numpy's PCG64 and cast to float32 (the values the
+    reference's f32 precision uses); bf16 mode rounds them on upload.
+    """
+    rng = np.random.default_rng(seed)
+    dt = np.float64 if config.precision == "f64" else np.float32
+    h, ff = config.embed_dim, config.ff_dim
+
+    def uniform(shape, fan_in):
+        b = 1.0 / math.sqrt(fan_in)
+        return rng.uniform(-b, b, size=shape).astype(dt)
+
+    w = {"tok_emb": uniform((config.vocab_size, h), 1), "pos_emb": uniform((config.max_positions, h), 1)}
+    for i in range(config.layers):
+        p = f"L{i}."
+        for name in ("wq", "wk", "wv", "wo"):
+            w[p + name] = uniform((h, h), h)
+            w[p + name.replace("w", "b")] = np.zeros(h, dt)
+        w[p + "ln1_g"], w[p + "ln1_b"] = np.ones(h, dt), np.zeros(h, dt)
+        w[p + "w1"], w[p + "b1"] = uniform((h, ff), h), np.zeros(ff, dt)
+        w[p + "w2"], w[p + "b2"] = uniform((ff, h), ff), np.zeros(h, dt)
+        w[p + "ln2_g"], w[p + "ln2_b"] = np.ones(h, dt), np.zeros(h, dt)
+    w["head_w"] = uniform((h,), h)
+    w["head_b"] = np.zeros((), dt)
+    return w
+
+
+# ---------------------------------------------------------------------------
+# Packed batches of (query, document) sequences.
+# ---------------------------------------------------------------------------
+
+class PackedBatch:
+    """Host-side packed varlen batch: ids int32 [T], cu_seqlens [n+1], query-group lengths [n]."""
+
+    def __init__(self, ids: np.ndarray, seq_lens, qgroup_lens):
+        self.ids = np.ascontiguousarray(ids, dtype=np.int32)
+        self.seq_lens = np.asarray(seq_lens, dtype=np.int64)
+        self.qgroup_lens = np.asarray(qgroup_lens, dtype=np.int64)
+        if self.ids.shape[0] != int(self.seq_lens.sum()):
+            raise EncoderError("ids length inconsistent with sequence lengths")
+
+    @property
+    def nseq(self) -> int:
+        return int(self.seq_lens.shape[0])
+
+    @property
+    def total_tokens(self) -> int:
+        return int(self.ids.shape[0])
+
+    @classmethod
+    def from_sequences(cls, seqs) -> "PackedBatch":
+        seqs = list(seqs)
+        if not seqs:
+            raise EncoderError("empty batch")
+        ids = np.concatenate([s.ids for s in seqs])
+        return cls(ids, [s.partition.seq_len for s in seqs], [s.partition.group_len("query") for s in seqs])
+
+    @classmethod
+    def from_pairs(cls, pairs, max_positions: int) -> "PackedBatch":
+        return cls.from_sequences(assemble_input(q, d, max_positions) for q, d in pairs)
+
+    @classmethod
+    def from_ids(cls, ids: np.ndarray, partition: SubsequencePartition) -> "PackedBatch":
+        ids = np.atleast_2d(np.asarray(ids))
+        b, s = ids.shape
+        return cls(ids.reshape(-1), [s] * b, [partition.group_len("query")] * b)
+
+
+@contextmanager
+def _fp32_gemms(enabled: bool):
+    """Full-precision fp32 cuBLAS GEMMs (TF32 off) for the parity path."""
+    if not enabled:
+        yield
+        return
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        yield
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+class CrossEncoder:
+    """Config + device weights; batched inference (R/encoder.py:450-538)."""
+
+    def __init__(self, config: EncoderConfig, weights: dict | None = None, seed: int = 0,
+                 device="cuda", attn_algo: str = "auto"):
+        self.config = config
+        self.device = torch.device(device)
+        self.attn_algo = attn_algo
+        host = init_weights(config, seed) if weights is None else weights
+        self.host_weights = host
+        self._upload(host)
+
+    @property
+    def weight_nbytes(self) -> int:
+        return sum(int(t.numel() * t.element_size()) for t in self._all_tensors())
+
+    def _all_tensors(self):
+        yield self.tok_emb
+        yield self.pos_emb
+        for L in self.layers:
+            yield from L.values()
+        yield self.head_w
+
+    def _upload(self, w: dict):
+        cfg, dev, cd = self.config, self.device, self.config.torch_dtype
+
+        def f32(a):
+            return torch.as_tensor(np.asarray(a, dtype=np.float32), device=dev).contiguous()
+
+        def gemm_w(a):  # reference stores (in, out) for x @ W; F.linear wants (out, in)
+            return torch.as_tensor(np.asarray(a, dtype=np.float32).T.copy(), device=dev).to(cd).contiguous()
+
+        self.tok_emb = f32(w["tok_emb"])
+        self.pos_emb = f32(w["pos_emb"])
+        self.layers = []
+        for i in range(cfg.layers):
+            p = f"L{i}."
+            wqkv = np.concatenate([w[p + "wq"], w[p + "wk"], w[p + "wv"]], axis=1)
+            bqkv = np.concatenate([w[p + "bq"], w[p + "bk"], w[p + "bv"]])
+            self.layers.append({
+                "wqkv": gemm_w(wqkv), "bqkv": f32(bqkv).to(cd),
+                "wo": gemm_w(w[p + "wo"]), "bo": f32(w[p + "bo"]).to(cd),
+                "ln1_g": f32(w[p + "ln1_g"]), "ln1_b": f32(w[p + "ln1_b"]),
+                "w1": gemm_w(w[p + "w1"]), "b1": f32(w[p + "b1"]).to(cd),
+                "w2": gemm_w(w[p + "w2"]), "b2": f32(w[p + "b2"]).to(cd),
+                "ln2_g": f32(w[p + "ln2_g"]), "ln2_b": f32(w[p + "ln2_b"]),
+            })
+        self.head_w = f32(w["head_w"])
+        self.head_b = float(np.asarray(w["head_b"]))
+
+    # -- validation -------------------------------------------------------
+
+    def _check_batch(self, batch: PackedBatch):
+        if batch.ids.size and (batch.ids.min() < 0 or batch.ids.max() >= self.config.vocab_size):
+            raise EncoderError("token id outside vocabulary")
+        if np.any(batch.seq_lens > self.config.max_positions):
+            raise EncoderError("sequence longer than max_positions")
+
+    def make_layout(self, batch: PackedBatch) -> PackedLayout:
+        qds = self.config.qds_global_every if self.config.pattern == "qds" else 0
+        return PackedLayout.from_lengths(batch.seq_lens, batch.qgroup_lens, device=self.device,
+                                         qds_every=qds)
+
+    # -- the packed hot loop ---------------------------------------------
+
+    def encode_packed(self, ids_dev: torch.Tensor, layout: PackedLayout, check_finite: bool = True,
+                      attn_hook=None) -> torch.Tensor:
+        """Final-layer fp32 activations [T, h] for a packed batch already on the device.
+
+        ``attn_hook(event)`` (optional) is called with "start"/"end" around each
+        attention launch so a caller can bracket it with CUDA events.
+        """
+        cfg = self.config
+        T, h, H = layout.total_tokens, cfg.embed_dim, cfg.heads
+        cd = cfg.torch_dtype
+        bf16 = cd == torch.bfloat16
+        dev = self.device
+        pattern = make_pattern(cfg.pattern, cfg.window)
+        stream = _lib.stream_handle()
+        x = torch.empty((T, h), dtype=torch.float32, device=dev)
+        xh = torch.empty((T, h), dtype=cd, device=dev) if bf16 else None
+        x1 = torch.empty_like(x)
+        x1h = torch.empty_like(xh) if bf16 else None
+        bad = torch.zeros(max(cfg.layers, 1), dtype=torch.int32, device=dev)
+        _lib.call("sc_embed", ids_dev.data_ptr(), layout.tok_pos.data_ptr(), self.tok_emb.data_ptr(),
+                  self.pos_emb.data_ptr(), x.data_ptr(), _lib.ptr(xh), T, h, stream, exc=EncoderError)
+        dcode = _lib.DTYPE_BF16 if bf16 else _lib.DTYPE_F32
+        o = torch.empty((T, h), dtype=cd, device=dev)
+        with _fp32_gemms(not bf16):
+            for i, L in enumerate(self.layers):
+                xin = xh if bf16 else x
+                qkv = F.linear(xin, L["wqkv"], L["bqkv"])
+                if attn_hook:
+                    attn_hook("start")
+                attend_packed(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], layout, pattern, H,
+                              math.sqrt(cfg.head_dim), cfg.padding, out=o, algo=self.attn_algo,
+                              check=(i == 0))
+                if attn_hook:
+                    attn_hook("end")
+                y = F.linear(o, L["wo"], L["bo"])
+                _lib.call("sc_residual_layernorm", x.data_ptr(), y.data_ptr(), dcode, None,
+                          L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), x1.data_ptr(), _lib.ptr(x1h),
+                          T, h, stream, exc=EncoderError)
+                f = F.linear(x1h if bf16 else x1, L["w1"], L["b1"])
+                _lib.call("sc_bias_gelu", f.data_ptr(), None, dcode, T, cfg.ff_dim, stream, exc=EncoderError)
+                f2 = F.linear(f, L["w2"], L["b2"])
+                _lib.call("sc_residual_layernorm", x1.data_ptr(), f2.data_ptr(), dcode, None,
+                          L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(), x.data_ptr(), _lib.ptr(xh),
+                          T, h, stream, exc=EncoderError)
+                if check_finite:
+                    _lib.call("sc_count_nonfinite", x.data_ptr(), x.numel(), bad[i:].data_ptr(), stream)
+        self._last_bad = bad if check_finite else None
+        return x
+
+    def _raise_if_nonfinite(self):
+        bad = getattr(self, "_last_bad", None)
+        if bad is None:
+            return
+        counts = bad.cpu().numpy()
+        nz = np.nonzero(counts[: self.config.layers])[0]
+        if nz.size:
+            raise NonFiniteActivationError(int(nz[0]))
+
+    def scores_from_hidden(self, x: torch.Tensor, layout: PackedLayout, out=None) -> torch.Tensor:
+        out = torch.empty(layout.nseq, dtype=torch.float32, device=self.device) if out is None else out
+        _lib.call("sc_cls_score", x.data_ptr(), layout.cu_seqlens.data_ptr(), layout.nseq,
+                  self.config.embed_dim, self.head_w.data_ptr(), self.head_b, out.data_ptr(),
+                  _lib.stream_handle(), exc=EncoderError)
+        return out
+
+    def score_packed(self, batch: PackedBatch, layout: PackedLayout | None = None) -> torch.Tensor:
+        """Relevance scores (nseq,) on the device for a packed varlen batch."""
+        self._check_batch(batch)
+        layout = layout or self.make_layout(batch)
+        ids = torch.from_numpy(batch.ids).to(self.device, non_blocking=True)
+        x = self.encode_packed(ids, layout)
+        return self.scores_from_hidden(x, layout)
+
+    # -- reference-signature API -----------------------------------------
+
+    def _check_ids(self, ids, partition: SubsequencePartition) -> np.ndarray:
+        ids = np.asarray(ids, dtype=np.int64)
+        if ids.ndim == 1:
+            ids = ids[None, :]
+        if ids.ndim != 2 or ids.shape[1] != partition.seq_len:
+            raise EncoderError(f"ids shape {ids.shape} inconsistent with partition length {partition.seq_len}")
+        if ids.shape[1] > self.config.max_positions:
+            raise EncoderError("sequence longer than max_positions")
+        if ids.min() < 0 or ids.max() >= self.config.vocab_size:
+            raise EncoderError("token id outside vocabulary")
+        return ids
+
+    def forward(self, ids, partition: SubsequencePartition) -> np.ndarray:
+        """Final-layer embeddings (batch, seq, embed) as float32 numpy (R/encoder.py:475-500)."""
+        ids = self._check_ids(ids, partition)
+        batch = PackedBatch.from_ids(ids, partition)
+        layout = self.make_layout(batch)
+        x = self.encode_packed(torch.from_numpy(batch.ids).to(self.device), layout)
+        out = x.reshape(ids.shape[0], ids.shape[1], -1).cpu().numpy()
+        self._raise_if_nonfinite()
+        return out
+
+    def score(self, ids, partition: SubsequencePartition) -> np.ndarray:
+        """Relevance scores (batch,) from the final [CLS] rows (R/encoder.py:502-509)."""
+        ids = self._check_ids(ids, partition)
+        batch = PackedBatch.from_ids(ids, partition)
+        sc = self.score_packed(batch).cpu().numpy()
+        self._raise_if_nonfinite()
+        return sc
+
+    def score_pair(self, query_ids, doc_ids) -> float:
+        """Relevance of one (query, document) pair (R/encoder.py:535-538)."""
+        seq = assemble_input(query_ids, doc_ids, self.config.max_positions)
+        return float(self.score(seq.ids, seq.partition)[0])
+
+    def score_pairs(self, pairs, max_tokens: int = 1 << 18) -> np.ndarray:
+        """Batched relevance of many (query_ids, doc_ids) pairs, packed in chunks of <= max_tokens."""
+        seqs = [assemble_input(q, d, self.config.max_positions) for q, d in pairs]
+        out, chunk, tok = [], [], 0
+        for s in seqs:
+            if chunk and tok + s.partition.seq_len > max_tokens:
+                out.append(self.score_packed(PackedBatch.from_sequences(chunk)))
+                chunk, tok = [], 0
+            chunk.append(s)
+            tok += s.partition.seq_len
+        if chunk:
+            out.append(self.score_packed(PackedBatch.from_sequences(chunk)))
+        res = torch.cat(out).cpu().numpy()
+        self._raise_if_nonfinite()
+        return res
+
+
+def encoder_forward(seq: TokenSequence, config: EncoderConfig, weights: dict) -> np.ndarray:
+    """Final-layer (seq, embed) matrix for a single sequence (R/encoder.py:541-544)."""
+    return CrossEncoder(config, weights).forward(seq.ids, seq.partition)[0]
+
+
+def relevance_score(last_layer, head_w, head_b=0.0) -> float:
+    """Linear readout of the [CLS] row (R/encoder.py:547-552)."""
+    last = np.asarray(last_layer)
+    if last.ndim != 2 or last.shape[0] < 1:
+        raise EncoderError("last layer matrix must be 2-D with a [CLS] row")
+    return float(last[0] @ np.asarray(head_w) + head_b)

@@ -1,0 +1,209 @@
+"""GPU parity: K1 index/mask, band kernels and fused attention vs the oracle / reference goldens.
+
+Tolerances (BASELINE.json north star): masks and indices bit-exact; fp32
+outputs within 1e-4; bf16 outputs within 2e-2.
+"""
+
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+from oracle import sparsecross_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2312_17649_b200 as pkg
+
+    return pkg
+
+
+def gold(name):
+    return np.load(os.path.join(GOLD, name))
+
+
+def run_attention(P, x, m, n, pattern, padding, dtype, algo="auto"):
+    """x: (3, H, s, d) numpy -> GPU output (H, s, d) float64 via the packed path (nseq=1)."""
+    _, H, s, d = x.shape
+    lay = P.PackedLayout.from_lengths([s], [m + 1], device="cuda",
+                                      qds_positions=[pattern.global_positions] if pattern.global_positions else None)
+    t = torch.from_numpy(np.ascontiguousarray(x.transpose(2, 0, 1, 3).reshape(s, 3 * H * d))).cuda().to(dtype)
+    out = P.attend_packed(t[:, :H * d], t[:, H * d:2 * H * d], t[:, 2 * H * d:], lay, pattern, H,
+                          math.sqrt(d), padding, algo=algo)
+    return out.double().cpu().numpy().reshape(s, H, d).transpose(1, 0, 2)
+
+
+def test_index_build_bit_exact(P):
+    rng = np.random.default_rng(3)
+    m = rng.integers(1, 30, size=37)
+    n = rng.integers(1, 300, size=37)
+    seq = m + n + 3
+    lay = P.PackedLayout.from_lengths(seq, m + 1, device="cuda", qds_every=30)
+    exp_seq, exp_grp, exp_rel, exp_pos, flags = [], [], [], [], []
+    for j, (mm, nn) in enumerate(zip(m, n)):
+        gid, rel = O.token_groups(((0, 1), (1, mm + 2), (mm + 2, mm + nn + 3)))
+        exp_seq += [j] * len(gid)
+        exp_grp += list(gid)
+        exp_rel += list(rel)
+        exp_pos += list(range(len(gid)))
+        gl = set(O.qds_global_positions(nn, 30))
+        flags += [1 if (g == 2 and r in gl) else 0 for g, r in zip(gid, rel)]
+    np.testing.assert_array_equal(lay.tok_seq.cpu().numpy(), exp_seq)
+    np.testing.assert_array_equal(lay.tok_group.cpu().numpy(), exp_grp)
+    np.testing.assert_array_equal(lay.tok_rel.cpu().numpy(), exp_rel)
+    np.testing.assert_array_equal(lay.tok_pos.cpu().numpy(), exp_pos)
+    np.testing.assert_array_equal(lay.tok_flags.cpu().numpy(), flags)
+    tiles = np.concatenate([[0], np.cumsum((n + 1 + 63) // 64)])
+    np.testing.assert_array_equal(lay.seq_tile_base.cpu().numpy(), tiles)
+    gcu = np.concatenate([[0], np.cumsum(n // 30)])
+    np.testing.assert_array_equal(lay.glob_cu.cpu().numpy(), gcu)
+
+
+@pytest.mark.parametrize("idx", range(len(cases.MASK_CASES)))
+def test_mask_export_bit_exact(P, idx):
+    """Device predicate == reference pattern_mask (R/reference.py:30-57), golden fixture."""
+    g = gold("masks.npz")
+    name, w, (m, n) = cases.MASK_CASES[idx]
+    s = m + n + 3
+    pat = P.make_pattern(name, w, cases.mask_globals(name, n))
+    lay = P.PackedLayout.from_lengths([s], [m + 1], device="cuda",
+                                      qds_positions=[pat.global_positions] if pat.global_positions else None)
+    want = np.unpackbits(g[f"mask_{idx}"])[: s * s].reshape(s, s).astype(bool)
+    np.testing.assert_array_equal(lay.mask(0, pat), want)
+
+
+@pytest.mark.parametrize("idx", range(len(cases.BAND_CASES)))
+def test_band_kernels(P, idx):
+    g = gold("band.npz")
+    s, t, w, d = cases.BAND_CASES[idx]
+    q, k, p, v = cases.band_inputs(idx, cases.BAND_CASES[idx])
+    np.testing.assert_array_equal(P.band_validity(s, w, t).cpu().numpy(), g[f"valid_{idx}"])
+    f = lambda a: torch.from_numpy(a.astype(np.float32)).cuda()
+    sc = P.band_scores(f(q), f(k), w).double().cpu().numpy()
+    np.testing.assert_allclose(sc, g[f"scores_{idx}"], atol=1e-4)
+    ap = P.band_apply(f(p), f(v), w).double().cpu().numpy()
+    np.testing.assert_allclose(ap, g[f"apply_{idx}"], atol=1e-4)
+    # padding neutrality: poisoned invalid slots do not change the output, bitwise
+    pp = p.copy()
+    pp[~O.band_validity(s, w, t)] = 1e6
+    np.testing.assert_array_equal(P.band_apply(f(pp), f(v), w).cpu().numpy(), P.band_apply(f(p), f(v), w).cpu().numpy())
+
+
+@pytest.mark.parametrize("algo", ["generic", "auto"])
+@pytest.mark.parametrize("idx", range(len(cases.ATTN_CASES)))
+def test_attention_fp32_vs_reference_golden(P, idx, algo):
+    g = gold("attention.npz")
+    case = cases.ATTN_CASES[idx]
+    name, w, pad, m, n, heads, d, dt = case
+    x = cases.attn_inputs(idx, case)
+    pat = P.make_pattern(name, w, cases.attn_globals(name, m, n))
+    got = run_attention(P, x, m, n, pat, pad, torch.float32, algo)
+    np.testing.assert_allclose(got, g[f"out_{idx}"], atol=1e-4, rtol=0)
+
+
+@pytest.mark.parametrize("idx", range(len(cases.ATTN_CASES)))
+def test_attention_bf16_vs_oracle(P, idx):
+    case = cases.ATTN_CASES[idx]
+    name, w, pad, m, n, heads, d, dt = case
+    x = cases.attn_inputs(idx, case)
+    xb = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).double().numpy()  # oracle sees bf16 inputs
+    pat = P.make_pattern(name, w, cases.attn_globals(name, m, n))
+    got = run_attention(P, xb, m, n, pat, pad, torch.bfloat16)
+    spans = cases.attn_spans(m, n)
+    opat = O.make_pattern(name, w, cases.attn_globals(name, m, n))
+    ref = np.concatenate(O.apply_pattern(spans, O.split_groups(spans, *xb), opat, math.sqrt(d), pad), axis=-2)
+    np.testing.assert_allclose(got, ref, atol=2e-2, rtol=0)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_sparse_query_rows_bitwise_independent_of_doc_and_cls(P, dtype):
+    """GPU analogue of T/test_attention.py:212-226."""
+    rng = np.random.default_rng(8)
+    m, n, H, d = 10, 300, 4, 64
+    s = m + n + 3
+    x = rng.standard_normal((3, H, s, d))
+    pat = P.sparse_pattern(4)
+    base = run_attention(P, x, m, n, pat, "exclude", dtype)
+    x2 = x.copy()
+    x2[1:, :, m + 2:, :] = rng.standard_normal((2, H, n + 1, d))
+    x2[1:, :, 0, :] = rng.standard_normal((2, H, d))
+    pert = run_attention(P, x2, m, n, pat, "exclude", dtype)
+    np.testing.assert_array_equal(base[:, 1:m + 2], pert[:, 1:m + 2])
+    assert not np.array_equal(base[:, m + 2:], pert[:, m + 2:])
+
+
+@pytest.mark.parametrize("name,w", [("sparse", 4), ("sparse", 16), ("longformer", 4), ("sparse", 64)])
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 1e-4), (torch.bfloat16, 2e-2)])
+def test_packed_varlen_batch_vs_oracle(P, name, w, dtype, tol):
+    rng = np.random.default_rng(11)
+    H, d = 3, 64
+    shapes = [(10, 164), (1, 1), (7, 530), (10, 4), (25, 97), (10, 64)]
+    seq = [m + n + 3 for m, n in shapes]
+    lay = P.PackedLayout.from_lengths(seq, [m + 1 for m, _ in shapes], device="cuda")
+    T = sum(seq)
+    x = torch.from_numpy(rng.standard_normal((T, 3 * H * d)).astype(np.float32)).cuda().to(dtype)
+    pat = P.make_pattern(name, w)
+    out = P.attend_packed(x[:, :H * d], x[:, H * d:2 * H * d], x[:, 2 * H * d:], lay, pat, H).double().cpu().numpy()
+    xin = x.double().cpu().numpy().reshape(T, 3, H, d)
+    opat = O.make_pattern(name, w)
+    r = 0
+    for (m, n), s in zip(shapes, seq):
+        blk = xin[r:r + s].transpose(1, 2, 0, 3)
+        spans = cases.attn_spans(m, n)
+        ref = np.concatenate(O.apply_pattern(spans, O.split_groups(spans, *blk), opat, math.sqrt(d)), axis=-2)
+        np.testing.assert_allclose(out[r:r + s].reshape(s, H, d).transpose(1, 0, 2), ref, atol=tol, rtol=0)
+        r += s
+
+
+@pytest.mark.parametrize("w", [1, 4, 16, 64, 256, math.inf])
+def test_full_size_document_vs_oracle(P, w):
+    """s = 4099 (q10 + d4086), H=12, d=64: the C3/C4 attention shape, fp32 and bf16."""
+    rng = np.random.default_rng(5)
+    m, n, d = 10, 4086, 64
+    H = 12 if w <= 64 else 2
+    s = m + n + 3
+    x = rng.standard_normal((3, H, s, d)).astype(np.float32)
+    spans = cases.attn_spans(m, n)
+    ref = np.concatenate(O.apply_pattern(spans, O.split_groups(spans, *x.astype(np.float64)),
+                                         O.make_pattern("sparse", w), 8.0), axis=-2)
+    got = run_attention(P, x, m, n, P.sparse_pattern(w), "exclude", torch.float32)
+    np.testing.assert_allclose(got, ref, atol=1e-4, rtol=0)
+    xb = torch.from_numpy(x).to(torch.bfloat16).double().numpy()
+    refb = np.concatenate(O.apply_pattern(spans, O.split_groups(spans, *xb), O.make_pattern("sparse", w), 8.0), axis=-2)
+    gotb = run_attention(P, xb, m, n, P.sparse_pattern(w), "exclude", torch.bfloat16)
+    np.testing.assert_allclose(gotb, refb, atol=2e-2, rtol=0)
+
+
+def test_compat_group_attention_numpy_roundtrip(P):
+    rng = np.random.default_rng(4)
+    m, n, H, d = 3, 9, 2, 8
+    s = m + n + 3
+    x = rng.standard_normal((3, 2, H, s, d)).astype(np.float32)  # leading (B=2, H)
+    spans = cases.attn_spans(m, n)
+    qkv = {g: tuple(a[..., lo:hi, :] for a in x) for g, (lo, hi) in zip(P.GROUPS, spans)}
+    pat = P.sparse_pattern(1)
+    outs = P.apply_pattern(P.SubsequencePartition(*spans), qkv, pat)
+    ref = O.apply_pattern(spans, {g: tuple(a.astype(np.float64) for a in v) for g, v in qkv.items()},
+                          O.make_pattern("sparse", 1), math.sqrt(d))
+    for a, b in zip(outs, ref):
+        assert isinstance(a, np.ndarray)
+        np.testing.assert_allclose(a, b, atol=1e-5)
+    doc = P.group_attention(qkv, "doc", pat, math.sqrt(d))
+    np.testing.assert_allclose(doc, ref[2], atol=1e-5)
+
+
+def test_zero_valid_row_raises(P):
+    pat = P.AttentionPattern("sparse", {"cls": (("cls", math.inf),), "query": (("query", math.inf),),
+                                        "doc": (("query", 0),)})
+    x = np.zeros((3, 1, 1 + 2 + 5, 4), np.float32)
+    with pytest.raises(P.AttentionError):
+        run_attention(P, x, 1, 4, pat, "exclude", torch.float32)
+    run_attention(P, x, 1, 4, pat, "zero-logit", torch.float32)  # padded slots keep rows alive

@@ -1,0 +1,114 @@
+"""CPU-only checks: C-ABI library loads and exports the header's symbols; host-side API logic."""
+
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import cases
+from oracle import sparsecross_oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "sparsecross_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:SC_API\s+)?(?:const\s+)?\w+\*?\s+\*?(sc_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2312_17649_b200 import _lib
+
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 14
+    for name in syms:
+        assert hasattr(lib, name), name
+    assert set(syms) == set(_lib.SIGNATURES)
+    assert lib.sc_version() >= 10000
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    from paper_2312_17649_b200 import _lib
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_invalid_arguments_map_to_reference_errors():
+    import paper_2312_17649_b200 as P
+    from paper_2312_17649_b200 import _lib
+
+    with pytest.raises(P.BandShapeError):
+        _lib.call("sc_band_validity", 3, -1, 3, None, None, exc=P.BandShapeError)
+    assert "window" in _lib.last_error()
+
+
+def test_patterns_and_links():
+    import paper_2312_17649_b200 as P
+
+    sp = P.sparse_pattern(4)
+    np.testing.assert_array_equal(sp.links().reshape(3, 3),
+                                  [[-1, -1, -1], [-2, -1, -2], [-1, -1, 4]])
+    np.testing.assert_array_equal(P.longformer_pattern(2).links().reshape(3, 3)[1], [-1, -1, -1])
+    with pytest.raises(P.AttentionError):
+        P.make_pattern("strided", 3)
+    with pytest.raises(P.AttentionError):
+        P.AttentionPattern("sparse", {"doc": (("doc", -1),)})
+    with pytest.raises(P.AttentionError):
+        P.AttentionPattern("sparse", {"doc": (("doc", 1),)}, global_positions=(2,))
+    lens = np.array([[1, 2, 5]])
+    bad = P.AttentionPattern("x", {"cls": (("cls", math.inf),), "query": (("query", math.inf),),
+                                   "doc": (("query", 0),)})
+    with pytest.raises(P.AttentionError):
+        P.attention.check_rows_have_keys(bad, lens, "exclude")
+    P.attention.check_rows_have_keys(bad, lens, "zero-logit")
+
+
+def test_partition_and_assembly_match_reference_rules():
+    import paper_2312_17649_b200 as P
+
+    seq = P.assemble_input(range(3, 13), range(3, 4088), max_positions=4096)
+    assert seq.ids.shape[0] == 4096 and seq.partition.group_len("doc") == 4084
+    ids, spans = O.assemble_input(list(range(3, 13)), list(range(3, 4088)), 4096)
+    np.testing.assert_array_equal(seq.ids, ids)
+    assert (seq.partition.cls_span, seq.partition.query_span, seq.partition.doc_span) == spans
+    with pytest.raises(P.EncoderError):
+        P.assemble_input(range(3, 20), [5], max_positions=12)
+    with pytest.raises(P.EncoderError):
+        P.SubsequencePartition((0, 1), (2, 4), (4, 6))
+    assert P.qds_global_positions(4086, 30)[-1] == 4079 and len(P.qds_global_positions(4086, 30)) == 136
+
+
+def test_init_weights_identical_to_oracle():
+    import paper_2312_17649_b200 as P
+
+    cfg = P.EncoderConfig(**cases.C1, precision="f32")
+    a = P.init_weights(cfg, 0)
+    b = O.init_weights(cases.C1, 0, np.float32)
+    assert a.keys() == b.keys()
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_packed_batch_layout():
+    import paper_2312_17649_b200 as P
+
+    seqs = [P.assemble_input([5, 6], [7, 8, 9]), P.assemble_input([4], [])]
+    pb = P.PackedBatch.from_sequences(seqs)
+    assert pb.total_tokens == 8 + 4 and pb.nseq == 2
+    np.testing.assert_array_equal(pb.seq_lens, [8, 4])
+    np.testing.assert_array_equal(pb.qgroup_lens, [3, 2])
+
+
+def test_interpolate_positions():
+    import paper_2312_17649_b200 as P
+
+    pos = np.array([[0.0, 0.0], [2.0, 4.0], [6.0, 8.0]])
+    out = P.interpolate_positions(pos, 5)
+    np.testing.assert_allclose(out[1], 0.5 * pos[0] + 0.5 * pos[1])
+    np.testing.assert_array_equal(out[-1], pos[-1])
