@@ -70,9 +70,9 @@ SC_API int sc_version(void);
 /* ---- K1: device index / mask construction ------------------------------ */
 
 /* Per-token sequence id, group id (0/1/2), group-relative index and position
- * (token index within its sequence), plus a per-sequence prefix of doc-row
- * tiles of `tile_rows` rows (seq_tile_base[nseq+1]) used by the band kernel
- * scheduler.  Replaces SubsequencePartition/_split_groups/_locate
+ * (token index within its sequence), plus per-sequence prefixes of doc-row
+ * tiles of `tile_rows` rows (seq_tile_base[nseq+1], the band kernel's
+ * scheduler) and of head rows = cls + query-group rows (seq_head_base[nseq+1]).  Replaces SubsequencePartition/_split_groups/_locate
  * (R/encoder.py:58-94, :299-303; R/reference.py:22-27).  qds_every > 0 also
  * fills tok_flags bit0 for QDS global doc tokens (R/encoder.py:180-193) and
  * their CSR lists glob_cu[nseq+1]/glob_pos (doc-relative); pass NULLs when 0.
@@ -80,8 +80,8 @@ SC_API int sc_version(void);
 SC_API int sc_index_build(const int32_t* cu_seqlens, const int32_t* qgroup_len, int32_t nseq,
                    int32_t total_tokens, int32_t tile_rows, int32_t qds_every,
                    int32_t* tok_seq, int32_t* tok_group, int32_t* tok_rel, int32_t* tok_pos,
-                   int32_t* seq_tile_base, uint8_t* tok_flags, int32_t* glob_cu,
-                   int32_t* glob_pos, void* stream);
+                   int32_t* seq_tile_base, int32_t* seq_head_base, uint8_t* tok_flags,
+                   int32_t* glob_cu, int32_t* glob_pos, void* stream);
 
 /* Dense (s x s) attendability bitmap of sequence `seq` (uint8, 1 = may attend),
  * exactly the attention kernels' predicate.  Replaces pattern_mask
@@ -110,9 +110,13 @@ SC_API int sc_band_apply(const void* p, const void* v, void* out, int64_t batch,
 
 /* ---- K2/K3: fused asymmetric windowed attention ------------------------- */
 
-/* Workspace for sc_attn_fwd (split-softmax partials of full-attention rows). */
+/* Workspace for sc_attn_fwd: split-softmax partials of the head rows that
+ * attend the whole document (CLS; query rows too under longformer/full),
+ * one (m, l, acc[d]) record per doc tile x head x full row.  max_qgroup_len
+ * is the largest qgroup_len of the batch. */
 SC_API size_t sc_attn_workspace_bytes(int32_t nseq, int32_t total_tokens, int32_t heads,
-                               int32_t head_dim, int32_t tile_rows);
+                               int32_t head_dim, int32_t tile_rows, int32_t max_qgroup_len,
+                               const int32_t* links);
 
 /* Attention of every token row of a packed batch under one pattern:
  * all three groups (cls, query, doc) of every sequence in one call.
@@ -120,7 +124,11 @@ SC_API size_t sc_attn_workspace_bytes(int32_t nseq, int32_t total_tokens, int32_
  * `dtype`); typical packed QKV [T][3][H][d]: k = q + H*d, v = q + 2*H*d,
  * row_stride = 3*H*d.  out: [T][H][d] with out_row_stride.  scale divides
  * the logits (sqrt(d) in the encoder, R/encoder.py:329).  tok_* /
- * seq_tile_base come from sc_index_build with the same tile_rows.
+ * seq_tile_base / seq_head_base come from sc_index_build with the same
+ * tile_rows; max_qgroup_len is the host-known max of qgroup_len (kernel
+ * selection only).  algo picks the kernel (SC_ATTN_*); AUTO runs the tiled
+ * band kernel (bf16, d = 64, finite doc window, no QDS) for doc rows plus the
+ * head-row combine, else the generic kernel.
  * status (optional, device int32) gets bit0 set if a row had zero valid keys.
  * Replaces group_attention x3 (R/attention.py:416-473), apply_pattern
  * (:510-537), attend_segments (:290-345), masked_segment_softmax (:228-257)
@@ -130,7 +138,8 @@ SC_API int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t row_
                 const int32_t* cu_seqlens, const int32_t* qgroup_len, int32_t nseq,
                 int32_t total_tokens, int32_t heads, int32_t head_dim,
                 const int32_t* links, int32_t padding, float scale, int32_t dtype,
-                const int32_t* tok_seq, const int32_t* seq_tile_base, int32_t tile_rows,
+                const int32_t* tok_seq, const int32_t* seq_tile_base,
+                const int32_t* seq_head_base, int32_t tile_rows, int32_t max_qgroup_len,
                 const uint8_t* tok_flags, const int32_t* glob_cu, const int32_t* glob_pos,
                 int32_t algo, void* workspace, size_t workspace_bytes, int32_t* status,
                 void* stream);

@@ -44,14 +44,14 @@ _f32 = C.c_float
 SIGNATURES = {
     "sc_last_error": (C.c_char_p, []),
     "sc_version": (C.c_int, []),
-    "sc_index_build": (C.c_int, [_p, _p, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
+    "sc_index_build": (C.c_int, [_p, _p, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "sc_mask_export": (C.c_int, [_p, _p, _i32, _i32, _i32, _p, _p, _p, _p]),
     "sc_band_validity": (C.c_int, [_i32, _i32, _i32, _p, _p]),
     "sc_band_scores": (C.c_int, [_p, _p, _p, _i64, _i32, _i32, _i32, _i32, _i32, _p]),
     "sc_band_apply": (C.c_int, [_p, _p, _p, _i64, _i32, _i32, _i32, _i32, _i32, _p]),
-    "sc_attn_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32, _i32]),
+    "sc_attn_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32, _i32, _i32, _p]),
     "sc_attn_fwd": (C.c_int, [_p, _p, _p, _i64, _p, _i64, _p, _p, _i32, _i32, _i32, _i32, _p, _i32,
-                              _f32, _i32, _p, _p, _i32, _p, _p, _p, _i32, _p, _sz, _p, _p]),
+                              _f32, _i32, _p, _p, _p, _i32, _i32, _p, _p, _p, _i32, _p, _sz, _p, _p]),
     "sc_embed": (C.c_int, [_p, _p, _p, _p, _p, _p, _i32, _i32, _p]),
     "sc_residual_layernorm": (C.c_int, [_p, _p, _i32, _p, _p, _p, _p, _p, _i32, _i32, _p]),
     "sc_bias_gelu": (C.c_int, [_p, _p, _i32, _i64, _i32, _p]),

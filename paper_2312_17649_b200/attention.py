@@ -184,14 +184,15 @@ def attend_packed(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: Pac
     if out is None:
         out = torch.empty((T, hd), dtype=q.dtype, device=q.device)
     algo_code = {"auto": _lib.ALGO_AUTO, "generic": _lib.ALGO_GENERIC, "band": _lib.ALGO_BAND_MMA}[algo]
-    ws = layout.attn_workspace(heads, d)
     links = pattern.links()
+    ws = layout.attn_workspace(heads, d, links)
     _lib.call(
         "sc_attn_fwd",
         q.data_ptr(), k.data_ptr(), v.data_ptr(), q.stride(0), out.data_ptr(), out.stride(0),
         layout.cu_seqlens.data_ptr(), layout.qgroup_len.data_ptr(), layout.nseq, T, heads, d,
         links.ctypes.data, _lib.PAD_EXCLUDE if padding == "exclude" else _lib.PAD_ZERO_LOGIT,
-        float(scale), dt, layout.tok_seq.data_ptr(), layout.seq_tile_base.data_ptr(), layout.tile_rows,
+        float(scale), dt, layout.tok_seq.data_ptr(), layout.seq_tile_base.data_ptr(),
+        layout.seq_head_base.data_ptr(), layout.tile_rows, layout.max_qgroup_len,
         _lib.ptr(layout.tok_flags) if qds else None, _lib.ptr(layout.glob_cu) if qds else None,
         _lib.ptr(layout.glob_pos) if qds else None, algo_code,
         _lib.ptr(ws), 0 if ws is None else ws.numel(), None, _lib.stream_handle(),

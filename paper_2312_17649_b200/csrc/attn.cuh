@@ -21,18 +21,34 @@ struct AttnArgs {
   const int32_t* glob_cu;
   const int32_t* glob_pos;
   int32_t* status;
-  int row_begin, row_end;  // token-row range to process
-  int only_group;          // -1 all groups, else only rows of that group
+  int row_begin, row_end;  // token-row range to process (all-rows mode)
+  // Head-row mode (generic kernel after the band kernel): items enumerate the
+  // cls + query-group rows of every sequence through head_base; a FULL doc
+  // link is served by merging the band kernel's per-tile partials.
+  const int32_t* head_base;  // [nseq+1] or nullptr for all-rows mode
+  int n_head_rows;
+  const float* partials;     // [tiles][H][fmax][d+2]: (m, l, acc[d]); nullptr = scan doc keys
+  const int32_t* tile_base;  // [nseq+1]
+  int fmax;
 };
 
 bool load_links(const int32_t* links, Links* L);
 int launch_attn_generic(const AttnArgs& a, int dtype, cudaStream_t st);
 
+// Rows of the query group that attend the whole document (FULL doc link):
+// their split-softmax partials are produced per doc tile by the band kernel.
+__host__ __device__ inline int full_rows_needed(const Links& L, int max_qgroup_len) {
+  if (L.w[1][2] == SC_LINK_FULL) return 1 + max_qgroup_len;
+  if (L.w[0][2] == SC_LINK_FULL) return 1;
+  return 0;
+}
+
 // Tiled band kernel (attn_band_mma.cu).  Returns SC_ERR_UNSUPPORTED when the
 // pattern/shape is outside its envelope (the caller then uses the generic kernel).
-size_t band_workspace_bytes(int nseq, int T, int H, int d, int tile_rows);
-int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* tok_seq,
-                     const int32_t* seq_tile_base, int tile_rows, void* ws, size_t ws_bytes,
-                     cudaStream_t st);
+size_t band_workspace_bytes(int nseq, int T, int H, int d, int tile_rows, int max_qgroup_len,
+                            const Links& L);
+int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
+                     const int32_t* seq_head_base, int tile_rows, int max_qgroup_len, void* ws,
+                     size_t ws_bytes, cudaStream_t st);
 
 }  // namespace sc

@@ -5,8 +5,11 @@
 using namespace sc;
 
 extern "C" size_t sc_attn_workspace_bytes(int32_t nseq, int32_t total_tokens, int32_t heads,
-                                          int32_t head_dim, int32_t tile_rows) {
-  return band_workspace_bytes(nseq, total_tokens, heads, head_dim, tile_rows);
+                                          int32_t head_dim, int32_t tile_rows,
+                                          int32_t max_qgroup_len, const int32_t* links) {
+  Links L;
+  if (!load_links(links, &L)) return 0;
+  return band_workspace_bytes(nseq, total_tokens, heads, head_dim, tile_rows, max_qgroup_len, L);
 }
 
 extern "C" int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t row_stride,
@@ -14,11 +17,13 @@ extern "C" int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t 
                            const int32_t* qgroup_len, int32_t nseq, int32_t total_tokens,
                            int32_t heads, int32_t head_dim, const int32_t* links, int32_t padding,
                            float scale, int32_t dtype, const int32_t* tok_seq,
-                           const int32_t* seq_tile_base, int32_t tile_rows,
-                           const uint8_t* tok_flags, const int32_t* glob_cu,
-                           const int32_t* glob_pos, int32_t algo, void* workspace,
-                           size_t workspace_bytes, int32_t* status, void* stream) {
-  AttnArgs a;
+                           const int32_t* seq_tile_base, const int32_t* seq_head_base,
+                           int32_t tile_rows, int32_t max_qgroup_len, const uint8_t* tok_flags,
+                           const int32_t* glob_cu, const int32_t* glob_pos, int32_t algo,
+                           void* workspace, size_t workspace_bytes, int32_t* status,
+                           void* stream) {
+  (void)tok_seq;
+  AttnArgs a = {};
   SC_CHECK_ARG(load_links(links, &a.links), "sc_attn_fwd: bad links");
   SC_CHECK_ARG(q && k && v && out && cu_seqlens && qgroup_len, "sc_attn_fwd: null pointer");
   SC_CHECK_ARG(nseq >= 1 && total_tokens >= 3 * nseq, "sc_attn_fwd: bad nseq/total_tokens");
@@ -30,17 +35,17 @@ extern "C" int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t 
   SC_CHECK_ARG(dtype == SC_DTYPE_F32 || dtype == SC_DTYPE_BF16, "sc_attn_fwd: bad dtype %d", dtype);
   SC_CHECK_ARG((glob_cu == nullptr) == (glob_pos == nullptr), "sc_attn_fwd: glob_cu/glob_pos must be both set or both NULL");
   SC_CHECK_ARG(glob_cu == nullptr || tok_flags != nullptr, "sc_attn_fwd: QDS globals need tok_flags");
+  SC_CHECK_ARG(algo == SC_ATTN_AUTO || algo == SC_ATTN_GENERIC || algo == SC_ATTN_BAND_MMA,
+               "sc_attn_fwd: bad algo %d", algo);
+  SC_CHECK_ARG(max_qgroup_len >= 1, "sc_attn_fwd: max_qgroup_len must be >= 1");
   a.q = q; a.k = k; a.v = v; a.ld = row_stride; a.out = out; a.ld_out = out_row_stride;
   a.cu = cu_seqlens; a.qlen = qgroup_len; a.nseq = nseq; a.T = total_tokens; a.H = heads;
   a.d = head_dim; a.padding = padding; a.scale = scale; a.flags = tok_flags; a.glob_cu = glob_cu;
   a.glob_pos = glob_pos; a.status = status; a.row_begin = 0; a.row_end = total_tokens;
-  a.only_group = -1;
   cudaStream_t st = (cudaStream_t)stream;
-  SC_CHECK_ARG(algo == SC_ATTN_AUTO || algo == SC_ATTN_GENERIC || algo == SC_ATTN_BAND_MMA,
-               "sc_attn_fwd: bad algo %d", algo);
   if (algo != SC_ATTN_GENERIC) {
-    int rc = launch_attn_band(a, dtype, tok_seq, seq_tile_base, tile_rows, workspace,
-                              workspace_bytes, st);
+    int rc = launch_attn_band(a, dtype, seq_tile_base, seq_head_base, tile_rows, max_qgroup_len,
+                              workspace, workspace_bytes, st);
     if (rc != SC_ERR_UNSUPPORTED || algo == SC_ATTN_BAND_MMA) return rc;
   }
   return launch_attn_generic(a, dtype, st);

@@ -1,10 +1,501 @@
-// Placeholder: tiled band kernel arrives in the next commit.
+// Tiled band attention for doc rows (the HBM-bound hot path of the sparse
+// cross-encoder, arXiv 2312.17649 Eqs. 1-3), bf16 I/O, fp32 softmax/accum.
+//
+// One CTA = one tile of BM=64 doc rows of one sequence, looping over heads.
+// Per head a 2-stage TMA pipeline (128B-swizzled boxes, mbarrier complete_tx)
+// stages in shared memory:
+//   Q   [64 x 64]        doc rows r0..r0+63
+//   Kb/Vb [64+2w x 64]   doc rows r0-w .. r0+63+w  (the band halo)
+//   Kg/Vg [32 x 64]      the sequence's cls + query-group rows (global keys)
+//   Qf  [32 x 64]        the same rows as queries ("full rows": CLS, and query
+//                        rows under longformer/full, that attend the whole doc)
+// Warps 0-3 each own 16 doc rows: S = Q K^T over {global keys} U {band keys}
+// with mma.sync m16n8k16 (bf16 -> fp32), band/validity mask, online softmax
+// in the exp2 domain, O += P V, bf16 stores.  Warp 4 computes split-softmax
+// partials (m, l, acc) of the full rows over this tile's own 64 doc keys,
+// so the CLS row never re-reads K/V from HBM; the head-row pass of the
+// generic kernel merges them.  Warp 5 is the TMA producer.
+//
+// Semantics: doc row r attends cls (if linked), query group (if linked) and
+// doc keys t with |t - r| <= w, 0 <= t < n_doc (R/band.py:48-52,
+// R/attention.py:125-139); zero-logit padding adds (2w+1 - #in-range) logit-0
+// slots (R/attention.py:244-247).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "attn.cuh"
+
 namespace sc {
-size_t band_workspace_bytes(int, int, int, int, int) { return 0; }
-int launch_attn_band(const AttnArgs&, int, const int32_t*, const int32_t*, int, void*, size_t,
-                     cudaStream_t) {
-  set_error("band kernel not built");
-  return SC_ERR_UNSUPPORTED;
+namespace bandk {
+
+constexpr int BM = 64;
+constexpr int D = 64;
+constexpr int ROWB = 128;  // bytes per smem row
+constexpr int GROWS = 32;  // global rows staged per head
+constexpr int NSTAGE = 2;
+constexpr int PRODW = 5;
+constexpr int FULLW = 4;
+constexpr int NTHREADS = 192;
+constexpr int MAX_W = 96;  // Kb box rows 64 + 2w <= 256 (TMA box limit)
+
+struct Params {
+  int nseq, H, w, nbc, kb_rows, fneed, fmax, padding;
+  int link_cls, link_query;
+  float scale_log2;
+  const int32_t* cu;
+  const int32_t* qlen;
+  const int32_t* tile_base;
+  __nv_bfloat16* out;
+  int64_t ld_out;
+  float* partials;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// 128B-swizzled address of (row, 16-byte chunk) in a 1024B-aligned buffer.
+__device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
+  return base + row * ROWB + ((chunk ^ (row & 7)) << 4);
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// A fragments of a 16-row x 64-dim Q block starting at smem row `row0`.
+__device__ __forceinline__ void load_q(uint32_t buf, int row0, int lane, uint32_t (&qa)[4][4]) {
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) ldsm_x4(swz(buf, row0 + (lane & 15), ks * 2 + (lane >> 4)), qa[ks]);
+}
+
+// S[2 n8 blocks] += Q(16x64) . K[key0 .. key0+15]^T
+__device__ __forceinline__ void qk16(uint32_t kbuf, int key0, int lane, const uint32_t (&qa)[4][4],
+                                     float (&s0)[4], float (&s1)[4]) {
+  const int krow = key0 + (lane & 7) + ((lane >> 4) << 3);
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    uint32_t b[4];
+    ldsm_x4(swz(kbuf, krow, ks * 2 + ((lane >> 3) & 1)), b);
+    mma16816(s0, qa[ks], b[0], b[1]);
+    mma16816(s1, qa[ks], b[2], b[3]);
+  }
+}
+
+// O(16x64) += P(16 x 16 keys) . V[key0 .. key0+15]
+__device__ __forceinline__ void pv16(uint32_t vbuf, int key0, int lane, const float (&p0)[4],
+                                     const float (&p1)[4], float (&o)[8][4]) {
+  uint32_t a[4] = {pack_bf16(p0[0], p0[1]), pack_bf16(p0[2], p0[3]), pack_bf16(p1[0], p1[1]),
+                   pack_bf16(p1[2], p1[3])};
+  const int vrow = key0 + (lane & 7) + (((lane >> 3) & 1) << 3);
+#pragma unroll
+  for (int np = 0; np < 4; ++np) {
+    uint32_t b[4];
+    ldsm_x4_t(swz(vbuf, vrow, np * 2 + (lane >> 4)), b);
+    mma16816(o[2 * np], a, b[0], b[1]);
+    mma16816(o[2 * np + 1], a, b[2], b[3]);
+  }
+}
+
+// Online-softmax update for NB n8 score blocks of rows (g, g+8); scores already
+// scaled to the log2 domain and masked to -inf.  Overwrites s with P.
+template <int NB>
+__device__ __forceinline__ void softmax_update(float (&s)[NB][4], float& m0, float& m1, float& l0,
+                                               float& l1, float (&o)[8][4]) {
+  float x0 = -INFINITY, x1 = -INFINITY;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    x0 = fmaxf(x0, fmaxf(s[b][0], s[b][1]));
+    x1 = fmaxf(x1, fmaxf(s[b][2], s[b][3]));
+  }
+  x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, 1));
+  x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, 2));
+  x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, 1));
+  x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, 2));
+  const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);
+  const float b0 = n0 == -INFINITY ? 0.f : n0, b1 = n1 == -INFINITY ? 0.f : n1;
+  const float a0 = exp2f(m0 - b0), a1 = exp2f(m1 - b1);
+  float r0 = 0.f, r1 = 0.f;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    s[b][0] = exp2f(s[b][0] - b0);
+    s[b][1] = exp2f(s[b][1] - b0);
+    s[b][2] = exp2f(s[b][2] - b1);
+    s[b][3] = exp2f(s[b][3] - b1);
+    r0 += s[b][0] + s[b][1];
+    r1 += s[b][2] + s[b][3];
+  }
+  l0 = l0 * a0 + r0;
+  l1 = l1 * a1 + r1;
+#pragma unroll
+  for (int nb = 0; nb < 8; ++nb) {
+    o[nb][0] *= a0;
+    o[nb][1] *= a0;
+    o[nb][2] *= a1;
+    o[nb][3] *= a1;
+  }
+  m0 = n0;
+  m1 = n1;
+}
+
+__global__ void __launch_bounds__(NTHREADS) band_attn_kernel(
+    const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQf,
+    const __grid_constant__ CUtensorMap tmKg, const __grid_constant__ CUtensorMap tmVg,
+    const __grid_constant__ CUtensorMap tmKb, const __grid_constant__ CUtensorMap tmVb, Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+  const int tile = blockIdx.x;
+  if (tile >= __ldg(p.tile_base + p.nseq)) return;
+  const int j = find_seq(p.tile_base, p.nseq, tile);
+  const SeqGroups g = seq_groups(p.cu, p.qlen, j);
+  const int n_doc = g.len[2];
+  const int r0 = (tile - __ldg(p.tile_base + j)) * BM;
+  const int rows_here = min(BM, n_doc - r0);
+  const int doc_row0 = g.start + g.off[2] + r0;
+  const int G = 1 + g.len[1];
+
+  const int q_bytes = BM * ROWB, f_bytes = GROWS * ROWB, kb_bytes = p.kb_rows * ROWB;
+  const int stage_bytes = q_bytes + 3 * f_bytes + 2 * kb_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * stage_bytes);
+  const uint32_t sm0 = smem_u32(smem);
+  auto q_buf = [&](int s) { return sm0 + s * stage_bytes; };
+  auto qf_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes; };
+  auto kg_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + f_bytes; };
+  auto vg_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + 2 * f_bytes; };
+  auto kb_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + 3 * f_bytes; };
+  auto vb_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + 3 * f_bytes + kb_bytes; };
+  const uint32_t full_bar = smem_u32(bars), empty_bar = smem_u32(bars + NSTAGE);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = p.w;
+  const int kb_box = BM + 2 * w;
+
+  // Zero the Kb/Vb rows the TMA box never writes (band chunks read up to kb_rows).
+  for (int s = 0; s < NSTAGE; ++s) {
+    uint8_t* kb = smem + s * stage_bytes + q_bytes + 3 * f_bytes;
+    for (int o = kb_box * ROWB + threadIdx.x * 16; o < kb_bytes; o += NTHREADS * 16) {
+      *reinterpret_cast<uint4*>(kb + o) = make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(kb + kb_bytes + o) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(full_bar + 8 * s, 1);
+      mbar_init(empty_bar + 8 * s, 5);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == PRODW) {
+    if (lane == 0) {
+      prefetch_map(&tmQ); prefetch_map(&tmKb); prefetch_map(&tmVb);
+      prefetch_map(&tmKg); prefetch_map(&tmVg); prefetch_map(&tmQf);
+      const uint32_t bytes = (uint32_t)(q_bytes + 3 * f_bytes + 2 * kb_box * ROWB);
+      for (int h = 0; h < p.H; ++h) {
+        const int s = h % NSTAGE;
+        if (h >= NSTAGE) mbar_wait(empty_bar + 8 * s, ((h / NSTAGE) & 1) ^ 1);
+        const uint32_t fb = full_bar + 8 * s;
+        mbar_expect_tx(fb, bytes);
+        const int col = h * D;
+        tma_load_2d(q_buf(s), &tmQ, col, doc_row0, fb);
+        tma_load_2d(qf_buf(s), &tmQf, col, g.start, fb);
+        tma_load_2d(kg_buf(s), &tmKg, col, g.start, fb);
+        tma_load_2d(vg_buf(s), &tmVg, col, g.start, fb);
+        tma_load_2d(kb_buf(s), &tmKb, col, doc_row0 - w, fb);
+        tma_load_2d(vb_buf(s), &tmVb, col, doc_row0 - w, fb);
+      }
+    }
+    return;
+  }
+
+  const int gq = lane >> 2, tq = lane & 3;
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ doc rows
+    const int wr0 = warp * 16;
+    const bool active = wr0 < rows_here;
+    const int ra = r0 + wr0 + gq, rb = ra + 8;  // doc-relative rows of this thread
+    float ninv_a = 0.f, ninv_b = 0.f;
+    if (p.padding == SC_PAD_ZERO_LOGIT && tq == 0) {
+      ninv_a = (float)(2 * w + 1 - max(0, min(n_doc, ra + w + 1) - max(0, ra - w)));
+      ninv_b = (float)(2 * w + 1 - max(0, min(n_doc, rb + w + 1) - max(0, rb - w)));
+    }
+    for (int h = 0; h < p.H; ++h) {
+      const int s = h % NSTAGE;
+      mbar_wait(full_bar + 8 * s, (h / NSTAGE) & 1);
+      if (active) {
+        uint32_t qa[4][4];
+        load_q(q_buf(s), wr0, lane, qa);
+        float o[8][4];
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
+        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+        if (p.padding == SC_PAD_ZERO_LOGIT) {  // virtual logit-0 slots (same on all quad lanes)
+          float na = __shfl_sync(0xffffffffu, ninv_a, lane & ~3);
+          float nbv = __shfl_sync(0xffffffffu, ninv_b, lane & ~3);
+          if (na > 0.f) { m0 = 0.f; l0 = ninv_a; }
+          if (nbv > 0.f) { m1 = 0.f; l1 = ninv_b; }
+        }
+        // global keys: cls (key 0) and the query group (keys 1..G-1)
+        for (int gc = 0; gc * 16 < G; ++gc) {
+          float sc[2][4] = {};
+          qk16(kg_buf(s), gc * 16, lane, qa, sc[0], sc[1]);
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int kg = gc * 16 + nb * 8 + 2 * tq + (e & 1);
+              const bool ok = kg < G && (kg == 0 ? p.link_cls : p.link_query);
+              sc[nb][e] = ok ? sc[nb][e] * p.scale_log2 : -INFINITY;
+            }
+          softmax_update<2>(sc, m0, m1, l0, l1, o);
+          pv16(vg_buf(s), gc * 16, lane, sc[0], sc[1], o);
+        }
+        // band keys: Kb row 0 = doc row r0 - w; this warp reads rows wr0 + [0, 32*nbc)
+        for (int bc = 0; bc < p.nbc; ++bc) {
+          const int kb0 = wr0 + 32 * bc;
+          float sc[4][4] = {};
+          qk16(kb_buf(s), kb0, lane, qa, sc[0], sc[1]);
+          qk16(kb_buf(s), kb0 + 16, lane, qa, sc[2], sc[3]);
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int c = 32 * bc + nb * 8 + 2 * tq + (e & 1);  // key offset from wr0 row base
+              const int ri = gq + ((e >> 1) << 3);                   // row within the 16
+              const int diff = c - ri;                               // t - r + w
+              const int t = r0 - w + wr0 + c;                        // doc-relative key
+              const bool ok = diff >= 0 && diff <= 2 * w && t >= 0 && t < n_doc;
+              sc[nb][e] = ok ? sc[nb][e] * p.scale_log2 : -INFINITY;
+            }
+          softmax_update<4>(sc, m0, m1, l0, l1, o);
+          pv16(vb_buf(s), kb0, lane, sc[0], sc[1], o);
+          pv16(vb_buf(s), kb0 + 16, lane, sc[2], sc[3], o);
+        }
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+        const float i0 = 1.f / l0, i1 = 1.f / l1;
+        __nv_bfloat16* out_h = p.out + h * D + 2 * tq;
+        if (ra < n_doc) {
+          uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq) * p.ld_out);
+#pragma unroll
+          for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][0] * i0, o[nb][1] * i0);
+        }
+        if (rb < n_doc) {
+          uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq + 8) * p.ld_out);
+#pragma unroll
+          for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][2] * i1, o[nb][3] * i1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_bar + 8 * s);
+    }
+  } else {
+    // ------------------------------------------- full-row split-softmax partials
+    for (int h = 0; h < p.H; ++h) {
+      const int s = h % NSTAGE;
+      mbar_wait(full_bar + 8 * s, (h / NSTAGE) & 1);
+      for (int fc = 0; fc * 16 < p.fneed; ++fc) {
+        uint32_t qa[4][4];
+        load_q(qf_buf(s), fc * 16, lane, qa);
+        float sc[8][4] = {};
+#pragma unroll
+        for (int np = 0; np < 4; ++np) qk16(kb_buf(s), w + np * 16, lane, qa, sc[2 * np], sc[2 * np + 1]);
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = nb * 8 + 2 * tq + (e & 1);
+            sc[nb][e] = c < rows_here ? sc[nb][e] * p.scale_log2 : -INFINITY;
+          }
+        float o[8][4];
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
+        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+        softmax_update<8>(sc, m0, m1, l0, l1, o);
+#pragma unroll
+        for (int kp = 0; kp < 4; ++kp) pv16(vb_buf(s), w + kp * 16, lane, sc[2 * kp], sc[2 * kp + 1], o);
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+        constexpr float kLn2 = 0.69314718055994530942f;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const int f = fc * 16 + gq + 8 * half;
+          if (f >= p.fneed) continue;
+          float* rec = p.partials + (((int64_t)tile * p.H + h) * p.fmax + f) * (D + 2);
+          if (tq == 0) {
+            rec[0] = (half ? m1 : m0) * kLn2;
+            rec[1] = half ? l1 : l0;
+          }
+#pragma unroll
+          for (int nb = 0; nb < 8; ++nb) {
+            rec[2 + nb * 8 + 2 * tq] = o[nb][2 * half];
+            rec[2 + nb * 8 + 2 * tq + 1] = o[nb][2 * half + 1];
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_bar + 8 * s);
+    }
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(ptr);
+  }
+  return fn;
+}
+
+static bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t ld_elems,
+                     int box_rows) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld_elems * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)D, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int kb_rows_for(int w) { return 48 + 32 * ((16 + 2 * w + 31) / 32); }
+
+}  // namespace bandk
+
+size_t band_workspace_bytes(int nseq, int T, int H, int d, int tile_rows, int max_qgroup_len,
+                            const Links& L) {
+  int f = full_rows_needed(L, max_qgroup_len);
+  if (f == 0 || tile_rows <= 0) return 0;
+  int64_t tiles = (T + tile_rows - 1) / tile_rows + nseq;
+  return (size_t)tiles * H * f * (d + 2) * sizeof(float);
+}
+
+int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
+                     const int32_t* seq_head_base, int tile_rows, int max_qgroup_len, void* ws,
+                     size_t ws_bytes, cudaStream_t st) {
+  using namespace bandk;
+  const Links& L = a.links;
+  const int w = L.w[2][2];
+  auto unsupported = [](const char* why) {
+    set_error("band kernel: %s", why);
+    return SC_ERR_UNSUPPORTED;
+  };
+  if (dtype != SC_DTYPE_BF16) return unsupported("needs bf16");
+  if (a.d != D) return unsupported("needs head_dim 64");
+  if (a.glob_cu) return unsupported("QDS global tokens");
+  if (w < 0 || w > MAX_W) return unsupported("doc->doc link must be a window <= 96");
+  for (int x : {L.w[2][0], L.w[2][1], L.w[0][2], L.w[1][2]})
+    if (x != SC_LINK_FULL && x != SC_LINK_NONE) return unsupported("windowed cross-group link");
+  if (max_qgroup_len + 1 > GROWS) return unsupported("query group longer than 31 rows");
+  if (tile_rows != BM || !seq_tile_base || !seq_head_base) return unsupported("layout tiles must be 64 rows");
+  if (((uintptr_t)a.q | (uintptr_t)a.k | (uintptr_t)a.v | (uintptr_t)a.out) & 15)
+    return unsupported("16-byte alignment");
+  if ((a.ld * 2) % 16 || a.ld_out % 2) return unsupported("row strides");
+  const int fneed = full_rows_needed(L, max_qgroup_len);
+  const size_t need = band_workspace_bytes(a.nseq, a.T, a.H, a.d, tile_rows, max_qgroup_len, L);
+  if (need > ws_bytes || (need && !ws)) return unsupported("workspace too small");
+
+  CUtensorMap mQ, mQf, mKg, mVg, mKb, mVb;
+  const int64_t cols = (int64_t)a.H * D;
+  if (!make_map(&mQ, a.q, cols, a.T, a.ld, BM) || !make_map(&mQf, a.q, cols, a.T, a.ld, GROWS) ||
+      !make_map(&mKg, a.k, cols, a.T, a.ld, GROWS) || !make_map(&mVg, a.v, cols, a.T, a.ld, GROWS) ||
+      !make_map(&mKb, a.k, cols, a.T, a.ld, BM + 2 * w) || !make_map(&mVb, a.v, cols, a.T, a.ld, BM + 2 * w))
+    return unsupported("cuTensorMapEncodeTiled failed");
+
+  Params p;
+  p.nseq = a.nseq; p.H = a.H; p.w = w; p.nbc = (16 + 2 * w + 31) / 32; p.kb_rows = kb_rows_for(w);
+  p.fneed = fneed; p.fmax = fneed; p.padding = a.padding;
+  p.link_cls = L.w[2][0] == SC_LINK_FULL; p.link_query = L.w[2][1] == SC_LINK_FULL;
+  p.scale_log2 = 1.4426950408889634f / a.scale;
+  p.cu = a.cu; p.qlen = a.qlen; p.tile_base = seq_tile_base;
+  p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
+  p.partials = static_cast<float*>(ws);
+
+  const int stage_bytes = (BM + 3 * GROWS + 2 * p.kb_rows) * ROWB;
+  const size_t smem = (size_t)NSTAGE * stage_bytes + 2 * NSTAGE * 8 + 1024;
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    if (cudaFuncSetAttribute(band_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return unsupported("shared memory request");
+    smem_set = smem;
+  }
+  const unsigned grid = (unsigned)((a.T + BM - 1) / BM + a.nseq);
+  band_attn_kernel<<<grid, NTHREADS, smem, st>>>(mQ, mQf, mKg, mVg, mKb, mVb, p);
+  SC_CHECK_LAUNCH("band_attn_kernel");
+
+  // Head rows (cls + query group): generic kernel, doc keys via the partials.
+  AttnArgs h = a;
+  h.head_base = seq_head_base;
+  h.n_head_rows = a.nseq * (1 + max_qgroup_len);
+  h.partials = static_cast<const float*>(ws);
+  h.tile_base = seq_tile_base;
+  h.fmax = fneed;
+  return launch_attn_generic(h, dtype, st);
+}
+
 }  // namespace sc

@@ -98,20 +98,27 @@ attn_generic_kernel(AttnArgs a) {
   __shared__ float qs_all[kGenWarps][kMaxD];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t item = (int64_t)blockIdx.x * kGenWarps + warp;
-  const int row = a.row_begin + (int)(item / a.H);
   const int h = (int)(item % a.H);
-  if (row >= a.row_end) return;
+  int row, j;
+  if (a.head_base) {  // head-row mode: item -> (sequence, cls/query row)
+    const int hr = (int)(item / a.H);
+    if (hr >= a.n_head_rows || hr >= __ldg(a.head_base + a.nseq)) return;
+    j = find_seq(a.head_base, a.nseq, hr);
+    row = __ldg(a.cu + j) + (hr - __ldg(a.head_base + j));
+  } else {
+    row = a.row_begin + (int)(item / a.H);
+    if (row >= a.row_end) return;
+    j = find_seq(a.cu, a.nseq, row);
+  }
 
   const T* Q = static_cast<const T*>(a.q);
   const T* K = static_cast<const T*>(a.k);
   const T* V = static_cast<const T*>(a.v);
   const int d = a.d, hoff = h * d;
 
-  const int j = find_seq(a.cu, a.nseq, row);
   const SeqGroups g = seq_groups(a.cu, a.qlen, j);
   const int i = row - g.start;
   const int gs = i == 0 ? 0 : (i < 1 + g.len[1] ? 1 : 2);
-  if (a.only_group >= 0 && gs != a.only_group) return;
   const int rs = i - g.off[gs];
   const bool qds = a.glob_cu != nullptr;
   const bool src_global = qds && gs == 2 && a.flags && (a.flags[row] & 1);
@@ -166,6 +173,26 @@ attn_generic_kernel(AttnArgs a) {
       }
       continue;
     }
+    if (tg == 2 && w == SC_LINK_FULL && a.partials && i < a.fmax) {
+      // Doc keys already reduced per tile by the band kernel: merge (m, l, acc).
+      const int tb = __ldg(a.tile_base + j), te = __ldg(a.tile_base + j + 1);
+      for (int t = tb; t < te; ++t) {
+        const float* rec = a.partials + (((int64_t)t * a.H + h) * a.fmax + i) * (d + 2);
+        float mt = rec[0], lt = rec[1];
+        if (!(lt > 0.f)) continue;
+        float mnew = fmaxf(st.m, mt);
+        float alpha = st.m == -INFINITY ? 0.f : expf(st.m - mnew);
+        float beta = expf(mt - mnew);
+        st.l = st.l * alpha + (lane == 0 ? lt * beta : 0.f);
+#pragma unroll
+        for (int e = 0; e < kMaxD / 32; ++e) {
+          int c = lane + 32 * e;
+          st.acc[e] = st.acc[e] * alpha + (c < d ? beta * rec[2 + c] : 0.f);
+        }
+        st.m = mnew;
+      }
+      continue;
+    }
     const int len = g.len[tg];
     int lo = 0, hi = len;
     if (w >= 0) { lo = max(0, rs - w); hi = min(len, rs + w + 1); }
@@ -196,7 +223,8 @@ attn_generic_kernel(AttnArgs a) {
 }
 
 int launch_attn_generic(const AttnArgs& a, int dtype, cudaStream_t st) {
-  int64_t items = (int64_t)(a.row_end - a.row_begin) * a.H;
+  int64_t rows = a.head_base ? a.n_head_rows : (a.row_end - a.row_begin);
+  int64_t items = rows * a.H;
   if (items <= 0) return SC_OK;
   unsigned blocks = (unsigned)((items + kGenWarps - 1) / kGenWarps);
   if (dtype == SC_DTYPE_F32)

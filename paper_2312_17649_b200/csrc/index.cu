@@ -21,14 +21,17 @@ void set_error(const char* fmt, ...) {
 // Single-CTA scan over sequences: doc-row tile prefix and QDS global counts.
 __global__ void seq_prefix_kernel(const int32_t* __restrict__ cu, const int32_t* __restrict__ qlen,
                                   int nseq, int tile_rows, int qds_every,
-                                  int32_t* __restrict__ tile_base, int32_t* __restrict__ glob_cu) {
+                                  int32_t* __restrict__ tile_base, int32_t* __restrict__ head_base,
+                                  int32_t* __restrict__ glob_cu) {
   __shared__ int32_t s_t[1024];
   __shared__ int32_t s_g[1024];
-  int carry_t = 0, carry_g = 0;
+  __shared__ int32_t s_h[1024];
+  int carry_t = 0, carry_g = 0, carry_h = 0;
   for (int base = 0; base < nseq; base += blockDim.x) {
     int j = base + threadIdx.x;
-    int nt = 0, ng = 0;
+    int nt = 0, ng = 0, nh = 0;
     if (j < nseq) {
+      nh = 1 + qlen[j];
       int s = cu[j + 1] - cu[j];
       int doc = s - 1 - qlen[j];
       nt = (doc + tile_rows - 1) / tile_rows;
@@ -36,26 +39,32 @@ __global__ void seq_prefix_kernel(const int32_t* __restrict__ cu, const int32_t*
     }
     s_t[threadIdx.x] = nt;
     s_g[threadIdx.x] = ng;
+    s_h[threadIdx.x] = nh;
     __syncthreads();
     // Hillis-Steele inclusive scan (blockDim <= 1024).
     for (int o = 1; o < blockDim.x; o <<= 1) {
       int at = threadIdx.x >= o ? s_t[threadIdx.x - o] : 0;
       int ag = threadIdx.x >= o ? s_g[threadIdx.x - o] : 0;
+      int ah = threadIdx.x >= o ? s_h[threadIdx.x - o] : 0;
       __syncthreads();
       s_t[threadIdx.x] += at;
       s_g[threadIdx.x] += ag;
+      s_h[threadIdx.x] += ah;
       __syncthreads();
     }
     if (j < nseq) {
       tile_base[j + 1] = carry_t + s_t[threadIdx.x];
+      if (head_base) head_base[j + 1] = carry_h + s_h[threadIdx.x];
       if (glob_cu) glob_cu[j + 1] = carry_g + s_g[threadIdx.x];
     }
     carry_t += s_t[blockDim.x - 1];
     carry_g += s_g[blockDim.x - 1];
+    carry_h += s_h[blockDim.x - 1];
     __syncthreads();
   }
   if (threadIdx.x == 0) {
     tile_base[0] = 0;
+    if (head_base) head_base[0] = 0;
     if (glob_cu) glob_cu[0] = 0;
   }
 }
@@ -144,8 +153,9 @@ extern "C" int sc_version(void) { return 10000; }
 extern "C" int sc_index_build(const int32_t* cu_seqlens, const int32_t* qgroup_len, int32_t nseq,
                               int32_t total_tokens, int32_t tile_rows, int32_t qds_every,
                               int32_t* tok_seq, int32_t* tok_group, int32_t* tok_rel,
-                              int32_t* tok_pos, int32_t* seq_tile_base, uint8_t* tok_flags,
-                              int32_t* glob_cu, int32_t* glob_pos, void* stream) {
+                              int32_t* tok_pos, int32_t* seq_tile_base, int32_t* seq_head_base,
+                              uint8_t* tok_flags, int32_t* glob_cu, int32_t* glob_pos,
+                              void* stream) {
   SC_CHECK_ARG(cu_seqlens && qgroup_len, "sc_index_build: null layout pointer");
   SC_CHECK_ARG(nseq >= 1 && total_tokens >= 3 * nseq, "sc_index_build: bad nseq/total_tokens");
   SC_CHECK_ARG(tile_rows >= 1, "sc_index_build: tile_rows must be >= 1");
@@ -155,7 +165,8 @@ extern "C" int sc_index_build(const int32_t* cu_seqlens, const int32_t* qgroup_l
                "sc_index_build: qds_every > 0 needs tok_flags, glob_cu, glob_pos");
   cudaStream_t st = (cudaStream_t)stream;
   seq_prefix_kernel<<<1, 1024, 0, st>>>(cu_seqlens, qgroup_len, nseq, tile_rows, qds_every,
-                                        seq_tile_base, qds_every > 0 ? glob_cu : nullptr);
+                                        seq_tile_base, seq_head_base,
+                                        qds_every > 0 ? glob_cu : nullptr);
   SC_CHECK_LAUNCH("seq_prefix_kernel");
   token_index_kernel<<<(total_tokens + 255) / 256, 256, 0, st>>>(
       cu_seqlens, qgroup_len, nseq, total_tokens, qds_every, tok_seq, tok_group, tok_rel, tok_pos,

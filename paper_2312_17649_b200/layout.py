@@ -49,6 +49,8 @@ class PackedLayout:
         self.tok_rel = torch.empty(T, **i32)
         self.tok_pos = torch.empty(T, **i32)
         self.seq_tile_base = torch.empty(self.nseq + 1, **i32)
+        self.seq_head_base = torch.empty(self.nseq + 1, **i32)
+        self.max_qgroup_len = int(self.qlen_host.max())
         self.tok_flags = self.glob_cu = self.glob_pos = None
         if self.qds_every or qds_positions is not None:
             self.tok_flags = torch.zeros(T, dtype=torch.uint8, device=dev)
@@ -57,7 +59,7 @@ class PackedLayout:
         _lib.call("sc_index_build", self.cu_seqlens.data_ptr(), self.qgroup_len.data_ptr(), self.nseq,
                   T, self.tile_rows, self.qds_every if qds_positions is None else 0,
                   self.tok_seq.data_ptr(), self.tok_group.data_ptr(), self.tok_rel.data_ptr(),
-                  self.tok_pos.data_ptr(), self.seq_tile_base.data_ptr(),
+                  self.tok_pos.data_ptr(), self.seq_tile_base.data_ptr(), self.seq_head_base.data_ptr(),
                   _lib.ptr(self.tok_flags) if qds_positions is None else None,
                   _lib.ptr(self.glob_cu) if qds_positions is None else None,
                   _lib.ptr(self.glob_pos) if qds_positions is None else None,
@@ -101,11 +103,11 @@ class PackedLayout:
             raise LayoutError("packed batch exceeds int32 token indexing")
         return cls(cu, qgroup_lens, device, tile_rows, qds_every, qds_positions)
 
-    def attn_workspace(self, heads: int, head_dim: int):
-        key = (heads, head_dim)
+    def attn_workspace(self, heads: int, head_dim: int, links: np.ndarray):
+        key = (heads, head_dim, links.tobytes())
         if key not in self._ws:
             n = _lib.load().sc_attn_workspace_bytes(self.nseq, self.total_tokens, heads, head_dim,
-                                                    self.tile_rows)
+                                                    self.tile_rows, self.max_qgroup_len, links.ctypes.data)
             self._ws[key] = torch.empty(n, dtype=torch.uint8, device=self.device) if n else None
         return self._ws[key]
 
