@@ -66,6 +66,8 @@ extern "C" {
 
 SC_API const char* sc_last_error(void);
 SC_API int sc_version(void);
+/* Kernels launched by this library so far in this process (all streams). */
+SC_API uint64_t sc_kernel_launches(void);
 
 /* ---- K1: device index / mask construction ------------------------------ */
 

@@ -44,6 +44,7 @@ _f32 = C.c_float
 SIGNATURES = {
     "sc_last_error": (C.c_char_p, []),
     "sc_version": (C.c_int, []),
+    "sc_kernel_launches": (C.c_uint64, []),
     "sc_index_build": (C.c_int, [_p, _p, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "sc_mask_export": (C.c_int, [_p, _p, _i32, _i32, _i32, _p, _p, _p, _p]),
     "sc_band_validity": (C.c_int, [_i32, _i32, _i32, _p, _p]),
@@ -60,7 +61,13 @@ SIGNATURES = {
 }
 
 # Entry points that launch device work (counted for the bench's gpu_launches).
-LAUNCHING = {n for n in SIGNATURES if n not in ("sc_last_error", "sc_version", "sc_attn_workspace_bytes")}
+LAUNCHING = {n for n in SIGNATURES
+             if n not in ("sc_last_error", "sc_version", "sc_kernel_launches", "sc_attn_workspace_bytes")}
+
+
+def kernel_launches() -> int:
+    """Kernels launched by the library in this process (the library's own counter)."""
+    return int(load().sc_kernel_launches())
 
 
 class LibraryNotBuiltError(RuntimeError):

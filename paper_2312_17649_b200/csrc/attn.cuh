@@ -27,9 +27,10 @@ struct AttnArgs {
   // link is served by merging the band kernel's per-tile partials.
   const int32_t* head_base;  // [nseq+1] or nullptr for all-rows mode
   int n_head_rows;
-  const float* partials;     // [tiles][H][fmax][d+2]: (m, l, acc[d]); nullptr = scan doc keys
+  const float* partials;     // [tiles*rec_per_tile][H][fmax][d+2]: (m, l, acc[d]); nullptr = scan doc keys
   const int32_t* tile_base;  // [nseq+1]
   int fmax;
+  int rec_per_tile;          // partial records per doc tile (one per 16-row warp block)
 };
 
 bool load_links(const int32_t* links, Links* L);

@@ -6,15 +6,15 @@
 // stages in shared memory:
 //   Q   [64 x 64]        doc rows r0..r0+63
 //   Kb/Vb [64+2w x 64]   doc rows r0-w .. r0+63+w  (the band halo)
-//   Kg/Vg [32 x 64]      the sequence's cls + query-group rows (global keys)
-//   Qf  [32 x 64]        the same rows as queries ("full rows": CLS, and query
+//   Kg/Vg [GR x 64]      the sequence's cls + query-group rows (global keys)
+//   Qf  [GR x 64]        the same rows as queries ("full rows": CLS, and query
 //                        rows under longformer/full, that attend the whole doc)
 // Warps 0-3 each own 16 doc rows: S = Q K^T over {global keys} U {band keys}
-// with mma.sync m16n8k16 (bf16 -> fp32), band/validity mask, online softmax
-// in the exp2 domain, O += P V, bf16 stores.  Warp 4 computes split-softmax
-// partials (m, l, acc) of the full rows over this tile's own 64 doc keys,
+// with mma.sync m16n8k16 (bf16 -> fp32), static band mask, online softmax in
+// the exp2 domain, O += P V, bf16 stores.  Then each warp emits the
+// split-softmax partial (m, l, acc) of the full rows over its own 16 doc keys,
 // so the CLS row never re-reads K/V from HBM; the head-row pass of the
-// generic kernel merges them.  Warp 5 is the TMA producer.
+// generic kernel merges them.  Warp 4 is the TMA producer.
 //
 // Semantics: doc row r attends cls (if linked), query group (if linked) and
 // doc keys t with |t - r| <= w, 0 <= t < n_doc (R/band.py:48-52,
@@ -31,17 +31,16 @@ namespace bandk {
 constexpr int BM = 64;
 constexpr int D = 64;
 constexpr int ROWB = 128;  // bytes per smem row
-constexpr int GROWS = 32;  // global rows staged per head
 constexpr int NSTAGE = 2;
-constexpr int PRODW = 5;
-constexpr int FULLW = 4;
-constexpr int NTHREADS = 192;
+constexpr int NDOCW = 4;
+constexpr int PRODW = 4;
+constexpr int NTHREADS = 160;
 constexpr int MAX_W = 96;  // Kb box rows 64 + 2w <= 256 (TMA box limit)
 
 struct Params {
-  int nseq, H, w, nbc, kb_rows, fneed, fmax, padding;
+  int nseq, H, w, kb_rows, fneed, fmax, padding;
   int link_cls, link_query;
-  float scale_log2;
+  float c2;  // log2(e) / scale: raw logit -> exp2 domain
   const int32_t* cu;
   const int32_t* qlen;
   const int32_t* tile_base;
@@ -109,6 +108,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ float ex2(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
 // A fragments of a 16-row x 64-dim Q block starting at smem row `row0`.
 __device__ __forceinline__ void load_q(uint32_t buf, int row0, int lane, uint32_t (&qa)[4][4]) {
@@ -116,10 +120,12 @@ __device__ __forceinline__ void load_q(uint32_t buf, int row0, int lane, uint32_
   for (int ks = 0; ks < 4; ++ks) ldsm_x4(swz(buf, row0 + (lane & 15), ks * 2 + (lane >> 4)), qa[ks]);
 }
 
-// S[2 n8 blocks] += Q(16x64) . K[key0 .. key0+15]^T
+// S[2 n8 blocks] = Q(16x64) . K[key0 .. key0+15]^T
 __device__ __forceinline__ void qk16(uint32_t kbuf, int key0, int lane, const uint32_t (&qa)[4][4],
                                      float (&s0)[4], float (&s1)[4]) {
   const int krow = key0 + (lane & 7) + ((lane >> 4) << 3);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s0[e] = s1[e] = 0.f;
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
     uint32_t b[4];
@@ -144,11 +150,11 @@ __device__ __forceinline__ void pv16(uint32_t vbuf, int key0, int lane, const fl
   }
 }
 
-// Online-softmax update for NB n8 score blocks of rows (g, g+8); scores already
-// scaled to the log2 domain and masked to -inf.  Overwrites s with P.
+// Online-softmax update over NB n8 blocks of RAW logits (masked to -inf) for
+// rows (g, g+8).  m is kept in raw-logit units; c2 = log2(e)/scale.  Overwrites s with P.
 template <int NB>
-__device__ __forceinline__ void softmax_update(float (&s)[NB][4], float& m0, float& m1, float& l0,
-                                               float& l1, float (&o)[8][4]) {
+__device__ __forceinline__ void softmax_update(float (&s)[NB][4], float c2, float& m0, float& m1,
+                                               float& l0, float& l1, float (&o)[8][4]) {
   float x0 = -INFINITY, x1 = -INFINITY;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
@@ -160,20 +166,20 @@ __device__ __forceinline__ void softmax_update(float (&s)[NB][4], float& m0, flo
   x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, 1));
   x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, 2));
   const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);
-  const float b0 = n0 == -INFINITY ? 0.f : n0, b1 = n1 == -INFINITY ? 0.f : n1;
-  const float a0 = exp2f(m0 - b0), a1 = exp2f(m1 - b1);
+  const float b0 = n0 == -INFINITY ? 0.f : n0 * c2, b1 = n1 == -INFINITY ? 0.f : n1 * c2;
+  const float a0 = ex2(fmaf(m0, c2, -b0)), a1 = ex2(fmaf(m1, c2, -b1));
   float r0 = 0.f, r1 = 0.f;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    s[b][0] = exp2f(s[b][0] - b0);
-    s[b][1] = exp2f(s[b][1] - b0);
-    s[b][2] = exp2f(s[b][2] - b1);
-    s[b][3] = exp2f(s[b][3] - b1);
+    s[b][0] = ex2(fmaf(s[b][0], c2, -b0));
+    s[b][1] = ex2(fmaf(s[b][1], c2, -b0));
+    s[b][2] = ex2(fmaf(s[b][2], c2, -b1));
+    s[b][3] = ex2(fmaf(s[b][3], c2, -b1));
     r0 += s[b][0] + s[b][1];
     r1 += s[b][2] + s[b][3];
   }
-  l0 = l0 * a0 + r0;
-  l1 = l1 * a1 + r1;
+  l0 = fmaf(l0, a0, r0);
+  l1 = fmaf(l1, a1, r1);
 #pragma unroll
   for (int nb = 0; nb < 8; ++nb) {
     o[nb][0] *= a0;
@@ -185,7 +191,15 @@ __device__ __forceinline__ void softmax_update(float (&s)[NB][4], float& m0, flo
   m1 = n1;
 }
 
-__global__ void __launch_bounds__(NTHREADS) band_attn_kernel(
+__device__ __forceinline__ void zero_o(float (&o)[8][4]) {
+#pragma unroll
+  for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
+}
+
+// NBC: band chunks of 32 keys per 16-row warp block (ceil((16+2w)/32)).
+// GR: global rows staged per head (16 or 32).
+template <int NBC, int GR>
+__global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQf,
     const __grid_constant__ CUtensorMap tmKg, const __grid_constant__ CUtensorMap tmVg,
     const __grid_constant__ CUtensorMap tmKb, const __grid_constant__ CUtensorMap tmVb, Params p) {
@@ -201,9 +215,12 @@ __global__ void __launch_bounds__(NTHREADS) band_attn_kernel(
   const int rows_here = min(BM, n_doc - r0);
   const int doc_row0 = g.start + g.off[2] + r0;
   const int G = 1 + g.len[1];
+  const int w = p.w;
+  constexpr int kb_rows = 48 + 32 * NBC;
+  constexpr int q_bytes = BM * ROWB, f_bytes = GR * ROWB, kb_bytes = kb_rows * ROWB;
+  constexpr int stage_bytes = q_bytes + 3 * f_bytes + 2 * kb_bytes;
+  const int kb_box = BM + 2 * w;
 
-  const int q_bytes = BM * ROWB, f_bytes = GROWS * ROWB, kb_bytes = p.kb_rows * ROWB;
-  const int stage_bytes = q_bytes + 3 * f_bytes + 2 * kb_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * stage_bytes);
   const uint32_t sm0 = smem_u32(smem);
   auto q_buf = [&](int s) { return sm0 + s * stage_bytes; };
@@ -215,8 +232,6 @@ __global__ void __launch_bounds__(NTHREADS) band_attn_kernel(
   const uint32_t full_bar = smem_u32(bars), empty_bar = smem_u32(bars + NSTAGE);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int w = p.w;
-  const int kb_box = BM + 2 * w;
 
   // Zero the Kb/Vb rows the TMA box never writes (band chunks read up to kb_rows).
   for (int s = 0; s < NSTAGE; ++s) {
@@ -229,7 +244,7 @@ __global__ void __launch_bounds__(NTHREADS) band_attn_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(full_bar + 8 * s, 1);
-      mbar_init(empty_bar + 8 * s, 5);
+      mbar_init(empty_bar + 8 * s, NDOCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -248,149 +263,175 @@ __global__ void __launch_bounds__(NTHREADS) band_attn_kernel(
         mbar_expect_tx(fb, bytes);
         const int col = h * D;
         tma_load_2d(q_buf(s), &tmQ, col, doc_row0, fb);
-        tma_load_2d(qf_buf(s), &tmQf, col, g.start, fb);
-        tma_load_2d(kg_buf(s), &tmKg, col, g.start, fb);
-        tma_load_2d(vg_buf(s), &tmVg, col, g.start, fb);
         tma_load_2d(kb_buf(s), &tmKb, col, doc_row0 - w, fb);
         tma_load_2d(vb_buf(s), &tmVb, col, doc_row0 - w, fb);
+        tma_load_2d(kg_buf(s), &tmKg, col, g.start, fb);
+        tma_load_2d(vg_buf(s), &tmVg, col, g.start, fb);
+        tma_load_2d(qf_buf(s), &tmQf, col, g.start, fb);
       }
     }
     return;
   }
 
+  // ------------------------------------------------------------ doc warps
   const int gq = lane >> 2, tq = lane & 3;
+  const int wr0 = warp * 16;
+  const bool active = wr0 < rows_here;
+  const int ra = r0 + wr0 + gq, rb = ra + 8;  // doc-relative rows of this thread
 
-  if (warp < 4) {
-    // ------------------------------------------------------------ doc rows
-    const int wr0 = warp * 16;
-    const bool active = wr0 < rows_here;
-    const int ra = r0 + wr0 + gq, rb = ra + 8;  // doc-relative rows of this thread
-    float ninv_a = 0.f, ninv_b = 0.f;
-    if (p.padding == SC_PAD_ZERO_LOGIT && tq == 0) {
-      ninv_a = (float)(2 * w + 1 - max(0, min(n_doc, ra + w + 1) - max(0, ra - w)));
-      ninv_b = (float)(2 * w + 1 - max(0, min(n_doc, rb + w + 1) - max(0, rb - w)));
-    }
-    for (int h = 0; h < p.H; ++h) {
-      const int s = h % NSTAGE;
-      mbar_wait(full_bar + 8 * s, (h / NSTAGE) & 1);
-      if (active) {
-        uint32_t qa[4][4];
-        load_q(q_buf(s), wr0, lane, qa);
-        float o[8][4];
+  // Static masks (tile independent except at sequence edges): bit (nb*4 + e)
+  // of bmask[bc] / gmask[gc] set when that score element is a valid key.
+  uint32_t bmask[NBC];
+  const bool edge = (r0 - w + wr0 < 0) || (r0 - w + wr0 + 32 * NBC > n_doc);
 #pragma unroll
-        for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
-        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-        if (p.padding == SC_PAD_ZERO_LOGIT) {  // virtual logit-0 slots (same on all quad lanes)
-          float na = __shfl_sync(0xffffffffu, ninv_a, lane & ~3);
-          float nbv = __shfl_sync(0xffffffffu, ninv_b, lane & ~3);
-          if (na > 0.f) { m0 = 0.f; l0 = ninv_a; }
-          if (nbv > 0.f) { m1 = 0.f; l1 = ninv_b; }
-        }
-        // global keys: cls (key 0) and the query group (keys 1..G-1)
-        for (int gc = 0; gc * 16 < G; ++gc) {
-          float sc[2][4] = {};
+  for (int bc = 0; bc < NBC; ++bc) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int c = 32 * bc + nb * 8 + 2 * tq + (e & 1);
+        const int diff = c - (gq + ((e >> 1) << 3));  // t - r + w
+        const int t = r0 - w + wr0 + c;
+        bool ok = diff >= 0 && diff <= 2 * w;
+        if (edge) ok = ok && t >= 0 && t < n_doc;
+        m |= (ok ? 1u : 0u) << (nb * 4 + e);
+      }
+    bmask[bc] = m;
+  }
+  uint32_t gmask[GR / 16];
+#pragma unroll
+  for (int gc = 0; gc < GR / 16; ++gc) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int kg = gc * 16 + nb * 8 + 2 * tq + (e & 1);
+        const bool ok = kg < G && (kg == 0 ? p.link_cls : p.link_query);
+        m |= (ok ? 1u : 0u) << (nb * 4 + e);
+      }
+    gmask[gc] = m;
+  }
+  // Own-key mask for the full-row partials (keys wr0 .. wr0+15 of this tile).
+  uint32_t fmask = 0;
+#pragma unroll
+  for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      fmask |= ((wr0 + nb * 8 + 2 * tq + (e & 1)) < rows_here ? 1u : 0u) << (nb * 4 + e);
+
+  float ninv_a = 0.f, ninv_b = 0.f;
+  if (p.padding == SC_PAD_ZERO_LOGIT) {
+    ninv_a = (float)(2 * w + 1 - max(0, min(n_doc, ra + w + 1) - max(0, ra - w)));
+    ninv_b = (float)(2 * w + 1 - max(0, min(n_doc, rb + w + 1) - max(0, rb - w)));
+  }
+  const float c2 = p.c2;
+  const int nglob = (G + 15) / 16;
+
+  for (int h = 0; h < p.H; ++h) {
+    const int s = h % NSTAGE;
+    mbar_wait(full_bar + 8 * s, (h / NSTAGE) & 1);
+    if (active) {
+      uint32_t qa[4][4];
+      load_q(q_buf(s), wr0, lane, qa);
+      float o[8][4];
+      zero_o(o);
+      float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+      if (ninv_a > 0.f) { m0 = 0.f; l0 = tq == 0 ? ninv_a : 0.f; }
+      if (ninv_b > 0.f) { m1 = 0.f; l1 = tq == 0 ? ninv_b : 0.f; }
+      // global keys: cls (key 0) and the query group (keys 1..G-1)
+#pragma unroll
+      for (int gc = 0; gc < GR / 16; ++gc) {
+        if (gc < nglob) {
+          float sc[2][4];
           qk16(kg_buf(s), gc * 16, lane, qa, sc[0], sc[1]);
 #pragma unroll
           for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int kg = gc * 16 + nb * 8 + 2 * tq + (e & 1);
-              const bool ok = kg < G && (kg == 0 ? p.link_cls : p.link_query);
-              sc[nb][e] = ok ? sc[nb][e] * p.scale_log2 : -INFINITY;
-            }
-          softmax_update<2>(sc, m0, m1, l0, l1, o);
+            for (int e = 0; e < 4; ++e)
+              if (!((gmask[gc] >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+          softmax_update<2>(sc, c2, m0, m1, l0, l1, o);
           pv16(vg_buf(s), gc * 16, lane, sc[0], sc[1], o);
         }
-        // band keys: Kb row 0 = doc row r0 - w; this warp reads rows wr0 + [0, 32*nbc)
-        for (int bc = 0; bc < p.nbc; ++bc) {
-          const int kb0 = wr0 + 32 * bc;
-          float sc[4][4] = {};
-          qk16(kb_buf(s), kb0, lane, qa, sc[0], sc[1]);
-          qk16(kb_buf(s), kb0 + 16, lane, qa, sc[2], sc[3]);
+      }
+      // band keys: Kb row 0 = doc row r0 - w; this warp reads rows wr0 + [0, 32*NBC)
 #pragma unroll
-          for (int nb = 0; nb < 4; ++nb)
+      for (int bc = 0; bc < NBC; ++bc) {
+        const int kb0 = wr0 + 32 * bc;
+        float sc[4][4];
+        qk16(kb_buf(s), kb0, lane, qa, sc[0], sc[1]);
+        qk16(kb_buf(s), kb0 + 16, lane, qa, sc[2], sc[3]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int c = 32 * bc + nb * 8 + 2 * tq + (e & 1);  // key offset from wr0 row base
-              const int ri = gq + ((e >> 1) << 3);                   // row within the 16
-              const int diff = c - ri;                               // t - r + w
-              const int t = r0 - w + wr0 + c;                        // doc-relative key
-              const bool ok = diff >= 0 && diff <= 2 * w && t >= 0 && t < n_doc;
-              sc[nb][e] = ok ? sc[nb][e] * p.scale_log2 : -INFINITY;
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (!((bmask[bc] >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+        softmax_update<4>(sc, c2, m0, m1, l0, l1, o);
+        pv16(vb_buf(s), kb0, lane, sc[0], sc[1], o);
+        pv16(vb_buf(s), kb0 + 16, lane, sc[2], sc[3], o);
+      }
+      l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+      l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+      const float i0 = 1.f / l0, i1 = 1.f / l1;
+      __nv_bfloat16* out_h = p.out + h * D + 2 * tq;
+      if (ra < n_doc) {
+        uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq) * p.ld_out);
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][0] * i0, o[nb][1] * i0);
+      }
+      if (rb < n_doc) {
+        uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq + 8) * p.ld_out);
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][2] * i1, o[nb][3] * i1);
+      }
+
+      // Full-row split-softmax partials over this warp's own 16 doc keys.
+#pragma unroll
+      for (int fc = 0; fc < GR / 16; ++fc) {
+        if (fc * 16 < p.fneed) {
+          load_q(qf_buf(s), fc * 16, lane, qa);
+          float sc[2][4];
+          qk16(kb_buf(s), w + wr0, lane, qa, sc[0], sc[1]);
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (!((fmask >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+          zero_o(o);
+          float fm0 = -INFINITY, fm1 = -INFINITY, fl0 = 0.f, fl1 = 0.f;
+          softmax_update<2>(sc, c2, fm0, fm1, fl0, fl1, o);
+          pv16(vb_buf(s), w + wr0, lane, sc[0], sc[1], o);
+          fl0 += __shfl_xor_sync(0xffffffffu, fl0, 1);
+          fl0 += __shfl_xor_sync(0xffffffffu, fl0, 2);
+          fl1 += __shfl_xor_sync(0xffffffffu, fl1, 1);
+          fl1 += __shfl_xor_sync(0xffffffffu, fl1, 2);
+          const float to_nat = c2 * 0.69314718055994530942f;  // raw logit -> natural units (1/scale)
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const int f = fc * 16 + gq + 8 * half;
+            if (f >= p.fneed) continue;
+            float* rec = p.partials + ((((int64_t)tile * NDOCW + warp) * p.H + h) * p.fmax + f) * (D + 2);
+            if (tq == 0) {
+              rec[0] = (half ? fm1 : fm0) * to_nat;
+              rec[1] = half ? fl1 : fl0;
             }
-          softmax_update<4>(sc, m0, m1, l0, l1, o);
-          pv16(vb_buf(s), kb0, lane, sc[0], sc[1], o);
-          pv16(vb_buf(s), kb0 + 16, lane, sc[2], sc[3], o);
-        }
-        l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-        l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-        l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-        l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-        const float i0 = 1.f / l0, i1 = 1.f / l1;
-        __nv_bfloat16* out_h = p.out + h * D + 2 * tq;
-        if (ra < n_doc) {
-          uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq) * p.ld_out);
 #pragma unroll
-          for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][0] * i0, o[nb][1] * i0);
-        }
-        if (rb < n_doc) {
-          uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq + 8) * p.ld_out);
-#pragma unroll
-          for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][2] * i1, o[nb][3] * i1);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty_bar + 8 * s);
-    }
-  } else {
-    // ------------------------------------------- full-row split-softmax partials
-    for (int h = 0; h < p.H; ++h) {
-      const int s = h % NSTAGE;
-      mbar_wait(full_bar + 8 * s, (h / NSTAGE) & 1);
-      for (int fc = 0; fc * 16 < p.fneed; ++fc) {
-        uint32_t qa[4][4];
-        load_q(qf_buf(s), fc * 16, lane, qa);
-        float sc[8][4] = {};
-#pragma unroll
-        for (int np = 0; np < 4; ++np) qk16(kb_buf(s), w + np * 16, lane, qa, sc[2 * np], sc[2 * np + 1]);
-#pragma unroll
-        for (int nb = 0; nb < 8; ++nb)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = nb * 8 + 2 * tq + (e & 1);
-            sc[nb][e] = c < rows_here ? sc[nb][e] * p.scale_log2 : -INFINITY;
-          }
-        float o[8][4];
-#pragma unroll
-        for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
-        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-        softmax_update<8>(sc, m0, m1, l0, l1, o);
-#pragma unroll
-        for (int kp = 0; kp < 4; ++kp) pv16(vb_buf(s), w + kp * 16, lane, sc[2 * kp], sc[2 * kp + 1], o);
-        l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-        l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-        l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-        l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-        constexpr float kLn2 = 0.69314718055994530942f;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          const int f = fc * 16 + gq + 8 * half;
-          if (f >= p.fneed) continue;
-          float* rec = p.partials + (((int64_t)tile * p.H + h) * p.fmax + f) * (D + 2);
-          if (tq == 0) {
-            rec[0] = (half ? m1 : m0) * kLn2;
-            rec[1] = half ? l1 : l0;
-          }
-#pragma unroll
-          for (int nb = 0; nb < 8; ++nb) {
-            rec[2 + nb * 8 + 2 * tq] = o[nb][2 * half];
-            rec[2 + nb * 8 + 2 * tq + 1] = o[nb][2 * half + 1];
+            for (int nb = 0; nb < 8; ++nb)
+              *reinterpret_cast<float2*>(rec + 2 + nb * 8 + 2 * tq) =
+                  make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty_bar + 8 * s);
+    } else if (p.fneed > 0) {
+      // No own keys in this block: mark its partial records empty.
+      for (int f = lane; f < p.fneed; f += 32)
+        p.partials[((((int64_t)tile * NDOCW + warp) * p.H + h) * p.fmax + f) * (D + 2) + 1] = 0.f;
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_bar + 8 * s);
   }
 }
 
@@ -423,7 +464,41 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t row
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static int kb_rows_for(int w) { return 48 + 32 * ((16 + 2 * w + 31) / 32); }
+using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, Params);
+
+template <int NBC, int GR>
+static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, cudaStream_t st) {
+  constexpr int stage_bytes = (BM + 3 * GR + 2 * (48 + 32 * NBC)) * ROWB;
+  constexpr size_t smem = (size_t)NSTAGE * stage_bytes + 2 * NSTAGE * 8 + 1024;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(band_attn_kernel<NBC, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess) {
+      set_error("band kernel: shared memory request of %zu bytes failed", smem);
+      return SC_ERR_UNSUPPORTED;
+    }
+    attr = true;
+  }
+  band_attn_kernel<NBC, GR><<<grid, NTHREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4],
+                                                          maps[5], p);
+  SC_CHECK_LAUNCH("band_attn_kernel");
+  return SC_OK;
+}
+
+template <int GR>
+static int launch_gr(int nbc, const CUtensorMap* maps, const Params& p, unsigned grid, cudaStream_t st) {
+  switch (nbc) {
+    case 1: return launch_one<1, GR>(maps, p, grid, st);
+    case 2: return launch_one<2, GR>(maps, p, grid, st);
+    case 3: return launch_one<3, GR>(maps, p, grid, st);
+    case 4: return launch_one<4, GR>(maps, p, grid, st);
+    case 5: return launch_one<5, GR>(maps, p, grid, st);
+    case 6: return launch_one<6, GR>(maps, p, grid, st);
+    case 7: return launch_one<7, GR>(maps, p, grid, st);
+  }
+  set_error("band kernel: window too large");
+  return SC_ERR_UNSUPPORTED;
+}
 
 }  // namespace bandk
 
@@ -432,7 +507,7 @@ size_t band_workspace_bytes(int nseq, int T, int H, int d, int tile_rows, int ma
   int f = full_rows_needed(L, max_qgroup_len);
   if (f == 0 || tile_rows <= 0) return 0;
   int64_t tiles = (T + tile_rows - 1) / tile_rows + nseq;
-  return (size_t)tiles * H * f * (d + 2) * sizeof(float);
+  return (size_t)tiles * bandk::NDOCW * H * f * (d + 2) * sizeof(float);
 }
 
 int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
@@ -451,7 +526,7 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   if (w < 0 || w > MAX_W) return unsupported("doc->doc link must be a window <= 96");
   for (int x : {L.w[2][0], L.w[2][1], L.w[0][2], L.w[1][2]})
     if (x != SC_LINK_FULL && x != SC_LINK_NONE) return unsupported("windowed cross-group link");
-  if (max_qgroup_len + 1 > GROWS) return unsupported("query group longer than 31 rows");
+  if (max_qgroup_len + 1 > 32) return unsupported("query group longer than 31 rows");
   if (tile_rows != BM || !seq_tile_base || !seq_head_base) return unsupported("layout tiles must be 64 rows");
   if (((uintptr_t)a.q | (uintptr_t)a.k | (uintptr_t)a.v | (uintptr_t)a.out) & 15)
     return unsupported("16-byte alignment");
@@ -459,34 +534,30 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   const int fneed = full_rows_needed(L, max_qgroup_len);
   const size_t need = band_workspace_bytes(a.nseq, a.T, a.H, a.d, tile_rows, max_qgroup_len, L);
   if (need > ws_bytes || (need && !ws)) return unsupported("workspace too small");
+  const int GR = (max_qgroup_len + 1 <= 16) ? 16 : 32;
 
-  CUtensorMap mQ, mQf, mKg, mVg, mKb, mVb;
+  CUtensorMap maps[6];
   const int64_t cols = (int64_t)a.H * D;
-  if (!make_map(&mQ, a.q, cols, a.T, a.ld, BM) || !make_map(&mQf, a.q, cols, a.T, a.ld, GROWS) ||
-      !make_map(&mKg, a.k, cols, a.T, a.ld, GROWS) || !make_map(&mVg, a.v, cols, a.T, a.ld, GROWS) ||
-      !make_map(&mKb, a.k, cols, a.T, a.ld, BM + 2 * w) || !make_map(&mVb, a.v, cols, a.T, a.ld, BM + 2 * w))
+  if (!make_map(&maps[0], a.q, cols, a.T, a.ld, BM) || !make_map(&maps[1], a.q, cols, a.T, a.ld, GR) ||
+      !make_map(&maps[2], a.k, cols, a.T, a.ld, GR) || !make_map(&maps[3], a.v, cols, a.T, a.ld, GR) ||
+      !make_map(&maps[4], a.k, cols, a.T, a.ld, BM + 2 * w) ||
+      !make_map(&maps[5], a.v, cols, a.T, a.ld, BM + 2 * w))
     return unsupported("cuTensorMapEncodeTiled failed");
 
   Params p;
-  p.nseq = a.nseq; p.H = a.H; p.w = w; p.nbc = (16 + 2 * w + 31) / 32; p.kb_rows = kb_rows_for(w);
+  p.nseq = a.nseq; p.H = a.H; p.w = w;
+  const int nbc = (16 + 2 * w + 31) / 32;
+  p.kb_rows = 48 + 32 * nbc;
   p.fneed = fneed; p.fmax = fneed; p.padding = a.padding;
   p.link_cls = L.w[2][0] == SC_LINK_FULL; p.link_query = L.w[2][1] == SC_LINK_FULL;
-  p.scale_log2 = 1.4426950408889634f / a.scale;
+  p.c2 = 1.4426950408889634f / a.scale;
   p.cu = a.cu; p.qlen = a.qlen; p.tile_base = seq_tile_base;
   p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
   p.partials = static_cast<float*>(ws);
 
-  const int stage_bytes = (BM + 3 * GROWS + 2 * p.kb_rows) * ROWB;
-  const size_t smem = (size_t)NSTAGE * stage_bytes + 2 * NSTAGE * 8 + 1024;
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    if (cudaFuncSetAttribute(band_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return unsupported("shared memory request");
-    smem_set = smem;
-  }
   const unsigned grid = (unsigned)((a.T + BM - 1) / BM + a.nseq);
-  band_attn_kernel<<<grid, NTHREADS, smem, st>>>(mQ, mQf, mKg, mVg, mKb, mVb, p);
-  SC_CHECK_LAUNCH("band_attn_kernel");
+  int rc = GR == 16 ? launch_gr<16>(nbc, maps, p, grid, st) : launch_gr<32>(nbc, maps, p, grid, st);
+  if (rc) return rc;
 
   // Head rows (cls + query group): generic kernel, doc keys via the partials.
   AttnArgs h = a;
@@ -495,6 +566,7 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   h.partials = static_cast<const float*>(ws);
   h.tile_base = seq_tile_base;
   h.fmax = fneed;
+  h.rec_per_tile = NDOCW;
   return launch_attn_generic(h, dtype, st);
 }
 

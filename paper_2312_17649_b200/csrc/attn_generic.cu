@@ -175,21 +175,44 @@ attn_generic_kernel(AttnArgs a) {
     }
     if (tg == 2 && w == SC_LINK_FULL && a.partials && i < a.fmax) {
       // Doc keys already reduced per tile by the band kernel: merge (m, l, acc).
-      const int tb = __ldg(a.tile_base + j), te = __ldg(a.tile_base + j + 1);
-      for (int t = tb; t < te; ++t) {
-        const float* rec = a.partials + (((int64_t)t * a.H + h) * a.fmax + i) * (d + 2);
-        float mt = rec[0], lt = rec[1];
-        if (!(lt > 0.f)) continue;
-        float mnew = fmaxf(st.m, mt);
-        float alpha = st.m == -INFINITY ? 0.f : expf(st.m - mnew);
-        float beta = expf(mt - mnew);
-        st.l = st.l * alpha + (lane == 0 ? lt * beta : 0.f);
+      // Lane-parallel: one global max over all tiles, then independent weighted sums.
+      const int tb = __ldg(a.tile_base + j) * a.rec_per_tile, te = __ldg(a.tile_base + j + 1) * a.rec_per_tile;
+      const int64_t rstride = (int64_t)a.H * a.fmax * (d + 2);
+      const float* rec0 = a.partials + (((int64_t)tb * a.H + h) * a.fmax + i) * (d + 2);
+      float mloc = -INFINITY;
+      for (int t = lane; t < te - tb; t += 32) {
+        const float* rec = rec0 + t * rstride;
+        if (rec[1] > 0.f) mloc = fmaxf(mloc, rec[0]);
+      }
+      const float mtiles = warp_max(mloc);
+      if (mtiles == -INFINITY) continue;
+      const float mnew = fmaxf(st.m, mtiles);
+      const float alpha = st.m == -INFINITY ? 0.f : expf(st.m - mnew);
+      st.l *= alpha;
 #pragma unroll
-        for (int e = 0; e < kMaxD / 32; ++e) {
-          int c = lane + 32 * e;
-          st.acc[e] = st.acc[e] * alpha + (c < d ? beta * rec[2 + c] : 0.f);
+      for (int e = 0; e < kMaxD / 32; ++e) st.acc[e] *= alpha;
+      st.m = mnew;
+      for (int base = 0; base < te - tb; base += 32) {
+        const int t = base + lane;
+        float beta = 0.f;
+        if (t < te - tb) {
+          const float* rec = rec0 + t * rstride;
+          const float lt = rec[1];
+          if (lt > 0.f) {
+            beta = expf(rec[0] - mnew);
+            st.l = fmaf(beta, lt, st.l);
+          }
         }
-        st.m = mnew;
+        const int cnt = min(32, te - tb - base);
+        for (int kk = 0; kk < cnt; ++kk) {
+          const float b = __shfl_sync(0xffffffffu, beta, kk);
+          const float* rec = rec0 + (base + kk) * rstride + 2;
+#pragma unroll
+          for (int e = 0; e < kMaxD / 32; ++e) {
+            int c = lane + 32 * e;
+            if (c < d && b != 0.f) st.acc[e] = fmaf(b, rec[c], st.acc[e]);
+          }
+        }
       }
       continue;
     }

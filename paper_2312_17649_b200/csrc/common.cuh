@@ -22,6 +22,9 @@ void set_error(const char* fmt, ...);
     }                                           \
   } while (0)
 
+// Process-wide count of kernels this library launched (sc_kernel_launches()).
+void count_launch();
+
 #define SC_CHECK_LAUNCH(name)                                                      \
   do {                                                                             \
     cudaError_t _e = cudaGetLastError();                                           \
@@ -29,6 +32,7 @@ void set_error(const char* fmt, ...);
       ::sc::set_error("%s: CUDA launch failed: %s", name, cudaGetErrorString(_e)); \
       return SC_ERR_CUDA;                                                          \
     }                                                                              \
+    ::sc::count_launch();                                                          \
   } while (0)
 
 // Link encoding of the attention pattern (src x tgt), see sparsecross_b200.h.

@@ -75,6 +75,63 @@ __global__ void residual_ln_kernel(const float* __restrict__ resid, const Y* __r
   }
 }
 
+// Vectorised variant for h % 128 == 0: lane covers 4 consecutive elements at
+// 4*lane + 128*e (float4 / 8-byte bf16x4 accesses, fully coalesced).
+__device__ __forceinline__ float4 load4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 load4(const __nv_bfloat16* p) {
+  uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+  float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
+  float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <typename Y, int kVec>
+__global__ void __launch_bounds__(256, 3) residual_ln_vec_kernel(
+    const float* __restrict__ resid, const Y* __restrict__ y, const float* __restrict__ bias,
+    const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ out,
+    __nv_bfloat16* __restrict__ out_h, int rows, int h) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const float* rr = resid + (int64_t)r * h;
+  const Y* yr = y + (int64_t)r * h;
+  float4 v[kVec];
+  float sum = 0.f;
+#pragma unroll
+  for (int e = 0; e < kVec; ++e) {
+    const int c = 4 * lane + 128 * e;
+    float4 a = load4(rr + c), b = load4(yr + c);
+    if (bias) {
+      float4 bb = load4(bias + c);
+      b.x += bb.x; b.y += bb.y; b.z += bb.z; b.w += bb.w;
+    }
+    v[e] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+    sum += (v[e].x + v[e].y) + (v[e].z + v[e].w);
+  }
+  const float mu = warp_sum(sum) / (float)h;
+  float sq = 0.f;
+#pragma unroll
+  for (int e = 0; e < kVec; ++e) {
+    v[e].x -= mu; v[e].y -= mu; v[e].z -= mu; v[e].w -= mu;
+    sq = fmaf(v[e].x, v[e].x, sq); sq = fmaf(v[e].y, v[e].y, sq);
+    sq = fmaf(v[e].z, v[e].z, sq); sq = fmaf(v[e].w, v[e].w, sq);
+  }
+  const float inv = 1.f / sqrtf(warp_sum(sq) / (float)h + kLnEps);
+#pragma unroll
+  for (int e = 0; e < kVec; ++e) {
+    const int c = 4 * lane + 128 * e;
+    const float4 g = load4(gamma + c), bt = load4(beta + c);
+    float4 o = make_float4(g.x * (v[e].x * inv) + bt.x, g.y * (v[e].y * inv) + bt.y,
+                           g.z * (v[e].z * inv) + bt.z, g.w * (v[e].w * inv) + bt.w);
+    *reinterpret_cast<float4*>(out + (int64_t)r * h + c) = o;
+    if (out_h) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+      uint2 u = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+      *reinterpret_cast<uint2*>(out_h + (int64_t)r * h + c) = u;
+    }
+  }
+}
+
 // Large-h fallback: block per row, three passes through L1/L2.
 template <typename Y>
 __global__ void residual_ln_big_kernel(const float* __restrict__ resid, const Y* __restrict__ y,
@@ -124,6 +181,35 @@ __global__ void bias_gelu_kernel(T* __restrict__ x, const float* __restrict__ bi
   }
 }
 
+// erf for the bf16 path: Abramowitz & Stegun 7.1.26, |abs error| <= 1.5e-7
+// (+ ~1e-7 from the approximate rcp/ex2), far below bf16 output resolution
+// (2^-9 relative); one MUFU.RCP + one MUFU.EX2 + 8 FMA instead of erff's
+// two-branch evaluation.  The fp32 parity path keeps erff.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float gelu_bf16path(float x) {
+  const float z = x * 0.70710678118654752440f;
+  const float a = fabsf(z);
+  const float t = rcp_approx(fmaf(0.3275911f, a, 1.f));
+  float p = fmaf(1.061405429f, t, -1.453152027f);
+  p = fmaf(p, t, 1.421413741f);
+  p = fmaf(p, t, -0.284496736f);
+  p = fmaf(p, t, 0.254829592f);
+  p *= t;
+  const float e = ex2_approx(-a * a * 1.4426950408889634f);
+  const float erf_abs = fmaf(-p, e, 1.f);
+  const float half_x = 0.5f * x;
+  return fmaf(half_x, copysignf(erf_abs, z), half_x);
+}
+
 // bf16, 8 elements per thread, cols % 8 == 0.
 __global__ void bias_gelu_bf16x8_kernel(__nv_bfloat16* __restrict__ x, const float* __restrict__ bias,
                                         int64_t n8, int cols) {
@@ -137,7 +223,7 @@ __global__ void bias_gelu_bf16x8_kernel(__nv_bfloat16* __restrict__ x, const flo
     for (int e = 0; e < 4; ++e) {
       float2 f = __bfloat1622float2(b[e]);
       if (bias) { f.x += __ldg(bias + c0 + 2 * e); f.y += __ldg(bias + c0 + 2 * e + 1); }
-      b[e] = __floats2bfloat162_rn(gelu_erf(f.x), gelu_erf(f.y));
+      b[e] = __floats2bfloat162_rn(gelu_bf16path(f.x), gelu_bf16path(f.y));
     }
     xv[i] = u;
   }
@@ -170,7 +256,16 @@ int launch_ln(const float* resid, const void* y, const float* bias, const float*
   __nv_bfloat16* oh = static_cast<__nv_bfloat16*>(out_h);
   unsigned blocks = (unsigned)((rows + 7) / 8);
   int per = (h + 31) / 32;
-  if (per <= 1) residual_ln_kernel<Y, 1><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  const bool vec = (h % 128 == 0) && !(((uintptr_t)resid | (uintptr_t)y | (uintptr_t)out |
+                                         (uintptr_t)out_h | (uintptr_t)gamma | (uintptr_t)beta |
+                                         (uintptr_t)bias) & 15);
+  if (vec && h == 768) residual_ln_vec_kernel<Y, 6><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  else if (vec && h == 384) residual_ln_vec_kernel<Y, 3><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  else if (vec && h == 1024) residual_ln_vec_kernel<Y, 8><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  else if (vec && h == 512) residual_ln_vec_kernel<Y, 4><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  else if (vec && h == 256) residual_ln_vec_kernel<Y, 2><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  else if (vec && h == 128) residual_ln_vec_kernel<Y, 1><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
+  else if (per <= 1) residual_ln_kernel<Y, 1><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
   else if (per <= 4) residual_ln_kernel<Y, 4><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
   else if (per <= 8) residual_ln_kernel<Y, 8><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
   else if (per <= 24) residual_ln_kernel<Y, 24><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);

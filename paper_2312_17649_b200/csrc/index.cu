@@ -10,6 +10,9 @@
 namespace sc {
 
 static thread_local char g_err[512] = "";
+static unsigned long long g_launches = 0;
+
+void count_launch() { __atomic_add_fetch(&g_launches, 1ULL, __ATOMIC_RELAXED); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -149,6 +152,8 @@ using namespace sc;
 extern "C" const char* sc_last_error(void) { return g_err; }
 
 extern "C" int sc_version(void) { return 10000; }
+
+extern "C" uint64_t sc_kernel_launches(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
 extern "C" int sc_index_build(const int32_t* cu_seqlens, const int32_t* qgroup_len, int32_t nseq,
                               int32_t total_tokens, int32_t tile_rows, int32_t qds_every,

@@ -1,0 +1,88 @@
+"""GPU checks of the encoder-loop kernels against plain PyTorch fp32 references of the same ops."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2312_17649_b200 import _lib
+
+    return _lib
+
+
+def torch_gelu_erf(x):
+    return 0.5 * x * (1.0 + torch.erf(x / math.sqrt(2.0)))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("cols", [3072, 64, 37])
+def test_bias_gelu(lib, dtype, cols):
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = (torch.randn((513, cols), device="cuda", generator=g) * 3).to(dtype)
+    bias = torch.randn(cols, device="cuda", generator=g)
+    ref = torch_gelu_erf(x.float() + bias)
+    y = x.clone()
+    lib.call("sc_bias_gelu", y.data_ptr(), bias.data_ptr(), 0 if dtype == torch.float32 else 1, 513, cols,
+             lib.stream_handle())
+    if dtype == torch.float32:
+        torch.testing.assert_close(y, ref, atol=2e-6, rtol=1e-6)
+    else:
+        # bf16 output: within one bf16 rounding of the exact-erf value
+        err = (y.float() - ref).abs() / ref.abs().clamp_min(1e-3)
+        assert err.max().item() <= 2 ** -8 + 1e-6
+
+
+@pytest.mark.parametrize("ydtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("h", [768, 32, 100, 2048])
+def test_residual_layernorm(lib, ydtype, h):
+    g = torch.Generator(device="cuda").manual_seed(1)
+    rows = 1000
+    resid = torch.randn((rows, h), device="cuda", generator=g)
+    y = torch.randn((rows, h), device="cuda", generator=g).to(ydtype)
+    gamma = torch.randn(h, device="cuda", generator=g)
+    beta = torch.randn(h, device="cuda", generator=g)
+    ref = torch.nn.functional.layer_norm(resid + y.float(), (h,), gamma, beta, eps=1e-12)
+    out = torch.empty_like(resid)
+    outh = torch.empty((rows, h), device="cuda", dtype=torch.bfloat16)
+    lib.call("sc_residual_layernorm", resid.data_ptr(), y.data_ptr(), 0 if ydtype == torch.float32 else 1, None,
+             gamma.data_ptr(), beta.data_ptr(), out.data_ptr(), outh.data_ptr(), rows, h, lib.stream_handle())
+    torch.testing.assert_close(out, ref, atol=2e-5, rtol=1e-5)
+    torch.testing.assert_close(outh, ref.to(torch.bfloat16), atol=0.02, rtol=0.01)
+
+
+def test_embed_and_cls_score(lib):
+    g = torch.Generator(device="cuda").manual_seed(2)
+    V, P, h, T = 50, 20, 96, 40
+    tok = torch.randn((V, h), device="cuda", generator=g)
+    pos = torch.randn((P, h), device="cuda", generator=g)
+    ids = torch.randint(0, V, (T,), device="cuda", generator=g, dtype=torch.int32)
+    tp = torch.cat([torch.arange(15), torch.arange(25)]).int().cuda()
+    x = torch.empty((T, h), device="cuda")
+    xh = torch.empty((T, h), device="cuda", dtype=torch.bfloat16)
+    lib.call("sc_embed", ids.data_ptr(), tp.data_ptr(), tok.data_ptr(), pos.data_ptr(), x.data_ptr(), xh.data_ptr(),
+             T, h, lib.stream_handle())
+    ref = tok[ids.long()] + pos[tp.long()]
+    torch.testing.assert_close(x, ref)
+    cu = torch.tensor([0, 15, 40], dtype=torch.int32, device="cuda")
+    w = torch.randn(h, device="cuda", generator=g)
+    sc = torch.empty(2, device="cuda")
+    lib.call("sc_cls_score", x.data_ptr(), cu.data_ptr(), 2, h, w.data_ptr(), 0.5, sc.data_ptr(), lib.stream_handle())
+    torch.testing.assert_close(sc, torch.stack([x[0] @ w, x[15] @ w]) + 0.5, atol=1e-4, rtol=1e-5)
+
+
+def test_kernel_launch_counter(lib):
+    n0 = lib.kernel_launches()
+    x = torch.zeros(10, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lib.call("sc_count_nonfinite", x.data_ptr(), 10, cnt.data_ptr(), lib.stream_handle())
+    assert lib.kernel_launches() == n0 + 1
+    assert cnt.item() == 0
+    x[3] = float("nan")
+    lib.call("sc_count_nonfinite", x.data_ptr(), 10, cnt.data_ptr(), lib.stream_handle())
+    assert cnt.item() > 0
