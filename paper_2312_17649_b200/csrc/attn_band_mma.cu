@@ -2,7 +2,7 @@
 // cross-encoder, arXiv 2312.17649 Eqs. 1-3), bf16 I/O, fp32 softmax/accum.
 //
 // One CTA = one tile of BM=64 doc rows of one sequence, looping over heads.
-// Per head a 2-stage TMA pipeline (128B-swizzled boxes, mbarrier complete_tx)
+// Per head a 2-3 stage TMA pipeline (128B-swizzled boxes, mbarrier complete_tx)
 // stages in shared memory:
 //   Q   [64 x 64]        doc rows r0..r0+63
 //   Kb/Vb [64+2w x 64]   doc rows r0-w .. r0+63+w  (the band halo)
@@ -11,8 +11,8 @@
 //                        rows under longformer/full, that attend the whole doc)
 // Warps 0-3 each own 16 doc rows: S = Q K^T over {global keys} U {band keys}
 // with mma.sync m16n8k16 (bf16 -> fp32), static band mask, online softmax in
-// the exp2 domain, O += P V, bf16 stores.  Then each warp emits the
-// split-softmax partial (m, l, acc) of the full rows over its own 16 doc keys,
+// the exp2 domain, O += P V, bf16 stores.  One warp per head (rotating)
+// also emits the split-softmax partial (m, l, acc) of the full rows over the tile's 64 doc keys,
 // so the CLS row never re-reads K/V from HBM; the head-row pass of the
 // generic kernel merges them.  Warp 4 is the TMA producer.
 //
@@ -31,7 +31,6 @@ namespace bandk {
 constexpr int BM = 64;
 constexpr int D = 64;
 constexpr int ROWB = 128;  // bytes per smem row
-constexpr int NSTAGE = 2;
 constexpr int NDOCW = 4;
 constexpr int PRODW = 4;
 constexpr int NTHREADS = 160;
@@ -195,11 +194,10 @@ __device__ __forceinline__ void zero_o(float (&o)[8][4]) {
 #pragma unroll
   for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
 }
-
 // NBC: band chunks of 32 keys per 16-row warp block (ceil((16+2w)/32)).
-// GR: global rows staged per head (16 or 32).
-template <int NBC, int GR>
-__global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
+// GR: global rows staged per head (16 or 32).  NS: pipeline stages.
+template <int NBC, int GR, int NS>
+__global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQf,
     const __grid_constant__ CUtensorMap tmKg, const __grid_constant__ CUtensorMap tmVg,
     const __grid_constant__ CUtensorMap tmKb, const __grid_constant__ CUtensorMap tmVb, Params p) {
@@ -221,7 +219,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
   constexpr int stage_bytes = q_bytes + 3 * f_bytes + 2 * kb_bytes;
   const int kb_box = BM + 2 * w;
 
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * stage_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * stage_bytes);
   const uint32_t sm0 = smem_u32(smem);
   auto q_buf = [&](int s) { return sm0 + s * stage_bytes; };
   auto qf_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes; };
@@ -229,12 +227,12 @@ __global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
   auto vg_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + 2 * f_bytes; };
   auto kb_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + 3 * f_bytes; };
   auto vb_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + 3 * f_bytes + kb_bytes; };
-  const uint32_t full_bar = smem_u32(bars), empty_bar = smem_u32(bars + NSTAGE);
+  const uint32_t full_bar = smem_u32(bars), empty_bar = smem_u32(bars + NS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // Zero the Kb/Vb rows the TMA box never writes (band chunks read up to kb_rows).
-  for (int s = 0; s < NSTAGE; ++s) {
+  for (int s = 0; s < NS; ++s) {
     uint8_t* kb = smem + s * stage_bytes + q_bytes + 3 * f_bytes;
     for (int o = kb_box * ROWB + threadIdx.x * 16; o < kb_bytes; o += NTHREADS * 16) {
       *reinterpret_cast<uint4*>(kb + o) = make_uint4(0, 0, 0, 0);
@@ -242,7 +240,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
     }
   }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NSTAGE; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(full_bar + 8 * s, 1);
       mbar_init(empty_bar + 8 * s, NDOCW);
     }
@@ -257,8 +255,8 @@ __global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
       prefetch_map(&tmKg); prefetch_map(&tmVg); prefetch_map(&tmQf);
       const uint32_t bytes = (uint32_t)(q_bytes + 3 * f_bytes + 2 * kb_box * ROWB);
       for (int h = 0; h < p.H; ++h) {
-        const int s = h % NSTAGE;
-        if (h >= NSTAGE) mbar_wait(empty_bar + 8 * s, ((h / NSTAGE) & 1) ^ 1);
+        const int s = h % NS;
+        if (h >= NS) mbar_wait(empty_bar + 8 * s, ((h / NS) & 1) ^ 1);
         const uint32_t fb = full_bar + 8 * s;
         mbar_expect_tx(fb, bytes);
         const int col = h * D;
@@ -280,7 +278,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
   const int ra = r0 + wr0 + gq, rb = ra + 8;  // doc-relative rows of this thread
 
   // Static masks (tile independent except at sequence edges): bit (nb*4 + e)
-  // of bmask[bc] / gmask[gc] set when that score element is a valid key.
+  // set when that score element is a valid key.
   uint32_t bmask[NBC];
   const bool edge = (r0 - w + wr0 < 0) || (r0 - w + wr0 + 32 * NBC > n_doc);
 #pragma unroll
@@ -313,13 +311,13 @@ __global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
       }
     gmask[gc] = m;
   }
-  // Own-key mask for the full-row partials (keys wr0 .. wr0+15 of this tile).
-  uint32_t fmask = 0;
+  // Own-key mask of the tile's 64 doc keys for the full-row partials.
+  uint32_t fmask[2] = {0u, 0u};
 #pragma unroll
-  for (int nb = 0; nb < 2; ++nb)
+  for (int nb = 0; nb < 8; ++nb)
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      fmask |= ((wr0 + nb * 8 + 2 * tq + (e & 1)) < rows_here ? 1u : 0u) << (nb * 4 + e);
+      fmask[nb >> 2] |= ((nb * 8 + 2 * tq + (e & 1)) < rows_here ? 1u : 0u) << ((nb & 3) * 4 + e);
 
   float ninv_a = 0.f, ninv_b = 0.f;
   if (p.padding == SC_PAD_ZERO_LOGIT) {
@@ -327,11 +325,10 @@ __global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
     ninv_b = (float)(2 * w + 1 - max(0, min(n_doc, rb + w + 1) - max(0, rb - w)));
   }
   const float c2 = p.c2;
-  const int nglob = (G + 15) / 16;
 
   for (int h = 0; h < p.H; ++h) {
-    const int s = h % NSTAGE;
-    mbar_wait(full_bar + 8 * s, (h / NSTAGE) & 1);
+    const int s = h % NS;
+    mbar_wait(full_bar + 8 * s, (h / NS) & 1);
     if (active) {
       uint32_t qa[4][4];
       load_q(q_buf(s), wr0, lane, qa);
@@ -340,10 +337,33 @@ __global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
       float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
       if (ninv_a > 0.f) { m0 = 0.f; l0 = tq == 0 ? ninv_a : 0.f; }
       if (ninv_b > 0.f) { m1 = 0.f; l1 = tq == 0 ? ninv_b : 0.f; }
-      // global keys: cls (key 0) and the query group (keys 1..G-1)
+      if constexpr (NBC == 1) {
+        // Single shot: all keys of the row block (globals + band) in one softmax.
+        constexpr int NG = GR / 8;
+        float sc[NG + 4][4];
 #pragma unroll
-      for (int gc = 0; gc < GR / 16; ++gc) {
-        if (gc < nglob) {
+        for (int gc = 0; gc < GR / 16; ++gc) qk16(kg_buf(s), gc * 16, lane, qa, sc[2 * gc], sc[2 * gc + 1]);
+        qk16(kb_buf(s), wr0, lane, qa, sc[NG], sc[NG + 1]);
+        qk16(kb_buf(s), wr0 + 16, lane, qa, sc[NG + 2], sc[NG + 3]);
+#pragma unroll
+        for (int nb = 0; nb < NG; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (!((gmask[nb >> 1] >> ((nb & 1) * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (!((bmask[0] >> (nb * 4 + e)) & 1)) sc[NG + nb][e] = -INFINITY;
+        softmax_update<NG + 4>(sc, c2, m0, m1, l0, l1, o);
+#pragma unroll
+        for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, lane, sc[2 * gc], sc[2 * gc + 1], o);
+        pv16(vb_buf(s), wr0, lane, sc[NG], sc[NG + 1], o);
+        pv16(vb_buf(s), wr0 + 16, lane, sc[NG + 2], sc[NG + 3], o);
+      } else {
+        // global keys: cls (key 0) and the query group (keys 1..G-1)
+#pragma unroll
+        for (int gc = 0; gc < GR / 16; ++gc) {
           float sc[2][4];
           qk16(kg_buf(s), gc * 16, lane, qa, sc[0], sc[1]);
 #pragma unroll
@@ -354,22 +374,22 @@ __global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
           softmax_update<2>(sc, c2, m0, m1, l0, l1, o);
           pv16(vg_buf(s), gc * 16, lane, sc[0], sc[1], o);
         }
-      }
-      // band keys: Kb row 0 = doc row r0 - w; this warp reads rows wr0 + [0, 32*NBC)
+        // band keys: Kb row 0 = doc row r0 - w; this warp reads rows wr0 + [0, 32*NBC)
 #pragma unroll
-      for (int bc = 0; bc < NBC; ++bc) {
-        const int kb0 = wr0 + 32 * bc;
-        float sc[4][4];
-        qk16(kb_buf(s), kb0, lane, qa, sc[0], sc[1]);
-        qk16(kb_buf(s), kb0 + 16, lane, qa, sc[2], sc[3]);
+        for (int bc = 0; bc < NBC; ++bc) {
+          const int kb0 = wr0 + 32 * bc;
+          float sc[4][4];
+          qk16(kb_buf(s), kb0, lane, qa, sc[0], sc[1]);
+          qk16(kb_buf(s), kb0 + 16, lane, qa, sc[2], sc[3]);
 #pragma unroll
-        for (int nb = 0; nb < 4; ++nb)
+          for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (!((bmask[bc] >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
-        softmax_update<4>(sc, c2, m0, m1, l0, l1, o);
-        pv16(vb_buf(s), kb0, lane, sc[0], sc[1], o);
-        pv16(vb_buf(s), kb0 + 16, lane, sc[2], sc[3], o);
+            for (int e = 0; e < 4; ++e)
+              if (!((bmask[bc] >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+          softmax_update<4>(sc, c2, m0, m1, l0, l1, o);
+          pv16(vb_buf(s), kb0, lane, sc[0], sc[1], o);
+          pv16(vb_buf(s), kb0 + 16, lane, sc[2], sc[3], o);
+        }
       }
       l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
       l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
@@ -387,23 +407,30 @@ __global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
 #pragma unroll
         for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][2] * i1, o[nb][3] * i1);
       }
+    }
 
-      // Full-row split-softmax partials over this warp's own 16 doc keys.
+    // Full-row split-softmax partials over the tile's 64 own doc keys; the
+    // designated warp rotates with the head so the extra work spreads evenly.
+    if (warp == (h & (NDOCW - 1))) {
 #pragma unroll
       for (int fc = 0; fc < GR / 16; ++fc) {
         if (fc * 16 < p.fneed) {
+          uint32_t qa[4][4];
           load_q(qf_buf(s), fc * 16, lane, qa);
-          float sc[2][4];
-          qk16(kb_buf(s), w + wr0, lane, qa, sc[0], sc[1]);
+          float sc[8][4];
 #pragma unroll
-          for (int nb = 0; nb < 2; ++nb)
+          for (int np = 0; np < 4; ++np) qk16(kb_buf(s), w + np * 16, lane, qa, sc[2 * np], sc[2 * np + 1]);
+#pragma unroll
+          for (int nb = 0; nb < 8; ++nb)
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              if (!((fmask >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+              if (!((fmask[nb >> 2] >> ((nb & 3) * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+          float o[8][4];
           zero_o(o);
           float fm0 = -INFINITY, fm1 = -INFINITY, fl0 = 0.f, fl1 = 0.f;
-          softmax_update<2>(sc, c2, fm0, fm1, fl0, fl1, o);
-          pv16(vb_buf(s), w + wr0, lane, sc[0], sc[1], o);
+          softmax_update<8>(sc, c2, fm0, fm1, fl0, fl1, o);
+#pragma unroll
+          for (int kp = 0; kp < 4; ++kp) pv16(vb_buf(s), w + kp * 16, lane, sc[2 * kp], sc[2 * kp + 1], o);
           fl0 += __shfl_xor_sync(0xffffffffu, fl0, 1);
           fl0 += __shfl_xor_sync(0xffffffffu, fl0, 2);
           fl1 += __shfl_xor_sync(0xffffffffu, fl1, 1);
@@ -413,7 +440,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
           for (int half = 0; half < 2; ++half) {
             const int f = fc * 16 + gq + 8 * half;
             if (f >= p.fneed) continue;
-            float* rec = p.partials + ((((int64_t)tile * NDOCW + warp) * p.H + h) * p.fmax + f) * (D + 2);
+            float* rec = p.partials + (((int64_t)tile * p.H + h) * p.fmax + f) * (D + 2);
             if (tq == 0) {
               rec[0] = (half ? fm1 : fm0) * to_nat;
               rec[1] = half ? fl1 : fl0;
@@ -425,10 +452,6 @@ __global__ void __launch_bounds__(NTHREADS, 3) band_attn_kernel(
           }
         }
       }
-    } else if (p.fneed > 0) {
-      // No own keys in this block: mark its partial records empty.
-      for (int f = lane; f < p.fneed; f += 32)
-        p.partials[((((int64_t)tile * NDOCW + warp) * p.H + h) * p.fmax + f) * (D + 2) + 1] = 0.f;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty_bar + 8 * s);
@@ -466,21 +489,29 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t row
 
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, Params);
 
+// Stage count: as many as fit two CTAs per SM (<= ~113 KB each), at least 2.
+template <int NBC, int GR>
+constexpr int stages_for() {
+  constexpr int stage_bytes = (BM + 3 * GR + 2 * (48 + 32 * NBC)) * ROWB;
+  return (3 * stage_bytes + 2048 <= 113 * 1024) ? 3 : 2;
+}
+
 template <int NBC, int GR>
 static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, cudaStream_t st) {
+  constexpr int NS = stages_for<NBC, GR>();
   constexpr int stage_bytes = (BM + 3 * GR + 2 * (48 + 32 * NBC)) * ROWB;
-  constexpr size_t smem = (size_t)NSTAGE * stage_bytes + 2 * NSTAGE * 8 + 1024;
+  constexpr size_t smem = (size_t)NS * stage_bytes + 2 * NS * 8 + 1024;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(band_attn_kernel<NBC, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess) {
       set_error("band kernel: shared memory request of %zu bytes failed", smem);
       return SC_ERR_UNSUPPORTED;
     }
     attr = true;
   }
-  band_attn_kernel<NBC, GR><<<grid, NTHREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4],
-                                                          maps[5], p);
+  band_attn_kernel<NBC, GR, NS><<<grid, NTHREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3],
+                                                              maps[4], maps[5], p);
   SC_CHECK_LAUNCH("band_attn_kernel");
   return SC_OK;
 }
@@ -507,7 +538,7 @@ size_t band_workspace_bytes(int nseq, int T, int H, int d, int tile_rows, int ma
   int f = full_rows_needed(L, max_qgroup_len);
   if (f == 0 || tile_rows <= 0) return 0;
   int64_t tiles = (T + tile_rows - 1) / tile_rows + nseq;
-  return (size_t)tiles * bandk::NDOCW * H * f * (d + 2) * sizeof(float);
+  return (size_t)tiles * H * f * (d + 2) * sizeof(float);
 }
 
 int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
@@ -566,7 +597,7 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   h.partials = static_cast<const float*>(ws);
   h.tile_base = seq_tile_base;
   h.fmax = fneed;
-  h.rec_per_tile = NDOCW;
+  h.rec_per_tile = 1;
   return launch_attn_generic(h, dtype, st);
 }
 

@@ -33,9 +33,10 @@ def test_bias_gelu(lib, dtype, cols):
     if dtype == torch.float32:
         torch.testing.assert_close(y, ref, atol=2e-6, rtol=1e-6)
     else:
-        # bf16 output: within one bf16 rounding of the exact-erf value
-        err = (y.float() - ref).abs() / ref.abs().clamp_min(1e-3)
-        assert err.max().item() <= 2 ** -8 + 1e-6
+        # bf16 output: one bf16 rounding (<= 2^-8 relative) of the exact-erf value,
+        # plus the erf approximation's absolute error (< 3e-7 on erf => < 1e-6 on GELU here)
+        excess = (y.float() - ref).abs() - 2 ** -8 * ref.abs()
+        assert excess.max().item() <= 2e-6
 
 
 @pytest.mark.parametrize("ydtype", [torch.float32, torch.bfloat16])
