@@ -12,9 +12,13 @@
 // Warps 0-3 each own 16 doc rows: S = Q K^T over {global keys} U {band keys}
 // with mma.sync m16n8k16 (bf16 -> fp32), static band mask, online softmax in
 // the exp2 domain, O += P V, bf16 stores.  One warp per head (rotating)
-// also emits the split-softmax partial (m, l, acc) of the full rows over the tile's 64 doc keys,
-// so the CLS row never re-reads K/V from HBM; the head-row pass of the
-// generic kernel merges them.  Warp 4 is the TMA producer.
+// also emits the split-softmax record (m, l, acc) of the "full rows" over the
+// tile's 64 doc keys, so the CLS row never re-reads K/V from HBM.  The first
+// tile of a sequence also computes the head rows (cls, query group) over the
+// global keys -- final for rows without a doc link (sparse query rows), a
+// record for the others -- and the last tile of a sequence to finish merges
+// the records into the CLS (and longformer query) rows.  Warp 4 is the TMA
+// producer.  One launch covers every row of the packed batch.
 //
 // Semantics: doc row r attends cls (if linked), query group (if linked) and
 // doc keys t with |t - r| <= w, 0 <= t < n_doc (R/band.py:48-52,
@@ -39,6 +43,10 @@ constexpr int MAX_W = 96;  // Kb box rows 64 + 2w <= 256 (TMA box limit)
 struct Params {
   int nseq, H, w, kb_rows, fneed, fmax, padding;
   int link_cls, link_query;
+  // head rows (cls = group 0, query = group 1): links to cls / query keys, doc FULL
+  int hl[2][2], hdoc[2];
+  int ntiles_max;      // record index of sequence j's global-key record = ntiles_max + j
+  int32_t* counters;   // [nseq] tiles finished per sequence (self-resetting)
   float c2;  // log2(e) / scale: raw logit -> exp2 domain
   const int32_t* cu;
   const int32_t* qlen;
@@ -325,6 +333,8 @@ __global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
     ninv_b = (float)(2 * w + 1 - max(0, min(n_doc, rb + w + 1) - max(0, rb - w)));
   }
   const float c2 = p.c2;
+  const int hl_bits = p.hl[0][0] | (p.hl[0][1] << 1) | (p.hl[1][0] << 2) | (p.hl[1][1] << 3);
+  const int hdoc_bits = p.hdoc[0] | (p.hdoc[1] << 1);
 
   for (int h = 0; h < p.H; ++h) {
     const int s = h % NS;
@@ -453,8 +463,129 @@ __global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
         }
       }
     }
+    // Head rows over the global keys (first tile of the sequence only): rows
+    // f < G (cls, query group) attend cls / query keys per their links.  Rows
+    // with a FULL doc link leave a split-softmax record (merged below); the
+    // others (sparse: query rows) are final and stored here.
+    if (r0 == 0 && warp == ((h + 2) & (NDOCW - 1))) {
+#pragma unroll
+      for (int fc = 0; fc < GR / 16; ++fc) {
+        if (fc * 16 < G) {
+          uint32_t qa[4][4];
+          load_q(qf_buf(s), fc * 16, lane, qa);
+          float sc[GR / 8][4];
+#pragma unroll
+          for (int gc = 0; gc < GR / 16; ++gc) qk16(kg_buf(s), gc * 16, lane, qa, sc[2 * gc], sc[2 * gc + 1]);
+#pragma unroll
+          for (int nb = 0; nb < GR / 8; ++nb)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int f = fc * 16 + gq + ((e >> 1) << 3);
+              const int kg = nb * 8 + 2 * tq + (e & 1);
+              const int grp = f == 0 ? 0 : 1;
+              const bool ok = f < G && kg < G && ((hl_bits >> (grp * 2 + (kg == 0 ? 0 : 1))) & 1);
+              if (!ok) sc[nb][e] = -INFINITY;
+            }
+          float o[8][4];
+          zero_o(o);
+          float hm0 = -INFINITY, hm1 = -INFINITY, hl0 = 0.f, hl1 = 0.f;
+          softmax_update<GR / 8>(sc, c2, hm0, hm1, hl0, hl1, o);
+#pragma unroll
+          for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, lane, sc[2 * gc], sc[2 * gc + 1], o);
+          hl0 += __shfl_xor_sync(0xffffffffu, hl0, 1);
+          hl0 += __shfl_xor_sync(0xffffffffu, hl0, 2);
+          hl1 += __shfl_xor_sync(0xffffffffu, hl1, 1);
+          hl1 += __shfl_xor_sync(0xffffffffu, hl1, 2);
+          const float to_nat = c2 * 0.69314718055994530942f;
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const int f = fc * 16 + gq + 8 * half;
+            if (f >= G) continue;
+            const int grp = f == 0 ? 0 : 1;
+            const float mm = half ? hm1 : hm0, ll = half ? hl1 : hl0;
+            if ((hdoc_bits >> grp) & 1) {
+              float* rec = p.partials + (((int64_t)(p.ntiles_max + j) * p.H + h) * p.fmax + f) * (D + 2);
+              if (tq == 0) {
+                rec[0] = ll > 0.f ? mm * to_nat : -INFINITY;
+                rec[1] = ll;
+              }
+#pragma unroll
+              for (int nb = 0; nb < 8; ++nb)
+                *reinterpret_cast<float2*>(rec + 2 + nb * 8 + 2 * tq) =
+                    make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
+            } else {
+              const float inv = ll > 0.f ? 1.f / ll : 0.f;
+              uint32_t* dst = reinterpret_cast<uint32_t*>(p.out + (int64_t)(g.start + f) * p.ld_out + h * D + 2 * tq);
+#pragma unroll
+              for (int nb = 0; nb < 8; ++nb)
+                dst[nb * 4] = pack_bf16(o[nb][2 * half] * inv, o[nb][2 * half + 1] * inv);
+            }
+          }
+        }
+      }
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty_bar + 8 * s);
+  }
+
+  // ---------------------------------------------------------------------
+  // The last CTA of a sequence merges the split-softmax records of the head
+  // rows with a FULL doc link: one record per doc tile + the global-key
+  // record of the first tile (threadFenceReduction pattern).
+  if (p.fneed == 0) return;
+  __threadfence();
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  int* s_flag = reinterpret_cast<int*>(smem + NS * stage_bytes + 2 * NS * 8);
+  if (threadIdx.x == 0) {
+    const int ntile_j = __ldg(p.tile_base + j + 1) - __ldg(p.tile_base + j);
+    const int old = atomicAdd(p.counters + j, 1);
+    *s_flag = (old == ntile_j - 1);
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (!*s_flag) return;
+  __threadfence();
+  if (threadIdx.x == 0) p.counters[j] = 0;  // ready for the next call
+  float* sbeta = reinterpret_cast<float*>(smem) + warp * 128;  // pipeline buffers are idle now
+  const int tb = __ldg(p.tile_base + j), te = __ldg(p.tile_base + j + 1);
+  const int nrec = te - tb + 1;  // doc tiles + the global-key record
+  const int64_t rstride = (int64_t)p.H * p.fmax * (D + 2);
+  for (int item = warp; item < p.H * G; item += NDOCW) {
+    const int h = item / G, f = item % G;
+    if (!((hdoc_bits >> (f == 0 ? 0 : 1)) & 1)) continue;
+    const float* trec = p.partials + (((int64_t)tb * p.H + h) * p.fmax + f) * (D + 2);
+    const float* grec = p.partials + (((int64_t)(p.ntiles_max + j) * p.H + h) * p.fmax + f) * (D + 2);
+    auto rec_of = [&](int r) { return r < nrec - 1 ? trec + r * rstride : grec; };
+    float mloc = -INFINITY;
+    for (int r = lane; r < nrec; r += 32) {
+      const float* rc = rec_of(r);
+      if (rc[1] > 0.f) mloc = fmaxf(mloc, rc[0]);
+    }
+    const float M = warp_max(mloc);
+    float lsum = 0.f, acc0 = 0.f, acc1 = 0.f;
+    for (int base = 0; base < nrec; base += 128) {
+      const int cnt = min(128, nrec - base);
+      for (int r = lane; r < cnt; r += 32) {
+        const float* rc = rec_of(base + r);
+        const float lt = rc[1];
+        const float b = lt > 0.f ? __expf(rc[0] - M) : 0.f;
+        sbeta[r] = b;
+        lsum = fmaf(b, lt, lsum);
+      }
+      __syncwarp();
+#pragma unroll 4
+      for (int r = 0; r < cnt; ++r) {
+        const float b = sbeta[r];
+        const float* rc = rec_of(base + r) + 2;
+        acc0 = fmaf(b, rc[lane], acc0);
+        acc1 = fmaf(b, rc[lane + 32], acc1);
+      }
+      __syncwarp();
+    }
+    const float l = warp_sum(lsum);
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* dst = p.out + (int64_t)(g.start + f) * p.ld_out + h * D;
+    dst[lane] = __float2bfloat16_rn(acc0 * inv);
+    dst[lane + 32] = __float2bfloat16_rn(acc1 * inv);
   }
 }
 
@@ -500,7 +631,7 @@ template <int NBC, int GR>
 static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, cudaStream_t st) {
   constexpr int NS = stages_for<NBC, GR>();
   constexpr int stage_bytes = (BM + 3 * GR + 2 * (48 + 32 * NBC)) * ROWB;
-  constexpr size_t smem = (size_t)NS * stage_bytes + 2 * NS * 8 + 1024;
+  constexpr size_t smem = (size_t)NS * stage_bytes + 2 * NS * 8 + 64 + 1024;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -537,8 +668,12 @@ size_t band_workspace_bytes(int nseq, int T, int H, int d, int tile_rows, int ma
                             const Links& L) {
   int f = full_rows_needed(L, max_qgroup_len);
   if (f == 0 || tile_rows <= 0) return 0;
-  int64_t tiles = (T + tile_rows - 1) / tile_rows + nseq;
-  return (size_t)tiles * H * f * (d + 2) * sizeof(float);
+  // records: one per doc tile (<= ceil(T/64) + nseq) + one global-key record per
+  // sequence, each H x f x (m, l, acc[d]); then the per-sequence tile counters.
+  int64_t recs = (T + tile_rows - 1) / tile_rows + 2 * (int64_t)nseq;
+  size_t rec_bytes = (size_t)recs * H * f * (d + 2) * sizeof(float);
+  rec_bytes = (rec_bytes + 255) & ~size_t(255);
+  return rec_bytes + (size_t)nseq * sizeof(int32_t);
 }
 
 int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
@@ -555,8 +690,8 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   if (a.d != D) return unsupported("needs head_dim 64");
   if (a.glob_cu) return unsupported("QDS global tokens");
   if (w < 0 || w > MAX_W) return unsupported("doc->doc link must be a window <= 96");
-  for (int x : {L.w[2][0], L.w[2][1], L.w[0][2], L.w[1][2]})
-    if (x != SC_LINK_FULL && x != SC_LINK_NONE) return unsupported("windowed cross-group link");
+  for (int x : {L.w[2][0], L.w[2][1], L.w[0][2], L.w[1][2], L.w[0][0], L.w[0][1], L.w[1][0], L.w[1][1]})
+    if (x != SC_LINK_FULL && x != SC_LINK_NONE) return unsupported("windowed link outside doc->doc");
   if (max_qgroup_len + 1 > 32) return unsupported("query group longer than 31 rows");
   if (tile_rows != BM || !seq_tile_base || !seq_head_base) return unsupported("layout tiles must be 64 rows");
   if (((uintptr_t)a.q | (uintptr_t)a.k | (uintptr_t)a.v | (uintptr_t)a.out) & 15)
@@ -585,20 +720,23 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   p.cu = a.cu; p.qlen = a.qlen; p.tile_base = seq_tile_base;
   p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
   p.partials = static_cast<float*>(ws);
-
+  for (int gsrc = 0; gsrc < 2; ++gsrc) {
+    p.hl[gsrc][0] = L.w[gsrc][0] == SC_LINK_FULL;
+    p.hl[gsrc][1] = L.w[gsrc][1] == SC_LINK_FULL;
+    p.hdoc[gsrc] = L.w[gsrc][2] == SC_LINK_FULL;
+  }
   const unsigned grid = (unsigned)((a.T + BM - 1) / BM + a.nseq);
-  int rc = GR == 16 ? launch_gr<16>(nbc, maps, p, grid, st) : launch_gr<32>(nbc, maps, p, grid, st);
-  if (rc) return rc;
-
-  // Head rows (cls + query group): generic kernel, doc keys via the partials.
-  AttnArgs h = a;
-  h.head_base = seq_head_base;
-  h.n_head_rows = a.nseq * (1 + max_qgroup_len);
-  h.partials = static_cast<const float*>(ws);
-  h.tile_base = seq_tile_base;
-  h.fmax = fneed;
-  h.rec_per_tile = 1;
-  return launch_attn_generic(h, dtype, st);
+  p.ntiles_max = (int)grid;
+  p.counters = nullptr;
+  if (need) {
+    const size_t rec_bytes = need - (size_t)a.nseq * sizeof(int32_t);
+    p.counters = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + rec_bytes);
+  }
+  // Doc rows, head rows over global keys (first tile) and the head-row merge
+  // (last tile of each sequence) in one launch.  (seq_head_base is unused:
+  // head rows are addressed through cu_seqlens.)
+  (void)seq_head_base;
+  return GR == 16 ? launch_gr<16>(nbc, maps, p, grid, st) : launch_gr<32>(nbc, maps, p, grid, st);
 }
 
 }  // namespace sc

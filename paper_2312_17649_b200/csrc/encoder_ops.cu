@@ -147,7 +147,8 @@ __global__ void residual_ln_big_kernel(const float* __restrict__ resid, const Y*
     s = warp_sum(s);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
     __syncthreads();
-    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    const int lane = threadIdx.x & 31;
+    float t = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.f;
     t = warp_sum(t);
     __syncthreads();
     return t;

@@ -108,7 +108,8 @@ class PackedLayout:
         if key not in self._ws:
             n = _lib.load().sc_attn_workspace_bytes(self.nseq, self.total_tokens, heads, head_dim,
                                                     self.tile_rows, self.max_qgroup_len, links.ctypes.data)
-            self._ws[key] = torch.empty(n, dtype=torch.uint8, device=self.device) if n else None
+            # zeroed: the tail holds self-resetting per-sequence tile counters
+            self._ws[key] = torch.zeros(n, dtype=torch.uint8, device=self.device) if n else None
         return self._ws[key]
 
     def mask(self, seq: int, pattern) -> np.ndarray:

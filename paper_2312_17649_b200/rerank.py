@@ -130,20 +130,26 @@ def gather_scores(local: torch.Tensor, counts, group=None) -> torch.Tensor:
     return torch.cat([out[r * mx: r * mx + c] for r, c in enumerate(counts)])
 
 
-def rerank_distributed(model: CrossEncoder, queries, top_k: int = 100, tag: str = "sparsecross",
-                       rank: int = 0, world: int = 1, group=None) -> list | None:
+def rerank_distributed(model: CrossEncoder | None, queries, top_k: int = 100, tag: str = "sparsecross",
+                       rank: int = 0, world: int = 1, group=None, score_fn=None) -> list | None:
     """Re-rank ``queries`` = [(qid, query_ids, [(doc_id, doc_ids), ...]), ...] over `world` ranks.
 
     Each rank scores a contiguous block of queries; scores are gathered with
     one all-gather; rank 0 returns the ranked run entries (others return None).
+    ``score_fn(query_ids, candidate_ids) -> float32 array`` overrides the GPU
+    scorer (used by the CPU multi-process tests).
     """
+    if score_fn is None:
+        def score_fn(qids, cands):
+            return score_candidates(model, qids, cands)
     lo, hi = shard_range(len(queries), world, rank)
-    local = [score_candidates(model, q[1], [c[1] for c in q[2]]) for q in queries[lo:hi]]
+    local = [np.asarray(score_fn(q[1], [c[1] for c in q[2]]), np.float32) for q in queries[lo:hi]]
     flat = np.concatenate(local) if local else np.zeros(0, np.float32)
     if world > 1:
         per_q = [len(q[2]) for q in queries]
         counts = [sum(per_q[slice(*shard_range(len(queries), world, r))]) for r in range(world)]
-        dev = model.device if torch.distributed.get_backend(group) == "nccl" else torch.device("cpu")
+        nccl = torch.distributed.get_backend(group) == "nccl"
+        dev = (model.device if model is not None else torch.device("cuda")) if nccl else torch.device("cpu")
         allv = gather_scores(torch.from_numpy(flat).to(dev), counts, group).cpu().numpy()
     else:
         allv = flat

@@ -207,3 +207,25 @@ def test_zero_valid_row_raises(P):
     with pytest.raises(P.AttentionError):
         run_attention(P, x, 1, 4, pat, "exclude", torch.float32)
     run_attention(P, x, 1, 4, pat, "zero-logit", torch.float32)  # padded slots keep rows alive
+
+
+@pytest.mark.parametrize("name", ["sparse", "longformer"])
+def test_band_kernel_repeatable_and_forced(P, name):
+    """Repeated calls reuse the workspace (self-resetting tile counters) and give identical bits."""
+    rng = np.random.default_rng(21)
+    H, d = 12, 64
+    shapes = [(10, 4086), (3, 70), (30, 500), (1, 1)]
+    seq = [m + n + 3 for m, n in shapes]
+    lay = P.PackedLayout.from_lengths(seq, [m + 1 for m, _ in shapes], device="cuda")
+    T = sum(seq)
+    x = torch.from_numpy(rng.standard_normal((T, 3 * H * d)).astype(np.float32)).cuda().to(torch.bfloat16)
+    pat = P.make_pattern(name, 4)
+    run = lambda algo: P.attend_packed(x[:, :H * d], x[:, H * d:2 * H * d], x[:, 2 * H * d:], lay, pat, H,
+                                       algo=algo).clone()
+    a, b, c = run("band"), run("band"), run("auto")
+    assert torch.equal(a, b) and torch.equal(a, c)
+    gen = run("generic").float()
+    assert (a.float() - gen).abs().max().item() < 2e-2
+    with pytest.raises(NotImplementedError):
+        xf = x.float()
+        P.attend_packed(xf[:, :H * d], xf[:, H * d:2 * H * d], xf[:, 2 * H * d:], lay, pat, H, algo="band")
