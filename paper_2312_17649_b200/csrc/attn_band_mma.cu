@@ -16,9 +16,9 @@
 // tile's 64 doc keys, so the CLS row never re-reads K/V from HBM.  The first
 // tile of a sequence also computes the head rows (cls, query group) over the
 // global keys -- final for rows without a doc link (sparse query rows), a
-// record for the others -- and the last tile of a sequence to finish merges
-// the records into the CLS (and longformer query) rows.  Warp 4 is the TMA
-// producer.  One launch covers every row of the packed batch.
+// record for the others -- and merge_full_rows_kernel (one warp per sequence,
+// head and row) folds the records into the CLS (and longformer query) rows.
+// Warp 4 is the TMA producer.
 //
 // Semantics: doc row r attends cls (if linked), query group (if linked) and
 // doc keys t with |t - r| <= w, 0 <= t < n_doc (R/band.py:48-52,
@@ -39,6 +39,7 @@ constexpr int NDOCW = 4;
 constexpr int PRODW = 4;
 constexpr int NTHREADS = 160;
 constexpr int MAX_W = 96;  // Kb box rows 64 + 2w <= 256 (TMA box limit)
+constexpr int REC = D + 4; // split-softmax record: m, l, pad, pad, acc[D] (16B-aligned acc)
 
 struct Params {
   int nseq, H, w, kb_rows, fneed, fmax, padding;
@@ -46,7 +47,6 @@ struct Params {
   // head rows (cls = group 0, query = group 1): links to cls / query keys, doc FULL
   int hl[2][2], hdoc[2];
   int ntiles_max;      // record index of sequence j's global-key record = ntiles_max + j
-  int32_t* counters;   // [nseq] tiles finished per sequence (self-resetting)
   float c2;  // log2(e) / scale: raw logit -> exp2 domain
   const int32_t* cu;
   const int32_t* qlen;
@@ -450,14 +450,14 @@ __global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
           for (int half = 0; half < 2; ++half) {
             const int f = fc * 16 + gq + 8 * half;
             if (f >= p.fneed) continue;
-            float* rec = p.partials + (((int64_t)tile * p.H + h) * p.fmax + f) * (D + 2);
+            float* rec = p.partials + (((int64_t)tile * p.H + h) * p.fmax + f) * REC;
             if (tq == 0) {
               rec[0] = (half ? fm1 : fm0) * to_nat;
               rec[1] = half ? fl1 : fl0;
             }
 #pragma unroll
             for (int nb = 0; nb < 8; ++nb)
-              *reinterpret_cast<float2*>(rec + 2 + nb * 8 + 2 * tq) =
+              *reinterpret_cast<float2*>(rec + 4 + nb * 8 + 2 * tq) =
                   make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
           }
         }
@@ -504,14 +504,14 @@ __global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
             const int grp = f == 0 ? 0 : 1;
             const float mm = half ? hm1 : hm0, ll = half ? hl1 : hl0;
             if ((hdoc_bits >> grp) & 1) {
-              float* rec = p.partials + (((int64_t)(p.ntiles_max + j) * p.H + h) * p.fmax + f) * (D + 2);
+              float* rec = p.partials + (((int64_t)(p.ntiles_max + j) * p.H + h) * p.fmax + f) * REC;
               if (tq == 0) {
                 rec[0] = ll > 0.f ? mm * to_nat : -INFINITY;
                 rec[1] = ll;
               }
 #pragma unroll
               for (int nb = 0; nb < 8; ++nb)
-                *reinterpret_cast<float2*>(rec + 2 + nb * 8 + 2 * tq) =
+                *reinterpret_cast<float2*>(rec + 4 + nb * 8 + 2 * tq) =
                     make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
             } else {
               const float inv = ll > 0.f ? 1.f / ll : 0.f;
@@ -528,65 +528,74 @@ __global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
     if (lane == 0) mbar_arrive(empty_bar + 8 * s);
   }
 
-  // ---------------------------------------------------------------------
-  // The last CTA of a sequence merges the split-softmax records of the head
-  // rows with a FULL doc link: one record per doc tile + the global-key
-  // record of the first tile (threadFenceReduction pattern).
-  if (p.fneed == 0) return;
-  __threadfence();
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  int* s_flag = reinterpret_cast<int*>(smem + NS * stage_bytes + 2 * NS * 8);
-  if (threadIdx.x == 0) {
-    const int ntile_j = __ldg(p.tile_base + j + 1) - __ldg(p.tile_base + j);
-    const int old = atomicAdd(p.counters + j, 1);
-    *s_flag = (old == ntile_j - 1);
-  }
-  asm volatile("bar.sync 1, 128;" ::: "memory");
-  if (!*s_flag) return;
-  __threadfence();
-  if (threadIdx.x == 0) p.counters[j] = 0;  // ready for the next call
-  float* sbeta = reinterpret_cast<float*>(smem) + warp * 128;  // pipeline buffers are idle now
+}
+
+// Merge of the split-softmax records into the head rows with a FULL doc link
+// (CLS; query rows under longformer): one warp per (sequence, head, row).
+// Records: one per doc tile of the sequence + the first tile's global-key
+// record.  Each lane loads whole records (16B vectors, all loads independent),
+// scales them by exp(m_r - M), and the warp reduces them through shared memory.
+constexpr int MERGE_WARPS = 4;
+
+__global__ void __launch_bounds__(MERGE_WARPS * 32) merge_full_rows_kernel(Params p) {
+  __shared__ float sacc[MERGE_WARPS][32][D + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t item = (int64_t)blockIdx.x * MERGE_WARPS + warp;
+  const int f = (int)(item % p.fmax);
+  const int h = (int)((item / p.fmax) % p.H);
+  const int j = (int)(item / ((int64_t)p.fmax * p.H));
+  if (j >= p.nseq) return;
+  const SeqGroups g = seq_groups(p.cu, p.qlen, j);
+  const int G = 1 + g.len[1];
+  if (f >= G || !p.hdoc[f == 0 ? 0 : 1]) return;
   const int tb = __ldg(p.tile_base + j), te = __ldg(p.tile_base + j + 1);
-  const int nrec = te - tb + 1;  // doc tiles + the global-key record
-  const int64_t rstride = (int64_t)p.H * p.fmax * (D + 2);
-  for (int item = warp; item < p.H * G; item += NDOCW) {
-    const int h = item / G, f = item % G;
-    if (!((hdoc_bits >> (f == 0 ? 0 : 1)) & 1)) continue;
-    const float* trec = p.partials + (((int64_t)tb * p.H + h) * p.fmax + f) * (D + 2);
-    const float* grec = p.partials + (((int64_t)(p.ntiles_max + j) * p.H + h) * p.fmax + f) * (D + 2);
-    auto rec_of = [&](int r) { return r < nrec - 1 ? trec + r * rstride : grec; };
-    float mloc = -INFINITY;
-    for (int r = lane; r < nrec; r += 32) {
-      const float* rc = rec_of(r);
-      if (rc[1] > 0.f) mloc = fmaxf(mloc, rc[0]);
-    }
-    const float M = warp_max(mloc);
-    float lsum = 0.f, acc0 = 0.f, acc1 = 0.f;
-    for (int base = 0; base < nrec; base += 128) {
-      const int cnt = min(128, nrec - base);
-      for (int r = lane; r < cnt; r += 32) {
-        const float* rc = rec_of(base + r);
-        const float lt = rc[1];
-        const float b = lt > 0.f ? __expf(rc[0] - M) : 0.f;
-        sbeta[r] = b;
-        lsum = fmaf(b, lt, lsum);
-      }
-      __syncwarp();
-#pragma unroll 4
-      for (int r = 0; r < cnt; ++r) {
-        const float b = sbeta[r];
-        const float* rc = rec_of(base + r) + 2;
-        acc0 = fmaf(b, rc[lane], acc0);
-        acc1 = fmaf(b, rc[lane + 32], acc1);
-      }
-      __syncwarp();
-    }
-    const float l = warp_sum(lsum);
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* dst = p.out + (int64_t)(g.start + f) * p.ld_out + h * D;
-    dst[lane] = __float2bfloat16_rn(acc0 * inv);
-    dst[lane + 32] = __float2bfloat16_rn(acc1 * inv);
+  const int nrec = te - tb + 1;
+  const int64_t rstride = (int64_t)p.H * p.fmax * REC;
+  const float* trec = p.partials + (((int64_t)tb * p.H + h) * p.fmax + f) * REC;
+  const float* grec = p.partials + (((int64_t)(p.ntiles_max + j) * p.H + h) * p.fmax + f) * REC;
+  auto rec_of = [&](int r) { return r < nrec - 1 ? trec + r * rstride : grec; };
+
+  float mloc = -INFINITY;
+  for (int r = lane; r < nrec; r += 32) {
+    const float2 ml = *reinterpret_cast<const float2*>(rec_of(r));
+    if (ml.y > 0.f) mloc = fmaxf(mloc, ml.x);
   }
+  const float M = warp_max(mloc);
+  float lsum = 0.f, acc0 = 0.f, acc1 = 0.f;
+  for (int base = 0; base < nrec; base += 32) {
+    const int r = base + lane;
+    float4 v[D / 4];
+    float b = 0.f;
+    if (r < nrec) {
+      const float* rc = rec_of(r);
+      const float2 ml = *reinterpret_cast<const float2*>(rc);
+#pragma unroll
+      for (int q = 0; q < D / 4; ++q) v[q] = *reinterpret_cast<const float4*>(rc + 4 + 4 * q);
+      if (ml.y > 0.f) {
+        b = __expf(ml.x - M);
+        lsum = fmaf(b, ml.y, lsum);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < D / 4; ++q) {
+      sacc[warp][lane][4 * q + 0] = b != 0.f ? b * v[q].x : 0.f;
+      sacc[warp][lane][4 * q + 1] = b != 0.f ? b * v[q].y : 0.f;
+      sacc[warp][lane][4 * q + 2] = b != 0.f ? b * v[q].z : 0.f;
+      sacc[warp][lane][4 * q + 3] = b != 0.f ? b * v[q].w : 0.f;
+    }
+    __syncwarp();
+    const int cnt = min(32, nrec - base);
+    for (int k = 0; k < cnt; ++k) {
+      acc0 += sacc[warp][k][lane];
+      acc1 += sacc[warp][k][lane + 32];
+    }
+    __syncwarp();
+  }
+  const float l = warp_sum(lsum);
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  __nv_bfloat16* dst = p.out + (int64_t)(g.start + f) * p.ld_out + h * D;
+  dst[lane] = __float2bfloat16_rn(acc0 * inv);
+  dst[lane + 32] = __float2bfloat16_rn(acc1 * inv);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -669,11 +678,9 @@ size_t band_workspace_bytes(int nseq, int T, int H, int d, int tile_rows, int ma
   int f = full_rows_needed(L, max_qgroup_len);
   if (f == 0 || tile_rows <= 0) return 0;
   // records: one per doc tile (<= ceil(T/64) + nseq) + one global-key record per
-  // sequence, each H x f x (m, l, acc[d]); then the per-sequence tile counters.
+  // sequence, each H x f x (m, l, pad, pad, acc[d]).
   int64_t recs = (T + tile_rows - 1) / tile_rows + 2 * (int64_t)nseq;
-  size_t rec_bytes = (size_t)recs * H * f * (d + 2) * sizeof(float);
-  rec_bytes = (rec_bytes + 255) & ~size_t(255);
-  return rec_bytes + (size_t)nseq * sizeof(int32_t);
+  return (size_t)recs * H * f * (d + 4) * sizeof(float);
 }
 
 int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
@@ -727,16 +734,15 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   }
   const unsigned grid = (unsigned)((a.T + BM - 1) / BM + a.nseq);
   p.ntiles_max = (int)grid;
-  p.counters = nullptr;
-  if (need) {
-    const size_t rec_bytes = need - (size_t)a.nseq * sizeof(int32_t);
-    p.counters = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + rec_bytes);
-  }
-  // Doc rows, head rows over global keys (first tile) and the head-row merge
-  // (last tile of each sequence) in one launch.  (seq_head_base is unused:
-  // head rows are addressed through cu_seqlens.)
+  // Doc rows + head rows over the global keys (first tile of each sequence).
+  // (seq_head_base is unused: head rows are addressed through cu_seqlens.)
   (void)seq_head_base;
-  return GR == 16 ? launch_gr<16>(nbc, maps, p, grid, st) : launch_gr<32>(nbc, maps, p, grid, st);
+  int rc = GR == 16 ? launch_gr<16>(nbc, maps, p, grid, st) : launch_gr<32>(nbc, maps, p, grid, st);
+  if (rc || fneed == 0) return rc;
+  const int64_t items = (int64_t)a.nseq * a.H * fneed;
+  merge_full_rows_kernel<<<(unsigned)((items + MERGE_WARPS - 1) / MERGE_WARPS), MERGE_WARPS * 32, 0, st>>>(p);
+  SC_CHECK_LAUNCH("merge_full_rows_kernel");
+  return SC_OK;
 }
 
 }  // namespace sc
