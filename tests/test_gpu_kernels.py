@@ -59,7 +59,7 @@ def test_residual_layernorm(lib, ydtype, h):
 
 def test_embed_and_cls_score(lib):
     g = torch.Generator(device="cuda").manual_seed(2)
-    V, P, h, T = 50, 20, 96, 40
+    V, P, h, T = 50, 30, 96, 40
     tok = torch.randn((V, h), device="cuda", generator=g)
     pos = torch.randn((P, h), device="cuda", generator=g)
     ids = torch.randint(0, V, (T,), device="cuda", generator=g, dtype=torch.int32)
