@@ -63,6 +63,7 @@ extern "C" {
 #define SC_ATTN_AUTO 0          /* pick the fastest kernel for the pattern      */
 #define SC_ATTN_GENERIC 1       /* warp-per-row CUDA-core kernel (any pattern)  */
 #define SC_ATTN_BAND_MMA 2      /* tiled band kernel (finite doc window)        */
+#define SC_ATTN_TC 3            /* tcgen05/TMEM kernel (wide or dense doc band) */
 
 SC_API const char* sc_last_error(void);
 SC_API int sc_version(void);

@@ -33,6 +33,7 @@ PAD_ZERO_LOGIT = 1
 ALGO_AUTO = 0
 ALGO_GENERIC = 1
 ALGO_BAND_MMA = 2
+ALGO_TC = 3
 
 _p = C.c_void_p
 _i32 = C.c_int32

@@ -183,7 +183,8 @@ def attend_packed(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: Pac
     dt = _dtype_code(q)
     if out is None:
         out = torch.empty((T, hd), dtype=q.dtype, device=q.device)
-    algo_code = {"auto": _lib.ALGO_AUTO, "generic": _lib.ALGO_GENERIC, "band": _lib.ALGO_BAND_MMA}[algo]
+    algo_code = {"auto": _lib.ALGO_AUTO, "generic": _lib.ALGO_GENERIC, "band": _lib.ALGO_BAND_MMA,
+                 "tc": _lib.ALGO_TC}[algo]
     links = pattern.links()
     ws = layout.attn_workspace(heads, d, links)
     _lib.call(

@@ -9,8 +9,14 @@ extern "C" size_t sc_attn_workspace_bytes(int32_t nseq, int32_t total_tokens, in
                                           int32_t max_qgroup_len, const int32_t* links) {
   Links L;
   if (!load_links(links, &L)) return 0;
-  return band_workspace_bytes(nseq, total_tokens, heads, head_dim, tile_rows, max_qgroup_len, L);
+  const size_t band = band_workspace_bytes(nseq, total_tokens, heads, head_dim, tile_rows, max_qgroup_len, L);
+  const size_t tc = tc_workspace_bytes(nseq);
+  return band > tc ? band : tc;
 }
+
+// AUTO kernel choice by doc window: the mma.sync band kernel while the band is
+// narrow (HBM-bound regime), the tcgen05 kernel once it is a dense contraction.
+static constexpr int kBandMaxWindow = 16;
 
 extern "C" int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t row_stride,
                            void* out, int64_t out_row_stride, const int32_t* cu_seqlens,
@@ -35,7 +41,8 @@ extern "C" int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t 
   SC_CHECK_ARG(dtype == SC_DTYPE_F32 || dtype == SC_DTYPE_BF16, "sc_attn_fwd: bad dtype %d", dtype);
   SC_CHECK_ARG((glob_cu == nullptr) == (glob_pos == nullptr), "sc_attn_fwd: glob_cu/glob_pos must be both set or both NULL");
   SC_CHECK_ARG(glob_cu == nullptr || tok_flags != nullptr, "sc_attn_fwd: QDS globals need tok_flags");
-  SC_CHECK_ARG(algo == SC_ATTN_AUTO || algo == SC_ATTN_GENERIC || algo == SC_ATTN_BAND_MMA,
+  SC_CHECK_ARG(algo == SC_ATTN_AUTO || algo == SC_ATTN_GENERIC || algo == SC_ATTN_BAND_MMA ||
+                   algo == SC_ATTN_TC,
                "sc_attn_fwd: bad algo %d", algo);
   SC_CHECK_ARG(max_qgroup_len >= 1, "sc_attn_fwd: max_qgroup_len must be >= 1");
   a.q = q; a.k = k; a.v = v; a.ld = row_stride; a.out = out; a.ld_out = out_row_stride;
@@ -43,10 +50,16 @@ extern "C" int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t 
   a.d = head_dim; a.padding = padding; a.scale = scale; a.flags = tok_flags; a.glob_cu = glob_cu;
   a.glob_pos = glob_pos; a.status = status; a.row_begin = 0; a.row_end = total_tokens;
   cudaStream_t st = (cudaStream_t)stream;
-  if (algo != SC_ATTN_GENERIC) {
+  const int w = a.links.w[2][2];
+  const bool narrow = w >= 0 && w <= kBandMaxWindow;
+  if (algo == SC_ATTN_BAND_MMA || (algo == SC_ATTN_AUTO && narrow)) {
     int rc = launch_attn_band(a, dtype, seq_tile_base, seq_head_base, tile_rows, max_qgroup_len,
                               workspace, workspace_bytes, st);
     if (rc != SC_ERR_UNSUPPORTED || algo == SC_ATTN_BAND_MMA) return rc;
+  }
+  if (algo == SC_ATTN_TC || algo == SC_ATTN_AUTO) {
+    int rc = launch_attn_tc(a, dtype, seq_head_base, max_qgroup_len, workspace, workspace_bytes, st);
+    if (rc != SC_ERR_UNSUPPORTED || algo == SC_ATTN_TC) return rc;
   }
   return launch_attn_generic(a, dtype, st);
 }

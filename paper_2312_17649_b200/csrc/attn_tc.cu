@@ -1,0 +1,501 @@
+// Tensor-core (tcgen05 / TMEM) attention for doc rows when the band is wide
+// enough to be a dense contraction (large w, w = inf, full pattern), bf16 I/O,
+// fp32 accumulation in tensor memory.  SURVEY §7 step 5: "the 128-row Q tile x
+// (128+2w) K tile runs as tcgen05 UMMA (bf16 -> fp32 TMEM accumulators), then a
+// masked online softmax, then PV UMMA".
+//
+// One CTA = 128 doc rows of one sequence x one head.  Warps:
+//   0-3  softmax / epilogue: thread = row; tcgen05.ld of S, mask, online
+//        softmax (exp2 domain), P (bf16) written back over S in TMEM,
+//        O rescale in TMEM when the row max grows, final O / l -> bf16.
+//   4    TMA producer: Q tile, the sequence's global rows (cls + query group)
+//        and a 2-stage ring of 128-key K/V blocks (128B-swizzled boxes).
+//   5    MMA issuer (one thread): S = Q K^T (SS, K-major) into TMEM, then
+//        O += P V with P read from TMEM (TS) and V as an MN-major SMEM operand.
+// Key blocks: the global block (cls + query keys, N = 32) then doc keys
+// [max(0, r0-w), min(n, r0+128+w)) in blocks of 128.  Semantics as the band
+// kernel (R/band.py:48-52, R/attention.py:125-139, :228-257).
+#include <cuda.h>
+
+#include "attn.cuh"
+
+namespace sc {
+namespace tck {
+
+constexpr int BM = 128, D = 64, BN = 128, GR = 32, NS = 2;
+constexpr int NTHREADS = 192;
+constexpr int TMEM_COLS = 256;  // S/P: [0,128), O: [128,192)
+constexpr int S_COL = 0, O_COL = 128;
+constexpr int ROWB = 128;
+
+struct Params {
+  int nseq, H, w;  // w < 0: whole document
+  int padding, link_cls, link_query;
+  float c2;
+  const int32_t* cu;
+  const int32_t* qlen;
+  const int32_t* tile_base;  // 128-row doc tiles per sequence (prefix)
+  __nv_bfloat16* out;
+  int64_t ld_out;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+// ---- tcgen05 helpers -------------------------------------------------------
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+// D[tmem] (+)= A[smem desc] . B[smem desc]
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
+      ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] . B[smem desc]
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }"
+      ::"r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+#define TC_LD32(addr, r)                                                                          \
+  asm volatile(                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                  \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),       \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),   \
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),            \
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),            \
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
+      : "r"(addr))
+
+#define TC_ST16(addr, r)                                                                          \
+  asm volatile(                                                                                   \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+      "%14,%15,%16};" ::"r"(addr),                                                                \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),     \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) \
+      : "memory")
+
+#define TC_ST32(addr, r)                                                                          \
+  asm volatile(                                                                                   \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"             \
+      ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),  \
+      "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]),           \
+      "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]),        \
+      "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),        \
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                                             \
+      : "memory")
+
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// SMEM matrix descriptor, 128B swizzle, SBO = 1024 B (8-row groups), version 1 (sm_100).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// Instruction descriptor, kind::f16: bf16 x bf16 -> f32, A K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+struct Smem {
+  // offsets (bytes) from the 1024-aligned base
+  static constexpr int Q = 0;
+  static constexpr int KG = Q + BM * ROWB;
+  static constexpr int VG = KG + GR * ROWB;
+  static constexpr int KV = VG + GR * ROWB;  // NS x (K block, V block)
+  static constexpr int STAGE = 2 * BN * ROWB;
+  static constexpr int BAR = KV + NS * STAGE;
+  // barriers: qbar, full[NS], empty[NS], s_full, p_full, pv_done, o_final; tmem holder
+  static constexpr int TOTAL = BAR + 16 * 8 + 16;
+};
+
+__global__ void __launch_bounds__(NTHREADS, 1) tc_attn_kernel(
+    const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKg,
+    const __grid_constant__ CUtensorMap tmVg, const __grid_constant__ CUtensorMap tmK,
+    const __grid_constant__ CUtensorMap tmV, Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tile = blockIdx.x, h = blockIdx.y;
+  if (tile >= __ldg(p.tile_base + p.nseq)) return;
+  const int j = find_seq(p.tile_base, p.nseq, tile);
+  const SeqGroups g = seq_groups(p.cu, p.qlen, j);
+  const int n_doc = g.len[2];
+  const int r0 = (tile - __ldg(p.tile_base + j)) * BM;
+  const int rows_here = min(BM, n_doc - r0);
+  const int doc0 = g.start + g.off[2];
+  const int G = 1 + g.len[1];
+  const bool has_glob = (p.link_cls || p.link_query);
+  const int w = p.w;
+  const int lo = w < 0 ? 0 : max(0, r0 - w);
+  const int hi = w < 0 ? n_doc : min(n_doc, r0 + rows_here + w);
+  const int nkb = (hi - lo + BN - 1) / BN;
+
+  const uint32_t sm0 = smem_u32(smem);
+  const uint32_t bar0 = sm0 + Smem::BAR;
+  const uint32_t qbar = bar0, full_bar = bar0 + 8, empty_bar = bar0 + 8 * (1 + NS);
+  const uint32_t s_full = bar0 + 8 * (1 + 2 * NS), p_full = s_full + 8, pv_done = s_full + 16,
+                 o_final = s_full + 24;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Smem::BAR + 16 * 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qbar, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full_bar + 8 * s, 1);
+      mbar_init(empty_bar + 8 * s, 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(pv_done, 1);
+    mbar_init(o_final, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 4) {
+    // ------------------------------------------------------------- TMA
+    if (lane == 0) {
+      const int col = h * D;
+      mbar_expect_tx(qbar, (BM + 2 * GR) * ROWB);
+      tma_load_2d(sm0 + Smem::Q, &tmQ, col, doc0 + r0, qbar);
+      tma_load_2d(sm0 + Smem::KG, &tmKg, col, g.start, qbar);
+      tma_load_2d(sm0 + Smem::VG, &tmVg, col, g.start, qbar);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % NS;
+        if (kb >= NS) mbar_wait(empty_bar + 8 * s, ((kb / NS) & 1) ^ 1);
+        mbar_expect_tx(full_bar + 8 * s, Smem::STAGE);
+        const uint32_t kbuf = sm0 + Smem::KV + s * Smem::STAGE;
+        tma_load_2d(kbuf, &tmK, col, doc0 + lo + kb * BN, full_bar + 8 * s);
+        tma_load_2d(kbuf + BN * ROWB, &tmV, col, doc0 + lo + kb * BN, full_bar + 8 * s);
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------- MMA
+    if (lane == 0) {
+      const uint32_t id_qk = idesc_bf16(BM, BN, 0), id_qg = idesc_bf16(BM, GR, 0),
+                     id_pv = idesc_bf16(BM, D, 1);
+      const uint32_t tS = tmem + S_COL, tO = tmem + O_COL;
+      mbar_wait(qbar, 0);
+      tc_fence_after();
+      const uint64_t qd = sw128_desc(sm0 + Smem::Q);
+      int blk = 0;  // S/P uses so far (phase bookkeeping)
+      uint32_t acc_o = 0;
+      if (has_glob) {
+        const uint64_t kd = sw128_desc(sm0 + Smem::KG);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) mma_ss(tS, qd + 2 * ks, kd + 2 * ks, id_qg, ks > 0);
+        tc_commit(s_full);
+        mbar_wait(p_full, blk & 1);
+        tc_fence_after();
+        const uint64_t vd = sw128_desc(sm0 + Smem::VG);
+#pragma unroll
+        for (int ks = 0; ks < GR / 16; ++ks) mma_ts(tO, tS + 8 * ks, vd + 128 * ks, id_pv, acc_o | ks);
+        acc_o = 1;
+        tc_commit(pv_done);
+        mbar_wait(pv_done, blk & 1);
+        ++blk;
+      }
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % NS;
+        mbar_wait(full_bar + 8 * s, (kb / NS) & 1);
+        tc_fence_after();
+        const uint32_t kbuf = sm0 + Smem::KV + s * Smem::STAGE;
+        const uint64_t kd = sw128_desc(kbuf), vd = sw128_desc(kbuf + BN * ROWB);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) mma_ss(tS, qd + 2 * ks, kd + 2 * ks, id_qk, ks > 0);
+        tc_commit(s_full);
+        mbar_wait(p_full, blk & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < BN / 16; ++ks) mma_ts(tO, tS + 8 * ks, vd + 128 * ks, id_pv, acc_o | ks);
+        acc_o = 1;
+        tc_commit(empty_bar + 8 * s);
+        tc_commit(pv_done);
+        mbar_wait(pv_done, blk & 1);
+        ++blk;
+      }
+      tc_commit(o_final);
+    }
+  } else {
+    // ------------------------------------------------------------- softmax (thread = row)
+    const int r = warp * 32 + lane;  // row within the tile (TMEM lane)
+    const int rr = r0 + r;           // doc-relative row
+    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+    const float c2 = p.c2;
+    float m = -INFINITY, l = 0.f;
+    if (p.padding == SC_PAD_ZERO_LOGIT && w >= 0) {
+      const int ninv = 2 * w + 1 - max(0, min(n_doc, rr + w + 1) - max(0, rr - w));
+      if (ninv > 0) { m = 0.f; l = (float)ninv; }
+    }
+    int blk = 0;
+    const int nblocks = (has_glob ? 1 : 0) + nkb;
+    for (int b = 0; b < nblocks; ++b) {
+      const bool glob = has_glob && b == 0;
+      const int kb = glob ? -1 : b - (has_glob ? 1 : 0);
+      const int ncols = glob ? GR : BN;
+      mbar_wait(s_full, blk & 1);
+      tc_fence_after();
+      // pass 1: masked row max
+      float mx = -INFINITY;
+      for (int c0 = 0; c0 < ncols; c0 += 32) {
+        uint32_t v[32];
+        TC_LD32(lane_addr + S_COL + c0, v);
+        tc_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int c = c0 + e;
+          bool ok;
+          if (glob) {
+            ok = c < G && (c == 0 ? p.link_cls : p.link_query);
+          } else {
+            const int t = lo + kb * BN + c;
+            ok = t < hi && (w < 0 || (t - rr <= w && rr - t <= w));
+          }
+          if (ok) mx = fmaxf(mx, __uint_as_float(v[e]));
+        }
+      }
+      const float mnew = fmaxf(m, mx);
+      const float base = mnew == -INFINITY ? 0.f : mnew * c2;
+      const float alpha = ex2(fmaf(m, c2, -base));
+      // rescale O (already accumulated blocks) when this row's max grew
+      const bool need = blk > 0 && alpha != 1.f;
+      if (__any_sync(0xffffffffu, need)) {
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 32) {
+          uint32_t v[32];
+          TC_LD32(lane_addr + O_COL + c0, v);
+          tc_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
+          TC_ST32(lane_addr + O_COL + c0, v);
+        }
+      }
+      // pass 2: P = exp2(s*c2 - base) (bf16) written over S columns [0, ncols/2)
+      float sum = 0.f;
+      for (int c0 = 0; c0 < ncols; c0 += 32) {
+        uint32_t v[32], pk[16];
+        TC_LD32(lane_addr + S_COL + c0, v);
+        tc_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          float pe[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int c = c0 + e + u;
+            bool ok;
+            if (glob) {
+              ok = c < G && (c == 0 ? p.link_cls : p.link_query);
+            } else {
+              const int t = lo + kb * BN + c;
+              ok = t < hi && (w < 0 || (t - rr <= w && rr - t <= w));
+            }
+            pe[u] = ok ? ex2(fmaf(__uint_as_float(v[e + u]), c2, -base)) : 0.f;
+          }
+          sum += pe[0] + pe[1];
+          pk[e / 2] = pack_bf16(pe[0], pe[1]);
+        }
+        TC_ST16(lane_addr + S_COL + c0 / 2, pk);
+      }
+      l = fmaf(l, alpha, sum);
+      m = mnew;
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      ++blk;
+    }
+    // epilogue: O / l -> bf16 row
+    mbar_wait(o_final, 0);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* dst = p.out + (int64_t)(doc0 + rr) * p.ld_out + h * D;
+#pragma unroll
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      uint32_t v[32];
+      TC_LD32(lane_addr + O_COL + c0, v);
+      tc_wait_ld();
+      if (r < rows_here) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_bf16(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
+          u.y = pack_bf16(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
+          u.z = pack_bf16(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
+          u.w = pack_bf16(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+          d4[q] = u;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS) : "memory");
+  }
+}
+
+// 128-row doc-tile prefix per sequence (single CTA scan).
+__global__ void tile128_prefix_kernel(const int32_t* __restrict__ cu, const int32_t* __restrict__ qlen, int nseq,
+                                      int32_t* __restrict__ base) {
+  __shared__ int32_t s[1024];
+  int carry = 0;
+  for (int b = 0; b < nseq; b += blockDim.x) {
+    const int j = b + threadIdx.x;
+    int n = 0;
+    if (j < nseq) n = (cu[j + 1] - cu[j] - 1 - qlen[j] + BM - 1) / BM;
+    s[threadIdx.x] = n;
+    __syncthreads();
+    for (int o = 1; o < blockDim.x; o <<= 1) {
+      int a = threadIdx.x >= o ? s[threadIdx.x - o] : 0;
+      __syncthreads();
+      s[threadIdx.x] += a;
+      __syncthreads();
+    }
+    if (j < nseq) base[j + 1] = carry + s[threadIdx.x];
+    carry += s[blockDim.x - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) base[0] = 0;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t ld, int box_rows) {
+  static EncodeFn enc = nullptr;
+  if (!enc) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    enc = reinterpret_cast<EncodeFn>(ptr);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)D, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace tck
+
+size_t tc_workspace_bytes(int nseq) { return (size_t)(nseq + 1) * sizeof(int32_t); }
+
+int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_head_base, int max_qgroup_len,
+                   void* ws, size_t ws_bytes, cudaStream_t st) {
+  using namespace tck;
+  const Links& L = a.links;
+  auto unsupported = [](const char* why) {
+    set_error("tcgen05 kernel: %s", why);
+    return SC_ERR_UNSUPPORTED;
+  };
+  if (dtype != SC_DTYPE_BF16) return unsupported("needs bf16");
+  if (a.d != D) return unsupported("needs head_dim 64");
+  if (a.glob_cu) return unsupported("QDS global tokens");
+  const int w = L.w[2][2];
+  if (w == SC_LINK_NONE) return unsupported("doc rows must attend doc keys");
+  if (L.w[2][0] != SC_LINK_FULL && L.w[2][0] != SC_LINK_NONE) return unsupported("windowed doc->cls");
+  if (L.w[2][1] != SC_LINK_FULL && L.w[2][1] != SC_LINK_NONE) return unsupported("windowed doc->query");
+  if (max_qgroup_len + 1 > GR) return unsupported("query group longer than 31 rows");
+  if (((uintptr_t)a.q | (uintptr_t)a.k | (uintptr_t)a.v | (uintptr_t)a.out) & 15) return unsupported("alignment");
+  if ((a.ld * 2) % 16 || (a.ld_out * 2) % 16) return unsupported("row strides");
+  if (!ws || ws_bytes < tc_workspace_bytes(a.nseq)) return unsupported("workspace too small");
+
+  CUtensorMap mQ, mKg, mVg, mK, mV;
+  const int64_t cols = (int64_t)a.H * D;
+  if (!make_map(&mQ, a.q, cols, a.T, a.ld, BM) || !make_map(&mKg, a.k, cols, a.T, a.ld, GR) ||
+      !make_map(&mVg, a.v, cols, a.T, a.ld, GR) || !make_map(&mK, a.k, cols, a.T, a.ld, BN) ||
+      !make_map(&mV, a.v, cols, a.T, a.ld, BN))
+    return unsupported("cuTensorMapEncodeTiled failed");
+
+  int32_t* tbase = static_cast<int32_t*>(ws);
+  tile128_prefix_kernel<<<1, 1024, 0, st>>>(a.cu, a.qlen, a.nseq, tbase);
+  SC_CHECK_LAUNCH("tile128_prefix_kernel");
+
+  Params p;
+  p.nseq = a.nseq; p.H = a.H; p.w = w == SC_LINK_FULL ? -1 : w; p.padding = a.padding;
+  p.link_cls = L.w[2][0] == SC_LINK_FULL; p.link_query = L.w[2][1] == SC_LINK_FULL;
+  p.c2 = 1.4426950408889634f / a.scale;
+  p.cu = a.cu; p.qlen = a.qlen; p.tile_base = tbase;
+  p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
+  const size_t smem = Smem::TOTAL + 1024;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(tc_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return unsupported("shared memory request");
+    attr = true;
+  }
+  dim3 grid((unsigned)((a.T + BM - 1) / BM + a.nseq), (unsigned)a.H);
+  tc_attn_kernel<<<grid, NTHREADS, smem, st>>>(mQ, mKg, mVg, mK, mV, p);
+  SC_CHECK_LAUNCH("tc_attn_kernel");
+  // Head rows (cls + query group): generic kernel in head-row mode, scanning the doc keys.
+  AttnArgs hd = a;
+  hd.head_base = seq_head_base;
+  hd.n_head_rows = a.nseq * (1 + max_qgroup_len);
+  hd.partials = nullptr;
+  return launch_attn_generic(hd, dtype, st);
+}
+
+}  // namespace sc

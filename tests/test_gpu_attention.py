@@ -229,3 +229,30 @@ def test_band_kernel_repeatable_and_forced(P, name):
     with pytest.raises(NotImplementedError):
         xf = x.float()
         P.attend_packed(xf[:, :H * d], xf[:, H * d:2 * H * d], xf[:, 2 * H * d:], lay, pat, H, algo="band")
+
+
+@pytest.mark.parametrize("name,w,pad", [("sparse", 0, "exclude"), ("sparse", 4, "exclude"), ("sparse", 64, "exclude"),
+                                        ("sparse", 256, "zero-logit"), ("sparse", math.inf, "exclude"),
+                                        ("longformer", 100, "exclude"), ("full", math.inf, "exclude"),
+                                        ("longformer", 33, "zero-logit")])
+def test_tcgen05_kernel_vs_oracle(P, name, w, pad):
+    """The tcgen05/TMEM kernel (forced) on a packed varlen batch vs the oracle at bf16 tolerance."""
+    rng = np.random.default_rng(17)
+    H, d = 4, 64
+    shapes = [(10, 300), (1, 1), (7, 130), (30, 127), (10, 700)]
+    seq = [m + n + 3 for m, n in shapes]
+    lay = P.PackedLayout.from_lengths(seq, [m + 1 for m, _ in shapes], device="cuda")
+    T = sum(seq)
+    x = torch.from_numpy(rng.standard_normal((T, 3 * H * d)).astype(np.float32)).cuda().to(torch.bfloat16)
+    pat = P.make_pattern(name, w)
+    out = P.attend_packed(x[:, :H * d], x[:, H * d:2 * H * d], x[:, 2 * H * d:], lay, pat, H, padding=pad,
+                          algo="tc").double().cpu().numpy()
+    xin = x.double().cpu().numpy().reshape(T, 3, H, d)
+    opat = O.make_pattern(name, w)
+    r = 0
+    for (m, n), s in zip(shapes, seq):
+        blk = xin[r:r + s].transpose(1, 2, 0, 3)
+        spans = cases.attn_spans(m, n)
+        ref = np.concatenate(O.apply_pattern(spans, O.split_groups(spans, *blk), opat, math.sqrt(d), pad), axis=-2)
+        np.testing.assert_allclose(out[r:r + s].reshape(s, H, d).transpose(1, 0, 2), ref, atol=2e-2, rtol=0)
+        r += s
