@@ -48,13 +48,16 @@ __host__ __device__ inline int full_rows_needed(const Links& L, int max_qgroup_l
 // pattern/shape is outside its envelope (the caller then uses the generic kernel).
 size_t band_workspace_bytes(int nseq, int T, int H, int d, int tile_rows, int max_qgroup_len,
                             const Links& L);
+// doc_rows = false: head rows only (cls/query rows + CLS split-softmax records),
+// used after the tcgen05 kernel has computed the doc rows.
 int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
                      const int32_t* seq_head_base, int tile_rows, int max_qgroup_len, void* ws,
-                     size_t ws_bytes, cudaStream_t st);
+                     size_t ws_bytes, cudaStream_t st, bool doc_rows = true);
 
 // tcgen05 / TMEM kernel for wide bands and dense doc rows (attn_tc.cu).
 size_t tc_workspace_bytes(int nseq);
-int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_head_base, int max_qgroup_len,
-                   void* ws, size_t ws_bytes, cudaStream_t st);
+int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
+                   const int32_t* seq_head_base, int tile_rows, int max_qgroup_len, void* ws,
+                   size_t ws_bytes, cudaStream_t st);
 
 }  // namespace sc

@@ -10,8 +10,8 @@ extern "C" size_t sc_attn_workspace_bytes(int32_t nseq, int32_t total_tokens, in
   Links L;
   if (!load_links(links, &L)) return 0;
   const size_t band = band_workspace_bytes(nseq, total_tokens, heads, head_dim, tile_rows, max_qgroup_len, L);
-  const size_t tc = tc_workspace_bytes(nseq);
-  return band > tc ? band : tc;
+  // the tcgen05 path uses [band records | 128-row tile prefix]
+  return ((band + 255) & ~size_t(255)) + tc_workspace_bytes(nseq);
 }
 
 // AUTO kernel choice by doc window: the mma.sync band kernel while the band is
@@ -58,7 +58,8 @@ extern "C" int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t 
     if (rc != SC_ERR_UNSUPPORTED || algo == SC_ATTN_BAND_MMA) return rc;
   }
   if (algo == SC_ATTN_TC || algo == SC_ATTN_AUTO) {
-    int rc = launch_attn_tc(a, dtype, seq_head_base, max_qgroup_len, workspace, workspace_bytes, st);
+    int rc = launch_attn_tc(a, dtype, seq_tile_base, seq_head_base, tile_rows, max_qgroup_len, workspace,
+                            workspace_bytes, st);
     if (rc != SC_ERR_UNSUPPORTED || algo == SC_ATTN_TC) return rc;
   }
   return launch_attn_generic(a, dtype, st);

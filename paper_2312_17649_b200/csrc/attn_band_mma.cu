@@ -44,6 +44,7 @@ constexpr int REC = D + 4; // split-softmax record: m, l, pad, pad, acc[D] (16B-
 struct Params {
   int nseq, H, w, kb_rows, fneed, fmax, padding;
   int link_cls, link_query;
+  int doc_rows;  // 0: head rows only (doc rows computed by the tcgen05 kernel)
   // head rows (cls = group 0, query = group 1): links to cls / query keys, doc FULL
   int hl[2][2], hdoc[2];
   int ntiles_max;      // record index of sequence j's global-key record = ntiles_max + j
@@ -261,14 +262,14 @@ __global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
     if (lane == 0) {
       prefetch_map(&tmQ); prefetch_map(&tmKb); prefetch_map(&tmVb);
       prefetch_map(&tmKg); prefetch_map(&tmVg); prefetch_map(&tmQf);
-      const uint32_t bytes = (uint32_t)(q_bytes + 3 * f_bytes + 2 * kb_box * ROWB);
+      const uint32_t bytes = (uint32_t)((p.doc_rows ? q_bytes : 0) + 3 * f_bytes + 2 * kb_box * ROWB);
       for (int h = 0; h < p.H; ++h) {
         const int s = h % NS;
         if (h >= NS) mbar_wait(empty_bar + 8 * s, ((h / NS) & 1) ^ 1);
         const uint32_t fb = full_bar + 8 * s;
         mbar_expect_tx(fb, bytes);
         const int col = h * D;
-        tma_load_2d(q_buf(s), &tmQ, col, doc_row0, fb);
+        if (p.doc_rows) tma_load_2d(q_buf(s), &tmQ, col, doc_row0, fb);
         tma_load_2d(kb_buf(s), &tmKb, col, doc_row0 - w, fb);
         tma_load_2d(vb_buf(s), &tmVb, col, doc_row0 - w, fb);
         tma_load_2d(kg_buf(s), &tmKg, col, g.start, fb);
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
   // ------------------------------------------------------------ doc warps
   const int gq = lane >> 2, tq = lane & 3;
   const int wr0 = warp * 16;
-  const bool active = wr0 < rows_here;
+  const bool active = p.doc_rows && wr0 < rows_here;
   const int ra = r0 + wr0 + gq, rb = ra + 8;  // doc-relative rows of this thread
 
   // Static masks (tile independent except at sequence edges): bit (nb*4 + e)
@@ -685,10 +686,11 @@ size_t band_workspace_bytes(int nseq, int T, int H, int d, int tile_rows, int ma
 
 int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
                      const int32_t* seq_head_base, int tile_rows, int max_qgroup_len, void* ws,
-                     size_t ws_bytes, cudaStream_t st) {
+                     size_t ws_bytes, cudaStream_t st, bool doc_rows) {
   using namespace bandk;
   const Links& L = a.links;
-  const int w = L.w[2][2];
+  // Head-rows-only mode stages just the tile's own 64 doc keys (no halo).
+  const int w = doc_rows ? L.w[2][2] : 0;
   auto unsupported = [](const char* why) {
     set_error("band kernel: %s", why);
     return SC_ERR_UNSUPPORTED;
@@ -718,7 +720,7 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
     return unsupported("cuTensorMapEncodeTiled failed");
 
   Params p;
-  p.nseq = a.nseq; p.H = a.H; p.w = w;
+  p.nseq = a.nseq; p.H = a.H; p.w = w; p.doc_rows = doc_rows ? 1 : 0;
   const int nbc = (16 + 2 * w + 31) / 32;
   p.kb_rows = 48 + 32 * nbc;
   p.fneed = fneed; p.fmax = fneed; p.padding = a.padding;

@@ -143,6 +143,33 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Row softmax of NC raw logits held as bits in v (masked entries = -inf):
+// updates the running max m, returns alpha = exp2((m_old - m_new) c2) and the
+// row sum of P, and writes P (bf16 pairs, packed in place) to TMEM at p_addr.
+template <int NC>
+__device__ __forceinline__ void row_softmax(uint32_t (&v)[NC], float c2, float& m, float& alpha, float& sum,
+                                            uint32_t p_addr) {
+  float mx = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < NC; ++e) mx = fmaxf(mx, __uint_as_float(v[e]));
+  const float mnew = fmaxf(m, mx);
+  const float base = mnew == -INFINITY ? 0.f : mnew * c2;
+  alpha = ex2(fmaf(m, c2, -base));
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int e = 0; e < NC; e += 2) {
+    const float p0 = ex2(fmaf(__uint_as_float(v[e]), c2, -base));
+    const float p1 = ex2(fmaf(__uint_as_float(v[e + 1]), c2, -base));
+    s0 += p0;
+    s1 += p1;
+    v[e / 2] = pack_bf16(p0, p1);
+  }
+  sum = s0 + s1;
+  m = mnew;
+#pragma unroll
+  for (int c = 0; c < NC / 2; c += 16) TC_ST16(p_addr + c, (&v[c]));
+}
+
 struct Smem {
   // offsets (bytes) from the 1024-aligned base
   static constexpr int Q = 0;
@@ -287,73 +314,47 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_attn_kernel(
     const int nblocks = (has_glob ? 1 : 0) + nkb;
     for (int b = 0; b < nblocks; ++b) {
       const bool glob = has_glob && b == 0;
-      const int kb = glob ? -1 : b - (has_glob ? 1 : 0);
-      const int ncols = glob ? GR : BN;
       mbar_wait(s_full, blk & 1);
       tc_fence_after();
-      // pass 1: masked row max
-      float mx = -INFINITY;
-      for (int c0 = 0; c0 < ncols; c0 += 32) {
-        uint32_t v[32];
-        TC_LD32(lane_addr + S_COL + c0, v);
+      float alpha, sum;
+      if (glob) {
+        uint32_t v[GR];
+        TC_LD32(lane_addr + S_COL, v);
         tc_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int c = c0 + e;
-          bool ok;
-          if (glob) {
-            ok = c < G && (c == 0 ? p.link_cls : p.link_query);
-          } else {
-            const int t = lo + kb * BN + c;
-            ok = t < hi && (w < 0 || (t - rr <= w && rr - t <= w));
+        for (int e = 0; e < GR; ++e)
+          if (!(e < G && (e == 0 ? p.link_cls : p.link_query))) v[e] = __float_as_uint(-INFINITY);
+        row_softmax<GR>(v, c2, m, alpha, sum, lane_addr + S_COL);
+      } else {
+        uint32_t v[BN];
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 32) TC_LD32(lane_addr + S_COL + c0, (&v[c0]));
+        tc_wait_ld();
+        const int k0 = lo + (b - (has_glob ? 1 : 0)) * BN;
+        const bool interior =
+            k0 + BN <= hi && (w < 0 || (k0 >= r0 + rows_here - 1 - w && k0 + BN - 1 <= r0 + w));
+        if (!interior) {
+#pragma unroll
+          for (int e = 0; e < BN; ++e) {
+            const int t = k0 + e;
+            if (!(t < hi && (w < 0 || (t - rr <= w && rr - t <= w)))) v[e] = __float_as_uint(-INFINITY);
           }
-          if (ok) mx = fmaxf(mx, __uint_as_float(v[e]));
         }
+        row_softmax<BN>(v, c2, m, alpha, sum, lane_addr + S_COL);
       }
-      const float mnew = fmaxf(m, mx);
-      const float base = mnew == -INFINITY ? 0.f : mnew * c2;
-      const float alpha = ex2(fmaf(m, c2, -base));
       // rescale O (already accumulated blocks) when this row's max grew
-      const bool need = blk > 0 && alpha != 1.f;
-      if (__any_sync(0xffffffffu, need)) {
+      if (__any_sync(0xffffffffu, blk > 0 && alpha != 1.f)) {
 #pragma unroll
         for (int c0 = 0; c0 < D; c0 += 32) {
-          uint32_t v[32];
-          TC_LD32(lane_addr + O_COL + c0, v);
+          uint32_t o[32];
+          TC_LD32(lane_addr + O_COL + c0, o);
           tc_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
-          TC_ST32(lane_addr + O_COL + c0, v);
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          TC_ST32(lane_addr + O_COL + c0, o);
         }
-      }
-      // pass 2: P = exp2(s*c2 - base) (bf16) written over S columns [0, ncols/2)
-      float sum = 0.f;
-      for (int c0 = 0; c0 < ncols; c0 += 32) {
-        uint32_t v[32], pk[16];
-        TC_LD32(lane_addr + S_COL + c0, v);
-        tc_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float pe[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int c = c0 + e + u;
-            bool ok;
-            if (glob) {
-              ok = c < G && (c == 0 ? p.link_cls : p.link_query);
-            } else {
-              const int t = lo + kb * BN + c;
-              ok = t < hi && (w < 0 || (t - rr <= w && rr - t <= w));
-            }
-            pe[u] = ok ? ex2(fmaf(__uint_as_float(v[e + u]), c2, -base)) : 0.f;
-          }
-          sum += pe[0] + pe[1];
-          pk[e / 2] = pack_bf16(pe[0], pe[1]);
-        }
-        TC_ST16(lane_addr + S_COL + c0 / 2, pk);
       }
       l = fmaf(l, alpha, sum);
-      m = mnew;
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -443,8 +444,9 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t row
 
 size_t tc_workspace_bytes(int nseq) { return (size_t)(nseq + 1) * sizeof(int32_t); }
 
-int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_head_base, int max_qgroup_len,
-                   void* ws, size_t ws_bytes, cudaStream_t st) {
+int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
+                   const int32_t* seq_head_base, int tile_rows, int max_qgroup_len, void* ws,
+                   size_t ws_bytes, cudaStream_t st) {
   using namespace tck;
   const Links& L = a.links;
   auto unsupported = [](const char* why) {
@@ -459,9 +461,15 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_head_base, i
   if (L.w[2][0] != SC_LINK_FULL && L.w[2][0] != SC_LINK_NONE) return unsupported("windowed doc->cls");
   if (L.w[2][1] != SC_LINK_FULL && L.w[2][1] != SC_LINK_NONE) return unsupported("windowed doc->query");
   if (max_qgroup_len + 1 > GR) return unsupported("query group longer than 31 rows");
+  // head rows go through the band kernel's head-rows-only mode: same link envelope
+  for (int x : {L.w[0][0], L.w[0][1], L.w[0][2], L.w[1][0], L.w[1][1], L.w[1][2]})
+    if (x != SC_LINK_FULL && x != SC_LINK_NONE) return unsupported("windowed head-row link");
+  if (tile_rows != 64 || !seq_tile_base || !seq_head_base) return unsupported("layout tiles must be 64 rows");
   if (((uintptr_t)a.q | (uintptr_t)a.k | (uintptr_t)a.v | (uintptr_t)a.out) & 15) return unsupported("alignment");
   if ((a.ld * 2) % 16 || (a.ld_out * 2) % 16) return unsupported("row strides");
-  if (!ws || ws_bytes < tc_workspace_bytes(a.nseq)) return unsupported("workspace too small");
+  // workspace = [band-kernel records (head rows) | 128-row tile prefix]
+  const size_t band_bytes = (band_workspace_bytes(a.nseq, a.T, a.H, a.d, tile_rows, max_qgroup_len, L) + 255) & ~size_t(255);
+  if (!ws || ws_bytes < band_bytes + tc_workspace_bytes(a.nseq)) return unsupported("workspace too small");
 
   CUtensorMap mQ, mKg, mVg, mK, mV;
   const int64_t cols = (int64_t)a.H * D;
@@ -470,7 +478,7 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_head_base, i
       !make_map(&mV, a.v, cols, a.T, a.ld, BN))
     return unsupported("cuTensorMapEncodeTiled failed");
 
-  int32_t* tbase = static_cast<int32_t*>(ws);
+  int32_t* tbase = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + band_bytes);
   tile128_prefix_kernel<<<1, 1024, 0, st>>>(a.cu, a.qlen, a.nseq, tbase);
   SC_CHECK_LAUNCH("tile128_prefix_kernel");
 
@@ -490,12 +498,10 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_head_base, i
   dim3 grid((unsigned)((a.T + BM - 1) / BM + a.nseq), (unsigned)a.H);
   tc_attn_kernel<<<grid, NTHREADS, smem, st>>>(mQ, mKg, mVg, mK, mV, p);
   SC_CHECK_LAUNCH("tc_attn_kernel");
-  // Head rows (cls + query group): generic kernel in head-row mode, scanning the doc keys.
-  AttnArgs hd = a;
-  hd.head_base = seq_head_base;
-  hd.n_head_rows = a.nseq * (1 + max_qgroup_len);
-  hd.partials = nullptr;
-  return launch_attn_generic(hd, dtype, st);
+  // Head rows (cls + query group): the band kernel in head-rows-only mode
+  // streams each doc key once for the CLS split-softmax records, then merges.
+  return launch_attn_band(a, dtype, seq_tile_base, seq_head_base, tile_rows, max_qgroup_len, ws,
+                          band_bytes, st, /*doc_rows=*/false);
 }
 
 }  // namespace sc
