@@ -87,6 +87,13 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
+// Pull a box into L2 only (no smem, no barrier): the producer runs one
+// pipeline round ahead so the next round's TMA loads are served from L2.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -160,7 +167,8 @@ __device__ __forceinline__ void pv16(uint32_t vbuf, int key0, int lane, const fl
 
 // Online-softmax update over NB n8 blocks of RAW logits (masked to -inf) for
 // rows (g, g+8).  m is kept in raw-logit units; c2 = log2(e)/scale.  Overwrites s with P.
-template <int NB>
+// kFresh: o is still zero (first update of a row block) -> skip the O rescale.
+template <int NB, bool kFresh = false>
 __device__ __forceinline__ void softmax_update(float (&s)[NB][4], float c2, float& m0, float& m1,
                                                float& l0, float& l1, float (&o)[8][4]) {
   float x0 = -INFINITY, x1 = -INFINITY;
@@ -188,12 +196,14 @@ __device__ __forceinline__ void softmax_update(float (&s)[NB][4], float c2, floa
   }
   l0 = fmaf(l0, a0, r0);
   l1 = fmaf(l1, a1, r1);
+  if constexpr (!kFresh) {
 #pragma unroll
-  for (int nb = 0; nb < 8; ++nb) {
-    o[nb][0] *= a0;
-    o[nb][1] *= a0;
-    o[nb][2] *= a1;
-    o[nb][3] *= a1;
+    for (int nb = 0; nb < 8; ++nb) {
+      o[nb][0] *= a0;
+      o[nb][1] *= a0;
+      o[nb][2] *= a1;
+      o[nb][3] *= a1;
+    }
   }
   m0 = n0;
   m1 = n1;
@@ -267,6 +277,12 @@ __global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
         const int s = h % NS;
         if (h >= NS) mbar_wait(empty_bar + 8 * s, ((h / NS) & 1) ^ 1);
         const uint32_t fb = full_bar + 8 * s;
+        if (h + NS < p.H) {  // L2 prefetch of the boxes this stage will hold next round
+          const int pc = (h + NS) * D;
+          if (p.doc_rows) tma_prefetch_2d(&tmQ, pc, doc_row0);
+          tma_prefetch_2d(&tmKb, pc, doc_row0 - w);
+          tma_prefetch_2d(&tmVb, pc, doc_row0 - w);
+        }
         mbar_expect_tx(fb, bytes);
         const int col = h * D;
         if (p.doc_rows) tma_load_2d(q_buf(s), &tmQ, col, doc_row0, fb);
@@ -366,7 +382,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             if (!((bmask[0] >> (nb * 4 + e)) & 1)) sc[NG + nb][e] = -INFINITY;
-        softmax_update<NG + 4>(sc, c2, m0, m1, l0, l1, o);
+        softmax_update<NG + 4, true>(sc, c2, m0, m1, l0, l1, o);
 #pragma unroll
         for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, lane, sc[2 * gc], sc[2 * gc + 1], o);
         pv16(vb_buf(s), wr0, lane, sc[NG], sc[NG + 1], o);
@@ -439,7 +455,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
           float o[8][4];
           zero_o(o);
           float fm0 = -INFINITY, fm1 = -INFINITY, fl0 = 0.f, fl1 = 0.f;
-          softmax_update<8>(sc, c2, fm0, fm1, fl0, fl1, o);
+          softmax_update<8, true>(sc, c2, fm0, fm1, fl0, fl1, o);
 #pragma unroll
           for (int kp = 0; kp < 4; ++kp) pv16(vb_buf(s), w + kp * 16, lane, sc[2 * kp], sc[2 * kp + 1], o);
           fl0 += __shfl_xor_sync(0xffffffffu, fl0, 1);
@@ -490,7 +506,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
           float o[8][4];
           zero_o(o);
           float hm0 = -INFINITY, hm1 = -INFINITY, hl0 = 0.f, hl1 = 0.f;
-          softmax_update<GR / 8>(sc, c2, hm0, hm1, hl0, hl1, o);
+          softmax_update<GR / 8, true>(sc, c2, hm0, hm1, hl0, hl1, o);
 #pragma unroll
           for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, lane, sc[2 * gc], sc[2 * gc + 1], o);
           hl0 += __shfl_xor_sync(0xffffffffu, hl0, 1);
@@ -644,6 +660,7 @@ static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, c
   constexpr size_t smem = (size_t)NS * stage_bytes + 2 * NS * 8 + 64 + 1024;
   static bool attr = false;
   if (!attr) {
+    cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess) {
       set_error("band kernel: shared memory request of %zu bytes failed", smem);

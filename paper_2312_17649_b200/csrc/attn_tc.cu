@@ -182,7 +182,7 @@ struct Smem {
   static constexpr int TOTAL = BAR + 16 * 8 + 16;
 };
 
-__global__ void __launch_bounds__(NTHREADS, 1) tc_attn_kernel(
+__global__ void __launch_bounds__(NTHREADS, 2) tc_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKg,
     const __grid_constant__ CUtensorMap tmVg, const __grid_constant__ CUtensorMap tmK,
     const __grid_constant__ CUtensorMap tmV, Params p) {
@@ -491,6 +491,8 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   const size_t smem = Smem::TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
+    // two CTAs per SM (2 x 256 TMEM columns): ask for the full shared-memory carveout
+    cudaFuncSetAttribute(tc_attn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (cudaFuncSetAttribute(tc_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return unsupported("shared memory request");
     attr = true;
