@@ -40,6 +40,9 @@ constexpr int PRODW = 4;
 constexpr int NTHREADS = 160;
 constexpr int MAX_W = 96;  // Kb box rows 64 + 2w <= 256 (TMA box limit)
 constexpr int REC = D + 4; // split-softmax record: m, l, pad, pad, acc[D] (16B-aligned acc)
+// Resident CTAs per SM the register/smem budget targets (measured on B200,
+// s=4099 H=12: 3 CTAs / 2 stages is best for w <= 8, 2 CTAs / 3 stages above).
+__host__ __device__ constexpr int min_ctas(int nbc) { return nbc == 1 ? 3 : 2; }
 
 struct Params {
   int nseq, H, w, kb_rows, fneed, fmax, padding;
@@ -216,7 +219,7 @@ __device__ __forceinline__ void zero_o(float (&o)[8][4]) {
 // NBC: band chunks of 32 keys per 16-row warp block (ceil((16+2w)/32)).
 // GR: global rows staged per head (16 or 32).  NS: pipeline stages.
 template <int NBC, int GR, int NS>
-__global__ void __launch_bounds__(NTHREADS, 2) band_attn_kernel(
+__global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQf,
     const __grid_constant__ CUtensorMap tmKg, const __grid_constant__ CUtensorMap tmVg,
     const __grid_constant__ CUtensorMap tmKb, const __grid_constant__ CUtensorMap tmVb, Params p) {
@@ -650,7 +653,8 @@ using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CU
 template <int NBC, int GR>
 constexpr int stages_for() {
   constexpr int stage_bytes = (BM + 3 * GR + 2 * (48 + 32 * NBC)) * ROWB;
-  return (3 * stage_bytes + 2048 <= 113 * 1024) ? 3 : 2;
+  constexpr int budget = 227 * 1024 / min_ctas(NBC) - 2048;
+  return (3 * stage_bytes <= budget) ? 3 : 2;
 }
 
 template <int NBC, int GR>
