@@ -39,5 +39,6 @@ from .encoder import (
     resolve_pattern,
 )
 from .layout import PackedLayout
+from .serialize import SerializationError, load_model, save_model
 
 __version__ = "0.1.0"

@@ -125,13 +125,30 @@ def gen_encoders(skip_long):
     np.savez_compressed(os.path.join(HERE, "encoder.npz"), **out)
 
 
+def gen_serialize():
+    """Model directories written by the reference's save_model (R/serialize.py:50-76)."""
+    import math as _m
+
+    from sparsecross import serialize as S
+
+    scores = {}
+    for tag, prec, window in (("f64", "f64", 2), ("f32", "f32", 2), ("inf", "f64", _m.inf)):
+        cfg = E.EncoderConfig(layers=1, embed_dim=8, heads=2, ff_dim=16, max_positions=32, vocab_size=20,
+                              pattern="sparse", window=window, precision=prec)
+        model = E.CrossEncoder(cfg, seed=42)
+        S.save_model(model, os.path.join(HERE, f"ref_model_{tag}"))
+        seq = E.assemble_input([3, 4, 5], [6, 7, 8, 9])
+        scores[f"score_{tag}"] = model.score(seq.ids, seq.partition)
+    np.savez_compressed(os.path.join(HERE, "serialize.npz"), **scores)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-long", action="store_true")
     ap.add_argument("--only", default="")
     args = ap.parse_args()
     steps = {"band": gen_band, "masks": gen_masks, "attention": gen_attention,
-             "encoder": lambda: gen_encoders(args.skip_long)}
+             "encoder": lambda: gen_encoders(args.skip_long), "serialize": gen_serialize}
     for name, fn in steps.items():
         if args.only and name not in args.only.split(","):
             continue
