@@ -50,9 +50,18 @@ def peaks():
 
 
 def workload(args):
+    """(encoder config, doc_len, s): documents (configs[2], s=4099) or passages (configs[1], s=177)."""
     doc_len = args.doc_len
     s = QUERY_LEN + doc_len + 3
     return dict(ELECTRA, max_positions=max(s, 512)), doc_len, s
+
+
+def workload_name(doc_len, s):
+    if doc_len <= 512:
+        return (f"ELECTRA-base sparse cross-encoder, passages {QUERY_LEN + doc_len} tok (q{QUERY_LEN}+p{doc_len}, "
+                f"s={s}), w=4 asymmetric, bf16 (BASELINE configs[1])")
+    return (f"ELECTRA-base sparse cross-encoder, documents {QUERY_LEN + doc_len} tok (q{QUERY_LEN}+d{doc_len}, "
+            f"s={s}), w=4 asymmetric, packed varlen batch (BASELINE configs[2])")
 
 
 def make_batch(P, cfg, doc_len, pairs, rank, seed=0, varlen=False):
@@ -167,7 +176,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
         "steps": len(timed), "warmup": args.warmup, "ms_per_step": t_layer * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generator ids, seed 0)",
-        "config": {"workload": "ELECTRA-base sparse CE, documents 4096 tok (s=4099), w=4", "seq_len": s,
+        "config": {"workload": workload_name(doc_len, s), "seq_len": s,
                    "doc_len": doc_len, "query_len": QUERY_LEN, "window": 4, "pattern": "sparse"},
         "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cpu_threads(), "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -220,7 +229,16 @@ def run_gpu(args):
         ev.record(stream)
         attn_events.append(ev)
 
+    use_graph = args.graph == "on" or (args.graph == "auto" and doc_len <= 512)
+    graphed = None
+    if use_graph:
+        from paper_2312_17649_b200.encoder import GraphedScorer
+
+        graphed = GraphedScorer(model, batch)
+
     def device_step(h=None):
+        if graphed is not None:
+            return gather(graphed(ids_dev))
         x = model.encode_packed(ids_dev, layout, check_finite=False, attn_hook=h)
         return gather(model.scores_from_hidden(x, layout))
 
@@ -256,10 +274,13 @@ def run_gpu(args):
     host_scores = torch.empty(n * world, dtype=torch.float32).pin_memory()
 
     def e2e_step():
-        ids = ids_host.to(dev, non_blocking=True)
-        lay = model.make_layout(batch)
-        x = model.encode_packed(ids, lay, check_finite=False)
-        sc = gather(model.scores_from_hidden(x, lay))
+        if graphed is not None:  # GraphedScorer.__call__: H2D of the pinned ids + replay
+            sc = gather(graphed(ids_host))
+        else:
+            ids = ids_host.to(dev, non_blocking=True)
+            lay = model.make_layout(batch)
+            x = model.encode_packed(ids, lay, check_finite=False)
+            sc = gather(model.scores_from_hidden(x, lay))
         host_scores.copy_(sc, non_blocking=True)
         return sc
 
@@ -280,6 +301,25 @@ def run_gpu(args):
 
     # ---- roofline of the attention kernel (sc_attn_fwd, band + head-row pass) ----
     attn_bytes = 4 * layout.total_tokens * cfg["embed_dim"] * 2  # Q,K,V read + O write, bf16
+    attn_where = "in-step CUDA events around every sc_attn_fwd launch of the timed region"
+    if not attn_ms:
+        # graph replay: time the same attention launch standalone on this step's layout
+        h, H = cfg["embed_dim"], cfg["heads"]
+        qkv = torch.randn((layout.total_tokens, 3 * h), device=dev).to(torch.bfloat16)
+        out = torch.empty((layout.total_tokens, h), device=dev, dtype=torch.bfloat16)
+        pat = P.make_pattern(cfg["pattern"], cfg["window"])
+        run = lambda: P.attend_packed(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], layout, pat, H, out=out, check=False)
+        for _ in range(3):
+            run()
+        for _ in range(20):
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            run()
+            a1.record(stream)
+            attn_events += [a0, a1]
+        torch.cuda.synchronize()
+        attn_ms = [attn_events[i].elapsed_time(attn_events[i + 1]) for i in range(0, len(attn_events), 2)]
+        attn_where = "standalone CUDA-event timing of sc_attn_fwd on this step's layout (step runs as a CUDA graph)"
     attn_avg_ms = statistics.mean(attn_ms)
     achieved = attn_bytes / (attn_avg_ms / 1e3) / 1e9
     gemm_flops_step = 2 * layout.total_tokens * cfg["layers"] * (4 * cfg["embed_dim"] ** 2 + 2 * cfg["embed_dim"] * cfg["ff_dim"])
@@ -308,8 +348,7 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic: reference-generator token ids (default_rng((seed,q,i))), random-init ELECTRA-base weights",
-            "config": {"workload": "ELECTRA-base sparse cross-encoder, documents 4096 tok (q10+d4086, s=4099), w=4 "
-                                   "asymmetric, packed varlen batch (BASELINE configs[2])",
+            "config": {"workload": workload_name(doc_len, s), "cuda_graph": use_graph,
                        "pairs_per_gpu": n, "global_batch": n * world, "seq_len": s, "doc_len": doc_len,
                        "query_len": QUERY_LEN, "varlen": bool(args.varlen), "pattern": "sparse", "window": 4,
                        "layers": 12, "hidden": 768, "heads": 12, "ff": 3072, "parallelism": f"dp{world}",
@@ -319,7 +358,8 @@ def run_gpu(args):
                          "peak_kind": peak_kind, "traffic": traffic,
                          "algorithmic_bytes_per_launch": attn_bytes, "avg_launch_ms": attn_avg_ms,
                          "launches": len(attn_ms), "frac_of_8TBs": achieved / 8000.0,
-                         "share_of_step": sum(attn_ms) / ms},
+                         "share_of_step": (sum(attn_ms) / ms) if not use_graph else None,
+                         "timing": attn_where},
             "step_roofline": {"bound": "tensor", "achieved": gemm_flops_step / (ms_max / args.steps / 1e3) / 1e12,
                               "peak": tf_sus, "unit": "TFLOP/s", "note": "GEMM FLOPs per step / step time vs sustained bf16"},
             "cpu_baseline": cpu,
@@ -345,6 +385,8 @@ def main():
     ap.add_argument("--pairs-per-gpu", type=int, default=64)
     ap.add_argument("--doc-len", type=int, default=4086)
     ap.add_argument("--varlen", action="store_true", help="doc lengths ~U{54..doc_len} instead of fixed")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the forward as a CUDA graph (auto: passages)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU oracle timing")
     args = ap.parse_args()

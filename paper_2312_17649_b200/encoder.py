@@ -451,6 +451,46 @@ class CrossEncoder:
         return res
 
 
+class GraphedScorer:
+    """CUDA-graph replay of the whole forward (embed, 12 layers, scores) for one packed-batch shape.
+
+    Passage-size batches (s = 177) are launch-bound: ~110 launches per forward.
+    The K1 index and the attention workspace are built once outside the graph;
+    each call copies the new ids into the static input buffer and replays.
+    """
+
+    def __init__(self, model: "CrossEncoder", batch: PackedBatch, warmup: int = 2):
+        model._check_batch(batch)
+        self.model = model
+        self.seq_lens = batch.seq_lens.copy()
+        self.qgroup_lens = batch.qgroup_lens.copy()
+        self.layout = model.make_layout(batch)
+        self.ids = torch.from_numpy(batch.ids).to(model.device)
+        side = torch.cuda.Stream(device=model.device)
+        side.wait_stream(torch.cuda.current_stream(model.device))
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self._forward()
+        torch.cuda.current_stream(model.device).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.scores = self._forward()
+
+    def _forward(self):
+        x = self.model.encode_packed(self.ids, self.layout, check_finite=False)
+        return self.model.scores_from_hidden(x, self.layout)
+
+    def matches(self, batch: PackedBatch) -> bool:
+        return np.array_equal(batch.seq_lens, self.seq_lens) and np.array_equal(batch.qgroup_lens, self.qgroup_lens)
+
+    def __call__(self, ids) -> torch.Tensor:
+        """Scores (nseq,) on the device for new ids of the captured shape (numpy or tensor, int32)."""
+        src = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)) if isinstance(ids, np.ndarray) else ids
+        self.ids.copy_(src, non_blocking=True)
+        self.graph.replay()
+        return self.scores
+
+
 def encoder_forward(seq: TokenSequence, config: EncoderConfig, weights: dict) -> np.ndarray:
     """Final-layer (seq, embed) matrix for a single sequence (R/encoder.py:541-544)."""
     return CrossEncoder(config, weights).forward(seq.ids, seq.partition)[0]

@@ -130,3 +130,19 @@ def test_rejects_out_of_vocabulary(P):
     seq = P.assemble_input([3, 4], [40])
     with pytest.raises(P.EncoderError):
         model.forward(seq.ids, seq.partition)
+
+
+def test_graphed_scorer_matches_eager(P):
+    from paper_2312_17649_b200.encoder import GraphedScorer
+
+    cfg = P.EncoderConfig(**cases.ELECTRA_PASSAGE, precision="bf16")
+    model = P.CrossEncoder(cfg, seed=0)
+    seqs = [rerank_ids(0, j, 164, cfg.vocab_size, cfg.max_positions, P) for j in range(16)]
+    batch = P.PackedBatch.from_sequences(seqs)
+    eager = model.score_packed(batch).cpu().numpy()
+    g = GraphedScorer(model, batch)
+    np.testing.assert_array_equal(g(batch.ids).cpu().numpy(), eager)
+    seqs2 = [rerank_ids(1, j, 164, cfg.vocab_size, cfg.max_positions, P) for j in range(16)]
+    b2 = P.PackedBatch.from_sequences(seqs2)
+    assert g.matches(b2)
+    np.testing.assert_array_equal(g(b2.ids).cpu().numpy(), model.score_packed(b2).cpu().numpy())
