@@ -261,6 +261,8 @@ def run_gpu(args):
         e1.record(stream)
         barrier()
     launches = _lib.kernel_launches() - launches0
+    if graphed is not None:  # replayed kernels: captured count x replays
+        launches += graphed.kernels_per_replay * args.steps
     ms = e0.elapsed_time(e1)
     attn_ms = [attn_events[i].elapsed_time(attn_events[i + 1]) for i in range(0, len(attn_events), 2)]
     t = torch.tensor([ms], device=dev)

@@ -473,8 +473,11 @@ class GraphedScorer:
                 self._forward()
         torch.cuda.current_stream(model.device).wait_stream(side)
         self.graph = torch.cuda.CUDAGraph()
+        n0 = _lib.kernel_launches()
         with torch.cuda.graph(self.graph):
             self.scores = self._forward()
+        # library kernels captured per replay (replays bypass the library's launch counter)
+        self.kernels_per_replay = _lib.kernel_launches() - n0
 
     def _forward(self):
         x = self.model.encode_packed(self.ids, self.layout, check_finite=False)
