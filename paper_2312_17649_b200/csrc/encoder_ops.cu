@@ -211,21 +211,56 @@ __device__ __forceinline__ float gelu_bf16path(float x) {
   return fmaf(half_x, copysignf(erf_abs, z), half_x);
 }
 
+// Same formula on pairs with Blackwell's packed FP32 pipe (FFMA2/FMUL2): halves
+// the FP instruction count of the issue-bound bf16 GELU pass.
+__device__ __forceinline__ float2 gelu2_bf16path(float2 x) {
+  const float2 z = __fmul2_rn(x, make_float2(0.70710678118654752440f, 0.70710678118654752440f));
+  const float2 a = make_float2(fabsf(z.x), fabsf(z.y));
+  const float2 d = __ffma2_rn(a, make_float2(0.3275911f, 0.3275911f), make_float2(1.f, 1.f));
+  const float2 t = make_float2(rcp_approx(d.x), rcp_approx(d.y));
+  float2 p = __ffma2_rn(make_float2(1.061405429f, 1.061405429f), t, make_float2(-1.453152027f, -1.453152027f));
+  p = __ffma2_rn(p, t, make_float2(1.421413741f, 1.421413741f));
+  p = __ffma2_rn(p, t, make_float2(-0.284496736f, -0.284496736f));
+  p = __ffma2_rn(p, t, make_float2(0.254829592f, 0.254829592f));
+  p = __fmul2_rn(p, t);
+  const float2 g = __fmul2_rn(__fmul2_rn(a, a), make_float2(-1.4426950408889634f, -1.4426950408889634f));
+  const float2 ne = make_float2(-ex2_approx(g.x), -ex2_approx(g.y));
+  const float2 erf_abs = __ffma2_rn(p, ne, make_float2(1.f, 1.f));
+  const float2 h = __fmul2_rn(x, make_float2(0.5f, 0.5f));
+  return __ffma2_rn(h, make_float2(copysignf(erf_abs.x, x.x), copysignf(erf_abs.y, x.y)), h);
+}
+
 // bf16, 8 elements per thread, cols % 8 == 0.
-__global__ void bias_gelu_bf16x8_kernel(__nv_bfloat16* __restrict__ x, const float* __restrict__ bias,
-                                        int64_t n8, int cols) {
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  uint4* xv = reinterpret_cast<uint4*>(x);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride) {
-    uint4 u = xv[i];
-    __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&u);
-    int c0 = (int)((i * 8) % cols);
+template <bool kBias>
+__device__ __forceinline__ void gelu_bf16x8(uint4& u, const float* __restrict__ bias, int64_t i, int cols) {
+  __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&u);
+  const int c0 = kBias ? (int)((i * 8) % cols) : 0;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      float2 f = __bfloat1622float2(b[e]);
-      if (bias) { f.x += __ldg(bias + c0 + 2 * e); f.y += __ldg(bias + c0 + 2 * e + 1); }
-      b[e] = __floats2bfloat162_rn(gelu_bf16path(f.x), gelu_bf16path(f.y));
-    }
+  for (int e = 0; e < 4; ++e) {
+    float2 f = __bfloat1622float2(b[e]);
+    if constexpr (kBias) { f.x += __ldg(bias + c0 + 2 * e); f.y += __ldg(bias + c0 + 2 * e + 1); }
+    b[e] = __float22bfloat162_rn(gelu2_bf16path(f));
+  }
+}
+
+// Two 16-byte vectors per thread per iteration (more loads in flight).
+template <bool kBias>
+__global__ void __launch_bounds__(256) bias_gelu_bf16x8_kernel(__nv_bfloat16* __restrict__ x,
+                                                              const float* __restrict__ bias, int64_t n8,
+                                                              int cols) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  uint4* xv = reinterpret_cast<uint4*>(x);
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + stride < n8; i += 2 * stride) {
+    uint4 u0 = xv[i], u1 = xv[i + stride];
+    gelu_bf16x8<kBias>(u0, bias, i, cols);
+    gelu_bf16x8<kBias>(u1, bias, i + stride, cols);
+    xv[i] = u0;
+    xv[i + stride] = u1;
+  }
+  if (i < n8) {
+    uint4 u = xv[i];
+    gelu_bf16x8<kBias>(u, bias, i, cols);
     xv[i] = u;
   }
 }
@@ -316,7 +351,10 @@ extern "C" int sc_bias_gelu(void* x, const float* bias, int32_t dtype, int64_t r
   if (dtype == SC_DTYPE_BF16 && cols % 8 == 0 && ((uintptr_t)x & 15) == 0) {
     int64_t n8 = n / 8;
     unsigned blocks = grid_cap(n8, 16);
-    bias_gelu_bf16x8_kernel<<<blocks, 256, 0, st>>>((__nv_bfloat16*)x, bias, n8, cols);
+    if (bias)
+      bias_gelu_bf16x8_kernel<true><<<blocks, 256, 0, st>>>((__nv_bfloat16*)x, bias, n8, cols);
+    else
+      bias_gelu_bf16x8_kernel<false><<<blocks, 256, 0, st>>>((__nv_bfloat16*)x, bias, n8, cols);
   } else if (dtype == SC_DTYPE_BF16) {
     unsigned blocks = grid_cap(n, 16);
     bias_gelu_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((__nv_bfloat16*)x, bias, n, cols);
