@@ -22,10 +22,17 @@
 namespace sc {
 namespace tck {
 
-constexpr int BM = 128, D = 64, BN = 128, GR = 32, NS = 2;
+#ifndef SC_TC_BN
+#define SC_TC_BN 64
+#endif
+// BN-key blocks; TMEM per CTA = S/P (BN columns) + O (64 columns), so BN = 64
+// fits three CTAs per SM (3 x 128 of 512 columns) to overlap their serialized
+// QK -> softmax -> PV chains.
+constexpr int BM = 128, D = 64, BN = SC_TC_BN, GR = 32, NS = 2;
 constexpr int NTHREADS = 192;
-constexpr int TMEM_COLS = 256;  // S/P: [0,128), O: [128,192)
-constexpr int S_COL = 0, O_COL = 128;
+constexpr int TMEM_COLS = BN + D <= 128 ? 128 : 256;
+constexpr int S_COL = 0, O_COL = BN;
+constexpr int CTAS_PER_SM = BN <= 64 ? 3 : 2;
 constexpr int ROWB = 128;
 
 struct Params {
@@ -182,7 +189,7 @@ struct Smem {
   static constexpr int TOTAL = BAR + 16 * 8 + 16;
 };
 
-__global__ void __launch_bounds__(NTHREADS, 2) tc_attn_kernel(
+__global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) tc_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKg,
     const __grid_constant__ CUtensorMap tmVg, const __grid_constant__ CUtensorMap tmK,
     const __grid_constant__ CUtensorMap tmV, Params p) {
