@@ -25,14 +25,20 @@ namespace tck {
 #ifndef SC_TC_BN
 #define SC_TC_BN 64
 #endif
-// BN-key blocks; TMEM per CTA = S/P (BN columns) + O (64 columns), so BN = 64
-// fits three CTAs per SM (3 x 128 of 512 columns) to overlap their serialized
-// QK -> softmax -> PV chains.
-constexpr int BM = 128, D = 64, BN = SC_TC_BN, GR = 32, NS = 2;
+// BN-key blocks (64: two CTAs per SM, each with a double-buffered S).
+constexpr int BM = 128, D = 64, BN = SC_TC_BN, GR = 32;
 constexpr int NTHREADS = 192;
-constexpr int TMEM_COLS = BN + D <= 128 ? 128 : 256;
-constexpr int S_COL = 0, O_COL = BN;
-constexpr int CTAS_PER_SM = BN <= 64 ? 3 : 2;
+constexpr int S_COL = 0;
+// NBUF S/P buffers in TMEM.  NBUF = 2 lets QK(b+2) overlap softmax(b+1) (wins
+// for long key ranges); NBUF = 1 keeps TMEM at 128 columns and registers low
+// enough for 3 CTAs per SM (wins for mid windows with few blocks per CTA).
+template <int NBUF>
+struct Cfg {
+  static constexpr int NS = NBUF == 2 ? 4 : 2;  // K/V ring stages
+  static constexpr int TMEM_COLS = NBUF * BN + D <= 128 ? 128 : (NBUF * BN + D <= 256 ? 256 : 512);
+  static constexpr int O_COL = NBUF * BN;
+  static constexpr int CTAS = NBUF == 2 ? 2 : 3;
+};
 constexpr int ROWB = 128;
 
 struct Params {
@@ -107,6 +113,14 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint3
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
       : "r"(addr))
 
+#define TC_LD16(addr, r)                                                                          \
+  asm volatile(                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),       \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),   \
+        "=r"(r[14]), "=r"(r[15])                                                                  \
+      : "r"(addr))
+
 #define TC_ST16(addr, r)                                                                          \
   asm volatile(                                                                                   \
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
@@ -177,6 +191,7 @@ __device__ __forceinline__ void row_softmax(uint32_t (&v)[NC], float c2, float& 
   for (int c = 0; c < NC / 2; c += 16) TC_ST16(p_addr + c, (&v[c]));
 }
 
+template <int NS>
 struct Smem {
   // offsets (bytes) from the 1024-aligned base
   static constexpr int Q = 0;
@@ -185,14 +200,18 @@ struct Smem {
   static constexpr int KV = VG + GR * ROWB;  // NS x (K block, V block)
   static constexpr int STAGE = 2 * BN * ROWB;
   static constexpr int BAR = KV + NS * STAGE;
-  // barriers: qbar, full[NS], empty[NS], s_full, p_full, pv_done, o_final; tmem holder
+  // barriers: qbar, full[NS], empty[NS], s_full[2], p_full[2], pv_done[2], o_final; tmem holder
   static constexpr int TOTAL = BAR + 16 * 8 + 16;
 };
 
-__global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) tc_attn_kernel(
+template <int NBUF>
+__global__ void __launch_bounds__(NTHREADS, Cfg<NBUF>::CTAS) tc_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKg,
     const __grid_constant__ CUtensorMap tmVg, const __grid_constant__ CUtensorMap tmK,
     const __grid_constant__ CUtensorMap tmV, Params p) {
+  using C = Cfg<NBUF>;
+  using SM = Smem<C::NS>;
+  constexpr int NS = C::NS, O_COL = C::O_COL, TMEM_COLS = C::TMEM_COLS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tile = blockIdx.x, h = blockIdx.y;
@@ -209,13 +228,15 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) tc_attn_kernel(
   const int lo = w < 0 ? 0 : max(0, r0 - w);
   const int hi = w < 0 ? n_doc : min(n_doc, r0 + rows_here + w);
   const int nkb = (hi - lo + BN - 1) / BN;
+  const int nblocks = (has_glob ? 1 : 0) + nkb;  // block b: global block first, then doc key blocks
 
   const uint32_t sm0 = smem_u32(smem);
-  const uint32_t bar0 = sm0 + Smem::BAR;
+  const uint32_t bar0 = sm0 + SM::BAR;
+  // barriers: qbar | full[NS] | empty[NS] | s_full[2] | p_full[2] | pv_done[2] | o_final
   const uint32_t qbar = bar0, full_bar = bar0 + 8, empty_bar = bar0 + 8 * (1 + NS);
-  const uint32_t s_full = bar0 + 8 * (1 + 2 * NS), p_full = s_full + 8, pv_done = s_full + 16,
-                 o_final = s_full + 24;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Smem::BAR + 16 * 8);
+  const uint32_t s_full = bar0 + 8 * (1 + 2 * NS), p_full = s_full + 16, pv_done = s_full + 32,
+                 o_final = s_full + 48;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + SM::BAR + 16 * 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -224,9 +245,11 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) tc_attn_kernel(
       mbar_init(full_bar + 8 * s, 1);
       mbar_init(empty_bar + 8 * s, 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
-    mbar_init(pv_done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(s_full + 8 * b, 1);
+      mbar_init(p_full + 8 * b, 4);
+      mbar_init(pv_done + 8 * b, 1);
+    }
     mbar_init(o_final, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -247,62 +270,68 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) tc_attn_kernel(
     if (lane == 0) {
       const int col = h * D;
       mbar_expect_tx(qbar, (BM + 2 * GR) * ROWB);
-      tma_load_2d(sm0 + Smem::Q, &tmQ, col, doc0 + r0, qbar);
-      tma_load_2d(sm0 + Smem::KG, &tmKg, col, g.start, qbar);
-      tma_load_2d(sm0 + Smem::VG, &tmVg, col, g.start, qbar);
+      tma_load_2d(sm0 + SM::Q, &tmQ, col, doc0 + r0, qbar);
+      tma_load_2d(sm0 + SM::KG, &tmKg, col, g.start, qbar);
+      tma_load_2d(sm0 + SM::VG, &tmVg, col, g.start, qbar);
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % NS;
         if (kb >= NS) mbar_wait(empty_bar + 8 * s, ((kb / NS) & 1) ^ 1);
-        mbar_expect_tx(full_bar + 8 * s, Smem::STAGE);
-        const uint32_t kbuf = sm0 + Smem::KV + s * Smem::STAGE;
+        mbar_expect_tx(full_bar + 8 * s, SM::STAGE);
+        const uint32_t kbuf = sm0 + SM::KV + s * SM::STAGE;
         tma_load_2d(kbuf, &tmK, col, doc0 + lo + kb * BN, full_bar + 8 * s);
         tma_load_2d(kbuf + BN * ROWB, &tmV, col, doc0 + lo + kb * BN, full_bar + 8 * s);
       }
     }
   } else if (warp == 5) {
-    // ------------------------------------------------------------- MMA
+    // ------------------------------------------------------------- MMA (one thread)
+    // S is double-buffered in TMEM: QK(b+2) is issued as soon as PV(b) has read
+    // P(b) out of the same buffer, so the tensor core runs ahead of softmax.
     if (lane == 0) {
       const uint32_t id_qk = idesc_bf16(BM, BN, 0), id_qg = idesc_bf16(BM, GR, 0),
                      id_pv = idesc_bf16(BM, D, 1);
-      const uint32_t tS = tmem + S_COL, tO = tmem + O_COL;
+      const uint32_t tO = tmem + O_COL;
       mbar_wait(qbar, 0);
       tc_fence_after();
-      const uint64_t qd = sw128_desc(sm0 + Smem::Q);
-      int blk = 0;  // S/P uses so far (phase bookkeeping)
-      uint32_t acc_o = 0;
-      if (has_glob) {
-        const uint64_t kd = sw128_desc(sm0 + Smem::KG);
+      const uint64_t qd = sw128_desc(sm0 + SM::Q);
+      auto issue_qk = [&](int b) {
+        const uint32_t tS = tmem + S_COL + (b % NBUF) * BN;
+        if (has_glob && b == 0) {
+          const uint64_t kd = sw128_desc(sm0 + SM::KG);
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) mma_ss(tS, qd + 2 * ks, kd + 2 * ks, id_qg, ks > 0);
-        tc_commit(s_full);
-        mbar_wait(p_full, blk & 1);
+          for (int ks = 0; ks < D / 16; ++ks) mma_ss(tS, qd + 2 * ks, kd + 2 * ks, id_qg, ks > 0);
+        } else {
+          const int kb = b - (has_glob ? 1 : 0), s = kb % NS;
+          mbar_wait(full_bar + 8 * s, (kb / NS) & 1);
+          tc_fence_after();
+          const uint64_t kd = sw128_desc(sm0 + SM::KV + s * SM::STAGE);
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) mma_ss(tS, qd + 2 * ks, kd + 2 * ks, id_qk, ks > 0);
+        }
+        tc_commit(s_full + 8 * (b % NBUF));
+      };
+      issue_qk(0);
+      if (NBUF == 2 && nblocks > 1) issue_qk(1);
+      for (int b = 0; b < nblocks; ++b) {
+        const int buf = b % NBUF;
+        mbar_wait(p_full + 8 * buf, (b / NBUF) & 1);
         tc_fence_after();
-        const uint64_t vd = sw128_desc(sm0 + Smem::VG);
+        const uint32_t tS = tmem + S_COL + buf * BN;
+        if (has_glob && b == 0) {
+          const uint64_t vd = sw128_desc(sm0 + SM::VG);
 #pragma unroll
-        for (int ks = 0; ks < GR / 16; ++ks) mma_ts(tO, tS + 8 * ks, vd + 128 * ks, id_pv, acc_o | ks);
-        acc_o = 1;
-        tc_commit(pv_done);
-        mbar_wait(pv_done, blk & 1);
-        ++blk;
-      }
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % NS;
-        mbar_wait(full_bar + 8 * s, (kb / NS) & 1);
-        tc_fence_after();
-        const uint32_t kbuf = sm0 + Smem::KV + s * Smem::STAGE;
-        const uint64_t kd = sw128_desc(kbuf), vd = sw128_desc(kbuf + BN * ROWB);
+          for (int ks = 0; ks < GR / 16; ++ks) mma_ts(tO, tS + 8 * ks, vd + 128 * ks, id_pv, ks > 0);
+        } else {
+          const int kb = b - (has_glob ? 1 : 0), s = kb % NS;
+          const uint64_t vd = sw128_desc(sm0 + SM::KV + s * SM::STAGE + BN * ROWB);
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) mma_ss(tS, qd + 2 * ks, kd + 2 * ks, id_qk, ks > 0);
-        tc_commit(s_full);
-        mbar_wait(p_full, blk & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < BN / 16; ++ks) mma_ts(tO, tS + 8 * ks, vd + 128 * ks, id_pv, acc_o | ks);
-        acc_o = 1;
-        tc_commit(empty_bar + 8 * s);
-        tc_commit(pv_done);
-        mbar_wait(pv_done, blk & 1);
-        ++blk;
+          for (int ks = 0; ks < BN / 16; ++ks) mma_ts(tO, tS + 8 * ks, vd + 128 * ks, id_pv, (b > 0 || ks > 0));
+          tc_commit(empty_bar + 8 * s);
+        }
+        tc_commit(pv_done + 8 * buf);
+        if (b + NBUF < nblocks) {
+          mbar_wait(pv_done + 8 * buf, (b / NBUF) & 1);  // P(b) consumed: S buffer free
+          issue_qk(b + NBUF);
+        }
       }
       tc_commit(o_final);
     }
@@ -312,31 +341,29 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) tc_attn_kernel(
     const int rr = r0 + r;           // doc-relative row
     const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
     const float c2 = p.c2;
+    // Lazy rescaling (FA4): the running max moves only when a block exceeds it
+    // by more than 2^8 in the exp2 domain, so O is rarely touched.
+    const float tau = 8.f / c2;
     float m = -INFINITY, l = 0.f;
     if (p.padding == SC_PAD_ZERO_LOGIT && w >= 0) {
       const int ninv = 2 * w + 1 - max(0, min(n_doc, rr + w + 1) - max(0, rr - w));
       if (ninv > 0) { m = 0.f; l = (float)ninv; }
     }
-    int blk = 0;
-    const int nblocks = (has_glob ? 1 : 0) + nkb;
     for (int b = 0; b < nblocks; ++b) {
+      const int buf = b % NBUF;
       const bool glob = has_glob && b == 0;
-      mbar_wait(s_full, blk & 1);
+      const uint32_t sa = lane_addr + S_COL + buf * BN;
+      mbar_wait(s_full + 8 * buf, (b / NBUF) & 1);
       tc_fence_after();
-      float alpha, sum;
+      uint32_t v[BN];
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 32) TC_LD32(sa + c0, (&v[c0]));
+      tc_wait_ld();
       if (glob) {
-        uint32_t v[GR];
-        TC_LD32(lane_addr + S_COL, v);
-        tc_wait_ld();
 #pragma unroll
-        for (int e = 0; e < GR; ++e)
-          if (!(e < G && (e == 0 ? p.link_cls : p.link_query))) v[e] = __float_as_uint(-INFINITY);
-        row_softmax<GR>(v, c2, m, alpha, sum, lane_addr + S_COL);
+        for (int e = 0; e < BN; ++e)
+          if (!(e < GR && e < G && (e == 0 ? p.link_cls : p.link_query))) v[e] = __float_as_uint(-INFINITY);
       } else {
-        uint32_t v[BN];
-#pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 32) TC_LD32(lane_addr + S_COL + c0, (&v[c0]));
-        tc_wait_ld();
         const int k0 = lo + (b - (has_glob ? 1 : 0)) * BN;
         const bool interior =
             k0 + BN <= hi && (w < 0 || (k0 >= r0 + rows_here - 1 - w && k0 + BN - 1 <= r0 + w));
@@ -347,26 +374,47 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) tc_attn_kernel(
             if (!(t < hi && (w < 0 || (t - rr <= w && rr - t <= w)))) v[e] = __float_as_uint(-INFINITY);
           }
         }
-        row_softmax<BN>(v, c2, m, alpha, sum, lane_addr + S_COL);
       }
-      // rescale O (already accumulated blocks) when this row's max grew
-      if (__any_sync(0xffffffffu, blk > 0 && alpha != 1.f)) {
+      float mx = -INFINITY;
 #pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 32) {
-          uint32_t o[32];
-          TC_LD32(lane_addr + O_COL + c0, o);
-          tc_wait_ld();
+      for (int e = 0; e < BN; ++e) mx = fmaxf(mx, __uint_as_float(v[e]));
+      const bool grow = mx > m + tau || (m == -INFINITY && mx != -INFINITY);
+      float alpha = 1.f;
+      if (__any_sync(0xffffffffu, grow)) {
+        const float mnew = grow ? fmaxf(m, mx) : m;
+        alpha = (grow && m != -INFINITY) ? ex2((m - mnew) * c2) : (grow ? 0.f : 1.f);
+        m = mnew;
+        if (b > 0) {  // O holds blocks < b: wait until PV(b-1) has landed, then rescale in TMEM
+          mbar_wait(pv_done + 8 * ((b - 1) % NBUF), ((b - 1) / NBUF) & 1);
+          tc_fence_after();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-          TC_ST32(lane_addr + O_COL + c0, o);
+          for (int c0 = 0; c0 < D; c0 += 16) {  // 16-column chunks: S row stays in registers
+            uint32_t o[16];
+            TC_LD16(lane_addr + O_COL + c0, o);
+            tc_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            TC_ST16(lane_addr + O_COL + c0, o);
+          }
         }
       }
-      l = fmaf(l, alpha, sum);
+      const float base = m == -INFINITY ? 0.f : m * c2;
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int e = 0; e < BN; e += 2) {
+        const float p0 = ex2(fmaf(__uint_as_float(v[e]), c2, -base));
+        const float p1 = ex2(fmaf(__uint_as_float(v[e + 1]), c2, -base));
+        s0 += p0;
+        s1 += p1;
+        v[e / 2] = pack_bf16(p0, p1);
+      }
+#pragma unroll
+      for (int c = 0; c < BN / 2; c += 16) TC_ST16(sa + c, (&v[c]));
+      l = fmaf(l, alpha, s0 + s1);
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
-      ++blk;
+      if (lane == 0) mbar_arrive(p_full + 8 * buf);
     }
     // epilogue: O / l -> bf16 row
     mbar_wait(o_final, 0);
@@ -375,18 +423,18 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM) tc_attn_kernel(
     __nv_bfloat16* dst = p.out + (int64_t)(doc0 + rr) * p.ld_out + h * D;
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 32) {
-      uint32_t v[32];
-      TC_LD32(lane_addr + O_COL + c0, v);
+      uint32_t o[32];
+      TC_LD32(lane_addr + O_COL + c0, o);
       tc_wait_ld();
       if (r < rows_here) {
         uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint4 u;
-          u.x = pack_bf16(__uint_as_float(v[8 * q + 0]) * inv, __uint_as_float(v[8 * q + 1]) * inv);
-          u.y = pack_bf16(__uint_as_float(v[8 * q + 2]) * inv, __uint_as_float(v[8 * q + 3]) * inv);
-          u.z = pack_bf16(__uint_as_float(v[8 * q + 4]) * inv, __uint_as_float(v[8 * q + 5]) * inv);
-          u.w = pack_bf16(__uint_as_float(v[8 * q + 6]) * inv, __uint_as_float(v[8 * q + 7]) * inv);
+          u.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+          u.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+          u.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+          u.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
           d4[q] = u;
         }
       }
@@ -447,6 +495,26 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t row
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int NBUF>
+static int launch_kernel(dim3 grid, const CUtensorMap& mQ, const CUtensorMap& mKg, const CUtensorMap& mVg,
+                         const CUtensorMap& mK, const CUtensorMap& mV, const Params& p, cudaStream_t st) {
+  const size_t smem = Smem<Cfg<NBUF>::NS>::TOTAL + 1024;
+  static bool attr = false;
+  if (!attr) {
+    // several CTAs per SM: ask for the full shared-memory carveout
+    cudaFuncSetAttribute(tc_attn_kernel<NBUF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (cudaFuncSetAttribute(tc_attn_kernel<NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess) {
+      set_error("tcgen05 kernel: shared memory request of %zu bytes failed", smem);
+      return SC_ERR_UNSUPPORTED;
+    }
+    attr = true;
+  }
+  tc_attn_kernel<NBUF><<<grid, NTHREADS, smem, st>>>(mQ, mKg, mVg, mK, mV, p);
+  SC_CHECK_LAUNCH("tc_attn_kernel");
+  return SC_OK;
+}
+
 }  // namespace tck
 
 size_t tc_workspace_bytes(int nseq) { return (size_t)(nseq + 1) * sizeof(int32_t); }
@@ -495,18 +563,13 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   p.c2 = 1.4426950408889634f / a.scale;
   p.cu = a.cu; p.qlen = a.qlen; p.tile_base = tbase;
   p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
-  const size_t smem = Smem::TOTAL + 1024;
-  static bool attr = false;
-  if (!attr) {
-    // two CTAs per SM (2 x 256 TMEM columns): ask for the full shared-memory carveout
-    cudaFuncSetAttribute(tc_attn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (cudaFuncSetAttribute(tc_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return unsupported("shared memory request");
-    attr = true;
-  }
   dim3 grid((unsigned)((a.T + BM - 1) / BM + a.nseq), (unsigned)a.H);
-  tc_attn_kernel<<<grid, NTHREADS, smem, st>>>(mQ, mKg, mVg, mK, mV, p);
-  SC_CHECK_LAUNCH("tc_attn_kernel");
+  // Double-buffer S when a row tile sweeps many key blocks (measured crossover:
+  // single buffer + 3 CTAs/SM is faster up to w = 256, double buffer for w = inf).
+  const bool long_range = w == SC_LINK_FULL || w > 256;
+  const int rc = long_range ? launch_kernel<2>(grid, mQ, mKg, mVg, mK, mV, p, st)
+                            : launch_kernel<1>(grid, mQ, mKg, mVg, mK, mV, p, st);
+  if (rc) return rc;
   // Head rows (cls + query group): the band kernel in head-rows-only mode
   // streams each doc key once for the CLS split-softmax records, then merges.
   return launch_attn_band(a, dtype, seq_tile_base, seq_head_base, tile_rows, max_qgroup_len, ws,
