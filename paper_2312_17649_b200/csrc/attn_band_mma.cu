@@ -77,7 +77,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok = 0;
   while (!ok) {
     asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000; selp.u32 %0, 1, 0, p; }"
         : "=r"(ok)
         : "r"(bar), "r"(parity)
         : "memory");
@@ -226,15 +226,10 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
-  const int tile = blockIdx.x;
-  if (tile >= __ldg(p.tile_base + p.nseq)) return;
-  const int j = find_seq(p.tile_base, p.nseq, tile);
-  const SeqGroups g = seq_groups(p.cu, p.qlen, j);
-  const int n_doc = g.len[2];
-  const int r0 = (tile - __ldg(p.tile_base + j)) * BM;
-  const int rows_here = min(BM, n_doc - r0);
-  const int doc_row0 = g.start + g.off[2] + r0;
-  const int G = 1 + g.len[1];
+  // Persistent: CTA b processes tiles b, b + gridDim.x, ...; the TMA ring runs
+  // continuously across tile boundaries (global head iteration counter `it`).
+  const int ntiles = __ldg(p.tile_base + p.nseq);
+  if ((int)blockIdx.x >= ntiles) return;
   const int w = p.w;
   constexpr int kb_rows = 48 + 32 * NBC;
   constexpr int q_bytes = BM * ROWB, f_bytes = GR * ROWB, kb_bytes = kb_rows * ROWB;
@@ -276,24 +271,30 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
       prefetch_map(&tmQ); prefetch_map(&tmKb); prefetch_map(&tmVb);
       prefetch_map(&tmKg); prefetch_map(&tmVg); prefetch_map(&tmQf);
       const uint32_t bytes = (uint32_t)((p.doc_rows ? q_bytes : 0) + 3 * f_bytes + 2 * kb_box * ROWB);
-      for (int h = 0; h < p.H; ++h) {
-        const int s = h % NS;
-        if (h >= NS) mbar_wait(empty_bar + 8 * s, ((h / NS) & 1) ^ 1);
-        const uint32_t fb = full_bar + 8 * s;
-        if (h + NS < p.H) {  // L2 prefetch of the boxes this stage will hold next round
-          const int pc = (h + NS) * D;
-          if (p.doc_rows) tma_prefetch_2d(&tmQ, pc, doc_row0);
-          tma_prefetch_2d(&tmKb, pc, doc_row0 - w);
-          tma_prefetch_2d(&tmVb, pc, doc_row0 - w);
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int j = find_seq(p.tile_base, p.nseq, tile);
+        const SeqGroups g = seq_groups(p.cu, p.qlen, j);
+        const int doc_row0 = g.start + g.off[2] + (tile - __ldg(p.tile_base + j)) * BM;
+        for (int h = 0; h < p.H; ++h, ++it) {
+          const int s = it % NS;
+          if (it >= NS) mbar_wait(empty_bar + 8 * s, ((it / NS) & 1) ^ 1);
+          const uint32_t fb = full_bar + 8 * s;
+          if (h + NS < p.H) {  // L2 prefetch of the boxes this stage will hold next round
+            const int pc = (h + NS) * D;
+            if (p.doc_rows) tma_prefetch_2d(&tmQ, pc, doc_row0);
+            tma_prefetch_2d(&tmKb, pc, doc_row0 - w);
+            tma_prefetch_2d(&tmVb, pc, doc_row0 - w);
+          }
+          mbar_expect_tx(fb, bytes);
+          const int col = h * D;
+          if (p.doc_rows) tma_load_2d(q_buf(s), &tmQ, col, doc_row0, fb);
+          tma_load_2d(kb_buf(s), &tmKb, col, doc_row0 - w, fb);
+          tma_load_2d(vb_buf(s), &tmVb, col, doc_row0 - w, fb);
+          tma_load_2d(kg_buf(s), &tmKg, col, g.start, fb);
+          tma_load_2d(vg_buf(s), &tmVg, col, g.start, fb);
+          tma_load_2d(qf_buf(s), &tmQf, col, g.start, fb);
         }
-        mbar_expect_tx(fb, bytes);
-        const int col = h * D;
-        if (p.doc_rows) tma_load_2d(q_buf(s), &tmQ, col, doc_row0, fb);
-        tma_load_2d(kb_buf(s), &tmKb, col, doc_row0 - w, fb);
-        tma_load_2d(vb_buf(s), &tmVb, col, doc_row0 - w, fb);
-        tma_load_2d(kg_buf(s), &tmKg, col, g.start, fb);
-        tma_load_2d(vg_buf(s), &tmVg, col, g.start, fb);
-        tma_load_2d(qf_buf(s), &tmQf, col, g.start, fb);
       }
     }
     return;
@@ -302,252 +303,262 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
   // ------------------------------------------------------------ doc warps
   const int gq = lane >> 2, tq = lane & 3;
   const int wr0 = warp * 16;
-  const bool active = p.doc_rows && wr0 < rows_here;
-  const int ra = r0 + wr0 + gq, rb = ra + 8;  // doc-relative rows of this thread
-
-  // Static masks (tile independent except at sequence edges): bit (nb*4 + e)
-  // set when that score element is a valid key.
-  uint32_t bmask[NBC];
-  const bool edge = (r0 - w + wr0 < 0) || (r0 - w + wr0 + 32 * NBC > n_doc);
-#pragma unroll
-  for (int bc = 0; bc < NBC; ++bc) {
-    uint32_t m = 0;
-#pragma unroll
-    for (int nb = 0; nb < 4; ++nb)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int c = 32 * bc + nb * 8 + 2 * tq + (e & 1);
-        const int diff = c - (gq + ((e >> 1) << 3));  // t - r + w
-        const int t = r0 - w + wr0 + c;
-        bool ok = diff >= 0 && diff <= 2 * w;
-        if (edge) ok = ok && t >= 0 && t < n_doc;
-        m |= (ok ? 1u : 0u) << (nb * 4 + e);
-      }
-    bmask[bc] = m;
-  }
-  uint32_t gmask[GR / 16];
-#pragma unroll
-  for (int gc = 0; gc < GR / 16; ++gc) {
-    uint32_t m = 0;
-#pragma unroll
-    for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int kg = gc * 16 + nb * 8 + 2 * tq + (e & 1);
-        const bool ok = kg < G && (kg == 0 ? p.link_cls : p.link_query);
-        m |= (ok ? 1u : 0u) << (nb * 4 + e);
-      }
-    gmask[gc] = m;
-  }
-  // Own-key mask of the tile's 64 doc keys for the full-row partials.
-  uint32_t fmask[2] = {0u, 0u};
-#pragma unroll
-  for (int nb = 0; nb < 8; ++nb)
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      fmask[nb >> 2] |= ((nb * 8 + 2 * tq + (e & 1)) < rows_here ? 1u : 0u) << ((nb & 3) * 4 + e);
-
-  float ninv_a = 0.f, ninv_b = 0.f;
-  if (p.padding == SC_PAD_ZERO_LOGIT) {
-    ninv_a = (float)(2 * w + 1 - max(0, min(n_doc, ra + w + 1) - max(0, ra - w)));
-    ninv_b = (float)(2 * w + 1 - max(0, min(n_doc, rb + w + 1) - max(0, rb - w)));
-  }
   const float c2 = p.c2;
   const int hl_bits = p.hl[0][0] | (p.hl[0][1] << 1) | (p.hl[1][0] << 2) | (p.hl[1][1] << 3);
   const int hdoc_bits = p.hdoc[0] | (p.hdoc[1] << 1);
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int j = find_seq(p.tile_base, p.nseq, tile);
+    const SeqGroups g = seq_groups(p.cu, p.qlen, j);
+    const int n_doc = g.len[2];
+    const int r0 = (tile - __ldg(p.tile_base + j)) * BM;
+    const int rows_here = min(BM, n_doc - r0);
+    const int doc_row0 = g.start + g.off[2] + r0;
+    const int G = 1 + g.len[1];
+    const bool active = p.doc_rows && wr0 < rows_here;
+    const int ra = r0 + wr0 + gq, rb = ra + 8;  // doc-relative rows of this thread
 
-  for (int h = 0; h < p.H; ++h) {
-    const int s = h % NS;
-    mbar_wait(full_bar + 8 * s, (h / NS) & 1);
-    if (active) {
-      uint32_t qa[4][4];
-      load_q(q_buf(s), wr0, lane, qa);
-      float o[8][4];
-      zero_o(o);
-      float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-      if (ninv_a > 0.f) { m0 = 0.f; l0 = tq == 0 ? ninv_a : 0.f; }
-      if (ninv_b > 0.f) { m1 = 0.f; l1 = tq == 0 ? ninv_b : 0.f; }
-      if constexpr (NBC == 1) {
-        // Single shot: all keys of the row block (globals + band) in one softmax.
-        constexpr int NG = GR / 8;
-        float sc[NG + 4][4];
-#pragma unroll
-        for (int gc = 0; gc < GR / 16; ++gc) qk16(kg_buf(s), gc * 16, lane, qa, sc[2 * gc], sc[2 * gc + 1]);
-        qk16(kb_buf(s), wr0, lane, qa, sc[NG], sc[NG + 1]);
-        qk16(kb_buf(s), wr0 + 16, lane, qa, sc[NG + 2], sc[NG + 3]);
-#pragma unroll
-        for (int nb = 0; nb < NG; ++nb)
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (!((gmask[nb >> 1] >> ((nb & 1) * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
-#pragma unroll
-        for (int nb = 0; nb < 4; ++nb)
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (!((bmask[0] >> (nb * 4 + e)) & 1)) sc[NG + nb][e] = -INFINITY;
-        softmax_update<NG + 4, true>(sc, c2, m0, m1, l0, l1, o);
-#pragma unroll
-        for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, lane, sc[2 * gc], sc[2 * gc + 1], o);
-        pv16(vb_buf(s), wr0, lane, sc[NG], sc[NG + 1], o);
-        pv16(vb_buf(s), wr0 + 16, lane, sc[NG + 2], sc[NG + 3], o);
-      } else {
-        // global keys: cls (key 0) and the query group (keys 1..G-1)
-#pragma unroll
-        for (int gc = 0; gc < GR / 16; ++gc) {
-          float sc[2][4];
-          qk16(kg_buf(s), gc * 16, lane, qa, sc[0], sc[1]);
-#pragma unroll
-          for (int nb = 0; nb < 2; ++nb)
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (!((gmask[gc] >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
-          softmax_update<2>(sc, c2, m0, m1, l0, l1, o);
-          pv16(vg_buf(s), gc * 16, lane, sc[0], sc[1], o);
+    // Static masks (tile independent except at sequence edges): bit (nb*4 + e)
+    // set when that score element is a valid key.
+    uint32_t bmask[NBC];
+    const bool edge = (r0 - w + wr0 < 0) || (r0 - w + wr0 + 32 * NBC > n_doc);
+  #pragma unroll
+    for (int bc = 0; bc < NBC; ++bc) {
+      uint32_t m = 0;
+  #pragma unroll
+      for (int nb = 0; nb < 4; ++nb)
+  #pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = 32 * bc + nb * 8 + 2 * tq + (e & 1);
+          const int diff = c - (gq + ((e >> 1) << 3));  // t - r + w
+          const int t = r0 - w + wr0 + c;
+          bool ok = diff >= 0 && diff <= 2 * w;
+          if (edge) ok = ok && t >= 0 && t < n_doc;
+          m |= (ok ? 1u : 0u) << (nb * 4 + e);
         }
-        // band keys: Kb row 0 = doc row r0 - w; this warp reads rows wr0 + [0, 32*NBC)
-#pragma unroll
-        for (int bc = 0; bc < NBC; ++bc) {
-          const int kb0 = wr0 + 32 * bc;
-          float sc[4][4];
-          qk16(kb_buf(s), kb0, lane, qa, sc[0], sc[1]);
-          qk16(kb_buf(s), kb0 + 16, lane, qa, sc[2], sc[3]);
-#pragma unroll
-          for (int nb = 0; nb < 4; ++nb)
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (!((bmask[bc] >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
-          softmax_update<4>(sc, c2, m0, m1, l0, l1, o);
-          pv16(vb_buf(s), kb0, lane, sc[0], sc[1], o);
-          pv16(vb_buf(s), kb0 + 16, lane, sc[2], sc[3], o);
+      bmask[bc] = m;
+    }
+    uint32_t gmask[GR / 16];
+  #pragma unroll
+    for (int gc = 0; gc < GR / 16; ++gc) {
+      uint32_t m = 0;
+  #pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+  #pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int kg = gc * 16 + nb * 8 + 2 * tq + (e & 1);
+          const bool ok = kg < G && (kg == 0 ? p.link_cls : p.link_query);
+          m |= (ok ? 1u : 0u) << (nb * 4 + e);
         }
-      }
-      l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-      l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-      l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-      l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-      const float i0 = 1.f / l0, i1 = 1.f / l1;
-      __nv_bfloat16* out_h = p.out + h * D + 2 * tq;
-      if (ra < n_doc) {
-        uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq) * p.ld_out);
-#pragma unroll
-        for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][0] * i0, o[nb][1] * i0);
-      }
-      if (rb < n_doc) {
-        uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq + 8) * p.ld_out);
-#pragma unroll
-        for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][2] * i1, o[nb][3] * i1);
-      }
+      gmask[gc] = m;
+    }
+    // Own-key mask of the tile's 64 doc keys for the full-row partials.
+    uint32_t fmask[2] = {0u, 0u};
+  #pragma unroll
+    for (int nb = 0; nb < 8; ++nb)
+  #pragma unroll
+      for (int e = 0; e < 4; ++e)
+        fmask[nb >> 2] |= ((nb * 8 + 2 * tq + (e & 1)) < rows_here ? 1u : 0u) << ((nb & 3) * 4 + e);
+
+    float ninv_a = 0.f, ninv_b = 0.f;
+    if (p.padding == SC_PAD_ZERO_LOGIT) {
+      ninv_a = (float)(2 * w + 1 - max(0, min(n_doc, ra + w + 1) - max(0, ra - w)));
+      ninv_b = (float)(2 * w + 1 - max(0, min(n_doc, rb + w + 1) - max(0, rb - w)));
     }
 
-    // Full-row split-softmax partials over the tile's 64 own doc keys; the
-    // designated warp rotates with the head so the extra work spreads evenly.
-    if (warp == (h & (NDOCW - 1))) {
-#pragma unroll
-      for (int fc = 0; fc < GR / 16; ++fc) {
-        if (fc * 16 < p.fneed) {
-          uint32_t qa[4][4];
-          load_q(qf_buf(s), fc * 16, lane, qa);
-          float sc[8][4];
-#pragma unroll
-          for (int np = 0; np < 4; ++np) qk16(kb_buf(s), w + np * 16, lane, qa, sc[2 * np], sc[2 * np + 1]);
-#pragma unroll
-          for (int nb = 0; nb < 8; ++nb)
-#pragma unroll
+    for (int h = 0; h < p.H; ++h, ++it) {
+      const int s = it % NS;
+      mbar_wait(full_bar + 8 * s, (it / NS) & 1);
+      if (active) {
+        uint32_t qa[4][4];
+        load_q(q_buf(s), wr0, lane, qa);
+        float o[8][4];
+        zero_o(o);
+        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+        if (ninv_a > 0.f) { m0 = 0.f; l0 = tq == 0 ? ninv_a : 0.f; }
+        if (ninv_b > 0.f) { m1 = 0.f; l1 = tq == 0 ? ninv_b : 0.f; }
+        if constexpr (NBC == 1) {
+          // Single shot: all keys of the row block (globals + band) in one softmax.
+          constexpr int NG = GR / 8;
+          float sc[NG + 4][4];
+  #pragma unroll
+          for (int gc = 0; gc < GR / 16; ++gc) qk16(kg_buf(s), gc * 16, lane, qa, sc[2 * gc], sc[2 * gc + 1]);
+          qk16(kb_buf(s), wr0, lane, qa, sc[NG], sc[NG + 1]);
+          qk16(kb_buf(s), wr0 + 16, lane, qa, sc[NG + 2], sc[NG + 3]);
+  #pragma unroll
+          for (int nb = 0; nb < NG; ++nb)
+  #pragma unroll
             for (int e = 0; e < 4; ++e)
-              if (!((fmask[nb >> 2] >> ((nb & 3) * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
-          float o[8][4];
-          zero_o(o);
-          float fm0 = -INFINITY, fm1 = -INFINITY, fl0 = 0.f, fl1 = 0.f;
-          softmax_update<8, true>(sc, c2, fm0, fm1, fl0, fl1, o);
-#pragma unroll
-          for (int kp = 0; kp < 4; ++kp) pv16(vb_buf(s), w + kp * 16, lane, sc[2 * kp], sc[2 * kp + 1], o);
-          fl0 += __shfl_xor_sync(0xffffffffu, fl0, 1);
-          fl0 += __shfl_xor_sync(0xffffffffu, fl0, 2);
-          fl1 += __shfl_xor_sync(0xffffffffu, fl1, 1);
-          fl1 += __shfl_xor_sync(0xffffffffu, fl1, 2);
-          const float to_nat = c2 * 0.69314718055994530942f;  // raw logit -> natural units (1/scale)
-#pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            const int f = fc * 16 + gq + 8 * half;
-            if (f >= p.fneed) continue;
-            float* rec = p.partials + (((int64_t)tile * p.H + h) * p.fmax + f) * REC;
-            if (tq == 0) {
-              rec[0] = (half ? fm1 : fm0) * to_nat;
-              rec[1] = half ? fl1 : fl0;
-            }
-#pragma unroll
-            for (int nb = 0; nb < 8; ++nb)
-              *reinterpret_cast<float2*>(rec + 4 + nb * 8 + 2 * tq) =
-                  make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
+              if (!((gmask[nb >> 1] >> ((nb & 1) * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+  #pragma unroll
+          for (int nb = 0; nb < 4; ++nb)
+  #pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (!((bmask[0] >> (nb * 4 + e)) & 1)) sc[NG + nb][e] = -INFINITY;
+          softmax_update<NG + 4, true>(sc, c2, m0, m1, l0, l1, o);
+  #pragma unroll
+          for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, lane, sc[2 * gc], sc[2 * gc + 1], o);
+          pv16(vb_buf(s), wr0, lane, sc[NG], sc[NG + 1], o);
+          pv16(vb_buf(s), wr0 + 16, lane, sc[NG + 2], sc[NG + 3], o);
+        } else {
+          // global keys: cls (key 0) and the query group (keys 1..G-1)
+  #pragma unroll
+          for (int gc = 0; gc < GR / 16; ++gc) {
+            float sc[2][4];
+            qk16(kg_buf(s), gc * 16, lane, qa, sc[0], sc[1]);
+  #pragma unroll
+            for (int nb = 0; nb < 2; ++nb)
+  #pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (!((gmask[gc] >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+            softmax_update<2>(sc, c2, m0, m1, l0, l1, o);
+            pv16(vg_buf(s), gc * 16, lane, sc[0], sc[1], o);
+          }
+          // band keys: Kb row 0 = doc row r0 - w; this warp reads rows wr0 + [0, 32*NBC)
+  #pragma unroll
+          for (int bc = 0; bc < NBC; ++bc) {
+            const int kb0 = wr0 + 32 * bc;
+            float sc[4][4];
+            qk16(kb_buf(s), kb0, lane, qa, sc[0], sc[1]);
+            qk16(kb_buf(s), kb0 + 16, lane, qa, sc[2], sc[3]);
+  #pragma unroll
+            for (int nb = 0; nb < 4; ++nb)
+  #pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (!((bmask[bc] >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+            softmax_update<4>(sc, c2, m0, m1, l0, l1, o);
+            pv16(vb_buf(s), kb0, lane, sc[0], sc[1], o);
+            pv16(vb_buf(s), kb0 + 16, lane, sc[2], sc[3], o);
           }
         }
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+        const float i0 = 1.f / l0, i1 = 1.f / l1;
+        __nv_bfloat16* out_h = p.out + h * D + 2 * tq;
+        if (ra < n_doc) {
+          uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq) * p.ld_out);
+  #pragma unroll
+          for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][0] * i0, o[nb][1] * i0);
+        }
+        if (rb < n_doc) {
+          uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq + 8) * p.ld_out);
+  #pragma unroll
+          for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][2] * i1, o[nb][3] * i1);
+        }
       }
-    }
-    // Head rows over the global keys (first tile of the sequence only): rows
-    // f < G (cls, query group) attend cls / query keys per their links.  Rows
-    // with a FULL doc link leave a split-softmax record (merged below); the
-    // others (sparse: query rows) are final and stored here.
-    if (r0 == 0 && warp == ((h + 2) & (NDOCW - 1))) {
-#pragma unroll
-      for (int fc = 0; fc < GR / 16; ++fc) {
-        if (fc * 16 < G) {
-          uint32_t qa[4][4];
-          load_q(qf_buf(s), fc * 16, lane, qa);
-          float sc[GR / 8][4];
-#pragma unroll
-          for (int gc = 0; gc < GR / 16; ++gc) qk16(kg_buf(s), gc * 16, lane, qa, sc[2 * gc], sc[2 * gc + 1]);
-#pragma unroll
-          for (int nb = 0; nb < GR / 8; ++nb)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int f = fc * 16 + gq + ((e >> 1) << 3);
-              const int kg = nb * 8 + 2 * tq + (e & 1);
-              const int grp = f == 0 ? 0 : 1;
-              const bool ok = f < G && kg < G && ((hl_bits >> (grp * 2 + (kg == 0 ? 0 : 1))) & 1);
-              if (!ok) sc[nb][e] = -INFINITY;
-            }
-          float o[8][4];
-          zero_o(o);
-          float hm0 = -INFINITY, hm1 = -INFINITY, hl0 = 0.f, hl1 = 0.f;
-          softmax_update<GR / 8, true>(sc, c2, hm0, hm1, hl0, hl1, o);
-#pragma unroll
-          for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, lane, sc[2 * gc], sc[2 * gc + 1], o);
-          hl0 += __shfl_xor_sync(0xffffffffu, hl0, 1);
-          hl0 += __shfl_xor_sync(0xffffffffu, hl0, 2);
-          hl1 += __shfl_xor_sync(0xffffffffu, hl1, 1);
-          hl1 += __shfl_xor_sync(0xffffffffu, hl1, 2);
-          const float to_nat = c2 * 0.69314718055994530942f;
-#pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            const int f = fc * 16 + gq + 8 * half;
-            if (f >= G) continue;
-            const int grp = f == 0 ? 0 : 1;
-            const float mm = half ? hm1 : hm0, ll = half ? hl1 : hl0;
-            if ((hdoc_bits >> grp) & 1) {
-              float* rec = p.partials + (((int64_t)(p.ntiles_max + j) * p.H + h) * p.fmax + f) * REC;
+
+      // Full-row split-softmax partials over the tile's 64 own doc keys; the
+      // designated warp rotates with the head so the extra work spreads evenly.
+      if (warp == (h & (NDOCW - 1))) {
+  #pragma unroll
+        for (int fc = 0; fc < GR / 16; ++fc) {
+          if (fc * 16 < p.fneed) {
+            uint32_t qa[4][4];
+            load_q(qf_buf(s), fc * 16, lane, qa);
+            float sc[8][4];
+  #pragma unroll
+            for (int np = 0; np < 4; ++np) qk16(kb_buf(s), w + np * 16, lane, qa, sc[2 * np], sc[2 * np + 1]);
+  #pragma unroll
+            for (int nb = 0; nb < 8; ++nb)
+  #pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (!((fmask[nb >> 2] >> ((nb & 3) * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+            float o[8][4];
+            zero_o(o);
+            float fm0 = -INFINITY, fm1 = -INFINITY, fl0 = 0.f, fl1 = 0.f;
+            softmax_update<8, true>(sc, c2, fm0, fm1, fl0, fl1, o);
+  #pragma unroll
+            for (int kp = 0; kp < 4; ++kp) pv16(vb_buf(s), w + kp * 16, lane, sc[2 * kp], sc[2 * kp + 1], o);
+            fl0 += __shfl_xor_sync(0xffffffffu, fl0, 1);
+            fl0 += __shfl_xor_sync(0xffffffffu, fl0, 2);
+            fl1 += __shfl_xor_sync(0xffffffffu, fl1, 1);
+            fl1 += __shfl_xor_sync(0xffffffffu, fl1, 2);
+            const float to_nat = c2 * 0.69314718055994530942f;  // raw logit -> natural units (1/scale)
+  #pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              const int f = fc * 16 + gq + 8 * half;
+              if (f >= p.fneed) continue;
+              float* rec = p.partials + (((int64_t)tile * p.H + h) * p.fmax + f) * REC;
               if (tq == 0) {
-                rec[0] = ll > 0.f ? mm * to_nat : -INFINITY;
-                rec[1] = ll;
+                rec[0] = (half ? fm1 : fm0) * to_nat;
+                rec[1] = half ? fl1 : fl0;
               }
-#pragma unroll
+  #pragma unroll
               for (int nb = 0; nb < 8; ++nb)
                 *reinterpret_cast<float2*>(rec + 4 + nb * 8 + 2 * tq) =
                     make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
-            } else {
-              const float inv = ll > 0.f ? 1.f / ll : 0.f;
-              uint32_t* dst = reinterpret_cast<uint32_t*>(p.out + (int64_t)(g.start + f) * p.ld_out + h * D + 2 * tq);
-#pragma unroll
-              for (int nb = 0; nb < 8; ++nb)
-                dst[nb * 4] = pack_bf16(o[nb][2 * half] * inv, o[nb][2 * half + 1] * inv);
             }
           }
         }
       }
+      // Head rows over the global keys (first tile of the sequence only): rows
+      // f < G (cls, query group) attend cls / query keys per their links.  Rows
+      // with a FULL doc link leave a split-softmax record (merged below); the
+      // others (sparse: query rows) are final and stored here.
+      if (r0 == 0 && warp == ((h + 2) & (NDOCW - 1))) {
+  #pragma unroll
+        for (int fc = 0; fc < GR / 16; ++fc) {
+          if (fc * 16 < G) {
+            uint32_t qa[4][4];
+            load_q(qf_buf(s), fc * 16, lane, qa);
+            float sc[GR / 8][4];
+  #pragma unroll
+            for (int gc = 0; gc < GR / 16; ++gc) qk16(kg_buf(s), gc * 16, lane, qa, sc[2 * gc], sc[2 * gc + 1]);
+  #pragma unroll
+            for (int nb = 0; nb < GR / 8; ++nb)
+  #pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int f = fc * 16 + gq + ((e >> 1) << 3);
+                const int kg = nb * 8 + 2 * tq + (e & 1);
+                const int grp = f == 0 ? 0 : 1;
+                const bool ok = f < G && kg < G && ((hl_bits >> (grp * 2 + (kg == 0 ? 0 : 1))) & 1);
+                if (!ok) sc[nb][e] = -INFINITY;
+              }
+            float o[8][4];
+            zero_o(o);
+            float hm0 = -INFINITY, hm1 = -INFINITY, hl0 = 0.f, hl1 = 0.f;
+            softmax_update<GR / 8, true>(sc, c2, hm0, hm1, hl0, hl1, o);
+  #pragma unroll
+            for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, lane, sc[2 * gc], sc[2 * gc + 1], o);
+            hl0 += __shfl_xor_sync(0xffffffffu, hl0, 1);
+            hl0 += __shfl_xor_sync(0xffffffffu, hl0, 2);
+            hl1 += __shfl_xor_sync(0xffffffffu, hl1, 1);
+            hl1 += __shfl_xor_sync(0xffffffffu, hl1, 2);
+            const float to_nat = c2 * 0.69314718055994530942f;
+  #pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              const int f = fc * 16 + gq + 8 * half;
+              if (f >= G) continue;
+              const int grp = f == 0 ? 0 : 1;
+              const float mm = half ? hm1 : hm0, ll = half ? hl1 : hl0;
+              if ((hdoc_bits >> grp) & 1) {
+                float* rec = p.partials + (((int64_t)(p.ntiles_max + j) * p.H + h) * p.fmax + f) * REC;
+                if (tq == 0) {
+                  rec[0] = ll > 0.f ? mm * to_nat : -INFINITY;
+                  rec[1] = ll;
+                }
+  #pragma unroll
+                for (int nb = 0; nb < 8; ++nb)
+                  *reinterpret_cast<float2*>(rec + 4 + nb * 8 + 2 * tq) =
+                      make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
+              } else {
+                const float inv = ll > 0.f ? 1.f / ll : 0.f;
+                uint32_t* dst = reinterpret_cast<uint32_t*>(p.out + (int64_t)(g.start + f) * p.ld_out + h * D + 2 * tq);
+  #pragma unroll
+                for (int nb = 0; nb < 8; ++nb)
+                  dst[nb * 4] = pack_bf16(o[nb][2 * half] * inv, o[nb][2 * half + 1] * inv);
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_bar + 8 * s);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty_bar + 8 * s);
-  }
 
+  }
 }
 
 // Merge of the split-softmax records into the head rows with a FULL doc link
@@ -672,8 +683,17 @@ static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, c
     }
     attr = true;
   }
-  band_attn_kernel<NBC, GR, NS><<<grid, NTHREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3],
-                                                              maps[4], maps[5], p);
+  // Persistent grid: every resident CTA slot (SMs x CTAs/SM) loops over tiles.
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (num_sms <= 0) num_sms = 148;
+  }
+  const unsigned slots = (unsigned)(num_sms * min_ctas(NBC));
+  band_attn_kernel<NBC, GR, NS><<<grid < slots ? grid : slots, NTHREADS, smem, st>>>(
+      maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], p);
   SC_CHECK_LAUNCH("band_attn_kernel");
   return SC_OK;
 }
@@ -755,7 +775,7 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
     p.hl[gsrc][1] = L.w[gsrc][1] == SC_LINK_FULL;
     p.hdoc[gsrc] = L.w[gsrc][2] == SC_LINK_FULL;
   }
-  const unsigned grid = (unsigned)((a.T + BM - 1) / BM + a.nseq);
+  const unsigned grid = (unsigned)((a.T + BM - 1) / BM + a.nseq);  // upper bound on tiles (record indexing)
   p.ntiles_max = (int)grid;
   // Doc rows + head rows over the global keys (first tile of each sequence).
   // (seq_head_base is unused: head rows are addressed through cu_seqlens.)
