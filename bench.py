@@ -303,9 +303,8 @@ def run_gpu(args):
 
     # ---- roofline of the attention kernel (sc_attn_fwd, band + head-row pass) ----
     attn_bytes = 4 * layout.total_tokens * cfg["embed_dim"] * 2  # Q,K,V read + O write, bf16
-    attn_where = "in-step CUDA events around every sc_attn_fwd launch of the timed region"
-    if not attn_ms:
-        # graph replay: time the same attention launch standalone on this step's layout
+    def attn_standalone_ms(reps=20):
+        """sc_attn_fwd alone on this step's layout and shapes, CUDA events on the launching stream."""
         h, H = cfg["embed_dim"], cfg["heads"]
         qkv = torch.randn((layout.total_tokens, 3 * h), device=dev).to(torch.bfloat16)
         out = torch.empty((layout.total_tokens, h), device=dev, dtype=torch.bfloat16)
@@ -313,16 +312,23 @@ def run_gpu(args):
         run = lambda: P.attend_packed(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], layout, pat, H, out=out, check=False)
         for _ in range(3):
             run()
-        for _ in range(20):
+        evs = []
+        for _ in range(reps):
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
             run()
             a1.record(stream)
-            attn_events += [a0, a1]
+            evs += [a0, a1]
         torch.cuda.synchronize()
-        attn_ms = [attn_events[i].elapsed_time(attn_events[i + 1]) for i in range(0, len(attn_events), 2)]
+        return [evs[i].elapsed_time(evs[i + 1]) for i in range(0, len(evs), 2)]
+
+    alone_ms = attn_standalone_ms()
+    attn_where = "in-step CUDA events around every sc_attn_fwd launch of the timed region"
+    if not attn_ms:  # graph replay: no per-launch events inside the graph
+        attn_ms = alone_ms
         attn_where = "standalone CUDA-event timing of sc_attn_fwd on this step's layout (step runs as a CUDA graph)"
     attn_avg_ms = statistics.mean(attn_ms)
+    alone_gbs = attn_bytes / (statistics.median(alone_ms) / 1e3) / 1e9
     achieved = attn_bytes / (attn_avg_ms / 1e3) / 1e9
     gemm_flops_step = 2 * layout.total_tokens * cfg["layers"] * (4 * cfg["embed_dim"] ** 2 + 2 * cfg["embed_dim"] * cfg["ff_dim"])
     traffic = None
@@ -361,7 +367,10 @@ def run_gpu(args):
                          "algorithmic_bytes_per_launch": attn_bytes, "avg_launch_ms": attn_avg_ms,
                          "launches": len(attn_ms), "frac_of_8TBs": achieved / 8000.0,
                          "share_of_step": (sum(attn_ms) / ms) if not use_graph else None,
-                         "timing": attn_where},
+                         "timing": attn_where,
+                         "standalone": {"achieved": alone_gbs, "frac": alone_gbs / hbm_peak,
+                                        "median_ms": statistics.median(alone_ms),
+                                        "note": "same launch timed alone (GPU not power-capped by the GEMMs)"}},
             "step_roofline": {"bound": "tensor", "achieved": gemm_flops_step / (ms_max / args.steps / 1e3) / 1e12,
                               "peak": tf_sus, "unit": "TFLOP/s", "note": "GEMM FLOPs per step / step time vs sustained bf16"},
             "cpu_baseline": cpu,
