@@ -312,15 +312,19 @@ def run_gpu(args):
         run = lambda: P.attend_packed(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], layout, pat, H, out=out, check=False)
         for _ in range(3):
             run()
-        evs = []
-        for _ in range(reps):
+        torch.cuda.synchronize()
+        # back-to-back launches between two events (a per-launch event pair would
+        # also time the host-side launch latency of an idle GPU); 5 trials
+        trials = []
+        for _ in range(5):
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
-            run()
+            for _ in range(reps):
+                run()
             a1.record(stream)
-            evs += [a0, a1]
-        torch.cuda.synchronize()
-        return [evs[i].elapsed_time(evs[i + 1]) for i in range(0, len(evs), 2)]
+            torch.cuda.synchronize()
+            trials.append(a0.elapsed_time(a1) / reps)
+        return trials
 
     alone_ms = attn_standalone_ms()
     attn_where = "in-step CUDA events around every sc_attn_fwd launch of the timed region"
@@ -370,7 +374,7 @@ def run_gpu(args):
                          "timing": attn_where,
                          "standalone": {"achieved": alone_gbs, "frac": alone_gbs / hbm_peak,
                                         "median_ms": statistics.median(alone_ms),
-                                        "note": "same launch timed alone (GPU not power-capped by the GEMMs)"}},
+                                        "note": "same launch, 20 back-to-back launches between CUDA events, median of 5 trials (GPU not power-capped by the GEMMs)"}},
             "step_roofline": {"bound": "tensor", "achieved": gemm_flops_step / (ms_max / args.steps / 1e3) / 1e12,
                               "peak": tf_sus, "unit": "TFLOP/s", "note": "GEMM FLOPs per step / step time vs sustained bf16"},
             "cpu_baseline": cpu,

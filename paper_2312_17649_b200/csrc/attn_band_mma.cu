@@ -97,6 +97,22 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, 
                ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1)
                : "memory");
 }
+// Shared -> global TMA store of a box (bulk-group completion).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// Wait until every committed bulk store has finished READING shared memory.
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void stsm_x4(uint32_t addr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+  asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1,%2,%3,%4};"
+               ::"r"(addr), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+               : "memory");
+}
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -222,7 +238,8 @@ template <int NBC, int GR, int NS>
 __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQf,
     const __grid_constant__ CUtensorMap tmKg, const __grid_constant__ CUtensorMap tmVg,
-    const __grid_constant__ CUtensorMap tmKb, const __grid_constant__ CUtensorMap tmVb, Params p) {
+    const __grid_constant__ CUtensorMap tmKb, const __grid_constant__ CUtensorMap tmVb,
+    const __grid_constant__ CUtensorMap tmO, Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
@@ -436,6 +453,23 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
         l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
         const float i0 = 1.f / l0, i1 = 1.f / l1;
+        if (wr0 + 16 <= rows_here) {
+          // Full 16-row block: stmatrix the bf16 O fragments into this warp's
+          // (now dead) Q rows -- same 128B swizzle as the TMA box -- and TMA-store
+          // them: 16 rows x 128 B leave in whole lines instead of 16 scattered
+          // 4-byte stores per row.
+          const uint32_t ob = q_buf(s);
+          const int srow = wr0 + (lane & 7) + (((lane >> 3) & 1) << 3);
+  #pragma unroll
+          for (int np = 0; np < 4; ++np)
+            stsm_x4(swz(ob, srow, 2 * np + (lane >> 4)),
+                    pack_bf16(o[2 * np][0] * i0, o[2 * np][1] * i0), pack_bf16(o[2 * np][2] * i1, o[2 * np][3] * i1),
+                    pack_bf16(o[2 * np + 1][0] * i0, o[2 * np + 1][1] * i0),
+                    pack_bf16(o[2 * np + 1][2] * i1, o[2 * np + 1][3] * i1));
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) tma_store_2d(&tmO, ob + wr0 * ROWB, h * D, doc_row0 + wr0);
+        } else {
         __nv_bfloat16* out_h = p.out + h * D + 2 * tq;
         if (ra < n_doc) {
           uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq) * p.ld_out);
@@ -446,6 +480,7 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
           uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq + 8) * p.ld_out);
   #pragma unroll
           for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][2] * i1, o[nb][3] * i1);
+        }
         }
       }
 
@@ -555,7 +590,10 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty_bar + 8 * s);
+      if (lane == 0) {
+        if (active) tma_store_wait_read();  // the stage's Q rows are about to be refilled
+        mbar_arrive(empty_bar + 8 * s);
+      }
     }
 
   }
@@ -658,7 +696,7 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t row
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, Params);
+using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, Params);
 
 // Stage count: as many as fit two CTAs per SM (<= ~113 KB each), at least 2.
 template <int NBC, int GR>
@@ -693,7 +731,7 @@ static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, c
   }
   const unsigned slots = (unsigned)(num_sms * min_ctas(NBC));
   band_attn_kernel<NBC, GR, NS><<<grid < slots ? grid : slots, NTHREADS, smem, st>>>(
-      maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], p);
+      maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
   SC_CHECK_LAUNCH("band_attn_kernel");
   return SC_OK;
 }
@@ -746,18 +784,19 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   if (tile_rows != BM || !seq_tile_base || !seq_head_base) return unsupported("layout tiles must be 64 rows");
   if (((uintptr_t)a.q | (uintptr_t)a.k | (uintptr_t)a.v | (uintptr_t)a.out) & 15)
     return unsupported("16-byte alignment");
-  if ((a.ld * 2) % 16 || a.ld_out % 2) return unsupported("row strides");
+  if ((a.ld * 2) % 16 || (a.ld_out * 2) % 16) return unsupported("row strides");
   const int fneed = full_rows_needed(L, max_qgroup_len);
   const size_t need = band_workspace_bytes(a.nseq, a.T, a.H, a.d, tile_rows, max_qgroup_len, L);
   if (need > ws_bytes || (need && !ws)) return unsupported("workspace too small");
   const int GR = (max_qgroup_len + 1 <= 16) ? 16 : 32;
 
-  CUtensorMap maps[6];
+  CUtensorMap maps[7];
   const int64_t cols = (int64_t)a.H * D;
   if (!make_map(&maps[0], a.q, cols, a.T, a.ld, BM) || !make_map(&maps[1], a.q, cols, a.T, a.ld, GR) ||
       !make_map(&maps[2], a.k, cols, a.T, a.ld, GR) || !make_map(&maps[3], a.v, cols, a.T, a.ld, GR) ||
       !make_map(&maps[4], a.k, cols, a.T, a.ld, BM + 2 * w) ||
-      !make_map(&maps[5], a.v, cols, a.T, a.ld, BM + 2 * w))
+      !make_map(&maps[5], a.v, cols, a.T, a.ld, BM + 2 * w) ||
+      !make_map(&maps[6], a.out, cols, a.T, a.ld_out, 16))
     return unsupported("cuTensorMapEncodeTiled failed");
 
   Params p;
