@@ -239,7 +239,7 @@ def run_gpu(args):
     def device_step(h=None):
         if graphed is not None:
             return gather(graphed(ids_dev))
-        x = model.encode_packed(ids_dev, layout, check_finite=False, attn_hook=h)
+        x = model.encode_packed(ids_dev, layout, attn_hook=h)
         return gather(model.scores_from_hidden(x, layout))
 
     def barrier():
@@ -281,7 +281,7 @@ def run_gpu(args):
         else:
             ids = ids_host.to(dev, non_blocking=True)
             lay = model.make_layout(batch)
-            x = model.encode_packed(ids, lay, check_finite=False)
+            x = model.encode_packed(ids, lay)
             sc = gather(model.scores_from_hidden(x, lay))
         host_scores.copy_(sc, non_blocking=True)
         return sc

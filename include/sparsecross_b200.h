@@ -149,8 +149,8 @@ SC_API int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t row_
 
 /* ---- Encoder-loop kernels (R/encoder.py:306-371, :475-509) -------------- */
 
-/* x[t] = tok_emb[ids[t]] + pos_emb[tok_pos[t]] (R/encoder.py:483); fp32 out,
- * optional bf16 copy (xh may be NULL).  emb tables are fp32 [*, hidden]. */
+/* x[t] = tok_emb[ids[t]] + pos_emb[tok_pos[t]] (R/encoder.py:483); fp32 x
+ * and bf16 xh are each optional (not both NULL).  emb tables are fp32 [*, hidden]. */
 SC_API int sc_embed(const int32_t* ids, const int32_t* tok_pos, const float* tok_emb,
              const float* pos_emb, float* x, void* xh, int32_t total_tokens, int32_t hidden,
              void* stream);
@@ -162,6 +162,18 @@ SC_API int sc_residual_layernorm(const float* resid, const void* y, int32_t y_dt
                           const float* bias, const float* gamma, const float* beta,
                           float* x_out, void* out_h, int32_t rows, int32_t hidden,
                           void* stream);
+
+/* Generalised residual LayerNorm: resid of resid_dtype (fp32 or bf16; the
+ * bf16 encoder keeps its residual stream in bf16), y of y_dtype, x_out (fp32)
+ * and out_h (bf16) each optional (not both NULL); resid may alias either
+ * output.  nonfinite_count (device int32, may be NULL) is incremented once per
+ * warp whose output holds a NaN/Inf: the reference's per-layer finite check
+ * (R/encoder.py:356-357) fused into the pass that writes the layer output. */
+SC_API int sc_residual_layernorm_ex(const void* resid, int32_t resid_dtype, const void* y,
+                             int32_t y_dtype, const float* bias, const float* gamma,
+                             const float* beta, float* x_out, void* out_h,
+                             int32_t* nonfinite_count, int32_t rows, int32_t hidden,
+                             void* stream);
 
 /* In-place exact-erf GELU with optional bias (R/encoder.py:258-259). */
 SC_API int sc_bias_gelu(void* x, const float* bias, int32_t dtype, int64_t rows, int32_t cols,

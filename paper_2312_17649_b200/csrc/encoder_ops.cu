@@ -22,21 +22,32 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const int32_t* __r
   const float* b = pe + (int64_t)__ldg(pos + r) * h;
   for (int c = threadIdx.x; c < h; c += blockDim.x) {
     float v = __ldg(a + c) + __ldg(b + c);
-    x[(int64_t)r * h + c] = v;
+    if (x) x[(int64_t)r * h + c] = v;
     if (xh) xh[(int64_t)r * h + c] = __float2bfloat16_rn(v);
   }
 }
 
+// Every LayerNorm variant: out = LN(resid + y (+ bias)) * gamma + beta with
+// fp32 statistics.  resid is fp32 or bf16 (the bf16 inference path keeps its
+// residual stream in bf16); `out` (fp32) and `out_h` (bf16) are each optional;
+// `bad` (optional) counts warps that produced a non-finite value -- the
+// reference's per-layer isfinite check (R/encoder.py:356-357) fused into the
+// pass that writes the layer output.
+__device__ __forceinline__ void flag_nonfinite(int32_t* bad, bool any_bad) {
+  if (bad && __any_sync(0xffffffffu, any_bad) && (threadIdx.x & 31) == 0) atomicAdd(bad, 1);
+}
+
 // One warp per row, row cached in registers (h <= 32 * kPer).
-template <typename Y, int kPer>
-__global__ void residual_ln_kernel(const float* __restrict__ resid, const Y* __restrict__ y,
+template <typename R, typename Y, int kPer>
+__global__ void residual_ln_kernel(const R* __restrict__ resid, const Y* __restrict__ y,
                                    const float* __restrict__ bias, const float* __restrict__ gamma,
                                    const float* __restrict__ beta, float* __restrict__ out,
-                                   __nv_bfloat16* __restrict__ out_h, int rows, int h) {
+                                   __nv_bfloat16* __restrict__ out_h, int32_t* __restrict__ bad,
+                                   int rows, int h) {
   int lane = threadIdx.x & 31;
   int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= rows) return;
-  const float* rr = resid + (int64_t)r * h;
+  const R* rr = resid + (int64_t)r * h;
   const Y* yr = y + (int64_t)r * h;
   float v[kPer];
   float sum = 0.f;
@@ -47,7 +58,7 @@ __global__ void residual_ln_kernel(const float* __restrict__ resid, const Y* __r
     if (c < h) {
       float t = to_f32(yr[c]);
       if (bias) t += __ldg(bias + c);
-      v[e] = rr[c] + t;
+      v[e] = to_f32(rr[c]) + t;
       sum += v[e];
     }
   }
@@ -63,16 +74,18 @@ __global__ void residual_ln_kernel(const float* __restrict__ resid, const Y* __r
   }
   float var = warp_sum(sq) / (float)h;
   float inv = 1.f / sqrtf(var + kLnEps);
-  float* orow = out + (int64_t)r * h;
+  bool nf = false;
 #pragma unroll
   for (int e = 0; e < kPer; ++e) {
     int c = lane + 32 * e;
     if (c < h) {
       float o = __ldg(gamma + c) * (v[e] * inv) + __ldg(beta + c);
-      orow[c] = o;
+      nf |= !isfinite(o);
+      if (out) out[(int64_t)r * h + c] = o;
       if (out_h) out_h[(int64_t)r * h + c] = __float2bfloat16_rn(o);
     }
   }
+  flag_nonfinite(bad, nf);
 }
 
 // Vectorised variant for h % 128 == 0: lane covers 4 consecutive elements at
@@ -84,16 +97,19 @@ __device__ __forceinline__ float4 load4(const __nv_bfloat16* p) {
   float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
   return make_float4(a.x, a.y, b.x, b.y);
 }
+__device__ __forceinline__ bool finite4(float4 o) {
+  return isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w);
+}
 
-template <typename Y, int kVec>
+template <typename R, typename Y, int kVec>
 __global__ void __launch_bounds__(256, 3) residual_ln_vec_kernel(
-    const float* __restrict__ resid, const Y* __restrict__ y, const float* __restrict__ bias,
+    const R* __restrict__ resid, const Y* __restrict__ y, const float* __restrict__ bias,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ out,
-    __nv_bfloat16* __restrict__ out_h, int rows, int h) {
+    __nv_bfloat16* __restrict__ out_h, int32_t* __restrict__ bad, int rows, int h) {
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= rows) return;
-  const float* rr = resid + (int64_t)r * h;
+  const R* rr = resid + (int64_t)r * h;
   const Y* yr = y + (int64_t)r * h;
   float4 v[kVec];
   float sum = 0.f;
@@ -117,32 +133,36 @@ __global__ void __launch_bounds__(256, 3) residual_ln_vec_kernel(
     sq = fmaf(v[e].z, v[e].z, sq); sq = fmaf(v[e].w, v[e].w, sq);
   }
   const float inv = 1.f / sqrtf(warp_sum(sq) / (float)h + kLnEps);
+  bool nf = false;
 #pragma unroll
   for (int e = 0; e < kVec; ++e) {
     const int c = 4 * lane + 128 * e;
     const float4 g = load4(gamma + c), bt = load4(beta + c);
     float4 o = make_float4(g.x * (v[e].x * inv) + bt.x, g.y * (v[e].y * inv) + bt.y,
                            g.z * (v[e].z * inv) + bt.z, g.w * (v[e].w * inv) + bt.w);
-    *reinterpret_cast<float4*>(out + (int64_t)r * h + c) = o;
+    nf |= !finite4(o);
+    if (out) *reinterpret_cast<float4*>(out + (int64_t)r * h + c) = o;
     if (out_h) {
       __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
       uint2 u = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
       *reinterpret_cast<uint2*>(out_h + (int64_t)r * h + c) = u;
     }
   }
+  flag_nonfinite(bad, nf);
 }
 
 // Large-h fallback: block per row, three passes through L1/L2.
-template <typename Y>
-__global__ void residual_ln_big_kernel(const float* __restrict__ resid, const Y* __restrict__ y,
+template <typename R, typename Y>
+__global__ void residual_ln_big_kernel(const R* __restrict__ resid, const Y* __restrict__ y,
                                        const float* __restrict__ bias, const float* __restrict__ gamma,
                                        const float* __restrict__ beta, float* __restrict__ out,
-                                       __nv_bfloat16* __restrict__ out_h, int rows, int h) {
+                                       __nv_bfloat16* __restrict__ out_h, int32_t* __restrict__ bad,
+                                       int rows, int h) {
   __shared__ float red[32];
   int r = blockIdx.x;
-  const float* rr = resid + (int64_t)r * h;
+  const R* rr = resid + (int64_t)r * h;
   const Y* yr = y + (int64_t)r * h;
-  auto val = [&](int c) { return rr[c] + to_f32(yr[c]) + (bias ? bias[c] : 0.f); };
+  auto val = [&](int c) { return to_f32(rr[c]) + to_f32(yr[c]) + (bias ? bias[c] : 0.f); };
   auto block_sum = [&](float s) {
     s = warp_sum(s);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -160,11 +180,44 @@ __global__ void residual_ln_big_kernel(const float* __restrict__ resid, const Y*
   for (int c = threadIdx.x; c < h; c += blockDim.x) { float t = val(c) - mu; q = fmaf(t, t, q); }
   float inv = 1.f / sqrtf(block_sum(q) / (float)h + kLnEps);
   __syncthreads();
+  // (each column is read and written by the same thread, so resid may alias out / out_h)
+  bool nf = false;
   for (int c = threadIdx.x; c < h; c += blockDim.x) {
-    float o = gamma[c] * ((val(c) - mu) * inv) + beta[c];
-    out[(int64_t)r * h + c] = o;
+    const float o = gamma[c] * ((val(c) - mu) * inv) + beta[c];
+    nf |= !isfinite(o);
+    if (out) out[(int64_t)r * h + c] = o;
     if (out_h) out_h[(int64_t)r * h + c] = __float2bfloat16_rn(o);
   }
+  flag_nonfinite(bad, nf);
+}
+
+template <typename R, typename Y>
+int launch_ln(const void* resid_v, const void* y, const float* bias, const float* gamma,
+              const float* beta, float* out, void* out_h, int32_t* bad, int rows, int h, cudaStream_t st) {
+  const R* resid = static_cast<const R*>(resid_v);
+  const Y* yy = static_cast<const Y*>(y);
+  __nv_bfloat16* oh = static_cast<__nv_bfloat16*>(out_h);
+  unsigned blocks = (unsigned)((rows + 7) / 8);
+  int per = (h + 31) / 32;
+  const bool vec = (h % 128 == 0) && !(((uintptr_t)resid | (uintptr_t)y | (uintptr_t)out |
+                                         (uintptr_t)out_h | (uintptr_t)gamma | (uintptr_t)beta |
+                                         (uintptr_t)bias) & 15);
+#define SC_LN_ARGS resid, yy, bias, gamma, beta, out, oh, bad, rows, h
+  if (vec && h == 768) residual_ln_vec_kernel<R, Y, 6><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  else if (vec && h == 384) residual_ln_vec_kernel<R, Y, 3><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  else if (vec && h == 1024) residual_ln_vec_kernel<R, Y, 8><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  else if (vec && h == 512) residual_ln_vec_kernel<R, Y, 4><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  else if (vec && h == 256) residual_ln_vec_kernel<R, Y, 2><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  else if (vec && h == 128) residual_ln_vec_kernel<R, Y, 1><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  else if (per <= 1) residual_ln_kernel<R, Y, 1><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  else if (per <= 4) residual_ln_kernel<R, Y, 4><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  else if (per <= 8) residual_ln_kernel<R, Y, 8><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  else if (per <= 24) residual_ln_kernel<R, Y, 24><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  else if (per <= 32) residual_ln_kernel<R, Y, 32><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  else residual_ln_big_kernel<R, Y><<<rows, 256, 0, st>>>(SC_LN_ARGS);
+#undef SC_LN_ARGS
+  SC_CHECK_LAUNCH("residual_ln_kernel");
+  return SC_OK;
 }
 
 __device__ __forceinline__ float gelu_erf(float x) {
@@ -243,25 +296,31 @@ __device__ __forceinline__ void gelu_bf16x8(uint4& u, const float* __restrict__ 
   }
 }
 
-// Two 16-byte vectors per thread per iteration (more loads in flight).
+// Four 16-byte vectors per thread per iteration, all loads issued before any
+// math: ~48 KB of loads in flight per SM at 4 CTAs x 256 threads, enough to
+// cover HBM latency (2 vectors/thread at 3 CTAs/SM measured 74% of copy BW,
+// stalled on long scoreboard).
 template <bool kBias>
-__global__ void __launch_bounds__(256) bias_gelu_bf16x8_kernel(__nv_bfloat16* __restrict__ x,
-                                                              const float* __restrict__ bias, int64_t n8,
-                                                              int cols) {
+__global__ void __launch_bounds__(256, 4) bias_gelu_bf16x8_kernel(__nv_bfloat16* __restrict__ x,
+                                                                 const float* __restrict__ bias, int64_t n8,
+                                                                 int cols) {
+  constexpr int U = 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   uint4* xv = reinterpret_cast<uint4*>(x);
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; i + stride < n8; i += 2 * stride) {
-    uint4 u0 = xv[i], u1 = xv[i + stride];
-    gelu_bf16x8<kBias>(u0, bias, i, cols);
-    gelu_bf16x8<kBias>(u1, bias, i + stride, cols);
-    xv[i] = u0;
-    xv[i + stride] = u1;
+  for (; i + (U - 1) * stride < n8; i += U * stride) {
+    uint4 u[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) u[k] = __ldcs(xv + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < U; ++k) gelu_bf16x8<kBias>(u[k], bias, i + k * stride, cols);
+#pragma unroll
+    for (int k = 0; k < U; ++k) __stcs(xv + i + k * stride, u[k]);
   }
-  if (i < n8) {
-    uint4 u = xv[i];
-    gelu_bf16x8<kBias>(u, bias, i, cols);
-    xv[i] = u;
+  for (; i < n8; i += stride) {
+    uint4 v = xv[i];
+    gelu_bf16x8<kBias>(v, bias, i, cols);
+    xv[i] = v;
   }
 }
 
@@ -285,32 +344,6 @@ __global__ void nonfinite_kernel(const float* __restrict__ x, int64_t n, int32_t
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicAdd(count, 1);
 }
 
-template <typename Y>
-int launch_ln(const float* resid, const void* y, const float* bias, const float* gamma,
-              const float* beta, float* out, void* out_h, int rows, int h, cudaStream_t st) {
-  const Y* yy = static_cast<const Y*>(y);
-  __nv_bfloat16* oh = static_cast<__nv_bfloat16*>(out_h);
-  unsigned blocks = (unsigned)((rows + 7) / 8);
-  int per = (h + 31) / 32;
-  const bool vec = (h % 128 == 0) && !(((uintptr_t)resid | (uintptr_t)y | (uintptr_t)out |
-                                         (uintptr_t)out_h | (uintptr_t)gamma | (uintptr_t)beta |
-                                         (uintptr_t)bias) & 15);
-  if (vec && h == 768) residual_ln_vec_kernel<Y, 6><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
-  else if (vec && h == 384) residual_ln_vec_kernel<Y, 3><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
-  else if (vec && h == 1024) residual_ln_vec_kernel<Y, 8><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
-  else if (vec && h == 512) residual_ln_vec_kernel<Y, 4><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
-  else if (vec && h == 256) residual_ln_vec_kernel<Y, 2><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
-  else if (vec && h == 128) residual_ln_vec_kernel<Y, 1><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
-  else if (per <= 1) residual_ln_kernel<Y, 1><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
-  else if (per <= 4) residual_ln_kernel<Y, 4><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
-  else if (per <= 8) residual_ln_kernel<Y, 8><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
-  else if (per <= 24) residual_ln_kernel<Y, 24><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
-  else if (per <= 32) residual_ln_kernel<Y, 32><<<blocks, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
-  else residual_ln_big_kernel<Y><<<rows, 256, 0, st>>>(resid, yy, bias, gamma, beta, out, oh, rows, h);
-  SC_CHECK_LAUNCH("residual_ln_kernel");
-  return SC_OK;
-}
-
 }  // namespace sc
 
 using namespace sc;
@@ -318,7 +351,7 @@ using namespace sc;
 extern "C" int sc_embed(const int32_t* ids, const int32_t* tok_pos, const float* tok_emb,
                         const float* pos_emb, float* x, void* xh, int32_t total_tokens,
                         int32_t hidden, void* stream) {
-  SC_CHECK_ARG(ids && tok_pos && tok_emb && pos_emb && x, "sc_embed: null pointer");
+  SC_CHECK_ARG(ids && tok_pos && tok_emb && pos_emb && (x || xh), "sc_embed: null pointer");
   SC_CHECK_ARG(total_tokens >= 0 && hidden >= 1, "sc_embed: bad shape");
   if (total_tokens == 0) return SC_OK;
   int threads = hidden >= 256 ? 256 : 32 * ((hidden + 31) / 32);
@@ -328,18 +361,33 @@ extern "C" int sc_embed(const int32_t* ids, const int32_t* tok_pos, const float*
   return SC_OK;
 }
 
+extern "C" int sc_residual_layernorm_ex(const void* resid, int32_t resid_dtype, const void* y,
+                                        int32_t y_dtype, const float* bias, const float* gamma,
+                                        const float* beta, float* x_out, void* out_h,
+                                        int32_t* nonfinite_count, int32_t rows, int32_t hidden,
+                                        void* stream) {
+  SC_CHECK_ARG(resid && y && gamma && beta && (x_out || out_h), "sc_residual_layernorm: null pointer");
+  SC_CHECK_ARG(rows >= 0 && hidden >= 1, "sc_residual_layernorm: bad shape");
+  SC_CHECK_ARG(resid_dtype == SC_DTYPE_F32 || resid_dtype == SC_DTYPE_BF16, "sc_residual_layernorm: bad resid dtype %d", resid_dtype);
+  SC_CHECK_ARG(y_dtype == SC_DTYPE_F32 || y_dtype == SC_DTYPE_BF16, "sc_residual_layernorm: bad dtype %d", y_dtype);
+  if (rows == 0) return SC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const float* b = bias;
+  if (resid_dtype == SC_DTYPE_F32) {
+    if (y_dtype == SC_DTYPE_F32) return launch_ln<float, float>(resid, y, b, gamma, beta, x_out, out_h, nonfinite_count, rows, hidden, st);
+    return launch_ln<float, __nv_bfloat16>(resid, y, b, gamma, beta, x_out, out_h, nonfinite_count, rows, hidden, st);
+  }
+  if (y_dtype == SC_DTYPE_F32) return launch_ln<__nv_bfloat16, float>(resid, y, b, gamma, beta, x_out, out_h, nonfinite_count, rows, hidden, st);
+  return launch_ln<__nv_bfloat16, __nv_bfloat16>(resid, y, b, gamma, beta, x_out, out_h, nonfinite_count, rows, hidden, st);
+}
+
 extern "C" int sc_residual_layernorm(const float* resid, const void* y, int32_t y_dtype,
                                      const float* bias, const float* gamma, const float* beta,
                                      float* x_out, void* out_h, int32_t rows, int32_t hidden,
                                      void* stream) {
-  SC_CHECK_ARG(resid && y && gamma && beta && x_out, "sc_residual_layernorm: null pointer");
-  SC_CHECK_ARG(rows >= 0 && hidden >= 1, "sc_residual_layernorm: bad shape");
-  if (rows == 0) return SC_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (y_dtype == SC_DTYPE_F32) return launch_ln<float>(resid, y, bias, gamma, beta, x_out, out_h, rows, hidden, st);
-  if (y_dtype == SC_DTYPE_BF16) return launch_ln<__nv_bfloat16>(resid, y, bias, gamma, beta, x_out, out_h, rows, hidden, st);
-  set_error("sc_residual_layernorm: bad dtype %d", y_dtype);
-  return SC_ERR_INVALID;
+  SC_CHECK_ARG(x_out, "sc_residual_layernorm: null pointer");
+  return sc_residual_layernorm_ex(resid, SC_DTYPE_F32, y, y_dtype, bias, gamma, beta, x_out, out_h, nullptr,
+                                  rows, hidden, stream);
 }
 
 extern "C" int sc_bias_gelu(void* x, const float* bias, int32_t dtype, int64_t rows, int32_t cols,
@@ -350,7 +398,7 @@ extern "C" int sc_bias_gelu(void* x, const float* bias, int32_t dtype, int64_t r
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == SC_DTYPE_BF16 && cols % 8 == 0 && ((uintptr_t)x & 15) == 0) {
     int64_t n8 = n / 8;
-    unsigned blocks = grid_cap(n8, 16);
+    unsigned blocks = grid_cap((n8 + 3) / 4, 4);
     if (bias)
       bias_gelu_bf16x8_kernel<true><<<blocks, 256, 0, st>>>((__nv_bfloat16*)x, bias, n8, cols);
     else

@@ -12,8 +12,10 @@ Per layer (post-LN BERT, R/encoder.py:306-371):
     x1  = LN(x + o @ Wo + bo)         cuBLAS + sc_residual_layernorm
     f   = gelu_erf(x1 @ W1 + b1)      cuBLAS + sc_bias_gelu
     x   = LN(x1 + f @ W2 + b2)        cuBLAS + sc_residual_layernorm
-The residual stream stays fp32 in both precisions; bf16 mode feeds bf16
-copies to the GEMMs and the attention.
+The fp32 path keeps an fp32 residual stream; the bf16 path keeps it in bf16
+(the GEMM inputs are bf16 anyway), with fp32 statistics inside the LayerNorm
+and an fp32 copy of the final layer for the score head.  The per-layer finite
+check (R/encoder.py:356-357) is fused into the second LayerNorm.
 """
 
 from __future__ import annotations
@@ -338,19 +340,26 @@ class CrossEncoder:
         dev = self.device
         pattern = make_pattern(cfg.pattern, cfg.window)
         stream = _lib.stream_handle()
+        # Residual stream: fp32 in the fp32 path; bf16 in the bf16 path (LN reads
+        # and writes 2-byte rows), with the final layer's LN also writing fp32 x.
         x = torch.empty((T, h), dtype=torch.float32, device=dev)
-        xh = torch.empty((T, h), dtype=cd, device=dev) if bf16 else None
-        x1 = torch.empty_like(x)
-        x1h = torch.empty_like(xh) if bf16 else None
+        if bf16:
+            xh = torch.empty((T, h), dtype=cd, device=dev)
+            x1 = torch.empty_like(xh)
+        else:
+            xh, x1 = None, torch.empty_like(x)
+        rdt = _lib.DTYPE_BF16 if bf16 else _lib.DTYPE_F32
         bad = torch.zeros(max(cfg.layers, 1), dtype=torch.int32, device=dev)
         _lib.call("sc_embed", ids_dev.data_ptr(), layout.tok_pos.data_ptr(), self.tok_emb.data_ptr(),
-                  self.pos_emb.data_ptr(), x.data_ptr(), _lib.ptr(xh), T, h, stream, exc=EncoderError)
+                  self.pos_emb.data_ptr(), x.data_ptr() if (not bf16 or cfg.layers == 0) else None,
+                  _lib.ptr(xh), T, h, stream, exc=EncoderError)
         dcode = _lib.DTYPE_BF16 if bf16 else _lib.DTYPE_F32
         o = torch.empty((T, h), dtype=cd, device=dev)
+        last = cfg.layers - 1
         with _fp32_gemms(not bf16):
             for i, L in enumerate(self.layers):
-                xin = xh if bf16 else x
-                qkv = F.linear(xin, L["wqkv"], L["bqkv"])
+                xr = xh if bf16 else x  # residual stream (and GEMM input) of this layer
+                qkv = F.linear(xr, L["wqkv"], L["bqkv"])
                 if attn_hook:
                     attn_hook("start")
                 attend_packed(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], layout, pattern, H,
@@ -359,17 +368,16 @@ class CrossEncoder:
                 if attn_hook:
                     attn_hook("end")
                 y = F.linear(o, L["wo"], L["bo"])
-                _lib.call("sc_residual_layernorm", x.data_ptr(), y.data_ptr(), dcode, None,
-                          L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), x1.data_ptr(), _lib.ptr(x1h),
-                          T, h, stream, exc=EncoderError)
-                f = F.linear(x1h if bf16 else x1, L["w1"], L["b1"])
+                _lib.call("sc_residual_layernorm_ex", xr.data_ptr(), rdt, y.data_ptr(), dcode, None,
+                          L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), None if bf16 else x1.data_ptr(),
+                          x1.data_ptr() if bf16 else None, None, T, h, stream, exc=EncoderError)
+                f = F.linear(x1, L["w1"], L["b1"])
                 _lib.call("sc_bias_gelu", f.data_ptr(), None, dcode, T, cfg.ff_dim, stream, exc=EncoderError)
                 f2 = F.linear(f, L["w2"], L["b2"])
-                _lib.call("sc_residual_layernorm", x1.data_ptr(), f2.data_ptr(), dcode, None,
-                          L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(), x.data_ptr(), _lib.ptr(xh),
-                          T, h, stream, exc=EncoderError)
-                if check_finite:
-                    _lib.call("sc_count_nonfinite", x.data_ptr(), x.numel(), bad[i:].data_ptr(), stream)
+                _lib.call("sc_residual_layernorm_ex", x1.data_ptr(), rdt, f2.data_ptr(), dcode, None,
+                          L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(),
+                          x.data_ptr() if (not bf16 or i == last) else None, _lib.ptr(xh),
+                          bad.data_ptr() + 4 * i if check_finite else None, T, h, stream, exc=EncoderError)
         self._last_bad = bad if check_finite else None
         return x
 

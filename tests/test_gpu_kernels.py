@@ -87,3 +87,41 @@ def test_kernel_launch_counter(lib):
     x[3] = float("nan")
     lib.call("sc_count_nonfinite", x.data_ptr(), 10, cnt.data_ptr(), lib.stream_handle())
     assert cnt.item() > 0
+
+
+@pytest.mark.parametrize("rdtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("h", [768, 100, 2048])
+def test_residual_layernorm_ex(lib, rdtype, h):
+    """bf16 / fp32 residual, each output optional, fused non-finite flag."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    rows = 777
+    resid = torch.randn((rows, h), device="cuda", generator=g).to(rdtype)
+    y = torch.randn((rows, h), device="cuda", generator=g).to(torch.bfloat16)
+    gamma = torch.randn(h, device="cuda", generator=g)
+    beta = torch.randn(h, device="cuda", generator=g)
+    ref = torch.nn.functional.layer_norm(resid.float() + y.float(), (h,), gamma, beta, eps=1e-12)
+    rd = 0 if rdtype == torch.float32 else 1
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = torch.empty((rows, h), device="cuda")
+    lib.call("sc_residual_layernorm_ex", resid.data_ptr(), rd, y.data_ptr(), 1, None, gamma.data_ptr(),
+             beta.data_ptr(), out.data_ptr(), None, bad.data_ptr(), rows, h, lib.stream_handle())
+    torch.testing.assert_close(out, ref, atol=2e-5, rtol=1e-5)
+    assert bad.item() == 0
+    # bf16-only output written in place over a bf16 residual
+    if rdtype == torch.bfloat16:
+        inplace = resid.clone()
+        lib.call("sc_residual_layernorm_ex", inplace.data_ptr(), 1, y.data_ptr(), 1, None, gamma.data_ptr(),
+                 beta.data_ptr(), None, inplace.data_ptr(), bad.data_ptr(), rows, h, lib.stream_handle())
+        # identical arithmetic to the fp32-output call above: bitwise its bf16 rounding
+        torch.testing.assert_close(inplace, out.to(torch.bfloat16), atol=0, rtol=0)
+    # a NaN / Inf in one row is counted
+    y2 = y.clone()
+    y2[5, 3] = float("nan")
+    y2[600, h - 1] = float("inf")
+    lib.call("sc_residual_layernorm_ex", resid.data_ptr(), rd, y2.data_ptr(), 1, None, gamma.data_ptr(),
+             beta.data_ptr(), out.data_ptr(), None, bad.data_ptr(), rows, h, lib.stream_handle())
+    torch.cuda.synchronize()
+    assert bad.item() >= 2
+    with pytest.raises(ValueError):
+        lib.call("sc_residual_layernorm_ex", resid.data_ptr(), rd, y.data_ptr(), 1, None, gamma.data_ptr(),
+                 beta.data_ptr(), None, None, None, rows, h, lib.stream_handle())
