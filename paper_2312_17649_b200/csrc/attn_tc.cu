@@ -22,22 +22,17 @@
 namespace sc {
 namespace tck {
 
-#ifndef SC_TC_BN
-#define SC_TC_BN 64
-#endif
-// BN-key blocks (64: two CTAs per SM, each with a double-buffered S).
-constexpr int BM = 128, D = 64, BN = SC_TC_BN, GR = 32;
+constexpr int BM = 128, D = 64;
 constexpr int NTHREADS = 192;
 constexpr int S_COL = 0;
-// NBUF S/P buffers in TMEM.  NBUF = 2 lets QK(b+2) overlap softmax(b+1) (wins
-// for long key ranges); NBUF = 1 keeps TMEM at 128 columns and registers low
-// enough for 3 CTAs per SM (wins for mid windows with few blocks per CTA).
-template <int NBUF>
+// Kernel configuration.  NBUF S/P buffers of BN key columns in TMEM (NBUF = 2
+// lets QK(b+2) overlap softmax(b+1)); GR global (cls + query) key rows; CTAS
+// resident CTAs per SM (TMEM NBUF*BN + D columns each); NS K/V ring stages.
+template <int NBUF_, int BN_, int GR_, int CTAS_, int NS_>
 struct Cfg {
-  static constexpr int NS = NBUF == 2 ? 4 : 2;  // K/V ring stages
+  static constexpr int NBUF = NBUF_, BN = BN_, GR = GR_, CTAS = CTAS_, NS = NS_;
   static constexpr int TMEM_COLS = NBUF * BN + D <= 128 ? 128 : (NBUF * BN + D <= 256 ? 256 : 512);
   static constexpr int O_COL = NBUF * BN;
-  static constexpr int CTAS = NBUF == 2 ? 2 : 3;
 };
 constexpr int ROWB = 128;
 
@@ -164,6 +159,41 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Max of NC raw logits (as bits) with independent 3-input max chains.
+template <int NC>
+__device__ __forceinline__ float row_max(const uint32_t (&v)[NC]) {
+  float a = -INFINITY, b = -INFINITY, c = -INFINITY, d = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < NC; e += 8) {
+    a = fmaxf(a, fmaxf(__uint_as_float(v[e + 0]), __uint_as_float(v[e + 1])));
+    b = fmaxf(b, fmaxf(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3])));
+    c = fmaxf(c, fmaxf(__uint_as_float(v[e + 4]), __uint_as_float(v[e + 5])));
+    d = fmaxf(d, fmaxf(__uint_as_float(v[e + 6]), __uint_as_float(v[e + 7])));
+  }
+  return fmaxf(fmaxf(a, b), fmaxf(c, d));
+}
+
+// P = exp2(v * c2 - base) for NC logits (FFMA2 for the argument pairs):
+// packed bf16 pairs written over v[0..NC/2), returns the fp32 row sum.
+// (An FA4-style polynomial exp2 on the FMA pipe for part of the columns was
+// measured slower at d = 64 for every split tried: the softmax here is
+// latency-bound, not MUFU-bound.)
+template <int NC>
+__device__ __forceinline__ float row_exp_pack(uint32_t (&v)[NC], float c2, float base) {
+  const float2 c2v = make_float2(c2, c2), nb = make_float2(-base, -base);
+  float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int e = 0; e < NC; e += 2) {
+    const float2 a = __ffma2_rn(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), c2v, nb);
+    const float2 pr = make_float2(ex2(a.x), ex2(a.y));
+    if ((e >> 1) & 1) s1 = __fadd2_rn(s1, pr);
+    else s0 = __fadd2_rn(s0, pr);
+    v[e / 2] = pack_bf16(pr.x, pr.y);
+  }
+  const float2 t = __fadd2_rn(s0, s1);
+  return t.x + t.y;
+}
+
 // Row softmax of NC raw logits held as bits in v (masked entries = -inf):
 // updates the running max m, returns alpha = exp2((m_old - m_new) c2) and the
 // row sum of P, and writes P (bf16 pairs, packed in place) to TMEM at p_addr.
@@ -191,27 +221,27 @@ __device__ __forceinline__ void row_softmax(uint32_t (&v)[NC], float c2, float& 
   for (int c = 0; c < NC / 2; c += 16) TC_ST16(p_addr + c, (&v[c]));
 }
 
-template <int NS>
+template <class C>
 struct Smem {
   // offsets (bytes) from the 1024-aligned base
   static constexpr int Q = 0;
   static constexpr int KG = Q + BM * ROWB;
-  static constexpr int VG = KG + GR * ROWB;
-  static constexpr int KV = VG + GR * ROWB;  // NS x (K block, V block)
-  static constexpr int STAGE = 2 * BN * ROWB;
-  static constexpr int BAR = KV + NS * STAGE;
+  static constexpr int VG = KG + C::GR * ROWB;
+  static constexpr int KV = VG + C::GR * ROWB;  // NS x (K block, V block)
+  static constexpr int STAGE = 2 * C::BN * ROWB;
+  static constexpr int BAR = KV + C::NS * STAGE;
   // barriers: qbar, full[NS], empty[NS], s_full[2], p_full[2], pv_done[2], o_final; tmem holder
   static constexpr int TOTAL = BAR + 16 * 8 + 16;
 };
 
-template <int NBUF>
-__global__ void __launch_bounds__(NTHREADS, Cfg<NBUF>::CTAS) tc_attn_kernel(
+template <class C>
+__global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKg,
     const __grid_constant__ CUtensorMap tmVg, const __grid_constant__ CUtensorMap tmK,
     const __grid_constant__ CUtensorMap tmV, Params p) {
-  using C = Cfg<NBUF>;
-  using SM = Smem<C::NS>;
-  constexpr int NS = C::NS, O_COL = C::O_COL, TMEM_COLS = C::TMEM_COLS;
+  using SM = Smem<C>;
+  constexpr int NS = C::NS, O_COL = C::O_COL, TMEM_COLS = C::TMEM_COLS, NBUF = C::NBUF, BN = C::BN,
+                GR = C::GR;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tile = blockIdx.x, h = blockIdx.y;
@@ -375,9 +405,7 @@ __global__ void __launch_bounds__(NTHREADS, Cfg<NBUF>::CTAS) tc_attn_kernel(
           }
         }
       }
-      float mx = -INFINITY;
-#pragma unroll
-      for (int e = 0; e < BN; ++e) mx = fmaxf(mx, __uint_as_float(v[e]));
+      const float mx = row_max<BN>(v);
       const bool grow = mx > m + tau || (m == -INFINITY && mx != -INFINITY);
       float alpha = 1.f;
       if (__any_sync(0xffffffffu, grow)) {
@@ -399,18 +427,10 @@ __global__ void __launch_bounds__(NTHREADS, Cfg<NBUF>::CTAS) tc_attn_kernel(
         }
       }
       const float base = m == -INFINITY ? 0.f : m * c2;
-      float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-      for (int e = 0; e < BN; e += 2) {
-        const float p0 = ex2(fmaf(__uint_as_float(v[e]), c2, -base));
-        const float p1 = ex2(fmaf(__uint_as_float(v[e + 1]), c2, -base));
-        s0 += p0;
-        s1 += p1;
-        v[e / 2] = pack_bf16(p0, p1);
-      }
+      const float rs = row_exp_pack<BN>(v, c2, base);
 #pragma unroll
       for (int c = 0; c < BN / 2; c += 16) TC_ST16(sa + c, (&v[c]));
-      l = fmaf(l, alpha, s0 + s1);
+      l = fmaf(l, alpha, rs);
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -495,25 +515,36 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t row
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int NBUF>
-static int launch_kernel(dim3 grid, const CUtensorMap& mQ, const CUtensorMap& mKg, const CUtensorMap& mVg,
-                         const CUtensorMap& mK, const CUtensorMap& mV, const Params& p, cudaStream_t st) {
-  const size_t smem = Smem<Cfg<NBUF>::NS>::TOTAL + 1024;
+template <class C>
+static int launch_kernel(dim3 grid, const CUtensorMap* maps, const Params& p, cudaStream_t st) {
+  const size_t smem = Smem<C>::TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
     // several CTAs per SM: ask for the full shared-memory carveout
-    cudaFuncSetAttribute(tc_attn_kernel<NBUF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (cudaFuncSetAttribute(tc_attn_kernel<NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    cudaFuncSetAttribute(tc_attn_kernel<C>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (cudaFuncSetAttribute(tc_attn_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess) {
       set_error("tcgen05 kernel: shared memory request of %zu bytes failed", smem);
       return SC_ERR_UNSUPPORTED;
     }
     attr = true;
   }
-  tc_attn_kernel<NBUF><<<grid, NTHREADS, smem, st>>>(mQ, mKg, mVg, mK, mV, p);
+  tc_attn_kernel<C><<<grid, NTHREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
   SC_CHECK_LAUNCH("tc_attn_kernel");
   return SC_OK;
 }
+
+// Variants (NBUF, BN, GR, CTAS, NS), measured on B200 at s=4099, H=12, 64 sequences
+// (us per sequence-layer, w = 64 / 256 / inf):
+//   VLONG  2 x 64-key S buffers, 2 CTAs/SM                 17.8 / 23.3 / 75.5
+//   VMID   2 x 32-key S buffers, 4 CTAs/SM, <= 15 globals   14.7 / 20.8 / 77.0
+//   VMID32 the same with 32 global rows                     15.1 / 22.9 / 110
+// (single-buffered S at 3-4 CTAs/SM: 19.0 / 26.8 / 94.6).  Four short
+// softmax chains per SM beat two long ones until the key range is the whole
+// document.
+using VLONG = Cfg<2, 64, 32, 2, 4>;
+using VMID = Cfg<2, 32, 16, 4, 3>;
+using VMID32 = Cfg<2, 32, 32, 4, 2>;
 
 }  // namespace tck
 
@@ -535,7 +566,7 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   if (w == SC_LINK_NONE) return unsupported("doc rows must attend doc keys");
   if (L.w[2][0] != SC_LINK_FULL && L.w[2][0] != SC_LINK_NONE) return unsupported("windowed doc->cls");
   if (L.w[2][1] != SC_LINK_FULL && L.w[2][1] != SC_LINK_NONE) return unsupported("windowed doc->query");
-  if (max_qgroup_len + 1 > GR) return unsupported("query group longer than 31 rows");
+  if (max_qgroup_len + 1 > 32) return unsupported("query group longer than 31 rows");
   // head rows go through the band kernel's head-rows-only mode: same link envelope
   for (int x : {L.w[0][0], L.w[0][1], L.w[0][2], L.w[1][0], L.w[1][1], L.w[1][2]})
     if (x != SC_LINK_FULL && x != SC_LINK_NONE) return unsupported("windowed head-row link");
@@ -546,11 +577,23 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   const size_t band_bytes = (band_workspace_bytes(a.nseq, a.T, a.H, a.d, tile_rows, max_qgroup_len, L) + 255) & ~size_t(255);
   if (!ws || ws_bytes < band_bytes + tc_workspace_bytes(a.nseq)) return unsupported("workspace too small");
 
-  CUtensorMap mQ, mKg, mVg, mK, mV;
+  // Variant choice (env SC_TC_VARIANT = 0/1/2 forces VLONG/VMID/VMID32, for measurement sweeps).
+  static int forced = -2;
+  if (forced == -2) {
+    const char* e = getenv("SC_TC_VARIANT");
+    forced = e ? atoi(e) : -1;
+  }
+  const bool long_range = w == SC_LINK_FULL || w > 256;
+  const bool small_gr = max_qgroup_len + 1 <= 16;
+  int var = forced >= 0 ? forced : (long_range ? 0 : (small_gr ? 1 : 2));
+  if (var == 1 && !small_gr) var = 2;
+  const int bn = var == 0 ? 64 : 32;
+  const int gr = var == 1 ? 16 : 32;
+  CUtensorMap maps[5];
   const int64_t cols = (int64_t)a.H * D;
-  if (!make_map(&mQ, a.q, cols, a.T, a.ld, BM) || !make_map(&mKg, a.k, cols, a.T, a.ld, GR) ||
-      !make_map(&mVg, a.v, cols, a.T, a.ld, GR) || !make_map(&mK, a.k, cols, a.T, a.ld, BN) ||
-      !make_map(&mV, a.v, cols, a.T, a.ld, BN))
+  if (!make_map(&maps[0], a.q, cols, a.T, a.ld, BM) || !make_map(&maps[1], a.k, cols, a.T, a.ld, gr) ||
+      !make_map(&maps[2], a.v, cols, a.T, a.ld, gr) || !make_map(&maps[3], a.k, cols, a.T, a.ld, bn) ||
+      !make_map(&maps[4], a.v, cols, a.T, a.ld, bn))
     return unsupported("cuTensorMapEncodeTiled failed");
 
   int32_t* tbase = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + band_bytes);
@@ -564,11 +607,9 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   p.cu = a.cu; p.qlen = a.qlen; p.tile_base = tbase;
   p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
   dim3 grid((unsigned)((a.T + BM - 1) / BM + a.nseq), (unsigned)a.H);
-  // Double-buffer S when a row tile sweeps many key blocks (measured crossover:
-  // single buffer + 3 CTAs/SM is faster up to w = 256, double buffer for w = inf).
-  const bool long_range = w == SC_LINK_FULL || w > 256;
-  const int rc = long_range ? launch_kernel<2>(grid, mQ, mKg, mVg, mK, mV, p, st)
-                            : launch_kernel<1>(grid, mQ, mKg, mVg, mK, mV, p, st);
+  const int rc = var == 0   ? launch_kernel<VLONG>(grid, maps, p, st)
+                 : var == 1 ? launch_kernel<VMID>(grid, maps, p, st)
+                            : launch_kernel<VMID32>(grid, maps, p, st);
   if (rc) return rc;
   // Head rows (cls + query group): the band kernel in head-rows-only mode
   // streams each doc key once for the CLS split-softmax records, then merges.

@@ -235,11 +235,12 @@ def test_band_kernel_repeatable_and_forced(P, name):
                                         ("sparse", 256, "zero-logit"), ("sparse", math.inf, "exclude"),
                                         ("longformer", 100, "exclude"), ("full", math.inf, "exclude"),
                                         ("longformer", 33, "zero-logit")])
-def test_tcgen05_kernel_vs_oracle(P, name, w, pad):
+@pytest.mark.parametrize("shapes", [[(10, 300), (1, 1), (7, 130), (30, 127), (10, 700)],  # 31-row query group
+                                    [(10, 300), (1, 1), (7, 130), (14, 127), (10, 700)]])  # <= 15 global rows
+def test_tcgen05_kernel_vs_oracle(P, name, w, pad, shapes):
     """The tcgen05/TMEM kernel (forced) on a packed varlen batch vs the oracle at bf16 tolerance."""
     rng = np.random.default_rng(17)
     H, d = 4, 64
-    shapes = [(10, 300), (1, 1), (7, 130), (30, 127), (10, 700)]
     seq = [m + n + 3 for m, n in shapes]
     lay = P.PackedLayout.from_lengths(seq, [m + 1 for m, _ in shapes], device="cuda")
     T = sum(seq)
