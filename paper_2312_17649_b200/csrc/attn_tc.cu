@@ -398,10 +398,16 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
         const bool interior =
             k0 + BN <= hi && (w < 0 || (k0 >= r0 + rows_here - 1 - w && k0 + BN - 1 <= r0 + w));
         if (!interior) {
+          // valid keys of this row in the block: e in [ea, eb) (band and document end)
+          const int ea = w < 0 ? 0 : min(max(rr - w - k0, 0), BN);
+          const int eb = max(min(min(hi, w < 0 ? hi : rr + w + 1) - k0, BN), ea);
 #pragma unroll
-          for (int e = 0; e < BN; ++e) {
-            const int t = k0 + e;
-            if (!(t < hi && (w < 0 || (t - rr <= w && rr - t <= w)))) v[e] = __float_as_uint(-INFINITY);
+          for (int c0 = 0; c0 < BN; c0 += 32) {
+            const int a = min(max(ea - c0, 0), 32), z = min(max(eb - c0, 0), 32);
+            const uint32_t keep = (z >= 32 ? 0xffffffffu : ((1u << z) - 1u)) & ~(a >= 32 ? 0xffffffffu : ((1u << a) - 1u));
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (!((keep >> e) & 1u)) v[c0 + e] = __float_as_uint(-INFINITY);
           }
         }
       }
