@@ -8,8 +8,8 @@ ELECTRA-base sparse cross-encoder (12 layers, h=768, 12 heads, ff=3072,
 vocab 30522, random-init weights with the reference's init_weights draw
 order), asymmetric pattern w=4, documents of 4096 tokens = q10 + d4086 + 3
 specials = s 4099 (T/test_bench.py:66-70), packed varlen batch of
-`--pairs-per-gpu` pairs per GPU, bf16 GEMMs/attention with an fp32 residual
-stream.  A "step" = one forward of the whole per-GPU batch (12 layers +
+`--pairs-per-gpu` pairs per GPU, bf16 GEMMs/attention/residual stream (fp32 LayerNorm
+statistics).  A "step" = one forward of the whole per-GPU batch (12 layers +
 scores) + one NCCL all-gather of the fp32 scores.
 
   python bench.py [--gpus N --steps K --warmup W]            # our arm
