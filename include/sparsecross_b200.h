@@ -121,6 +121,15 @@ SC_API size_t sc_attn_workspace_bytes(int32_t nseq, int32_t total_tokens, int32_
                                int32_t head_dim, int32_t tile_rows, int32_t max_qgroup_len,
                                const int32_t* links);
 
+/* The same for a batch with QDS global doc tokens (R/attention.py:403-470):
+ * adds room for n_global_tokens compact [q|k|v] rows (the dense global-key
+ * segment and the global rows' full attention run from that copy).  The
+ * workspace must be zero-filled before its first use (self-resetting
+ * counters live in it); sc_attn_fwd leaves it reusable. */
+SC_API size_t sc_attn_workspace_bytes_qds(int32_t nseq, int32_t total_tokens, int32_t heads,
+                               int32_t head_dim, int32_t tile_rows, int32_t max_qgroup_len,
+                               const int32_t* links, int32_t n_global_tokens);
+
 /* Attention of every token row of a packed batch under one pattern:
  * all three groups (cls, query, doc) of every sequence in one call.
  * q/k/v: row r, head h at base + r*row_stride + h*head_dim (elements of
@@ -129,9 +138,11 @@ SC_API size_t sc_attn_workspace_bytes(int32_t nseq, int32_t total_tokens, int32_
  * the logits (sqrt(d) in the encoder, R/encoder.py:329).  tok_* /
  * seq_tile_base / seq_head_base come from sc_index_build with the same
  * tile_rows; max_qgroup_len is the host-known max of qgroup_len (kernel
- * selection only).  algo picks the kernel (SC_ATTN_*); AUTO runs the tiled
- * band kernel (bf16, d = 64, finite doc window, no QDS) for doc rows plus the
- * head-row combine, else the generic kernel.
+ * selection only).  algo picks the kernel (SC_ATTN_*); AUTO runs, in bf16
+ * with d = 64: the tiled band kernel for doc windows <= 40 without QDS
+ * globals, else the tcgen05 kernel (wider or full windows, and QDS with its
+ * globals) -- each plus the head-row combine -- and the generic kernel for
+ * everything else (fp32, other head dims, windowed head-row links).
  * status (optional, device int32) gets bit0 set if a row had zero valid keys.
  * Replaces group_attention x3 (R/attention.py:416-473), apply_pattern
  * (:510-537), attend_segments (:290-345), masked_segment_softmax (:228-257)

@@ -55,7 +55,7 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
                      size_t ws_bytes, cudaStream_t st, bool doc_rows = true);
 
 // tcgen05 / TMEM kernel for wide bands and dense doc rows (attn_tc.cu).
-size_t tc_workspace_bytes(int nseq);
+size_t tc_workspace_bytes(int nseq, int H, int n_global);  // n_global: QDS global doc tokens
 int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
                    const int32_t* seq_head_base, int tile_rows, int max_qgroup_len, void* ws,
                    size_t ws_bytes, cudaStream_t st);

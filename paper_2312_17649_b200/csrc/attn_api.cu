@@ -4,14 +4,20 @@
 
 using namespace sc;
 
+extern "C" size_t sc_attn_workspace_bytes_qds(int32_t nseq, int32_t total_tokens, int32_t heads,
+                                              int32_t head_dim, int32_t tile_rows, int32_t max_qgroup_len,
+                                              const int32_t* links, int32_t n_global_tokens) {
+  Links L;
+  if (!load_links(links, &L) || n_global_tokens < 0) return 0;
+  const size_t band = band_workspace_bytes(nseq, total_tokens, heads, head_dim, tile_rows, max_qgroup_len, L);
+  // the tcgen05 path uses [band records | tile prefixes | QDS compact q/k/v rows]
+  return ((band + 255) & ~size_t(255)) + tc_workspace_bytes(nseq, heads, n_global_tokens);
+}
+
 extern "C" size_t sc_attn_workspace_bytes(int32_t nseq, int32_t total_tokens, int32_t heads,
                                           int32_t head_dim, int32_t tile_rows,
                                           int32_t max_qgroup_len, const int32_t* links) {
-  Links L;
-  if (!load_links(links, &L)) return 0;
-  const size_t band = band_workspace_bytes(nseq, total_tokens, heads, head_dim, tile_rows, max_qgroup_len, L);
-  // the tcgen05 path uses [band records | 128-row tile prefix]
-  return ((band + 255) & ~size_t(255)) + tc_workspace_bytes(nseq);
+  return sc_attn_workspace_bytes_qds(nseq, total_tokens, heads, head_dim, tile_rows, max_qgroup_len, links, 0);
 }
 
 // AUTO kernel choice by doc window: the mma.sync band kernel while the band is

@@ -776,7 +776,9 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   };
   if (dtype != SC_DTYPE_BF16) return unsupported("needs bf16");
   if (a.d != D) return unsupported("needs head_dim 64");
-  if (a.glob_cu) return unsupported("QDS global tokens");
+  // QDS head rows attend every key (like longformer), so head-rows-only mode
+  // ignores the globals; QDS doc rows need the tcgen05 kernel's dense segment.
+  if (a.glob_cu && doc_rows) return unsupported("QDS global tokens");
   if (w < 0 || w > MAX_W) return unsupported("doc->doc link must be a window <= 96");
   for (int x : {L.w[2][0], L.w[2][1], L.w[0][2], L.w[1][2], L.w[0][0], L.w[0][1], L.w[1][0], L.w[1][1]})
     if (x != SC_LINK_FULL && x != SC_LINK_NONE) return unsupported("windowed link outside doc->doc");

@@ -43,6 +43,15 @@ struct Params {
   const int32_t* cu;
   const int32_t* qlen;
   const int32_t* tile_base;  // 128-row doc tiles per sequence (prefix)
+  // QDS (R/attention.py:403-413, :434-470).  Doc-rows pass (qds = 1): a dense
+  // key segment over the sequence's global doc tokens (gathered into a compact
+  // [q|k|v] buffer) and band slots hitting a global excluded.  Global-rows pass
+  // (global_rows = 1): the global doc rows, queries from the compact buffer,
+  // attend every key; tile_base then counts 128-row tiles over the globals.
+  int qds, global_rows;
+  const uint8_t* flags;      // per-token QDS global flag (bit 0)
+  const int32_t* glob_cu;    // [nseq+1] prefix of global counts
+  const int32_t* glob_pos;   // doc-relative positions of the globals
   __nv_bfloat16* out;
   int64_t ld_out;
 };
@@ -238,7 +247,8 @@ template <class C>
 __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKg,
     const __grid_constant__ CUtensorMap tmVg, const __grid_constant__ CUtensorMap tmK,
-    const __grid_constant__ CUtensorMap tmV, Params p) {
+    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmKq,
+    const __grid_constant__ CUtensorMap tmVq, Params p) {
   using SM = Smem<C>;
   constexpr int NS = C::NS, O_COL = C::O_COL, TMEM_COLS = C::TMEM_COLS, NBUF = C::NBUF, BN = C::BN,
                 GR = C::GR;
@@ -250,15 +260,19 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
   const SeqGroups g = seq_groups(p.cu, p.qlen, j);
   const int n_doc = g.len[2];
   const int r0 = (tile - __ldg(p.tile_base + j)) * BM;
-  const int rows_here = min(BM, n_doc - r0);
+  const int gq0 = (p.qds || p.global_rows) ? __ldg(p.glob_cu + j) : 0;  // first compact row of seq j
+  const int n_gq = (p.qds || p.global_rows) ? __ldg(p.glob_cu + j + 1) - gq0 : 0;
+  const int rows_here = min(BM, (p.global_rows ? n_gq : n_doc) - r0);
   const int doc0 = g.start + g.off[2];
   const int G = 1 + g.len[1];
   const bool has_glob = (p.link_cls || p.link_query);
-  const int w = p.w;
+  const int w = p.global_rows ? -1 : p.w;
   const int lo = w < 0 ? 0 : max(0, r0 - w);
   const int hi = w < 0 ? n_doc : min(n_doc, r0 + rows_here + w);
-  const int nkb = (hi - lo + BN - 1) / BN;
-  const int nblocks = (has_glob ? 1 : 0) + nkb;  // block b: global block first, then doc key blocks
+  const int ngd = p.qds ? (n_gq + BN - 1) / BN : 0;  // key blocks over the compact QDS globals
+  const int nkb = ngd + (hi - lo + BN - 1) / BN;       // K/V ring blocks: QDS globals, then band
+  // block b: cls/query block first, then the ring blocks
+  const int nblocks = (has_glob ? 1 : 0) + nkb;
 
   const uint32_t sm0 = smem_u32(smem);
   const uint32_t bar0 = sm0 + SM::BAR;
@@ -300,7 +314,7 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
     if (lane == 0) {
       const int col = h * D;
       mbar_expect_tx(qbar, (BM + 2 * GR) * ROWB);
-      tma_load_2d(sm0 + SM::Q, &tmQ, col, doc0 + r0, qbar);
+      tma_load_2d(sm0 + SM::Q, &tmQ, col, p.global_rows ? gq0 + r0 : doc0 + r0, qbar);
       tma_load_2d(sm0 + SM::KG, &tmKg, col, g.start, qbar);
       tma_load_2d(sm0 + SM::VG, &tmVg, col, g.start, qbar);
       for (int kb = 0; kb < nkb; ++kb) {
@@ -308,8 +322,13 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
         if (kb >= NS) mbar_wait(empty_bar + 8 * s, ((kb / NS) & 1) ^ 1);
         mbar_expect_tx(full_bar + 8 * s, SM::STAGE);
         const uint32_t kbuf = sm0 + SM::KV + s * SM::STAGE;
-        tma_load_2d(kbuf, &tmK, col, doc0 + lo + kb * BN, full_bar + 8 * s);
-        tma_load_2d(kbuf + BN * ROWB, &tmV, col, doc0 + lo + kb * BN, full_bar + 8 * s);
+        if (kb < ngd) {
+          tma_load_2d(kbuf, &tmKq, col, gq0 + kb * BN, full_bar + 8 * s);
+          tma_load_2d(kbuf + BN * ROWB, &tmVq, col, gq0 + kb * BN, full_bar + 8 * s);
+        } else {
+          tma_load_2d(kbuf, &tmK, col, doc0 + lo + (kb - ngd) * BN, full_bar + 8 * s);
+          tma_load_2d(kbuf + BN * ROWB, &tmV, col, doc0 + lo + (kb - ngd) * BN, full_bar + 8 * s);
+        }
       }
     }
   } else if (warp == 5) {
@@ -393,10 +412,31 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
 #pragma unroll
         for (int e = 0; e < BN; ++e)
           if (!(e < GR && e < G && (e == 0 ? p.link_cls : p.link_query))) v[e] = __float_as_uint(-INFINITY);
+      } else if (b - (has_glob ? 1 : 0) < ngd) {
+        // QDS global-doc block: compact rows gq0 + kb*BN + e, valid while < n_gq
+        const int nval = n_gq - (b - (has_glob ? 1 : 0)) * BN;
+#pragma unroll
+        for (int e = 0; e < BN; ++e)
+          if (e >= nval) v[e] = __float_as_uint(-INFINITY);
       } else {
-        const int k0 = lo + (b - (has_glob ? 1 : 0)) * BN;
-        const bool interior =
+        const int k0 = lo + (b - (has_glob ? 1 : 0) - ngd) * BN;
+        bool interior =
             k0 + BN <= hi && (w < 0 || (k0 >= r0 + rows_here - 1 - w && k0 + BN - 1 <= r0 + w));
+        if (p.qds) {
+          // band slots that hit a global doc token are covered by the dense
+          // global segment: hard-excluded in both padding modes (R/attention.py:326-331)
+#pragma unroll
+          for (int c0 = 0; c0 < BN; c0 += 32) {
+            const int t = k0 + c0 + lane;
+            const uint32_t gm = __ballot_sync(0xffffffffu, t < n_doc && (__ldg(p.flags + doc0 + t) & 1));
+            if (gm) {
+              interior = false;
+#pragma unroll
+              for (int e = 0; e < 32; ++e)
+                if ((gm >> e) & 1u) v[c0 + e] = __float_as_uint(-INFINITY);
+            }
+          }
+        }
         if (!interior) {
           // valid keys of this row in the block: e in [ea, eb) (band and document end)
           const int ea = w < 0 ? 0 : min(max(rr - w - k0, 0), BN);
@@ -446,7 +486,8 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
     mbar_wait(o_final, 0);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* dst = p.out + (int64_t)(doc0 + rr) * p.ld_out + h * D;
+    const int orow = p.global_rows ? (r < rows_here ? __ldg(p.glob_pos + gq0 + rr) : 0) : rr;
+    __nv_bfloat16* dst = p.out + (int64_t)(doc0 + orow) * p.ld_out + h * D;
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 32) {
       uint32_t o[32];
@@ -474,15 +515,17 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
   }
 }
 
-// 128-row doc-tile prefix per sequence (single CTA scan).
+// 128-row tile prefix per sequence (single CTA scan): over the doc rows, or
+// (glob_cu != nullptr) over the QDS global doc rows.
 __global__ void tile128_prefix_kernel(const int32_t* __restrict__ cu, const int32_t* __restrict__ qlen, int nseq,
-                                      int32_t* __restrict__ base) {
+                                      const int32_t* __restrict__ glob_cu, int32_t* __restrict__ base) {
   __shared__ int32_t s[1024];
   int carry = 0;
   for (int b = 0; b < nseq; b += blockDim.x) {
     const int j = b + threadIdx.x;
     int n = 0;
-    if (j < nseq) n = (cu[j + 1] - cu[j] - 1 - qlen[j] + BM - 1) / BM;
+    if (j < nseq)
+      n = glob_cu ? (glob_cu[j + 1] - glob_cu[j] + BM - 1) / BM : (cu[j + 1] - cu[j] - 1 - qlen[j] + BM - 1) / BM;
     s[threadIdx.x] = n;
     __syncthreads();
     for (int o = 1; o < blockDim.x; o <<= 1) {
@@ -496,6 +539,27 @@ __global__ void tile128_prefix_kernel(const int32_t* __restrict__ cu, const int3
     __syncthreads();
   }
   if (threadIdx.x == 0) base[0] = 0;
+}
+
+// QDS: copy the q, k, v rows of every global doc token into the compact
+// [n_glob][q | k | v] buffer (one warp per row, 16-byte vectors).
+__global__ void qds_gather_kernel(const int32_t* __restrict__ cu, const int32_t* __restrict__ qlen, int nseq,
+                                  const int32_t* __restrict__ glob_cu, const int32_t* __restrict__ glob_pos,
+                                  const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
+                                  const __nv_bfloat16* __restrict__ v, int64_t ld, int hd, int cap,
+                                  __nv_bfloat16* __restrict__ dst, int32_t* __restrict__ status) {
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int total = __ldg(glob_cu + nseq);
+  if (i == 0 && lane == 0 && total > cap && status) *status = SC_ERR_INVALID;
+  if (i >= min(total, cap)) return;
+  const int j = find_seq(glob_cu, nseq, i);
+  const int64_t row = (int64_t)__ldg(cu + j) + 1 + __ldg(qlen + j) + __ldg(glob_pos + i);
+  const __nv_bfloat16* src[3] = {q + row * ld, k + row * ld, v + row * ld};
+  __nv_bfloat16* d = dst + (int64_t)i * 3 * hd;
+#pragma unroll
+  for (int part = 0; part < 3; ++part)
+    for (int c = lane * 8; c < hd; c += 256)
+      *reinterpret_cast<uint4*>(d + part * hd + c) = __ldg(reinterpret_cast<const uint4*>(src[part] + c));
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -535,7 +599,7 @@ static int launch_kernel(dim3 grid, const CUtensorMap* maps, const Params& p, cu
     }
     attr = true;
   }
-  tc_attn_kernel<C><<<grid, NTHREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
+  tc_attn_kernel<C><<<grid, NTHREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
   SC_CHECK_LAUNCH("tc_attn_kernel");
   return SC_OK;
 }
@@ -554,7 +618,11 @@ using VMID32 = Cfg<2, 32, 32, 4, 2>;
 
 }  // namespace tck
 
-size_t tc_workspace_bytes(int nseq) { return (size_t)(nseq + 1) * sizeof(int32_t); }
+// [doc-tile prefix | global-tile prefix] (+ the compact QDS [q|k|v] rows).
+static size_t tc_prefix_bytes(int nseq) { return ((size_t)2 * (nseq + 1) * sizeof(int32_t) + 255) & ~size_t(255); }
+size_t tc_workspace_bytes(int nseq, int H, int n_global) {
+  return tc_prefix_bytes(nseq) + (size_t)n_global * 3 * H * tck::D * sizeof(__nv_bfloat16);
+}
 
 int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
                    const int32_t* seq_head_base, int tile_rows, int max_qgroup_len, void* ws,
@@ -565,11 +633,13 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
     set_error("tcgen05 kernel: %s", why);
     return SC_ERR_UNSUPPORTED;
   };
+  const bool qds = a.glob_cu != nullptr;
   if (dtype != SC_DTYPE_BF16) return unsupported("needs bf16");
   if (a.d != D) return unsupported("needs head_dim 64");
-  if (a.glob_cu) return unsupported("QDS global tokens");
+  if (qds && (!a.flags || !a.glob_pos)) return unsupported("QDS needs tok_flags and glob_pos");
   const int w = L.w[2][2];
   if (w == SC_LINK_NONE) return unsupported("doc rows must attend doc keys");
+  if (qds && w == SC_LINK_FULL) return unsupported("QDS with a full doc->doc link");
   if (L.w[2][0] != SC_LINK_FULL && L.w[2][0] != SC_LINK_NONE) return unsupported("windowed doc->cls");
   if (L.w[2][1] != SC_LINK_FULL && L.w[2][1] != SC_LINK_NONE) return unsupported("windowed doc->query");
   if (max_qgroup_len + 1 > 32) return unsupported("query group longer than 31 rows");
@@ -579,9 +649,11 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   if (tile_rows != 64 || !seq_tile_base || !seq_head_base) return unsupported("layout tiles must be 64 rows");
   if (((uintptr_t)a.q | (uintptr_t)a.k | (uintptr_t)a.v | (uintptr_t)a.out) & 15) return unsupported("alignment");
   if ((a.ld * 2) % 16 || (a.ld_out * 2) % 16) return unsupported("row strides");
-  // workspace = [band-kernel records (head rows) | 128-row tile prefix]
+  // workspace = [band-kernel records (head rows) | tile prefixes | QDS compact rows]
   const size_t band_bytes = (band_workspace_bytes(a.nseq, a.T, a.H, a.d, tile_rows, max_qgroup_len, L) + 255) & ~size_t(255);
-  if (!ws || ws_bytes < band_bytes + tc_workspace_bytes(a.nseq)) return unsupported("workspace too small");
+  if (!ws || ws_bytes < band_bytes + tc_prefix_bytes(a.nseq)) return unsupported("workspace too small");
+  const size_t row_bytes = (size_t)3 * a.H * D * sizeof(__nv_bfloat16);
+  const int cap = qds ? (int)((ws_bytes - band_bytes - tc_prefix_bytes(a.nseq)) / row_bytes) : 0;
 
   // Variant choice (env SC_TC_VARIANT = 0/1/2 forces VLONG/VMID/VMID32, for measurement sweeps).
   static int forced = -2;
@@ -593,18 +665,43 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   const bool small_gr = max_qgroup_len + 1 <= 16;
   int var = forced >= 0 ? forced : (long_range ? 0 : (small_gr ? 1 : 2));
   if (var == 1 && !small_gr) var = 2;
-  const int bn = var == 0 ? 64 : 32;
-  const int gr = var == 1 ? 16 : 32;
-  CUtensorMap maps[5];
   const int64_t cols = (int64_t)a.H * D;
-  if (!make_map(&maps[0], a.q, cols, a.T, a.ld, BM) || !make_map(&maps[1], a.k, cols, a.T, a.ld, gr) ||
-      !make_map(&maps[2], a.v, cols, a.T, a.ld, gr) || !make_map(&maps[3], a.k, cols, a.T, a.ld, bn) ||
-      !make_map(&maps[4], a.v, cols, a.T, a.ld, bn))
-    return unsupported("cuTensorMapEncodeTiled failed");
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  int32_t* tbase = reinterpret_cast<int32_t*>(wsb + band_bytes);
+  int32_t* gtbase = tbase + a.nseq + 1;
+  __nv_bfloat16* compact = reinterpret_cast<__nv_bfloat16*>(wsb + band_bytes + tc_prefix_bytes(a.nseq));
+  const int64_t cld = 3 * cols;  // compact row stride (elements)
+  auto build_maps = [&](CUtensorMap* maps, int v, bool global_rows) {
+    const int bn = v == 0 ? 64 : 32, gr = v == 1 ? 16 : 32;
+    const int crow = cap > 0 ? cap : 1;
+    bool ok = global_rows ? make_map(&maps[0], compact, cols, crow, cld, BM) : make_map(&maps[0], a.q, cols, a.T, a.ld, BM);
+    ok = ok && make_map(&maps[1], a.k, cols, a.T, a.ld, gr) && make_map(&maps[2], a.v, cols, a.T, a.ld, gr) &&
+         make_map(&maps[3], a.k, cols, a.T, a.ld, bn) && make_map(&maps[4], a.v, cols, a.T, a.ld, bn);
+    if (qds) ok = ok && make_map(&maps[5], compact + cols, cols, crow, cld, bn) &&
+                  make_map(&maps[6], compact + 2 * cols, cols, crow, cld, bn);
+    else { maps[5] = maps[3]; maps[6] = maps[4]; }
+    return ok;
+  };
+  auto launch_var = [&](int v, dim3 grid, const CUtensorMap* maps, const Params& p) {
+    return v == 0 ? launch_kernel<VLONG>(grid, maps, p, st)
+         : v == 1 ? launch_kernel<VMID>(grid, maps, p, st)
+                  : launch_kernel<VMID32>(grid, maps, p, st);
+  };
 
-  int32_t* tbase = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + band_bytes);
-  tile128_prefix_kernel<<<1, 1024, 0, st>>>(a.cu, a.qlen, a.nseq, tbase);
+  tile128_prefix_kernel<<<1, 1024, 0, st>>>(a.cu, a.qlen, a.nseq, nullptr, tbase);
   SC_CHECK_LAUNCH("tile128_prefix_kernel");
+  if (qds) {
+    tile128_prefix_kernel<<<1, 1024, 0, st>>>(a.cu, a.qlen, a.nseq, a.glob_cu, gtbase);
+    SC_CHECK_LAUNCH("tile128_prefix_kernel");
+    if (cap > 0) {
+      qds_gather_kernel<<<(cap + 7) / 8, 256, 0, st>>>(a.cu, a.qlen, a.nseq, a.glob_cu, a.glob_pos,
+                                                       static_cast<const __nv_bfloat16*>(a.q),
+                                                       static_cast<const __nv_bfloat16*>(a.k),
+                                                       static_cast<const __nv_bfloat16*>(a.v), a.ld,
+                                                       (int)cols, cap, compact, a.status);
+      SC_CHECK_LAUNCH("qds_gather_kernel");
+    }
+  }
 
   Params p;
   p.nseq = a.nseq; p.H = a.H; p.w = w == SC_LINK_FULL ? -1 : w; p.padding = a.padding;
@@ -612,11 +709,22 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   p.c2 = 1.4426950408889634f / a.scale;
   p.cu = a.cu; p.qlen = a.qlen; p.tile_base = tbase;
   p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
-  dim3 grid((unsigned)((a.T + BM - 1) / BM + a.nseq), (unsigned)a.H);
-  const int rc = var == 0   ? launch_kernel<VLONG>(grid, maps, p, st)
-                 : var == 1 ? launch_kernel<VMID>(grid, maps, p, st)
-                            : launch_kernel<VMID32>(grid, maps, p, st);
+  p.qds = qds ? 1 : 0; p.global_rows = 0;
+  p.flags = a.flags; p.glob_cu = a.glob_cu; p.glob_pos = a.glob_pos;
+  CUtensorMap maps[7];
+  if (!build_maps(maps, var, false)) return unsupported("cuTensorMapEncodeTiled failed");
+  int rc = launch_var(var, dim3((unsigned)((a.T + BM - 1) / BM + a.nseq), (unsigned)a.H), maps, p);
   if (rc) return rc;
+  if (qds && cap > 0) {
+    // QDS global doc rows: every key of their sequence (R/attention.py:461-470)
+    Params pg = p;
+    pg.qds = 0; pg.global_rows = 1; pg.tile_base = gtbase; pg.link_cls = pg.link_query = 1;
+    const int vg = forced >= 0 ? var : 0;
+    CUtensorMap gmaps[7];
+    if (!build_maps(gmaps, vg, true)) return unsupported("cuTensorMapEncodeTiled failed");
+    rc = launch_var(vg, dim3((unsigned)((cap + BM - 1) / BM + a.nseq), (unsigned)a.H), gmaps, pg);
+    if (rc) return rc;
+  }
   // Head rows (cls + query group): the band kernel in head-rows-only mode
   // streams each doc key once for the CLS split-softmax records, then merges.
   return launch_attn_band(a, dtype, seq_tile_base, seq_head_base, tile_rows, max_qgroup_len, ws,

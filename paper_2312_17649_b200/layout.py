@@ -64,6 +64,11 @@ class PackedLayout:
                   _lib.ptr(self.glob_cu) if qds_positions is None else None,
                   _lib.ptr(self.glob_pos) if qds_positions is None else None,
                   _lib.stream_handle(), exc=LayoutError)
+        # host-side count of QDS global doc tokens (sizes the compact q/k/v copy)
+        self.n_global = 0
+        if self.qds_every:
+            doc_tokens = self.group_lens_host[:, 2] - 1  # the doc group minus its final [SEP]
+            self.n_global = int((doc_tokens // self.qds_every).sum())
         if qds_positions is not None:
             self._set_globals(qds_positions)
         self._ws = {}
@@ -83,6 +88,7 @@ class PackedLayout:
             pos += plist
             cu.append(len(pos))
         self.qds_every = -1  # marks "globals present, explicit list"
+        self.n_global = len(pos)
         self.tok_flags.copy_(torch.from_numpy(flags))
         self.glob_cu.copy_(torch.from_numpy(np.asarray(cu, np.int32)))
         if pos:
@@ -106,8 +112,9 @@ class PackedLayout:
     def attn_workspace(self, heads: int, head_dim: int, links: np.ndarray):
         key = (heads, head_dim, links.tobytes())
         if key not in self._ws:
-            n = _lib.load().sc_attn_workspace_bytes(self.nseq, self.total_tokens, heads, head_dim,
-                                                    self.tile_rows, self.max_qgroup_len, links.ctypes.data)
+            n = _lib.load().sc_attn_workspace_bytes_qds(self.nseq, self.total_tokens, heads, head_dim,
+                                                        self.tile_rows, self.max_qgroup_len, links.ctypes.data,
+                                                        self.n_global)
             # zeroed: the tail holds self-resetting per-sequence tile counters
             self._ws[key] = torch.zeros(n, dtype=torch.uint8, device=self.device) if n else None
         return self._ws[key]

@@ -23,11 +23,13 @@ def main():
     ap.add_argument("--patterns", default="sparse")
     ap.add_argument("--algo", default="auto")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--qds-every", type=int, default=30, help="QDS global-token spacing (pattern qds)")
     args = ap.parse_args()
     H, d, m = 12, 64, 10
     s = m + args.doc + 3
     T = s * args.nseq
     lay = P.PackedLayout.from_lengths([s] * args.nseq, [m + 1] * args.nseq)
+    lay_qds = None
     g = torch.Generator(device="cuda").manual_seed(0)
     qkv = torch.randn((T, 3 * H * d), device="cuda", generator=g).to(torch.bfloat16)
     out = torch.empty((T, H * d), device="cuda", dtype=torch.bfloat16)
@@ -36,7 +38,13 @@ def main():
         for ws in args.windows.split(","):
             w = math.inf if ws == "inf" else int(ws)
             pat = P.make_pattern(pname, w)
-            f = lambda: P.attend_packed(qkv[:, :H * d], qkv[:, H * d:2 * H * d], qkv[:, 2 * H * d:], lay, pat, H,
+            L = lay
+            if pname == "qds":  # global doc tokens every --qds-every positions (R/encoder.py:180-184)
+                if lay_qds is None:
+                    lay_qds = P.PackedLayout.from_lengths([s] * args.nseq, [m + 1] * args.nseq,
+                                                          qds_every=args.qds_every)
+                L = lay_qds
+            f = lambda: P.attend_packed(qkv[:, :H * d], qkv[:, H * d:2 * H * d], qkv[:, 2 * H * d:], L, pat, H,
                                         out=out, algo=args.algo, check=False)
             for _ in range(3):
                 f()

@@ -257,3 +257,29 @@ def test_tcgen05_kernel_vs_oracle(P, name, w, pad, shapes):
         ref = np.concatenate(O.apply_pattern(spans, O.split_groups(spans, *blk), opat, math.sqrt(d), pad), axis=-2)
         np.testing.assert_allclose(out[r:r + s].reshape(s, H, d).transpose(1, 0, 2), ref, atol=2e-2, rtol=0)
         r += s
+
+
+@pytest.mark.parametrize("w,pad", [(0, "exclude"), (4, "exclude"), (4, "zero-logit"), (64, "exclude"), (300, "zero-logit")])
+@pytest.mark.parametrize("algo", ["tc", "auto"])
+def test_qds_tcgen05_vs_oracle(P, w, pad, algo):
+    """QDS (R/attention.py:403-470) on the tcgen05 path: doc rows get the dense global-token segment
+    with band slots at globals excluded, global doc rows attend every key; packed varlen, bf16."""
+    rng = np.random.default_rng(29)
+    H, d, every = 4, 64, 30
+    shapes = [(10, 700), (1, 1), (7, 29), (3, 30), (14, 200), (10, 1000)]
+    seq = [m + n + 3 for m, n in shapes]
+    lay = P.PackedLayout.from_lengths(seq, [m + 1 for m, _ in shapes], device="cuda", qds_every=every)
+    T = sum(seq)
+    x = torch.from_numpy(rng.standard_normal((T, 3 * H * d)).astype(np.float32)).cuda().to(torch.bfloat16)
+    pat = P.make_pattern("qds", w)
+    out = P.attend_packed(x[:, :H * d], x[:, H * d:2 * H * d], x[:, 2 * H * d:], lay, pat, H, padding=pad,
+                          algo=algo).double().cpu().numpy()
+    xin = x.double().cpu().numpy().reshape(T, 3, H, d)
+    r = 0
+    for (m, n), s in zip(shapes, seq):
+        blk = xin[r:r + s].transpose(1, 2, 0, 3)
+        spans = cases.attn_spans(m, n)
+        opat = O.make_pattern("qds", w, O.qds_global_positions(n, every))
+        ref = np.concatenate(O.apply_pattern(spans, O.split_groups(spans, *blk), opat, math.sqrt(d), pad), axis=-2)
+        np.testing.assert_allclose(out[r:r + s].reshape(s, H, d).transpose(1, 0, 2), ref, atol=2e-2, rtol=0)
+        r += s
