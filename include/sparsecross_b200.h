@@ -64,6 +64,9 @@ extern "C" {
 #define SC_ATTN_GENERIC 1       /* warp-per-row CUDA-core kernel (any pattern)  */
 #define SC_ATTN_BAND_MMA 2      /* tiled band kernel (finite doc window)        */
 #define SC_ATTN_TC 3            /* tcgen05/TMEM kernel (wide or dense doc band) */
+#define SC_ATTN_HEAD_ROWS 4     /* only the cls + query-group rows of every sequence
+                                   (other rows untouched): a last layer whose only
+                                   consumer is the [CLS] score, R/encoder.py:506 */
 
 SC_API const char* sc_last_error(void);
 SC_API int sc_version(void);

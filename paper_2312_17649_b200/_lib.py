@@ -34,6 +34,7 @@ ALGO_AUTO = 0
 ALGO_GENERIC = 1
 ALGO_BAND_MMA = 2
 ALGO_TC = 3
+ALGO_HEAD_ROWS = 4
 
 _p = C.c_void_p
 _i32 = C.c_int32

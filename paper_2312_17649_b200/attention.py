@@ -154,12 +154,16 @@ def _dtype_code(t: torch.Tensor) -> int:
 def attend_packed(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: PackedLayout,
                   pattern: AttentionPattern, heads: int, scale: float | None = None,
                   padding: str = "exclude", out: torch.Tensor | None = None,
-                  algo: str = "auto", check: bool = True) -> torch.Tensor:
+                  algo: str = "auto", check: bool = True, rows: str = "all") -> torch.Tensor:
     """Pattern attention over every row of a packed batch (all groups, all sequences).
 
     q/k/v: [T, >=heads*d] views sharing a row stride (e.g. the thirds of a
     packed QKV projection [T, 3*heads*d]).  Returns out [T, heads*d].
+    rows="head" computes only the cls + query-group rows of every sequence
+    (the other rows of ``out`` are left untouched).
     """
+    if rows not in ("all", "head"):
+        raise AttentionError(f"rows must be 'all' or 'head', got {rows!r}")
     if padding not in PADDING_MODES:
         raise AttentionError(f"unknown padding mode {padding!r}")
     T = layout.total_tokens
@@ -185,6 +189,8 @@ def attend_packed(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: Pac
         out = torch.empty((T, hd), dtype=q.dtype, device=q.device)
     algo_code = {"auto": _lib.ALGO_AUTO, "generic": _lib.ALGO_GENERIC, "band": _lib.ALGO_BAND_MMA,
                  "tc": _lib.ALGO_TC}[algo]
+    if rows == "head":
+        algo_code = _lib.ALGO_HEAD_ROWS
     links = pattern.links()
     ws = layout.attn_workspace(heads, d, links)
     _lib.call(

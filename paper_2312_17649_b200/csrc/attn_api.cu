@@ -52,7 +52,7 @@ extern "C" int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t 
   SC_CHECK_ARG((glob_cu == nullptr) == (glob_pos == nullptr), "sc_attn_fwd: glob_cu/glob_pos must be both set or both NULL");
   SC_CHECK_ARG(glob_cu == nullptr || tok_flags != nullptr, "sc_attn_fwd: QDS globals need tok_flags");
   SC_CHECK_ARG(algo == SC_ATTN_AUTO || algo == SC_ATTN_GENERIC || algo == SC_ATTN_BAND_MMA ||
-                   algo == SC_ATTN_TC,
+                   algo == SC_ATTN_TC || algo == SC_ATTN_HEAD_ROWS,
                "sc_attn_fwd: bad algo %d", algo);
   SC_CHECK_ARG(max_qgroup_len >= 1, "sc_attn_fwd: max_qgroup_len must be >= 1");
   a.q = q; a.k = k; a.v = v; a.ld = row_stride; a.out = out; a.ld_out = out_row_stride;
@@ -60,6 +60,18 @@ extern "C" int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t 
   a.d = head_dim; a.padding = padding; a.scale = scale; a.flags = tok_flags; a.glob_cu = glob_cu;
   a.glob_pos = glob_pos; a.status = status; a.row_begin = 0; a.row_end = total_tokens;
   cudaStream_t st = (cudaStream_t)stream;
+  if (algo == SC_ATTN_HEAD_ROWS) {
+    // cls + query-group rows only: the band kernel's head-rows mode streams every
+    // doc key once for the split-softmax records; else the generic kernel per head row
+    int rc = launch_attn_band(a, dtype, seq_tile_base, seq_head_base, tile_rows, max_qgroup_len, workspace,
+                              workspace_bytes, st, /*doc_rows=*/false);
+    if (rc != SC_ERR_UNSUPPORTED) return rc;
+    SC_CHECK_ARG(seq_head_base, "sc_attn_fwd: head-rows mode needs seq_head_base");
+    a.head_base = seq_head_base;
+    a.n_head_rows = nseq * (1 + max_qgroup_len);
+    a.partials = nullptr;
+    return launch_attn_generic(a, dtype, st);
+  }
   const int w = a.links.w[2][2];
   const bool narrow = w >= 0 && w <= kBandMaxWindow;
   if (algo == SC_ATTN_BAND_MMA || (algo == SC_ATTN_AUTO && narrow)) {

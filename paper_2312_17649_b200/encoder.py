@@ -265,10 +265,16 @@ class CrossEncoder:
     """Config + device weights; batched inference (R/encoder.py:450-538)."""
 
     def __init__(self, config: EncoderConfig, weights: dict | None = None, seed: int = 0,
-                 device="cuda", attn_algo: str = "auto"):
+                 device="cuda", attn_algo: str = "auto", prune_last_layer: bool = False):
+        """``prune_last_layer``: the scoring entry points (score*, GraphedScorer) run
+        the last layer for the [CLS] rows only past the K/V projection -- the score
+        reads nothing else (R/encoder.py:506).  Scores are unchanged; the reference's
+        finite check then covers the last layer's [CLS] rows only.  ``forward``
+        always computes every row."""
         self.config = config
         self.device = torch.device(device)
         self.attn_algo = attn_algo
+        self.prune_last_layer = prune_last_layer
         host = init_weights(config, seed) if weights is None else weights
         self.host_weights = host
         self._upload(host)
@@ -327,11 +333,14 @@ class CrossEncoder:
     # -- the packed hot loop ---------------------------------------------
 
     def encode_packed(self, ids_dev: torch.Tensor, layout: PackedLayout, check_finite: bool = True,
-                      attn_hook=None) -> torch.Tensor:
+                      attn_hook=None, cls_only: bool = False) -> torch.Tensor:
         """Final-layer fp32 activations [T, h] for a packed batch already on the device.
 
         ``attn_hook(event)`` (optional) is called with "start"/"end" around each
         attention launch so a caller can bracket it with CUDA events.
+        ``cls_only``: the last layer runs attention for the head rows only and the
+        rest of the layer for the [CLS] rows only; returns [nseq, h] (row j =
+        sequence j's [CLS]).
         """
         cfg = self.config
         T, h, H = layout.total_tokens, cfg.embed_dim, cfg.heads
@@ -359,6 +368,9 @@ class CrossEncoder:
         with _fp32_gemms(not bf16):
             for i, L in enumerate(self.layers):
                 xr = xh if bf16 else x  # residual stream (and GEMM input) of this layer
+                if cls_only and i == last:
+                    self._last_bad = bad if check_finite else None
+                    return self._cls_last_layer(L, xr, layout, pattern, bad if check_finite else None, i)
                 qkv = F.linear(xr, L["wqkv"], L["bqkv"])
                 if attn_hook:
                     attn_hook("start")
@@ -381,6 +393,36 @@ class CrossEncoder:
         self._last_bad = bad if check_finite else None
         return x
 
+    def _cls_last_layer(self, L, xr, layout, pattern, bad, i):
+        """Last layer for the [CLS] rows only (R/encoder.py:306-371 restricted to the rows
+        R/encoder.py:506 reads): K/V of every token, attention of the head rows, then
+        Wo / LN / FFN / LN on nseq rows.  Returns fp32 [nseq, h]."""
+        cfg = self.config
+        h, H = cfg.embed_dim, cfg.heads
+        bf16 = cfg.torch_dtype == torch.bfloat16
+        dcode = _lib.DTYPE_BF16 if bf16 else _lib.DTYPE_F32
+        stream = _lib.stream_handle()
+        qkv = F.linear(xr, L["wqkv"], L["bqkv"])
+        o = torch.empty((layout.total_tokens, h), dtype=xr.dtype, device=self.device)
+        attend_packed(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], layout, pattern, H,
+                      math.sqrt(cfg.head_dim), cfg.padding, out=o, algo=self.attn_algo, check=False, rows="head")
+        cls = layout.cls_rows
+        n = layout.nseq
+        y = F.linear(o.index_select(0, cls), L["wo"], L["bo"])
+        xc = xr.index_select(0, cls)
+        x1 = torch.empty_like(xc)
+        _lib.call("sc_residual_layernorm_ex", xc.data_ptr(), dcode, y.data_ptr(), dcode, None,
+                  L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), None if bf16 else x1.data_ptr(),
+                  x1.data_ptr() if bf16 else None, None, n, h, stream, exc=EncoderError)
+        f = F.linear(x1, L["w1"], L["b1"])
+        _lib.call("sc_bias_gelu", f.data_ptr(), None, dcode, n, cfg.ff_dim, stream, exc=EncoderError)
+        f2 = F.linear(f, L["w2"], L["b2"])
+        out = torch.empty((n, h), dtype=torch.float32, device=self.device)
+        _lib.call("sc_residual_layernorm_ex", x1.data_ptr(), dcode, f2.data_ptr(), dcode, None,
+                  L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(), out.data_ptr(), None,
+                  None if bad is None else bad.data_ptr() + 4 * i, n, h, stream, exc=EncoderError)
+        return out
+
     def _raise_if_nonfinite(self):
         bad = getattr(self, "_last_bad", None)
         if bad is None:
@@ -391,8 +433,10 @@ class CrossEncoder:
             raise NonFiniteActivationError(int(nz[0]))
 
     def scores_from_hidden(self, x: torch.Tensor, layout: PackedLayout, out=None) -> torch.Tensor:
+        """Scores from final activations: [T, h] (all rows) or [nseq, h] (cls_only)."""
         out = torch.empty(layout.nseq, dtype=torch.float32, device=self.device) if out is None else out
-        _lib.call("sc_cls_score", x.data_ptr(), layout.cu_seqlens.data_ptr(), layout.nseq,
+        cu = layout.cu_seqlens if x.shape[0] == layout.total_tokens else layout.ident_cu
+        _lib.call("sc_cls_score", x.data_ptr(), cu.data_ptr(), layout.nseq,
                   self.config.embed_dim, self.head_w.data_ptr(), self.head_b, out.data_ptr(),
                   _lib.stream_handle(), exc=EncoderError)
         return out
@@ -402,7 +446,7 @@ class CrossEncoder:
         self._check_batch(batch)
         layout = layout or self.make_layout(batch)
         ids = torch.from_numpy(batch.ids).to(self.device, non_blocking=True)
-        x = self.encode_packed(ids, layout)
+        x = self.encode_packed(ids, layout, cls_only=self.prune_last_layer)
         return self.scores_from_hidden(x, layout)
 
     # -- reference-signature API -----------------------------------------
@@ -488,7 +532,7 @@ class GraphedScorer:
         self.kernels_per_replay = _lib.kernel_launches() - n0
 
     def _forward(self):
-        x = self.model.encode_packed(self.ids, self.layout, check_finite=False)
+        x = self.model.encode_packed(self.ids, self.layout, check_finite=False, cls_only=self.model.prune_last_layer)
         return self.model.scores_from_hidden(x, self.layout)
 
     def matches(self, batch: PackedBatch) -> bool:

@@ -48,6 +48,8 @@ class PackedLayout:
         self.tok_group = torch.empty(T, **i32)
         self.tok_rel = torch.empty(T, **i32)
         self.tok_pos = torch.empty(T, **i32)
+        self.cls_rows = torch.from_numpy(self.cu_host[:-1].astype(np.int64)).to(dev)  # each sequence's [CLS] row
+        self.ident_cu = torch.arange(self.nseq + 1, **i32)  # row j = sequence j (per-sequence [CLS] arrays)
         self.seq_tile_base = torch.empty(self.nseq + 1, **i32)
         self.seq_head_base = torch.empty(self.nseq + 1, **i32)
         self.max_qgroup_len = int(self.qlen_host.max())

@@ -4,6 +4,7 @@ Scores within 1e-4 (fp32) / 2e-2 (bf16); identical per-query rankings on the
 fp32 path (bf16 cannot promise ranking identity).
 """
 
+import math
 import os
 
 import numpy as np
@@ -146,3 +147,39 @@ def test_graphed_scorer_matches_eager(P):
     b2 = P.PackedBatch.from_sequences(seqs2)
     assert g.matches(b2)
     np.testing.assert_array_equal(g(b2.ids).cpu().numpy(), model.score_packed(b2).cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["sparse", "longformer", "qds", "full"])
+@pytest.mark.parametrize("precision,tol", [("f32", 1e-5), ("bf16", 2e-2)])
+def test_prune_last_layer_scores_unchanged(P, name, precision, tol):
+    """Last layer on the [CLS] rows only (the score reads x[:,0], R/encoder.py:506): same scores."""
+    cfg = P.EncoderConfig(**{**cases.ELECTRA_PASSAGE, "layers": 3, "pattern": name, "precision": precision})
+    full = P.CrossEncoder(cfg, seed=0)
+    pruned = P.CrossEncoder(cfg, weights=full.host_weights, prune_last_layer=True)
+    seqs = [rerank_ids(2, j, int(n), cfg.vocab_size, cfg.max_positions, P) for j, n in enumerate([164, 90, 7, 300])]
+    batch = P.PackedBatch.from_sequences(seqs)
+    a = full.score_packed(batch).cpu().numpy()
+    b = pruned.score_packed(batch).cpu().numpy()
+    np.testing.assert_allclose(b, a, atol=tol, rtol=0)
+
+
+@pytest.mark.parametrize("name,w", [("sparse", 4), ("longformer", 4), ("qds", 4), ("full", math.inf), ("sparse", 100)])
+def test_head_rows_mode_matches_full_attention(P, name, w):
+    rng = np.random.default_rng(31)
+    H, d = 12, 64
+    shapes = [(10, 700), (1, 1), (14, 300)]
+    seq = [m + n + 3 for m, n in shapes]
+    lay = P.PackedLayout.from_lengths(seq, [m + 1 for m, _ in shapes], device="cuda",
+                                      qds_every=30 if name == "qds" else 0)
+    T = sum(seq)
+    x = torch.from_numpy(rng.standard_normal((T, 3 * H * d)).astype(np.float32)).cuda().to(torch.bfloat16)
+    pat = P.make_pattern(name, w)
+    args = (x[:, :H * d], x[:, H * d:2 * H * d], x[:, 2 * H * d:], lay, pat, H)
+    full = P.attend_packed(*args).float()
+    head = P.attend_packed(*args, out=torch.zeros_like(full).to(torch.bfloat16), rows="head").float()
+    r = 0
+    for m, n in shapes:
+        rows = slice(r, r + m + 2)  # cls + query group
+        torch.testing.assert_close(head[rows], full[rows], atol=1e-2, rtol=0)
+        assert head[r + m + 2: r + m + n + 3].abs().max().item() == 0  # doc rows untouched
+        r += m + n + 3
