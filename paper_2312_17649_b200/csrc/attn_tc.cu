@@ -15,12 +15,11 @@
 // Key blocks: the global block (cls + query keys, N = 32) then doc keys
 // [max(0, r0-w), min(n, r0+128+w)) in blocks of 128.  Semantics as the band
 // kernel (R/band.py:48-52, R/attention.py:125-139, :228-257).
-#include <cuda.h>
-
-#include "attn.cuh"
+#include "tc_common.cuh"
 
 namespace sc {
 namespace tck {
+using namespace tcx;
 
 constexpr int BM = 128, D = 64;
 constexpr int NTHREADS = 192;
@@ -55,180 +54,6 @@ struct Params {
   __nv_bfloat16* out;
   int64_t ld_out;
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok = 0;
-  while (!ok) {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
-
-// ---- tcgen05 helpers -------------------------------------------------------
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-// D[tmem] (+)= A[smem desc] . B[smem desc]
-__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
-      ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-// D[tmem] (+)= A[tmem] . B[smem desc]
-__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p; }"
-      ::"r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
-#define TC_LD32(addr, r)                                                                          \
-  asm volatile(                                                                                   \
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                  \
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),       \
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),   \
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),            \
-        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),            \
-        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
-      : "r"(addr))
-
-#define TC_LD16(addr, r)                                                                          \
-  asm volatile(                                                                                   \
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),       \
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),   \
-        "=r"(r[14]), "=r"(r[15])                                                                  \
-      : "r"(addr))
-
-#define TC_ST16(addr, r)                                                                          \
-  asm volatile(                                                                                   \
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
-      "%14,%15,%16};" ::"r"(addr),                                                                \
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),     \
-      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) \
-      : "memory")
-
-#define TC_ST32(addr, r)                                                                          \
-  asm volatile(                                                                                   \
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"             \
-      ::"r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),  \
-      "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]),           \
-      "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]),        \
-      "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),        \
-      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                                             \
-      : "memory")
-
-__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-// SMEM matrix descriptor, 128B swizzle, SBO = 1024 B (8-row groups), version 1 (sm_100).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
-  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-// Instruction descriptor, kind::f16: bf16 x bf16 -> f32, A K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int b_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
-}
-
-__device__ __forceinline__ float ex2(float x) {
-  float r;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
-// Max of NC raw logits (as bits) with independent 3-input max chains.
-template <int NC>
-__device__ __forceinline__ float row_max(const uint32_t (&v)[NC]) {
-  float a = -INFINITY, b = -INFINITY, c = -INFINITY, d = -INFINITY;
-#pragma unroll
-  for (int e = 0; e < NC; e += 8) {
-    a = fmaxf(a, fmaxf(__uint_as_float(v[e + 0]), __uint_as_float(v[e + 1])));
-    b = fmaxf(b, fmaxf(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3])));
-    c = fmaxf(c, fmaxf(__uint_as_float(v[e + 4]), __uint_as_float(v[e + 5])));
-    d = fmaxf(d, fmaxf(__uint_as_float(v[e + 6]), __uint_as_float(v[e + 7])));
-  }
-  return fmaxf(fmaxf(a, b), fmaxf(c, d));
-}
-
-// P = exp2(v * c2 - base) for NC logits (FFMA2 for the argument pairs):
-// packed bf16 pairs written over v[0..NC/2), returns the fp32 row sum.
-// (An FA4-style polynomial exp2 on the FMA pipe for part of the columns was
-// measured slower at d = 64 for every split tried: the softmax here is
-// latency-bound, not MUFU-bound.)
-template <int NC>
-__device__ __forceinline__ float row_exp_pack(uint32_t (&v)[NC], float c2, float base) {
-  const float2 c2v = make_float2(c2, c2), nb = make_float2(-base, -base);
-  float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int e = 0; e < NC; e += 2) {
-    const float2 a = __ffma2_rn(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), c2v, nb);
-    const float2 pr = make_float2(ex2(a.x), ex2(a.y));
-    if ((e >> 1) & 1) s1 = __fadd2_rn(s1, pr);
-    else s0 = __fadd2_rn(s0, pr);
-    v[e / 2] = pack_bf16(pr.x, pr.y);
-  }
-  const float2 t = __fadd2_rn(s0, s1);
-  return t.x + t.y;
-}
-
-// Row softmax of NC raw logits held as bits in v (masked entries = -inf):
-// updates the running max m, returns alpha = exp2((m_old - m_new) c2) and the
-// row sum of P, and writes P (bf16 pairs, packed in place) to TMEM at p_addr.
-template <int NC>
-__device__ __forceinline__ void row_softmax(uint32_t (&v)[NC], float c2, float& m, float& alpha, float& sum,
-                                            uint32_t p_addr) {
-  float mx = -INFINITY;
-#pragma unroll
-  for (int e = 0; e < NC; ++e) mx = fmaxf(mx, __uint_as_float(v[e]));
-  const float mnew = fmaxf(m, mx);
-  const float base = mnew == -INFINITY ? 0.f : mnew * c2;
-  alpha = ex2(fmaf(m, c2, -base));
-  float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-  for (int e = 0; e < NC; e += 2) {
-    const float p0 = ex2(fmaf(__uint_as_float(v[e]), c2, -base));
-    const float p1 = ex2(fmaf(__uint_as_float(v[e + 1]), c2, -base));
-    s0 += p0;
-    s1 += p1;
-    v[e / 2] = pack_bf16(p0, p1);
-  }
-  sum = s0 + s1;
-  m = mnew;
-#pragma unroll
-  for (int c = 0; c < NC / 2; c += 16) TC_ST16(p_addr + c, (&v[c]));
-}
 
 template <class C>
 struct Smem {
@@ -562,29 +387,6 @@ __global__ void qds_gather_kernel(const int32_t* __restrict__ cu, const int32_t*
       *reinterpret_cast<uint4*>(d + part * hd + c) = __ldg(reinterpret_cast<const uint4*>(src[part] + c));
 }
 
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t ld, int box_rows) {
-  static EncodeFn enc = nullptr;
-  if (!enc) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return false;
-    enc = reinterpret_cast<EncodeFn>(ptr);
-  }
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-  cuuint32_t box[2] = {(cuuint32_t)D, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <class C>
 static int launch_kernel(dim3 grid, const CUtensorMap* maps, const Params& p, cudaStream_t st) {
   const size_t smem = Smem<C>::TOTAL + 1024;
@@ -688,8 +490,6 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
                   : launch_kernel<VMID32>(grid, maps, p, st);
   };
 
-  tile128_prefix_kernel<<<1, 1024, 0, st>>>(a.cu, a.qlen, a.nseq, nullptr, tbase);
-  SC_CHECK_LAUNCH("tile128_prefix_kernel");
   if (qds) {
     tile128_prefix_kernel<<<1, 1024, 0, st>>>(a.cu, a.qlen, a.nseq, a.glob_cu, gtbase);
     SC_CHECK_LAUNCH("tile128_prefix_kernel");
@@ -711,6 +511,8 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
   p.qds = qds ? 1 : 0; p.global_rows = 0;
   p.flags = a.flags; p.glob_cu = a.glob_cu; p.glob_pos = a.glob_pos;
+  tile128_prefix_kernel<<<1, 1024, 0, st>>>(a.cu, a.qlen, a.nseq, nullptr, tbase);
+  SC_CHECK_LAUNCH("tile128_prefix_kernel");
   CUtensorMap maps[7];
   if (!build_maps(maps, var, false)) return unsupported("cuTensorMapEncodeTiled failed");
   int rc = launch_var(var, dim3((unsigned)((a.T + BM - 1) / BM + a.nseq), (unsigned)a.H), maps, p);
