@@ -17,7 +17,8 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .encoder import CrossEncoder, EncoderError, PackedBatch, assemble_input
+from .encoder import CrossEncoder, EncoderError, PackedBatch
+from .tokenizer import CLS_ID, SEP_ID
 
 
 class EvaluationError(ValueError):
@@ -85,29 +86,61 @@ def rerank(scorer, query, candidates, top_k: int = 100, query_id: str = "q", tag
     return rank_entries(query_id, [c[0] for c in candidates], scores, top_k, tag)
 
 
-def score_candidates(model: CrossEncoder, query_ids, candidate_ids, max_tokens: int = 1 << 18) -> np.ndarray:
-    """fp32 scores of every (query, candidate) pair, packed varlen on the GPU; unscorable -> -inf."""
-    seqs, ok = [], []
-    for doc in candidate_ids:
-        try:
-            seqs.append(assemble_input(query_ids, doc, model.config.max_positions))
-            ok.append(True)
-        except EncoderError:
-            ok.append(False)
-    scores = np.full(len(candidate_ids), -np.inf, dtype=np.float32)
-    if seqs:
-        got, chunk, tok = [], [], 0
-        for s in seqs:
-            if chunk and tok + s.partition.seq_len > max_tokens:
-                got.append(model.score_packed(PackedBatch.from_sequences(chunk)))
-                chunk, tok = [], 0
-            chunk.append(s)
-            tok += s.partition.seq_len
-        got.append(model.score_packed(PackedBatch.from_sequences(chunk)))
-        vals = torch.cat(got).cpu().numpy()
-        model._raise_if_nonfinite()
-        scores[np.asarray(ok)] = vals
-    return scores
+def pack_pairs(query_ids, candidate_ids, max_positions: int | None = None) -> PackedBatch:
+    """Vectorised ``assemble_input`` for one query and many documents (R/encoder.py:154-177):
+    [CLS] q [SEP] d [SEP] per pair, the doc tail truncated to max_positions - m - 3, the
+    query never truncated; returns the packed varlen batch."""
+    q = np.asarray(query_ids, dtype=np.int32).reshape(-1)
+    m = int(q.shape[0])
+    if m < 1:
+        raise EncoderError("query must contain at least one token")
+    if max_positions is not None and m + 3 > max_positions:
+        raise EncoderError(f"query of {m} tokens cannot fit in {max_positions} positions")
+    keep = None if max_positions is None else max_positions - m - 3
+    docs = [np.asarray(d, dtype=np.int32).reshape(-1)[:keep] for d in candidate_ids]
+    if not docs:
+        raise EncoderError("empty batch")
+    seq = np.array([m + 3 + d.shape[0] for d in docs], dtype=np.int64)
+    off = np.zeros(len(docs) + 1, dtype=np.int64)
+    np.cumsum(seq, out=off[1:])
+    ids = np.empty(int(off[-1]), dtype=np.int32)
+    for o, d in zip(off[:-1], docs):
+        ids[o] = CLS_ID
+        ids[o + 1: o + 1 + m] = q
+        ids[o + 1 + m] = SEP_ID
+        ids[o + 2 + m: o + 2 + m + d.shape[0]] = d
+        ids[o + 2 + m + d.shape[0]] = SEP_ID
+    return PackedBatch(ids, seq, np.full(len(docs), m + 1, dtype=np.int64))
+
+
+def score_candidates(model: CrossEncoder, query_ids, candidate_ids, max_tokens: int = 1 << 18,
+                     as_tensor: bool = False):
+    """fp32 scores of every (query, candidate) pair, packed varlen on the GPU.
+
+    Chunks of <= max_tokens tokens are launched back to back without a host
+    sync (the next chunk is packed on the host while the GPU runs).  With
+    ``as_tensor`` the device tensor is returned (no D2H copy)."""
+    maxpos = model.config.max_positions
+    m = len(np.asarray(query_ids).reshape(-1))
+    if m < 1 or m + 3 > maxpos:  # assemble_input raises for every pair: the reference scores -inf
+        if as_tensor:
+            return torch.full((len(candidate_ids),), -math.inf, dtype=torch.float32, device=model.device)
+        return np.full(len(candidate_ids), -np.inf, dtype=np.float32)
+    got, lo = [], 0
+    lens = [min(len(d) + m + 3, maxpos) for d in candidate_ids]
+    while lo < len(candidate_ids):
+        hi, tok = lo, 0
+        while hi < len(candidate_ids) and (hi == lo or tok + lens[hi] <= max_tokens):
+            tok += lens[hi]
+            hi += 1
+        got.append(model.score_packed(pack_pairs(query_ids, candidate_ids[lo:hi], maxpos)))
+        lo = hi
+    vals = torch.cat(got)
+    if as_tensor:
+        return vals
+    out = vals.cpu().numpy()
+    model._raise_if_nonfinite()
+    return out
 
 
 def shard_range(n: int, world: int, rank: int) -> tuple:
@@ -139,20 +172,25 @@ def rerank_distributed(model: CrossEncoder | None, queries, top_k: int = 100, ta
     ``score_fn(query_ids, candidate_ids) -> float32 array`` overrides the GPU
     scorer (used by the CPU multi-process tests).
     """
-    if score_fn is None:
-        def score_fn(qids, cands):
-            return score_candidates(model, qids, cands)
     lo, hi = shard_range(len(queries), world, rank)
-    local = [np.asarray(score_fn(q[1], [c[1] for c in q[2]]), np.float32) for q in queries[lo:hi]]
-    flat = np.concatenate(local) if local else np.zeros(0, np.float32)
+    if score_fn is None:
+        # GPU path: every query's chunks are launched back to back (host packing of the
+        # next chunk overlaps the GPU); scores stay on the device until the gather
+        parts = [score_candidates(model, q[1], [c[1] for c in q[2]], as_tensor=True) for q in queries[lo:hi]]
+        flat_t = torch.cat(parts) if parts else torch.zeros(0, dtype=torch.float32, device=model.device)
+    else:
+        local = [np.asarray(score_fn(q[1], [c[1] for c in q[2]]), np.float32) for q in queries[lo:hi]]
+        flat_t = torch.from_numpy(np.concatenate(local) if local else np.zeros(0, np.float32))
     if world > 1:
         per_q = [len(q[2]) for q in queries]
         counts = [sum(per_q[slice(*shard_range(len(queries), world, r))]) for r in range(world)]
         nccl = torch.distributed.get_backend(group) == "nccl"
         dev = (model.device if model is not None else torch.device("cuda")) if nccl else torch.device("cpu")
-        allv = gather_scores(torch.from_numpy(flat).to(dev), counts, group).cpu().numpy()
+        allv = gather_scores(flat_t.to(dev), counts, group).cpu().numpy()
     else:
-        allv = flat
+        allv = flat_t.cpu().numpy()
+    if model is not None and score_fn is None:
+        model._raise_if_nonfinite()
     if rank != 0:
         return None
     entries, off = [], 0

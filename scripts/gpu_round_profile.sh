@@ -10,7 +10,10 @@ timeout 900 python bench.py > $OUT/bench_n1.json 2> $OUT/bench_n1.err
 timeout 600 python bench.py --impl reference > $OUT/bench_reference_n1.json 2> $OUT/bench_reference_n1.err
 timeout 600 python bench.py --doc-len 164 --pairs-per-gpu 1024 --no-cpu-baseline > $OUT/bench_passages_n1.json 2> $OUT/bench_passages.err
 timeout 600 python bench.py --varlen --no-cpu-baseline > $OUT/bench_varlen_n1.json 2> $OUT/bench_varlen.err
+timeout 600 python scripts/rerank_c5.py --queries 50 --run-file $OUT/c5_run_q50.txt > $OUT/rerank_c5_n1.json 2> $OUT/rerank_c5.err
+timeout 600 python scripts/rerank_c5.py --queries 50 --prune-last-layer >> $OUT/rerank_c5_n1.json 2>> $OUT/rerank_c5.err
 timeout 600 python scripts/attn_sweep.py --windows 1,4,16,32,64,128,256,inf > $OUT/sweep.jsonl 2>&1
+timeout 300 python scripts/attn_sweep.py --windows 4,64 --patterns qds >> $OUT/sweep.jsonl 2>&1
 timeout 300 python scripts/attn_sweep.py --windows inf --patterns full,longformer >> $OUT/sweep.jsonl 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_launches.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:band_attn -c 1 -o $OUT/band_w4 python scripts/attn_sweep.py --windows 4 --iters 1 > $OUT/ncu_band.log 2>&1

@@ -112,3 +112,21 @@ def test_interpolate_positions():
     out = P.interpolate_positions(pos, 5)
     np.testing.assert_allclose(out[1], 0.5 * pos[0] + 0.5 * pos[1])
     np.testing.assert_array_equal(out[-1], pos[-1])
+
+
+def test_pack_pairs_matches_assemble_input():
+    """Vectorised candidate packing == per-pair assemble_input (R/encoder.py:154-177), incl. truncation."""
+    from paper_2312_17649_b200.encoder import PackedBatch, assemble_input
+    from paper_2312_17649_b200.rerank import pack_pairs
+
+    rng = np.random.default_rng(4)
+    for m, maxpos in [(10, 4099), (7, 200), (1, 20)]:
+        q = rng.integers(3, 1000, size=m)
+        docs = [rng.integers(3, 1000, size=int(n)) for n in [0, 1, 5, 150, 4086, 5000]]
+        a = pack_pairs(q, docs, maxpos)
+        b = PackedBatch.from_sequences([assemble_input(q, d, maxpos) for d in docs])
+        np.testing.assert_array_equal(a.ids, b.ids)
+        np.testing.assert_array_equal(a.seq_lens, b.seq_lens)
+        np.testing.assert_array_equal(a.qgroup_lens, b.qgroup_lens)
+    with pytest.raises(ValueError):
+        pack_pairs(rng.integers(3, 9, size=30), docs, 20)
