@@ -323,7 +323,23 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
   const float c2 = p.c2;
   const int hl_bits = p.hl[0][0] | (p.hl[0][1] << 1) | (p.hl[1][0] << 2) | (p.hl[1][1] << 3);
   const int hdoc_bits = p.hdoc[0] | (p.hdoc[1] << 1);
-  int it = 0;
+  // Band mask of an interior tile (no sequence edge in reach): bit (nb*4 + e) of
+  // chunk bc set when that score element is inside the +-w band.  Tile-independent.
+  uint32_t bmask_int[NBC];
+#pragma unroll
+  for (int bc = 0; bc < NBC; ++bc) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int diff = 32 * bc + nb * 8 + 2 * tq + (e & 1) - (gq + ((e >> 1) << 3));  // t - r + w
+        m |= (diff >= 0 && diff <= 2 * w ? 1u : 0u) << (nb * 4 + e);
+      }
+    bmask_int[bc] = m;
+  }
+  int it = 0, last_j = -1;
+  uint32_t gmask[GR / 16];
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int j = find_seq(p.tile_base, p.nseq, tile);
     const SeqGroups g = seq_groups(p.cu, p.qlen, j);
@@ -341,41 +357,44 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
     const bool edge = (r0 - w + wr0 < 0) || (r0 - w + wr0 + 32 * NBC > n_doc);
   #pragma unroll
     for (int bc = 0; bc < NBC; ++bc) {
-      uint32_t m = 0;
+      uint32_t m = bmask_int[bc];
+      if (edge) {  // sequence start / end in reach: drop keys outside [0, n_doc)
   #pragma unroll
-      for (int nb = 0; nb < 4; ++nb)
+        for (int nb = 0; nb < 4; ++nb)
   #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int c = 32 * bc + nb * 8 + 2 * tq + (e & 1);
-          const int diff = c - (gq + ((e >> 1) << 3));  // t - r + w
-          const int t = r0 - w + wr0 + c;
-          bool ok = diff >= 0 && diff <= 2 * w;
-          if (edge) ok = ok && t >= 0 && t < n_doc;
-          m |= (ok ? 1u : 0u) << (nb * 4 + e);
-        }
+          for (int e = 0; e < 4; ++e) {
+            const int t = r0 - w + wr0 + 32 * bc + nb * 8 + 2 * tq + (e & 1);
+            if (t < 0 || t >= n_doc) m &= ~(1u << (nb * 4 + e));
+          }
+      }
       bmask[bc] = m;
     }
-    uint32_t gmask[GR / 16];
+    if (j != last_j) {  // global-key mask: per sequence (query-group length, links)
+      last_j = j;
   #pragma unroll
-    for (int gc = 0; gc < GR / 16; ++gc) {
-      uint32_t m = 0;
+      for (int gc = 0; gc < GR / 16; ++gc) {
+        uint32_t m = 0;
   #pragma unroll
-      for (int nb = 0; nb < 2; ++nb)
+        for (int nb = 0; nb < 2; ++nb)
   #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int kg = gc * 16 + nb * 8 + 2 * tq + (e & 1);
-          const bool ok = kg < G && (kg == 0 ? p.link_cls : p.link_query);
-          m |= (ok ? 1u : 0u) << (nb * 4 + e);
-        }
-      gmask[gc] = m;
+          for (int e = 0; e < 4; ++e) {
+            const int kg = gc * 16 + nb * 8 + 2 * tq + (e & 1);
+            const bool ok = kg < G && (kg == 0 ? p.link_cls : p.link_query);
+            m |= (ok ? 1u : 0u) << (nb * 4 + e);
+          }
+        gmask[gc] = m;
+      }
     }
     // Own-key mask of the tile's 64 doc keys for the full-row partials.
-    uint32_t fmask[2] = {0u, 0u};
+    uint32_t fmask[2] = {0xffffu, 0xffffu};
+    if (rows_here < BM) {
+      fmask[0] = fmask[1] = 0u;
   #pragma unroll
-    for (int nb = 0; nb < 8; ++nb)
+      for (int nb = 0; nb < 8; ++nb)
   #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        fmask[nb >> 2] |= ((nb * 8 + 2 * tq + (e & 1)) < rows_here ? 1u : 0u) << ((nb & 3) * 4 + e);
+        for (int e = 0; e < 4; ++e)
+          fmask[nb >> 2] |= ((nb * 8 + 2 * tq + (e & 1)) < rows_here ? 1u : 0u) << ((nb & 3) * 4 + e);
+    }
 
     float ninv_a = 0.f, ninv_b = 0.f;
     if (p.padding == SC_PAD_ZERO_LOGIT) {
@@ -452,7 +471,9 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
         l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
         l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-        const float i0 = 1.f / l0, i1 = 1.f / l1;
+        float i0, i1;  // approximate reciprocal: O leaves as bf16
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(i0) : "f"(l0));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(i1) : "f"(l1));
         if (wr0 + 16 <= rows_here) {
           // Full 16-row block: stmatrix the bf16 O fragments into this warp's
           // (now dead) Q rows -- same 128B swizzle as the TMA box -- and TMA-store
