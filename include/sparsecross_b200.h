@@ -142,7 +142,7 @@ SC_API size_t sc_attn_workspace_bytes_qds(int32_t nseq, int32_t total_tokens, in
  * seq_tile_base / seq_head_base come from sc_index_build with the same
  * tile_rows; max_qgroup_len is the host-known max of qgroup_len (kernel
  * selection only).  algo picks the kernel (SC_ATTN_*); AUTO runs, in bf16
- * with d = 64: the tiled band kernel for doc windows <= 40 without QDS
+ * with d = 64: the tiled band kernel for doc windows <= 56 without QDS
  * globals, else the tcgen05 kernel (wider or full windows, and QDS with its
  * globals) -- each plus the head-row combine -- and the generic kernel for
  * everything else (fp32, other head dims, windowed head-row links).

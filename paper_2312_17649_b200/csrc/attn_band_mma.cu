@@ -184,6 +184,54 @@ __device__ __forceinline__ void pv16(uint32_t vbuf, int key0, int lane, const fl
   }
 }
 
+// Per-lane byte offsets of the ldmatrix / stmatrix row addresses inside a
+// 16-row block whose first row is a multiple of 8 (then the 128B swizzle term
+// depends on the lane only): q = A fragments of Q, k = B fragments of K
+// (non-transposed), v = B fragments of V (transposed) and the stmatrix layout.
+struct LaneOff {
+  uint32_t q[4], k[4], v[4];
+};
+__device__ __forceinline__ LaneOff lane_offsets(int lane) {
+  LaneOff o;
+  const int l7 = lane & 7;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o.q[i] = (lane & 15) * ROWB + (((2 * i + (lane >> 4)) ^ l7) << 4);
+    o.k[i] = (l7 + ((lane >> 4) << 3)) * ROWB + (((2 * i + ((lane >> 3) & 1)) ^ l7) << 4);
+    o.v[i] = (l7 + (((lane >> 3) & 1) << 3)) * ROWB + (((2 * i + (lane >> 4)) ^ l7) << 4);
+  }
+  return o;
+}
+// Aligned variants (row0 / key0 multiples of 8): one add per ldmatrix.
+__device__ __forceinline__ void load_q(uint32_t buf, int row0, const LaneOff& lo, uint32_t (&qa)[4][4]) {
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) ldsm_x4(buf + row0 * ROWB + lo.q[ks], qa[ks]);
+}
+__device__ __forceinline__ void qk16(uint32_t kbuf, int key0, const LaneOff& lo, const uint32_t (&qa)[4][4],
+                                     float (&s0)[4], float (&s1)[4]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s0[e] = s1[e] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    uint32_t b[4];
+    ldsm_x4(kbuf + key0 * ROWB + lo.k[ks], b);
+    mma16816(s0, qa[ks], b[0], b[1]);
+    mma16816(s1, qa[ks], b[2], b[3]);
+  }
+}
+__device__ __forceinline__ void pv16(uint32_t vbuf, int key0, const LaneOff& lo, const float (&p0)[4],
+                                     const float (&p1)[4], float (&o)[8][4]) {
+  uint32_t a[4] = {pack_bf16(p0[0], p0[1]), pack_bf16(p0[2], p0[3]), pack_bf16(p1[0], p1[1]),
+                   pack_bf16(p1[2], p1[3])};
+#pragma unroll
+  for (int np = 0; np < 4; ++np) {
+    uint32_t b[4];
+    ldsm_x4_t(vbuf + key0 * ROWB + lo.v[np], b);
+    mma16816(o[2 * np], a, b[0], b[1]);
+    mma16816(o[2 * np + 1], a, b[2], b[3]);
+  }
+}
+
 // Online-softmax update over NB n8 blocks of RAW logits (masked to -inf) for
 // rows (g, g+8).  m is kept in raw-logit units; c2 = log2(e)/scale.  Overwrites s with P.
 // kFresh: o is still zero (first update of a row block) -> skip the O rescale.
@@ -320,6 +368,7 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
   // ------------------------------------------------------------ doc warps
   const int gq = lane >> 2, tq = lane & 3;
   const int wr0 = warp * 16;
+  const LaneOff LO = lane_offsets(lane);
   const float c2 = p.c2;
   const int hl_bits = p.hl[0][0] | (p.hl[0][1] << 1) | (p.hl[1][0] << 2) | (p.hl[1][1] << 3);
   const int hdoc_bits = p.hdoc[0] | (p.hdoc[1] << 1);
@@ -407,7 +456,7 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
       mbar_wait(full_bar + 8 * s, (it / NS) & 1);
       if (active) {
         uint32_t qa[4][4];
-        load_q(q_buf(s), wr0, lane, qa);
+        load_q(q_buf(s), wr0, LO, qa);
         float o[8][4];
         zero_o(o);
         float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
@@ -418,9 +467,9 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
           constexpr int NG = GR / 8;
           float sc[NG + 4][4];
   #pragma unroll
-          for (int gc = 0; gc < GR / 16; ++gc) qk16(kg_buf(s), gc * 16, lane, qa, sc[2 * gc], sc[2 * gc + 1]);
-          qk16(kb_buf(s), wr0, lane, qa, sc[NG], sc[NG + 1]);
-          qk16(kb_buf(s), wr0 + 16, lane, qa, sc[NG + 2], sc[NG + 3]);
+          for (int gc = 0; gc < GR / 16; ++gc) qk16(kg_buf(s), gc * 16, LO, qa, sc[2 * gc], sc[2 * gc + 1]);
+          qk16(kb_buf(s), wr0, LO, qa, sc[NG], sc[NG + 1]);
+          qk16(kb_buf(s), wr0 + 16, LO, qa, sc[NG + 2], sc[NG + 3]);
   #pragma unroll
           for (int nb = 0; nb < NG; ++nb)
   #pragma unroll
@@ -433,38 +482,38 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
               if (!((bmask[0] >> (nb * 4 + e)) & 1)) sc[NG + nb][e] = -INFINITY;
           softmax_update<NG + 4, true>(sc, c2, m0, m1, l0, l1, o);
   #pragma unroll
-          for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, lane, sc[2 * gc], sc[2 * gc + 1], o);
-          pv16(vb_buf(s), wr0, lane, sc[NG], sc[NG + 1], o);
-          pv16(vb_buf(s), wr0 + 16, lane, sc[NG + 2], sc[NG + 3], o);
+          for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, LO, sc[2 * gc], sc[2 * gc + 1], o);
+          pv16(vb_buf(s), wr0, LO, sc[NG], sc[NG + 1], o);
+          pv16(vb_buf(s), wr0 + 16, LO, sc[NG + 2], sc[NG + 3], o);
         } else {
           // global keys: cls (key 0) and the query group (keys 1..G-1)
   #pragma unroll
           for (int gc = 0; gc < GR / 16; ++gc) {
             float sc[2][4];
-            qk16(kg_buf(s), gc * 16, lane, qa, sc[0], sc[1]);
+            qk16(kg_buf(s), gc * 16, LO, qa, sc[0], sc[1]);
   #pragma unroll
             for (int nb = 0; nb < 2; ++nb)
   #pragma unroll
               for (int e = 0; e < 4; ++e)
                 if (!((gmask[gc] >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
             softmax_update<2>(sc, c2, m0, m1, l0, l1, o);
-            pv16(vg_buf(s), gc * 16, lane, sc[0], sc[1], o);
+            pv16(vg_buf(s), gc * 16, LO, sc[0], sc[1], o);
           }
           // band keys: Kb row 0 = doc row r0 - w; this warp reads rows wr0 + [0, 32*NBC)
   #pragma unroll
           for (int bc = 0; bc < NBC; ++bc) {
             const int kb0 = wr0 + 32 * bc;
             float sc[4][4];
-            qk16(kb_buf(s), kb0, lane, qa, sc[0], sc[1]);
-            qk16(kb_buf(s), kb0 + 16, lane, qa, sc[2], sc[3]);
+            qk16(kb_buf(s), kb0, LO, qa, sc[0], sc[1]);
+            qk16(kb_buf(s), kb0 + 16, LO, qa, sc[2], sc[3]);
   #pragma unroll
             for (int nb = 0; nb < 4; ++nb)
   #pragma unroll
               for (int e = 0; e < 4; ++e)
                 if (!((bmask[bc] >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
             softmax_update<4>(sc, c2, m0, m1, l0, l1, o);
-            pv16(vb_buf(s), kb0, lane, sc[0], sc[1], o);
-            pv16(vb_buf(s), kb0 + 16, lane, sc[2], sc[3], o);
+            pv16(vb_buf(s), kb0, LO, sc[0], sc[1], o);
+            pv16(vb_buf(s), kb0 + 16, LO, sc[2], sc[3], o);
           }
         }
         l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
@@ -480,10 +529,9 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
           // them: 16 rows x 128 B leave in whole lines instead of 16 scattered
           // 4-byte stores per row.
           const uint32_t ob = q_buf(s);
-          const int srow = wr0 + (lane & 7) + (((lane >> 3) & 1) << 3);
   #pragma unroll
           for (int np = 0; np < 4; ++np)
-            stsm_x4(swz(ob, srow, 2 * np + (lane >> 4)),
+            stsm_x4(ob + wr0 * ROWB + LO.v[np],
                     pack_bf16(o[2 * np][0] * i0, o[2 * np][1] * i0), pack_bf16(o[2 * np][2] * i1, o[2 * np][3] * i1),
                     pack_bf16(o[2 * np + 1][0] * i0, o[2 * np + 1][1] * i0),
                     pack_bf16(o[2 * np + 1][2] * i1, o[2 * np + 1][3] * i1));
@@ -512,7 +560,7 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         for (int fc = 0; fc < GR / 16; ++fc) {
           if (fc * 16 < p.fneed) {
             uint32_t qa[4][4];
-            load_q(qf_buf(s), fc * 16, lane, qa);
+            load_q(qf_buf(s), fc * 16, LO, qa);
             float sc[8][4];
   #pragma unroll
             for (int np = 0; np < 4; ++np) qk16(kb_buf(s), w + np * 16, lane, qa, sc[2 * np], sc[2 * np + 1]);
@@ -558,10 +606,10 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         for (int fc = 0; fc < GR / 16; ++fc) {
           if (fc * 16 < G) {
             uint32_t qa[4][4];
-            load_q(qf_buf(s), fc * 16, lane, qa);
+            load_q(qf_buf(s), fc * 16, LO, qa);
             float sc[GR / 8][4];
   #pragma unroll
-            for (int gc = 0; gc < GR / 16; ++gc) qk16(kg_buf(s), gc * 16, lane, qa, sc[2 * gc], sc[2 * gc + 1]);
+            for (int gc = 0; gc < GR / 16; ++gc) qk16(kg_buf(s), gc * 16, LO, qa, sc[2 * gc], sc[2 * gc + 1]);
   #pragma unroll
             for (int nb = 0; nb < GR / 8; ++nb)
   #pragma unroll
@@ -577,7 +625,7 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
             float hm0 = -INFINITY, hm1 = -INFINITY, hl0 = 0.f, hl1 = 0.f;
             softmax_update<GR / 8, true>(sc, c2, hm0, hm1, hl0, hl1, o);
   #pragma unroll
-            for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, lane, sc[2 * gc], sc[2 * gc + 1], o);
+            for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, LO, sc[2 * gc], sc[2 * gc + 1], o);
             hl0 += __shfl_xor_sync(0xffffffffu, hl0, 1);
             hl0 += __shfl_xor_sync(0xffffffffu, hl0, 2);
             hl1 += __shfl_xor_sync(0xffffffffu, hl1, 1);
