@@ -30,7 +30,7 @@ import torch.nn.functional as F
 
 from . import _lib
 from .attention import FULL, GROUPS, AttentionError, attend_packed, is_full, make_pattern
-from .layout import PackedLayout
+from .layout import PackedLayout, to_device
 from .tokenizer import CLS_ID, NUM_SPECIAL_TOKENS, SEP_ID
 
 LAYER_NORM_EPS = 1e-12                         # R/encoder.py:41
@@ -445,7 +445,7 @@ class CrossEncoder:
         """Relevance scores (nseq,) on the device for a packed varlen batch."""
         self._check_batch(batch)
         layout = layout or self.make_layout(batch)
-        ids = torch.from_numpy(batch.ids).to(self.device, non_blocking=True)
+        ids = to_device(batch.ids, self.device)
         x = self.encode_packed(ids, layout, cls_only=self.prune_last_layer)
         return self.scores_from_hidden(x, layout)
 

@@ -23,6 +23,16 @@ class LayoutError(ValueError):
     pass
 
 
+def to_device(a: np.ndarray, device) -> torch.Tensor:
+    """Host array -> device tensor without a host/device sync: staged through a pinned
+    buffer (torch's caching host allocator keeps it alive until the copy has run), so
+    the host can pack the next batch while the GPU still works on this one."""
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if torch.device(device).type != "cuda":
+        return t.to(device)
+    return t.pin_memory().to(device, non_blocking=True)
+
+
 class PackedLayout:
     """Device index of a packed batch; reusable across all encoder layers."""
 
@@ -41,14 +51,14 @@ class PackedLayout:
         self.qds_every = int(qds_every) if qds_every else 0
         dev = self.device
         T = self.total_tokens
-        self.cu_seqlens = torch.from_numpy(self.cu_host).to(dev, non_blocking=False)
-        self.qgroup_len = torch.from_numpy(self.qlen_host).to(dev)
+        self.cu_seqlens = to_device(self.cu_host, dev)
+        self.qgroup_len = to_device(self.qlen_host, dev)
         i32 = dict(dtype=torch.int32, device=dev)
         self.tok_seq = torch.empty(T, **i32)
         self.tok_group = torch.empty(T, **i32)
         self.tok_rel = torch.empty(T, **i32)
         self.tok_pos = torch.empty(T, **i32)
-        self.cls_rows = torch.from_numpy(self.cu_host[:-1].astype(np.int64)).to(dev)  # each sequence's [CLS] row
+        self.cls_rows = to_device(self.cu_host[:-1].astype(np.int64), dev)  # each sequence's [CLS] row
         self.ident_cu = torch.arange(self.nseq + 1, **i32)  # row j = sequence j (per-sequence [CLS] arrays)
         self.seq_tile_base = torch.empty(self.nseq + 1, **i32)
         self.seq_head_base = torch.empty(self.nseq + 1, **i32)
