@@ -46,6 +46,7 @@ __host__ __device__ constexpr int min_ctas(int nbc) { return nbc == 1 ? 3 : 2; }
 
 struct Params {
   int nseq, H, w, kb_rows, fneed, fmax, padding;
+  int reverse;  // visit tiles last-to-first: the producing GEMM's most recent output rows are still in L2
   int link_cls, link_query;
   int doc_rows;  // 0: head rows only (doc rows computed by the tcgen05 kernel)
   // head rows (cls = group 0, query = group 1): links to cls / query keys, doc FULL
@@ -337,7 +338,8 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
       prefetch_map(&tmKg); prefetch_map(&tmVg); prefetch_map(&tmQf);
       const uint32_t bytes = (uint32_t)((p.doc_rows ? q_bytes : 0) + 3 * f_bytes + 2 * kb_box * ROWB);
       int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
+        const int tile = p.reverse ? ntiles - 1 - tix : tix;
         const int j = find_seq(p.tile_base, p.nseq, tile);
         const SeqGroups g = seq_groups(p.cu, p.qlen, j);
         const int doc_row0 = g.start + g.off[2] + (tile - __ldg(p.tile_base + j)) * BM;
@@ -389,7 +391,8 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
   }
   int it = 0, last_j = -1;
   uint32_t gmask[GR / 16];
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
+    const int tile = p.reverse ? ntiles - 1 - tix : tix;
     const int j = find_seq(p.tile_base, p.nseq, tile);
     const SeqGroups g = seq_groups(p.cu, p.qlen, j);
     const int n_doc = g.len[2];
@@ -887,6 +890,12 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   }
   const unsigned grid = (unsigned)((a.T + BM - 1) / BM + a.nseq);  // upper bound on tiles (record indexing)
   p.ntiles_max = (int)grid;
+  static int rev = -1;
+  if (rev < 0) {
+    const char* e = getenv("SC_BAND_REVERSE");
+    rev = e ? (atoi(e) != 0) : 1;
+  }
+  p.reverse = rev;
   // Doc rows + head rows over the global keys (first tile of each sequence).
   // (seq_head_base is unused: head rows are addressed through cu_seqlens.)
   (void)seq_head_base;

@@ -7,6 +7,17 @@ namespace sc {
 
 constexpr float kLnEps = 1e-12f;  // R/encoder.py:41
 
+// Elementwise passes walk their rows last-to-first (the producing GEMM's most
+// recent output is still in L2); SC_ELT_REVERSE=0 restores forward order (A/B).
+static bool elt_reverse() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SC_ELT_REVERSE");
+    v = e ? (atoi(e) != 0) : 1;
+  }
+  return v != 0;
+}
+
 // Grid-stride launch size: enough CTAs for `per_sm` waves of 256 threads over 148 SMs.
 static inline unsigned grid_cap(int64_t n, int per_sm) {
   int64_t b = (n + 255) / 256, cap = 148LL * per_sm;
@@ -101,13 +112,14 @@ __device__ __forceinline__ bool finite4(float4 o) {
   return isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(o.w);
 }
 
-template <typename R, typename Y, int kVec>
+template <typename R, typename Y, int kVec, bool kRev = true>
 __global__ void __launch_bounds__(256, 3) residual_ln_vec_kernel(
     const R* __restrict__ resid, const Y* __restrict__ y, const float* __restrict__ bias,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ out,
     __nv_bfloat16* __restrict__ out_h, int32_t* __restrict__ bad, int rows, int h) {
   const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // rows last-to-first: the producing GEMM's most recent output rows are still in L2
+  const int r = (kRev ? gridDim.x - 1 - blockIdx.x : blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= rows) return;
   const R* rr = resid + (int64_t)r * h;
   const Y* yr = y + (int64_t)r * h;
@@ -203,7 +215,8 @@ int launch_ln(const void* resid_v, const void* y, const float* bias, const float
                                          (uintptr_t)out_h | (uintptr_t)gamma | (uintptr_t)beta |
                                          (uintptr_t)bias) & 15);
 #define SC_LN_ARGS resid, yy, bias, gamma, beta, out, oh, bad, rows, h
-  if (vec && h == 768) residual_ln_vec_kernel<R, Y, 6><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  if (vec && h == 768 && !elt_reverse()) residual_ln_vec_kernel<R, Y, 6, false><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
+  else if (vec && h == 768) residual_ln_vec_kernel<R, Y, 6><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
   else if (vec && h == 384) residual_ln_vec_kernel<R, Y, 3><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
   else if (vec && h == 1024) residual_ln_vec_kernel<R, Y, 8><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
   else if (vec && h == 512) residual_ln_vec_kernel<R, Y, 4><<<blocks, 256, 0, st>>>(SC_LN_ARGS);
@@ -300,27 +313,30 @@ __device__ __forceinline__ void gelu_bf16x8(uint4& u, const float* __restrict__ 
 // math: ~48 KB of loads in flight per SM at 4 CTAs x 256 threads, enough to
 // cover HBM latency (2 vectors/thread at 3 CTAs/SM measured 74% of copy BW,
 // stalled on long scoreboard).
-template <bool kBias>
+template <bool kBias, bool kRev = true>
 __global__ void __launch_bounds__(256, 4) bias_gelu_bf16x8_kernel(__nv_bfloat16* __restrict__ x,
                                                                  const float* __restrict__ bias, int64_t n8,
                                                                  int cols) {
   constexpr int U = 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   uint4* xv = reinterpret_cast<uint4*>(x);
+  // walked last-to-first (vector n8-1-i): the W1 GEMM's most recent output is still in L2
+  const int64_t last = n8 - 1;
+  auto at = [&](int64_t k) { return kRev ? last - k : k; };
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + (U - 1) * stride < n8; i += U * stride) {
     uint4 u[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) u[k] = __ldcs(xv + i + k * stride);
+    for (int k = 0; k < U; ++k) u[k] = __ldcs(xv + at(i + k * stride));
 #pragma unroll
-    for (int k = 0; k < U; ++k) gelu_bf16x8<kBias>(u[k], bias, i + k * stride, cols);
+    for (int k = 0; k < U; ++k) gelu_bf16x8<kBias>(u[k], bias, at(i + k * stride), cols);
 #pragma unroll
-    for (int k = 0; k < U; ++k) __stcs(xv + i + k * stride, u[k]);
+    for (int k = 0; k < U; ++k) __stcs(xv + at(i + k * stride), u[k]);
   }
   for (; i < n8; i += stride) {
-    uint4 v = xv[i];
-    gelu_bf16x8<kBias>(v, bias, i, cols);
-    xv[i] = v;
+    uint4 v = xv[at(i)];
+    gelu_bf16x8<kBias>(v, bias, at(i), cols);
+    xv[at(i)] = v;
   }
 }
 
@@ -401,8 +417,10 @@ extern "C" int sc_bias_gelu(void* x, const float* bias, int32_t dtype, int64_t r
     unsigned blocks = grid_cap((n8 + 3) / 4, 4);
     if (bias)
       bias_gelu_bf16x8_kernel<true><<<blocks, 256, 0, st>>>((__nv_bfloat16*)x, bias, n8, cols);
-    else
+    else if (elt_reverse())
       bias_gelu_bf16x8_kernel<false><<<blocks, 256, 0, st>>>((__nv_bfloat16*)x, bias, n8, cols);
+    else
+      bias_gelu_bf16x8_kernel<false, false><<<blocks, 256, 0, st>>>((__nv_bfloat16*)x, bias, n8, cols);
   } else if (dtype == SC_DTYPE_BF16) {
     unsigned blocks = grid_cap(n, 16);
     bias_gelu_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((__nv_bfloat16*)x, bias, n, cols);
