@@ -14,12 +14,16 @@ from .attention import (
     AttentionPattern,
     apply_pattern,
     attend_packed,
+    attend_segments,
     full_pattern,
+    full_attention,
     group_attention,
     longformer_pattern,
     make_pattern,
+    masked_segment_softmax,
     qds_pattern,
     sparse_pattern,
+    windowed_cross_attention,
 )
 from .band import BandShapeError, band_apply, band_pv, band_qk, band_scores, band_validity
 from .encoder import (

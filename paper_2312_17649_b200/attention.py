@@ -296,3 +296,105 @@ def apply_pattern(partition, qkv: dict, pattern: AttentionPattern, scale: float 
     if scale is None:
         scale = math.sqrt(qkv["cls"][0].shape[-1])
     return tuple(_run_groups(qkv, pattern, scale, padding))
+
+
+# ---------------------------------------------------------------------------
+# Segment-level API (R/attention.py:228-400): arbitrary (K_i, V_i, w_i) tuples.
+# Band segments run on the sc_band_scores / sc_band_apply kernels, dense ones on
+# cuBLAS, the joint softmax in fp32 on the device.  Not the encoder hot path
+# (that is attend_packed's fused kernels), but the same numerics.
+# ---------------------------------------------------------------------------
+
+def masked_segment_softmax(values, valids, scale: float, padding: str = "exclude"):
+    """Joint softmax over score blocks with optional validity masks (R/attention.py:228-257).
+
+    values: tensors (..., rows, width_i); valids: matching bool masks or None.
+    In zero-logit mode invalid slots take part with logit 0."""
+    if padding not in PADDING_MODES:
+        raise AttentionError(f"unknown padding mode {padding!r}")
+    scaled = []
+    for val, ok in zip(values, valids):
+        y = val.float() / scale
+        if ok is not None:
+            fill = 0.0 if padding == "zero-logit" else -math.inf
+            y = torch.where(ok, y, torch.full_like(y, fill))
+        scaled.append(y)
+    row_max = torch.stack([y.amax(dim=-1) for y in scaled]).amax(dim=0)
+    if bool(torch.isneginf(row_max).any()):
+        raise AttentionError("a row has zero valid entries across all segments")
+    exps = [torch.exp(y - row_max[..., None]) for y in scaled]
+    denom = sum(e.sum(dim=-1, keepdim=True) for e in exps)
+    return [e / denom for e in exps]
+
+
+def attend_segments(q, segments, scale: float, padding: str = "exclude"):
+    """Windowed cross-attention core (R/attention.py:290-345).
+
+    segments: nonempty list of (k, v, window, extra_invalid); extra_invalid is an
+    optional bool (rows, 2w+1) mask of additionally excluded band slots (hard
+    exclusions in both padding modes) and must be None for unwindowed segments.
+    numpy in -> numpy out (float64 results are computed in fp32 on the device)."""
+    from .band import band_apply, band_scores, band_validity
+
+    if not segments:
+        raise AttentionError("segment tuple must be nonempty")
+    qt, was_np = _to_device(q)
+    qf = qt.float()
+    s = qf.shape[-2]
+    values, valids, metas = [], [], []
+    for k, v, window, extra in segments:
+        kt = _to_device(k)[0].float()
+        vt = _to_device(v)[0].float()
+        if qf.shape[-1] != kt.shape[-1]:
+            raise AttentionError("query/key feature dims differ")
+        if kt.shape[-2] != vt.shape[-2]:
+            raise AttentionError("key/value row counts differ")
+        if is_full(window):
+            if extra is not None:
+                raise AttentionError("extra_invalid only applies to windowed segments")
+            sc = torch.matmul(qf, kt.transpose(-1, -2))
+            ok = None
+        else:
+            w = int(window)
+            sc = band_scores(qf, kt, w)
+            ok = band_validity(s, w, kt.shape[-2], device=qf.device)
+            if extra is not None:
+                ex = _to_device(extra)[0].bool()
+                if padding == "zero-logit":
+                    sc = torch.where(ex, torch.full_like(sc, -math.inf), sc)
+                else:
+                    ok = ok & ~ex
+        values.append(sc)
+        valids.append(ok)
+        metas.append((vt, window))
+    probs = masked_segment_softmax(values, valids, scale, padding)
+    out = None
+    for p, (vt, window) in zip(probs, metas):
+        part = torch.matmul(p, vt) if is_full(window) else band_apply(p.contiguous(), vt, int(window))
+        out = part if out is None else out + part
+    if was_np:
+        return out.cpu().numpy().astype(np.asarray(q).dtype, copy=False)
+    return out
+
+
+def windowed_cross_attention(q, kv, padding: str = "exclude"):
+    """Attention of Q over (K_i, V_i, w_i) target segments, scale sqrt(d) (R/attention.py:381-400)."""
+    kv = list(kv)
+    if not kv:
+        raise AttentionError("segment tuple must be nonempty")
+    d = np.asarray(q).shape[-1] if not isinstance(q, torch.Tensor) else q.shape[-1]
+    segs = []
+    for k, v, window in kv:
+        vd = v.shape[-1]
+        if vd != d:
+            raise AttentionError("value feature dim differs from query")
+        segs.append((k, v, window, None))
+    return attend_segments(q, segs, math.sqrt(d), padding)
+
+
+def full_attention(q, k, v):
+    """Scaled dot-product attention softmax(Q K^T / sqrt(d)) V (R/attention.py:276-287)."""
+    qs, ks, vs = (x.shape for x in (q, k, v))
+    if qs[-1] != ks[-1] or ks[-2] != vs[-2]:
+        raise AttentionError(f"incompatible shapes: Q {tuple(qs)}, K {tuple(ks)}, V {tuple(vs)}")
+    return attend_segments(q, [(k, v, FULL, None)], math.sqrt(qs[-1]))

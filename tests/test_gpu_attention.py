@@ -283,3 +283,41 @@ def test_qds_tcgen05_vs_oracle(P, w, pad, algo):
         ref = np.concatenate(O.apply_pattern(spans, O.split_groups(spans, *blk), opat, math.sqrt(d), pad), axis=-2)
         np.testing.assert_allclose(out[r:r + s].reshape(s, H, d).transpose(1, 0, 2), ref, atol=2e-2, rtol=0)
         r += s
+
+
+@pytest.mark.parametrize("pad", ["exclude", "zero-logit"])
+@pytest.mark.parametrize("windows", [(math.inf, math.inf, 2), (0,), (3, math.inf), (40,)])
+def test_windowed_cross_attention_vs_oracle(P, pad, windows):
+    """Segment-level API (R/attention.py:290-400) on the device vs the oracle, numpy in / numpy out."""
+    rng = np.random.default_rng(37)
+    s, d = 23, 16
+    q = rng.standard_normal((2, s, d))
+    kv, segs = [], []
+    for i, w in enumerate(windows):
+        t = s if math.isfinite(w) else 5 + 3 * i
+        k, v = rng.standard_normal((2, t, d)), rng.standard_normal((2, t, d))
+        kv.append((k, v, w))
+        segs.append((k, v, w, None))
+    got = P.windowed_cross_attention(q, kv, pad) if pad == "exclude" else \
+        P.attend_segments(q, [(k, v, w, None) for k, v, w in kv], math.sqrt(d), pad)
+    ref = O.attend_segments(q, segs, math.sqrt(d), pad)
+    assert isinstance(got, np.ndarray) and got.dtype == q.dtype
+    np.testing.assert_allclose(got, ref, atol=1e-4, rtol=0)
+
+
+def test_full_attention_and_exclusions(P):
+    rng = np.random.default_rng(41)
+    q, k, v = (rng.standard_normal((3, 9, 8)).astype(np.float32) for _ in range(3))
+    ref = O.attend_segments(q, [(k, v, math.inf, None)], math.sqrt(8))
+    np.testing.assert_allclose(P.full_attention(q, k, v), ref, atol=1e-5)
+    # extra_invalid band exclusions (the QDS mechanism), both padding modes
+    extra = rng.random((9, 5)) < 0.3
+    extra[:, 2] = False  # keep the diagonal so every row has a valid slot
+    for pad in ("exclude", "zero-logit"):
+        segs = [(k, v, 2, extra)]
+        np.testing.assert_allclose(P.attend_segments(q, segs, 3.0, pad), O.attend_segments(q, segs, 3.0, pad),
+                                   atol=1e-5)
+    with pytest.raises(P.AttentionError):
+        P.attend_segments(q, [], 1.0)
+    with pytest.raises(P.AttentionError):
+        P.full_attention(q, k[:, :4], v)
