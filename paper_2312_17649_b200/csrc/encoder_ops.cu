@@ -48,6 +48,29 @@ __device__ __forceinline__ void flag_nonfinite(int32_t* bad, bool any_bad) {
   if (bad && __any_sync(0xffffffffu, any_bad) && (threadIdx.x & 31) == 0) atomicAdd(bad, 1);
 }
 
+// Vectorised embedding (h % 128 == 0, 16-byte aligned tables): one warp per
+// token, float4 table reads, bf16x4 / float4 stores.
+__global__ void __launch_bounds__(256) embed_vec_kernel(const int32_t* __restrict__ ids,
+                                                        const int32_t* __restrict__ pos,
+                                                        const float* __restrict__ tok,
+                                                        const float* __restrict__ pe, float* __restrict__ x,
+                                                        __nv_bfloat16* __restrict__ xh, int T, int h) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= T) return;
+  const float4* a = reinterpret_cast<const float4*>(tok + (int64_t)__ldg(ids + r) * h);
+  const float4* b = reinterpret_cast<const float4*>(pe + (int64_t)__ldg(pos + r) * h);
+  for (int c = lane; c < h / 4; c += 32) {
+    const float4 u = __ldg(a + c), v = __ldg(b + c);
+    const float4 s = make_float4(u.x + v.x, u.y + v.y, u.z + v.z, u.w + v.w);
+    if (x) reinterpret_cast<float4*>(x + (int64_t)r * h)[c] = s;
+    if (xh) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(s.x, s.y), hi = __floats2bfloat162_rn(s.z, s.w);
+      reinterpret_cast<uint2*>(xh + (int64_t)r * h)[c] =
+          make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    }
+  }
+}
+
 // One warp per row, row cached in registers (h <= 32 * kPer).
 template <typename R, typename Y, int kPer>
 __global__ void residual_ln_kernel(const R* __restrict__ resid, const Y* __restrict__ y,
@@ -370,9 +393,15 @@ extern "C" int sc_embed(const int32_t* ids, const int32_t* tok_pos, const float*
   SC_CHECK_ARG(ids && tok_pos && tok_emb && pos_emb && (x || xh), "sc_embed: null pointer");
   SC_CHECK_ARG(total_tokens >= 0 && hidden >= 1, "sc_embed: bad shape");
   if (total_tokens == 0) return SC_OK;
-  int threads = hidden >= 256 ? 256 : 32 * ((hidden + 31) / 32);
-  embed_kernel<<<total_tokens, threads, 0, (cudaStream_t)stream>>>(
-      ids, tok_pos, tok_emb, pos_emb, x, (__nv_bfloat16*)xh, total_tokens, hidden);
+  const bool vec = hidden % 128 == 0 && !(((uintptr_t)tok_emb | (uintptr_t)pos_emb | (uintptr_t)x | (uintptr_t)xh) & 15);
+  if (vec) {
+    embed_vec_kernel<<<(total_tokens + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
+        ids, tok_pos, tok_emb, pos_emb, x, (__nv_bfloat16*)xh, total_tokens, hidden);
+  } else {
+    int threads = hidden >= 256 ? 256 : 32 * ((hidden + 31) / 32);
+    embed_kernel<<<total_tokens, threads, 0, (cudaStream_t)stream>>>(
+        ids, tok_pos, tok_emb, pos_emb, x, (__nv_bfloat16*)xh, total_tokens, hidden);
+  }
   SC_CHECK_LAUNCH("embed_kernel");
   return SC_OK;
 }

@@ -57,9 +57,10 @@ def test_residual_layernorm(lib, ydtype, h):
     torch.testing.assert_close(outh, ref.to(torch.bfloat16), atol=0.02, rtol=0.01)
 
 
-def test_embed_and_cls_score(lib):
+@pytest.mark.parametrize("h", [96, 768])
+def test_embed_and_cls_score(lib, h):
     g = torch.Generator(device="cuda").manual_seed(2)
-    V, P, h, T = 50, 30, 96, 40
+    V, P, T = 50, 30, 40
     tok = torch.randn((V, h), device="cuda", generator=g)
     pos = torch.randn((P, h), device="cuda", generator=g)
     ids = torch.randint(0, V, (T,), device="cuda", generator=g, dtype=torch.int32)
@@ -70,6 +71,7 @@ def test_embed_and_cls_score(lib):
              T, h, lib.stream_handle())
     ref = tok[ids.long()] + pos[tp.long()]
     torch.testing.assert_close(x, ref)
+    torch.testing.assert_close(xh, ref.to(torch.bfloat16))
     cu = torch.tensor([0, 15, 40], dtype=torch.int32, device="cuda")
     w = torch.randn(h, device="cuda", generator=g)
     sc = torch.empty(2, device="cuda")
