@@ -233,6 +233,37 @@ __device__ __forceinline__ void pv16(uint32_t vbuf, int key0, const LaneOff& lo,
   }
 }
 
+// Single n8 block variants for the last 8 band keys of a row block (w <= 4:
+// 16 rows + 2w keys fit 24 columns): S = Q . K[key0 .. key0+7]^T, and
+// O += P . V[key0 .. key0+7] with m16n8k8 (key0 a multiple of 8).
+__device__ __forceinline__ void mma1688(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(b0));
+}
+__device__ __forceinline__ void qk8(uint32_t kbuf, int key0, int lane, const uint32_t (&qa)[4][4], float (&s0)[4]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s0[e] = 0.f;
+#pragma unroll
+  for (int k2 = 0; k2 < 2; ++k2) {
+    uint32_t b[4];
+    ldsm_x4(swz(kbuf, key0 + (lane & 7), 4 * k2 + (lane >> 3)), b);
+    mma16816(s0, qa[2 * k2], b[0], b[1]);
+    mma16816(s0, qa[2 * k2 + 1], b[2], b[3]);
+  }
+}
+__device__ __forceinline__ void pv8(uint32_t vbuf, int key0, int lane, const float (&p0)[4], float (&o)[8][4]) {
+  const uint32_t a0 = pack_bf16(p0[0], p0[1]), a1 = pack_bf16(p0[2], p0[3]);
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    uint32_t b[4];
+    ldsm_x4_t(swz(vbuf, key0 + (lane & 7), 4 * half + (lane >> 3)), b);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mma1688(o[4 * half + i], a0, a1, b[i]);
+  }
+}
+
 // Online-softmax update over NB n8 blocks of RAW logits (masked to -inf) for
 // rows (g, g+8).  m is kept in raw-logit units; c2 = log2(e)/scale.  Overwrites s with P.
 // kFresh: o is still zero (first update of a row block) -> skip the O rescale.
@@ -283,7 +314,8 @@ __device__ __forceinline__ void zero_o(float (&o)[8][4]) {
 }
 // NBC: band chunks of 32 keys per 16-row warp block (ceil((16+2w)/32)).
 // GR: global rows staged per head (16 or 32).  NS: pipeline stages.
-template <int NBC, int GR, int NS>
+// NBB: band n8 blocks of the single-shot path (NBC = 1): 3 when 16 + 2w <= 24.
+template <int NBC, int GR, int NS, int NBB = 4>
 __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQf,
     const __grid_constant__ CUtensorMap tmKg, const __grid_constant__ CUtensorMap tmVg,
@@ -468,26 +500,28 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         if constexpr (NBC == 1) {
           // Single shot: all keys of the row block (globals + band) in one softmax.
           constexpr int NG = GR / 8;
-          float sc[NG + 4][4];
+          float sc[NG + NBB][4];
   #pragma unroll
           for (int gc = 0; gc < GR / 16; ++gc) qk16(kg_buf(s), gc * 16, LO, qa, sc[2 * gc], sc[2 * gc + 1]);
           qk16(kb_buf(s), wr0, LO, qa, sc[NG], sc[NG + 1]);
-          qk16(kb_buf(s), wr0 + 16, LO, qa, sc[NG + 2], sc[NG + 3]);
+          if constexpr (NBB == 4) qk16(kb_buf(s), wr0 + 16, LO, qa, sc[NG + 2], sc[NG + 3]);
+          else qk8(kb_buf(s), wr0 + 16, lane, qa, sc[NG + 2]);
   #pragma unroll
           for (int nb = 0; nb < NG; ++nb)
   #pragma unroll
             for (int e = 0; e < 4; ++e)
               if (!((gmask[nb >> 1] >> ((nb & 1) * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
   #pragma unroll
-          for (int nb = 0; nb < 4; ++nb)
+          for (int nb = 0; nb < NBB; ++nb)
   #pragma unroll
             for (int e = 0; e < 4; ++e)
               if (!((bmask[0] >> (nb * 4 + e)) & 1)) sc[NG + nb][e] = -INFINITY;
-          softmax_update<NG + 4, true>(sc, c2, m0, m1, l0, l1, o);
+          softmax_update<NG + NBB, true>(sc, c2, m0, m1, l0, l1, o);
   #pragma unroll
           for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, LO, sc[2 * gc], sc[2 * gc + 1], o);
           pv16(vb_buf(s), wr0, LO, sc[NG], sc[NG + 1], o);
-          pv16(vb_buf(s), wr0 + 16, LO, sc[NG + 2], sc[NG + 3], o);
+          if constexpr (NBB == 4) pv16(vb_buf(s), wr0 + 16, LO, sc[NG + 2], sc[NG + 3], o);
+          else pv8(vb_buf(s), wr0 + 16, lane, sc[NG + 2], o);
         } else {
           // global keys: cls (key 0) and the query group (keys 1..G-1)
   #pragma unroll
@@ -778,15 +812,15 @@ constexpr int stages_for() {
   return (3 * stage_bytes <= budget) ? 3 : 2;
 }
 
-template <int NBC, int GR>
+template <int NBC, int GR, int NBB = 4>
 static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, cudaStream_t st) {
   constexpr int NS = stages_for<NBC, GR>();
   constexpr int stage_bytes = (BM + 3 * GR + 2 * (48 + 32 * NBC)) * ROWB;
   constexpr size_t smem = (size_t)NS * stage_bytes + 2 * NS * 8 + 64 + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS, NBB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS, NBB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess) {
       set_error("band kernel: shared memory request of %zu bytes failed", smem);
       return SC_ERR_UNSUPPORTED;
@@ -802,7 +836,7 @@ static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, c
     if (num_sms <= 0) num_sms = 148;
   }
   const unsigned slots = (unsigned)(num_sms * min_ctas(NBC));
-  band_attn_kernel<NBC, GR, NS><<<grid < slots ? grid : slots, NTHREADS, smem, st>>>(
+  band_attn_kernel<NBC, GR, NS, NBB><<<grid < slots ? grid : slots, NTHREADS, smem, st>>>(
       maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
   SC_CHECK_LAUNCH("band_attn_kernel");
   return SC_OK;
@@ -811,7 +845,7 @@ static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, c
 template <int GR>
 static int launch_gr(int nbc, const CUtensorMap* maps, const Params& p, unsigned grid, cudaStream_t st) {
   switch (nbc) {
-    case 1: return launch_one<1, GR>(maps, p, grid, st);
+    case 1: return p.w <= 4 ? launch_one<1, GR, 3>(maps, p, grid, st) : launch_one<1, GR>(maps, p, grid, st);
     case 2: return launch_one<2, GR>(maps, p, grid, st);
     case 3: return launch_one<3, GR>(maps, p, grid, st);
     case 4: return launch_one<4, GR>(maps, p, grid, st);
