@@ -189,6 +189,15 @@ SC_API int sc_residual_layernorm_ex(const void* resid, int32_t resid_dtype, cons
                              int32_t* nonfinite_count, int32_t rows, int32_t hidden,
                              void* stream);
 
+/* Fused FFN up-projection (bf16): out[M][N] = gelu_erf(a[M][K] w[N][K]^T + bias)
+ * (R/encoder.py:350-351 with :258-259), one tcgen05 GEMM whose epilogue applies
+ * bias and GELU before the single bf16 store.  a, w, out bf16 row-major with
+ * row strides lda / ldw / ldo (elements); bias fp32 [N] or NULL.  Returns
+ * SC_ERR_UNSUPPORTED unless N % 256 == 0, K % 64 == 0 and rows are 16-byte
+ * aligned (callers then use cuBLAS + sc_bias_gelu). */
+SC_API int sc_gemm_bias_gelu(const void* a, int64_t lda, const void* w, int64_t ldw, const float* bias,
+                      void* out, int64_t ldo, int32_t M, int32_t N, int32_t K, void* stream);
+
 /* In-place exact-erf GELU with optional bias (R/encoder.py:258-259). */
 SC_API int sc_bias_gelu(void* x, const float* bias, int32_t dtype, int64_t rows, int32_t cols,
                  void* stream);

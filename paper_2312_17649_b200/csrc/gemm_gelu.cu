@@ -1,0 +1,218 @@
+// Fused FFN up-projection for the bf16 encoder: out = gelu_erf(A W^T + b)
+// (R/encoder.py:350-351, :258-259) in one tcgen05 GEMM whose epilogue applies
+// the bias and the exact-erf GELU before the single bf16 store -- the separate
+// GELU pass (read + write of the [T, 3072] activation, 14% of the encoder step
+// after cuBLAS) disappears.
+//
+// Persistent, warp-specialised, 1 CTA per SM:
+//   warp 0    TMA producer: A [128 x 64] and W [256 x 64] boxes (128B swizzle)
+//             into a 4-stage mbarrier ring
+//   warp 1    TMEM owner + single-thread tcgen05.mma issuer: D[128 x 256] fp32
+//             in TMEM, double-buffered across tiles (2 x 256 columns)
+//   warps 2-5 epilogue: tcgen05.ld of a 64-column chunk, + bias, GELU, bf16,
+//             swizzled st.shared into a staging buffer, TMA store; the next
+//             tile's mainloop runs into the other TMEM buffer meanwhile.
+// A is [M, K] row-major (K-major), W is [N, K] row-major (nn.Linear layout),
+// both UMMA operands K-major; requires N % 256 == 0, K % 64 == 0.
+#include "gelu.cuh"
+#include "tc_common.cuh"
+
+namespace sc {
+namespace gg {
+using namespace tcx;
+
+constexpr int BM = 128, BN = 256, BK = 64, NS = 4, ROWB = 128;
+constexpr int NTHREADS = 192;
+constexpr int A_BYTES = BM * ROWB, B_BYTES = BN * ROWB, STAGE = A_BYTES + B_BYTES;
+constexpr int STG_BYTES = BM * ROWB;  // one 128-row x 64-column bf16 staging chunk
+constexpr int SMEM_STG = NS * STAGE;
+constexpr int SMEM_BAR = SMEM_STG + 2 * STG_BYTES;
+constexpr int SMEM_TOTAL = SMEM_BAR + (2 * NS + 4) * 8 + 16;
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__global__ void __launch_bounds__(NTHREADS, 1) gemm_bias_gelu_kernel(
+    const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+    const __grid_constant__ CUtensorMap tmO, const float* __restrict__ bias, int M, int N, int K) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sm0 = smem_u32(smem);
+  const uint32_t bar0 = sm0 + SMEM_BAR;
+  const uint32_t full_bar = bar0, empty_bar = bar0 + 8 * NS, acc_full = bar0 + 16 * NS, acc_empty = acc_full + 16;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + SMEM_BAR + (2 * NS + 4) * 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_n = N / BN, tiles = ((M + BM - 1) / BM) * tiles_n, nk = K / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full_bar + 8 * s, 1);
+      mbar_init(empty_bar + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(acc_full + 8 * b, 1);
+      mbar_init(acc_empty + 8 * b, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      prefetch_map(&tmA);
+      prefetch_map(&tmB);
+      int it = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % NS;
+          if (it >= NS) mbar_wait(empty_bar + 8 * s, ((it / NS) & 1) ^ 1);
+          mbar_expect_tx(full_bar + 8 * s, STAGE);
+          tma_load_2d(sm0 + s * STAGE, &tmA, kb * BK, m0, full_bar + 8 * s);
+          tma_load_2d(sm0 + s * STAGE + A_BYTES, &tmB, kb * BK, n0, full_bar + 8 * s);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(BM, BN, 0);
+      int it = 0, i = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
+        const int buf = i & 1;
+        if (i >= 2) mbar_wait(acc_empty + 8 * buf, ((i >> 1) & 1) ^ 1);  // epilogue drained this buffer
+        tc_fence_after();
+        const uint32_t tD = tmem + buf * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % NS;
+          mbar_wait(full_bar + 8 * s, (it / NS) & 1);
+          tc_fence_after();
+          const uint64_t ad = sw128_desc(sm0 + s * STAGE), bd = sw128_desc(sm0 + s * STAGE + A_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < BK / 16; ++ks) mma_ss(tD, ad + 2 * ks, bd + 2 * ks, idesc, (kb > 0 || ks > 0));
+          tc_commit(empty_bar + 8 * s);
+        }
+        tc_commit(acc_full + 8 * buf);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------- epilogue
+    const int q = warp & 3;               // TMEM lane quadrant of this warp
+    const int r = q * 32 + lane;          // row within the tile
+    const int et = threadIdx.x - 64;      // epilogue thread 0..127
+    int i = 0, chunk = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
+      const int buf = i & 1;
+      const int m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+      mbar_wait(acc_full + 8 * buf, (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 64; ++c, ++chunk) {
+        uint32_t v[64];
+        TC_LD32(taddr + c * 64, v);
+        TC_LD32(taddr + c * 64 + 32, (&v[32]));
+        tc_wait_ld();
+        if (c == BN / 64 - 1) {  // accumulator fully read: hand the TMEM buffer back
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty + 8 * buf);
+        }
+        const float* bc = bias + n0 + c * 64;
+        uint32_t pk[32];
+#pragma unroll
+        for (int e = 0; e < 64; e += 2) {
+          float2 x = make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1]));
+          if (bias) {
+            const float2 bb = __ldg(reinterpret_cast<const float2*>(bc + e));
+            x.x += bb.x;
+            x.y += bb.y;
+          }
+          const float2 g = gelu2_bf16path(x);
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(g.x, g.y);
+          pk[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        // staging buffer (chunk & 1) is free once the TMA store issued two chunks ago has read it
+        const uint32_t stg = sm0 + SMEM_STG + (chunk & 1) * STG_BYTES;
+        if (et == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        epi_sync();
+#pragma unroll
+        for (int p16 = 0; p16 < 8; ++p16) {
+          const uint32_t addr = stg + r * ROWB + ((p16 ^ (r & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * p16]),
+                       "r"(pk[4 * p16 + 1]), "r"(pk[4 * p16 + 2]), "r"(pk[4 * p16 + 3])
+                       : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        epi_sync();
+        if (et == 0) tma_store_2d(&tmO, stg, n0 + c * 64, m0);
+      }
+    }
+    if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+}  // namespace gg
+}  // namespace sc
+
+using namespace sc;
+
+extern "C" int sc_gemm_bias_gelu(const void* a, int64_t lda, const void* w, int64_t ldw, const float* bias,
+                                 void* out, int64_t ldo, int32_t M, int32_t N, int32_t K, void* stream) {
+  using namespace gg;
+  SC_CHECK_ARG(a && w && out && M >= 0 && N >= 1 && K >= 1, "sc_gemm_bias_gelu: bad arguments");
+  if (M == 0) return SC_OK;
+  if (N % BN || K % BK || lda < K || ldw < K || ldo < N || (lda * 2) % 16 || (ldw * 2) % 16 || (ldo * 2) % 16 ||
+      (((uintptr_t)a | (uintptr_t)w | (uintptr_t)out) & 15) || (bias && ((uintptr_t)bias & 7))) {
+    set_error("sc_gemm_bias_gelu: needs N %% 256 == 0, K %% 64 == 0 and 16-byte aligned rows");
+    return SC_ERR_UNSUPPORTED;
+  }
+  CUtensorMap mA, mB, mO;
+  if (!make_map(&mA, a, K, M, lda, BM) || !make_map(&mB, w, K, N, ldw, BN) || !make_map(&mO, out, N, M, ldo, BM)) {
+    set_error("sc_gemm_bias_gelu: cuTensorMapEncodeTiled failed");
+    return SC_ERR_UNSUPPORTED;
+  }
+  static bool attr = false;
+  const size_t smem = SMEM_TOTAL + 1024;
+  if (!attr) {
+    if (cudaFuncSetAttribute(gemm_bias_gelu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess) {
+      set_error("sc_gemm_bias_gelu: shared memory request of %zu bytes failed", smem);
+      return SC_ERR_UNSUPPORTED;
+    }
+    attr = true;
+  }
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (num_sms <= 0) num_sms = 148;
+  }
+  const int tiles = ((M + BM - 1) / BM) * (N / BN);
+  gemm_bias_gelu_kernel<<<tiles < num_sms ? tiles : num_sms, NTHREADS, smem, (cudaStream_t)stream>>>(
+      mA, mB, mO, bias, M, N, K);
+  SC_CHECK_LAUNCH("gemm_bias_gelu_kernel");
+  return SC_OK;
+}

@@ -265,7 +265,8 @@ class CrossEncoder:
     """Config + device weights; batched inference (R/encoder.py:450-538)."""
 
     def __init__(self, config: EncoderConfig, weights: dict | None = None, seed: int = 0,
-                 device="cuda", attn_algo: str = "auto", prune_last_layer: bool = False):
+                 device="cuda", attn_algo: str = "auto", prune_last_layer: bool = False,
+                 fused_ffn: bool = True):
         """``prune_last_layer``: the scoring entry points (score*, GraphedScorer) run
         the last layer for the [CLS] rows only past the K/V projection -- the score
         reads nothing else (R/encoder.py:506).  Scores are unchanged; the reference's
@@ -275,6 +276,8 @@ class CrossEncoder:
         self.device = torch.device(device)
         self.attn_algo = attn_algo
         self.prune_last_layer = prune_last_layer
+        # bf16: W1 + bias + GELU as one tcgen05 GEMM (sc_gemm_bias_gelu); False -> cuBLAS + GELU pass
+        self.fused_ffn = fused_ffn
         host = init_weights(config, seed) if weights is None else weights
         self.host_weights = host
         self._upload(host)
@@ -310,7 +313,7 @@ class CrossEncoder:
                 "wqkv": gemm_w(wqkv), "bqkv": f32(bqkv).to(cd),
                 "wo": gemm_w(w[p + "wo"]), "bo": f32(w[p + "bo"]).to(cd),
                 "ln1_g": f32(w[p + "ln1_g"]), "ln1_b": f32(w[p + "ln1_b"]),
-                "w1": gemm_w(w[p + "w1"]), "b1": f32(w[p + "b1"]).to(cd),
+                "w1": gemm_w(w[p + "w1"]), "b1": f32(w[p + "b1"]).to(cd), "b1_f32": f32(w[p + "b1"]),
                 "w2": gemm_w(w[p + "w2"]), "b2": f32(w[p + "b2"]).to(cd),
                 "ln2_g": f32(w[p + "ln2_g"]), "ln2_b": f32(w[p + "ln2_b"]),
             })
@@ -383,8 +386,7 @@ class CrossEncoder:
                 _lib.call("sc_residual_layernorm_ex", xr.data_ptr(), rdt, y.data_ptr(), dcode, None,
                           L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), None if bf16 else x1.data_ptr(),
                           x1.data_ptr() if bf16 else None, None, T, h, stream, exc=EncoderError)
-                f = F.linear(x1, L["w1"], L["b1"])
-                _lib.call("sc_bias_gelu", f.data_ptr(), None, dcode, T, cfg.ff_dim, stream, exc=EncoderError)
+                f = self._ffn_up(x1, L, T, stream)
                 f2 = F.linear(f, L["w2"], L["b2"])
                 _lib.call("sc_residual_layernorm_ex", x1.data_ptr(), rdt, f2.data_ptr(), dcode, None,
                           L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(),
@@ -392,6 +394,26 @@ class CrossEncoder:
                           bad.data_ptr() + 4 * i if check_finite else None, T, h, stream, exc=EncoderError)
         self._last_bad = bad if check_finite else None
         return x
+
+    def _ffn_up(self, x1: torch.Tensor, L: dict, rows: int, stream) -> torch.Tensor:
+        """gelu_erf(x1 W1^T + b1) (R/encoder.py:350-351): bf16 -> the fused tcgen05 GEMM with the
+        bias + GELU epilogue (sc_gemm_bias_gelu); fp32 parity path (or an unsupported shape) ->
+        cuBLAS + the separate sc_bias_gelu pass."""
+        cfg = self.config
+        if cfg.torch_dtype == torch.bfloat16 and self.fused_ffn:
+            f = torch.empty((rows, cfg.ff_dim), dtype=torch.bfloat16, device=self.device)
+            rc = _lib.load().sc_gemm_bias_gelu(x1.data_ptr(), x1.stride(0), L["w1"].data_ptr(), L["w1"].stride(0),
+                                               L["b1_f32"].data_ptr(), f.data_ptr(), f.stride(0), rows,
+                                               cfg.ff_dim, cfg.embed_dim, stream)
+            if rc == _lib.SC_OK:
+                _lib.launch_calls += 1
+                return f
+            if rc != _lib.SC_ERR_UNSUPPORTED:
+                raise EncoderError(_lib.last_error())
+        f = F.linear(x1, L["w1"], L["b1"])
+        dcode = _lib.DTYPE_BF16 if cfg.torch_dtype == torch.bfloat16 else _lib.DTYPE_F32
+        _lib.call("sc_bias_gelu", f.data_ptr(), None, dcode, rows, cfg.ff_dim, stream, exc=EncoderError)
+        return f
 
     def _cls_last_layer(self, L, xr, layout, pattern, bad, i):
         """Last layer for the [CLS] rows only (R/encoder.py:306-371 restricted to the rows
@@ -414,8 +436,7 @@ class CrossEncoder:
         _lib.call("sc_residual_layernorm_ex", xc.data_ptr(), dcode, y.data_ptr(), dcode, None,
                   L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), None if bf16 else x1.data_ptr(),
                   x1.data_ptr() if bf16 else None, None, n, h, stream, exc=EncoderError)
-        f = F.linear(x1, L["w1"], L["b1"])
-        _lib.call("sc_bias_gelu", f.data_ptr(), None, dcode, n, cfg.ff_dim, stream, exc=EncoderError)
+        f = self._ffn_up(x1, L, n, stream)
         f2 = F.linear(f, L["w2"], L["b2"])
         out = torch.empty((n, h), dtype=torch.float32, device=self.device)
         _lib.call("sc_residual_layernorm_ex", x1.data_ptr(), dcode, f2.data_ptr(), dcode, None,

@@ -183,3 +183,18 @@ def test_head_rows_mode_matches_full_attention(P, name, w):
         torch.testing.assert_close(head[rows], full[rows], atol=1e-2, rtol=0)
         assert head[r + m + 2: r + m + n + 3].abs().max().item() == 0  # doc rows untouched
         r += m + n + 3
+
+
+def test_fused_ffn_matches_cublas_path(P):
+    """bf16 encoder with the fused tcgen05 W1+bias+GELU GEMM == cuBLAS + GELU pass (bf16 tolerance)."""
+    cfg = P.EncoderConfig(**{**cases.ELECTRA_PASSAGE, "layers": 4, "precision": "bf16"})
+    fused = P.CrossEncoder(cfg, seed=0)
+    plain = P.CrossEncoder(cfg, weights=fused.host_weights, fused_ffn=False)
+    seqs = [rerank_ids(3, j, int(n), cfg.vocab_size, cfg.max_positions, P) for j, n in enumerate([164, 90, 7, 300, 41])]
+    batch = P.PackedBatch.from_sequences(seqs)
+    a = fused.score_packed(batch).cpu().numpy()
+    b = plain.score_packed(batch).cpu().numpy()
+    np.testing.assert_allclose(a, b, atol=2e-2, rtol=0)
+    ref = np.array([P.CrossEncoder(P.EncoderConfig(**{**cases.ELECTRA_PASSAGE, "layers": 4, "precision": "f32"}),
+                                   weights=fused.host_weights).score(s.ids, s.partition)[0] for s in seqs[:2]])
+    np.testing.assert_allclose(a[:2], ref, atol=2e-2, rtol=0)

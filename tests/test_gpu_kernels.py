@@ -127,3 +127,23 @@ def test_residual_layernorm_ex(lib, rdtype, h):
     with pytest.raises(ValueError):
         lib.call("sc_residual_layernorm_ex", resid.data_ptr(), rd, y.data_ptr(), 1, None, gamma.data_ptr(),
                  beta.data_ptr(), None, None, None, rows, h, lib.stream_handle())
+
+
+@pytest.mark.parametrize("M,N,K", [(1000, 3072, 768), (128, 256, 64), (37, 512, 192)])
+@pytest.mark.parametrize("with_bias", [True, False])
+def test_gemm_bias_gelu_vs_torch(lib, M, N, K, with_bias):
+    """Fused tcgen05 FFN up-projection: gelu_erf(x W^T + b) vs a plain PyTorch fp32 reference."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = (torch.randn((M, K), device="cuda", generator=g)).to(torch.bfloat16)
+    w = (torch.randn((N, K), device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    b = torch.randn(N, device="cuda", generator=g) if with_bias else None
+    ref = torch_gelu_erf(x.float() @ w.float().t() + (b if with_bias else 0.0))
+    out = torch.empty((M, N), device="cuda", dtype=torch.bfloat16)
+    lib.call("sc_gemm_bias_gelu", x.data_ptr(), K, w.data_ptr(), K, None if b is None else b.data_ptr(),
+             out.data_ptr(), N, M, N, K, lib.stream_handle())
+    # one bf16 rounding of the output (fp32 accumulation order differs from torch's)
+    excess = (out.float() - ref).abs() - 2 ** -8 * ref.abs()
+    assert excess.max().item() <= 2e-3
+    with pytest.raises(NotImplementedError):
+        lib.call("sc_gemm_bias_gelu", x.data_ptr(), K, w.data_ptr(), K, None, out.data_ptr(), N, M, N - 8, K,
+                 lib.stream_handle())
