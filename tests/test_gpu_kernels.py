@@ -147,3 +147,26 @@ def test_gemm_bias_gelu_vs_torch(lib, M, N, K, with_bias):
     with pytest.raises(NotImplementedError):
         lib.call("sc_gemm_bias_gelu", x.data_ptr(), K, w.data_ptr(), K, None, out.data_ptr(), N, M, N - 8, K,
                  lib.stream_handle())
+
+
+def test_gemm_bias_gelu_cta_pair_variant():
+    """The opt-in cta_group::2 variant (SC_GEMM_2SM=1) gives the same result as the one-CTA kernel."""
+    import subprocess
+    import sys
+    code = (
+        "import math, torch, sys; sys.path.insert(0, '.');"
+        "from paper_2312_17649_b200 import _lib;"
+        "g = torch.Generator(device='cuda').manual_seed(7);"
+        "x = torch.randn((700, 768), device='cuda', generator=g).to(torch.bfloat16);"
+        "w = (torch.randn((1024, 768), device='cuda', generator=g) / 28).to(torch.bfloat16);"
+        "b = torch.randn(1024, device='cuda', generator=g);"
+        "o = torch.empty((700, 1024), device='cuda', dtype=torch.bfloat16);"
+        "_lib.call('sc_gemm_bias_gelu', x.data_ptr(), 768, w.data_ptr(), 768, b.data_ptr(), o.data_ptr(), 1024, 700, 1024, 768, _lib.stream_handle());"
+        "ref = torch.nn.functional.gelu(x.float() @ w.float().t() + b);"
+        "err = ((o.float() - ref).abs() - 2 ** -8 * ref.abs()).max().item();"
+        "assert err <= 2e-3, err; print('ok', err)")
+    import os
+    env = dict(os.environ, SC_GEMM_2SM="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
