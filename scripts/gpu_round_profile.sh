@@ -19,5 +19,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:band_attn -c 1 -o $OUT/band_w4 python scripts/attn_sweep.py --windows 4 --iters 1 > $OUT/ncu_band.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc_attn -c 1 -o $OUT/tc_w256 python scripts/attn_sweep.py --windows 256 --iters 1 > $OUT/ncu_tc.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc_attn -c 1 -o $OUT/tc_full python scripts/attn_sweep.py --windows inf --patterns full --iters 1 >> $OUT/ncu_tc.log 2>&1
-timeout 600 ncu --set full --clock-control none -k regex:"bias_gelu|residual_ln" -s 30 -c 2 -o $OUT/elt python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_elt.log 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:"gemm_bias_gelu|residual_ln" -s 30 -c 2 -o $OUT/elt python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_elt.log 2>&1
 ls -la $OUT
