@@ -39,6 +39,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
 }
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+template <bool kGelu = true>
 __global__ void __launch_bounds__(NTHREADS, 1) gemm_bias_gelu_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
     const __grid_constant__ CUtensorMap tmO, const float* __restrict__ bias, int M, int N, int K) {
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_bias_gelu_kernel(
         for (int e = 0; e < 64; e += 2) {
           const float2 x = __fadd2_rn(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])),
                                       *reinterpret_cast<const float2*>(bc + e));
-          const float2 g = gelu2_bf16path_1mufu(x);
+          const float2 g = kGelu ? gelu2_bf16path_1mufu(x) : x;
           __nv_bfloat162 h2 = __floats2bfloat162_rn(g.x, g.y);
           pk[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
         }
@@ -422,16 +423,27 @@ extern "C" int sc_gemm_bias_gelu(const void* a, int64_t lda, const void* w, int6
   static bool attr = false;
   const size_t smem = SMEM_TOTAL + 1024;
   if (!attr) {
-    if (cudaFuncSetAttribute(gemm_bias_gelu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess) {
+    if (cudaFuncSetAttribute(gemm_bias_gelu_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(gemm_bias_gelu_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess) {
       set_error("sc_gemm_bias_gelu: shared memory request of %zu bytes failed", smem);
       return SC_ERR_UNSUPPORTED;
     }
     attr = true;
   }
   const int tiles = ((M + BM - 1) / BM) * (N / BN);
-  gemm_bias_gelu_kernel<<<tiles < num_sms ? tiles : num_sms, NTHREADS, smem, (cudaStream_t)stream>>>(
-      mA, mB, mO, bias, M, N, K);
+  static int no_gelu = -1;  // SC_GEMM_NO_GELU=1: bias-only epilogue (measurement of the mainloop alone)
+  if (no_gelu < 0) {
+    const char* e = getenv("SC_GEMM_NO_GELU");
+    no_gelu = e ? (atoi(e) != 0) : 0;
+  }
+  if (no_gelu)
+    gemm_bias_gelu_kernel<false><<<tiles < num_sms ? tiles : num_sms, NTHREADS, smem, (cudaStream_t)stream>>>(
+        mA, mB, mO, bias, M, N, K);
+  else
+    gemm_bias_gelu_kernel<true><<<tiles < num_sms ? tiles : num_sms, NTHREADS, smem, (cudaStream_t)stream>>>(
+        mA, mB, mO, bias, M, N, K);
   SC_CHECK_LAUNCH("gemm_bias_gelu_kernel");
   return SC_OK;
 }
