@@ -198,6 +198,18 @@ SC_API int sc_residual_layernorm_ex(const void* resid, int32_t resid_dtype, cons
 SC_API int sc_gemm_bias_gelu(const void* a, int64_t lda, const void* w, int64_t ldw, const float* bias,
                       void* out, int64_t ldo, int32_t M, int32_t N, int32_t K, void* stream);
 
+/* Fused output projection + residual + LayerNorm (bf16): out[M][768] =
+ * LN(resid + a[M][K] w[768][K]^T + bias) * gamma + beta, eps 1e-12 (R/encoder.py:345-347,
+ * :352-354, :267-273): a cluster of three CTAs per 128-row block, each owning a
+ * 256-column slice, exchanging per-row (mean, M2) through distributed shared
+ * memory.  resid/out bf16 (may not alias), out_f32 (fp32 copy) and
+ * nonfinite_count (R/encoder.py:356-357) optional.  SC_ERR_UNSUPPORTED unless
+ * N == 768, K % 64 == 0 and rows are 16-byte aligned. */
+SC_API int sc_gemm_residual_layernorm(const void* a, int64_t lda, const void* w, int64_t ldw, const float* bias,
+                               const void* resid, int64_t ldr, const float* gamma, const float* beta,
+                               void* out, int64_t ldo, float* out_f32, int64_t ldf,
+                               int32_t* nonfinite_count, int32_t M, int32_t N, int32_t K, void* stream);
+
 /* In-place exact-erf GELU with optional bias (R/encoder.py:258-259). */
 SC_API int sc_bias_gelu(void* x, const float* bias, int32_t dtype, int64_t rows, int32_t cols,
                  void* stream);

@@ -16,28 +16,18 @@
 // A is [M, K] row-major (K-major), W is [N, K] row-major (nn.Linear layout),
 // both UMMA operands K-major; requires N % 256 == 0, K % 64 == 0.
 #include "gelu.cuh"
-#include "tc_common.cuh"
+#include "gemm_common.cuh"
 
 namespace sc {
 namespace gg {
 using namespace tcx;
 
-constexpr int BM = 128, BN = 256, BK = 64, NS = 4, ROWB = 128;
-constexpr int NTHREADS = 192;
-constexpr int A_BYTES = BM * ROWB, B_BYTES = BN * ROWB, STAGE = A_BYTES + B_BYTES;
-constexpr int STG_BYTES = BM * ROWB;  // one 128-row x 64-column bf16 staging chunk
+constexpr int NS = 4;
 constexpr int SMEM_STG = NS * STAGE;
 constexpr int SMEM_BAR = SMEM_STG + 2 * STG_BYTES;
 constexpr int SMEM_BIAS = SMEM_BAR + (2 * NS + 4) * 8 + 16;  // BN fp32 bias slice of the current tile
 constexpr int SMEM_TOTAL = SMEM_BIAS + BN * 4;
 
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
-               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(src)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 template <bool kGelu = true>
 __global__ void __launch_bounds__(NTHREADS, 1) gemm_bias_gelu_kernel(

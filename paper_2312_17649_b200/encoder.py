@@ -266,7 +266,7 @@ class CrossEncoder:
 
     def __init__(self, config: EncoderConfig, weights: dict | None = None, seed: int = 0,
                  device="cuda", attn_algo: str = "auto", prune_last_layer: bool = False,
-                 fused_ffn: bool = True):
+                 fused_ffn: bool = True, fused_ln: bool = False):
         """``prune_last_layer``: the scoring entry points (score*, GraphedScorer) run
         the last layer for the [CLS] rows only past the K/V projection -- the score
         reads nothing else (R/encoder.py:506).  Scores are unchanged; the reference's
@@ -278,6 +278,8 @@ class CrossEncoder:
         self.prune_last_layer = prune_last_layer
         # bf16: W1 + bias + GELU as one tcgen05 GEMM (sc_gemm_bias_gelu); False -> cuBLAS + GELU pass
         self.fused_ffn = fused_ffn
+        # bf16, opt-in: Wo / W2 + bias + residual + LayerNorm as cluster-of-3 tcgen05 GEMMs
+        self.fused_ln = fused_ln
         host = init_weights(config, seed) if weights is None else weights
         self.host_weights = host
         self._upload(host)
@@ -382,18 +384,44 @@ class CrossEncoder:
                               check=(i == 0))
                 if attn_hook:
                     attn_hook("end")
-                y = F.linear(o, L["wo"], L["bo"])
-                _lib.call("sc_residual_layernorm_ex", xr.data_ptr(), rdt, y.data_ptr(), dcode, None,
-                          L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), None if bf16 else x1.data_ptr(),
-                          x1.data_ptr() if bf16 else None, None, T, h, stream, exc=EncoderError)
+                if not (bf16 and self.fused_ln and self._proj_ln(o, L, "wo", "bo", "ln1", xr, x1, None, None, T,
+                                                                  stream)):
+                    y = F.linear(o, L["wo"], L["bo"])
+                    _lib.call("sc_residual_layernorm_ex", xr.data_ptr(), rdt, y.data_ptr(), dcode, None,
+                              L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), None if bf16 else x1.data_ptr(),
+                              x1.data_ptr() if bf16 else None, None, T, h, stream, exc=EncoderError)
                 f = self._ffn_up(x1, L, T, stream)
-                f2 = F.linear(f, L["w2"], L["b2"])
-                _lib.call("sc_residual_layernorm_ex", x1.data_ptr(), rdt, f2.data_ptr(), dcode, None,
-                          L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(),
-                          x.data_ptr() if (not bf16 or i == last) else None, _lib.ptr(xh),
-                          bad.data_ptr() + 4 * i if check_finite else None, T, h, stream, exc=EncoderError)
+                x32 = x if (not bf16 or i == last) else None
+                bad_i = bad[i:i + 1] if check_finite else None
+                if not (bf16 and self.fused_ln and self._proj_ln(f, L, "w2", "b2", "ln2", x1, xh, x32, bad_i, T,
+                                                                  stream)):
+                    f2 = F.linear(f, L["w2"], L["b2"])
+                    _lib.call("sc_residual_layernorm_ex", x1.data_ptr(), rdt, f2.data_ptr(), dcode, None,
+                              L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(), _lib.ptr(x32), _lib.ptr(xh),
+                              _lib.ptr(bad_i), T, h, stream, exc=EncoderError)
         self._last_bad = bad if check_finite else None
         return x
+
+    def _proj_ln(self, a, L, wname, bname, lnname, resid, out, out32, bad, rows, stream) -> bool:
+        """Opt-in (fused_ln): LN(resid + a W^T + b) as one cluster-of-3 tcgen05 GEMM
+        (sc_gemm_residual_layernorm).  Returns False when the shape is unsupported.
+        Measured slower than cuBLAS + the LayerNorm pass at the bench shape
+        (Wo 0.57 vs 0.44 ms, W2 1.22 vs 1.03 ms), hence not the default."""
+        W = L[wname]
+        b = L.get(bname + "_f32")
+        if b is None:
+            b = L[bname + "_f32"] = L[bname].float()
+        rc = _lib.load().sc_gemm_residual_layernorm(
+            a.data_ptr(), a.stride(0), W.data_ptr(), W.stride(0), b.data_ptr(), resid.data_ptr(), resid.stride(0),
+            L[lnname + "_g"].data_ptr(), L[lnname + "_b"].data_ptr(), out.data_ptr(), out.stride(0),
+            _lib.ptr(out32), 0 if out32 is None else out32.stride(0), _lib.ptr(bad), rows, W.shape[0], W.shape[1],
+            stream)
+        if rc == _lib.SC_OK:
+            _lib.launch_calls += 1
+            return True
+        if rc != _lib.SC_ERR_UNSUPPORTED:
+            raise EncoderError(_lib.last_error())
+        return False
 
     def _ffn_up(self, x1: torch.Tensor, L: dict, rows: int, stream) -> torch.Tensor:
         """gelu_erf(x1 W1^T + b1) (R/encoder.py:350-351): bf16 -> the fused tcgen05 GEMM with the

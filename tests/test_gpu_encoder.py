@@ -198,3 +198,14 @@ def test_fused_ffn_matches_cublas_path(P):
     ref = np.array([P.CrossEncoder(P.EncoderConfig(**{**cases.ELECTRA_PASSAGE, "layers": 4, "precision": "f32"}),
                                    weights=fused.host_weights).score(s.ids, s.partition)[0] for s in seqs[:2]])
     np.testing.assert_allclose(a[:2], ref, atol=2e-2, rtol=0)
+
+
+def test_fused_layernorm_projection_matches(P):
+    """Opt-in fused Wo/W2 + residual + LayerNorm (cluster-of-3 tcgen05 GEMM) == default path (bf16 tolerance)."""
+    cfg = P.EncoderConfig(**{**cases.ELECTRA_PASSAGE, "layers": 3, "precision": "bf16"})
+    base = P.CrossEncoder(cfg, seed=0)
+    fused = P.CrossEncoder(cfg, weights=base.host_weights, fused_ln=True)
+    seqs = [rerank_ids(4, j, int(n), cfg.vocab_size, cfg.max_positions, P) for j, n in enumerate([164, 33, 250])]
+    batch = P.PackedBatch.from_sequences(seqs)
+    np.testing.assert_allclose(fused.score_packed(batch).cpu().numpy(), base.score_packed(batch).cpu().numpy(),
+                               atol=2e-2, rtol=0)

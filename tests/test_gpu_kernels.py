@@ -170,3 +170,37 @@ def test_gemm_bias_gelu_cta_pair_variant():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("M,K", [(1000, 768), (37, 3072), (256, 192)])
+def test_gemm_residual_layernorm_vs_torch(lib, M, K):
+    """Cluster-of-3 fused projection + residual + LayerNorm vs a plain PyTorch fp32 reference."""
+    N = 768
+    g = torch.Generator(device="cuda").manual_seed(9)
+    a = torch.randn((M, K), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((N, K), device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    b = torch.randn(N, device="cuda", generator=g) * 0.1
+    resid = torch.randn((M, N), device="cuda", generator=g).to(torch.bfloat16)
+    gamma = 1 + 0.1 * torch.randn(N, device="cuda", generator=g)
+    beta = 0.1 * torch.randn(N, device="cuda", generator=g)
+    ref = torch.nn.functional.layer_norm(resid.float() + a.float() @ w.float().t() + b, (N,), gamma, beta, eps=1e-12)
+    out = torch.empty((M, N), device="cuda", dtype=torch.bfloat16)
+    out32 = torch.empty((M, N), device="cuda")
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lib.call("sc_gemm_residual_layernorm", a.data_ptr(), K, w.data_ptr(), K, b.data_ptr(), resid.data_ptr(), N,
+             gamma.data_ptr(), beta.data_ptr(), out.data_ptr(), N, out32.data_ptr(), N, bad.data_ptr(), M, N, K,
+             lib.stream_handle())
+    torch.testing.assert_close(out32, ref, atol=2e-3, rtol=1e-3)
+    torch.testing.assert_close(out.float(), ref, atol=2e-2, rtol=1e-2)
+    assert bad.item() == 0
+    # bf16-only output, no bias; a NaN in one row is counted
+    a2 = a.clone()
+    a2[min(5, M - 1), 0] = float("nan")
+    lib.call("sc_gemm_residual_layernorm", a2.data_ptr(), K, w.data_ptr(), K, None, resid.data_ptr(), N,
+             gamma.data_ptr(), beta.data_ptr(), out.data_ptr(), N, None, N, bad.data_ptr(), M, N, K,
+             lib.stream_handle())
+    torch.cuda.synchronize()
+    assert bad.item() >= 1
+    with pytest.raises(NotImplementedError):
+        lib.call("sc_gemm_residual_layernorm", a.data_ptr(), K, w.data_ptr(), K, None, resid.data_ptr(), N,
+                 gamma.data_ptr(), beta.data_ptr(), out.data_ptr(), N, None, N, None, M, 512, K, lib.stream_handle())
