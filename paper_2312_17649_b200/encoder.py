@@ -9,9 +9,12 @@ many (query, document) pairs of different lengths in one pass.
 Per layer (post-LN BERT, R/encoder.py:306-371):
     qkv = x @ [Wq|Wk|Wv] + b          cuBLAS (bf16, or fp32 with TF32 off)
     o   = attention(qkv)              sc_attn_fwd (sm_100a kernels)
-    x1  = LN(x + o @ Wo + bo)         cuBLAS + sc_residual_layernorm
-    f   = gelu_erf(x1 @ W1 + b1)      cuBLAS + sc_bias_gelu
-    x   = LN(x1 + f @ W2 + b2)        cuBLAS + sc_residual_layernorm
+    x1  = LN(x + o @ Wo + bo)         cuBLAS + sc_residual_layernorm_ex
+    f   = gelu_erf(x1 @ W1 + b1)      bf16: sc_gemm_bias_gelu (one tcgen05 GEMM, bias + GELU
+                                      epilogue); fp32: cuBLAS + sc_bias_gelu
+    x   = LN(x1 + f @ W2 + b2)        cuBLAS + sc_residual_layernorm_ex
+(opt-in ``fused_ln``: the two LayerNorm lines as cluster-of-3 tcgen05 GEMMs,
+sc_gemm_residual_layernorm.)
 The fp32 path keeps an fp32 residual stream; the bf16 path keeps it in bf16
 (the GEMM inputs are bf16 anyway), with fp32 statistics inside the LayerNorm
 and an fp32 copy of the final layer for the score head.  The per-layer finite
