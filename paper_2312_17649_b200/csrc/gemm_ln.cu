@@ -8,7 +8,7 @@
 // (st.shared::cluster + a remote mbarrier arrive), combines the three partials
 // (Chan et al.) and normalises its own columns.  The separate residual +
 // LayerNorm pass (read y and resid, write out: 6 B/element, 11% of the step)
-// disappears; the epilogue reads resid (2 B) and writes out (2 B).
+// disappears; the epilogue reads resid (2 B, TMA-staged) and writes out (2 B).
 //
 // Roles per CTA as in gemm_gelu.cu (warp 0 TMA, warp 1 MMA, warps 2-5
 // epilogue); TMEM double-buffered.  The epilogue makes two passes over its
@@ -23,11 +23,12 @@ using namespace gg;
 
 constexpr int NS = 3, NCL = 3;  // stages (smem: 3 x 48 KB + staging + stats), CTAs per cluster (3 x 256 = 768 columns)
 constexpr int SMEM_STG = NS * STAGE;
-constexpr int SMEM_STATS = SMEM_STG + 2 * STG_BYTES;          // [2 bufs][3 ranks][128 rows] float2 (mean, M2)
+constexpr int SMEM_RES = SMEM_STG + 2 * STG_BYTES;            // 2 x 16 KB residual chunks (columns 0-127)
+constexpr int SMEM_STATS = SMEM_RES + 2 * STG_BYTES;          // [2 bufs][3 ranks][128 rows] float2 (mean, M2)
 constexpr int STATS_BYTES = 2 * NCL * BM * 8;
 constexpr int SMEM_VEC = SMEM_STATS + STATS_BYTES;             // bias, gamma, beta slices (3 x 256 fp32)
 constexpr int SMEM_BAR = SMEM_VEC + 3 * BN * 4;
-constexpr int SMEM_TOTAL = SMEM_BAR + (2 * NS + 6) * 8 + 16;
+constexpr int SMEM_TOTAL = SMEM_BAR + (2 * NS + 8) * 8 + 16;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -60,8 +61,8 @@ __device__ __forceinline__ void wait_cluster(uint32_t bar, uint32_t parity) {
 }
 __global__ void __cluster_dims__(NCL, 1, 1) __launch_bounds__(NTHREADS, 1) gemm_res_ln_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-    const __grid_constant__ CUtensorMap tmO, const float* __restrict__ bias,
-    const __nv_bfloat16* __restrict__ resid, int64_t ldr, const float* __restrict__ gamma,
+    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmR, const float* __restrict__ bias,
+    const float* __restrict__ gamma,
     const float* __restrict__ beta, float* __restrict__ out_f32, int64_t ldf, int32_t* __restrict__ bad,
     int M, int K) {
   extern __shared__ uint8_t smem_raw[];
@@ -70,7 +71,8 @@ __global__ void __cluster_dims__(NCL, 1, 1) __launch_bounds__(NTHREADS, 1) gemm_
   const uint32_t bar0 = sm0 + SMEM_BAR;
   const uint32_t full_bar = bar0, empty_bar = bar0 + 8 * NS, acc_full = bar0 + 16 * NS, acc_empty = acc_full + 16,
                  stats_bar = acc_full + 32;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + SMEM_BAR + (2 * NS + 6) * 8);
+  const uint32_t res_bar = stats_bar + 16;  // [2]: residual columns 0-127 / 128-255 landed
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + SMEM_BAR + (2 * NS + 8) * 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int cl = blockIdx.x / NCL, ncl = gridDim.x / NCL;
@@ -85,7 +87,8 @@ __global__ void __cluster_dims__(NCL, 1, 1) __launch_bounds__(NTHREADS, 1) gemm_
     for (int b = 0; b < 2; ++b) {
       mbar_init(acc_full + 8 * b, 1);
       mbar_init(acc_empty + 8 * b, 4);
-      mbar_init(stats_bar + 8 * b, 4 * (NCL - 1));  // the peers' four epilogue warps each
+      mbar_init(stats_bar + 8 * b, BM * (NCL - 1));  // every epilogue thread of both peers
+      mbar_init(res_bar + 8 * b, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -151,21 +154,40 @@ __global__ void __cluster_dims__(NCL, 1, 1) __launch_bounds__(NTHREADS, 1) gemm_
       const int buf = i & 1;
       const int m0 = t * BM, row = m0 + r;
       const bool live = row < M;
-      const __nv_bfloat16* rr = resid + (int64_t)(live ? row : 0) * ldr + n0;
+      // residual tile by TMA (four 64-column chunks, 128B swizzle): columns 0-127 into
+      // the dedicated buffers, 128-255 into the output staging buffers once the
+      // previous tile's stores have read them; both land while the mainloop runs
+      if (et == 0) {
+        if (i == 0) {  // later tiles' columns 0-127 were prefetched after the previous pass 1
+          mbar_expect_tx(res_bar, 2 * STG_BYTES);
+          tma_load_2d(sm0 + SMEM_RES, &tmR, n0, m0, res_bar);
+          tma_load_2d(sm0 + SMEM_RES + STG_BYTES, &tmR, n0 + 64, m0, res_bar);
+        }
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_expect_tx(res_bar + 8, 2 * STG_BYTES);
+        tma_load_2d(sm0 + SMEM_STG, &tmR, n0 + 128, m0, res_bar + 8);
+        tma_load_2d(sm0 + SMEM_STG + STG_BYTES, &tmR, n0 + 192, m0, res_bar + 8);
+      }
       mbar_wait(acc_full + 8 * buf, (i >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * BN;
-      // pass 1: y = acc + bias + resid (resid read once, 16-byte loads), written back
-      // over the accumulator in TMEM; shifted sums around the row's first value
-      // give the slice mean and centred M2 in one sweep.
+      // pass 1: y = acc + bias + resid, written back over the accumulator in TMEM;
+      // shifted sums around the row's first value give the slice mean and
+      // centred M2 in one sweep.
       float piv = 0.f, s1 = 0.f, s2 = 0.f;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
+        if (c0 == 0 || c0 == 128) mbar_wait(res_bar + (c0 ? 8 : 0), i & 1);
+        const int ch = c0 >> 6;  // 64-column residual chunk
+        const uint8_t* rbase = smem + (ch < 2 ? SMEM_RES + ch * STG_BYTES : SMEM_STG + (ch - 2) * STG_BYTES);
         uint32_t v[32];
         TC_LD32(taddr + c0, v);
         uint4 rw[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) rw[k] = *reinterpret_cast<const uint4*>(rr + c0 + 8 * k);
+        for (int k = 0; k < 4; ++k) {
+          const int p16 = ((c0 & 63) >> 3) + k;
+          rw[k] = *reinterpret_cast<const uint4*>(rbase + r * ROWB + ((p16 ^ (r & 7)) << 4));
+        }
         tc_wait_ld();
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -187,6 +209,12 @@ __global__ void __cluster_dims__(NCL, 1, 1) __launch_bounds__(NTHREADS, 1) gemm_
         TC_ST32(taddr + c0, v);
       }
       tc_wait_st();
+      epi_sync();  // residual chunks read: staging free for the output, dedicated buffers for the next tile
+      if (et == 0 && t + ncl < tiles) {
+        mbar_expect_tx(res_bar, 2 * STG_BYTES);
+        tma_load_2d(sm0 + SMEM_RES, &tmR, n0, (t + ncl) * BM, res_bar);
+        tma_load_2d(sm0 + SMEM_RES + STG_BYTES, &tmR, n0 + 64, (t + ncl) * BM, res_bar);
+      }
       const float mean_s = piv + s1 * (1.f / BN);
       const float m2 = fmaxf(s2 - s1 * s1 * (1.f / BN), 0.f);
       // exchange (mean, M2) of the three 256-column slices through distributed shared memory
@@ -197,12 +225,9 @@ __global__ void __cluster_dims__(NCL, 1, 1) __launch_bounds__(NTHREADS, 1) gemm_
         const uint32_t peer = (rank + pr) % NCL;
         st_cluster_f2(map_peer(slot + (rank * BM + r) * 8, peer), mean_s, m2);
       }
-      asm volatile("fence.acq_rel.cluster;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
+      // each thread's remote arrive releases its own stores (no cluster-wide fence)
 #pragma unroll
-        for (int pr = 1; pr < NCL; ++pr) arrive_remote(map_peer(stats_bar + 8 * buf, (rank + pr) % NCL));
-      }
+      for (int pr = 1; pr < NCL; ++pr) arrive_remote(map_peer(stats_bar + 8 * buf, (rank + pr) % NCL));
       wait_cluster(stats_bar + 8 * buf, (i >> 1) & 1);
       float mean = 0.f;
       float2 st[NCL];
@@ -294,8 +319,9 @@ extern "C" int sc_gemm_residual_layernorm(const void* a, int64_t lda, const void
     set_error("sc_gemm_residual_layernorm: needs N == 768, K %% 64 == 0 and 16-byte aligned rows");
     return SC_ERR_UNSUPPORTED;
   }
-  CUtensorMap mA, mB, mO;
-  if (!make_map(&mA, a, K, M, lda, BM) || !make_map(&mB, w, K, N, ldw, BN) || !make_map(&mO, out, N, M, ldo, BM)) {
+  CUtensorMap mA, mB, mO, mR;
+  if (!make_map(&mA, a, K, M, lda, BM) || !make_map(&mB, w, K, N, ldw, BN) || !make_map(&mO, out, N, M, ldo, BM) ||
+      !make_map(&mR, resid, N, M, ldr, BM)) {
     set_error("sc_gemm_residual_layernorm: cuTensorMapEncodeTiled failed");
     return SC_ERR_UNSUPPORTED;
   }
@@ -330,7 +356,7 @@ extern "C" int sc_gemm_residual_layernorm(const void* a, int64_t lda, const void
   const int tiles = (M + BM - 1) / BM;
   const int ncl = tiles < clusters ? tiles : clusters;
   gemm_res_ln_kernel<<<NCL * ncl, NTHREADS, smem, (cudaStream_t)stream>>>(
-      mA, mB, mO, bias, static_cast<const __nv_bfloat16*>(resid), ldr, gamma, beta, out_f32, ldf, nonfinite_count, M, K);
+      mA, mB, mO, mR, bias, gamma, beta, out_f32, ldf, nonfinite_count, M, K);
   SC_CHECK_LAUNCH("gemm_res_ln_kernel");
   return SC_OK;
 }

@@ -409,7 +409,7 @@ class CrossEncoder:
         """Opt-in (fused_ln): LN(resid + a W^T + b) as one cluster-of-3 tcgen05 GEMM
         (sc_gemm_residual_layernorm).  Returns False when the shape is unsupported.
         Measured slower than cuBLAS + the LayerNorm pass at the bench shape
-        (Wo 0.57 vs 0.44 ms, W2 1.22 vs 1.03 ms), hence not the default."""
+        (Wo 0.49 vs 0.43 ms, W2 1.14-1.20 vs 1.03-1.07 ms), hence not the default."""
         W = L[wname]
         b = L.get(bname + "_f32")
         if b is None:
