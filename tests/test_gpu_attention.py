@@ -321,3 +321,40 @@ def test_full_attention_and_exclusions(P):
         P.attend_segments(q, [], 1.0)
     with pytest.raises(P.AttentionError):
         P.full_attention(q, k[:, :4], v)
+
+
+@pytest.mark.parametrize("name", ["sparse", "longformer", "qds"])
+def test_head_rows_mode_fp32_generic(P, name):
+    """rows='head' in fp32 (band kernel unsupported -> generic head-row mode) == the full call on the head rows."""
+    rng = np.random.default_rng(43)
+    H, d = 2, 16
+    shapes = [(10, 200), (1, 1), (5, 64)]
+    seq = [m + n + 3 for m, n in shapes]
+    lay = P.PackedLayout.from_lengths(seq, [m + 1 for m, _ in shapes], device="cuda",
+                                      qds_every=30 if name == "qds" else 0)
+    T = sum(seq)
+    x = torch.from_numpy(rng.standard_normal((T, 3 * H * d)).astype(np.float32)).cuda()
+    pat = P.make_pattern(name, 4)
+    args = (x[:, :H * d], x[:, H * d:2 * H * d], x[:, 2 * H * d:], lay, pat, H)
+    full = P.attend_packed(*args)
+    head = P.attend_packed(*args, out=torch.zeros_like(full), rows="head")
+    r = 0
+    for m, n in shapes:
+        torch.testing.assert_close(head[r:r + m + 2], full[r:r + m + 2], atol=1e-5, rtol=0)
+        assert head[r + m + 2:r + m + n + 3].abs().max().item() == 0
+        r += m + n + 3
+
+
+def test_qds_full_size_bf16_tc_vs_fp32_generic(P):
+    """QDS at s = 4099, H = 12, d = 64: the tcgen05 QDS path (bf16) vs the generic kernel in fp32."""
+    rng = np.random.default_rng(47)
+    H, d, m, n = 12, 64, 10, 4086
+    s = m + n + 3
+    lay = P.PackedLayout.from_lengths([s, s], [m + 1, m + 1], device="cuda", qds_every=30)
+    x = torch.from_numpy(rng.standard_normal((2 * s, 3 * H * d)).astype(np.float32)).cuda()
+    xb = x.to(torch.bfloat16)
+    pat = P.make_pattern("qds", 4)
+    ref = P.attend_packed(xb.float()[:, :H * d], xb.float()[:, H * d:2 * H * d], xb.float()[:, 2 * H * d:], lay,
+                          pat, H, algo="generic")
+    got = P.attend_packed(xb[:, :H * d], xb[:, H * d:2 * H * d], xb[:, 2 * H * d:], lay, pat, H).float()
+    assert (got - ref).abs().max().item() < 2e-2
