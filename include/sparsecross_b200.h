@@ -114,6 +114,21 @@ SC_API int sc_band_scores(const void* q, const void* k, void* out, int64_t batch
 SC_API int sc_band_apply(const void* p, const void* v, void* out, int64_t batch, int32_t s,
                   int32_t t, int32_t d, int32_t window, int32_t dtype, void* stream);
 
+/* Adjoint of sc_band_scores (R/band.py:239-253): grad_q[b,i,:] = sum_j
+ * g[b,i,j] k[b,i+j-w,:], grad_k[b,r,:] = sum over slots addressing key r of
+ * g * q; invalid slots of grad_band are never read.  grad_q [batch,s,d],
+ * grad_k [batch,t,d], written (not accumulated). */
+SC_API int sc_band_scores_backward(const void* grad_band, const void* q, const void* k, void* grad_q,
+                   void* grad_k, int64_t batch, int32_t s, int32_t t, int32_t d, int32_t window,
+                   int32_t dtype, void* stream);
+
+/* Adjoint of sc_band_apply (R/band.py:256-274): grad_p[b,i,j] =
+ * grad_out[b,i,:] . v[b,i+j-w,:] (0 at invalid slots), grad_v[b,r,:] = sum
+ * over slots addressing r of p * grad_out.  Written, not accumulated. */
+SC_API int sc_band_apply_backward(const void* grad_out, const void* p, const void* v, void* grad_p,
+                   void* grad_v, int64_t batch, int32_t s, int32_t t, int32_t d, int32_t window,
+                   int32_t dtype, void* stream);
+
 /* ---- K2/K3: fused asymmetric windowed attention ------------------------- */
 
 /* Workspace for sc_attn_fwd: split-softmax partials of the head rows that
@@ -160,6 +175,26 @@ SC_API int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t row_
                 const uint8_t* tok_flags, const int32_t* glob_cu, const int32_t* glob_pos,
                 int32_t algo, void* workspace, size_t workspace_bytes, int32_t* status,
                 void* stream);
+
+/* Backward of sc_attn_fwd for fine-tuning (R/attention.py:260-269, :348-378,
+ * :476-507; R/band.py:239-274): given q/k/v and the forward output `out`
+ * (same layout, dtype and pattern arguments as sc_attn_fwd) and the output
+ * gradient `dout` ([T][H][d], dout_row_stride, `dtype`), writes fp32 dq, dk
+ * and dv (row r, head h at base + r*grad_row_stride + h*d; e.g. the thirds of
+ * one [T][3][H][d] buffer).  Deterministic: two gather-form kernels, no
+ * atomics.  Rows whose forward had no valid key get zero gradients.
+ * tok_flags/glob_cu/glob_pos as in sc_attn_fwd (NULL without QDS).
+ * workspace: sc_attn_bwd_workspace_bytes(T, H) bytes (per-row softmax
+ * statistics).  head_dim <= 128. */
+SC_API size_t sc_attn_bwd_workspace_bytes(int32_t total_tokens, int32_t heads);
+SC_API int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t row_stride,
+                const void* out, int64_t out_row_stride, const void* dout, int64_t dout_row_stride,
+                float* dq, float* dk, float* dv, int64_t grad_row_stride,
+                const int32_t* cu_seqlens, const int32_t* qgroup_len, int32_t nseq,
+                int32_t total_tokens, int32_t heads, int32_t head_dim,
+                const int32_t* links, int32_t padding, float scale, int32_t dtype,
+                const uint8_t* tok_flags, const int32_t* glob_cu, const int32_t* glob_pos,
+                void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- Encoder-loop kernels (R/encoder.py:306-371, :475-509) -------------- */
 

@@ -384,3 +384,134 @@ def flop_count(pattern, group_lens, h, layers, ff_dim):
         att += lens["doc"] * g * h + g * s * h
     return {"attention": 2 * att * layers, "projections": 4 * s * h * h * layers,
             "feed_forward": 2 * s * h * ff_dim * layers}
+
+
+# ---------------------------------------------------------------------------
+# Adjoints  (R/band.py:239-274, R/attention.py:260-269, :348-378, :476-507)
+# -- the checker for the fine-tuning path
+# ---------------------------------------------------------------------------
+
+def _band_scatter(g: np.ndarray, x: np.ndarray, w: int, t: int) -> np.ndarray:
+    """out[..., r, :] = sum over valid slots (i, j) with i+j-w == r of g[..., i, j] x[..., i, :]."""
+    s = g.shape[-2]
+    out = np.zeros(g.shape[:-2] + (t, x.shape[-1]), dtype=np.result_type(g, x))
+    for j in range(2 * w + 1):
+        lo, hi = max(0, w - j), min(s, t + w - j)      # rows whose slot j lands in [0, t)
+        if lo < hi:
+            out[..., lo + j - w:hi + j - w, :] += g[..., lo:hi, j:j + 1] * x[..., lo:hi, :]
+    return out
+
+
+def band_scores_backward(grad_band, q, k, w):
+    """R/band.py:239-253 -- (grad_q, grad_k) of band_scores; invalid slots never read."""
+    return band_apply(grad_band, k, w), _band_scatter(
+        np.where(band_validity(q.shape[-2], w, k.shape[-2]), grad_band, 0.0), q, w, k.shape[-2])
+
+
+def band_apply_backward(grad_out, p, v, w):
+    """R/band.py:256-274 -- (grad_p, grad_v) of band_apply; grad_p is 0 at invalid slots."""
+    ok = band_validity(p.shape[-2], w, v.shape[-2])
+    return band_scores(grad_out, v, w), _band_scatter(np.where(ok, p, 0.0), grad_out, w, v.shape[-2])
+
+
+def attend_segments_backward(q, segments, scale, grad_out, padding="exclude"):
+    """R/attention.py:348-378 (+ the softmax adjoint :260-269), recomputing the probabilities.
+
+    Returns (grad_q, [(grad_k, grad_v) per segment]).  Zero-logit padding
+    slots carry probability but a constant logit, so only valid slots reach q/k.
+    """
+    s = q.shape[-2]
+    vals, oks = [], []
+    for k, v, w, extra in segments:
+        if not _finite(w):
+            vals.append(q @ np.swapaxes(k, -1, -2))
+            oks.append(None)
+            continue
+        sc = band_scores(q, k, int(w))
+        ok = band_validity(s, int(w), k.shape[-2])
+        if extra is not None:
+            if padding == "zero-logit":
+                sc = np.where(extra, -np.inf, sc)
+            else:
+                ok = ok & ~extra
+        vals.append(sc)
+        oks.append(ok)
+    probs = masked_segment_softmax(vals, oks, scale, padding)
+    gps, gvs = [], []
+    for p, (k, v, w, _e) in zip(probs, segments):
+        if not _finite(w):
+            gps.append(grad_out @ np.swapaxes(v, -1, -2))
+            gvs.append(np.swapaxes(p, -1, -2) @ grad_out)
+        else:
+            gp, gv = band_apply_backward(grad_out, p, v, int(w))
+            gps.append(gp)
+            gvs.append(gv)
+    dot = sum(np.sum(p * gp, axis=-1, keepdims=True) for p, gp in zip(probs, gps))
+    gq = np.zeros_like(q)
+    kv = []
+    for p, gp, gv, (k, v, w, _e) in zip(probs, gps, gvs, segments):
+        ga = p * (gp - dot) / scale
+        if not _finite(w):
+            gq = gq + ga @ k
+            gk = np.swapaxes(ga, -1, -2) @ q
+        else:
+            dq_part, gk = band_scores_backward(ga, q, k, int(w))
+            gq = gq + dq_part
+        kv.append((gk, gv))
+    return gq, kv
+
+
+def _group_segments(qkv, source, pattern):
+    gl = pattern["globals"]
+    segs, where = [], []
+    for tgt, w in pattern["targets"][source]:
+        extra = None
+        if gl and source == "doc" and tgt == "doc" and _finite(w):
+            extra = _qds_exclusions(qkv["doc"][1].shape[-2], int(w), gl)
+        segs.append((qkv[tgt][1], qkv[tgt][2], w, extra))
+        where.append((tgt, None))
+    if gl and source == "doc":
+        idx = np.asarray(gl)
+        segs.append((qkv["doc"][1][..., idx, :], qkv["doc"][2][..., idx, :], FULL, None))
+        where.append(("doc", idx))
+    return segs, where
+
+
+def apply_pattern_backward(spans, qkv, pattern, grad_out, scale=None, padding="exclude"):
+    """R/attention.py:476-507 assembled like R/encoder.py:421-435: (dq, dk, dv) over the whole
+    sequence for grad_out (..., s, d).  QDS global doc rows: windowed result discarded, dense
+    recompute over every group."""
+    if scale is None:
+        scale = math.sqrt(qkv["cls"][0].shape[-1])
+    span = dict(zip(GROUPS, spans))
+    dq = np.zeros_like(grad_out)
+    dk = np.zeros_like(grad_out)
+    dv = np.zeros_like(grad_out)
+    gl = pattern["globals"]
+    for src in GROUPS:
+        lo, hi = span[src]
+        q = qkv[src][0]
+        go = grad_out[..., lo:hi, :]
+        segs, where = _group_segments(qkv, src, pattern)
+        if gl and src == "doc":
+            idx = np.asarray(gl)
+            go_local = np.array(go)
+            go_local[..., idx, :] = 0.0
+            gq, kv = attend_segments_backward(q, segs, scale, go_local, padding)
+            gsegs = [(qkv[g][1], qkv[g][2], FULL, None) for g in GROUPS]
+            gq_g, kv_g = attend_segments_backward(q[..., idx, :], gsegs, scale, go[..., idx, :], padding)
+            gq[..., idx, :] += gq_g
+            kv += kv_g
+            where += [(g, None) for g in GROUPS]
+        else:
+            gq, kv = attend_segments_backward(q, segs, scale, go, padding)
+        dq[..., lo:hi, :] += gq
+        for (tgt, idx), (gk, gv) in zip(where, kv):
+            t0, t1 = span[tgt]
+            if idx is None:
+                dk[..., t0:t1, :] += gk
+                dv[..., t0:t1, :] += gv
+            else:
+                dk[..., t0 + idx, :] += gk
+                dv[..., t0 + idx, :] += gv
+    return dq, dk, dv

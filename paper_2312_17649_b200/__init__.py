@@ -1,7 +1,8 @@
 """B200-native hot path of the sparse cross-encoder (arXiv 2312.17649).
 
 Drop-in for the reference package's attention module and encoder forward
-(``sparsecross.attention`` / ``sparsecross.encoder``): same names, argument
+(``sparsecross.attention`` / ``sparsecross.encoder``), plus GPU fine-tuning
+(``sparsecross.training``, backward kernels): same names, argument
 meaning and error classes, computed by sm_100a CUDA kernels behind the C ABI
 in ``include/sparsecross_b200.h``.  No CPU fallback exists.
 """
@@ -25,7 +26,18 @@ from .attention import (
     sparse_pattern,
     windowed_cross_attention,
 )
-from .band import BandShapeError, band_apply, band_pv, band_qk, band_scores, band_validity
+from .band import (
+    BandShapeError,
+    band_apply,
+    band_apply_backward,
+    band_pv,
+    band_pv_backward,
+    band_qk,
+    band_qk_backward,
+    band_scores,
+    band_scores_backward,
+    band_validity,
+)
 from .encoder import (
     CrossEncoder,
     EncoderConfig,
@@ -44,5 +56,21 @@ from .encoder import (
 )
 from .layout import PackedLayout
 from .serialize import SerializationError, load_model, save_model
+from .training import (
+    AdamW,
+    SyntheticTask,
+    TrainableCrossEncoder,
+    TrainingDivergedError,
+    TrainingError,
+    Triple,
+    grad_check,
+    margin_mse_grad,
+    margin_mse_loss,
+    ranknet_grad,
+    ranknet_loss,
+    train_toy,
+    validation_ndcg,
+    write_trace_csv,
+)
 
 __version__ = "0.1.0"

@@ -56,6 +56,11 @@ SIGNATURES = {
     "sc_attn_workspace_bytes_qds": (_sz, [_i32, _i32, _i32, _i32, _i32, _i32, _p, _i32]),
     "sc_attn_fwd": (C.c_int, [_p, _p, _p, _i64, _p, _i64, _p, _p, _i32, _i32, _i32, _i32, _p, _i32,
                               _f32, _i32, _p, _p, _p, _i32, _i32, _p, _p, _p, _i32, _p, _sz, _p, _p]),
+    "sc_band_scores_backward": (C.c_int, [_p, _p, _p, _p, _p, _i64, _i32, _i32, _i32, _i32, _i32, _p]),
+    "sc_band_apply_backward": (C.c_int, [_p, _p, _p, _p, _p, _i64, _i32, _i32, _i32, _i32, _i32, _p]),
+    "sc_attn_bwd_workspace_bytes": (_sz, [_i32, _i32]),
+    "sc_attn_bwd": (C.c_int, [_p, _p, _p, _i64, _p, _i64, _p, _i64, _p, _p, _p, _i64, _p, _p, _i32, _i32, _i32,
+                              _i32, _p, _i32, _f32, _i32, _p, _p, _p, _p, _sz, _p]),
     "sc_embed": (C.c_int, [_p, _p, _p, _p, _p, _p, _i32, _i32, _p]),
     "sc_residual_layernorm": (C.c_int, [_p, _p, _i32, _p, _p, _p, _p, _p, _i32, _i32, _p]),
     "sc_residual_layernorm_ex": (C.c_int, [_p, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _i32, _i32, _p]),
@@ -70,7 +75,7 @@ SIGNATURES = {
 # Entry points that launch device work (counted for the bench's gpu_launches).
 LAUNCHING = {n for n in SIGNATURES
              if n not in ("sc_last_error", "sc_version", "sc_kernel_launches", "sc_attn_workspace_bytes",
-                          "sc_attn_workspace_bytes_qds")}
+                          "sc_attn_workspace_bytes_qds", "sc_attn_bwd_workspace_bytes")}
 
 
 def kernel_launches() -> int:

@@ -92,3 +92,57 @@ def band_pv(p: torch.Tensor, v: torch.Tensor, window: int) -> torch.Tensor:
     if p.dim() != 2 or v.dim() != 2:
         raise BandShapeError("P and V must be 2-D")
     return band_apply(p, v, window)
+
+
+def band_scores_backward(grad_band: torch.Tensor, q: torch.Tensor, k: torch.Tensor, window: int):
+    """Adjoint of band_scores (R/band.py:239-253): (grad_q, grad_k); invalid slots never read."""
+    w = _check_window(window)
+    if grad_band.shape[-1] != 2 * w + 1 or grad_band.shape[-2] != q.shape[-2]:
+        raise BandShapeError("gradient band inconsistent with forward shapes")
+    if not (grad_band.dtype == q.dtype == k.dtype):
+        raise BandShapeError("gradient, q and k dtypes differ")
+    lead = torch.broadcast_shapes(grad_band.shape[:-2], q.shape[:-2], k.shape[:-2])
+    g = grad_band.expand(*lead, *grad_band.shape[-2:]).reshape(-1, *grad_band.shape[-2:]).contiguous()
+    qf = q.expand(*lead, *q.shape[-2:]).reshape(-1, *q.shape[-2:]).contiguous()
+    kf = k.expand(*lead, *k.shape[-2:]).reshape(-1, *k.shape[-2:]).contiguous()
+    B, s, d = qf.shape
+    t = kf.shape[1]
+    gq, gk = torch.empty_like(qf), torch.empty_like(kf)
+    _lib.call("sc_band_scores_backward", g.data_ptr(), qf.data_ptr(), kf.data_ptr(), gq.data_ptr(), gk.data_ptr(),
+              B, s, t, d, w, _dt(qf), _lib.stream_handle(), exc=BandShapeError)
+    return gq.reshape(*lead, s, d), gk.reshape(*lead, t, d)
+
+
+def band_apply_backward(grad_out: torch.Tensor, p: torch.Tensor, v: torch.Tensor, window: int):
+    """Adjoint of band_apply (R/band.py:256-274): (grad_p, grad_v); grad_p is 0 at invalid slots."""
+    w = _check_window(window)
+    if p.shape[-1] != 2 * w + 1:
+        raise BandShapeError(f"band width {p.shape[-1]} inconsistent with window {w}")
+    if grad_out.shape[-2] != p.shape[-2] or grad_out.shape[-1] != v.shape[-1]:
+        raise BandShapeError("grad_out shape inconsistent with forward output")
+    if not (grad_out.dtype == p.dtype == v.dtype):
+        raise BandShapeError("gradient, p and v dtypes differ")
+    lead = torch.broadcast_shapes(grad_out.shape[:-2], p.shape[:-2], v.shape[:-2])
+    go = grad_out.expand(*lead, *grad_out.shape[-2:]).reshape(-1, *grad_out.shape[-2:]).contiguous()
+    pf = p.expand(*lead, *p.shape[-2:]).reshape(-1, *p.shape[-2:]).contiguous()
+    vf = v.expand(*lead, *v.shape[-2:]).reshape(-1, *v.shape[-2:]).contiguous()
+    B, s, _ = pf.shape
+    t, d = vf.shape[1], vf.shape[2]
+    gp, gv = torch.empty_like(pf), torch.empty_like(vf)
+    _lib.call("sc_band_apply_backward", go.data_ptr(), pf.data_ptr(), vf.data_ptr(), gp.data_ptr(), gv.data_ptr(),
+              B, s, t, d, w, _dt(pf), _lib.stream_handle(), exc=BandShapeError)
+    return gp.reshape(*lead, s, 2 * w + 1), gv.reshape(*lead, t, d)
+
+
+def band_qk_backward(grad_band: torch.Tensor, q: torch.Tensor, k: torch.Tensor, window: int):
+    """2-D adjoint of band_qk (R/band.py:316-328)."""
+    if q.dim() != 2 or k.dim() != 2 or grad_band.dim() != 2:
+        raise BandShapeError("gradient band, Q and K must be 2-D")
+    return band_scores_backward(grad_band, q, k, window)
+
+
+def band_pv_backward(grad_out: torch.Tensor, p: torch.Tensor, v: torch.Tensor, window: int):
+    """2-D adjoint of band_pv (R/band.py:331-341)."""
+    if grad_out.dim() != 2 or p.dim() != 2 or v.dim() != 2:
+        raise BandShapeError("grad_out, P and V must be 2-D")
+    return band_apply_backward(grad_out, p, v, window)

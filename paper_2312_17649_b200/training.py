@@ -1,0 +1,615 @@
+"""GPU fine-tuning of the sparse cross-encoder (R/training.py, R/encoder.py:374-533).
+
+SURVEY §8(f)-4: the reference's backward path -- band adjoints
+(R/band.py:239-274), the segment/group attention adjoints (R/attention.py:
+260-269, :348-378, :476-507), ``layer_backward`` / ``CrossEncoder.backward``
+(R/encoder.py:374-443, :511-533) -- and its toy trainer (AdamW, margin-MSE /
+RankNet, the synthetic term-overlap task, ``train_toy``, ``grad_check``),
+rebuilt on the device:
+
+* attention forward = ``sc_attn_fwd`` (the inference kernels), attention
+  backward = ``sc_attn_bwd`` (query-major dQ + key-major dK/dV kernels over
+  the transposed pattern: every pattern, window, padding mode and the QDS
+  globals, deterministic) behind a ``torch.autograd.Function``;
+* the dense layers (QKV / Wo / FFN GEMMs, post-LN LayerNorm with eps 1e-12,
+  exact-erf GELU, embeddings, the [CLS] head) are cuBLAS / torch ops whose
+  adjoints torch's autograd supplies -- fp32 with TF32 off for the parity
+  path, or bf16 autocast (``precision="bf16"``);
+* AdamW keeps the reference's update exactly (decoupled decay on every
+  tensor, bias correction, linear warmup then linear decay).
+
+Gradients come back keyed like the reference's ``grads`` dict
+(``L{i}.wq`` ... ``head_b``, ``tok_emb``, ``pos_emb``) with the reference's
+shapes ((in, out) weight matrices).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from . import _lib
+from .attention import AttentionError, attend_packed, make_pattern
+from .encoder import (
+    LAYER_NORM_EPS,
+    CrossEncoder,
+    EncoderConfig,
+    EncoderError,
+    NonFiniteActivationError,
+    PackedBatch,
+    _fp32_gemms,
+    assemble_input,
+    init_weights,
+)
+from .layout import PackedLayout, to_device
+from .tokenizer import NUM_SPECIAL_TOKENS
+
+
+class TrainingError(ValueError):
+    """Bad trainer arguments (R/training.py:22-23)."""
+
+
+class TrainingDivergedError(RuntimeError):
+    """A non-finite loss; ``step`` is the 1-based step index (R/training.py:26-29)."""
+
+    def __init__(self, step: int):
+        super().__init__(f"loss became non-finite at step {step}")
+        self.step = step
+
+
+# ---------------------------------------------------------------------------
+# Attention with a device adjoint.
+# ---------------------------------------------------------------------------
+
+class PatternAttention(torch.autograd.Function):
+    """out = attention(qkv) under a pattern; backward through ``sc_attn_bwd``.
+
+    qkv: contiguous [T, 3*H*d] (the fused projection), fp32 or bf16.
+    Returns out [T, H*d] of the same dtype.  The adjoint writes dq, dk and dv
+    in fp32 into one [T, 3*H*d] buffer (deterministic, no atomics).
+    """
+
+    @staticmethod
+    def forward(ctx, qkv, layout: PackedLayout, pattern, heads: int, scale: float, padding: str,
+                check: bool = True):
+        hd = qkv.shape[1] // 3
+        out = attend_packed(qkv[:, :hd], qkv[:, hd:2 * hd], qkv[:, 2 * hd:], layout, pattern, heads, scale,
+                            padding, check=check)
+        ctx.save_for_backward(qkv, out)
+        ctx.meta = (layout, pattern, heads, scale, padding)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        qkv, out = ctx.saved_tensors
+        layout, pattern, heads, scale, padding = ctx.meta
+        dout = dout.to(qkv.dtype).contiguous()
+        T, hd3 = qkv.shape
+        hd = hd3 // 3
+        g = torch.empty((T, hd3), dtype=torch.float32, device=qkv.device)
+        attention_backward(qkv, out, dout, g, layout, pattern, heads, scale, padding)
+        return g.to(qkv.dtype), None, None, None, None, None, None
+
+
+def attention_backward(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor, grad: torch.Tensor,
+                       layout: PackedLayout, pattern, heads: int, scale: float, padding: str) -> None:
+    """Writes grad[:, :hd] = dQ, grad[:, hd:2hd] = dK, grad[:, 2hd:] = dV (fp32 [T, 3*H*d])."""
+    T, hd3 = qkv.shape
+    hd = hd3 // 3
+    d = hd // heads
+    es = qkv.element_size()
+    qds = pattern.name == "qds" and layout.tok_flags is not None
+    base, gbase = qkv.data_ptr(), grad.data_ptr()
+    ws_bytes = _lib.load().sc_attn_bwd_workspace_bytes(T, heads)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=qkv.device)
+    _lib.call(
+        "sc_attn_bwd",
+        base, base + hd * es, base + 2 * hd * es, qkv.stride(0), out.data_ptr(), out.stride(0),
+        dout.data_ptr(), dout.stride(0), gbase, gbase + hd * 4, gbase + 2 * hd * 4, grad.stride(0),
+        layout.cu_seqlens.data_ptr(), layout.qgroup_len.data_ptr(), layout.nseq, T, heads, d,
+        pattern.links().ctypes.data, _lib.PAD_EXCLUDE if padding == "exclude" else _lib.PAD_ZERO_LOGIT,
+        float(scale), _lib.DTYPE_BF16 if qkv.dtype == torch.bfloat16 else _lib.DTYPE_F32,
+        _lib.ptr(layout.tok_flags) if qds else None, _lib.ptr(layout.glob_cu) if qds else None,
+        _lib.ptr(layout.glob_pos) if qds else None, ws.data_ptr(), ws_bytes, _lib.stream_handle(),
+        exc=AttentionError,
+    )
+
+
+# ---------------------------------------------------------------------------
+# Trainable encoder.
+# ---------------------------------------------------------------------------
+
+class TrainableCrossEncoder:
+    """Reference-named fp32 device parameters with a differentiable packed forward.
+
+    Mirrors ``CrossEncoder`` of R/encoder.py:450-538 for training:
+    ``score(ids, partition, want_cache=True)`` -> (scores, cache) and
+    ``backward(cache, grad_scores)`` -> grads dict.  ``weights`` holds
+    leaf tensors with ``requires_grad``; AdamW updates them in place.
+    """
+
+    def __init__(self, config: EncoderConfig, weights: dict | None = None, seed: int = 0, device="cuda"):
+        self.config = config
+        self.device = torch.device(device)
+        host = init_weights(config, seed) if weights is None else weights
+        self.weights = {
+            name: torch.tensor(np.asarray(a, dtype=np.float32), device=self.device).requires_grad_(True)
+            for name, a in host.items()
+        }
+        self.pattern = make_pattern(config.pattern, config.window)
+
+    @property
+    def host_weights(self) -> dict:
+        """numpy copies in the config's storage dtype (save_model / the inference CrossEncoder)."""
+        dt = np.float64 if self.config.precision == "f64" else np.float32
+        return {n: t.detach().cpu().numpy().astype(dt) for n, t in self.weights.items()}
+
+    @property
+    def weight_nbytes(self) -> int:
+        return sum(int(t.numel() * t.element_size()) for t in self.weights.values())
+
+    def to_inference(self, **kw) -> CrossEncoder:
+        """The inference engine (fused kernels, graphs) over the current weights."""
+        return CrossEncoder(self.config, self.host_weights, device=self.device, **kw)
+
+    def gemm_mode(self):
+        """fp32 configs: full-precision cuBLAS (TF32 off) for the forward and the adjoint GEMMs."""
+        return _fp32_gemms(self.config.precision != "bf16")
+
+    def make_layout(self, batch: PackedBatch) -> PackedLayout:
+        qds = self.config.qds_global_every if self.config.pattern == "qds" else 0
+        return PackedLayout.from_lengths(batch.seq_lens, batch.qgroup_lens, device=self.device, qds_every=qds)
+
+    # -- differentiable packed forward -------------------------------------
+
+    def hidden_packed(self, ids_dev: torch.Tensor, layout: PackedLayout, check_finite: bool = True) -> torch.Tensor:
+        """Final-layer activations [T, h] with the autograd graph (R/encoder.py:475-500)."""
+        cfg, W = self.config, self.weights
+        h, H = cfg.embed_dim, cfg.heads
+        bf16 = cfg.precision == "bf16"
+        scale = math.sqrt(cfg.head_dim)
+        x = W["tok_emb"][ids_dev.long()] + W["pos_emb"][layout.tok_pos.long()]
+        flags = []
+        with self.gemm_mode(), torch.autocast("cuda", dtype=torch.bfloat16, enabled=bf16):
+            for i in range(cfg.layers):
+                p = f"L{i}."
+                wqkv = torch.cat([W[p + "wq"], W[p + "wk"], W[p + "wv"]], dim=1)
+                bqkv = torch.cat([W[p + "bq"], W[p + "bk"], W[p + "bv"]])
+                qkv = torch.addmm(bqkv, x, wqkv).contiguous()
+                o = PatternAttention.apply(qkv, layout, self.pattern, H, scale, cfg.padding, i == 0)
+                r1 = x + torch.addmm(W[p + "bo"], o, W[p + "wo"])
+                ln1 = F.layer_norm(r1, (h,), W[p + "ln1_g"], W[p + "ln1_b"], LAYER_NORM_EPS)
+                g1 = F.gelu(torch.addmm(W[p + "b1"], ln1, W[p + "w1"]))
+                r2 = ln1 + torch.addmm(W[p + "b2"], g1, W[p + "w2"])
+                x = F.layer_norm(r2, (h,), W[p + "ln2_g"], W[p + "ln2_b"], LAYER_NORM_EPS)
+                if check_finite:
+                    flags.append(torch.isfinite(x.detach()).all())
+        if flags:
+            ok = torch.stack(flags).cpu()
+            if not bool(ok.all()):
+                raise NonFiniteActivationError(int((~ok).nonzero()[0, 0]))
+        return x.float()
+
+    def score_packed(self, ids_dev: torch.Tensor, layout: PackedLayout, check_finite: bool = True) -> torch.Tensor:
+        """Scores [nseq] = x[cls] . head_w + head_b, differentiable (R/encoder.py:502-509)."""
+        x = self.hidden_packed(ids_dev, layout, check_finite)
+        return x[layout.cls_rows] @ self.weights["head_w"] + self.weights["head_b"]
+
+    # -- reference-shaped entry points ---------------------------------------
+
+    def _check_ids(self, ids, partition) -> np.ndarray:
+        ids = np.asarray(ids, dtype=np.int64)
+        if ids.ndim == 1:
+            ids = ids[None, :]
+        if ids.ndim != 2 or ids.shape[1] != partition.seq_len:
+            raise EncoderError(f"ids shape {ids.shape} inconsistent with partition length {partition.seq_len}")
+        if ids.shape[1] > self.config.max_positions:
+            raise EncoderError("sequence longer than max_positions")
+        if ids.min() < 0 or ids.max() >= self.config.vocab_size:
+            raise EncoderError("token id outside vocabulary")
+        return ids
+
+    def score(self, ids, partition, want_cache: bool = False):
+        """Scores (batch,) as numpy; with ``want_cache`` also the cache ``backward`` consumes."""
+        ids = self._check_ids(ids, partition)
+        batch = PackedBatch.from_ids(ids, partition)
+        layout = self.make_layout(batch)
+        ids_dev = to_device(batch.ids, self.device)
+        if not want_cache:
+            with torch.no_grad():
+                return self.score_packed(ids_dev, layout).double().cpu().numpy()
+        s = self.score_packed(ids_dev, layout)
+        return s.detach().double().cpu().numpy(), {"scores": s, "layout": layout}
+
+    def forward(self, ids, partition) -> np.ndarray:
+        """Final-layer embeddings (batch, seq, embed) (R/encoder.py:475-500)."""
+        ids = self._check_ids(ids, partition)
+        batch = PackedBatch.from_ids(ids, partition)
+        layout = self.make_layout(batch)
+        with torch.no_grad():
+            x = self.hidden_packed(to_device(batch.ids, self.device), layout)
+        return x.double().cpu().numpy().reshape(ids.shape[0], ids.shape[1], -1)
+
+    def backward(self, cache: dict, grad_scores) -> dict:
+        """Weight gradients of sum(grad_scores * scores) (R/encoder.py:511-533), as device fp32 tensors."""
+        s = cache["scores"]
+        g = torch.as_tensor(np.asarray(grad_scores, dtype=np.float32) if not torch.is_tensor(grad_scores)
+                            else grad_scores, device=s.device, dtype=s.dtype).reshape(s.shape)
+        names = sorted(self.weights)
+        with self.gemm_mode():
+            grads = torch.autograd.grad(s, [self.weights[n] for n in names], grad_outputs=g, allow_unused=True)
+        return {n: (torch.zeros_like(self.weights[n]) if gr is None else gr) for n, gr in zip(names, grads)}
+
+
+# ---------------------------------------------------------------------------
+# Losses (R/training.py:36-75).  Inputs: floats, numpy arrays or tensors.
+# ---------------------------------------------------------------------------
+
+def _f64(x):
+    if torch.is_tensor(x):
+        return x.detach().double()
+    return torch.as_tensor(np.asarray(x, dtype=np.float64))
+
+
+def margin_mse_loss(s_pos, s_neg, t_pos, t_neg) -> float:
+    """mean(((s+ - s-) - (t+ - t-))^2) in float64 (R/training.py:36-41)."""
+    sp, sn, tp, tn = (_f64(a) for a in (s_pos, s_neg, t_pos, t_neg))
+    dev = sp.device
+    gap = (sp - sn) - (tp.to(dev) - tn.to(dev))
+    return float(torch.mean(gap * gap))
+
+
+def margin_mse_grad(s_pos, s_neg, t_pos, t_neg):
+    """(dL/ds+, dL/ds-) = (2 gap / n, -2 gap / n) (R/training.py:44-47)."""
+    sp, sn, tp, tn = (_f64(a) for a in (s_pos, s_neg, t_pos, t_neg))
+    dev = sp.device
+    gap = (sp - sn) - (tp.to(dev) - tn.to(dev))
+    scale = 2.0 / max(gap.numel(), 1)
+    return _like(scale * gap, s_pos), _like(-scale * gap, s_pos)
+
+
+def ranknet_loss(s_pos, s_neg) -> float:
+    """mean(log(1 + exp(-(s+ - s-)))), overflow-safe (R/training.py:50-53)."""
+    delta = _f64(s_pos) - _f64(s_neg).to(_f64(s_pos).device)
+    return float(torch.mean(torch.logaddexp(torch.zeros_like(delta), -delta)))
+
+
+def ranknet_grad(s_pos, s_neg):
+    """d/ds+ = -sigmoid(-(s+ - s-)) / n (R/training.py:56-60)."""
+    delta = _f64(s_pos) - _f64(s_neg).to(_f64(s_pos).device)
+    g = -torch.sigmoid(-delta) / max(delta.numel(), 1)
+    return _like(g, s_pos), _like(-g, s_pos)
+
+
+def _like(t: torch.Tensor, ref):
+    if torch.is_tensor(ref):
+        return t
+    out = t.cpu().numpy()
+    return out if out.ndim else float(out)
+
+
+LOSSES = ("margin_mse", "ranknet")
+
+
+# ---------------------------------------------------------------------------
+# Optimizer (R/training.py:79-137) on device tensors.
+# ---------------------------------------------------------------------------
+
+class AdamW:
+    """Adam moments, bias correction, decoupled decay, linear warmup / decay.
+
+    ``step(weights, grads)`` applies, for every name in sorted order,
+    ``w -= lr_t * ((m/bc1) / (sqrt(v/bc2) + eps) + weight_decay * w)`` with
+    the moments kept in ``moment_dtype`` (float64 like the reference by
+    default).
+    """
+
+    def __init__(self, lr: float, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.01,
+                 warmup_steps: int = 0, total_steps: int | None = None, moment_dtype=torch.float64):
+        self.lr = lr
+        self.beta1, self.beta2 = betas
+        self.eps = eps
+        self.weight_decay = weight_decay
+        self.warmup_steps = warmup_steps
+        self.total_steps = total_steps
+        self.step_count = 0
+        self.moment_dtype = moment_dtype
+        self._m: dict = {}
+        self._v: dict = {}
+
+    def current_lr(self) -> float:
+        t = self.step_count
+        if self.warmup_steps > 0 and t <= self.warmup_steps:
+            return self.lr * t / self.warmup_steps
+        if self.total_steps is not None and self.total_steps > self.warmup_steps:
+            frac = (t - self.warmup_steps) / (self.total_steps - self.warmup_steps)
+            return self.lr * max(0.0, 1.0 - min(1.0, frac))
+        return self.lr
+
+    @torch.no_grad()
+    def step(self, weights: dict, grads: dict) -> None:
+        self.step_count += 1
+        t = self.step_count
+        lr_t = self.current_lr()
+        bc1 = 1.0 - self.beta1 ** t
+        bc2 = 1.0 - self.beta2 ** t
+        for name in sorted(weights):
+            w = weights[name]
+            g = grads[name]
+            g = (g if torch.is_tensor(g) else torch.as_tensor(np.asarray(g))).to(w.device, self.moment_dtype)
+            m = self._m.get(name)
+            if m is None:
+                m = self._m[name] = torch.zeros_like(g)
+                self._v[name] = torch.zeros_like(g)
+            v = self._v[name]
+            m.mul_(self.beta1).add_(g, alpha=1.0 - self.beta1)
+            v.mul_(self.beta2).addcmul_(g, g, value=1.0 - self.beta2)
+            update = (m / bc1) / ((v / bc2).sqrt() + self.eps)
+            w.sub_((lr_t * (update + self.weight_decay * w.to(self.moment_dtype))).to(w.dtype))
+
+
+# ---------------------------------------------------------------------------
+# Synthetic term-overlap task (R/training.py:140-227): host-side sampling with
+# the reference's random draws, so a seed yields the reference's triples.
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class Triple:
+    query: tuple
+    positive: tuple
+    negative: tuple
+    teacher_pos: float | None = None
+    teacher_neg: float | None = None
+
+    def __post_init__(self):
+        if tuple(self.positive) == tuple(self.negative):
+            raise TrainingError("positive and negative documents must differ")
+        if (self.teacher_pos is None) != (self.teacher_neg is None):
+            raise TrainingError("teacher scores must be present for both documents or neither")
+
+
+@dataclass(frozen=True)
+class ValidationQuery:
+    query_id: str
+    query: tuple
+    candidates: list
+    relevance: dict
+
+
+@dataclass(frozen=True)
+class SyntheticTask:
+    """Queries of distinct vocabulary terms; positives hold all of them, negatives none."""
+
+    vocab_words: int = 64
+    query_terms: int = 4
+    doc_len: int = 16
+
+    def __post_init__(self):
+        if self.query_terms < 1 or self.doc_len < self.query_terms:
+            raise TrainingError("doc_len must be >= query_terms >= 1")
+        if self.vocab_words < 2 * self.query_terms:
+            raise TrainingError("vocabulary too small for disjoint distractors")
+
+    @property
+    def vocab_size(self) -> int:
+        return NUM_SPECIAL_TOKENS + self.vocab_words
+
+    def overlap(self, query, doc) -> int:
+        return len(set(query) & set(doc))
+
+    def _draw_query(self, rng) -> tuple:
+        words = np.arange(NUM_SPECIAL_TOKENS, self.vocab_size)
+        return tuple(int(t) for t in rng.choice(words, size=self.query_terms, replace=False))
+
+    def _draw_doc(self, rng, query, count: int) -> tuple:
+        # draw order: the `count` query terms, the filler, then one shuffle
+        q = np.asarray(query)
+        picked = rng.choice(q, size=count, replace=False) if count else np.empty(0, int)
+        pool = np.setdiff1d(np.arange(NUM_SPECIAL_TOKENS, self.vocab_size), q)
+        filler = rng.choice(pool, size=self.doc_len - count, replace=True)
+        doc = np.concatenate([picked, filler])
+        rng.shuffle(doc)
+        return tuple(int(t) for t in doc)
+
+    def sample_triple(self, rng) -> Triple:
+        query = self._draw_query(rng)
+        pos = self._draw_doc(rng, query, self.query_terms)
+        neg = self._draw_doc(rng, query, 0)
+        return Triple(query, pos, neg, teacher_pos=float(self.query_terms), teacher_neg=0.0)
+
+    def sample_validation(self, rng, n_queries: int, per_level: int = 4) -> list:
+        pools = []
+        for qi in range(n_queries):
+            query = self._draw_query(rng)
+            cands, rel = [], {}
+            for level in range(self.query_terms + 1):
+                for _ in range(per_level):
+                    did = f"d{len(cands)}"
+                    cands.append((did, self._draw_doc(rng, query, level)))
+                    rel[did] = level
+            perm = rng.permutation(len(cands))
+            pools.append(ValidationQuery(f"q{qi}", query, [cands[j] for j in perm], rel))
+        return pools
+
+
+def _dcg(gains) -> float:
+    """sum (2^g - 1) / log2(rank + 1) (R/evaluation.py:94-95)."""
+    return sum((2.0 ** g - 1.0) / math.log2(r + 1) for r, g in enumerate(gains, 1))
+
+
+def validation_ndcg(model, val_set, k: int = 10):
+    """(per-query nDCG@k, mean); pools ranked by (-score, position) (R/training.py:230-255)."""
+    per_query = {}
+    for vq in val_set:
+        seqs = [assemble_input(vq.query, doc, model.config.max_positions) for _, doc in vq.candidates]
+        scores = model.score(np.stack([s.ids for s in seqs]), seqs[0].partition)
+        order = sorted(range(len(seqs)), key=lambda j: (-float(scores[j]), j))
+        gains = [vq.relevance.get(vq.candidates[j][0], 0) for j in order[:k]]
+        idcg = _dcg(sorted(vq.relevance.values(), reverse=True)[:k])
+        per_query[vq.query_id] = _dcg(gains) / idcg if idcg > 0 else 0.0
+    mean = sum(per_query.values()) / len(per_query) if per_query else 0.0
+    return per_query, mean
+
+
+# ---------------------------------------------------------------------------
+# Training loop (R/training.py:258-357).
+# ---------------------------------------------------------------------------
+
+@dataclass
+class TraceRow:
+    step: int
+    loss: float
+    ndcg10: float | None = None
+
+
+@dataclass
+class TrainResult:
+    model: TrainableCrossEncoder
+    trace: list = field(default_factory=list)
+
+    @property
+    def final_ndcg(self):
+        for row in reversed(self.trace):
+            if row.ndcg10 is not None:
+                return row.ndcg10
+        return None
+
+
+def _batch_arrays(triples, max_positions):
+    """[positives; negatives] ids (2B, s) and their shared partition (R/training.py:277-284)."""
+    seqs = [assemble_input(t.query, t.positive, max_positions) for t in triples]
+    seqs += [assemble_input(t.query, t.negative, max_positions) for t in triples]
+    if len({s.ids.shape[0] for s in seqs}) != 1:
+        raise TrainingError("triples in one batch must share sequence length")
+    return np.stack([s.ids for s in seqs]), seqs[0].partition
+
+
+def _loss_tensor(name, scores, triples):
+    b = len(triples)
+    sp, sn = scores[:b].double(), scores[b:].double()
+    if name == "margin_mse":
+        if any(t.teacher_pos is None for t in triples):
+            raise TrainingError("margin_mse requires teacher scores on every triple")
+        tgap = torch.tensor([t.teacher_pos - t.teacher_neg for t in triples], dtype=torch.float64,
+                            device=scores.device)
+        gap = (sp - sn) - tgap
+        return torch.mean(gap * gap)
+    delta = sp - sn
+    return torch.mean(torch.logaddexp(torch.zeros_like(delta), -delta))
+
+
+def train_step(model: TrainableCrossEncoder, opt: AdamW, triples, loss: str = "margin_mse",
+               step: int | None = None) -> float:
+    """One optimisation step on a batch of triples; returns the loss value."""
+    ids, partition = _batch_arrays(triples, model.config.max_positions)
+    ids = model._check_ids(ids, partition)
+    batch = PackedBatch.from_ids(ids, partition)
+    layout = model.make_layout(batch)
+    scores = model.score_packed(to_device(batch.ids, model.device), layout)
+    lt = _loss_tensor(loss, scores, triples)
+    value = float(lt.detach())
+    if not math.isfinite(value):
+        raise TrainingDivergedError(opt.step_count + 1 if step is None else step)
+    names = sorted(model.weights)
+    with model.gemm_mode():
+        gr = torch.autograd.grad(lt, [model.weights[n] for n in names], allow_unused=True)
+    grads = {n: (torch.zeros_like(model.weights[n]) if g is None else g) for n, g in zip(names, gr)}
+    opt.step(model.weights, grads)
+    return value
+
+
+def train_toy(config: EncoderConfig, dataset, steps: int, lr: float, seed: int = 0, batch_pairs: int = 16,
+              loss: str = "margin_mse", weight_decay: float = 0.01, warmup_fraction: float = 0.01,
+              lr_decay: bool = True, eval_every: int = 0, val_set=None, val_k: int = 10,
+              device="cuda") -> TrainResult:
+    """Train a fresh model on triples (R/training.py:287-357), on the GPU.
+
+    ``dataset``: a SyntheticTask (sampled afresh each step with the
+    reference's RNG stream) or a fixed sequence of triples cycled in order.
+    """
+    if loss not in LOSSES:
+        raise TrainingError(f"unknown loss {loss!r}; expected one of {LOSSES}")
+    synthetic = isinstance(dataset, SyntheticTask)
+    if synthetic and config.vocab_size < dataset.vocab_size:
+        raise TrainingError("encoder vocabulary smaller than task vocabulary")
+    if not synthetic and not dataset:
+        raise TrainingError("fixed dataset must be nonempty")
+    model = TrainableCrossEncoder(config, seed=seed, device=device)
+    opt = AdamW(lr, weight_decay=weight_decay, warmup_steps=max(1, round(warmup_fraction * steps)),
+                total_steps=steps if lr_decay else None)
+    rng = np.random.default_rng(seed + 0x5EED)
+    result = TrainResult(model)
+    cursor = 0
+    for step in range(1, steps + 1):
+        if synthetic:
+            triples = [dataset.sample_triple(rng) for _ in range(batch_pairs)]
+        else:
+            triples = [dataset[(cursor + i) % len(dataset)] for i in range(batch_pairs)]
+            cursor += batch_pairs
+        value = train_step(model, opt, triples, loss, step)
+        row = TraceRow(step, value)
+        if val_set is not None and (step == steps or (eval_every > 0 and step % eval_every == 0)):
+            row.ndcg10 = validation_ndcg(model, val_set, val_k)[1]
+        result.trace.append(row)
+    return result
+
+
+def write_trace_csv(trace, path) -> None:
+    """step,loss,ndcg10 (R/training.py:360-365)."""
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write("step,loss,ndcg10\n")
+        for row in trace:
+            nd = "" if row.ndcg10 is None else f"{row.ndcg10:.6f}"
+            fh.write(f"{row.step},{row.loss:.8f},{nd}\n")
+
+
+def grad_check(model: TrainableCrossEncoder, triples, eps: float = 1e-3, samples: int = 8,
+               loss: str = "margin_mse", seed: int = 0) -> float:
+    """Max relative error of directional derivatives: analytic <grad, u> vs central differences.
+
+    The reference (R/training.py:372-433) perturbs single float64
+    coordinates; the device path computes in fp32, where a single-coordinate
+    difference drowns in rounding, so this checks ``samples`` random
+    Rademacher directions spanning every weight tensor instead.
+    """
+    triples = list(triples)
+    ids, partition = _batch_arrays(triples, model.config.max_positions)
+    batch = PackedBatch.from_ids(model._check_ids(ids, partition), partition)
+    layout = model.make_layout(batch)
+    ids_dev = to_device(batch.ids, model.device)
+    names = sorted(model.weights)
+
+    def loss_value():
+        with torch.no_grad():
+            return float(_loss_tensor(loss, model.score_packed(ids_dev, layout), triples))
+
+    lt = _loss_tensor(loss, model.score_packed(ids_dev, layout), triples)
+    with model.gemm_mode():
+        grads = torch.autograd.grad(lt, [model.weights[n] for n in names], allow_unused=True)
+    gen = torch.Generator(device=model.device).manual_seed(seed)
+    worst = 0.0
+    for _ in range(samples):
+        dirs = [torch.randint(0, 2, model.weights[n].shape, generator=gen, device=model.device).float() * 2 - 1
+                for n in names]
+        analytic = sum(float((g * u).sum()) for g, u in zip(grads, dirs) if g is not None)
+        orig = [model.weights[n].detach().clone() for n in names]
+        with torch.no_grad():
+            for n, w0, u in zip(names, orig, dirs):
+                model.weights[n].copy_(w0 + eps * u)
+        up = loss_value()
+        with torch.no_grad():
+            for n, w0, u in zip(names, orig, dirs):
+                model.weights[n].copy_(w0 - eps * u)
+        down = loss_value()
+        with torch.no_grad():
+            for n, w0 in zip(names, orig):
+                model.weights[n].copy_(w0)
+        fd = (up - down) / (2 * eps)
+        denom = max(abs(analytic), abs(fd))
+        err = abs(analytic - fd) if denom < 1e-6 else abs(analytic - fd) / denom
+        worst = max(worst, err)
+    return worst

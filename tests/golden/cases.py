@@ -98,3 +98,44 @@ ELECTRA_DOC = dict(ELECTRA_PASSAGE, max_positions=4099)
 def tiny_sequence(seed, m, n, vocab):
     rng = np.random.default_rng(seed)
     return rng.integers(3, vocab, size=m), rng.integers(3, vocab, size=n)
+
+
+# ---- backward / training fixtures -------------------------
+
+def band_grad_inputs(idx, case):
+    """Upstream gradients (grad_band (s, 2w+1), grad_out (s, d)) for band case ``idx``."""
+    s, t, w, d = case
+    rng = np.random.default_rng((77, idx))
+    return rng.standard_normal((s, 2 * w + 1)), rng.standard_normal((s, d))
+
+
+def attn_grad_out(idx, case):
+    """Output gradient (heads, s, d) for attention case ``idx``."""
+    _name, _w, _pad, m, n, heads, d, dt = case
+    rng = np.random.default_rng((4321, idx))
+    g = rng.standard_normal((heads, m + n + 3, d))
+    return g.astype(np.float32 if dt == "f32" else np.float64)
+
+
+def grad_projection(idx, d):
+    """(d, 4) projection the large attention-gradient fixtures are stored through."""
+    return np.random.default_rng((999, idx)).standard_normal((d, 4))
+
+
+TRAIN_GRAD_SCORES = np.array([0.7, -1.3])
+
+TASK = dict(vocab_words=12, query_terms=2, doc_len=6)   # T/test_training.py:28
+
+
+def task_config_kw(pattern, window):
+    """T/test_training.py:31-43 (vocab = 3 special + 12 words)."""
+    return dict(layers=2, embed_dim=32, heads=4, ff_dim=64, max_positions=16, vocab_size=15,
+                pattern=pattern, window=window)
+
+
+def adamw_inputs():
+    rng = np.random.default_rng(55)
+    ws = {"a": rng.standard_normal((3, 4)), "b": rng.standard_normal(5), "c": np.array(0.25)}
+    gs = [{n: rng.standard_normal(np.shape(a)) * (0.0 if step == 2 and n == "b" else 1.0)
+           for n, a in ws.items()} for step in range(5)]
+    return ws, gs

@@ -142,13 +142,98 @@ def gen_serialize():
     np.savez_compressed(os.path.join(HERE, "serialize.npz"), **scores)
 
 
+def _group_backward_full(pt, qkv, pat, scale, pad, grad_out):
+    """dq/dk/dv (heads, s, d) through the reference's group adjoints, assembled like
+    layer_backward (R/encoder.py:421-435)."""
+    spans = {g: pt.span(g) for g in A.GROUPS}
+    caches = {g: A.group_attention(qkv, g, pat, scale, pad, want_cache=True)[1] for g in A.GROUPS}
+    shape = grad_out.shape
+    dq, dk, dv = np.zeros(shape, grad_out.dtype), np.zeros(shape, grad_out.dtype), np.zeros(shape, grad_out.dtype)
+    for g in A.GROUPS:
+        lo, hi = spans[g]
+        gq, contribs = A.group_attention_backward(caches[g], grad_out[..., lo:hi, :], g, pat)
+        dq[..., lo:hi, :] += gq
+        for target, idx, gk, gv in contribs:
+            t0, t1 = spans[target]
+            if idx is None:
+                dk[..., t0:t1, :] += gk
+                dv[..., t0:t1, :] += gv
+            else:
+                dk[..., t0 + idx, :] += gk
+                dv[..., t0 + idx, :] += gv
+    return dq, dk, dv
+
+
+def gen_training():
+    """Backward / training fixtures from the reference's own adjoints and trainer."""
+    from sparsecross import training as TR
+
+    out = {}
+    # band adjoints (R/band.py:239-274)
+    for i, case in enumerate(cases.BAND_CASES):
+        s, t, w, d = case
+        q, k, p, v = cases.band_inputs(i, case)
+        gb, go = cases.band_grad_inputs(i, case)
+        out[f"band_gq_{i}"], out[f"band_gk_{i}"] = B.band_scores_backward(gb, q, k, w)
+        out[f"band_gp_{i}"], out[f"band_gv_{i}"] = B.band_apply_backward(go, p, v, w)
+    # attention adjoints over every ATTN_CASE (R/attention.py:260-269, :348-378, :476-507)
+    for i, case in enumerate(cases.ATTN_CASES):
+        name, w, pad, m, n, heads, d, dt = case
+        x = cases.attn_inputs(i, case)
+        go = cases.attn_grad_out(i, case)
+        pt = part(m, n)
+        qkv = {g: tuple(a[:, lo:hi, :] for a in x) for g, (lo, hi) in zip(A.GROUPS, cases.attn_spans(m, n))}
+        pat = A.make_pattern(name, w, cases.attn_globals(name, m, n))
+        dq, dk, dv = _group_backward_full(pt, qkv, pat, math.sqrt(d), pad, go)
+        big = dq.size > 8000  # large cases: 4 random projections per row (cases.grad_projection)
+        for tag, g in (("dq", dq), ("dk", dk), ("dv", dv)):
+            out[f"attn_{tag}_{i}"] = g @ cases.grad_projection(i, d) if big else g
+    # encoder weight gradients (R/encoder.py:511-533), tiny configs, every pattern x padding, f64
+    for name in ("full", "longformer", "qds", "sparse"):
+        for pad in ("exclude", "zero-logit"):
+            cfg = E.EncoderConfig(**cases.TINY, pattern=name, padding=pad, precision="f64")
+            model = E.CrossEncoder(cfg, seed=15)
+            seqs = [E.assemble_input(*cases.tiny_sequence(16 + j, 4, 13, cfg.vocab_size), cfg.max_positions)
+                    for j in range(2)]
+            ids = np.stack([sq.ids for sq in seqs])
+            scores, cache = model.score(ids, seqs[0].partition, want_cache=True)
+            grads = model.backward(cache, cases.TRAIN_GRAD_SCORES)
+            key = f"grad_{name}_{pad}"
+            out[key + "_scores"] = scores
+            for wn, g in grads.items():
+                out[f"{key}|{wn}"] = np.asarray(g)
+    # trainer: task sampling, AdamW, a short train_toy run (R/training.py:79-357)
+    task = TR.SyntheticTask(**cases.TASK)
+    rng = np.random.default_rng(3)
+    trip = [task.sample_triple(rng) for _ in range(5)]
+    out["task_triples"] = np.array([list(t.query) + list(t.positive) + list(t.negative) for t in trip])
+    val = task.sample_validation(np.random.default_rng(4), 2, per_level=2)
+    out["task_val"] = np.array([[int(dj[1:]) for dj, _ in vq.candidates] for vq in val])
+    out["task_val_docs"] = np.array([[list(doc) for _, doc in vq.candidates] for vq in val])
+    ws, gs = cases.adamw_inputs()
+    opt = TR.AdamW(lr=0.05, weight_decay=0.1, warmup_steps=2, total_steps=6)
+    for step in range(5):
+        opt.step(ws, gs[step])
+    for n, a in ws.items():
+        out[f"adamw|{n}"] = a
+    for pattern, window in (("full", 4), ("sparse", 1), ("qds", 4)):
+        cfg = E.EncoderConfig(**cases.task_config_kw(pattern, window), precision="f32")
+        res = TR.train_toy(cfg, task, steps=3, lr=1e-3, seed=0, batch_pairs=4)
+        key = f"toy_{pattern}_{window}"
+        out[key + "_loss"] = np.array([r.loss for r in res.trace])
+        for wn, a in res.model.weights.items():
+            out[f"{key}|{wn}"] = a
+    np.savez_compressed(os.path.join(HERE, "training.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-long", action="store_true")
     ap.add_argument("--only", default="")
     args = ap.parse_args()
     steps = {"band": gen_band, "masks": gen_masks, "attention": gen_attention,
-             "encoder": lambda: gen_encoders(args.skip_long), "serialize": gen_serialize}
+             "encoder": lambda: gen_encoders(args.skip_long), "serialize": gen_serialize,
+             "training": gen_training}
     for name, fn in steps.items():
         if args.only and name not in args.only.split(","):
             continue
