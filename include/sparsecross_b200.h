@@ -183,7 +183,11 @@ SC_API int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t row_
  * and dv (row r, head h at base + r*grad_row_stride + h*d; e.g. the thirds of
  * one [T][3][H][d] buffer).  Deterministic: two gather-form kernels, no
  * atomics.  Rows whose forward had no valid key get zero gradients.
- * tok_flags/glob_cu/glob_pos as in sc_attn_fwd (NULL without QDS).
+ * tok_flags/glob_cu/glob_pos, seq_tile_base/tile_rows (from sc_index_build)
+ * and max_qgroup_len as in sc_attn_fwd (QDS pointers NULL without QDS).
+ * bf16, head_dim 64, no QDS, a finite doc window <= 24, tile_rows 64 and
+ * max_qgroup_len <= 31 take the tiled tensor-core path for the doc band
+ * (one host read of the tile count); anything else the generic kernels.
  * workspace: sc_attn_bwd_workspace_bytes(T, H) bytes (per-row softmax
  * statistics).  head_dim <= 128. */
 SC_API size_t sc_attn_bwd_workspace_bytes(int32_t total_tokens, int32_t heads);
@@ -194,6 +198,7 @@ SC_API int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t row_
                 int32_t total_tokens, int32_t heads, int32_t head_dim,
                 const int32_t* links, int32_t padding, float scale, int32_t dtype,
                 const uint8_t* tok_flags, const int32_t* glob_cu, const int32_t* glob_pos,
+                const int32_t* seq_tile_base, int32_t tile_rows, int32_t max_qgroup_len,
                 void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- Encoder-loop kernels (R/encoder.py:306-371, :475-509) -------------- */

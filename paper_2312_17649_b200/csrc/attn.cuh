@@ -34,6 +34,22 @@ struct AttnArgs {
 };
 
 bool load_links(const int32_t* links, Links* L);
+
+// Tiled doc-band attention backward (attn_bwd_band.cu): bf16, head_dim 64, doc tiles of 64 rows.
+struct BandBwdArgs {
+  const __nv_bfloat16 *q, *k, *v, *out, *dout;
+  int64_t ld, ld_out, ld_dout;
+  float *dq, *dk, *dv;
+  int64_t ld_grad;
+  float2* stats;                  // [T*H] (lse, D), shared with the generic kernels
+  const int32_t *cu, *qlen, *tile_base;
+  int nseq, H, w;                 // w = doc->doc window
+  Links links;
+  int padding;
+  float inv_scale;
+};
+// phase 0: doc-row statistics + dQ; phase 1: doc-key dK / dV.  max_head = 1 + max qgroup_len (<= 32).
+int launch_attn_bwd_band(const BandBwdArgs& a, int ntiles, int max_head, int phase, cudaStream_t st);
 int launch_attn_generic(const AttnArgs& a, int dtype, cudaStream_t st);
 
 // Rows of the query group that attend the whole document (FULL doc link):

@@ -18,18 +18,36 @@
 //      and reduces dK_j, dV_j in registers.
 // Global QDS rows attend every key densely (their windowed result is
 // discarded by the reference, R/attention.py:461-470, :488-493).
+#include <stdlib.h>
+
 #include "attn.cuh"
 
 namespace sc {
 
 constexpr int kBwdWarps = 4;
 constexpr int kBwdMaxD = 128;
-constexpr int kBwdE = kBwdMaxD / 32;
+constexpr int kLongRange = 32;  // ranges of >= this many rows go lane-parallel (coop_dots)
 
-template <typename T>
-__device__ __forceinline__ float dot_sv(const float* __restrict__ xs, const T* __restrict__ r, int d) {
+// A head row lives in registers: lane holds dims lane + 32e, e < E (E = ceil(d/32)).
+template <typename T, int E>
+__device__ __forceinline__ void load_vec(float (&x)[E], const T* __restrict__ r, int lane, int d) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int c = lane + 32 * e;
+    x[e] = c < d ? to_f32(r[c]) : 0.f;
+  }
+}
+
+template <typename T, int E>
+__device__ __forceinline__ float dot_part(const float (&x)[E], const T* __restrict__ r, float (&y)[E], int lane,
+                                          int d) {
   float acc = 0.f;
-  for (int c = 0; c < d; ++c) acc = fmaf(xs[c], to_f32(r[c]), acc);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int c = lane + 32 * e;
+    y[e] = c < d ? to_f32(r[c]) : 0.f;
+    acc = fmaf(x[e], y[e], acc);
+  }
   return acc;
 }
 
@@ -42,63 +60,178 @@ struct BwdArgs {
   float* dv;
   int64_t ld_grad;
   float2* stats;  // [T*H]: (lse, D); lse = +inf for rows without keys
+  int mode;       // 0: every row; 1: only the head rows (cls + query group) of every sequence
+  int maxh;       // mode 1: 1 + max qgroup_len (items per sequence)
 };
+
+// Item -> (row, head).  Mode 1 enumerates nseq x maxh slots, skipping slots past a sequence's head rows.
+__device__ __forceinline__ bool map_item(const BwdArgs& b, int64_t item, int& row, int& h) {
+  const AttnArgs& a = b.a;
+  h = (int)(item % a.H);
+  const int64_t r = item / a.H;
+  if (b.mode == 0) {
+    row = (int)r;
+    return row < a.T;
+  }
+  const int j = (int)(r / b.maxh), i = (int)(r % b.maxh);
+  if (j >= a.nseq || i >= 1 + a.qlen[j]) return false;
+  row = a.cu[j] + i;
+  return true;
+}
 
 __device__ __forceinline__ bool is_global(const AttnArgs& a, int row) {
   return a.glob_cu != nullptr && a.flags && (a.flags[row] & 1);
 }
 
-// Key rows of source row (gs, rs) of sequence j in forward slot order, 32 per call of fn(valid, key_row).
-template <typename F>
-__device__ __forceinline__ void for_each_key_chunk(const AttnArgs& a, const SeqGroups& g, int j, int gs, int rs,
-                                                   bool src_global, int lane, F&& fn) {
+// A run of candidate rows: rows base + t for t in [lo, hi) (or glob_pos[lo..hi) when pos != null),
+// minus rows rejected by `skip`.
+struct Range {
+  int base, lo, hi;
+  const int32_t* pos;
+  int skip;  // 0 none, 1 drop QDS-global rows, 2 keep only non-global rows (same test)
+};
+
+__device__ __forceinline__ int range_row(const Range& R, int t) { return R.base + (R.pos ? R.pos[t] : t); }
+
+// Key ranges of source row (gs, rs) of sequence j, forward slot order.  Returns the count.
+__device__ __forceinline__ int key_ranges(const AttnArgs& a, const SeqGroups& g, int j, int gs, int rs,
+                                          bool src_global, Range (&out)[4]) {
   const bool qds = a.glob_cu != nullptr;
-  int seg_t[4], seg_w[4], nseg = 0;
-  if (src_global) {
-    for (int t = 0; t < 3; ++t) { seg_t[nseg] = t; seg_w[nseg] = SC_LINK_FULL; ++nseg; }
-  } else {
-    for (int t = 0; t < 3; ++t) {
-      const int w = a.links.w[gs][t];
-      if (w != SC_LINK_NONE) { seg_t[nseg] = t; seg_w[nseg] = w; ++nseg; }
-    }
-    if (qds && gs == 2) { seg_t[nseg] = 3; seg_w[nseg] = SC_LINK_FULL; ++nseg; }
+  int n = 0;
+  for (int t = 0; t < 3; ++t) {
+    const int w = src_global ? SC_LINK_FULL : a.links.w[gs][t];
+    if (w == SC_LINK_NONE) continue;
+    int lo = 0, hi = g.len[t];
+    if (w >= 0) { lo = max(0, rs - w); hi = min(g.len[t], rs + w + 1); }
+    out[n++] = Range{g.start + g.off[t], lo, hi, nullptr, (qds && gs == 2 && t == 2 && w >= 0) ? 1 : 0};
   }
-  for (int sgi = 0; sgi < nseg; ++sgi) {
-    const int tg = seg_t[sgi], w = seg_w[sgi];
-    if (tg == 3) {
-      const int gb = a.glob_cu[j], ge = a.glob_cu[j + 1];
-      for (int base = gb; base < ge; base += 32) {
-        const int idx = base + lane;
-        const bool valid = idx < ge;
-        fn(valid, valid ? g.start + g.off[2] + a.glob_pos[idx] : g.start);
-      }
-      continue;
+  if (qds && gs == 2 && !src_global)
+    out[n++] = Range{g.start + g.off[2], a.glob_cu[j], a.glob_cu[j + 1], a.glob_pos, 0};
+  return n;
+}
+
+// Source ranges whose slots address key (tg, r) of sequence j (the transposed pattern).
+__device__ __forceinline__ int source_ranges(const AttnArgs& a, const SeqGroups& g, int j, int tg, int r,
+                                             bool key_global, Range (&out)[5]) {
+  const bool qds = a.glob_cu != nullptr;
+  int n = 0;
+  for (int gs = 0; gs < 3; ++gs) {
+    const int w = a.links.w[gs][tg];
+    const bool qds_doc = qds && gs == 2;
+    if (w == SC_LINK_NONE || (qds_doc && tg == 2 && w >= 0 && key_global)) continue;
+    int lo = 0, hi = g.len[gs];
+    if (w >= 0) { lo = max(0, r - w); hi = min(g.len[gs], r + w + 1); }
+    out[n++] = Range{g.start + g.off[gs], lo, hi, nullptr, qds_doc ? 1 : 0};
+  }
+  if (qds) {
+    if (key_global) out[n++] = Range{g.start + g.off[2], 0, g.len[2], nullptr, 1};  // dense globals segment
+    out[n++] = Range{g.start + g.off[2], a.glob_cu[j], a.glob_cu[j + 1], a.glob_pos, 0};  // global rows
+  }
+  return n;
+}
+
+// Visit the rows of a range: full 32-row chunks lane-parallel (chunk(valid, row)), the rest in
+// groups of kGroup rows processed together by the whole warp (group(rows, ok)) so their loads and
+// reductions overlap.  Work units (chunks / groups, counted across ranges by `unit`) are dealt
+// round-robin to the nsplit warps cooperating on one item.
+constexpr int kGroup = 4;
+
+template <typename Group, typename Chunk>
+__device__ __forceinline__ void visit(const AttnArgs& a, const Range& R, int lane, int split, int nsplit, int& unit,
+                                      Group&& group, Chunk&& chunk) {
+  int t = R.lo;
+  if (R.hi - R.lo >= kLongRange) {
+    for (; t + 32 <= R.hi; t += 32) {
+      if (unit++ % nsplit != split) continue;
+      const int row = range_row(R, t + lane);
+      const bool valid = !(R.skip && is_global(a, row));
+      chunk(valid, row);
     }
-    const int len = g.len[tg];
-    int lo = 0, hi = len;
-    if (w >= 0) { lo = max(0, rs - w); hi = min(len, rs + w + 1); }
-    const bool excl = qds && gs == 2 && tg == 2 && w >= 0;
-    for (int base = lo; base < hi; base += 32) {
-      const int t = base + lane;
-      bool valid = t < hi;
-      const int key_row = g.start + g.off[tg] + (valid ? t : lo);
-      if (valid && excl && is_global(a, key_row)) valid = false;
-      fn(valid, key_row);
+  }
+  for (; t < R.hi; t += kGroup) {
+    if (unit++ % nsplit != split) continue;
+    int rows[kGroup];
+    bool ok[kGroup];
+#pragma unroll
+    for (int u = 0; u < kGroup; ++u) {
+      ok[u] = t + u < R.hi;
+      rows[u] = range_row(R, ok[u] ? t + u : t);
+      if (ok[u] && R.skip && is_global(a, rows[u])) ok[u] = false;
     }
+    group(rows, ok);
   }
 }
 
-// Kernel 1: lse_i, D_i and dQ_i, one warp per (row, head).
+// N independent warp reductions, interleaved.
+template <int N>
+__device__ __forceinline__ void warp_sum_n(float (&v)[N]) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int u = 0; u < N; ++u) v[u] += __shfl_xor_sync(0xffffffffu, v[u], off);
+  }
+}
+
+// Lane-private dot product of a shared-memory row x with one global row (16-byte loads when aligned).
 template <typename T>
-__global__ void __launch_bounds__(kBwdWarps * 32) attn_bwd_dq_kernel(BwdArgs b) {
-  __shared__ float qs_all[kBwdWarps][kBwdMaxD];
-  __shared__ float do_all[kBwdWarps][kBwdMaxD];
+__device__ __forceinline__ float lane_dot(const float* __restrict__ x, const T* __restrict__ r, int d) {
+  float acc = 0.f;
+  constexpr int V = 16 / sizeof(T);
+  if ((d % V) == 0 && (reinterpret_cast<uintptr_t>(r) & 15) == 0) {
+    const uint4* rv = reinterpret_cast<const uint4*>(r);
+    for (int c = 0; c < d / V; ++c) {
+      const uint4 u = __ldg(rv + c);
+      if constexpr (sizeof(T) == 2) {
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(b2[e]);
+          acc = fmaf(x[V * c + 2 * e], f.x, fmaf(x[V * c + 2 * e + 1], f.y, acc));
+        }
+      } else {
+        const float* f = reinterpret_cast<const float*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc = fmaf(x[V * c + e], f[e], acc);
+      }
+    }
+    return acc;
+  }
+  for (int c = 0; c < d; ++c) acc = fmaf(x[c], to_f32(r[c]), acc);
+  return acc;
+}
+
+// Per-warp staging of register rows (lane holds dims lane + 32e) into shared memory.
+template <int E>
+__device__ __forceinline__ void stash(float* dst, const float (&x)[E], int lane, int d) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int c = lane + 32 * e;
+    if (c < d) dst[c] = x[e];
+  }
+}
+
+// Item geometry.  NS == 1: one warp per item, kBwdWarps items per CTA.  NS > 1: one CTA of NS warps
+// per item, the warps splitting the item's key (or source) ranges; partials reduced in shared memory
+// in warp order (deterministic).
+template <int NS>
+struct ItemSlot {
+  static constexpr int kWarpsPerCta = NS > 1 ? NS : kBwdWarps;
+  __device__ static int64_t item(int warp) { return NS > 1 ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * kBwdWarps + warp; }
+  __device__ static int split(int warp) { return NS > 1 ? warp : 0; }
+};
+
+// Kernel 1: lse_i, D_i and dQ_i per (row, head).
+template <typename T, int E, int NS>
+__global__ void __launch_bounds__(ItemSlot<NS>::kWarpsPerCta * 32) attn_bwd_dq_kernel(BwdArgs b) {
+  constexpr int WPC = ItemSlot<NS>::kWarpsPerCta;
+  __shared__ float xs_all[WPC][2][kBwdMaxD];
+  __shared__ float red_ml[NS][2];
+  __shared__ float red_v[NS > 1 ? NS : 1][kBwdMaxD];
   const AttnArgs& a = b.a;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t item = (int64_t)blockIdx.x * kBwdWarps + warp;
-  const int h = (int)(item % a.H);
-  const int row = (int)(item / a.H);
-  if (row >= a.T) return;
+  const int split = ItemSlot<NS>::split(warp);
+  int row, h;
+  if (!map_item(b, ItemSlot<NS>::item(warp), row, h)) return;  // uniform per CTA when NS > 1
   const int j = find_seq(a.cu, a.nseq, row);
   const T* Q = static_cast<const T*>(a.q);
   const T* K = static_cast<const T*>(a.k);
@@ -106,27 +239,33 @@ __global__ void __launch_bounds__(kBwdWarps * 32) attn_bwd_dq_kernel(BwdArgs b) 
   const T* O = static_cast<const T*>(a.out);
   const T* dO = static_cast<const T*>(b.dout);
   const int d = a.d, hoff = h * d;
+  const float inv_scale = 1.f / a.scale;
   const SeqGroups g = seq_groups(a.cu, a.qlen, j);
   const int i = row - g.start;
   const int gs = i == 0 ? 0 : (i < 1 + g.len[1] ? 1 : 2);
   const int rs = i - g.off[gs];
   const bool src_global = gs == 2 && is_global(a, row);
 
-  float* qs = qs_all[warp];
-  float* dos = do_all[warp];
-  float dpart = 0.f;
-  for (int c = lane; c < d; c += 32) {
-    qs[c] = to_f32(Q[(int64_t)row * a.ld + hoff + c]);
-    const float go = to_f32(dO[(int64_t)row * b.ld_dout + hoff + c]);
-    dos[c] = go;
-    dpart = fmaf(go, to_f32(O[(int64_t)row * a.ld_out + hoff + c]), dpart);
-  }
+  float qr[E], dr[E], o[E];
+  load_vec<T, E>(qr, Q + (int64_t)row * a.ld + hoff, lane, d);
+  load_vec<T, E>(dr, dO + (int64_t)row * b.ld_dout + hoff, lane, d);
+  load_vec<T, E>(o, O + (int64_t)row * a.ld_out + hoff, lane, d);
+  float* qs = xs_all[warp][0];
+  float* ds_ = xs_all[warp][1];
+  stash<E>(qs, qr, lane, d);
+  stash<E>(ds_, dr, lane, d);
   __syncwarp();
+  float dpart = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) dpart = fmaf(dr[e], o[e], dpart);
   const float D = warp_sum(dpart);
 
-  // row max and normaliser; zero-logit padding slots enter with logit 0
-  float m = -INFINITY, lsum = 0.f;
-  if (a.padding == SC_PAD_ZERO_LOGIT && !src_global) {
+  Range R[4];
+  const int nr = key_ranges(a, g, j, gs, rs, src_global, R);
+
+  // pass 1: row max and normaliser (uniform per warp); zero-logit padding slots enter with logit 0
+  float m = -INFINITY, l = 0.f;
+  if (split == 0 && a.padding == SC_PAD_ZERO_LOGIT && !src_global) {
     int n_inv = 0;
     for (int t = 0; t < 3; ++t) {
       const int w = a.links.w[gs][t];
@@ -134,165 +273,280 @@ __global__ void __launch_bounds__(kBwdWarps * 32) attn_bwd_dq_kernel(BwdArgs b) 
       const int lo = max(0, rs - w), hi = min(g.len[t], rs + w + 1);
       n_inv += (2 * w + 1) - max(0, hi - lo);
     }
-    if (n_inv > 0) { m = 0.f; lsum = lane == 0 ? (float)n_inv : 0.f; }
+    if (n_inv > 0) { m = 0.f; l = (float)n_inv; }
   }
-  for_each_key_chunk(a, g, j, gs, rs, src_global, lane, [&](bool valid, int key_row) {
-    const float s = valid ? dot_sv<T>(qs, K + (int64_t)key_row * a.ld + hoff, d) / a.scale : -INFINITY;
-    const float cmax = warp_max(s);
-    if (cmax == -INFINITY) return;
-    const float mnew = fmaxf(m, cmax);
-    lsum = lsum * (m == -INFINITY ? 0.f : expf(m - mnew)) + (valid ? expf(s - mnew) : 0.f);
-    m = mnew;
-  });
-  const float l = warp_sum(lsum);
+  auto fold = [&](float s) {  // uniform logit
+    if (s > m) { l = l * expf(m - s) + 1.f; m = s; }
+    else l += expf(s - m);
+  };
+  int unit = 0;
+  for (int ri = 0; ri < nr; ++ri) {
+    visit(a, R[ri], lane, split, NS, unit,
+          [&](const int (&kr)[kGroup], const bool (&ok)[kGroup]) {
+            float sp[kGroup];
+#pragma unroll
+            for (int u = 0; u < kGroup; ++u) {
+              float y[E];
+              sp[u] = ok[u] ? dot_part<T, E>(qr, K + (int64_t)kr[u] * a.ld + hoff, y, lane, d) : 0.f;
+            }
+            warp_sum_n<kGroup>(sp);
+#pragma unroll
+            for (int u = 0; u < kGroup; ++u)
+              if (ok[u]) fold(sp[u] * inv_scale);
+          },
+          [&](bool valid, int kr) {
+            const float s = valid ? lane_dot<T>(qs, K + (int64_t)kr * a.ld + hoff, d) * inv_scale : -INFINITY;
+            const float cmax = warp_max(s);
+            if (cmax == -INFINITY) return;
+            const float mnew = fmaxf(m, cmax);
+            const float csum = warp_sum(valid ? expf(s - mnew) : 0.f);
+            l = l * (m == -INFINITY ? 0.f : expf(m - mnew)) + csum;
+            m = mnew;
+          });
+  }
+  if constexpr (NS > 1) {  // combine the warps' (m, l) in warp order
+    if (lane == 0) { red_ml[split][0] = m; red_ml[split][1] = l; }
+    __syncthreads();
+    m = -INFINITY;
+    for (int u = 0; u < NS; ++u) m = fmaxf(m, red_ml[u][0]);
+    l = 0.f;
+    for (int u = 0; u < NS; ++u)
+      if (red_ml[u][0] != -INFINITY) l += red_ml[u][1] * expf(red_ml[u][0] - m);
+  }
   const float lse = l > 0.f ? m + logf(l) : INFINITY;
-  if (lane == 0) b.stats[item] = make_float2(lse, D);
+  if (lane == 0 && split == 0) b.stats[(int64_t)row * a.H + h] = make_float2(lse, D);
 
-  float dq[kBwdE];
+  // pass 2: dQ_i = sum_j dS_ij K_j
+  float dq[E];
 #pragma unroll
-  for (int e = 0; e < kBwdE; ++e) dq[e] = 0.f;
+  for (int e = 0; e < E; ++e) dq[e] = 0.f;
   if (l > 0.f) {
-    for_each_key_chunk(a, g, j, gs, rs, src_global, lane, [&](bool valid, int key_row) {
-      float ds = 0.f;
-      if (valid) {
-        const float s = dot_sv<T>(qs, K + (int64_t)key_row * a.ld + hoff, d) / a.scale;
-        const float p = expf(s - lse);
-        ds = p * (dot_sv<T>(dos, V + (int64_t)key_row * a.ld + hoff, d) - D) / a.scale;
-      }
-      unsigned live = __ballot_sync(0xffffffffu, valid);
-      while (live) {
-        const int kk = __ffs(live) - 1;
-        live &= live - 1;
-        const float dsk = __shfl_sync(0xffffffffu, ds, kk);
-        const T* kr = K + (int64_t)__shfl_sync(0xffffffffu, key_row, kk) * a.ld + hoff;
+    unit = 0;
+    for (int ri = 0; ri < nr; ++ri) {
+      visit(a, R[ri], lane, split, NS, unit,
+            [&](const int (&kr)[kGroup], const bool (&ok)[kGroup]) {
+              float kv[kGroup][E], sp[2 * kGroup];
 #pragma unroll
-        for (int e = 0; e < kBwdE; ++e) {
-          const int c = lane + 32 * e;
-          if (c < d) dq[e] = fmaf(dsk, to_f32(kr[c]), dq[e]);
-        }
-      }
-    });
+              for (int u = 0; u < kGroup; ++u) {
+                float vv[E];
+                sp[u] = ok[u] ? dot_part<T, E>(qr, K + (int64_t)kr[u] * a.ld + hoff, kv[u], lane, d) : 0.f;
+                sp[kGroup + u] = ok[u] ? dot_part<T, E>(dr, V + (int64_t)kr[u] * a.ld + hoff, vv, lane, d) : 0.f;
+              }
+              warp_sum_n<2 * kGroup>(sp);
+#pragma unroll
+              for (int u = 0; u < kGroup; ++u) {
+                if (!ok[u]) continue;
+                const float dsv = expf(sp[u] * inv_scale - lse) * (sp[kGroup + u] - D) * inv_scale;
+#pragma unroll
+                for (int e = 0; e < E; ++e) dq[e] = fmaf(dsv, kv[u][e], dq[e]);
+              }
+            },
+            [&](bool valid, int kr) {
+              float dsv = 0.f;
+              if (valid) {
+                const float sd = lane_dot<T>(qs, K + (int64_t)kr * a.ld + hoff, d);
+                const float dp = lane_dot<T>(ds_, V + (int64_t)kr * a.ld + hoff, d);
+                dsv = expf(sd * inv_scale - lse) * (dp - D) * inv_scale;
+              }
+              const unsigned vm = __ballot_sync(0xffffffffu, valid && dsv != 0.f);
+#pragma unroll
+              for (int kk = 0; kk < 32; ++kk) {
+                const float dsk = __shfl_sync(0xffffffffu, dsv, kk);
+                const T* krp = K + (int64_t)__shfl_sync(0xffffffffu, kr, kk) * a.ld + hoff;
+                if ((vm >> kk) & 1u) {
+#pragma unroll
+                  for (int e = 0; e < E; ++e) {
+                    const int c = lane + 32 * e;
+                    if (c < d) dq[e] = fmaf(dsk, to_f32(krp[c]), dq[e]);
+                  }
+                }
+              }
+            });
+    }
+  }
+  if constexpr (NS > 1) {
+    stash<E>(red_v[split], dq, lane, d);
+    __syncthreads();
+    if (split != 0) return;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int c = lane + 32 * e;
+      float acc = 0.f;
+      if (c < d)
+        for (int u = 0; u < NS; ++u) acc += red_v[u][c];
+      dq[e] = acc;
+    }
   }
   float* dqr = b.dq + (int64_t)row * b.ld_grad + hoff;
 #pragma unroll
-  for (int e = 0; e < kBwdE; ++e) {
+  for (int e = 0; e < E; ++e) {
     const int c = lane + 32 * e;
     if (c < d) dqr[c] = dq[e];
   }
 }
 
-// Kernel 2: dK_j, dV_j, one warp per (key row, head), over the transposed pattern.
-template <typename T>
-__global__ void __launch_bounds__(kBwdWarps * 32) attn_bwd_dkv_kernel(BwdArgs b) {
-  __shared__ float ks_all[kBwdWarps][kBwdMaxD];
-  __shared__ float vs_all[kBwdWarps][kBwdMaxD];
+// Kernel 2: dK_j, dV_j per (key row, head), over the transposed pattern.
+template <typename T, int E, int NS>
+__global__ void __launch_bounds__(ItemSlot<NS>::kWarpsPerCta * 32) attn_bwd_dkv_kernel(BwdArgs b) {
+  constexpr int WPC = ItemSlot<NS>::kWarpsPerCta;
+  __shared__ float xs_all[WPC][2][kBwdMaxD];
+  __shared__ float red_k[NS > 1 ? NS : 1][kBwdMaxD];
+  __shared__ float red_vv[NS > 1 ? NS : 1][kBwdMaxD];
   const AttnArgs& a = b.a;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t item = (int64_t)blockIdx.x * kBwdWarps + warp;
-  const int h = (int)(item % a.H);
-  const int krow = (int)(item / a.H);
-  if (krow >= a.T) return;
+  const int split = ItemSlot<NS>::split(warp);
+  int krow, h;
+  if (!map_item(b, ItemSlot<NS>::item(warp), krow, h)) return;
   const int j = find_seq(a.cu, a.nseq, krow);
   const T* Q = static_cast<const T*>(a.q);
   const T* K = static_cast<const T*>(a.k);
   const T* V = static_cast<const T*>(a.v);
   const T* dO = static_cast<const T*>(b.dout);
   const int d = a.d, hoff = h * d;
+  const float inv_scale = 1.f / a.scale;
   const SeqGroups g = seq_groups(a.cu, a.qlen, j);
   const int i = krow - g.start;
   const int tg = i == 0 ? 0 : (i < 1 + g.len[1] ? 1 : 2);
   const int r = i - g.off[tg];
-  const bool qds = a.glob_cu != nullptr;
   const bool key_global = tg == 2 && is_global(a, krow);
 
-  float* ks = ks_all[warp];
-  float* vs = vs_all[warp];
-  for (int c = lane; c < d; c += 32) {
-    ks[c] = to_f32(K[(int64_t)krow * a.ld + hoff + c]);
-    vs[c] = to_f32(V[(int64_t)krow * a.ld + hoff + c]);
-  }
+  float kr[E], vr[E];
+  load_vec<T, E>(kr, K + (int64_t)krow * a.ld + hoff, lane, d);
+  load_vec<T, E>(vr, V + (int64_t)krow * a.ld + hoff, lane, d);
+  float* ks = xs_all[warp][0];
+  float* vs = xs_all[warp][1];
+  stash<E>(ks, kr, lane, d);
+  stash<E>(vs, vr, lane, d);
   __syncwarp();
-
-  float dk[kBwdE], dv[kBwdE];
+  float dk[E], dv[E];
 #pragma unroll
-  for (int e = 0; e < kBwdE; ++e) { dk[e] = 0.f; dv[e] = 0.f; }
+  for (int e = 0; e < E; ++e) { dk[e] = 0.f; dv[e] = 0.f; }
 
-  // One slot of source row `src` addressing this key (valid lanes only contribute).
-  auto chunk = [&](bool valid, int src) {
-    float p = 0.f, ds = 0.f;
-    if (valid) {
-      const float2 st = b.stats[(int64_t)src * a.H + h];
-      const float s = dot_sv<T>(ks, Q + (int64_t)src * a.ld + hoff, d) / a.scale;
-      p = expf(s - st.x);
-      ds = p * (dot_sv<T>(vs, dO + (int64_t)src * b.ld_dout + hoff, d) - st.y) / a.scale;
-    }
-    unsigned live = __ballot_sync(0xffffffffu, valid && p != 0.f);
-    while (live) {
-      const int kk = __ffs(live) - 1;
-      live &= live - 1;
-      const float pk = __shfl_sync(0xffffffffu, p, kk), dsk = __shfl_sync(0xffffffffu, ds, kk);
-      const int sr = __shfl_sync(0xffffffffu, src, kk);
-      const T* qr = Q + (int64_t)sr * a.ld + hoff;
-      const T* gr = dO + (int64_t)sr * b.ld_dout + hoff;
+  Range R[5];
+  const int nr = source_ranges(a, g, j, tg, r, key_global, R);
+  int unit = 0;
+  for (int ri = 0; ri < nr; ++ri) {
+    visit(a, R[ri], lane, split, NS, unit,
+          [&](const int (&src)[kGroup], const bool (&ok)[kGroup]) {
+            float qv[kGroup][E], gv[kGroup][E], sp[2 * kGroup];
+            float2 st[kGroup];
 #pragma unroll
-      for (int e = 0; e < kBwdE; ++e) {
-        const int c = lane + 32 * e;
-        if (c < d) {
-          dk[e] = fmaf(dsk, to_f32(qr[c]), dk[e]);
-          dv[e] = fmaf(pk, to_f32(gr[c]), dv[e]);
-        }
-      }
-    }
-  };
-
-  // Source groups by link (src gs -> this key's group tg).  QDS doc sources:
-  // non-global rows follow the link (minus windowed doc-doc slots on global
-  // keys) plus the dense globals segment; global rows attend every key.
-  for (int gs = 0; gs < 3; ++gs) {
-    const int w = a.links.w[gs][tg];
-    const bool qds_doc = qds && gs == 2;
-    if (w != SC_LINK_NONE && !(qds_doc && tg == 2 && w >= 0 && key_global)) {
-      int lo = 0, hi = g.len[gs];
-      if (w >= 0) { lo = max(0, r - w); hi = min(g.len[gs], r + w + 1); }
-      for (int base = lo; base < hi; base += 32) {
-        const int t = base + lane;
-        bool valid = t < hi;
-        const int src = g.start + g.off[gs] + (valid ? t : lo);
-        if (valid && qds_doc && is_global(a, src)) valid = false;
-        chunk(valid, src);
-      }
+            for (int u = 0; u < kGroup; ++u) {
+              sp[u] = ok[u] ? dot_part<T, E>(kr, Q + (int64_t)src[u] * a.ld + hoff, qv[u], lane, d) : 0.f;
+              sp[kGroup + u] =
+                  ok[u] ? dot_part<T, E>(vr, dO + (int64_t)src[u] * b.ld_dout + hoff, gv[u], lane, d) : 0.f;
+              st[u] = ok[u] ? b.stats[(int64_t)src[u] * a.H + h] : make_float2(INFINITY, 0.f);
+            }
+            warp_sum_n<2 * kGroup>(sp);
+#pragma unroll
+            for (int u = 0; u < kGroup; ++u) {
+              if (!ok[u]) continue;
+              const float p = expf(sp[u] * inv_scale - st[u].x);
+              const float dsv = p * (sp[kGroup + u] - st[u].y) * inv_scale;
+#pragma unroll
+              for (int e = 0; e < E; ++e) {
+                dk[e] = fmaf(dsv, qv[u][e], dk[e]);
+                dv[e] = fmaf(p, gv[u][e], dv[e]);
+              }
+            }
+          },
+          [&](bool valid, int src) {
+            float p = 0.f, dsv = 0.f;
+            if (valid) {
+              const float2 st = b.stats[(int64_t)src * a.H + h];
+              const float sd = lane_dot<T>(ks, Q + (int64_t)src * a.ld + hoff, d);
+              const float dp = lane_dot<T>(vs, dO + (int64_t)src * b.ld_dout + hoff, d);
+              p = expf(sd * inv_scale - st.x);
+              dsv = p * (dp - st.y) * inv_scale;
+            }
+            const unsigned live = __ballot_sync(0xffffffffu, valid && p != 0.f);
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) {
+              const float pk = __shfl_sync(0xffffffffu, p, kk), dsk = __shfl_sync(0xffffffffu, dsv, kk);
+              const int sr = __shfl_sync(0xffffffffu, src, kk);
+              if ((live >> kk) & 1u) {
+                const T* qp = Q + (int64_t)sr * a.ld + hoff;
+                const T* gp = dO + (int64_t)sr * b.ld_dout + hoff;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                  const int c = lane + 32 * e;
+                  if (c < d) {
+                    dk[e] = fmaf(dsk, to_f32(qp[c]), dk[e]);
+                    dv[e] = fmaf(pk, to_f32(gp[c]), dv[e]);
+                  }
+                }
+              }
+            }
+          });
+  }
+  if constexpr (NS > 1) {
+    stash<E>(red_k[split], dk, lane, d);
+    stash<E>(red_vv[split], dv, lane, d);
+    __syncthreads();
+    if (split != 0) return;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int c = lane + 32 * e;
+      float ak = 0.f, av = 0.f;
+      if (c < d)
+        for (int u = 0; u < NS; ++u) { ak += red_k[u][c]; av += red_vv[u][c]; }
+      dk[e] = ak;
+      dv[e] = av;
     }
   }
-  if (qds) {
-    const int dlo = g.start + g.off[2], dlen = g.len[2];
-    if (key_global) {  // dense globals segment of every non-global doc row
-      for (int base = 0; base < dlen; base += 32) {
-        const int t = base + lane;
-        const int src = dlo + min(t, dlen - 1);
-        chunk(t < dlen && !is_global(a, src), src);
-      }
-    }
-    // global doc rows attend every key of every group
-    const int gb = a.glob_cu[j], ge = a.glob_cu[j + 1];
-    for (int base = gb; base < ge; base += 32) {
-      const int idx = base + lane;
-      const bool valid = idx < ge;
-      chunk(valid, valid ? dlo + a.glob_pos[idx] : dlo);
-    }
-  }
-
   float* dkr = b.dk + (int64_t)krow * b.ld_grad + hoff;
   float* dvr = b.dv + (int64_t)krow * b.ld_grad + hoff;
 #pragma unroll
-  for (int e = 0; e < kBwdE; ++e) {
+  for (int e = 0; e < E; ++e) {
     const int c = lane + 32 * e;
     if (c < d) { dkr[c] = dk[e]; dvr[c] = dv[e]; }
   }
 }
 
+// Mode 0: one warp per (row, head).  Mode 1 (head rows / keys, long dense ranges): a CTA of
+// kHeadSplit warps per (row, head).
+constexpr int kHeadSplit = 8;
+
+template <typename T, int E>
+int launch_generic(const BwdArgs& b, int which, cudaStream_t st) {
+  if (b.mode == 0) {
+    const int64_t items = (int64_t)b.a.T * b.a.H;
+    const unsigned blocks = (unsigned)((items + kBwdWarps - 1) / kBwdWarps);
+    if (which == 0) attn_bwd_dq_kernel<T, E, 1><<<blocks, kBwdWarps * 32, 0, st>>>(b);
+    else attn_bwd_dkv_kernel<T, E, 1><<<blocks, kBwdWarps * 32, 0, st>>>(b);
+  } else {
+    const unsigned blocks = (unsigned)((int64_t)b.a.nseq * b.maxh * b.a.H);
+    if (which == 0) attn_bwd_dq_kernel<T, E, kHeadSplit><<<blocks, kHeadSplit * 32, 0, st>>>(b);
+    else attn_bwd_dkv_kernel<T, E, kHeadSplit><<<blocks, kHeadSplit * 32, 0, st>>>(b);
+  }
+  SC_CHECK_LAUNCH(which == 0 ? "attn_bwd_dq_kernel" : "attn_bwd_dkv_kernel");
+  return SC_OK;
+}
+
+template <typename T>
+int launch_generic_d(const BwdArgs& b, int which, cudaStream_t st) {
+  const int d = b.a.d;
+  if (d <= 32) return launch_generic<T, 1>(b, which, st);
+  if (d <= 64) return launch_generic<T, 2>(b, which, st);
+  return launch_generic<T, 4>(b, which, st);
+}
+
+int launch_generic_any(const BwdArgs& b, int dtype, int which, cudaStream_t st) {
+  return dtype == SC_DTYPE_F32 ? launch_generic_d<float>(b, which, st) : launch_generic_d<__nv_bfloat16>(b, which, st);
+}
+
 }  // namespace sc
 
 using namespace sc;
+
+// SC_BWD_GENERIC=1 forces the generic kernels (A/B experiments, parity cross-checks).
+static bool force_generic() {
+  static const bool v = [] {
+    const char* e = getenv("SC_BWD_GENERIC");
+    return e && atoi(e) != 0;
+  }();
+  return v;
+}
 
 extern "C" size_t sc_attn_bwd_workspace_bytes(int32_t total_tokens, int32_t heads) {
   return (size_t)(total_tokens > 0 ? total_tokens : 0) * (size_t)(heads > 0 ? heads : 0) * sizeof(float2);
@@ -303,7 +557,8 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
                            float* dv, int64_t grad_row_stride, const int32_t* cu_seqlens, const int32_t* qgroup_len,
                            int32_t nseq, int32_t total_tokens, int32_t heads, int32_t head_dim, const int32_t* links,
                            int32_t padding, float scale, int32_t dtype, const uint8_t* tok_flags,
-                           const int32_t* glob_cu, const int32_t* glob_pos, void* workspace, size_t workspace_bytes,
+                           const int32_t* glob_cu, const int32_t* glob_pos, const int32_t* seq_tile_base,
+                           int32_t tile_rows, int32_t max_qgroup_len, void* workspace, size_t workspace_bytes,
                            void* stream) {
   BwdArgs b = {};
   AttnArgs& a = b.a;
@@ -319,19 +574,46 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
                "sc_attn_bwd: QDS globals need tok_flags, glob_cu and glob_pos");
   SC_CHECK_ARG(workspace && workspace_bytes >= sc_attn_bwd_workspace_bytes(total_tokens, heads),
                "sc_attn_bwd: workspace must hold sc_attn_bwd_workspace_bytes(T, H) bytes");
+  SC_CHECK_ARG(max_qgroup_len >= 1, "sc_attn_bwd: max_qgroup_len must be >= 1");
   a.q = q; a.k = k; a.v = v; a.ld = row_stride; a.out = const_cast<void*>(out); a.ld_out = out_row_stride;
   a.cu = cu_seqlens; a.qlen = qgroup_len; a.nseq = nseq; a.T = total_tokens; a.H = heads; a.d = head_dim;
   a.padding = padding; a.scale = scale; a.flags = tok_flags; a.glob_cu = glob_cu; a.glob_pos = glob_pos;
   b.dout = dout; b.ld_dout = dout_row_stride; b.dq = dq; b.dk = dk; b.dv = dv; b.ld_grad = grad_row_stride;
   b.stats = static_cast<float2*>(workspace);
-  const int64_t items = (int64_t)total_tokens * heads;
-  const unsigned blocks = (unsigned)((items + kBwdWarps - 1) / kBwdWarps);
+  b.maxh = 1 + max_qgroup_len;
   cudaStream_t st = (cudaStream_t)stream;
-  if (dtype == SC_DTYPE_F32) attn_bwd_dq_kernel<float><<<blocks, kBwdWarps * 32, 0, st>>>(b);
-  else attn_bwd_dq_kernel<__nv_bfloat16><<<blocks, kBwdWarps * 32, 0, st>>>(b);
-  SC_CHECK_LAUNCH("attn_bwd_dq_kernel");
-  if (dtype == SC_DTYPE_F32) attn_bwd_dkv_kernel<float><<<blocks, kBwdWarps * 32, 0, st>>>(b);
-  else attn_bwd_dkv_kernel<__nv_bfloat16><<<blocks, kBwdWarps * 32, 0, st>>>(b);
-  SC_CHECK_LAUNCH("attn_bwd_dkv_kernel");
-  return SC_OK;
+
+  // Fast path: bf16, d = 64, no QDS, a finite doc->doc window <= 24, head groups <= 32 rows, 64-row
+  // tiles from sc_index_build: doc rows / keys on the tiled tensor-core kernels, head rows / keys generic.
+  const int wdd = a.links.w[2][2];
+  const bool aligned = ((row_stride | out_row_stride | dout_row_stride) % 8) == 0 &&
+                       (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out | (uintptr_t)dout) % 16) == 0 &&
+                       grad_row_stride % 2 == 0 && ((uintptr_t)dq | (uintptr_t)dk | (uintptr_t)dv) % 8 == 0;
+  const bool fast = dtype == SC_DTYPE_BF16 && head_dim == 64 && glob_cu == nullptr && seq_tile_base &&
+                    tile_rows == 64 && wdd >= 0 && wdd <= 24 && b.maxh <= 32 && aligned &&
+                    !force_generic();
+  if (!fast) {
+    b.mode = 0;
+    int rc = launch_generic_any(b, dtype, 0, st);
+    return rc ? rc : launch_generic_any(b, dtype, 1, st);
+  }
+  BandBwdArgs p = {};
+  p.q = (const __nv_bfloat16*)q; p.k = (const __nv_bfloat16*)k; p.v = (const __nv_bfloat16*)v;
+  p.out = (const __nv_bfloat16*)out; p.dout = (const __nv_bfloat16*)dout;
+  p.ld = row_stride; p.ld_out = out_row_stride; p.ld_dout = dout_row_stride;
+  p.dq = dq; p.dk = dk; p.dv = dv; p.ld_grad = grad_row_stride; p.stats = b.stats;
+  p.cu = cu_seqlens; p.qlen = qgroup_len; p.tile_base = seq_tile_base; p.nseq = nseq; p.H = heads; p.w = wdd;
+  p.links = a.links; p.padding = padding; p.inv_scale = 1.f / scale;
+  int ntiles = 0;
+  if (cudaMemcpyAsync(&ntiles, seq_tile_base + nseq, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    set_error("sc_attn_bwd: reading the tile count failed");
+    return SC_ERR_CUDA;
+  }
+  b.mode = 1;
+  int rc = launch_generic_any(b, dtype, 0, st);               // head rows: stats + dQ
+  if (!rc && ntiles) rc = launch_attn_bwd_band(p, ntiles, b.maxh, 0, st);  // doc rows: stats + dQ
+  if (!rc && ntiles) rc = launch_attn_bwd_band(p, ntiles, b.maxh, 1, st);  // doc keys: dK, dV
+  if (!rc) rc = launch_generic_any(b, dtype, 1, st);          // head keys: dK, dV
+  return rc;
 }

@@ -1,0 +1,491 @@
+// Tiled tensor-core attention backward for the doc band (SURVEY §8(f)-4 fast path).
+//
+// The generic adjoint (attn_bwd.cu) spends ~30 instructions per (row, key)
+// pair; for a +-w band that is the whole cost.  Here the doc rows and doc keys
+// are processed in 64-row tiles with mma.sync m16n8k16 (bf16 in, fp32
+// accumulate), FlashAttention-2 style, split into two gather-form kernels so
+// the result stays deterministic:
+//   A (query-major, one CTA per 64 doc rows x head): recompute S over the
+//     row's band keys and its head keys (cls / query group, <= 32 slots),
+//     the row statistics lse_i and D_i = dO_i . O_i (stored for kernel B),
+//     P, dP = dO V^T, dS = P (dP - D) / scale and dQ = dS K;
+//   B (key-major, one CTA per 64 doc keys x head): S^T over the keys' band
+//     sources and head sources (cls / query rows attending the doc), P^T
+//     from the sources' lse, dS^T, dV = P^T dO and dK = dS^T Q.
+// The cls / query rows and keys (long dense ranges) go through the generic
+// kernels in head mode.  Semantics as attn_bwd.cu; the reference chain is
+// R/attention.py:260-269, :348-378, :476-507 and R/band.py:239-274.
+#include "attn.cuh"
+
+namespace sc {
+namespace bwdband {
+
+constexpr int ROWB = 128;          // bytes per 64-dim bf16 row
+constexpr int TILE = 64;           // rows (kernel A) / keys (kernel B) per CTA
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t swz(uint32_t base, int row, int chunk) {
+  return base + row * ROWB + ((chunk ^ (row & 7)) << 4);
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float ex2(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// 16-byte async copy; src_bytes = 0 zero-fills the destination.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// A fragments (16 rows x 64 dims) of the block starting at smem row `row0`.
+__device__ __forceinline__ void load_a(uint32_t buf, int row0, int lane, uint32_t (&a)[4][4]) {
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) ldsm_x4(swz(buf, row0 + (lane & 15), ks * 2 + (lane >> 4)), a[ks]);
+}
+// C[2 n8 tiles] += A(16x64) . B[row0 .. row0+15]^T  (B rows = the n index, 64 dims = k)
+__device__ __forceinline__ void mm_nt16(uint32_t bbuf, int row0, int lane, const uint32_t (&a)[4][4],
+                                        float (&c0)[4], float (&c1)[4]) {
+  const int brow = row0 + (lane & 7) + ((lane >> 4) << 3);
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    uint32_t b[4];
+    ldsm_x4(swz(bbuf, brow, ks * 2 + ((lane >> 3) & 1)), b);
+    mma16816(c0, a[ks], b[0], b[1]);
+    mma16816(c1, a[ks], b[2], b[3]);
+  }
+}
+// O(16x64) += P(16 x 16, as two C-layout n8 tiles) . B[row0 .. row0+15]  (B rows = the k index)
+__device__ __forceinline__ void mm_nn16(uint32_t bbuf, int row0, int lane, const float (&p0)[4],
+                                        const float (&p1)[4], float (&o)[8][4]) {
+  uint32_t a[4] = {pack_bf16(p0[0], p0[1]), pack_bf16(p0[2], p0[3]), pack_bf16(p1[0], p1[1]),
+                   pack_bf16(p1[2], p1[3])};
+  const int brow = row0 + (lane & 7) + (((lane >> 3) & 1) << 3);
+#pragma unroll
+  for (int np = 0; np < 4; ++np) {
+    uint32_t b[4];
+    ldsm_x4_t(swz(bbuf, brow, np * 2 + (lane >> 4)), b);
+    mma16816(o[2 * np], a, b[0], b[1]);
+    mma16816(o[2 * np + 1], a, b[2], b[3]);
+  }
+}
+
+// Stage `nrows` rows (64 bf16 each) into a swizzled smem buffer; rowptr(i) == nullptr zero-fills.
+template <typename F>
+__device__ __forceinline__ void stage_rows(uint32_t buf, int nrows, const __nv_bfloat16* any, F&& rowptr) {
+  for (int idx = threadIdx.x; idx < nrows * 8; idx += blockDim.x) {
+    const int r = idx >> 3, c = idx & 7;
+    const __nv_bfloat16* p = rowptr(r);
+    cp_async16(swz(buf, r, c), p ? p + c * 8 : any, p ? 16 : 0);
+  }
+}
+
+using Args = BandBwdArgs;
+
+// Is doc position `pos` (group-relative) within a link of window w of position `r`?
+__device__ __forceinline__ bool linked(int w, int r, int pos) {
+  return w == SC_LINK_FULL || (w >= 0 && abs(r - pos) <= w);
+}
+
+// Kernel A: doc rows [r0, r0+64) of one sequence, one head.  NB band keys per warp, NH head-key slots.
+template <int NB, int NH>
+__global__ void __launch_bounds__(128) band_dq_kernel(Args p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int KR = 48 + NB;  // band key rows staged per CTA
+  const int tile = blockIdx.x, h = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = find_seq(p.tile_base, p.nseq, tile);
+  const SeqGroups g = seq_groups(p.cu, p.qlen, j);
+  const int dlen = g.len[2], dstart = g.start + g.off[2];
+  const int r0 = (tile - p.tile_base[j]) * TILE;
+  const int w = p.w, hoff = h * 64;
+  const int nhead = 1 + g.len[1];
+
+  const uint32_t sQ = smem_u32(smem), sdO = sQ + TILE * ROWB, sK = sdO + TILE * ROWB, sV = sK + KR * ROWB,
+                 sKH = sV + KR * ROWB, sVH = sKH + NH * ROWB;
+  float* sD = reinterpret_cast<float*>(smem + (2 * TILE + 2 * KR + 2 * NH) * ROWB);
+
+  stage_rows(sQ, TILE, p.q, [&](int r) {
+    return r0 + r < dlen ? p.q + (int64_t)(dstart + r0 + r) * p.ld + hoff : nullptr; });
+  stage_rows(sdO, TILE, p.q, [&](int r) {
+    return r0 + r < dlen ? p.dout + (int64_t)(dstart + r0 + r) * p.ld_dout + hoff : nullptr; });
+  stage_rows(sK, KR, p.q, [&](int r) {
+    const int pos = r0 - w + r;
+    return pos >= 0 && pos < dlen ? p.k + (int64_t)(dstart + pos) * p.ld + hoff : nullptr; });
+  stage_rows(sV, KR, p.q, [&](int r) {
+    const int pos = r0 - w + r;
+    return pos >= 0 && pos < dlen ? p.v + (int64_t)(dstart + pos) * p.ld + hoff : nullptr; });
+  stage_rows(sKH, NH, p.q, [&](int r) { return r < nhead ? p.k + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
+  stage_rows(sVH, NH, p.q, [&](int r) { return r < nhead ? p.v + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
+  cp_async_wait_all();
+  __syncthreads();
+  {  // D_i = dO_i . O_i, two threads per row
+    const int r = threadIdx.x >> 1, half = threadIdx.x & 1;
+    float acc = 0.f;
+    if (r0 + r < dlen) {
+      const __nv_bfloat16* orow = p.out + (int64_t)(dstart + r0 + r) * p.ld_out + hoff + half * 32;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint4 ov = *reinterpret_cast<const uint4*>(orow + c * 8);
+        uint4 gv;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(gv.x), "=r"(gv.y), "=r"(gv.z), "=r"(gv.w)
+                     : "r"(swz(sdO, r, half * 4 + c)));
+        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 of = __bfloat1622float2(o2[e]), gf = __bfloat1622float2(g2[e]);
+          acc = fmaf(of.x, gf.x, fmaf(of.y, gf.y, acc));
+        }
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (half == 0) sD[r] = acc;
+  }
+  __syncthreads();
+
+  const int gq = lane >> 2, tq = lane & 3;
+  const int ra = 16 * warp + gq;         // tile-relative rows of this thread: ra, ra + 8
+  const int rsA = r0 + ra, rsB = rsA + 8;  // doc-relative
+  const float c2 = p.inv_scale * LOG2E;
+  constexpr int NT = NB / 8, NHT = NH / 8;
+
+  uint32_t qa[4][4];
+  load_a(sQ, 16 * warp, lane, qa);
+  float s[NT][4], sh[NHT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+#pragma unroll
+  for (int i = 0; i < NHT; ++i) sh[i][0] = sh[i][1] = sh[i][2] = sh[i][3] = 0.f;
+#pragma unroll
+  for (int kp = 0; kp < NB / 16; ++kp) mm_nt16(sK, 16 * warp + 16 * kp, lane, qa, s[2 * kp], s[2 * kp + 1]);
+#pragma unroll
+  for (int kp = 0; kp < NH / 16; ++kp) mm_nt16(sKH, 16 * kp, lane, qa, sh[2 * kp], sh[2 * kp + 1]);
+
+  // masks: band key kb of this warp sits at doc position r0 + 16*warp - w + kb
+  const int kpos0 = r0 + 16 * warp - w;
+  const int L20 = p.links.w[2][0], L21 = p.links.w[2][1];
+  auto band_ok = [&](int rs, int kb) {
+    const int kp = kpos0 + kb;
+    return rs < dlen && kp >= 0 && kp < dlen && abs(kp - rs) <= w;
+  };
+  auto head_ok = [&](int rs, int sl) {
+    if (rs >= dlen || sl >= nhead) return false;
+    return sl == 0 ? linked(L20, rs, 0) : linked(L21, rs, sl - 1);
+  };
+  float mA = -INFINITY, mB = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int rs = e < 2 ? rsA : rsB, kb = 8 * i + 2 * tq + (e & 1);
+      s[i][e] = band_ok(rs, kb) ? s[i][e] * c2 : -INFINITY;
+      if (e < 2) mA = fmaxf(mA, s[i][e]); else mB = fmaxf(mB, s[i][e]);
+    }
+#pragma unroll
+  for (int i = 0; i < NHT; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int rs = e < 2 ? rsA : rsB, sl = 8 * i + 2 * tq + (e & 1);
+      sh[i][e] = head_ok(rs, sl) ? sh[i][e] * c2 : -INFINITY;
+      if (e < 2) mA = fmaxf(mA, sh[i][e]); else mB = fmaxf(mB, sh[i][e]);
+    }
+  mA = fmaxf(mA, __shfl_xor_sync(0xffffffffu, mA, 1));
+  mA = fmaxf(mA, __shfl_xor_sync(0xffffffffu, mA, 2));
+  mB = fmaxf(mB, __shfl_xor_sync(0xffffffffu, mB, 1));
+  mB = fmaxf(mB, __shfl_xor_sync(0xffffffffu, mB, 2));
+  // zero-logit padding: out-of-range windowed slots join with logit 0
+  auto n_invalid = [&](int rs) {
+    int n = 0;
+    for (int t = 0; t < 3; ++t) {
+      const int wt = p.links.w[2][t];
+      if (wt < 0) continue;
+      const int lo = max(0, rs - wt), hi = min(g.len[t], rs + wt + 1);
+      n += (2 * wt + 1) - max(0, hi - lo);
+    }
+    return n;
+  };
+  const int nA = p.padding == SC_PAD_ZERO_LOGIT && rsA < dlen ? n_invalid(rsA) : 0;
+  const int nB = p.padding == SC_PAD_ZERO_LOGIT && rsB < dlen ? n_invalid(rsB) : 0;
+  if (nA > 0) mA = fmaxf(mA, 0.f);
+  if (nB > 0) mB = fmaxf(mB, 0.f);
+  const float mAs = mA == -INFINITY ? 0.f : mA, mBs = mB == -INFINITY ? 0.f : mB;
+  float lA = 0.f, lB = 0.f;
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    s[i][0] = ex2(s[i][0] - mAs); s[i][1] = ex2(s[i][1] - mAs);
+    s[i][2] = ex2(s[i][2] - mBs); s[i][3] = ex2(s[i][3] - mBs);
+    lA += s[i][0] + s[i][1];
+    lB += s[i][2] + s[i][3];
+  }
+#pragma unroll
+  for (int i = 0; i < NHT; ++i) {
+    sh[i][0] = ex2(sh[i][0] - mAs); sh[i][1] = ex2(sh[i][1] - mAs);
+    sh[i][2] = ex2(sh[i][2] - mBs); sh[i][3] = ex2(sh[i][3] - mBs);
+    lA += sh[i][0] + sh[i][1];
+    lB += sh[i][2] + sh[i][3];
+  }
+  lA += __shfl_xor_sync(0xffffffffu, lA, 1);
+  lA += __shfl_xor_sync(0xffffffffu, lA, 2);
+  lB += __shfl_xor_sync(0xffffffffu, lB, 1);
+  lB += __shfl_xor_sync(0xffffffffu, lB, 2);
+  lA += nA * ex2(-mAs);
+  lB += nB * ex2(-mBs);
+  const float iA = lA > 0.f ? 1.f / lA : 0.f, iB = lB > 0.f ? 1.f / lB : 0.f;
+  const float DA = sD[ra], DB = sD[ra + 8];
+  if (tq == 0) {
+    if (rsA < dlen)
+      p.stats[(int64_t)(dstart + rsA) * p.H + h] =
+          make_float2(lA > 0.f ? (mAs + log2f(lA)) * LN2 : INFINITY, DA);
+    if (rsB < dlen)
+      p.stats[(int64_t)(dstart + rsB) * p.H + h] =
+          make_float2(lB > 0.f ? (mBs + log2f(lB)) * LN2 : INFINITY, DB);
+  }
+
+  // dP = dO V^T over the same slots; dS = P (dP - D) / scale (P normalised in place)
+  uint32_t da[4][4];
+  load_a(sdO, 16 * warp, lane, da);
+  float dp[NT][4], dph[NHT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) dp[i][0] = dp[i][1] = dp[i][2] = dp[i][3] = 0.f;
+#pragma unroll
+  for (int i = 0; i < NHT; ++i) dph[i][0] = dph[i][1] = dph[i][2] = dph[i][3] = 0.f;
+#pragma unroll
+  for (int kp = 0; kp < NB / 16; ++kp) mm_nt16(sV, 16 * warp + 16 * kp, lane, da, dp[2 * kp], dp[2 * kp + 1]);
+#pragma unroll
+  for (int kp = 0; kp < NH / 16; ++kp) mm_nt16(sVH, 16 * kp, lane, da, dph[2 * kp], dph[2 * kp + 1]);
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    s[i][0] *= iA * (dp[i][0] - DA) * p.inv_scale; s[i][1] *= iA * (dp[i][1] - DA) * p.inv_scale;
+    s[i][2] *= iB * (dp[i][2] - DB) * p.inv_scale; s[i][3] *= iB * (dp[i][3] - DB) * p.inv_scale;
+  }
+#pragma unroll
+  for (int i = 0; i < NHT; ++i) {
+    sh[i][0] *= iA * (dph[i][0] - DA) * p.inv_scale; sh[i][1] *= iA * (dph[i][1] - DA) * p.inv_scale;
+    sh[i][2] *= iB * (dph[i][2] - DB) * p.inv_scale; sh[i][3] *= iB * (dph[i][3] - DB) * p.inv_scale;
+  }
+
+  // dQ = dS K
+  float o[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+#pragma unroll
+  for (int kp = 0; kp < NB / 16; ++kp) mm_nn16(sK, 16 * warp + 16 * kp, lane, s[2 * kp], s[2 * kp + 1], o);
+#pragma unroll
+  for (int kp = 0; kp < NH / 16; ++kp) mm_nn16(sKH, 16 * kp, lane, sh[2 * kp], sh[2 * kp + 1], o);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = 8 * i + 2 * tq;
+    if (rsA < dlen)
+      *reinterpret_cast<float2*>(p.dq + (int64_t)(dstart + rsA) * p.ld_grad + hoff + c) = make_float2(o[i][0], o[i][1]);
+    if (rsB < dlen)
+      *reinterpret_cast<float2*>(p.dq + (int64_t)(dstart + rsB) * p.ld_grad + hoff + c) = make_float2(o[i][2], o[i][3]);
+  }
+}
+
+// Kernel B: doc keys [k0, k0+64) of one sequence, one head.  Sources: the band doc rows
+// [k0 - w, k0 + 64 + w) and the head rows (cls / query) attending the doc.
+template <int NB, int NH>
+__global__ void __launch_bounds__(128) band_dkv_kernel(Args p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int KR = 48 + NB;
+  const int tile = blockIdx.x, h = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j = find_seq(p.tile_base, p.nseq, tile);
+  const SeqGroups g = seq_groups(p.cu, p.qlen, j);
+  const int dlen = g.len[2], dstart = g.start + g.off[2];
+  const int k0 = (tile - p.tile_base[j]) * TILE;
+  const int w = p.w, hoff = h * 64;
+  const int nhead = 1 + g.len[1];
+
+  const uint32_t sK = smem_u32(smem), sV = sK + TILE * ROWB, sQ = sV + TILE * ROWB, sdO = sQ + KR * ROWB,
+                 sQH = sdO + KR * ROWB, sdOH = sQH + NH * ROWB;
+  float2* sSt = reinterpret_cast<float2*>(smem + (2 * TILE + 2 * KR + 2 * NH) * ROWB);  // [KR + NH]
+
+  stage_rows(sK, TILE, p.q, [&](int r) {
+    return k0 + r < dlen ? p.k + (int64_t)(dstart + k0 + r) * p.ld + hoff : nullptr; });
+  stage_rows(sV, TILE, p.q, [&](int r) {
+    return k0 + r < dlen ? p.v + (int64_t)(dstart + k0 + r) * p.ld + hoff : nullptr; });
+  stage_rows(sQ, KR, p.q, [&](int r) {
+    const int pos = k0 - w + r;
+    return pos >= 0 && pos < dlen ? p.q + (int64_t)(dstart + pos) * p.ld + hoff : nullptr; });
+  stage_rows(sdO, KR, p.q, [&](int r) {
+    const int pos = k0 - w + r;
+    return pos >= 0 && pos < dlen ? p.dout + (int64_t)(dstart + pos) * p.ld_dout + hoff : nullptr; });
+  stage_rows(sQH, NH, p.q, [&](int r) { return r < nhead ? p.q + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
+  stage_rows(sdOH, NH, p.q, [&](int r) {
+    return r < nhead ? p.dout + (int64_t)(g.start + r) * p.ld_dout + hoff : nullptr; });
+  for (int r = threadIdx.x; r < KR + NH; r += blockDim.x) {
+    float2 st = make_float2(INFINITY, 0.f);
+    if (r < KR) {
+      const int pos = k0 - w + r;
+      if (pos >= 0 && pos < dlen) st = p.stats[(int64_t)(dstart + pos) * p.H + h];
+    } else if (r - KR < nhead) {
+      st = p.stats[(int64_t)(g.start + r - KR) * p.H + h];
+    }
+    st.x *= LOG2E;  // lse in log2 units
+    sSt[r] = st;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  const int gq = lane >> 2, tq = lane & 3;
+  const int kA = k0 + 16 * warp + gq, kB = kA + 8;  // doc-relative keys of this thread
+  const float c2 = p.inv_scale * LOG2E;
+  constexpr int NT = NB / 8, NHT = NH / 8;
+
+  uint32_t ka[4][4];
+  load_a(sK, 16 * warp, lane, ka);
+  float s[NT][4], sh[NHT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+#pragma unroll
+  for (int i = 0; i < NHT; ++i) sh[i][0] = sh[i][1] = sh[i][2] = sh[i][3] = 0.f;
+#pragma unroll
+  for (int kp = 0; kp < NB / 16; ++kp) mm_nt16(sQ, 16 * warp + 16 * kp, lane, ka, s[2 * kp], s[2 * kp + 1]);
+#pragma unroll
+  for (int kp = 0; kp < NH / 16; ++kp) mm_nt16(sQH, 16 * kp, lane, ka, sh[2 * kp], sh[2 * kp + 1]);
+
+  // source cb of this warp = doc row k0 + 16*warp - w + cb (smem row 16*warp + cb)
+  const int spos0 = k0 + 16 * warp - w;
+  const int L02 = p.links.w[0][2], L12 = p.links.w[1][2];
+  // P^T = exp(S^T / scale - lse_src) on valid slots
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int key = e < 2 ? kA : kB, cb = 8 * i + 2 * tq + (e & 1), sp = spos0 + cb;
+      const bool ok = key < dlen && sp >= 0 && sp < dlen && abs(sp - key) <= w;
+      s[i][e] = ok ? ex2(s[i][e] * c2 - sSt[16 * warp + cb].x) : 0.f;
+    }
+#pragma unroll
+  for (int i = 0; i < NHT; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int key = e < 2 ? kA : kB, sl = 8 * i + 2 * tq + (e & 1);
+      const bool ok = key < dlen && sl < nhead && (sl == 0 ? linked(L02, 0, key) : linked(L12, sl - 1, key));
+      sh[i][e] = ok ? ex2(sh[i][e] * c2 - sSt[KR + sl].x) : 0.f;
+    }
+
+  // dV = P^T dO
+  float dv[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dv[i][0] = dv[i][1] = dv[i][2] = dv[i][3] = 0.f;
+#pragma unroll
+  for (int kp = 0; kp < NB / 16; ++kp) mm_nn16(sdO, 16 * warp + 16 * kp, lane, s[2 * kp], s[2 * kp + 1], dv);
+#pragma unroll
+  for (int kp = 0; kp < NH / 16; ++kp) mm_nn16(sdOH, 16 * kp, lane, sh[2 * kp], sh[2 * kp + 1], dv);
+
+  // dP^T = V dO^T; dS^T = P^T (dP^T - D_src) / scale
+  uint32_t va[4][4];
+  load_a(sV, 16 * warp, lane, va);
+  float dp[NT][4], dph[NHT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) dp[i][0] = dp[i][1] = dp[i][2] = dp[i][3] = 0.f;
+#pragma unroll
+  for (int i = 0; i < NHT; ++i) dph[i][0] = dph[i][1] = dph[i][2] = dph[i][3] = 0.f;
+#pragma unroll
+  for (int kp = 0; kp < NB / 16; ++kp) mm_nt16(sdO, 16 * warp + 16 * kp, lane, va, dp[2 * kp], dp[2 * kp + 1]);
+#pragma unroll
+  for (int kp = 0; kp < NH / 16; ++kp) mm_nt16(sdOH, 16 * kp, lane, va, dph[2 * kp], dph[2 * kp + 1]);
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int cb = 8 * i + 2 * tq + (e & 1);
+      s[i][e] *= (dp[i][e] - sSt[16 * warp + cb].y) * p.inv_scale;
+    }
+#pragma unroll
+  for (int i = 0; i < NHT; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int sl = 8 * i + 2 * tq + (e & 1);
+      sh[i][e] *= (dph[i][e] - sSt[KR + sl].y) * p.inv_scale;
+    }
+
+  // dK = dS^T Q
+  float dk[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dk[i][0] = dk[i][1] = dk[i][2] = dk[i][3] = 0.f;
+#pragma unroll
+  for (int kp = 0; kp < NB / 16; ++kp) mm_nn16(sQ, 16 * warp + 16 * kp, lane, s[2 * kp], s[2 * kp + 1], dk);
+#pragma unroll
+  for (int kp = 0; kp < NH / 16; ++kp) mm_nn16(sQH, 16 * kp, lane, sh[2 * kp], sh[2 * kp + 1], dk);
+
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = 8 * i + 2 * tq;
+    if (kA < dlen) {
+      const int64_t off = (int64_t)(dstart + kA) * p.ld_grad + hoff + c;
+      *reinterpret_cast<float2*>(p.dk + off) = make_float2(dk[i][0], dk[i][1]);
+      *reinterpret_cast<float2*>(p.dv + off) = make_float2(dv[i][0], dv[i][1]);
+    }
+    if (kB < dlen) {
+      const int64_t off = (int64_t)(dstart + kB) * p.ld_grad + hoff + c;
+      *reinterpret_cast<float2*>(p.dk + off) = make_float2(dk[i][2], dk[i][3]);
+      *reinterpret_cast<float2*>(p.dv + off) = make_float2(dv[i][2], dv[i][3]);
+    }
+  }
+}
+
+template <int NB, int NH>
+size_t smem_bytes() {
+  return (size_t)(2 * TILE + 2 * (48 + NB) + 2 * NH) * ROWB + (48 + NB + NH) * sizeof(float2);
+}
+
+template <int NB, int NH>
+int launch_pair(const Args& a, int ntiles, int phase, cudaStream_t st) {
+  const size_t sm = smem_bytes<NB, NH>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(band_dq_kernel<NB, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(band_dkv_kernel<NB, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  dim3 grid(ntiles, a.H);
+  if (phase == 0) {
+    band_dq_kernel<NB, NH><<<grid, 128, sm, st>>>(a);
+    SC_CHECK_LAUNCH("band_dq_kernel");
+  } else {
+    band_dkv_kernel<NB, NH><<<grid, 128, sm, st>>>(a);
+    SC_CHECK_LAUNCH("band_dkv_kernel");
+  }
+  return SC_OK;
+}
+
+}  // namespace bwdband
+
+// Doc-band phase of the fast path: phase 0 = kernel A (doc-row stats + dQ), 1 = kernel B (doc dK/dV).
+int launch_attn_bwd_band(const BandBwdArgs& a, int ntiles, int max_head, int phase, cudaStream_t st) {
+  using namespace bwdband;
+  const bool wide = a.w > 8;
+  if (max_head <= 16) return wide ? launch_pair<64, 16>(a, ntiles, phase, st) : launch_pair<32, 16>(a, ntiles, phase, st);
+  return wide ? launch_pair<64, 32>(a, ntiles, phase, st) : launch_pair<32, 32>(a, ntiles, phase, st);
+}
+
+}  // namespace sc

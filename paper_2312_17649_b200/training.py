@@ -114,7 +114,8 @@ def attention_backward(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor,
         pattern.links().ctypes.data, _lib.PAD_EXCLUDE if padding == "exclude" else _lib.PAD_ZERO_LOGIT,
         float(scale), _lib.DTYPE_BF16 if qkv.dtype == torch.bfloat16 else _lib.DTYPE_F32,
         _lib.ptr(layout.tok_flags) if qds else None, _lib.ptr(layout.glob_cu) if qds else None,
-        _lib.ptr(layout.glob_pos) if qds else None, ws.data_ptr(), ws_bytes, _lib.stream_handle(),
+        _lib.ptr(layout.glob_pos) if qds else None, layout.seq_tile_base.data_ptr(), layout.tile_rows,
+        layout.max_qgroup_len, ws.data_ptr(), ws_bytes, _lib.stream_handle(),
         exc=AttentionError,
     )
 

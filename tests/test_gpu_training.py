@@ -317,3 +317,39 @@ def test_trained_weights_serve_through_inference_engine(P):
     a = res.model.score(seq.ids[None], seq.partition)
     b = eng.score(seq.ids[None], seq.partition)
     np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("pattern,window,padding", [
+    ("sparse", 4, "exclude"), ("sparse", 8, "zero-logit"), ("longformer", 16, "exclude"),
+    ("sparse", 24, "exclude"), ("longformer", 2, "zero-logit"), ("sparse", 0, "exclude"),
+])
+def test_attention_backward_bf16_tiled_path_vs_fp32(P, pattern, window, padding):
+    """bf16 d=64 batches take the tiled tensor-core doc-band kernels; compare with the fp32
+    generic adjoint on the same (bf16-rounded) inputs, ragged docs incl. 1-token and 64-multiples."""
+    from paper_2312_17649_b200.training import attention_backward
+
+    rng = np.random.default_rng(5)
+    m = rng.integers(1, 30, size=9)
+    n = np.concatenate([rng.integers(1, 300, size=6), [1, 63, 128]])
+    seq = m + n + 3
+    H, d = 3, 64
+    lay = P.PackedLayout.from_lengths(seq, m + 1, device="cuda")
+    pat = P.make_pattern(pattern, window)
+    T = int(seq.sum())
+    gen = torch.Generator("cuda").manual_seed(11)
+    qkv = torch.randn(T, 3 * H * d, device="cuda", generator=gen).bfloat16()
+    dout = torch.randn(T, H * d, device="cuda", generator=gen).bfloat16()
+    out16 = P.attend_packed(qkv[:, :H * d], qkv[:, H * d:2 * H * d], qkv[:, 2 * H * d:], lay, pat, H,
+                            padding=padding)
+    g16 = torch.empty(T, 3 * H * d, device="cuda")
+    attention_backward(qkv, out16, dout, g16, lay, pat, H, 8.0, padding)
+    q32 = qkv.float()
+    out32 = P.attend_packed(q32[:, :H * d], q32[:, H * d:2 * H * d], q32[:, 2 * H * d:], lay, pat, H,
+                            padding=padding, algo="generic")
+    g32 = torch.empty_like(g16)
+    attention_backward(q32, out32, dout.float(), g32, lay, pat, H, 8.0, padding)
+    assert torch.isfinite(g16).all()
+    for c in range(3):
+        a, b = g16[:, c * H * d:(c + 1) * H * d], g32[:, c * H * d:(c + 1) * H * d]
+        err = float((a - b).abs().max())
+        assert err <= 3e-2 * max(1.0, float(b.abs().max())), (c, err)
