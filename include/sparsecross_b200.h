@@ -250,6 +250,16 @@ SC_API int sc_gemm_residual_layernorm(const void* a, int64_t lda, const void* w,
                                void* out, int64_t ldo, float* out_f32, int64_t ldf,
                                int32_t* nonfinite_count, int32_t M, int32_t N, int32_t K, void* stream);
 
+/* ---- Fine-tuning --------------------------------------- */
+
+/* One fused AdamW step over a flat fp32 buffer of n parameters (R/training.py:
+ * 114-137): m = b1 m + (1-b1) g, v = b2 v + (1-b2) g^2,
+ * w -= lr * ((m/bc1) / (sqrt(v/bc2) + eps) + weight_decay * w) with
+ * bc = 1 - beta^step; fp64 arithmetic, fp32 storage.  lr is the scheduled rate
+ * of this step.  All buffers 16-byte aligned. */
+SC_API int sc_adamw_step(float* w, const float* g, float* m, float* v, int64_t n, double lr, double beta1,
+                  double beta2, double eps, double weight_decay, int64_t step, void* stream);
+
 /* In-place exact-erf GELU with optional bias (R/encoder.py:258-259). */
 SC_API int sc_bias_gelu(void* x, const float* bias, int32_t dtype, int64_t rows, int32_t cols,
                  void* stream);

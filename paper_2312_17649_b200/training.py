@@ -124,6 +124,16 @@ def attention_backward(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor,
 # Trainable encoder.
 # ---------------------------------------------------------------------------
 
+class ParamDict(dict):
+    """Reference-named parameters that are views of one flat fp32 device buffer (``flat``),
+    so the optimizer updates every tensor with one fused kernel (sc_adamw_step)."""
+
+    def __init__(self, items, flat: torch.Tensor, order):
+        super().__init__(items)
+        self.flat = flat
+        self.order = list(order)
+
+
 class TrainableCrossEncoder:
     """Reference-named fp32 device parameters with a differentiable packed forward.
 
@@ -137,10 +147,16 @@ class TrainableCrossEncoder:
         self.config = config
         self.device = torch.device(device)
         host = init_weights(config, seed) if weights is None else weights
-        self.weights = {
-            name: torch.tensor(np.asarray(a, dtype=np.float32), device=self.device).requires_grad_(True)
-            for name, a in host.items()
-        }
+        order = sorted(host)
+        arrs = [np.asarray(host[n], dtype=np.float32) for n in order]
+        flat = torch.empty(sum(a.size for a in arrs), dtype=torch.float32, device=self.device)
+        views, off = {}, 0
+        for n, a in zip(order, arrs):
+            v = flat[off:off + a.size].view(a.shape)
+            v.copy_(torch.from_numpy(a.copy()))
+            views[n] = v.requires_grad_(True)
+            off += a.size
+        self.weights = ParamDict(views, flat, order)
         self.pattern = make_pattern(config.pattern, config.window)
 
     @property
@@ -304,13 +320,15 @@ class AdamW:
     """Adam moments, bias correction, decoupled decay, linear warmup / decay.
 
     ``step(weights, grads)`` applies, for every name in sorted order,
-    ``w -= lr_t * ((m/bc1) / (sqrt(v/bc2) + eps) + weight_decay * w)`` with
-    the moments kept in ``moment_dtype`` (float64 like the reference by
-    default).
+    ``w -= lr_t * ((m/bc1) / (sqrt(v/bc2) + eps) + weight_decay * w)``.
+    Device parameters from ``TrainableCrossEncoder`` (a ``ParamDict`` over one
+    flat buffer) take one fused kernel per step (``sc_adamw_step``: fp64
+    arithmetic, fp32 moments).  ``moment_dtype=torch.float64`` keeps the
+    reference's float64 moments exactly (per-tensor torch ops).
     """
 
     def __init__(self, lr: float, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.01,
-                 warmup_steps: int = 0, total_steps: int | None = None, moment_dtype=torch.float64):
+                 warmup_steps: int = 0, total_steps: int | None = None, moment_dtype=torch.float32):
         self.lr = lr
         self.beta1, self.beta2 = betas
         self.eps = eps
@@ -336,6 +354,9 @@ class AdamW:
         self.step_count += 1
         t = self.step_count
         lr_t = self.current_lr()
+        if isinstance(weights, ParamDict) and weights.flat.is_cuda and self.moment_dtype == torch.float32:
+            self._fused_step(weights, grads, lr_t, t)
+            return
         bc1 = 1.0 - self.beta1 ** t
         bc2 = 1.0 - self.beta2 ** t
         for name in sorted(weights):
@@ -351,6 +372,17 @@ class AdamW:
             v.mul_(self.beta2).addcmul_(g, g, value=1.0 - self.beta2)
             update = (m / bc1) / ((v / bc2).sqrt() + self.eps)
             w.sub_((lr_t * (update + self.weight_decay * w.to(self.moment_dtype))).to(w.dtype))
+
+
+    def _fused_step(self, weights: ParamDict, grads: dict, lr_t: float, t: int) -> None:
+        flat = weights.flat
+        g = torch.cat([torch.as_tensor(grads[n], device=flat.device).reshape(-1).float() for n in weights.order])
+        if self._m.get("__flat__") is None:
+            self._m["__flat__"] = torch.zeros_like(flat)
+            self._v["__flat__"] = torch.zeros_like(flat)
+        _lib.call("sc_adamw_step", flat.data_ptr(), g.data_ptr(), self._m["__flat__"].data_ptr(),
+                  self._v["__flat__"].data_ptr(), flat.numel(), float(lr_t), float(self.beta1), float(self.beta2),
+                  float(self.eps), float(self.weight_decay), int(t), _lib.stream_handle(), exc=TrainingError)
 
 
 # ---------------------------------------------------------------------------

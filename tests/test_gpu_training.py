@@ -353,3 +353,26 @@ def test_attention_backward_bf16_tiled_path_vs_fp32(P, pattern, window, padding)
         a, b = g16[:, c * H * d:(c + 1) * H * d], g32[:, c * H * d:(c + 1) * H * d]
         err = float((a - b).abs().max())
         assert err <= 3e-2 * max(1.0, float(b.abs().max())), (c, err)
+
+
+def test_fused_adamw_matches_float64_reference_path(P):
+    """sc_adamw_step on a ParamDict == the per-tensor float64 path (the reference's update)."""
+    from paper_2312_17649_b200.training import AdamW, ParamDict
+
+    ws, gs = cases.adamw_inputs()
+    order = sorted(ws)
+    flat = torch.cat([torch.tensor(np.asarray(ws[n], np.float32)).reshape(-1) for n in order]).cuda()
+    views, off = {}, 0
+    for n in order:
+        k = int(np.size(ws[n]))
+        views[n] = flat[off:off + k].view(np.shape(ws[n]))
+        off += k
+    pd = ParamDict(views, flat, order)
+    ref = {n: torch.tensor(np.asarray(ws[n], np.float32)).double() for n in order}
+    o1 = AdamW(lr=0.05, weight_decay=0.1, warmup_steps=2, total_steps=6)
+    o2 = AdamW(lr=0.05, weight_decay=0.1, warmup_steps=2, total_steps=6, moment_dtype=torch.float64)
+    for step in range(5):
+        o1.step(pd, {n: torch.tensor(np.asarray(gs[step][n], np.float32)).cuda() for n in order})
+        o2.step(ref, {n: torch.tensor(np.asarray(gs[step][n], np.float32)).double() for n in order})
+    for n in order:
+        np.testing.assert_allclose(pd[n].cpu().numpy(), ref[n].numpy(), rtol=1e-6, atol=1e-7)

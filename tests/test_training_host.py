@@ -63,7 +63,7 @@ class TestAdamW:
     def test_matches_reference_updates(self, G):
         ws, gs = cases.adamw_inputs()
         tw = {n: torch.tensor(a) for n, a in ws.items()}
-        opt = TR.AdamW(lr=0.05, weight_decay=0.1, warmup_steps=2, total_steps=6)
+        opt = TR.AdamW(lr=0.05, weight_decay=0.1, warmup_steps=2, total_steps=6, moment_dtype=torch.float64)
         for step in range(5):
             opt.step(tw, {n: torch.tensor(g) for n, g in gs[step].items()})
         for n in ws:
