@@ -188,9 +188,11 @@ SC_API int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t row_
  * bf16, head_dim 64, no QDS, a finite doc window <= 24, tile_rows 64 and
  * max_qgroup_len <= 31 take the tiled tensor-core path for the doc band
  * (one host read of the tile count); anything else the generic kernels.
- * workspace: sc_attn_bwd_workspace_bytes(T, H) bytes (per-row softmax
- * statistics).  head_dim <= 128. */
-SC_API size_t sc_attn_bwd_workspace_bytes(int32_t total_tokens, int32_t heads);
+ * workspace: sc_attn_bwd_workspace_bytes(T, H, nseq, max_qgroup_len) bytes
+ * (per-row softmax statistics + per-tile head-key partials of the tiled
+ * path; T*H*8 bytes is the minimum).  head_dim <= 128. */
+SC_API size_t sc_attn_bwd_workspace_bytes(int32_t total_tokens, int32_t heads, int32_t nseq,
+                                          int32_t max_qgroup_len);
 SC_API int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t row_stride,
                 const void* out, int64_t out_row_stride, const void* dout, int64_t dout_row_stride,
                 float* dq, float* dk, float* dv, int64_t grad_row_stride,

@@ -62,6 +62,7 @@ struct BwdArgs {
   float2* stats;  // [T*H]: (lse, D); lse = +inf for rows without keys
   int mode;       // 0: every row; 1: only the head rows (cls + query group) of every sequence
   int maxh;       // mode 1: 1 + max qgroup_len (items per sequence)
+  int skip_doc_sources;  // dK/dV kernel: doc-row sources are summed elsewhere (tiled path partials)
 };
 
 // Item -> (row, head).  Mode 1 enumerates nseq x maxh slots, skipping slots past a sequence's head rows.
@@ -112,10 +113,10 @@ __device__ __forceinline__ int key_ranges(const AttnArgs& a, const SeqGroups& g,
 
 // Source ranges whose slots address key (tg, r) of sequence j (the transposed pattern).
 __device__ __forceinline__ int source_ranges(const AttnArgs& a, const SeqGroups& g, int j, int tg, int r,
-                                             bool key_global, Range (&out)[5]) {
+                                             bool key_global, bool skip_doc, Range (&out)[5]) {
   const bool qds = a.glob_cu != nullptr;
   int n = 0;
-  for (int gs = 0; gs < 3; ++gs) {
+  for (int gs = 0; gs < (skip_doc ? 2 : 3); ++gs) {
     const int w = a.links.w[gs][tg];
     const bool qds_doc = qds && gs == 2;
     if (w == SC_LINK_NONE || (qds_doc && tg == 2 && w >= 0 && key_global)) continue;
@@ -423,7 +424,7 @@ __global__ void __launch_bounds__(ItemSlot<NS>::kWarpsPerCta * 32) attn_bwd_dkv_
   for (int e = 0; e < E; ++e) { dk[e] = 0.f; dv[e] = 0.f; }
 
   Range R[5];
-  const int nr = source_ranges(a, g, j, tg, r, key_global, R);
+  const int nr = source_ranges(a, g, j, tg, r, key_global, b.skip_doc_sources != 0, R);
   int unit = 0;
   for (int ri = 0; ri < nr; ++ri) {
     visit(a, R[ri], lane, split, NS, unit,
@@ -503,14 +504,18 @@ __global__ void __launch_bounds__(ItemSlot<NS>::kWarpsPerCta * 32) attn_bwd_dkv_
   }
 }
 
-// Mode 0: one warp per (row, head).  Mode 1 (head rows / keys, long dense ranges): a CTA of
-// kHeadSplit warps per (row, head).
-constexpr int kHeadSplit = 8;
+// Mode 0: one warp per (row, head).  Mode 1 (head rows / keys): a CTA of kHeadSplit warps per
+// (row, head) when sequences are long (dense ranges of thousands of keys), else one warp each.
+constexpr int kHeadSplit = 16;
+constexpr int kSplitMinAvgLen = 768;
 
 template <typename T, int E>
 int launch_generic(const BwdArgs& b, int which, cudaStream_t st) {
-  if (b.mode == 0) {
-    const int64_t items = (int64_t)b.a.T * b.a.H;
+  // (the head keys' dK/dV pass without doc sources only sees the short cls / query ranges)
+  const bool split = b.mode == 1 && (int64_t)b.a.T >= (int64_t)kSplitMinAvgLen * b.a.nseq &&
+                     !(which == 1 && b.skip_doc_sources);
+  if (!split) {
+    const int64_t items = b.mode == 0 ? (int64_t)b.a.T * b.a.H : (int64_t)b.a.nseq * b.maxh * b.a.H;
     const unsigned blocks = (unsigned)((items + kBwdWarps - 1) / kBwdWarps);
     if (which == 0) attn_bwd_dq_kernel<T, E, 1><<<blocks, kBwdWarps * 32, 0, st>>>(b);
     else attn_bwd_dkv_kernel<T, E, 1><<<blocks, kBwdWarps * 32, 0, st>>>(b);
@@ -548,8 +553,21 @@ static bool force_generic() {
   return v;
 }
 
-extern "C" size_t sc_attn_bwd_workspace_bytes(int32_t total_tokens, int32_t heads) {
+static size_t stats_bytes(int32_t total_tokens, int32_t heads) {
   return (size_t)(total_tokens > 0 ? total_tokens : 0) * (size_t)(heads > 0 ? heads : 0) * sizeof(float2);
+}
+
+// Head-key partials of the tiled path: <= T/64 + nseq tiles x H x 2 x NH x 64 fp32.
+static size_t part_bytes(int32_t total_tokens, int32_t heads, int32_t nseq, int32_t max_qgroup_len) {
+  const int nh = 1 + max_qgroup_len <= 16 ? 16 : 32;
+  const size_t tiles = (size_t)(total_tokens / 64 + 1) + (size_t)(nseq > 0 ? nseq : 0);
+  return tiles * (size_t)(heads > 0 ? heads : 0) * 2 * nh * 64 * sizeof(float);
+}
+
+extern "C" size_t sc_attn_bwd_workspace_bytes(int32_t total_tokens, int32_t heads, int32_t nseq,
+                                              int32_t max_qgroup_len) {
+  return ((stats_bytes(total_tokens, heads) + 255) & ~(size_t)255) +
+         part_bytes(total_tokens, heads, nseq, max_qgroup_len);
 }
 
 extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t row_stride, const void* out,
@@ -572,9 +590,9 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
   SC_CHECK_ARG(dtype == SC_DTYPE_F32 || dtype == SC_DTYPE_BF16, "sc_attn_bwd: bad dtype %d", dtype);
   SC_CHECK_ARG((glob_cu == nullptr) == (glob_pos == nullptr) && (glob_cu == nullptr || tok_flags != nullptr),
                "sc_attn_bwd: QDS globals need tok_flags, glob_cu and glob_pos");
-  SC_CHECK_ARG(workspace && workspace_bytes >= sc_attn_bwd_workspace_bytes(total_tokens, heads),
-               "sc_attn_bwd: workspace must hold sc_attn_bwd_workspace_bytes(T, H) bytes");
   SC_CHECK_ARG(max_qgroup_len >= 1, "sc_attn_bwd: max_qgroup_len must be >= 1");
+  SC_CHECK_ARG(workspace && workspace_bytes >= stats_bytes(total_tokens, heads),
+               "sc_attn_bwd: workspace must hold sc_attn_bwd_workspace_bytes(T, H, nseq, max_qgroup_len) bytes");
   a.q = q; a.k = k; a.v = v; a.ld = row_stride; a.out = const_cast<void*>(out); a.ld_out = out_row_stride;
   a.cu = cu_seqlens; a.qlen = qgroup_len; a.nseq = nseq; a.T = total_tokens; a.H = heads; a.d = head_dim;
   a.padding = padding; a.scale = scale; a.flags = tok_flags; a.glob_cu = glob_cu; a.glob_pos = glob_pos;
@@ -604,6 +622,10 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
   p.dq = dq; p.dk = dk; p.dv = dv; p.ld_grad = grad_row_stride; p.stats = b.stats;
   p.cu = cu_seqlens; p.qlen = qgroup_len; p.tile_base = seq_tile_base; p.nseq = nseq; p.H = heads; p.w = wdd;
   p.links = a.links; p.padding = padding; p.inv_scale = 1.f / scale;
+  // head-key partials when the workspace has room (else the generic head-key pass sums doc sources)
+  const size_t soff = (stats_bytes(total_tokens, heads) + 255) & ~(size_t)255;
+  if (workspace_bytes >= soff + part_bytes(total_tokens, heads, nseq, max_qgroup_len))
+    p.head_part = reinterpret_cast<float*>(static_cast<char*>(workspace) + soff);
   int ntiles = 0;
   if (cudaMemcpyAsync(&ntiles, seq_tile_base + nseq, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess) {
@@ -614,6 +636,8 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
   int rc = launch_generic_any(b, dtype, 0, st);               // head rows: stats + dQ
   if (!rc && ntiles) rc = launch_attn_bwd_band(p, ntiles, b.maxh, 0, st);  // doc rows: stats + dQ
   if (!rc && ntiles) rc = launch_attn_bwd_band(p, ntiles, b.maxh, 1, st);  // doc keys: dK, dV
-  if (!rc) rc = launch_generic_any(b, dtype, 1, st);          // head keys: dK, dV
+  b.skip_doc_sources = p.head_part != nullptr && ntiles > 0;
+  if (!rc) rc = launch_generic_any(b, dtype, 1, st);          // head keys: dK, dV (non-doc sources)
+  if (!rc && b.skip_doc_sources) rc = launch_attn_bwd_band(p, ntiles, b.maxh, 2, st);  // + doc sources
   return rc;
 }

@@ -126,8 +126,8 @@ __global__ void __launch_bounds__(128) band_dq_kernel(Args p) {
   const int nhead = 1 + g.len[1];
 
   const uint32_t sQ = smem_u32(smem), sdO = sQ + TILE * ROWB, sK = sdO + TILE * ROWB, sV = sK + KR * ROWB,
-                 sKH = sV + KR * ROWB, sVH = sKH + NH * ROWB;
-  float* sD = reinterpret_cast<float*>(smem + (2 * TILE + 2 * KR + 2 * NH) * ROWB);
+                 sKH = sV + KR * ROWB, sVH = sKH + NH * ROWB, sPT = sVH + NH * ROWB, sST = sPT + NH * ROWB;
+  float* sD = reinterpret_cast<float*>(smem + (2 * TILE + 2 * KR + 4 * NH) * ROWB);
 
   stage_rows(sQ, TILE, p.q, [&](int r) {
     return r0 + r < dlen ? p.q + (int64_t)(dstart + r0 + r) * p.ld + hoff : nullptr; });
@@ -284,10 +284,27 @@ __global__ void __launch_bounds__(128) band_dq_kernel(Args p) {
     s[i][0] *= iA * (dp[i][0] - DA) * p.inv_scale; s[i][1] *= iA * (dp[i][1] - DA) * p.inv_scale;
     s[i][2] *= iB * (dp[i][2] - DB) * p.inv_scale; s[i][3] *= iB * (dp[i][3] - DB) * p.inv_scale;
   }
+  const bool part = p.head_part != nullptr;
+  // head-key columns, transposed into smem ([slot][row], bf16) for the per-tile head dK / dV partials
+  auto st_t = [&](uint32_t buf, int sl, int row, float x) {
+    const __nv_bfloat16 hv = __float2bfloat16_rn(x);
+    asm volatile("st.shared.b16 [%0], %1;" ::"r"(swz(buf, sl, row >> 3) + (row & 7) * 2),
+                 "h"(*reinterpret_cast<const unsigned short*>(&hv)));
+  };
 #pragma unroll
   for (int i = 0; i < NHT; ++i) {
+    if (part) {
+      const int sl = 8 * i + 2 * tq;
+      st_t(sPT, sl, ra, sh[i][0] * iA); st_t(sPT, sl + 1, ra, sh[i][1] * iA);
+      st_t(sPT, sl, ra + 8, sh[i][2] * iB); st_t(sPT, sl + 1, ra + 8, sh[i][3] * iB);
+    }
     sh[i][0] *= iA * (dph[i][0] - DA) * p.inv_scale; sh[i][1] *= iA * (dph[i][1] - DA) * p.inv_scale;
     sh[i][2] *= iB * (dph[i][2] - DB) * p.inv_scale; sh[i][3] *= iB * (dph[i][3] - DB) * p.inv_scale;
+    if (part) {
+      const int sl = 8 * i + 2 * tq;
+      st_t(sST, sl, ra, sh[i][0]); st_t(sST, sl + 1, ra, sh[i][1]);
+      st_t(sST, sl, ra + 8, sh[i][2]); st_t(sST, sl + 1, ra + 8, sh[i][3]);
+    }
   }
 
   // dQ = dS K
@@ -306,6 +323,58 @@ __global__ void __launch_bounds__(128) band_dq_kernel(Args p) {
     if (rsB < dlen)
       *reinterpret_cast<float2*>(p.dq + (int64_t)(dstart + rsB) * p.ld_grad + hoff + c) = make_float2(o[i][2], o[i][3]);
   }
+  if (!part) return;
+
+  // Per-tile head-key partials: dV_h = P_h^T dO, dK_h = dS_h^T Q over this tile's 64 rows.
+  // Jobs (which, n-half, m-tile) spread over the warps; summed per sequence by head_part_reduce.
+  __syncthreads();
+  for (int job = warp; job < 4 * (NH / 16); job += 4) {
+    const int which = job & 1, nh = (job >> 1) & 1, mt = job >> 2;
+    uint32_t a[4][4];
+    load_a(which ? sST : sPT, 16 * mt, lane, a);
+    const uint32_t bbuf = which ? sQ : sdO;
+    float acc[4][4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) acc[x][0] = acc[x][1] = acc[x][2] = acc[x][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+      for (int q2 = 0; q2 < 2; ++q2) {
+        uint32_t b[4];
+        ldsm_x4_t(swz(bbuf, 16 * ks + (lane & 7) + (((lane >> 3) & 1) << 3), (2 * nh + q2) * 2 + (lane >> 4)), b);
+        mma16816(acc[2 * q2], a[ks], b[0], b[1]);
+        mma16816(acc[2 * q2 + 1], a[ks], b[2], b[3]);
+      }
+    }
+    float* dst = p.head_part + (((int64_t)tile * p.H + h) * 2 + which) * NH * 64;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int c = 8 * (4 * nh + x) + 2 * tq, sl = 16 * mt + gq;
+      *reinterpret_cast<float2*>(dst + sl * 64 + c) = make_float2(acc[x][0], acc[x][1]);
+      *reinterpret_cast<float2*>(dst + (sl + 8) * 64 + c) = make_float2(acc[x][2], acc[x][3]);
+    }
+  }
+}
+
+// dK / dV of the head keys (cls / query rows) += the sum over the sequence's doc tiles of the
+// kernel-A partials, in tile order (deterministic).  One thread per (seq, head, which, slot, dim).
+template <int NH>
+__global__ void __launch_bounds__(256) head_part_reduce_kernel(Args p) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int dim = (int)(idx & 63);
+  int64_t r = idx >> 6;
+  const int sl = (int)(r % NH); r /= NH;
+  const int which = (int)(r & 1); r >>= 1;
+  const int h = (int)(r % p.H);
+  const int j = (int)(r / p.H);
+  if (j >= p.nseq) return;
+  const SeqGroups g = seq_groups(p.cu, p.qlen, j);
+  if (sl >= 1 + g.len[1]) return;
+  float acc = 0.f;
+  for (int t = p.tile_base[j]; t < p.tile_base[j + 1]; ++t)
+    acc += p.head_part[(((int64_t)t * p.H + h) * 2 + which) * NH * 64 + sl * 64 + dim];
+  float* dst = (which ? p.dk : p.dv) + (int64_t)(g.start + sl) * p.ld_grad + h * 64 + dim;
+  *dst += acc;
 }
 
 // Kernel B: doc keys [k0, k0+64) of one sequence, one head.  Sources: the band doc rows
@@ -455,7 +524,7 @@ __global__ void __launch_bounds__(128) band_dkv_kernel(Args p) {
 
 template <int NB, int NH>
 size_t smem_bytes() {
-  return (size_t)(2 * TILE + 2 * (48 + NB) + 2 * NH) * ROWB + (48 + NB + NH) * sizeof(float2);
+  return (size_t)(2 * TILE + 2 * (48 + NB) + 4 * NH) * ROWB + (48 + NB + NH) * sizeof(float2);
 }
 
 template <int NB, int NH>
@@ -471,6 +540,10 @@ int launch_pair(const Args& a, int ntiles, int phase, cudaStream_t st) {
   if (phase == 0) {
     band_dq_kernel<NB, NH><<<grid, 128, sm, st>>>(a);
     SC_CHECK_LAUNCH("band_dq_kernel");
+  } else if (phase == 2) {
+    const int64_t n = (int64_t)a.nseq * a.H * 2 * NH * 64;
+    head_part_reduce_kernel<NH><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a);
+    SC_CHECK_LAUNCH("head_part_reduce_kernel");
   } else {
     band_dkv_kernel<NB, NH><<<grid, 128, sm, st>>>(a);
     SC_CHECK_LAUNCH("band_dkv_kernel");
@@ -480,7 +553,8 @@ int launch_pair(const Args& a, int ntiles, int phase, cudaStream_t st) {
 
 }  // namespace bwdband
 
-// Doc-band phase of the fast path: phase 0 = kernel A (doc-row stats + dQ), 1 = kernel B (doc dK/dV).
+// Doc-band phases of the fast path: 0 = kernel A (doc-row stats + dQ [+ head-key partials]),
+// 1 = kernel B (doc dK/dV), 2 = add the summed head-key partials into the head keys' dK/dV.
 int launch_attn_bwd_band(const BandBwdArgs& a, int ntiles, int max_head, int phase, cudaStream_t st) {
   using namespace bwdband;
   const bool wide = a.w > 8;

@@ -104,7 +104,7 @@ def attention_backward(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor,
     es = qkv.element_size()
     qds = pattern.name == "qds" and layout.tok_flags is not None
     base, gbase = qkv.data_ptr(), grad.data_ptr()
-    ws_bytes = _lib.load().sc_attn_bwd_workspace_bytes(T, heads)
+    ws_bytes = _lib.load().sc_attn_bwd_workspace_bytes(T, heads, layout.nseq, layout.max_qgroup_len)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=qkv.device)
     _lib.call(
         "sc_attn_bwd",
