@@ -262,6 +262,30 @@ SC_API int sc_gemm_residual_layernorm(const void* a, int64_t lda, const void* w,
 SC_API int sc_adamw_step(float* w, const float* g, float* m, float* v, int64_t n, double lr, double beta1,
                   double beta2, double eps, double weight_decay, int64_t step, void* stream);
 
+/* y = LN(a + b) (b may be NULL) with gamma/beta, eps, fp32 y and per-row
+ * mean / rstd for sc_layernorm_bwd (R/encoder.py:267-273).  a, b: [rows x
+ * cols] contiguous, fp32 or bf16.  cols % 4 == 0, cols <= 1024, 8-byte
+ * aligned rows (else SC_ERR_UNSUPPORTED). */
+SC_API int sc_layernorm_fwd(const void* a, int32_t a_dtype, const void* b, int32_t b_dtype, const float* gamma,
+                     const float* beta, float* y, float* mean, float* rstd, int32_t rows, int32_t cols,
+                     float eps, void* stream);
+
+/* Adjoint of sc_layernorm_fwd (R/encoder.py:276-285): dx (fp32, the gradient
+ * of both a and b) and dgamma / dbeta (fp32 [cols], written).  partials:
+ * 2 * sc_ln_partials(rows) * cols floats of scratch.  Deterministic. */
+SC_API int sc_layernorm_bwd(const float* dy, const void* a, int32_t a_dtype, const void* b, int32_t b_dtype,
+                     const float* gamma, const float* mean, const float* rstd, float* dx, float* dgamma,
+                     float* dbeta, float* partials, int32_t rows, int32_t cols, void* stream);
+
+/* out[c] = sum_r x[r, c] (fp32 out; x fp32 or bf16 with row stride ld): the
+ * bias gradients of layer_backward (R/encoder.py:403-441).  partials:
+ * sc_ln_partials(rows) * cols floats of scratch.  Deterministic. */
+SC_API int sc_colsum(const void* x, int32_t dtype, int64_t ld, int32_t rows, int32_t cols, float* out,
+              float* partials, void* stream);
+
+/* Number of per-CTA partial rows the two reductions above use for `rows`. */
+SC_API int sc_ln_partials(int32_t rows);
+
 /* In-place exact-erf GELU with optional bias (R/encoder.py:258-259). */
 SC_API int sc_bias_gelu(void* x, const float* bias, int32_t dtype, int64_t rows, int32_t cols,
                  void* stream);

@@ -70,6 +70,10 @@ SIGNATURES = {
                                              _i32, _i32, _i32, _p]),
     "sc_adamw_step": (C.c_int, [_p, _p, _p, _p, _i64, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                 _i64, _p]),
+    "sc_layernorm_fwd": (C.c_int, [_p, _i32, _p, _i32, _p, _p, _p, _p, _p, _i32, _i32, _f32, _p]),
+    "sc_layernorm_bwd": (C.c_int, [_p, _p, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _i32, _i32, _p]),
+    "sc_colsum": (C.c_int, [_p, _i32, _i64, _i32, _i32, _p, _p, _p]),
+    "sc_ln_partials": (C.c_int, [_i32]),
     "sc_cls_score": (C.c_int, [_p, _p, _i32, _i32, _p, _f32, _p, _p]),
     "sc_count_nonfinite": (C.c_int, [_p, _i64, _p, _p]),
 }
@@ -77,7 +81,7 @@ SIGNATURES = {
 # Entry points that launch device work (counted for the bench's gpu_launches).
 LAUNCHING = {n for n in SIGNATURES
              if n not in ("sc_last_error", "sc_version", "sc_kernel_launches", "sc_attn_workspace_bytes",
-                          "sc_attn_workspace_bytes_qds", "sc_attn_bwd_workspace_bytes")}
+                          "sc_attn_workspace_bytes_qds", "sc_attn_bwd_workspace_bytes", "sc_ln_partials")}
 
 
 def kernel_launches() -> int:

@@ -1,0 +1,317 @@
+// Dense-layer kernels of the fine-tuning step, replacing the
+// reference's layer_norm / layer_norm_backward (R/encoder.py:267-285) and the
+// bias sums of layer_backward (R/encoder.py:398-443):
+//   * ln_fwd_kernel:  y = LN(a + b) with per-row mean / rstd kept for the
+//     backward (residual add fused; a, b fp32 or bf16);
+//   * ln_bwd_kernel:  dx = rstd (g dy - mean(g dy) - xhat mean(g dy xhat)),
+//     recomputing xhat from a + b, plus per-CTA partial column sums of
+//     dy * xhat and dy (dgamma, dbeta);
+//   * colsum_kernel:  per-CTA partial column sums of a [rows x cols] matrix
+//     (bias gradients);
+//   * colsum_reduce_kernel: the partials summed in CTA order.
+// Warp per row, lane holds columns lane + 32e; every reduction has a fixed
+// order, so the gradients are bit-reproducible.
+#include "common.cuh"
+
+namespace sc {
+
+constexpr int kLnMaxV = 32;  // columns per lane -> cols <= 1024
+constexpr int kLnWarps = 8;
+
+// 4 consecutive columns as float4 (fp32 rows: 16-byte loads; bf16 rows: 8-byte loads).
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ld4(const __nv_bfloat16* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+
+// Lane owns column groups q = lane + 32k (k < KV), columns 4q .. 4q+3; cols % 4 == 0.
+template <typename TA, typename TB, int KV>
+__global__ void __launch_bounds__(kLnWarps * 32, 4) ln_fwd_kernel(const TA* __restrict__ a, const TB* __restrict__ b,
+                                                                  const float* __restrict__ gamma,
+                                                                  const float* __restrict__ beta,
+                                                                  float* __restrict__ y, float* __restrict__ mean,
+                                                                  float* __restrict__ rstd, int rows, int cols,
+                                                                  float eps) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * kLnWarps + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int64_t base = (int64_t)row * cols;
+  const int ng = cols >> 2;
+  float4 x[KV];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    const int q = lane + 32 * k;
+    x[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (q < ng) {
+      x[k] = ld4(a + base + 4 * q);
+      if (b) x[k] = add4(x[k], ld4(b + base + 4 * q));
+    }
+    s += (x[k].x + x[k].y) + (x[k].z + x[k].w);
+  }
+  const float mu = warp_sum(s) / cols;
+  float v = 0.f;
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    if (lane + 32 * k < ng) {
+      const float d0 = x[k].x - mu, d1 = x[k].y - mu, d2 = x[k].z - mu, d3 = x[k].w - mu;
+      v = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, v))));
+    }
+  }
+  const float rs = rsqrtf(warp_sum(v) / cols + eps);
+#pragma unroll
+  for (int k = 0; k < KV; ++k) {
+    const int q = lane + 32 * k;
+    if (q < ng) {
+      const float4 g = ld4(gamma + 4 * q), bb = ld4(beta + 4 * q);
+      *reinterpret_cast<float4*>(y + base + 4 * q) =
+          make_float4((x[k].x - mu) * rs * g.x + bb.x, (x[k].y - mu) * rs * g.y + bb.y,
+                      (x[k].z - mu) * rs * g.z + bb.z, (x[k].w - mu) * rs * g.w + bb.w);
+    }
+  }
+  if (lane == 0) { mean[row] = mu; rstd[row] = rs; }
+}
+
+// Grid: a fixed number of CTAs; warp w of CTA k handles rows (k * kLnWarps + w) + i * stride.
+// dgamma / dbeta accumulate in the warp's own shared-memory row (no atomics), then the CTA sums
+// its warps in order into one partial row.
+template <typename TA, typename TB, int KV>
+__global__ void __launch_bounds__(kLnWarps * 32, 2) ln_bwd_kernel(const float* __restrict__ dy,
+                                                                  const TA* __restrict__ a, const TB* __restrict__ b,
+                                                                  const float* __restrict__ gamma,
+                                                                  const float* __restrict__ mean,
+                                                                  const float* __restrict__ rstd,
+                                                                  float* __restrict__ dx, float* __restrict__ part_g,
+                                                                  float* __restrict__ part_b, int rows, int cols) {
+  extern __shared__ float4 lnsm[];  // [2][kLnWarps][ng] float4
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ng = cols >> 2;
+  float4* accg = lnsm + warp * ng;
+  float4* accb = lnsm + (kLnWarps + warp) * ng;
+  for (int q = lane; q < ng; q += 32) accg[q] = accb[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float inv_cols = 1.f / cols;
+  const int stride = gridDim.x * kLnWarps;
+  for (int row = blockIdx.x * kLnWarps + warp; row < rows; row += stride) {
+    const int64_t base = (int64_t)row * cols;
+    const float mu = mean[row], rs = rstd[row];
+    float4 xh[KV], gd[KV];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      const int q = lane + 32 * k;
+      xh[k] = gd[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (q < ng) {
+        float4 xv = ld4(a + base + 4 * q);
+        if (b) xv = add4(xv, ld4(b + base + 4 * q));
+        const float4 d = ld4(dy + base + 4 * q), g = ld4(gamma + 4 * q);
+        xh[k] = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
+        gd[k] = make_float4(d.x * g.x, d.y * g.y, d.z * g.z, d.w * g.w);
+        float4 ag = accg[q], ab = accb[q];
+        ag.x = fmaf(d.x, xh[k].x, ag.x); ag.y = fmaf(d.y, xh[k].y, ag.y);
+        ag.z = fmaf(d.z, xh[k].z, ag.z); ag.w = fmaf(d.w, xh[k].w, ag.w);
+        accg[q] = ag;
+        accb[q] = add4(ab, d);
+        s1 += (gd[k].x + gd[k].y) + (gd[k].z + gd[k].w);
+        s2 = fmaf(gd[k].x, xh[k].x, fmaf(gd[k].y, xh[k].y, fmaf(gd[k].z, xh[k].z, fmaf(gd[k].w, xh[k].w, s2))));
+      }
+    }
+    const float m1 = warp_sum(s1) * inv_cols, m2 = warp_sum(s2) * inv_cols;
+#pragma unroll
+    for (int k = 0; k < KV; ++k) {
+      const int q = lane + 32 * k;
+      if (q < ng)
+        *reinterpret_cast<float4*>(dx + base + 4 * q) =
+            make_float4(rs * (gd[k].x - m1 - xh[k].x * m2), rs * (gd[k].y - m1 - xh[k].y * m2),
+                        rs * (gd[k].z - m1 - xh[k].z * m2), rs * (gd[k].w - m1 - xh[k].w * m2));
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < ng; q += blockDim.x) {
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f), bb = g;
+    for (int w = 0; w < kLnWarps; ++w) {
+      g = add4(g, lnsm[w * ng + q]);
+      bb = add4(bb, lnsm[(kLnWarps + w) * ng + q]);
+    }
+    *reinterpret_cast<float4*>(part_g + (int64_t)blockIdx.x * cols + 4 * q) = g;
+    *reinterpret_cast<float4*>(part_b + (int64_t)blockIdx.x * cols + 4 * q) = bb;
+  }
+}
+
+// CTA k sums rows [k * rpc, (k+1) * rpc) of x, 8 columns per thread with 16-byte loads when possible.
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, int64_t ld, int rows, int cols, int rpc,
+                                                     float* __restrict__ part) {
+  const int r0 = blockIdx.x * rpc, r1 = min(rows, r0 + rpc);
+  for (int c0 = threadIdx.x * 8; c0 < cols; c0 += blockDim.x * 8) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const bool vec = c0 + 8 <= cols && ((ld * sizeof(T)) % 16 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(x) + c0 * sizeof(T)) % 16 == 0);
+    for (int r = r0; r < r1; ++r) {
+      const T* p = x + (int64_t)r * ld + c0;
+      if (vec) {
+        if constexpr (sizeof(T) == 2) {
+          const uint4 u = *reinterpret_cast<const uint4*>(p);
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h[e]);
+            acc[2 * e] += f.x;
+            acc[2 * e + 1] += f.y;
+          }
+        } else {
+          const float4 u0 = *reinterpret_cast<const float4*>(p), u1 = *reinterpret_cast<const float4*>(p + 4);
+          acc[0] += u0.x; acc[1] += u0.y; acc[2] += u0.z; acc[3] += u0.w;
+          acc[4] += u1.x; acc[5] += u1.y; acc[6] += u1.z; acc[7] += u1.w;
+        }
+      } else {
+        for (int e = 0; e < 8 && c0 + e < cols; ++e) acc[e] += to_f32(p[e]);
+      }
+    }
+    for (int e = 0; e < 8 && c0 + e < cols; ++e) part[(int64_t)blockIdx.x * cols + c0 + e] = acc[e];
+  }
+}
+
+// out[c] = sum over partial rows k of part[k][c], in k order: block = 32 columns x 8 warps, warp w
+// sums rows k = w (mod 8), the 8 warp sums are added in warp order.
+__global__ void __launch_bounds__(256) colsum_reduce_kernel(const float* __restrict__ part, int nparts, int cols,
+                                                            float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  float acc = 0.f;
+  if (c < cols)
+    for (int k = warp; k < nparts; k += 8) acc += part[(int64_t)k * cols + c];
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && c < cols) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    out[c] = t;
+  }
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <typename TA, typename TB, int KV>
+void ln_launch(bool fwd, const void* a, const void* b, const float* gamma, const float* beta, const float* dy,
+               float* y, float* mean, float* rstd, float* dx, float* pg, float* pb, int rows, int cols, float eps,
+               unsigned blocks, cudaStream_t st) {
+  if (fwd) {
+    ln_fwd_kernel<TA, TB, KV><<<blocks, kLnWarps * 32, 0, st>>>((const TA*)a, (const TB*)b, gamma, beta, y, mean,
+                                                                 rstd, rows, cols, eps);
+  } else {
+    const size_t sm = (size_t)2 * kLnWarps * cols * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(ln_bwd_kernel<TA, TB, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           2 * kLnWarps * kLnMaxV * 32 * (int)sizeof(float));
+      attr = true;
+    }
+    ln_bwd_kernel<TA, TB, KV><<<blocks, kLnWarps * 32, sm, st>>>(dy, (const TA*)a, (const TB*)b, gamma, mean, rstd,
+                                                                  dx, pg, pb, rows, cols);
+  }
+}
+
+template <int KV>
+void ln_dispatch_types(bool af, bool bf, bool fwd, const void* a, const void* b, const float* gamma,
+                       const float* beta, const float* dy, float* y, float* mean, float* rstd, float* dx, float* pg,
+                       float* pb, int rows, int cols, float eps, unsigned blocks, cudaStream_t st) {
+  using B16 = __nv_bfloat16;
+  if (af && bf) ln_launch<float, float, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st);
+  else if (af) ln_launch<float, B16, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st);
+  else if (bf) ln_launch<B16, float, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st);
+  else ln_launch<B16, B16, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st);
+}
+
+// Column groups (of 4) per lane rounded up to an instantiated width.
+void ln_dispatch(bool af, bool bf, bool fwd, const void* a, const void* b, const float* gamma, const float* beta,
+                 const float* dy, float* y, float* mean, float* rstd, float* dx, float* pg, float* pb, int rows,
+                 int cols, float eps, unsigned blocks, cudaStream_t st) {
+  const int kv = (cols / 4 + 31) / 32;
+#define SC_LN_CASE(W) \
+  if (kv <= W) return ln_dispatch_types<W>(af, bf, fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st);
+  SC_LN_CASE(1) SC_LN_CASE(2) SC_LN_CASE(4) SC_LN_CASE(6) SC_LN_CASE(8)
+#undef SC_LN_CASE
+}
+
+}  // namespace sc
+
+using namespace sc;
+
+extern "C" int sc_ln_partials(int32_t rows) {
+  const int cap = num_sms() * 2;
+  return rows < cap ? (rows > 0 ? rows : 1) : cap;
+}
+
+extern "C" int sc_layernorm_fwd(const void* a, int32_t a_dtype, const void* b, int32_t b_dtype, const float* gamma,
+                                const float* beta, float* y, float* mean, float* rstd, int32_t rows, int32_t cols,
+                                float eps, void* stream) {
+  SC_CHECK_ARG(a && gamma && beta && y && mean && rstd, "sc_layernorm_fwd: null pointer");
+  SC_CHECK_ARG(rows >= 0 && cols >= 1, "sc_layernorm_fwd: bad shape");
+  if (cols > kLnMaxV * 32 || cols % 4 || ((uintptr_t)a | (uintptr_t)b | (uintptr_t)y | (uintptr_t)gamma | (uintptr_t)beta) % 8) {
+    set_error("sc_layernorm_fwd: needs cols %% 4 == 0, cols <= %d and 8-byte aligned rows", kLnMaxV * 32);
+    return SC_ERR_UNSUPPORTED;
+  }
+  SC_CHECK_ARG((a_dtype == SC_DTYPE_F32 || a_dtype == SC_DTYPE_BF16) &&
+               (!b || b_dtype == SC_DTYPE_F32 || b_dtype == SC_DTYPE_BF16), "sc_layernorm_fwd: bad dtype");
+  if (rows == 0) return SC_OK;
+  const unsigned blocks = (unsigned)((rows + kLnWarps - 1) / kLnWarps);
+  ln_dispatch(a_dtype == SC_DTYPE_F32, !b || b_dtype == SC_DTYPE_F32, true, a, b, gamma, beta, nullptr, y, mean, rstd,
+              nullptr, nullptr, nullptr, rows, cols, eps, blocks, (cudaStream_t)stream);
+  SC_CHECK_LAUNCH("ln_fwd_kernel");
+  return SC_OK;
+}
+
+extern "C" int sc_layernorm_bwd(const float* dy, const void* a, int32_t a_dtype, const void* b, int32_t b_dtype,
+                                const float* gamma, const float* mean, const float* rstd, float* dx, float* dgamma,
+                                float* dbeta, float* partials, int32_t rows, int32_t cols, void* stream) {
+  SC_CHECK_ARG(dy && a && gamma && mean && rstd && dx && dgamma && dbeta && partials, "sc_layernorm_bwd: null pointer");
+  SC_CHECK_ARG(rows >= 0 && cols >= 1, "sc_layernorm_bwd: bad shape");
+  if (cols > kLnMaxV * 32 || cols % 4 || ((uintptr_t)a | (uintptr_t)b | (uintptr_t)dy | (uintptr_t)dx | (uintptr_t)gamma) % 8) {
+    set_error("sc_layernorm_bwd: needs cols %% 4 == 0, cols <= %d and 8-byte aligned rows", kLnMaxV * 32);
+    return SC_ERR_UNSUPPORTED;
+  }
+  SC_CHECK_ARG((a_dtype == SC_DTYPE_F32 || a_dtype == SC_DTYPE_BF16) &&
+               (!b || b_dtype == SC_DTYPE_F32 || b_dtype == SC_DTYPE_BF16), "sc_layernorm_bwd: bad dtype");
+  const int nparts = sc_ln_partials(rows);
+  cudaStream_t st = (cudaStream_t)stream;
+  float* pg = partials;
+  float* pb = partials + (int64_t)nparts * cols;
+  if (rows > 0)
+    ln_dispatch(a_dtype == SC_DTYPE_F32, !b || b_dtype == SC_DTYPE_F32, false, a, b, gamma, nullptr, dy, nullptr,
+                (float*)mean, (float*)rstd, dx, pg, pb, rows, cols, 0.f, (unsigned)nparts, st);
+  SC_CHECK_LAUNCH("ln_bwd_kernel");
+  colsum_reduce_kernel<<<(cols + 31) / 32, 256, 0, st>>>(pg, nparts, cols, dgamma);
+  SC_CHECK_LAUNCH("colsum_reduce_kernel");
+  colsum_reduce_kernel<<<(cols + 31) / 32, 256, 0, st>>>(pb, nparts, cols, dbeta);
+  SC_CHECK_LAUNCH("colsum_reduce_kernel");
+  return SC_OK;
+}
+
+extern "C" int sc_colsum(const void* x, int32_t dtype, int64_t ld, int32_t rows, int32_t cols, float* out,
+                         float* partials, void* stream) {
+  SC_CHECK_ARG(x && out && partials, "sc_colsum: null pointer");
+  SC_CHECK_ARG(rows >= 0 && cols >= 1 && ld >= cols, "sc_colsum: bad shape");
+  SC_CHECK_ARG(dtype == SC_DTYPE_F32 || dtype == SC_DTYPE_BF16, "sc_colsum: bad dtype");
+  const int nparts = sc_ln_partials(rows);
+  const int rpc = (rows + nparts - 1) / nparts;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SC_DTYPE_F32) colsum_kernel<float><<<nparts, 256, 0, st>>>((const float*)x, ld, rows, cols, rpc, partials);
+  else colsum_kernel<__nv_bfloat16><<<nparts, 256, 0, st>>>((const __nv_bfloat16*)x, ld, rows, cols, rpc, partials);
+  SC_CHECK_LAUNCH("colsum_kernel");
+  colsum_reduce_kernel<<<(cols + 31) / 32, 256, 0, st>>>(partials, nparts, cols, out);
+  SC_CHECK_LAUNCH("colsum_reduce_kernel");
+  return SC_OK;
+}

@@ -11,10 +11,11 @@ rebuilt on the device:
   backward = ``sc_attn_bwd`` (query-major dQ + key-major dK/dV kernels over
   the transposed pattern: every pattern, window, padding mode and the QDS
   globals, deterministic) behind a ``torch.autograd.Function``;
-* the dense layers (QKV / Wo / FFN GEMMs, post-LN LayerNorm with eps 1e-12,
-  exact-erf GELU, embeddings, the [CLS] head) are cuBLAS / torch ops whose
-  adjoints torch's autograd supplies -- fp32 with TF32 off for the parity
-  path, or bf16 autocast (``precision="bf16"``);
+* the dense layers: GEMMs on cuBLAS (``Linear``: bf16 or fp32 with TF32 off,
+  weight gradients accumulated in fp32, bias gradients by ``sc_colsum``),
+  residual add + post-LN LayerNorm (eps 1e-12) by ``sc_layernorm_fwd`` /
+  ``sc_layernorm_bwd``, exact-erf GELU, embeddings and the [CLS] head by torch
+  ops and autograd;
 * AdamW keeps the reference's update exactly (decoupled decay on every
   tensor, bias correction, linear warmup then linear decay).
 
@@ -121,6 +122,93 @@ def attention_backward(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor,
 
 
 # ---------------------------------------------------------------------------
+# Dense-layer blocks with device adjoints.
+# ---------------------------------------------------------------------------
+
+def _dcode(t: torch.Tensor) -> int:
+    return _lib.DTYPE_BF16 if t.dtype == torch.bfloat16 else _lib.DTYPE_F32
+
+
+class ResidualLayerNorm(torch.autograd.Function):
+    """y = LN(a + b) (fp32 out) with sc_layernorm_fwd / sc_layernorm_bwd (R/encoder.py:267-285).
+
+    a, b: [rows, cols] contiguous fp32 or bf16 (b may be None).  The backward
+    recomputes xhat from a + b and the saved per-row mean / rstd.
+    """
+
+    @staticmethod
+    def forward(ctx, a, b, gamma, beta):
+        rows, cols = a.shape
+        y = torch.empty(rows, cols, dtype=torch.float32, device=a.device)
+        mean = torch.empty(rows, dtype=torch.float32, device=a.device)
+        rstd = torch.empty_like(mean)
+        _lib.call("sc_layernorm_fwd", a.data_ptr(), _dcode(a), _lib.ptr(b), 0 if b is None else _dcode(b),
+                  gamma.data_ptr(), beta.data_ptr(), y.data_ptr(), mean.data_ptr(), rstd.data_ptr(), rows, cols,
+                  float(LAYER_NORM_EPS), _lib.stream_handle(), exc=EncoderError)
+        ctx.save_for_backward(a, b, gamma, mean, rstd)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        a, b, gamma, mean, rstd = ctx.saved_tensors
+        rows, cols = a.shape
+        dy = dy.float().contiguous()
+        dx = torch.empty(rows, cols, dtype=torch.float32, device=a.device)
+        dg = torch.empty(cols, dtype=torch.float32, device=a.device)
+        db = torch.empty_like(dg)
+        parts = torch.empty(2 * _lib.load().sc_ln_partials(rows) * cols, dtype=torch.float32, device=a.device)
+        _lib.call("sc_layernorm_bwd", dy.data_ptr(), a.data_ptr(), _dcode(a), _lib.ptr(b),
+                  0 if b is None else _dcode(b), gamma.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
+                  dg.data_ptr(), db.data_ptr(), parts.data_ptr(), rows, cols, _lib.stream_handle(), exc=EncoderError)
+        return dx.to(a.dtype), (None if b is None else dx.to(b.dtype)), dg, db
+
+
+def residual_layer_norm(a, b, gamma, beta):
+    if a.shape[1] > 1024 or a.shape[1] % 4:  # outside the kernel's envelope: torch's LayerNorm on the device
+        return F.layer_norm(a.float() + (0 if b is None else b.float()), (a.shape[1],), gamma, beta, LAYER_NORM_EPS)
+    return ResidualLayerNorm.apply(a.contiguous(), None if b is None else b.contiguous(), gamma, beta)
+
+
+def column_sum(x: torch.Tensor) -> torch.Tensor:
+    """fp32 column sums of a [rows, cols] matrix (sc_colsum, deterministic)."""
+    rows, cols = x.shape
+    out = torch.empty(cols, dtype=torch.float32, device=x.device)
+    parts = torch.empty(_lib.load().sc_ln_partials(rows) * cols, dtype=torch.float32, device=x.device)
+    _lib.call("sc_colsum", x.data_ptr(), _dcode(x), x.stride(0), rows, cols, out.data_ptr(), parts.data_ptr(),
+              _lib.stream_handle(), exc=EncoderError)
+    return out
+
+
+class Linear(torch.autograd.Function):
+    """out = x @ w + bias in compute dtype `cdt` (w in the reference's (in, out) layout, fp32 master).
+
+    Backward: dX = dY w^T and dW = x^T dY on cuBLAS (dW accumulated and returned in fp32), the
+    bias gradient by sc_colsum.
+    """
+
+    @staticmethod
+    def forward(ctx, x, w, bias, cdt):
+        xc = x.to(cdt).contiguous()
+        wc = w.to(cdt)
+        out = torch.addmm(bias.to(cdt), xc, wc)
+        ctx.save_for_backward(xc, wc)
+        ctx.meta = (cdt, x.dtype)
+        return out
+
+    @staticmethod
+    def backward(ctx, go):
+        xc, wc = ctx.saved_tensors
+        cdt, xdt = ctx.meta
+        go = go.to(cdt).contiguous()
+        dx = torch.mm(go, wc.t())
+        if cdt == torch.float32:
+            dw = torch.mm(xc.t(), go)
+        else:
+            dw = torch.mm(xc.t(), go, out_dtype=torch.float32)
+        return dx.to(xdt), dw, column_sum(go), None
+
+
+# ---------------------------------------------------------------------------
 # Trainable encoder.
 # ---------------------------------------------------------------------------
 
@@ -190,19 +278,20 @@ class TrainableCrossEncoder:
         bf16 = cfg.precision == "bf16"
         scale = math.sqrt(cfg.head_dim)
         x = W["tok_emb"][ids_dev.long()] + W["pos_emb"][layout.tok_pos.long()]
+        cd = torch.bfloat16 if bf16 else torch.float32
         flags = []
-        with self.gemm_mode(), torch.autocast("cuda", dtype=torch.bfloat16, enabled=bf16):
+        with self.gemm_mode():
             for i in range(cfg.layers):
                 p = f"L{i}."
                 wqkv = torch.cat([W[p + "wq"], W[p + "wk"], W[p + "wv"]], dim=1)
                 bqkv = torch.cat([W[p + "bq"], W[p + "bk"], W[p + "bv"]])
-                qkv = torch.addmm(bqkv, x, wqkv).contiguous()
+                qkv = Linear.apply(x, wqkv, bqkv, cd)
                 o = PatternAttention.apply(qkv, layout, self.pattern, H, scale, cfg.padding, i == 0)
-                r1 = x + torch.addmm(W[p + "bo"], o, W[p + "wo"])
-                ln1 = F.layer_norm(r1, (h,), W[p + "ln1_g"], W[p + "ln1_b"], LAYER_NORM_EPS)
-                g1 = F.gelu(torch.addmm(W[p + "b1"], ln1, W[p + "w1"]))
-                r2 = ln1 + torch.addmm(W[p + "b2"], g1, W[p + "w2"])
-                x = F.layer_norm(r2, (h,), W[p + "ln2_g"], W[p + "ln2_b"], LAYER_NORM_EPS)
+                ln1 = residual_layer_norm(x, Linear.apply(o, W[p + "wo"], W[p + "bo"], cd), W[p + "ln1_g"],
+                                          W[p + "ln1_b"])
+                g1 = F.gelu(Linear.apply(ln1, W[p + "w1"], W[p + "b1"], cd))
+                x = residual_layer_norm(ln1, Linear.apply(g1, W[p + "w2"], W[p + "b2"], cd), W[p + "ln2_g"],
+                                        W[p + "ln2_b"])
                 if check_finite:
                     flags.append(torch.isfinite(x.detach()).all())
         if flags:

@@ -376,3 +376,45 @@ def test_fused_adamw_matches_float64_reference_path(P):
         o2.step(ref, {n: torch.tensor(np.asarray(gs[step][n], np.float32)).double() for n in order})
     for n in order:
         np.testing.assert_allclose(pd[n].cpu().numpy(), ref[n].numpy(), rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("cols", [16, 96, 768, 1000])
+@pytest.mark.parametrize("adt,bdt", [(torch.float32, torch.bfloat16), (torch.float32, None),
+                                     (torch.bfloat16, torch.float32), (torch.float32, torch.float32)])
+def test_residual_layernorm_kernels_vs_torch(P, cols, adt, bdt):
+    from paper_2312_17649_b200.training import ResidualLayerNorm
+
+    gen = torch.Generator("cuda").manual_seed(cols)
+    rows = 1531
+    a = (torch.randn(rows, cols, device="cuda", generator=gen) * 3 + 1).to(adt).requires_grad_(True)
+    b = None if bdt is None else torch.randn(rows, cols, device="cuda", generator=gen).to(bdt).requires_grad_(True)
+    g = (torch.rand(cols, device="cuda", generator=gen) + 0.5).requires_grad_(True)
+    be = torch.randn(cols, device="cuda", generator=gen).requires_grad_(True)
+    y = ResidualLayerNorm.apply(a, b, g, be)
+    dy = torch.randn(rows, cols, device="cuda", generator=gen)
+    y.backward(dy)
+    a64 = a.detach().double().requires_grad_(True)
+    b64 = None if b is None else b.detach().double().requires_grad_(True)
+    g64, be64 = g.detach().double().requires_grad_(True), be.detach().double().requires_grad_(True)
+    x = a64 + (0 if b64 is None else b64)
+    y64 = torch.nn.functional.layer_norm(x, (cols,), g64, be64, 1e-12)
+    y64.backward(dy.double())
+    close(y.detach().cpu().numpy(), y64.detach().cpu().numpy(), 2e-5)
+    tol_x = 2e-5 if adt == torch.float32 else 2e-2
+    close(a.grad.float().cpu().numpy(), a64.grad.cpu().numpy(), tol_x)
+    if b is not None:
+        close(b.grad.float().cpu().numpy(), b64.grad.cpu().numpy(), 2e-2 if bdt == torch.bfloat16 else 2e-5)
+    close(g.grad.cpu().numpy(), g64.grad.cpu().numpy(), 1e-4)
+    close(be.grad.cpu().numpy(), be64.grad.cpu().numpy(), 1e-4)
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("rows,cols", [(1, 8), (777, 3072), (5000, 768), (33, 13)])
+def test_colsum_vs_torch(P, dt, rows, cols):
+    from paper_2312_17649_b200.training import column_sum
+
+    x = torch.randn(rows, cols + 5, device="cuda").to(dt)[:, :cols]  # strided rows
+    got = column_sum(x)
+    want = x.double().sum(0)
+    close(got.cpu().numpy(), want.cpu().numpy(), 1e-5)
+    assert torch.equal(column_sum(x), got)  # deterministic
