@@ -200,10 +200,10 @@ class Linear(torch.autograd.Function):
         xc, wc = ctx.saved_tensors
         cdt, xdt = ctx.meta
         go = go.to(cdt).contiguous()
-        dx = torch.mm(go, wc.t())
         if cdt == torch.float32:
-            dw = torch.mm(xc.t(), go)
-        else:
+            dx, dw = torch.mm(go, wc.t()), torch.mm(xc.t(), go)
+        else:  # fp32 outputs straight from the bf16 GEMMs (no cast passes)
+            dx = torch.mm(go, wc.t(), out_dtype=torch.float32) if xdt == torch.float32 else torch.mm(go, wc.t())
             dw = torch.mm(xc.t(), go, out_dtype=torch.float32)
         return dx.to(xdt), dw, column_sum(go), None
 
