@@ -257,23 +257,27 @@ SC_API int sc_gemm_residual_layernorm(const void* a, int64_t lda, const void* w,
 /* One fused AdamW step over a flat fp32 buffer of n parameters (R/training.py:
  * 114-137): m = b1 m + (1-b1) g, v = b2 v + (1-b2) g^2,
  * w -= lr * ((m/bc1) / (sqrt(v/bc2) + eps) + weight_decay * w) with
- * bc = 1 - beta^step; fp64 arithmetic, fp32 storage.  lr is the scheduled rate
- * of this step.  All buffers 16-byte aligned. */
-SC_API int sc_adamw_step(float* w, const float* g, float* m, float* v, int64_t n, double lr, double beta1,
-                  double beta2, double eps, double weight_decay, int64_t step, void* stream);
+ * bc = 1 - beta^step; fp64 arithmetic, fp32 storage; w_bf16 (optional)
+ * receives a bf16 copy of the updated weights.  lr is the scheduled rate of
+ * this step.  All buffers 16-byte aligned. */
+SC_API int sc_adamw_step(float* w, const float* g, float* m, float* v, void* w_bf16, int64_t n, double lr,
+                  double beta1, double beta2, double eps, double weight_decay, int64_t step, void* stream);
 
-/* y = LN(a + b) (b may be NULL) with gamma/beta, eps, fp32 y and per-row
- * mean / rstd for sc_layernorm_bwd (R/encoder.py:267-273).  a, b: [rows x
+/* y = LN(a + b) (b may be NULL) with gamma/beta, eps, fp32 y (plus an
+ * optional bf16 copy y_bf16 for the next GEMM) and per-row mean / rstd for
+ * sc_layernorm_bwd (R/encoder.py:267-273).  a, b: [rows x
  * cols] contiguous, fp32 or bf16.  cols % 4 == 0, cols <= 1024, 8-byte
  * aligned rows (else SC_ERR_UNSUPPORTED). */
 SC_API int sc_layernorm_fwd(const void* a, int32_t a_dtype, const void* b, int32_t b_dtype, const float* gamma,
-                     const float* beta, float* y, float* mean, float* rstd, int32_t rows, int32_t cols,
-                     float eps, void* stream);
+                     const float* beta, float* y, void* y_bf16, float* mean, float* rstd, int32_t rows,
+                     int32_t cols, float eps, void* stream);
 
-/* Adjoint of sc_layernorm_fwd (R/encoder.py:276-285): dx (fp32, the gradient
- * of both a and b) and dgamma / dbeta (fp32 [cols], written).  partials:
+/* Adjoint of sc_layernorm_fwd (R/encoder.py:276-285) for the upstream
+ * gradient dy (+ dy_bf16, the gradient of the bf16 copy, optional): dx (fp32,
+ * the gradient of both a and b) and dgamma / dbeta (fp32 [cols], written).  partials:
  * 2 * sc_ln_partials(rows) * cols floats of scratch.  Deterministic. */
-SC_API int sc_layernorm_bwd(const float* dy, const void* a, int32_t a_dtype, const void* b, int32_t b_dtype,
+SC_API int sc_layernorm_bwd(const float* dy, const void* dy_bf16, const void* a, int32_t a_dtype, const void* b,
+                     int32_t b_dtype,
                      const float* gamma, const float* mean, const float* rstd, float* dx, float* dgamma,
                      float* dbeta, float* partials, int32_t rows, int32_t cols, void* stream);
 

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(kLnWarps * 32, 4) ln_fwd_kernel(const TA* __re
                                                                   const float* __restrict__ beta,
                                                                   float* __restrict__ y, float* __restrict__ mean,
                                                                   float* __restrict__ rstd, int rows, int cols,
-                                                                  float eps) {
+                                                                  float eps, __nv_bfloat16* __restrict__ y16) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * kLnWarps + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -68,9 +68,16 @@ __global__ void __launch_bounds__(kLnWarps * 32, 4) ln_fwd_kernel(const TA* __re
     const int q = lane + 32 * k;
     if (q < ng) {
       const float4 g = ld4(gamma + 4 * q), bb = ld4(beta + 4 * q);
-      *reinterpret_cast<float4*>(y + base + 4 * q) =
-          make_float4((x[k].x - mu) * rs * g.x + bb.x, (x[k].y - mu) * rs * g.y + bb.y,
-                      (x[k].z - mu) * rs * g.z + bb.z, (x[k].w - mu) * rs * g.w + bb.w);
+      const float4 o = make_float4((x[k].x - mu) * rs * g.x + bb.x, (x[k].y - mu) * rs * g.y + bb.y,
+                                   (x[k].z - mu) * rs * g.z + bb.z, (x[k].w - mu) * rs * g.w + bb.w);
+      *reinterpret_cast<float4*>(y + base + 4 * q) = o;
+      if (y16) {  // bf16 copy for the next GEMM
+        __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&lo);
+        u.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(y16 + base + 4 * q) = u;
+      }
     }
   }
   if (lane == 0) { mean[row] = mu; rstd[row] = rs; }
@@ -86,7 +93,8 @@ __global__ void __launch_bounds__(kLnWarps * 32, 2) ln_bwd_kernel(const float* _
                                                                   const float* __restrict__ mean,
                                                                   const float* __restrict__ rstd,
                                                                   float* __restrict__ dx, float* __restrict__ part_g,
-                                                                  float* __restrict__ part_b, int rows, int cols) {
+                                                                  float* __restrict__ part_b, int rows, int cols,
+                                                                  const __nv_bfloat16* __restrict__ dy16) {
   extern __shared__ float4 lnsm[];  // [2][kLnWarps][ng] float4
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ng = cols >> 2;
@@ -107,7 +115,9 @@ __global__ void __launch_bounds__(kLnWarps * 32, 2) ln_bwd_kernel(const float* _
       if (q < ng) {
         float4 xv = ld4(a + base + 4 * q);
         if (b) xv = add4(xv, ld4(b + base + 4 * q));
-        const float4 d = ld4(dy + base + 4 * q), g = ld4(gamma + 4 * q);
+        float4 d = ld4(dy + base + 4 * q);
+        if (dy16) d = add4(d, ld4(dy16 + base + 4 * q));  // gradient of the bf16 copy of y
+        const float4 g = ld4(gamma + 4 * q);
         xh[k] = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
         gd[k] = make_float4(d.x * g.x, d.y * g.y, d.z * g.z, d.w * g.w);
         float4 ag = accg[q], ab = accb[q];
@@ -213,10 +223,10 @@ int num_sms() {
 template <typename TA, typename TB, int KV>
 void ln_launch(bool fwd, const void* a, const void* b, const float* gamma, const float* beta, const float* dy,
                float* y, float* mean, float* rstd, float* dx, float* pg, float* pb, int rows, int cols, float eps,
-               unsigned blocks, cudaStream_t st) {
+               unsigned blocks, cudaStream_t st, void* aux) {
   if (fwd) {
     ln_fwd_kernel<TA, TB, KV><<<blocks, kLnWarps * 32, 0, st>>>((const TA*)a, (const TB*)b, gamma, beta, y, mean,
-                                                                 rstd, rows, cols, eps);
+                                                                 rstd, rows, cols, eps, (__nv_bfloat16*)aux);
   } else {
     const size_t sm = (size_t)2 * kLnWarps * cols * sizeof(float);
     static bool attr = false;
@@ -226,28 +236,28 @@ void ln_launch(bool fwd, const void* a, const void* b, const float* gamma, const
       attr = true;
     }
     ln_bwd_kernel<TA, TB, KV><<<blocks, kLnWarps * 32, sm, st>>>(dy, (const TA*)a, (const TB*)b, gamma, mean, rstd,
-                                                                  dx, pg, pb, rows, cols);
+                                                                  dx, pg, pb, rows, cols, (const __nv_bfloat16*)aux);
   }
 }
 
 template <int KV>
 void ln_dispatch_types(bool af, bool bf, bool fwd, const void* a, const void* b, const float* gamma,
                        const float* beta, const float* dy, float* y, float* mean, float* rstd, float* dx, float* pg,
-                       float* pb, int rows, int cols, float eps, unsigned blocks, cudaStream_t st) {
+                       float* pb, int rows, int cols, float eps, unsigned blocks, cudaStream_t st, void* aux) {
   using B16 = __nv_bfloat16;
-  if (af && bf) ln_launch<float, float, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st);
-  else if (af) ln_launch<float, B16, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st);
-  else if (bf) ln_launch<B16, float, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st);
-  else ln_launch<B16, B16, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st);
+  if (af && bf) ln_launch<float, float, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux);
+  else if (af) ln_launch<float, B16, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux);
+  else if (bf) ln_launch<B16, float, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux);
+  else ln_launch<B16, B16, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux);
 }
 
 // Column groups (of 4) per lane rounded up to an instantiated width.
 void ln_dispatch(bool af, bool bf, bool fwd, const void* a, const void* b, const float* gamma, const float* beta,
                  const float* dy, float* y, float* mean, float* rstd, float* dx, float* pg, float* pb, int rows,
-                 int cols, float eps, unsigned blocks, cudaStream_t st) {
+                 int cols, float eps, unsigned blocks, cudaStream_t st, void* aux) {
   const int kv = (cols / 4 + 31) / 32;
 #define SC_LN_CASE(W) \
-  if (kv <= W) return ln_dispatch_types<W>(af, bf, fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st);
+  if (kv <= W) return ln_dispatch_types<W>(af, bf, fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux);
   SC_LN_CASE(1) SC_LN_CASE(2) SC_LN_CASE(4) SC_LN_CASE(6) SC_LN_CASE(8)
 #undef SC_LN_CASE
 }
@@ -262,11 +272,12 @@ extern "C" int sc_ln_partials(int32_t rows) {
 }
 
 extern "C" int sc_layernorm_fwd(const void* a, int32_t a_dtype, const void* b, int32_t b_dtype, const float* gamma,
-                                const float* beta, float* y, float* mean, float* rstd, int32_t rows, int32_t cols,
-                                float eps, void* stream) {
+                                const float* beta, float* y, void* y_bf16, float* mean, float* rstd, int32_t rows,
+                                int32_t cols, float eps, void* stream) {
   SC_CHECK_ARG(a && gamma && beta && y && mean && rstd, "sc_layernorm_fwd: null pointer");
   SC_CHECK_ARG(rows >= 0 && cols >= 1, "sc_layernorm_fwd: bad shape");
-  if (cols > kLnMaxV * 32 || cols % 4 || ((uintptr_t)a | (uintptr_t)b | (uintptr_t)y | (uintptr_t)gamma | (uintptr_t)beta) % 8) {
+  if (cols > kLnMaxV * 32 || cols % 4 ||
+      ((uintptr_t)a | (uintptr_t)b | (uintptr_t)y | (uintptr_t)y_bf16 | (uintptr_t)gamma | (uintptr_t)beta) % 8) {
     set_error("sc_layernorm_fwd: needs cols %% 4 == 0, cols <= %d and 8-byte aligned rows", kLnMaxV * 32);
     return SC_ERR_UNSUPPORTED;
   }
@@ -275,17 +286,19 @@ extern "C" int sc_layernorm_fwd(const void* a, int32_t a_dtype, const void* b, i
   if (rows == 0) return SC_OK;
   const unsigned blocks = (unsigned)((rows + kLnWarps - 1) / kLnWarps);
   ln_dispatch(a_dtype == SC_DTYPE_F32, !b || b_dtype == SC_DTYPE_F32, true, a, b, gamma, beta, nullptr, y, mean, rstd,
-              nullptr, nullptr, nullptr, rows, cols, eps, blocks, (cudaStream_t)stream);
+              nullptr, nullptr, nullptr, rows, cols, eps, blocks, (cudaStream_t)stream, y_bf16);
   SC_CHECK_LAUNCH("ln_fwd_kernel");
   return SC_OK;
 }
 
-extern "C" int sc_layernorm_bwd(const float* dy, const void* a, int32_t a_dtype, const void* b, int32_t b_dtype,
+extern "C" int sc_layernorm_bwd(const float* dy, const void* dy_bf16, const void* a, int32_t a_dtype, const void* b,
+                                int32_t b_dtype,
                                 const float* gamma, const float* mean, const float* rstd, float* dx, float* dgamma,
                                 float* dbeta, float* partials, int32_t rows, int32_t cols, void* stream) {
   SC_CHECK_ARG(dy && a && gamma && mean && rstd && dx && dgamma && dbeta && partials, "sc_layernorm_bwd: null pointer");
   SC_CHECK_ARG(rows >= 0 && cols >= 1, "sc_layernorm_bwd: bad shape");
-  if (cols > kLnMaxV * 32 || cols % 4 || ((uintptr_t)a | (uintptr_t)b | (uintptr_t)dy | (uintptr_t)dx | (uintptr_t)gamma) % 8) {
+  if (cols > kLnMaxV * 32 || cols % 4 ||
+      ((uintptr_t)a | (uintptr_t)b | (uintptr_t)dy | (uintptr_t)dy_bf16 | (uintptr_t)dx | (uintptr_t)gamma) % 8) {
     set_error("sc_layernorm_bwd: needs cols %% 4 == 0, cols <= %d and 8-byte aligned rows", kLnMaxV * 32);
     return SC_ERR_UNSUPPORTED;
   }
@@ -297,7 +310,7 @@ extern "C" int sc_layernorm_bwd(const float* dy, const void* a, int32_t a_dtype,
   float* pb = partials + (int64_t)nparts * cols;
   if (rows > 0)
     ln_dispatch(a_dtype == SC_DTYPE_F32, !b || b_dtype == SC_DTYPE_F32, false, a, b, gamma, nullptr, dy, nullptr,
-                (float*)mean, (float*)rstd, dx, pg, pb, rows, cols, 0.f, (unsigned)nparts, st);
+                (float*)mean, (float*)rstd, dx, pg, pb, rows, cols, 0.f, (unsigned)nparts, st, (void*)dy_bf16);
   SC_CHECK_LAUNCH("ln_bwd_kernel");
   colsum_reduce_kernel<<<(cols + 31) / 32, 256, 0, st>>>(pg, nparts, cols, dgamma);
   SC_CHECK_LAUNCH("colsum_reduce_kernel");

@@ -132,41 +132,49 @@ def _dcode(t: torch.Tensor) -> int:
 class ResidualLayerNorm(torch.autograd.Function):
     """y = LN(a + b) (fp32 out) with sc_layernorm_fwd / sc_layernorm_bwd (R/encoder.py:267-285).
 
-    a, b: [rows, cols] contiguous fp32 or bf16 (b may be None).  The backward
-    recomputes xhat from a + b and the saved per-row mean / rstd.
+    a, b: [rows, cols] contiguous fp32 or bf16 (b may be None).  With ``want16`` it also returns
+    a bf16 copy of y for the next GEMM; the backward sums the gradients of both outputs inside
+    the kernel and recomputes xhat from a + b and the saved per-row mean / rstd.
     """
 
     @staticmethod
-    def forward(ctx, a, b, gamma, beta):
+    def forward(ctx, a, b, gamma, beta, want16=False):
         rows, cols = a.shape
         y = torch.empty(rows, cols, dtype=torch.float32, device=a.device)
+        y16 = torch.empty(rows, cols, dtype=torch.bfloat16, device=a.device) if want16 else None
         mean = torch.empty(rows, dtype=torch.float32, device=a.device)
         rstd = torch.empty_like(mean)
         _lib.call("sc_layernorm_fwd", a.data_ptr(), _dcode(a), _lib.ptr(b), 0 if b is None else _dcode(b),
-                  gamma.data_ptr(), beta.data_ptr(), y.data_ptr(), mean.data_ptr(), rstd.data_ptr(), rows, cols,
-                  float(LAYER_NORM_EPS), _lib.stream_handle(), exc=EncoderError)
+                  gamma.data_ptr(), beta.data_ptr(), y.data_ptr(), _lib.ptr(y16), mean.data_ptr(), rstd.data_ptr(),
+                  rows, cols, float(LAYER_NORM_EPS), _lib.stream_handle(), exc=EncoderError)
         ctx.save_for_backward(a, b, gamma, mean, rstd)
+        ctx.set_materialize_grads(False)
+        if want16:
+            return y, y16
         return y
 
     @staticmethod
-    def backward(ctx, dy):
+    def backward(ctx, dy, dy16=None):
         a, b, gamma, mean, rstd = ctx.saved_tensors
         rows, cols = a.shape
-        dy = dy.float().contiguous()
+        dy = torch.zeros(rows, cols, dtype=torch.float32, device=a.device) if dy is None else dy.float().contiguous()
+        dy16 = None if dy16 is None else dy16.to(torch.bfloat16).contiguous()
         dx = torch.empty(rows, cols, dtype=torch.float32, device=a.device)
         dg = torch.empty(cols, dtype=torch.float32, device=a.device)
         db = torch.empty_like(dg)
         parts = torch.empty(2 * _lib.load().sc_ln_partials(rows) * cols, dtype=torch.float32, device=a.device)
-        _lib.call("sc_layernorm_bwd", dy.data_ptr(), a.data_ptr(), _dcode(a), _lib.ptr(b),
+        _lib.call("sc_layernorm_bwd", dy.data_ptr(), _lib.ptr(dy16), a.data_ptr(), _dcode(a), _lib.ptr(b),
                   0 if b is None else _dcode(b), gamma.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
                   dg.data_ptr(), db.data_ptr(), parts.data_ptr(), rows, cols, _lib.stream_handle(), exc=EncoderError)
-        return dx.to(a.dtype), (None if b is None else dx.to(b.dtype)), dg, db
+        return dx.to(a.dtype), (None if b is None else dx.to(b.dtype)), dg, db, None
 
 
-def residual_layer_norm(a, b, gamma, beta):
+def residual_layer_norm(a, b, gamma, beta, want16=False):
+    """LN(a + b) -> y, or (y, bf16 copy of y) with want16."""
     if a.shape[1] > 1024 or a.shape[1] % 4:  # outside the kernel's envelope: torch's LayerNorm on the device
-        return F.layer_norm(a.float() + (0 if b is None else b.float()), (a.shape[1],), gamma, beta, LAYER_NORM_EPS)
-    return ResidualLayerNorm.apply(a.contiguous(), None if b is None else b.contiguous(), gamma, beta)
+        y = F.layer_norm(a.float() + (0 if b is None else b.float()), (a.shape[1],), gamma, beta, LAYER_NORM_EPS)
+        return (y, y.to(torch.bfloat16)) if want16 else y
+    return ResidualLayerNorm.apply(a.contiguous(), None if b is None else b.contiguous(), gamma, beta, want16)
 
 
 def column_sum(x: torch.Tensor) -> torch.Tensor:
@@ -182,15 +190,16 @@ def column_sum(x: torch.Tensor) -> torch.Tensor:
 class Linear(torch.autograd.Function):
     """out = x @ w + bias in compute dtype `cdt` (w in the reference's (in, out) layout, fp32 master).
 
-    Backward: dX = dY w^T and dW = x^T dY on cuBLAS (dW accumulated and returned in fp32), the
-    bias gradient by sc_colsum.
+    ``w16`` / ``b16``: optional compute-dtype copies of w / bias (the optimizer's bf16 shadow), so
+    the forward does not cast the weights.  Backward: dX = dY w^T and dW = x^T dY on cuBLAS (dW
+    accumulated and returned in fp32), the bias gradient by sc_colsum.
     """
 
     @staticmethod
-    def forward(ctx, x, w, bias, cdt):
+    def forward(ctx, x, w, w16, bias, b16, cdt):
         xc = x.to(cdt).contiguous()
-        wc = w.to(cdt)
-        out = torch.addmm(bias.to(cdt), xc, wc)
+        wc = w16 if w16 is not None else w.to(cdt)
+        out = torch.addmm(b16 if b16 is not None else bias.to(cdt), xc, wc)
         ctx.save_for_backward(xc, wc)
         ctx.meta = (cdt, x.dtype)
         return out
@@ -205,7 +214,7 @@ class Linear(torch.autograd.Function):
         else:  # fp32 outputs straight from the bf16 GEMMs (no cast passes)
             dx = torch.mm(go, wc.t(), out_dtype=torch.float32) if xdt == torch.float32 else torch.mm(go, wc.t())
             dw = torch.mm(xc.t(), go, out_dtype=torch.float32)
-        return dx.to(xdt), dw, column_sum(go), None
+        return dx.to(xdt), dw, None, column_sum(go), None, None
 
 
 # ---------------------------------------------------------------------------
@@ -216,10 +225,29 @@ class ParamDict(dict):
     """Reference-named parameters that are views of one flat fp32 device buffer (``flat``),
     so the optimizer updates every tensor with one fused kernel (sc_adamw_step)."""
 
-    def __init__(self, items, flat: torch.Tensor, order):
+    def __init__(self, items, flat: torch.Tensor, order, shadow: torch.Tensor | None = None):
         super().__init__(items)
         self.flat = flat
         self.order = list(order)
+        self.shadow = shadow          # optional bf16 copy of `flat`, kept current by the fused AdamW
+        self.shadow_version = -1      # flat._version the shadow was last synced at
+        self.shadow_views = {}
+        if shadow is not None:
+            off = 0
+            for n in self.order:
+                k = items[n].numel()
+                self.shadow_views[n] = shadow[off:off + k].view(items[n].shape)
+                off += k
+
+    def bf16_views(self) -> dict:
+        """bf16 views of the weights, re-synced if the fp32 weights were modified in place."""
+        if self.shadow is None:
+            return None
+        if self.shadow_version != self.flat._version:
+            with torch.no_grad():
+                self.shadow.copy_(self.flat)
+            self.shadow_version = self.flat._version
+        return self.shadow_views
 
 
 class TrainableCrossEncoder:
@@ -244,7 +272,9 @@ class TrainableCrossEncoder:
             v.copy_(torch.from_numpy(a.copy()))
             views[n] = v.requires_grad_(True)
             off += a.size
-        self.weights = ParamDict(views, flat, order)
+        shadow = torch.empty(flat.numel(), dtype=torch.bfloat16, device=self.device) \
+            if config.precision == "bf16" else None
+        self.weights = ParamDict(views, flat, order, shadow)
         self.pattern = make_pattern(config.pattern, config.window)
 
     @property
@@ -279,19 +309,36 @@ class TrainableCrossEncoder:
         scale = math.sqrt(cfg.head_dim)
         x = W["tok_emb"][ids_dev.long()] + W["pos_emb"][layout.tok_pos.long()]
         cd = torch.bfloat16 if bf16 else torch.float32
+        S = W.bf16_views() if (bf16 and isinstance(W, ParamDict)) else None
+
+        def lin(xin, wname, bname, w=None, w16=None):
+            w = W[wname] if w is None else w
+            if S is not None and w16 is None:
+                w16 = S[wname]
+            return Linear.apply(xin, w, w16, W[bname], None if S is None else S[bname], cd)
+
         flags = []
+        xh = x  # GEMM input of the layer (bf16 copy of the previous LayerNorm in the bf16 path)
         with self.gemm_mode():
             for i in range(cfg.layers):
                 p = f"L{i}."
                 wqkv = torch.cat([W[p + "wq"], W[p + "wk"], W[p + "wv"]], dim=1)
                 bqkv = torch.cat([W[p + "bq"], W[p + "bk"], W[p + "bv"]])
-                qkv = Linear.apply(x, wqkv, bqkv, cd)
+                w16 = None if S is None else torch.cat([S[p + "wq"], S[p + "wk"], S[p + "wv"]], dim=1)
+                b16 = None if S is None else torch.cat([S[p + "bq"], S[p + "bk"], S[p + "bv"]])
+                qkv = Linear.apply(xh, wqkv, w16, bqkv, b16, cd)
                 o = PatternAttention.apply(qkv, layout, self.pattern, H, scale, cfg.padding, i == 0)
-                ln1 = residual_layer_norm(x, Linear.apply(o, W[p + "wo"], W[p + "bo"], cd), W[p + "ln1_g"],
-                                          W[p + "ln1_b"])
-                g1 = F.gelu(Linear.apply(ln1, W[p + "w1"], W[p + "b1"], cd))
-                x = residual_layer_norm(ln1, Linear.apply(g1, W[p + "w2"], W[p + "b2"], cd), W[p + "ln2_g"],
-                                        W[p + "ln2_b"])
+                if bf16:
+                    ln1, ln1h = residual_layer_norm(x, lin(o, p + "wo", p + "bo"), W[p + "ln1_g"], W[p + "ln1_b"],
+                                                    want16=True)
+                else:
+                    ln1 = ln1h = residual_layer_norm(x, lin(o, p + "wo", p + "bo"), W[p + "ln1_g"], W[p + "ln1_b"])
+                g1 = F.gelu(lin(ln1h, p + "w1", p + "b1"))
+                if bf16:
+                    x, xh = residual_layer_norm(ln1, lin(g1, p + "w2", p + "b2"), W[p + "ln2_g"], W[p + "ln2_b"],
+                                                want16=True)
+                else:
+                    x = xh = residual_layer_norm(ln1, lin(g1, p + "w2", p + "b2"), W[p + "ln2_g"], W[p + "ln2_b"])
                 if check_finite:
                     flags.append(torch.isfinite(x.detach()).all())
         if flags:
@@ -469,8 +516,9 @@ class AdamW:
         if self._m.get("__flat__") is None:
             self._m["__flat__"] = torch.zeros_like(flat)
             self._v["__flat__"] = torch.zeros_like(flat)
+        shadow = weights.shadow if weights.shadow_version == flat._version else None
         _lib.call("sc_adamw_step", flat.data_ptr(), g.data_ptr(), self._m["__flat__"].data_ptr(),
-                  self._v["__flat__"].data_ptr(), flat.numel(), float(lr_t), float(self.beta1), float(self.beta2),
+                  self._v["__flat__"].data_ptr(), _lib.ptr(shadow), flat.numel(), float(lr_t), float(self.beta1), float(self.beta2),
                   float(self.eps), float(self.weight_decay), int(t), _lib.stream_handle(), exc=TrainingError)
 
 
