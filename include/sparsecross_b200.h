@@ -287,6 +287,18 @@ SC_API int sc_layernorm_bwd(const float* dy, const void* dy_bf16, const void* a,
 SC_API int sc_colsum(const void* x, int32_t dtype, int64_t ld, int32_t rows, int32_t cols, float* out,
               float* partials, void* stream);
 
+/* Exact-erf GELU (R/encoder.py:258-259), out of place; n % 8 == 0, 16-byte
+ * aligned (else SC_ERR_UNSUPPORTED).  fp32: erff; bf16: one-MUFU erfc fit
+ * (|error| <= 2e-6, below bf16 resolution), as in the forward epilogue. */
+SC_API int sc_gelu_fwd(const void* x, void* y, int32_t dtype, int64_t n, void* stream);
+
+/* dx = dy * gelu'(x) (R/encoder.py:262-264, :408) over [rows x cols]
+ * contiguous, and (dbias != NULL) the column sums of dx in fp32 -- the bias
+ * gradient of the GEMM that produced x -- with sc_ln_partials(rows) * cols
+ * floats of partials.  cols % 8 == 0, 16-byte aligned.  Deterministic. */
+SC_API int sc_gelu_bwd(const void* x, const void* dy, void* dx, int32_t dtype, int32_t rows, int32_t cols,
+                float* dbias, float* partials, void* stream);
+
 /* Number of per-CTA partial rows the two reductions above use for `rows`. */
 SC_API int sc_ln_partials(int32_t rows);
 

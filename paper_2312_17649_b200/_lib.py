@@ -74,6 +74,8 @@ SIGNATURES = {
     "sc_layernorm_bwd": (C.c_int, [_p, _p, _p, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _i32, _i32, _p]),
     "sc_colsum": (C.c_int, [_p, _i32, _i64, _i32, _i32, _p, _p, _p]),
     "sc_ln_partials": (C.c_int, [_i32]),
+    "sc_gelu_fwd": (C.c_int, [_p, _p, _i32, _i64, _p]),
+    "sc_gelu_bwd": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _p, _p, _p]),
     "sc_cls_score": (C.c_int, [_p, _p, _i32, _i32, _p, _f32, _p, _p]),
     "sc_count_nonfinite": (C.c_int, [_p, _i64, _p, _p]),
 }

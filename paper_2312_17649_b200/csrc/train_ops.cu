@@ -337,3 +337,197 @@ extern "C" int sc_colsum(const void* x, int32_t dtype, int64_t ld, int32_t rows,
   SC_CHECK_LAUNCH("colsum_reduce_kernel");
   return SC_OK;
 }
+
+// ---- exact-erf GELU forward / backward (R/encoder.py:258-264) -------------------------------
+//   gelu(x)  = 0.5 x (1 + erf(x / sqrt 2))
+//   gelu'(x) = 0.5 (1 + erf(x / sqrt 2)) + x exp(-x^2 / 2) / sqrt(2 pi)
+// The backward also reduces the column sums of dx (the bias gradient of the GEMM that produced x),
+// per-CTA partials like colsum_kernel.
+
+namespace sc {
+
+// fp32 (parity) path: erff / expf.
+__device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  return 0.5f * (1.f + erff(x * 0.70710678118654752f)) + x * expf(-0.5f * x * x) * 0.3989422804014327f;
+}
+
+// bf16 path: one MUFU op per element.  With z = x / sqrt 2, e = exp(-z^2):
+//   Phi(x) = 1 - 0.5 e R(|z|) (x >= 0) or 0.5 e R(|z|) (x < 0), R the degree-10 erfcx fit of
+//   gelu.cuh (|z| clamped at 4), and phi(x) = e / sqrt(2 pi); gelu = x Phi, gelu' = Phi + x phi.
+__device__ __forceinline__ void gelu_parts_fast(float x, float& Phi, float& phi) {
+  const float z = x * 0.70710678118654752f;
+  const float a = fminf(fabsf(z), 4.f);
+  float p = fmaf(1.1544991139089689e-05f, a, -0.00027032289654016495f);
+  p = fmaf(p, a, 0.0028087019454687834f);
+  p = fmaf(p, a, -0.017178276553750038f);
+  p = fmaf(p, a, 0.06945336610078812f);
+  p = fmaf(p, a, -0.19890554249286652f);
+  p = fmaf(p, a, 0.4261739253997803f);
+  p = fmaf(p, a, -0.7184767723083496f);
+  p = fmaf(p, a, 0.9914032816886902f);
+  p = fmaf(p, a, -1.1274118423461914f);
+  p = fmaf(p, a, 0.9999727010726929f);
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.4426950408889634f));
+  const float he = 0.5f * e * p;
+  Phi = x >= 0.f ? 1.f - he : he;
+  phi = e * 0.3989422804014327f;
+}
+template <typename T>
+__device__ __forceinline__ float gelu_t(float x) {
+  if constexpr (sizeof(T) == 2) {
+    float Phi, phi;
+    gelu_parts_fast(x, Phi, phi);
+    return x * Phi;
+  } else {
+    return gelu_f(x);
+  }
+}
+template <typename T>
+__device__ __forceinline__ float gelu_grad_t(float x) {
+  if constexpr (sizeof(T) == 2) {
+    float Phi, phi;
+    gelu_parts_fast(x, Phi, phi);
+    return fmaf(x, phi, Phi);
+  } else {
+    return gelu_grad_f(x);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void ld8(const T* p, float (&v)[8]) {
+  if constexpr (sizeof(T) == 2) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      v[2 * e] = f.x;
+      v[2 * e + 1] = f.y;
+    }
+  } else {
+    const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void st8(T* p, const float (&v)[8]) {
+  if constexpr (sizeof(T) == 2) {
+    uint4 u;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+      w[e] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(p) = u;
+  } else {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) gelu_fwd_kernel(const T* __restrict__ x, T* __restrict__ y, int64_t n8) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    float v[8];
+    ld8(x + 8 * i, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = gelu_t<T>(v[e]);
+    st8(y + 8 * i, v);
+  }
+}
+
+// CTA k: rows [k * rpc, (k+1) * rpc); thread t: columns 8t .. 8t+7 (+ 8 * blockDim per pass).
+template <typename T>
+__global__ void __launch_bounds__(256) gelu_bwd_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                                                       T* __restrict__ dx, int rows, int cols, int rpc,
+                                                       float* __restrict__ part) {
+  const int r0 = blockIdx.x * rpc, r1 = min(rows, r0 + rpc);
+  for (int c0 = 8 * threadIdx.x; c0 < cols; c0 += 8 * blockDim.x) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int r = r0;
+    for (; r + 1 < r1; r += 2) {  // two rows in flight
+      const int64_t off0 = (int64_t)r * cols + c0, off1 = off0 + cols;
+      float x0[8], g0[8], x1[8], g1[8];
+      ld8(x + off0, x0);
+      ld8(dy + off0, g0);
+      ld8(x + off1, x1);
+      ld8(dy + off1, g1);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        x0[e] = g0[e] * gelu_grad_t<T>(x0[e]);
+        x1[e] = g1[e] * gelu_grad_t<T>(x1[e]);
+        acc[e] += x0[e];
+        acc[e] += x1[e];
+      }
+      st8(dx + off0, x0);
+      st8(dx + off1, x1);
+    }
+    for (; r < r1; ++r) {
+      const int64_t off = (int64_t)r * cols + c0;
+      float xv[8], gv[8];
+      ld8(x + off, xv);
+      ld8(dy + off, gv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        xv[e] = gv[e] * gelu_grad_t<T>(xv[e]);
+        acc[e] += xv[e];
+      }
+      st8(dx + off, xv);
+    }
+    if (part) {
+      float4* o = reinterpret_cast<float4*>(part + (int64_t)blockIdx.x * cols + c0);
+      o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+  }
+}
+
+}  // namespace sc
+
+extern "C" int sc_gelu_fwd(const void* x, void* y, int32_t dtype, int64_t n, void* stream) {
+  SC_CHECK_ARG(x && y, "sc_gelu_fwd: null pointer");
+  SC_CHECK_ARG(dtype == SC_DTYPE_F32 || dtype == SC_DTYPE_BF16, "sc_gelu_fwd: bad dtype");
+  if (n % 8 || ((uintptr_t)x | (uintptr_t)y) % 16) {
+    set_error("sc_gelu_fwd: needs n %% 8 == 0 and 16-byte aligned buffers");
+    return SC_ERR_UNSUPPORTED;
+  }
+  if (n == 0) return SC_OK;
+  const int64_t n8 = n / 8;
+  const int64_t want = (n8 + 255) / 256, cap = (int64_t)num_sms() * 16;
+  const unsigned blocks = (unsigned)(want < cap ? want : cap);
+  if (dtype == SC_DTYPE_F32) gelu_fwd_kernel<float><<<blocks, 256, 0, (cudaStream_t)stream>>>((const float*)x, (float*)y, n8);
+  else gelu_fwd_kernel<__nv_bfloat16><<<blocks, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)x, (__nv_bfloat16*)y, n8);
+  SC_CHECK_LAUNCH("gelu_fwd_kernel");
+  return SC_OK;
+}
+
+extern "C" int sc_gelu_bwd(const void* x, const void* dy, void* dx, int32_t dtype, int32_t rows, int32_t cols,
+                           float* dbias, float* partials, void* stream) {
+  SC_CHECK_ARG(x && dy && dx, "sc_gelu_bwd: null pointer");
+  SC_CHECK_ARG(dtype == SC_DTYPE_F32 || dtype == SC_DTYPE_BF16, "sc_gelu_bwd: bad dtype");
+  SC_CHECK_ARG(rows >= 0 && cols >= 1 && (!dbias || partials), "sc_gelu_bwd: bad shape / missing partials");
+  if (cols % 8 || ((uintptr_t)x | (uintptr_t)dy | (uintptr_t)dx) % 16) {
+    set_error("sc_gelu_bwd: needs cols %% 8 == 0 and 16-byte aligned rows");
+    return SC_ERR_UNSUPPORTED;
+  }
+  if (rows == 0) return SC_OK;
+  const int nparts = sc_ln_partials(rows);
+  const int rpc = (rows + nparts - 1) / nparts;
+  const int threads = min(256, max(32, (cols / 8 + 31) / 32 * 32));
+  cudaStream_t st = (cudaStream_t)stream;
+  float* part = dbias ? partials : nullptr;
+  if (dtype == SC_DTYPE_F32)
+    gelu_bwd_kernel<float><<<nparts, threads, 0, st>>>((const float*)x, (const float*)dy, (float*)dx, rows, cols, rpc, part);
+  else
+    gelu_bwd_kernel<__nv_bfloat16><<<nparts, threads, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)dy,
+                                                               (__nv_bfloat16*)dx, rows, cols, rpc, part);
+  SC_CHECK_LAUNCH("gelu_bwd_kernel");
+  if (dbias) {
+    colsum_reduce_kernel<<<(cols + 31) / 32, 256, 0, st>>>(partials, nparts, cols, dbias);
+    SC_CHECK_LAUNCH("colsum_reduce_kernel");
+  }
+  return SC_OK;
+}

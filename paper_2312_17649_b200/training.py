@@ -14,8 +14,9 @@ rebuilt on the device:
 * the dense layers: GEMMs on cuBLAS (``Linear``: bf16 or fp32 with TF32 off,
   weight gradients accumulated in fp32, bias gradients by ``sc_colsum``),
   residual add + post-LN LayerNorm (eps 1e-12) by ``sc_layernorm_fwd`` /
-  ``sc_layernorm_bwd``, exact-erf GELU, embeddings and the [CLS] head by torch
-  ops and autograd;
+  ``sc_layernorm_bwd``, exact-erf GELU by ``sc_gelu_fwd`` / ``sc_gelu_bwd``
+  (the latter also reducing the W1 bias gradient), embeddings and the [CLS]
+  head by torch ops and autograd;
 * AdamW keeps the reference's update exactly (decoupled decay on every
   tensor, bias correction, linear warmup then linear decay).
 
@@ -217,6 +218,45 @@ class Linear(torch.autograd.Function):
         return dx.to(xdt), dw, None, column_sum(go), None, None
 
 
+class LinearGelu(torch.autograd.Function):
+    """gelu(x @ w + bias) (R/encoder.py:350-351) with sc_gelu_fwd / sc_gelu_bwd; the backward's
+    GELU kernel also reduces the bias gradient (no second pass over dF)."""
+
+    @staticmethod
+    def forward(ctx, x, w, w16, bias, b16, cdt):
+        xc = x.to(cdt).contiguous()
+        wc = w16 if w16 is not None else w.to(cdt)
+        f = torch.addmm(b16 if b16 is not None else bias.to(cdt), xc, wc)
+        g = torch.empty_like(f)
+        _lib.call("sc_gelu_fwd", f.data_ptr(), g.data_ptr(), _dcode(f), f.numel(), _lib.stream_handle(),
+                  exc=EncoderError)
+        ctx.save_for_backward(xc, wc, f)
+        ctx.meta = (cdt, x.dtype)
+        return g
+
+    @staticmethod
+    def backward(ctx, dg):
+        xc, wc, f = ctx.saved_tensors
+        cdt, xdt = ctx.meta
+        rows, cols = f.shape
+        dg = dg.to(cdt).contiguous()
+        df = torch.empty_like(f)
+        db = torch.empty(cols, dtype=torch.float32, device=f.device)
+        parts = torch.empty(_lib.load().sc_ln_partials(rows) * cols, dtype=torch.float32, device=f.device)
+        _lib.call("sc_gelu_bwd", f.data_ptr(), dg.data_ptr(), df.data_ptr(), _dcode(f), rows, cols, db.data_ptr(),
+                  parts.data_ptr(), _lib.stream_handle(), exc=EncoderError)
+        if cdt == torch.float32:
+            dx, dw = torch.mm(df, wc.t()), torch.mm(xc.t(), df)
+        else:
+            dx = torch.mm(df, wc.t(), out_dtype=torch.float32) if xdt == torch.float32 else torch.mm(df, wc.t())
+            dw = torch.mm(xc.t(), df, out_dtype=torch.float32)
+        return dx.to(xdt), dw, None, db, None, None
+
+
+def _gelu_ok(cols: int) -> bool:
+    return cols % 8 == 0
+
+
 # ---------------------------------------------------------------------------
 # Trainable encoder.
 # ---------------------------------------------------------------------------
@@ -333,7 +373,11 @@ class TrainableCrossEncoder:
                                                     want16=True)
                 else:
                     ln1 = ln1h = residual_layer_norm(x, lin(o, p + "wo", p + "bo"), W[p + "ln1_g"], W[p + "ln1_b"])
-                g1 = F.gelu(lin(ln1h, p + "w1", p + "b1"))
+                if _gelu_ok(cfg.ff_dim):
+                    g1 = LinearGelu.apply(ln1h, W[p + "w1"], None if S is None else S[p + "w1"], W[p + "b1"],
+                                          None if S is None else S[p + "b1"], cd)
+                else:
+                    g1 = F.gelu(lin(ln1h, p + "w1", p + "b1"))
                 if bf16:
                     x, xh = residual_layer_norm(ln1, lin(g1, p + "w2", p + "b2"), W[p + "ln2_g"], W[p + "ln2_b"],
                                                 want16=True)

@@ -418,3 +418,31 @@ def test_colsum_vs_torch(P, dt, rows, cols):
     want = x.double().sum(0)
     close(got.cpu().numpy(), want.cpu().numpy(), 1e-5)
     assert torch.equal(column_sum(x), got)  # deterministic
+
+
+@pytest.mark.parametrize("dt,tol", [(torch.float32, 1e-5), (torch.bfloat16, 2e-2)])
+def test_linear_gelu_vs_torch(P, dt, tol):
+    from paper_2312_17649_b200.training import LinearGelu
+
+    gen = torch.Generator("cuda").manual_seed(2)
+    x = torch.randn(1000, 96, device="cuda", generator=gen).requires_grad_(True)
+    w = (torch.randn(96, 256, device="cuda", generator=gen) * 0.2).requires_grad_(True)
+    b = torch.randn(256, device="cuda", generator=gen).requires_grad_(True)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        y = LinearGelu.apply(x, w, None, b, None, dt)
+        gy = torch.randn(y.shape, device="cuda", generator=gen)
+        y.backward(gy.to(y.dtype))
+        x64, w64, b64 = (t.detach().double().requires_grad_(True) for t in (x, w, b))
+        if dt == torch.bfloat16:  # the reference sees the same bf16-rounded GEMM inputs
+            x64 = x.detach().bfloat16().double().requires_grad_(True)
+            w64 = w.detach().bfloat16().double().requires_grad_(True)
+        y64 = torch.nn.functional.gelu(x64 @ w64 + b64)
+        y64.backward(gy.to(y.dtype).double())
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    close(y.float().detach().cpu().numpy(), y64.detach().cpu().numpy(), tol)
+    close(x.grad.cpu().numpy(), x64.grad.cpu().numpy(), tol)
+    close(w.grad.cpu().numpy(), w64.grad.cpu().numpy(), tol)
+    close(b.grad.cpu().numpy(), b64.grad.cpu().numpy(), tol)
