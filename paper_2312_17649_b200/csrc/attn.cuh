@@ -50,7 +50,7 @@ struct BandBwdArgs {
   float* head_part;               // [tiles][H][2][NH][64] per-tile head-key dV / dK partials, or nullptr
 };
 // phase 0: doc-row statistics + dQ (+ head-key partials); 1: doc-key dK / dV; 2: head-key partial
-// reduction.  max_head = 1 + max qgroup_len (<= 32); NH = 16 when max_head <= 16, else 32.
+// reduction; 3: head-row statistics + dQ.  max_head = 1 + max qgroup_len (<= 32); NH = 16 when max_head <= 16, else 32.
 int launch_attn_bwd_band(const BandBwdArgs& a, int ntiles, int max_head, int phase, cudaStream_t st);
 int launch_attn_generic(const AttnArgs& a, int dtype, cudaStream_t st);
 

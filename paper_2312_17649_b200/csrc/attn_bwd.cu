@@ -633,7 +633,7 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
     return SC_ERR_CUDA;
   }
   b.mode = 1;
-  int rc = launch_generic_any(b, dtype, 0, st);               // head rows: stats + dQ
+  int rc = launch_attn_bwd_band(p, ntiles, b.maxh, 3, st);   // head rows: stats + dQ (tensor cores)
   if (!rc && ntiles) rc = launch_attn_bwd_band(p, ntiles, b.maxh, 0, st);  // doc rows: stats + dQ
   if (!rc && ntiles) rc = launch_attn_bwd_band(p, ntiles, b.maxh, 1, st);  // doc keys: dK, dV
   b.skip_doc_sources = p.head_part != nullptr && ntiles > 0;

@@ -522,6 +522,244 @@ __global__ void __launch_bounds__(128) band_dkv_kernel(Args p) {
   }
 }
 
+
+// Head rows (cls + query group, <= NH) of one sequence x one head against every key of the
+// sequence: S = Qh K^T on mma.sync with M = the head rows, keys in 64-row chunks dealt to the
+// 8 warps round-robin (each warp stages its chunk with cp.async into its own buffer).  Pass 1:
+// per-row max / sum, combined across warps in order -> lse; pass 2: P, dP = dOh V^T, dS and
+// dQ_h = dS K, reduced across warps in order.  Writes the head rows' (lse, D) and dQ.
+constexpr int kHeadWarps = 8;
+
+template <int NH>
+__global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int MT = NH / 16;
+  const int j = blockIdx.x, h = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const SeqGroups g = seq_groups(p.cu, p.qlen, j);
+  const int slen = g.len[0] + g.len[1] + g.len[2];
+  const int nhead = 1 + g.len[1];
+  const int hoff = h * 64;
+  const uint32_t sQ = smem_u32(smem), sdO = sQ + NH * ROWB;
+  const uint32_t sKw = sdO + NH * ROWB + warp * 2 * TILE * ROWB, sVw = sKw + TILE * ROWB;
+  float* red = reinterpret_cast<float*>(smem + (2 * NH + 2 * kHeadWarps * TILE) * ROWB);  // [warps][NH][2]
+  float* sD = red + kHeadWarps * NH * 2;                                                  // [NH]
+  float* sL = sD + NH;                                                                     // [NH] lse (log2)
+  float* red_o = sL + NH;                                                                  // [warps][NH][64]
+
+  stage_rows(sQ, NH, p.q, [&](int r) { return r < nhead ? p.q + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
+  stage_rows(sdO, NH, p.q, [&](int r) {
+    return r < nhead ? p.dout + (int64_t)(g.start + r) * p.ld_dout + hoff : nullptr; });
+  cp_async_wait_all();
+  __syncthreads();
+  // D_i = dO_i . O_i: eight threads per row
+  for (int r = threadIdx.x >> 3; r < NH; r += kHeadWarps * 4) {
+    const int part = threadIdx.x & 7;
+    float acc = 0.f;
+    if (r < nhead) {
+      const uint4 ov = *reinterpret_cast<const uint4*>(p.out + (int64_t)(g.start + r) * p.ld_out + hoff + part * 8);
+      uint4 gv;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(gv.x), "=r"(gv.y), "=r"(gv.z), "=r"(gv.w)
+                   : "r"(swz(sdO, r, part)));
+      const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 of = __bfloat1622float2(o2[e]), gf = __bfloat1622float2(g2[e]);
+        acc = fmaf(of.x, gf.x, fmaf(of.y, gf.y, acc));
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    if (part == 0) sD[r] = acc;
+  }
+
+  const int gq = lane >> 2, tq = lane & 3;
+  const float c2 = p.inv_scale * LOG2E;
+  uint32_t qa[MT][4][4];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) load_a(sQ, 16 * mt, lane, qa[mt]);
+  // row i (head slot) attends key t (sequence-relative)?
+  auto ok = [&](int i, int t) {
+    if (i >= nhead || t >= slen) return false;
+    const int gs = i == 0 ? 0 : 1, rs = i == 0 ? 0 : i - 1;
+    const int tg = t == 0 ? 0 : (t < 1 + g.len[1] ? 1 : 2), rt = t - g.off[tg];
+    return linked(p.links.w[gs][tg], rs, rt);
+  };
+  auto stage_chunk = [&](uint32_t buf, const __nv_bfloat16* base, int k0) {
+    for (int idx = lane; idx < TILE * 8; idx += 32) {
+      const int r = idx >> 3, c = idx & 7;
+      const bool in = k0 + r < slen;
+      cp_async16(swz(buf, r, c), in ? base + (int64_t)(g.start + k0 + r) * p.ld + hoff + c * 8 : p.q, in ? 16 : 0);
+    }
+    cp_async_wait_all();
+    __syncwarp();
+  };
+  const int nchunks = (slen + TILE - 1) / TILE;
+
+  // pass 1: per-row max and sum (rows 16 mt + gq and + 8 of each m-tile)
+  float m[MT][2], l[MT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) m[mt][0] = m[mt][1] = -INFINITY, l[mt][0] = l[mt][1] = 0.f;
+  for (int ch = warp; ch < nchunks; ch += kHeadWarps) {
+    const int k0 = ch * TILE;
+    stage_chunk(sKw, p.k, k0);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      float sv[8][4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sv[i][0] = sv[i][1] = sv[i][2] = sv[i][3] = 0.f;
+#pragma unroll
+      for (int kp = 0; kp < 4; ++kp) mm_nt16(sKw, 16 * kp, lane, qa[mt], sv[2 * kp], sv[2 * kp + 1]);
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int i = 16 * mt + gq + 8 * hr;
+        float cm = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int t = k0 + 8 * nt + 2 * tq + e;
+            sv[nt][2 * hr + e] = ok(i, t) ? sv[nt][2 * hr + e] * c2 : -INFINITY;
+            cm = fmaxf(cm, sv[nt][2 * hr + e]);
+          }
+        cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+        cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+        // (no early exit: the shuffles below need the whole warp)
+        const float mn = fmaxf(m[mt][hr], cm);
+        const float ms = mn == -INFINITY ? 0.f : mn;
+        float cs = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) cs += ex2(sv[nt][2 * hr] - ms) + ex2(sv[nt][2 * hr + 1] - ms);
+        cs += __shfl_xor_sync(0xffffffffu, cs, 1);
+        cs += __shfl_xor_sync(0xffffffffu, cs, 2);
+        if (cm != -INFINITY) {
+          l[mt][hr] = l[mt][hr] * (m[mt][hr] == -INFINITY ? 0.f : ex2(m[mt][hr] - mn)) + cs;
+          m[mt][hr] = mn;
+        }
+      }
+    }
+  }
+  if (tq == 0) {
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int i = 16 * mt + gq + 8 * hr;
+        red[(warp * NH + i) * 2] = m[mt][hr];
+        red[(warp * NH + i) * 2 + 1] = l[mt][hr];
+      }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NH; i += blockDim.x) {  // combine in warp order (+ zero-logit slots)
+    float mm = -INFINITY;
+    for (int w = 0; w < kHeadWarps; ++w) mm = fmaxf(mm, red[(w * NH + i) * 2]);
+    int n_inv = 0;
+    if (p.padding == SC_PAD_ZERO_LOGIT && i < nhead) {
+      const int gs = i == 0 ? 0 : 1, rs = i == 0 ? 0 : i - 1;
+      for (int t = 0; t < 3; ++t) {
+        const int wt = p.links.w[gs][t];
+        if (wt < 0) continue;
+        const int lo = max(0, rs - wt), hi = min(g.len[t], rs + wt + 1);
+        n_inv += (2 * wt + 1) - max(0, hi - lo);
+      }
+    }
+    if (n_inv > 0) mm = fmaxf(mm, 0.f);
+    float ll = 0.f;
+    for (int w = 0; w < kHeadWarps; ++w) {
+      const float mw = red[(w * NH + i) * 2];
+      if (mw != -INFINITY) ll += red[(w * NH + i) * 2 + 1] * ex2(mw - mm);
+    }
+    ll += n_inv * ex2(-mm);
+    const float lse2 = ll > 0.f ? mm + log2f(ll) : INFINITY;
+    sL[i] = lse2;
+    if (i < nhead) p.stats[(int64_t)(g.start + i) * p.H + h] = make_float2(lse2 * LN2, sD[i]);
+  }
+  __syncthreads();
+
+  // pass 2: dQ_h = sum_t dS_it K_t
+  uint32_t da[MT][4][4];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) load_a(sdO, 16 * mt, lane, da[mt]);
+  float o[MT][8][4];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[mt][i][0] = o[mt][i][1] = o[mt][i][2] = o[mt][i][3] = 0.f;
+  for (int ch = warp; ch < nchunks; ch += kHeadWarps) {
+    const int k0 = ch * TILE;
+    stage_chunk(sKw, p.k, k0);
+    stage_chunk(sVw, p.v, k0);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      float sv[8][4], dp[8][4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sv[i][e] = dp[i][e] = 0.f;
+#pragma unroll
+      for (int kp = 0; kp < 4; ++kp) {
+        mm_nt16(sKw, 16 * kp, lane, qa[mt], sv[2 * kp], sv[2 * kp + 1]);
+        mm_nt16(sVw, 16 * kp, lane, da[mt], dp[2 * kp], dp[2 * kp + 1]);
+      }
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+        const int i = 16 * mt + gq + 8 * hr;
+        const float lse2 = sL[i], Di = sD[i];
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int t = k0 + 8 * nt + 2 * tq + e;
+            const float pr = ok(i, t) ? ex2(sv[nt][2 * hr + e] * c2 - lse2) : 0.f;
+            sv[nt][2 * hr + e] = pr * (dp[nt][2 * hr + e] - Di) * p.inv_scale;
+          }
+      }
+#pragma unroll
+      for (int kp = 0; kp < 4; ++kp) mm_nn16(sKw, 16 * kp, lane, sv[2 * kp], sv[2 * kp + 1], o[mt]);
+    }
+  }
+  // reduce dQ over the warps in order
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const int c = 8 * nt + 2 * tq, i0 = 16 * mt + gq;
+      red_o[(warp * NH + i0) * 64 + c] = o[mt][nt][0];
+      red_o[(warp * NH + i0) * 64 + c + 1] = o[mt][nt][1];
+      red_o[(warp * NH + i0 + 8) * 64 + c] = o[mt][nt][2];
+      red_o[(warp * NH + i0 + 8) * 64 + c + 1] = o[mt][nt][3];
+    }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < NH * 64; idx += blockDim.x) {
+    const int i = idx >> 6, c = idx & 63;
+    if (i >= nhead) continue;
+    float acc = 0.f;
+    for (int w = 0; w < kHeadWarps; ++w) acc += red_o[(w * NH + i) * 64 + c];
+    p.dq[(int64_t)(g.start + i) * p.ld_grad + hoff + c] = acc;
+  }
+}
+
+template <int NH>
+size_t head_smem_bytes() {
+  return (size_t)(2 * NH + 2 * kHeadWarps * TILE) * ROWB +
+         (size_t)(kHeadWarps * NH * 2 + 2 * NH + kHeadWarps * NH * 64) * sizeof(float);
+}
+
+template <int NH>
+int launch_head(const Args& a, cudaStream_t st) {
+  const size_t sm = head_smem_bytes<NH>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(head_dq_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  head_dq_kernel<NH><<<dim3(a.nseq, a.H), kHeadWarps * 32, sm, st>>>(a);
+  SC_CHECK_LAUNCH("head_dq_kernel");
+  return SC_OK;
+}
+
 template <int NB, int NH>
 size_t smem_bytes() {
   return (size_t)(2 * TILE + 2 * (48 + NB) + 4 * NH) * ROWB + (48 + NB + NH) * sizeof(float2);
@@ -553,10 +791,12 @@ int launch_pair(const Args& a, int ntiles, int phase, cudaStream_t st) {
 
 }  // namespace bwdband
 
-// Doc-band phases of the fast path: 0 = kernel A (doc-row stats + dQ [+ head-key partials]),
-// 1 = kernel B (doc dK/dV), 2 = add the summed head-key partials into the head keys' dK/dV.
+// Phases of the fast path: 0 = kernel A (doc-row stats + dQ [+ head-key partials]),
+// 1 = kernel B (doc dK/dV), 2 = add the summed head-key partials into the head keys' dK/dV,
+// 3 = head rows' stats + dQ (tensor cores).
 int launch_attn_bwd_band(const BandBwdArgs& a, int ntiles, int max_head, int phase, cudaStream_t st) {
   using namespace bwdband;
+  if (phase == 3) return max_head <= 16 ? launch_head<16>(a, st) : launch_head<32>(a, st);
   const bool wide = a.w > 8;
   if (max_head <= 16) return wide ? launch_pair<64, 16>(a, ntiles, phase, st) : launch_pair<32, 16>(a, ntiles, phase, st);
   return wide ? launch_pair<64, 32>(a, ntiles, phase, st) : launch_pair<32, 32>(a, ntiles, phase, st);
