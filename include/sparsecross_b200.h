@@ -186,8 +186,10 @@ SC_API int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t row_
  * tok_flags/glob_cu/glob_pos, seq_tile_base/tile_rows (from sc_index_build)
  * and max_qgroup_len as in sc_attn_fwd (QDS pointers NULL without QDS).
  * bf16, head_dim 64, no QDS, a finite doc window <= 24, tile_rows 64 and
- * max_qgroup_len <= 31 take the tiled tensor-core path for the doc band
- * (one host read of the tile count); anything else the generic kernels.
+ * max_qgroup_len <= 31 take the tiled tensor-core path for the doc band;
+ * anything else the generic kernels.  n_tiles = seq_tile_base[nseq] when the
+ * caller knows it (then the call never synchronises and is CUDA-graph
+ * capturable), or -1 to read it from the device.
  * workspace: sc_attn_bwd_workspace_bytes(T, H, nseq, max_qgroup_len) bytes
  * (per-row softmax statistics + per-tile head-key partials of the tiled
  * path; T*H*8 bytes is the minimum).  head_dim <= 128. */
@@ -201,7 +203,7 @@ SC_API int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t row_
                 const int32_t* links, int32_t padding, float scale, int32_t dtype,
                 const uint8_t* tok_flags, const int32_t* glob_cu, const int32_t* glob_pos,
                 const int32_t* seq_tile_base, int32_t tile_rows, int32_t max_qgroup_len,
-                void* workspace, size_t workspace_bytes, void* stream);
+                int32_t n_tiles, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- Encoder-loop kernels (R/encoder.py:306-371, :475-509) -------------- */
 

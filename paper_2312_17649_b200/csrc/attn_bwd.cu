@@ -576,8 +576,8 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
                            int32_t nseq, int32_t total_tokens, int32_t heads, int32_t head_dim, const int32_t* links,
                            int32_t padding, float scale, int32_t dtype, const uint8_t* tok_flags,
                            const int32_t* glob_cu, const int32_t* glob_pos, const int32_t* seq_tile_base,
-                           int32_t tile_rows, int32_t max_qgroup_len, void* workspace, size_t workspace_bytes,
-                           void* stream) {
+                           int32_t tile_rows, int32_t max_qgroup_len, int32_t n_tiles, void* workspace,
+                           size_t workspace_bytes, void* stream) {
   BwdArgs b = {};
   AttnArgs& a = b.a;
   SC_CHECK_ARG(load_links(links, &a.links), "sc_attn_bwd: bad links");
@@ -626,9 +626,10 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
   const size_t soff = (stats_bytes(total_tokens, heads) + 255) & ~(size_t)255;
   if (workspace_bytes >= soff + part_bytes(total_tokens, heads, nseq, max_qgroup_len))
     p.head_part = reinterpret_cast<float*>(static_cast<char*>(workspace) + soff);
-  int ntiles = 0;
-  if (cudaMemcpyAsync(&ntiles, seq_tile_base + nseq, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-      cudaStreamSynchronize(st) != cudaSuccess) {
+  int ntiles = n_tiles;
+  if (ntiles < 0 && (cudaMemcpyAsync(&ntiles, seq_tile_base + nseq, sizeof(int), cudaMemcpyDeviceToHost, st) !=
+                         cudaSuccess ||
+                     cudaStreamSynchronize(st) != cudaSuccess)) {
     set_error("sc_attn_bwd: reading the tile count failed");
     return SC_ERR_CUDA;
   }

@@ -63,6 +63,8 @@ class PackedLayout:
         self.seq_tile_base = torch.empty(self.nseq + 1, **i32)
         self.seq_head_base = torch.empty(self.nseq + 1, **i32)
         self.max_qgroup_len = int(self.qlen_host.max())
+        # doc tiles of tile_rows rows over all sequences (host copy of seq_tile_base[nseq])
+        self.n_tiles = int(((self.group_lens_host[:, 2] + self.tile_rows - 1) // self.tile_rows).sum())
         self.tok_flags = self.glob_cu = self.glob_pos = None
         if self.qds_every or qds_positions is not None:
             self.tok_flags = torch.zeros(T, dtype=torch.uint8, device=dev)

@@ -117,7 +117,7 @@ def attention_backward(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor,
         float(scale), _lib.DTYPE_BF16 if qkv.dtype == torch.bfloat16 else _lib.DTYPE_F32,
         _lib.ptr(layout.tok_flags) if qds else None, _lib.ptr(layout.glob_cu) if qds else None,
         _lib.ptr(layout.glob_pos) if qds else None, layout.seq_tile_base.data_ptr(), layout.tile_rows,
-        layout.max_qgroup_len, ws.data_ptr(), ws_bytes, _lib.stream_handle(),
+        layout.max_qgroup_len, layout.n_tiles, ws.data_ptr(), ws_bytes, _lib.stream_handle(),
         exc=AttentionError,
     )
 
@@ -288,6 +288,14 @@ class ParamDict(dict):
                 self.shadow.copy_(self.flat)
             self.shadow_version = self.flat._version
         return self.shadow_views
+
+
+class GradDict(dict):
+    """Gradients that are views of one flat fp32 buffer in ParamDict order (``flat``)."""
+
+    def __init__(self, flat: torch.Tensor):
+        super().__init__()
+        self.flat = flat
 
 
 class TrainableCrossEncoder:
@@ -556,7 +564,11 @@ class AdamW:
 
     def _fused_step(self, weights: ParamDict, grads: dict, lr_t: float, t: int) -> None:
         flat = weights.flat
-        g = torch.cat([torch.as_tensor(grads[n], device=flat.device).reshape(-1).float() for n in weights.order])
+        gf = getattr(grads, "flat", None)
+        if gf is not None and gf.numel() == flat.numel() and gf.dtype == torch.float32:
+            g = gf
+        else:
+            g = torch.cat([torch.as_tensor(grads[n], device=flat.device).reshape(-1).float() for n in weights.order])
         if self._m.get("__flat__") is None:
             self._m["__flat__"] = torch.zeros_like(flat)
             self._v["__flat__"] = torch.zeros_like(flat)
@@ -734,6 +746,72 @@ def train_step(model: TrainableCrossEncoder, opt: AdamW, triples, loss: str = "m
     grads = {n: (torch.zeros_like(model.weights[n]) if g is None else g) for n, g in zip(names, gr)}
     opt.step(model.weights, grads)
     return value
+
+
+class GraphedTrainStep:
+    """One fine-tuning step (forward, loss, backward) captured as a CUDA graph for a fixed batch
+    shape, plus the fused AdamW update outside the graph (its step-dependent scalars change).
+
+    The packed layout, the static id / teacher buffers and every intermediate live in the
+    graph's memory pool; each call copies new ids (and teacher margins) in, replays, and
+    applies AdamW.  Margin-MSE or RankNet loss, as in ``train_step``.
+    """
+
+    def __init__(self, model: TrainableCrossEncoder, opt: AdamW, batch: PackedBatch, loss: str = "margin_mse",
+                 warmup: int = 2):
+        if loss not in LOSSES:
+            raise TrainingError(f"unknown loss {loss!r}; expected one of {LOSSES}")
+        if batch.nseq % 2:
+            raise TrainingError("a training batch holds positives then negatives (even nseq)")
+        self.model, self.opt, self.loss = model, opt, loss
+        self.layout = model.make_layout(batch)
+        self.ids = to_device(batch.ids, model.device)
+        self.teacher_gap = torch.zeros(batch.nseq // 2, dtype=torch.float64, device=model.device)
+        self.names = sorted(model.weights)
+        W = model.weights
+        if isinstance(W, ParamDict):
+            W.bf16_views()  # sync the shadow before capture
+        side = torch.cuda.Stream(device=model.device)
+        side.wait_stream(torch.cuda.current_stream(model.device))
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self._fwd_bwd()
+        torch.cuda.current_stream(model.device).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.loss_value, self.grad_flat = self._fwd_bwd()
+
+    def _fwd_bwd(self):
+        m = self.model
+        s = m.score_packed(self.ids, self.layout, check_finite=False)
+        b = s.shape[0] // 2
+        delta = s[:b].double() - s[b:].double()
+        if self.loss == "margin_mse":
+            gap = delta - self.teacher_gap
+            lt = torch.mean(gap * gap)
+        else:
+            lt = torch.mean(torch.logaddexp(torch.zeros_like(delta), -delta))
+        with m.gemm_mode():
+            gr = torch.autograd.grad(lt, [m.weights[n] for n in self.names], allow_unused=True)
+        flat = torch.cat([(torch.zeros_like(m.weights[n]) if g is None else g).reshape(-1).float()
+                          for n, g in zip(self.names, gr)])
+        return lt.detach(), flat
+
+    def __call__(self, ids, teacher_gap=None) -> torch.Tensor:
+        """One step on new ids of the captured shape; returns the loss (device scalar, float64)."""
+        src = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)) if isinstance(ids, np.ndarray) else ids
+        self.ids.copy_(src, non_blocking=True)
+        if teacher_gap is not None:
+            self.teacher_gap.copy_(torch.as_tensor(teacher_gap, dtype=torch.float64), non_blocking=True)
+        self.graph.replay()
+        W = self.model.weights
+        grads, off = GradDict(self.grad_flat), 0
+        for n in self.names:  # == ParamDict.order (sorted names)
+            k = W[n].numel()
+            grads[n] = self.grad_flat[off:off + k].view(W[n].shape)
+            off += k
+        self.opt.step(W, grads)
+        return self.loss_value
 
 
 def train_toy(config: EncoderConfig, dataset, steps: int, lr: float, seed: int = 0, batch_pairs: int = 16,

@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--layers", type=int, default=12)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--graph", action="store_true", help="CUDA-graph forward+backward (GraphedTrainStep)")
     a = ap.parse_args()
     w = math.inf if a.window == math.inf else int(a.window)
     s = a.query_len + a.doc_len + 3
@@ -56,8 +57,29 @@ def main():
     teacher = torch.randn(n, device="cuda", dtype=torch.float64)
     names = sorted(model.weights)
 
+    graphed = None
+    if a.graph:
+        graphed = TR.GraphedTrainStep(model, opt, batch)
+        gap = (teacher[:a.pairs] - teacher[a.pairs:]).cpu().numpy()
+
     def step(times=None):
         e = [ev() for _ in range(4)]
+        if graphed is not None:
+            e[0].record()
+            graphed.graph.replay()
+            e[1].record()
+            e[2].record()
+            W = model.weights
+            grads, off = TR.GradDict(graphed.grad_flat), 0
+            for n in names:
+                k = W[n].numel()
+                grads[n] = graphed.grad_flat[off:off + k].view(W[n].shape)
+                off += k
+            opt.step(W, grads)
+            e[3].record()
+            if times is not None:
+                times.append(e)
+            return
         e[0].record()
         scores = model.score_packed(ids_dev, layout, check_finite=False)
         gap = (scores[:a.pairs].double() - scores[a.pairs:].double()) - (teacher[:a.pairs] - teacher[a.pairs:])
@@ -110,7 +132,7 @@ def main():
     es = qkv.element_size()
     bytes_bwd = T * hd * (5 * es + 3 * 4) + T * cfg.heads * 8  # q,k,v,o,dO in; dq,dk,dv fp32 out; stats
     print(json.dumps({
-        "metric": "finetune_step", "tokens": T, "pairs": a.pairs, "seq_len": s, "pattern": a.pattern,
+        "metric": "finetune_step", "graph": a.graph, "tokens": T, "pairs": a.pairs, "seq_len": s, "pattern": a.pattern,
         "window": a.window, "precision": a.precision, "layers": a.layers,
         "ms_step": total, "ms_forward": fwd, "ms_backward": bwd, "ms_adamw": optm,
         "tokens_per_s": T / total * 1e3, "pairs_per_s": n / total * 1e3,

@@ -446,3 +446,29 @@ def test_linear_gelu_vs_torch(P, dt, tol):
     close(x.grad.cpu().numpy(), x64.grad.cpu().numpy(), tol)
     close(w.grad.cpu().numpy(), w64.grad.cpu().numpy(), tol)
     close(b.grad.cpu().numpy(), b64.grad.cpu().numpy(), tol)
+
+
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+def test_graphed_train_step_matches_eager(P, precision):
+    """GraphedTrainStep (CUDA-graph forward+backward, fused AdamW) == eager train_step."""
+    from paper_2312_17649_b200.training import GraphedTrainStep, _batch_arrays, train_step
+
+    task = P.SyntheticTask(**TASK_KW)
+    cfg = task_cfg(P, "sparse", 2, precision=precision)
+    rng = np.random.default_rng(0)
+    batches = [[task.sample_triple(rng) for _ in range(4)] for _ in range(3)]
+    m1 = P.TrainableCrossEncoder(cfg, seed=0)
+    o1 = P.AdamW(1e-3)
+    eager = [train_step(m1, o1, b) for b in batches]
+    m2 = P.TrainableCrossEncoder(cfg, seed=0)
+    o2 = P.AdamW(1e-3)
+    ids, part = _batch_arrays(batches[0], cfg.max_positions)
+    g = GraphedTrainStep(m2, o2, P.PackedBatch.from_ids(ids, part), warmup=0)
+    graphed = []
+    for b in batches:
+        ids, part = _batch_arrays(b, cfg.max_positions)
+        gap = np.array([t.teacher_pos - t.teacher_neg for t in b])
+        graphed.append(float(g(ids.reshape(-1), gap)))
+    np.testing.assert_allclose(graphed, eager, rtol=1e-6)
+    for n in m1.weights:
+        torch.testing.assert_close(m2.weights[n], m1.weights[n], rtol=1e-5, atol=1e-6)
