@@ -729,8 +729,10 @@ def _loss_tensor(name, scores, triples):
 
 
 def train_step(model: TrainableCrossEncoder, opt: AdamW, triples, loss: str = "margin_mse",
-               step: int | None = None) -> float:
-    """One optimisation step on a batch of triples; returns the loss value."""
+               step: int | None = None, process_group=None) -> float:
+    """One optimisation step on a batch of triples; returns the loss value.  Under
+    torch.distributed with ``process_group`` (or the default group) set up, each rank passes its
+    own triples and the gradients are averaged before the update (data parallel)."""
     ids, partition = _batch_arrays(triples, model.config.max_positions)
     ids = model._check_ids(ids, partition)
     batch = PackedBatch.from_ids(ids, partition)
@@ -744,8 +746,46 @@ def train_step(model: TrainableCrossEncoder, opt: AdamW, triples, loss: str = "m
     with model.gemm_mode():
         gr = torch.autograd.grad(lt, [model.weights[n] for n in names], allow_unused=True)
     grads = {n: (torch.zeros_like(model.weights[n]) if g is None else g) for n, g in zip(names, gr)}
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(process_group) > 1:
+        grads = flat_gradients(model, grads)
+        allreduce_gradients(grads, process_group)
     opt.step(model.weights, grads)
     return value
+
+
+def allreduce_gradients(grads, group=None) -> None:
+    """Data-parallel fine-tuning: average the gradients over the ranks of `group`, in place.
+
+    One collective on the flat fp32 buffer when the gradients are a ``GradDict`` (NCCL over
+    NVLink on the GPU; any torch.distributed backend works), else one per tensor.  Every rank
+    then applies the same AdamW update to identical weights.
+    """
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return
+    world = dist.get_world_size(group)
+    if world == 1:
+        return
+    flat = getattr(grads, "flat", None)
+    tensors = [flat] if flat is not None else [g for g in grads.values() if torch.is_tensor(g)]
+    for t in tensors:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        t.div_(world)
+
+
+def flat_gradients(model: "TrainableCrossEncoder", grads_by_name: dict) -> "GradDict":
+    """Copy per-tensor gradients into one flat fp32 buffer in ParamDict order."""
+    names = sorted(model.weights)
+    flat = torch.cat([grads_by_name[n].reshape(-1).float() for n in names])
+    out, off = GradDict(flat), 0
+    for n in names:
+        k = model.weights[n].numel()
+        out[n] = flat[off:off + k].view(model.weights[n].shape)
+        off += k
+    return out
 
 
 class GraphedTrainStep:
@@ -758,12 +798,13 @@ class GraphedTrainStep:
     """
 
     def __init__(self, model: TrainableCrossEncoder, opt: AdamW, batch: PackedBatch, loss: str = "margin_mse",
-                 warmup: int = 2):
+                 warmup: int = 2, process_group=None):
         if loss not in LOSSES:
             raise TrainingError(f"unknown loss {loss!r}; expected one of {LOSSES}")
         if batch.nseq % 2:
             raise TrainingError("a training batch holds positives then negatives (even nseq)")
         self.model, self.opt, self.loss = model, opt, loss
+        self.process_group = process_group  # data parallel: gradients averaged over its ranks
         self.layout = model.make_layout(batch)
         self.ids = to_device(batch.ids, model.device)
         self.teacher_gap = torch.zeros(batch.nseq // 2, dtype=torch.float64, device=model.device)
@@ -810,6 +851,7 @@ class GraphedTrainStep:
             k = W[n].numel()
             grads[n] = self.grad_flat[off:off + k].view(W[n].shape)
             off += k
+        allreduce_gradients(grads, self.process_group)
         self.opt.step(W, grads)
         return self.loss_value
 

@@ -86,3 +86,45 @@ def test_trec_run_roundtrip(tmp_path):
     assert parse_run(format_run(entries).splitlines()) == entries
     with pytest.raises(ValueError):
         parse_run(["q1 Q0 d1 1 0.5"])
+
+
+def _dp_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2312_17649_b200.training import AdamW, GradDict, allreduce_gradients
+
+    # every rank: the same weights, its own gradients; after the all-reduce every rank holds the
+    # mean and applies the same AdamW update
+    w = {"a": torch.arange(6, dtype=torch.float64).reshape(2, 3) / 10, "b": torch.ones(4, dtype=torch.float64)}
+    opt = AdamW(0.1, weight_decay=0.01, moment_dtype=torch.float64)
+    for step in range(3):
+        gen = torch.Generator().manual_seed(100 * step + rank)
+        flat = torch.randn(10, dtype=torch.float64, generator=gen)
+        g = GradDict(flat)
+        g["a"], g["b"] = flat[:6].view(2, 3), flat[6:]
+        allreduce_gradients(g)
+        opt.step(w, g)
+    torch.save({k: v.clone() for k, v in w.items()}, f"{out_path}.{rank}")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_data_parallel_gradient_average_gloo(tmp_path):
+    from paper_2312_17649_b200.training import AdamW
+
+    world, port = 2, _free_port()
+    out = str(tmp_path / "w")
+    mp.spawn(_dp_worker, args=(world, port, out), nprocs=world, join=True)
+    got = [torch.load(f"{out}.{r}") for r in range(world)]
+    # single-process reference on the mean gradient
+    w = {"a": torch.arange(6, dtype=torch.float64).reshape(2, 3) / 10, "b": torch.ones(4, dtype=torch.float64)}
+    opt = AdamW(0.1, weight_decay=0.01, moment_dtype=torch.float64)
+    for step in range(3):
+        fl = sum(torch.randn(10, dtype=torch.float64, generator=torch.Generator().manual_seed(100 * step + r))
+                 for r in range(world)) / world
+        opt.step(w, {"a": fl[:6].view(2, 3), "b": fl[6:]})
+    for r in range(world):
+        for k in w:
+            assert torch.equal(got[r][k], got[0][k])
+            torch.testing.assert_close(got[r][k], w[k], rtol=1e-12, atol=1e-12)
