@@ -352,18 +352,16 @@ class TrainableCrossEncoder:
     def hidden_packed(self, ids_dev: torch.Tensor, layout: PackedLayout, check_finite: bool = True) -> torch.Tensor:
         """Final-layer activations [T, h] with the autograd graph (R/encoder.py:475-500)."""
         cfg, W = self.config, self.weights
-        h, H = cfg.embed_dim, cfg.heads
+        H = cfg.heads
         bf16 = cfg.precision == "bf16"
         scale = math.sqrt(cfg.head_dim)
         x = W["tok_emb"][ids_dev.long()] + W["pos_emb"][layout.tok_pos.long()]
         cd = torch.bfloat16 if bf16 else torch.float32
         S = W.bf16_views() if (bf16 and isinstance(W, ParamDict)) else None
 
-        def lin(xin, wname, bname, w=None, w16=None):
-            w = W[wname] if w is None else w
-            if S is not None and w16 is None:
-                w16 = S[wname]
-            return Linear.apply(xin, w, w16, W[bname], None if S is None else S[bname], cd)
+        def lin(xin, wname, bname):
+            return Linear.apply(xin, W[wname], None if S is None else S[wname], W[bname],
+                                None if S is None else S[bname], cd)
 
         flags = []
         xh = x  # GEMM input of the layer (bf16 copy of the previous LayerNorm in the bf16 path)
