@@ -61,6 +61,9 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int sr
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // A fragments (16 rows x 64 dims) of the block starting at smem row `row0`.
 __device__ __forceinline__ void load_a(uint32_t buf, int row0, int lane, uint32_t (&a)[4][4]) {
@@ -129,44 +132,23 @@ __global__ void __launch_bounds__(128) band_dq_kernel(Args p) {
                  sKH = sV + KR * ROWB, sVH = sKH + NH * ROWB, sPT = sVH + NH * ROWB, sST = sPT + NH * ROWB;
   float* sD = reinterpret_cast<float*>(smem + (2 * TILE + 2 * KR + 4 * NH) * ROWB);
 
+  // two cp.async groups: what S needs (Q, K band, head keys), then what dP needs (dO, V band,
+  // head values) -- the second lands while the first is being used
   stage_rows(sQ, TILE, p.q, [&](int r) {
     return r0 + r < dlen ? p.q + (int64_t)(dstart + r0 + r) * p.ld + hoff : nullptr; });
-  stage_rows(sdO, TILE, p.q, [&](int r) {
-    return r0 + r < dlen ? p.dout + (int64_t)(dstart + r0 + r) * p.ld_dout + hoff : nullptr; });
   stage_rows(sK, KR, p.q, [&](int r) {
     const int pos = r0 - w + r;
     return pos >= 0 && pos < dlen ? p.k + (int64_t)(dstart + pos) * p.ld + hoff : nullptr; });
+  stage_rows(sKH, NH, p.q, [&](int r) { return r < nhead ? p.k + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
+  cp_async_commit();
+  stage_rows(sdO, TILE, p.q, [&](int r) {
+    return r0 + r < dlen ? p.dout + (int64_t)(dstart + r0 + r) * p.ld_dout + hoff : nullptr; });
   stage_rows(sV, KR, p.q, [&](int r) {
     const int pos = r0 - w + r;
     return pos >= 0 && pos < dlen ? p.v + (int64_t)(dstart + pos) * p.ld + hoff : nullptr; });
-  stage_rows(sKH, NH, p.q, [&](int r) { return r < nhead ? p.k + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
   stage_rows(sVH, NH, p.q, [&](int r) { return r < nhead ? p.v + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
-  cp_async_wait_all();
-  __syncthreads();
-  {  // D_i = dO_i . O_i, two threads per row
-    const int r = threadIdx.x >> 1, half = threadIdx.x & 1;
-    float acc = 0.f;
-    if (r0 + r < dlen) {
-      const __nv_bfloat16* orow = p.out + (int64_t)(dstart + r0 + r) * p.ld_out + hoff + half * 32;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint4 ov = *reinterpret_cast<const uint4*>(orow + c * 8);
-        uint4 gv;
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(gv.x), "=r"(gv.y), "=r"(gv.z), "=r"(gv.w)
-                     : "r"(swz(sdO, r, half * 4 + c)));
-        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
-        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 of = __bfloat1622float2(o2[e]), gf = __bfloat1622float2(g2[e]);
-          acc = fmaf(of.x, gf.x, fmaf(of.y, gf.y, acc));
-        }
-      }
-    }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    if (half == 0) sD[r] = acc;
-  }
+  cp_async_commit();
+  cp_async_wait_group<1>();
   __syncthreads();
 
   const int gq = lane >> 2, tq = lane & 3;
@@ -257,6 +239,33 @@ __global__ void __launch_bounds__(128) band_dq_kernel(Args p) {
   lA += nA * ex2(-mAs);
   lB += nB * ex2(-mBs);
   const float iA = lA > 0.f ? 1.f / lA : 0.f, iB = lB > 0.f ? 1.f / lB : 0.f;
+  cp_async_wait_group<0>();
+  __syncthreads();
+  {  // D_i = dO_i . O_i, two threads per row
+    const int r = threadIdx.x >> 1, half = threadIdx.x & 1;
+    float acc = 0.f;
+    if (r0 + r < dlen) {
+      const __nv_bfloat16* orow = p.out + (int64_t)(dstart + r0 + r) * p.ld_out + hoff + half * 32;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint4 ov = *reinterpret_cast<const uint4*>(orow + c * 8);
+        uint4 gv;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(gv.x), "=r"(gv.y), "=r"(gv.z), "=r"(gv.w)
+                     : "r"(swz(sdO, r, half * 4 + c)));
+        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 of = __bfloat1622float2(o2[e]), gf = __bfloat1622float2(g2[e]);
+          acc = fmaf(of.x, gf.x, fmaf(of.y, gf.y, acc));
+        }
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (half == 0) sD[r] = acc;
+  }
+  __syncthreads();
   const float DA = sD[ra], DB = sD[ra + 8];
   if (tq == 0) {
     if (rsA < dlen)
@@ -398,17 +407,19 @@ __global__ void __launch_bounds__(128) band_dkv_kernel(Args p) {
 
   stage_rows(sK, TILE, p.q, [&](int r) {
     return k0 + r < dlen ? p.k + (int64_t)(dstart + k0 + r) * p.ld + hoff : nullptr; });
-  stage_rows(sV, TILE, p.q, [&](int r) {
-    return k0 + r < dlen ? p.v + (int64_t)(dstart + k0 + r) * p.ld + hoff : nullptr; });
   stage_rows(sQ, KR, p.q, [&](int r) {
     const int pos = k0 - w + r;
     return pos >= 0 && pos < dlen ? p.q + (int64_t)(dstart + pos) * p.ld + hoff : nullptr; });
+  stage_rows(sQH, NH, p.q, [&](int r) { return r < nhead ? p.q + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
+  cp_async_commit();
+  stage_rows(sV, TILE, p.q, [&](int r) {
+    return k0 + r < dlen ? p.v + (int64_t)(dstart + k0 + r) * p.ld + hoff : nullptr; });
   stage_rows(sdO, KR, p.q, [&](int r) {
     const int pos = k0 - w + r;
     return pos >= 0 && pos < dlen ? p.dout + (int64_t)(dstart + pos) * p.ld_dout + hoff : nullptr; });
-  stage_rows(sQH, NH, p.q, [&](int r) { return r < nhead ? p.q + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
   stage_rows(sdOH, NH, p.q, [&](int r) {
     return r < nhead ? p.dout + (int64_t)(g.start + r) * p.ld_dout + hoff : nullptr; });
+  cp_async_commit();
   for (int r = threadIdx.x; r < KR + NH; r += blockDim.x) {
     float2 st = make_float2(INFINITY, 0.f);
     if (r < KR) {
@@ -420,7 +431,7 @@ __global__ void __launch_bounds__(128) band_dkv_kernel(Args p) {
     st.x *= LOG2E;  // lse in log2 units
     sSt[r] = st;
   }
-  cp_async_wait_all();
+  cp_async_wait_group<1>();
   __syncthreads();
 
   const int gq = lane >> 2, tq = lane & 3;
@@ -461,6 +472,8 @@ __global__ void __launch_bounds__(128) band_dkv_kernel(Args p) {
       sh[i][e] = ok ? ex2(sh[i][e] * c2 - sSt[KR + sl].x) : 0.f;
     }
 
+  cp_async_wait_group<0>();
+  __syncthreads();
   // dV = P^T dO
   float dv[8][4];
 #pragma unroll
