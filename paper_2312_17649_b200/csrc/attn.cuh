@@ -48,6 +48,9 @@ struct BandBwdArgs {
   int padding;
   float inv_scale;
   float* head_part;               // [tiles][H][2][NH][64] per-tile head-key dV / dK partials, or nullptr
+  // head-row pass split over key ranges (head_ks > 1): per (seq, head, split) (m, l) and dQ partials
+  float* head_split;              // [nseq][H][head_ks][NH][2 + 64]
+  int head_ks, head_phase;
 };
 // phase 0: doc-row statistics + dQ (+ head-key partials); 1: doc-key dK / dV; 2: head-key partial
 // reduction; 3: head-row statistics + dQ.  max_head = 1 + max qgroup_len (<= 32); NH = 16 when max_head <= 16, else 32.

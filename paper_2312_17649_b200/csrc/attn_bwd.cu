@@ -20,6 +20,8 @@
 // discarded by the reference, R/attention.py:461-470, :488-493).
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "attn.cuh"
 
 namespace sc {
@@ -564,10 +566,16 @@ static size_t part_bytes(int32_t total_tokens, int32_t heads, int32_t nseq, int3
   return tiles * (size_t)(heads > 0 ? heads : 0) * 2 * nh * 64 * sizeof(float);
 }
 
+// Head-row pass split over key ranges: nseq x H x kMaxHeadSplit x 32 rows x (m, l, dq[64]).
+constexpr int kMaxHeadSplit = 8;
+static size_t split_bytes(int32_t heads, int32_t nseq) {
+  return (size_t)(nseq > 0 ? nseq : 0) * (heads > 0 ? heads : 0) * kMaxHeadSplit * 32 * 66 * sizeof(float);
+}
+
 extern "C" size_t sc_attn_bwd_workspace_bytes(int32_t total_tokens, int32_t heads, int32_t nseq,
                                               int32_t max_qgroup_len) {
   return ((stats_bytes(total_tokens, heads) + 255) & ~(size_t)255) +
-         part_bytes(total_tokens, heads, nseq, max_qgroup_len);
+         ((part_bytes(total_tokens, heads, nseq, max_qgroup_len) + 255) & ~(size_t)255) + split_bytes(heads, nseq);
 }
 
 extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t row_stride, const void* out,
@@ -624,8 +632,20 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
   p.links = a.links; p.padding = padding; p.inv_scale = 1.f / scale;
   // head-key partials when the workspace has room (else the generic head-key pass sums doc sources)
   const size_t soff = (stats_bytes(total_tokens, heads) + 255) & ~(size_t)255;
-  if (workspace_bytes >= soff + part_bytes(total_tokens, heads, nseq, max_qgroup_len))
+  const size_t pbytes = (part_bytes(total_tokens, heads, nseq, max_qgroup_len) + 255) & ~(size_t)255;
+  if (workspace_bytes >= soff + pbytes)
     p.head_part = reinterpret_cast<float*>(static_cast<char*>(workspace) + soff);
+  // head-row pass: split each (sequence, head)'s keys over CTAs when there are too few of them
+  p.head_ks = 1;
+  if (workspace_bytes >= soff + pbytes + split_bytes(heads, nseq)) {
+    p.head_split = reinterpret_cast<float*>(static_cast<char*>(workspace) + soff + pbytes);
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int items = nseq * heads;
+    const int want = (2 * sms + items - 1) / items;
+    const int by_len = (int)((int64_t)total_tokens / nseq / 64 / 8);  // >= one 64-key chunk per warp
+    p.head_ks = std::max(1, std::min({kMaxHeadSplit, want, by_len}));
+  }
   int ntiles = n_tiles;
   if (ntiles < 0 && (cudaMemcpyAsync(&ntiles, seq_tile_base + nseq, sizeof(int), cudaMemcpyDeviceToHost, st) !=
                          cudaSuccess ||

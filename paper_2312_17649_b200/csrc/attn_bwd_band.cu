@@ -534,7 +534,11 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
   float m[MT][2], l[MT][2];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) m[mt][0] = m[mt][1] = -INFINITY, l[mt][0] = l[mt][1] = 0.f;
-  for (int ch = warp; ch < nchunks; ch += kHeadWarps) {
+  const int KS = p.head_ks, ks = blockIdx.z;
+  const bool split = KS > 1;
+  float* part = split ? p.head_split + (((int64_t)j * p.H + h) * KS) * NH * 66 : nullptr;  // [KS][NH][66]
+  if (!split || p.head_phase == 1)
+  for (int ch = warp + kHeadWarps * ks; ch < nchunks; ch += kHeadWarps * KS) {
     const int k0 = ch * TILE;
     stage_chunk(sKw, p.k, k0);
 #pragma unroll
@@ -585,8 +589,25 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
   }
   __syncthreads();
   for (int i = threadIdx.x; i < NH; i += blockDim.x) {  // combine in warp order (+ zero-logit slots)
-    float mm = -INFINITY;
-    for (int w = 0; w < kHeadWarps; ++w) mm = fmaxf(mm, red[(w * NH + i) * 2]);
+    float mm = -INFINITY, ll = 0.f;
+    if (!split || p.head_phase == 1) {
+      for (int w = 0; w < kHeadWarps; ++w) mm = fmaxf(mm, red[(w * NH + i) * 2]);
+      for (int w = 0; w < kHeadWarps; ++w) {
+        const float mw = red[(w * NH + i) * 2];
+        if (mw != -INFINITY) ll += red[(w * NH + i) * 2 + 1] * ex2(mw - mm);
+      }
+      if (split) {  // phase 1: this split's (m, l)
+        part[((int64_t)ks * NH + i) * 66] = mm;
+        part[((int64_t)ks * NH + i) * 66 + 1] = ll;
+        continue;
+      }
+    } else {  // phase 2: combine the splits in order
+      for (int u = 0; u < KS; ++u) mm = fmaxf(mm, part[((int64_t)u * NH + i) * 66]);
+      for (int u = 0; u < KS; ++u) {
+        const float mu = part[((int64_t)u * NH + i) * 66];
+        if (mu != -INFINITY) ll += part[((int64_t)u * NH + i) * 66 + 1] * ex2(mu - mm);
+      }
+    }
     int n_inv = 0;
     if (p.padding == SC_PAD_ZERO_LOGIT && i < nhead) {
       const int gs = i == 0 ? 0 : 1, rs = i == 0 ? 0 : i - 1;
@@ -597,17 +618,16 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
         n_inv += (2 * wt + 1) - max(0, hi - lo);
       }
     }
-    if (n_inv > 0) mm = fmaxf(mm, 0.f);
-    float ll = 0.f;
-    for (int w = 0; w < kHeadWarps; ++w) {
-      const float mw = red[(w * NH + i) * 2];
-      if (mw != -INFINITY) ll += red[(w * NH + i) * 2 + 1] * ex2(mw - mm);
+    if (n_inv > 0) {
+      const float mn = fmaxf(mm, 0.f);
+      ll = (mm == -INFINITY ? 0.f : ll * ex2(mm - mn)) + n_inv * ex2(-mn);
+      mm = mn;
     }
-    ll += n_inv * ex2(-mm);
     const float lse2 = ll > 0.f ? mm + log2f(ll) : INFINITY;
     sL[i] = lse2;
-    if (i < nhead) p.stats[(int64_t)(g.start + i) * p.H + h] = make_float2(lse2 * LN2, sD[i]);
+    if (i < nhead && ks == 0) p.stats[(int64_t)(g.start + i) * p.H + h] = make_float2(lse2 * LN2, sD[i]);
   }
+  if (split && p.head_phase == 1) return;
   __syncthreads();
 
   // pass 2: dQ_h = sum_t dS_it K_t
@@ -619,7 +639,7 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
   for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
     for (int i = 0; i < 8; ++i) o[mt][i][0] = o[mt][i][1] = o[mt][i][2] = o[mt][i][3] = 0.f;
-  for (int ch = warp; ch < nchunks; ch += kHeadWarps) {
+  for (int ch = warp + kHeadWarps * ks; ch < nchunks; ch += kHeadWarps * KS) {
     const int k0 = ch * TILE;
     stage_chunk(sKw, p.k, k0);
     stage_chunk(sVw, p.v, k0);
@@ -669,8 +689,27 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
     if (i >= nhead) continue;
     float acc = 0.f;
     for (int w = 0; w < kHeadWarps; ++w) acc += red_o[(w * NH + i) * 64 + c];
-    p.dq[(int64_t)(g.start + i) * p.ld_grad + hoff + c] = acc;
+    if (split) part[((int64_t)ks * NH + i) * 66 + 2 + c] = acc;
+    else p.dq[(int64_t)(g.start + i) * p.ld_grad + hoff + c] = acc;
   }
+}
+
+// Head-row dQ = sum of the splits' partials, in split order.
+template <int NH>
+__global__ void __launch_bounds__(256) head_split_reduce_kernel(Args p) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (int)(idx & 63);
+  int64_t r = idx >> 6;
+  const int i = (int)(r % NH);
+  r /= NH;
+  const int h = (int)(r % p.H), j = (int)(r / p.H);
+  if (j >= p.nseq) return;
+  const SeqGroups g = seq_groups(p.cu, p.qlen, j);
+  if (i >= 1 + g.len[1]) return;
+  const float* part = p.head_split + (((int64_t)j * p.H + h) * p.head_ks) * NH * 66;
+  float acc = 0.f;
+  for (int u = 0; u < p.head_ks; ++u) acc += part[((int64_t)u * NH + i) * 66 + 2 + c];
+  p.dq[(int64_t)(g.start + i) * p.ld_grad + h * 64 + c] = acc;
 }
 
 template <int NH>
@@ -687,8 +726,25 @@ int launch_head(const Args& a, cudaStream_t st) {
     cudaFuncSetAttribute(head_dq_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
-  head_dq_kernel<NH><<<dim3(a.nseq, a.H), kHeadWarps * 32, sm, st>>>(a);
+  if (a.head_ks <= 1 || !a.head_split) {
+    Args b = a;
+    b.head_ks = 1;
+    head_dq_kernel<NH><<<dim3(a.nseq, a.H, 1), kHeadWarps * 32, sm, st>>>(b);
+    SC_CHECK_LAUNCH("head_dq_kernel");
+    return SC_OK;
+  }
+  // key ranges split over head_ks CTAs per (sequence, head): (m, l) partials, then dQ partials
+  // with the combined lse, then the ordered sum
+  Args b = a;
+  b.head_phase = 1;
+  head_dq_kernel<NH><<<dim3(a.nseq, a.H, a.head_ks), kHeadWarps * 32, sm, st>>>(b);
   SC_CHECK_LAUNCH("head_dq_kernel");
+  b.head_phase = 2;
+  head_dq_kernel<NH><<<dim3(a.nseq, a.H, a.head_ks), kHeadWarps * 32, sm, st>>>(b);
+  SC_CHECK_LAUNCH("head_dq_kernel");
+  const int64_t n = (int64_t)a.nseq * a.H * NH * 64;
+  head_split_reduce_kernel<NH><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(b);
+  SC_CHECK_LAUNCH("head_split_reduce_kernel");
   return SC_OK;
 }
 
