@@ -472,3 +472,43 @@ def test_graphed_train_step_matches_eager(P, precision):
     np.testing.assert_allclose(graphed, eager, rtol=1e-6)
     for n in m1.weights:
         torch.testing.assert_close(m2.weights[n], m1.weights[n], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("pattern,window,padding", [("sparse", 4, "exclude"), ("longformer", 8, "zero-logit")])
+def test_attention_backward_long_sequences_split_head_pass(P, pattern, window, padding):
+    """Few long sequences: the head-row pass splits each (sequence, head)'s keys over CTAs
+    (ordered partial reductions); bf16 tiled path vs the fp32 generic adjoint."""
+    from paper_2312_17649_b200.training import attention_backward
+
+    m = np.array([10, 25])
+    n = np.array([2600, 3333])
+    seq = m + n + 3
+    H, d = 2, 64
+    lay = P.PackedLayout.from_lengths(seq, m + 1, device="cuda")
+    pat = P.make_pattern(pattern, window)
+    T = int(seq.sum())
+    gen = torch.Generator("cuda").manual_seed(17)
+    qkv = torch.randn(T, 3 * H * d, device="cuda", generator=gen).bfloat16()
+    dout = torch.randn(T, H * d, device="cuda", generator=gen).bfloat16()
+    out16 = P.attend_packed(qkv[:, :H * d], qkv[:, H * d:2 * H * d], qkv[:, 2 * H * d:], lay, pat, H,
+                            padding=padding)
+    g16 = torch.empty(T, 3 * H * d, device="cuda")
+    attention_backward(qkv, out16, dout, g16, lay, pat, H, 8.0, padding)
+    q32 = qkv.float()
+    out32 = P.attend_packed(q32[:, :H * d], q32[:, H * d:2 * H * d], q32[:, 2 * H * d:], lay, pat, H,
+                            padding=padding, algo="generic")
+    g32 = torch.empty_like(g16)
+    attention_backward(q32, out32, dout.float(), g32, lay, pat, H, 8.0, padding)
+    for c in range(3):
+        a, b = g16[:, c * H * d:(c + 1) * H * d], g32[:, c * H * d:(c + 1) * H * d]
+        err = float((a - b).abs().max())
+        assert err <= 3e-2 * max(1.0, float(b.abs().max())), (c, err)
+    # the head rows (cls + query group) specifically
+    for j in range(2):
+        r0 = int(lay.cu_host[j])
+        a, b = g16[r0:r0 + m[j] + 2, :H * d], g32[r0:r0 + m[j] + 2, :H * d]
+        assert float((a - b).abs().max()) <= 3e-2 * max(1.0, float(b.abs().max()))
+    # deterministic
+    g16b = torch.empty_like(g16)
+    attention_backward(qkv, out16, dout, g16b, lay, pat, H, 8.0, padding)
+    assert torch.equal(g16, g16b)
