@@ -256,6 +256,13 @@ SC_API int sc_gemm_residual_layernorm(const void* a, int64_t lda, const void* w,
 
 /* ---- Fine-tuning --------------------------------------- */
 
+/* sc_gemm_bias_gelu that also stores the pre-activation pre = A W^T + b
+ * (bf16, row stride ldp): the fine-tuning forward keeps it for the GELU
+ * adjoint (R/encoder.py:262-264, :408).  Same envelope. */
+SC_API int sc_gemm_bias_gelu_pre(const void* a, int64_t lda, const void* w, int64_t ldw, const float* bias,
+                          void* out, int64_t ldo, void* pre, int64_t ldp, int32_t M, int32_t N, int32_t K,
+                          void* stream);
+
 /* One fused AdamW step over a flat fp32 buffer of n parameters (R/training.py:
  * 114-137): m = b1 m + (1-b1) g, v = b2 v + (1-b2) g^2,
  * w -= lr * ((m/bc1) / (sqrt(v/bc2) + eps) + weight_decay * w) with

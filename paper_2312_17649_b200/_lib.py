@@ -66,6 +66,7 @@ SIGNATURES = {
     "sc_residual_layernorm_ex": (C.c_int, [_p, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _i32, _i32, _p]),
     "sc_bias_gelu": (C.c_int, [_p, _p, _i32, _i64, _i32, _p]),
     "sc_gemm_bias_gelu": (C.c_int, [_p, _i64, _p, _i64, _p, _p, _i64, _i32, _i32, _i32, _p]),
+    "sc_gemm_bias_gelu_pre": (C.c_int, [_p, _i64, _p, _i64, _p, _p, _i64, _p, _i64, _i32, _i32, _i32, _p]),
     "sc_gemm_residual_layernorm": (C.c_int, [_p, _i64, _p, _i64, _p, _p, _i64, _p, _p, _p, _i64, _p, _i64, _p,
                                              _i32, _i32, _i32, _p]),
     "sc_adamw_step": (C.c_int, [_p, _p, _p, _p, _p, _i64, C.c_double, C.c_double, C.c_double, C.c_double,

@@ -22,17 +22,32 @@ namespace sc {
 namespace gg {
 using namespace tcx;
 
+// Shared-memory layout of one instantiation: NSV pipeline stages, then 2 staging chunks per output
+// (kPre: a second output holding the pre-activation A W^T + b, for the fine-tuning backward).
+template <int NSV, bool kPre>
+struct Lay {
+  static constexpr int NOUT = kPre ? 2 : 1;
+  static constexpr int STG = NSV * STAGE;
+  static constexpr int BAR = STG + 2 * NOUT * STG_BYTES;
+  static constexpr int BIAS = BAR + (2 * NSV + 4) * 8 + 16;  // BN fp32 bias slice of the current tile
+  static constexpr int TOTAL = BIAS + BN * 4;
+};
 constexpr int NS = 4;
-constexpr int SMEM_STG = NS * STAGE;
-constexpr int SMEM_BAR = SMEM_STG + 2 * STG_BYTES;
-constexpr int SMEM_BIAS = SMEM_BAR + (2 * NS + 4) * 8 + 16;  // BN fp32 bias slice of the current tile
-constexpr int SMEM_TOTAL = SMEM_BIAS + BN * 4;
+constexpr int SMEM_STG = Lay<NS, false>::STG;
+constexpr int SMEM_BAR = Lay<NS, false>::BAR;
+constexpr int SMEM_BIAS = Lay<NS, false>::BIAS;
+constexpr int SMEM_TOTAL = Lay<NS, false>::TOTAL;
+constexpr int NS_PRE = 3;  // the dual-output variant trades a stage for the extra staging chunks
 
 
-template <bool kGelu = true>
+template <bool kGelu = true, bool kPre = false, int NSV = NS>
 __global__ void __launch_bounds__(NTHREADS, 1) gemm_bias_gelu_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-    const __grid_constant__ CUtensorMap tmO, const float* __restrict__ bias, int M, int N, int K) {
+    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmP,
+    const float* __restrict__ bias, int M, int N, int K) {
+  constexpr int NS = NSV;
+  using L = Lay<NS, kPre>;
+  constexpr int SMEM_STG = L::STG, SMEM_BAR = L::BAR, SMEM_BIAS = L::BIAS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sm0 = smem_u32(smem);
@@ -133,7 +148,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_bias_gelu_kernel(
           if (lane == 0) mbar_arrive(acc_empty + 8 * buf);
         }
         const float* bc = sb + c * 64;
-        uint32_t pk[32];
+        uint32_t pk[32], pp[kPre ? 32 : 1];
 #pragma unroll
         for (int e = 0; e < 64; e += 2) {
           const float2 x = __fadd2_rn(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])),
@@ -141,10 +156,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_bias_gelu_kernel(
           const float2 g = kGelu ? gelu2_bf16path_1mufu(x) : x;
           __nv_bfloat162 h2 = __floats2bfloat162_rn(g.x, g.y);
           pk[e / 2] = *reinterpret_cast<uint32_t*>(&h2);
+          if constexpr (kPre) {
+            __nv_bfloat162 x2 = __floats2bfloat162_rn(x.x, x.y);
+            pp[e / 2] = *reinterpret_cast<uint32_t*>(&x2);
+          }
         }
-        // staging buffer (chunk & 1) is free once the TMA store issued two chunks ago has read it
-        const uint32_t stg = sm0 + SMEM_STG + (chunk & 1) * STG_BYTES;
-        if (et == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        // staging chunk(s) (chunk & 1) are free once the TMA stores issued two chunks ago have read
+        // them (one store group per output per chunk)
+        const uint32_t stg = sm0 + SMEM_STG + (chunk & 1) * L::NOUT * STG_BYTES;
+        if (et == 0) {
+          if constexpr (kPre) asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
         epi_sync();
 #pragma unroll
         for (int p16 = 0; p16 < 8; ++p16) {
@@ -152,10 +175,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_bias_gelu_kernel(
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk[4 * p16]),
                        "r"(pk[4 * p16 + 1]), "r"(pk[4 * p16 + 2]), "r"(pk[4 * p16 + 3])
                        : "memory");
+          if constexpr (kPre)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr + STG_BYTES), "r"(pp[4 * p16]),
+                         "r"(pp[4 * p16 + 1]), "r"(pp[4 * p16 + 2]), "r"(pp[4 * p16 + 3])
+                         : "memory");
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         epi_sync();
-        if (et == 0) tma_store_2d(&tmO, stg, n0 + c * 64, m0);
+        if (et == 0) {
+          tma_store_2d(&tmO, stg, n0 + c * 64, m0);
+          if constexpr (kPre) tma_store_2d(&tmP, stg + STG_BYTES, n0 + c * 64, m0);
+        }
       }
     }
     if (et == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -365,9 +395,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1) gemm_bi
 
 using namespace sc;
 
-extern "C" int sc_gemm_bias_gelu(const void* a, int64_t lda, const void* w, int64_t ldw, const float* bias,
-                                 void* out, int64_t ldo, int32_t M, int32_t N, int32_t K, void* stream) {
+static int gemm_bias_gelu_impl(const void* a, int64_t lda, const void* w, int64_t ldw, const float* bias,
+                               void* out, int64_t ldo, void* pre, int64_t ldp, int32_t M, int32_t N, int32_t K,
+                               void* stream) {
   using namespace gg;
+  if (pre && (ldp < N || (ldp * 2) % 16 || ((uintptr_t)pre & 15))) {
+    set_error("sc_gemm_bias_gelu_pre: the pre-activation rows must be 16-byte aligned");
+    return SC_ERR_UNSUPPORTED;
+  }
   SC_CHECK_ARG(a && w && out && M >= 0 && N >= 1 && K >= 1, "sc_gemm_bias_gelu: bad arguments");
   if (M == 0) return SC_OK;
   if (N % BN || K % BK || lda < K || ldw < K || ldo < N || (lda * 2) % 16 || (ldw * 2) % 16 || (ldo * 2) % 16 ||
@@ -422,6 +457,28 @@ extern "C" int sc_gemm_bias_gelu(const void* a, int64_t lda, const void* w, int6
     }
     attr = true;
   }
+  if (pre) {  // dual output: gelu(x) and the pre-activation x = A W^T + b
+    static bool attr_pre = false;
+    const size_t smem_pre = Lay<NS_PRE, true>::TOTAL + 1024;
+    if (!attr_pre) {
+      if (cudaFuncSetAttribute(gemm_bias_gelu_kernel<true, true, NS_PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem_pre) != cudaSuccess) {
+        set_error("sc_gemm_bias_gelu: shared memory request of %zu bytes failed", smem_pre);
+        return SC_ERR_UNSUPPORTED;
+      }
+      attr_pre = true;
+    }
+    CUtensorMap mP;
+    if (!make_map(&mP, pre, N, M, ldp, BM)) {
+      set_error("sc_gemm_bias_gelu: cuTensorMapEncodeTiled failed");
+      return SC_ERR_UNSUPPORTED;
+    }
+    const int tiles_p = ((M + BM - 1) / BM) * (N / BN);
+    gemm_bias_gelu_kernel<true, true, NS_PRE><<<tiles_p < num_sms ? tiles_p : num_sms, NTHREADS, smem_pre,
+                                                (cudaStream_t)stream>>>(mA, mB, mO, mP, bias, M, N, K);
+    SC_CHECK_LAUNCH("gemm_bias_gelu_kernel");
+    return SC_OK;
+  }
   const int tiles = ((M + BM - 1) / BM) * (N / BN);
   static int no_gelu = -1;  // SC_GEMM_NO_GELU=1: bias-only epilogue (measurement of the mainloop alone)
   if (no_gelu < 0) {
@@ -430,10 +487,22 @@ extern "C" int sc_gemm_bias_gelu(const void* a, int64_t lda, const void* w, int6
   }
   if (no_gelu)
     gemm_bias_gelu_kernel<false><<<tiles < num_sms ? tiles : num_sms, NTHREADS, smem, (cudaStream_t)stream>>>(
-        mA, mB, mO, bias, M, N, K);
+        mA, mB, mO, mO, bias, M, N, K);
   else
     gemm_bias_gelu_kernel<true><<<tiles < num_sms ? tiles : num_sms, NTHREADS, smem, (cudaStream_t)stream>>>(
-        mA, mB, mO, bias, M, N, K);
+        mA, mB, mO, mO, bias, M, N, K);
   SC_CHECK_LAUNCH("gemm_bias_gelu_kernel");
   return SC_OK;
+}
+
+extern "C" int sc_gemm_bias_gelu(const void* a, int64_t lda, const void* w, int64_t ldw, const float* bias,
+                                 void* out, int64_t ldo, int32_t M, int32_t N, int32_t K, void* stream) {
+  return gemm_bias_gelu_impl(a, lda, w, ldw, bias, out, ldo, nullptr, 0, M, N, K, stream);
+}
+
+extern "C" int sc_gemm_bias_gelu_pre(const void* a, int64_t lda, const void* w, int64_t ldw, const float* bias,
+                                     void* out, int64_t ldo, void* pre, int64_t ldp, int32_t M, int32_t N, int32_t K,
+                                     void* stream) {
+  SC_CHECK_ARG(pre, "sc_gemm_bias_gelu_pre: null pre-activation output");
+  return gemm_bias_gelu_impl(a, lda, w, ldw, bias, out, ldo, pre, ldp, M, N, K, stream);
 }

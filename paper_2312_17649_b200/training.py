@@ -226,10 +226,20 @@ class LinearGelu(torch.autograd.Function):
     def forward(ctx, x, w, w16, bias, b16, cdt):
         xc = x.to(cdt).contiguous()
         wc = w16 if w16 is not None else w.to(cdt)
-        f = torch.addmm(b16 if b16 is not None else bias.to(cdt), xc, wc)
-        g = torch.empty_like(f)
-        _lib.call("sc_gelu_fwd", f.data_ptr(), g.data_ptr(), _dcode(f), f.numel(), _lib.stream_handle(),
-                  exc=EncoderError)
+        rows, k = xc.shape
+        n = wc.shape[1]
+        if cdt == torch.bfloat16 and n % 256 == 0 and k % 64 == 0:
+            # one tcgen05 GEMM writing gelu(x W + b) and the pre-activation (sc_gemm_bias_gelu_pre)
+            f = torch.empty(rows, n, dtype=cdt, device=xc.device)
+            g = torch.empty_like(f)
+            wt = wc.t().contiguous()  # [N, K] (nn.Linear layout)
+            _lib.call("sc_gemm_bias_gelu_pre", xc.data_ptr(), k, wt.data_ptr(), k, bias.float().contiguous().data_ptr(),
+                      g.data_ptr(), n, f.data_ptr(), n, rows, n, k, _lib.stream_handle(), exc=EncoderError)
+        else:
+            f = torch.addmm(b16 if b16 is not None else bias.to(cdt), xc, wc)
+            g = torch.empty_like(f)
+            _lib.call("sc_gelu_fwd", f.data_ptr(), g.data_ptr(), _dcode(f), f.numel(), _lib.stream_handle(),
+                      exc=EncoderError)
         ctx.save_for_backward(xc, wc, f)
         ctx.meta = (cdt, x.dtype)
         return g

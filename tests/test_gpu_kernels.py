@@ -204,3 +204,21 @@ def test_gemm_residual_layernorm_vs_torch(lib, M, K):
     with pytest.raises(NotImplementedError):
         lib.call("sc_gemm_residual_layernorm", a.data_ptr(), K, w.data_ptr(), K, None, resid.data_ptr(), N,
                  gamma.data_ptr(), beta.data_ptr(), out.data_ptr(), N, None, N, None, M, 512, K, lib.stream_handle())
+
+
+def test_gemm_bias_gelu_pre_dual_output():
+    """sc_gemm_bias_gelu_pre: the fused W1 GEMM also storing the pre-activation (fine-tuning)."""
+    import paper_2312_17649_b200._lib as L
+
+    torch.manual_seed(3)
+    M, N, K = 1000, 512, 192
+    a = torch.randn(M, K, device="cuda").bfloat16()
+    w = (torch.randn(N, K, device="cuda") * 0.1).bfloat16()
+    b = torch.randn(N, device="cuda")
+    g = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    f = torch.empty_like(g)
+    L.call("sc_gemm_bias_gelu_pre", a.data_ptr(), K, w.data_ptr(), K, b.data_ptr(), g.data_ptr(), N, f.data_ptr(),
+           N, M, N, K, L.stream_handle())
+    pre = a.float() @ w.float().t() + b
+    torch.testing.assert_close(f.float(), pre, rtol=2e-2, atol=2e-2)
+    torch.testing.assert_close(g.float(), torch.nn.functional.gelu(pre), rtol=2e-2, atol=2e-2)
