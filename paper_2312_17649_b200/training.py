@@ -802,7 +802,10 @@ class GraphedTrainStep:
 
     The packed layout, the static id / teacher buffers and every intermediate live in the
     graph's memory pool; each call copies new ids (and teacher margins) in, replays, and
-    applies AdamW.  Margin-MSE or RankNet loss, as in ``train_step``.
+    applies AdamW.  Margin-MSE or RankNet loss, as in ``train_step``.  The replayed forward
+    reads the bf16 shadow weights the fused AdamW keeps current: change the weights only
+    through this object's optimizer (or call ``model.weights.bf16_views()`` after an in-place
+    edit, before the next call).
     """
 
     def __init__(self, model: TrainableCrossEncoder, opt: AdamW, batch: PackedBatch, loss: str = "margin_mse",
