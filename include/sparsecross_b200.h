@@ -179,9 +179,9 @@ SC_API int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t row_
 /* Backward of sc_attn_fwd for fine-tuning (R/attention.py:260-269, :348-378,
  * :476-507; R/band.py:239-274): given q/k/v and the forward output `out`
  * (same layout, dtype and pattern arguments as sc_attn_fwd) and the output
- * gradient `dout` ([T][H][d], dout_row_stride, `dtype`), writes fp32 dq, dk
- * and dv (row r, head h at base + r*grad_row_stride + h*d; e.g. the thirds of
- * one [T][3][H][d] buffer).  Deterministic: two gather-form kernels, no
+ * gradient `dout` ([T][H][d], dout_row_stride, `dtype`), writes dq, dk and
+ * dv in `grad_dtype` (fp32 accumulation either way; row r, head h at base +
+ * r*grad_row_stride + h*d; e.g. the thirds of one [T][3][H][d] buffer).  Deterministic: two gather-form kernels, no
  * atomics.  Rows whose forward had no valid key get zero gradients.
  * tok_flags/glob_cu/glob_pos, seq_tile_base/tile_rows (from sc_index_build)
  * and max_qgroup_len as in sc_attn_fwd (QDS pointers NULL without QDS).
@@ -197,7 +197,7 @@ SC_API size_t sc_attn_bwd_workspace_bytes(int32_t total_tokens, int32_t heads, i
                                           int32_t max_qgroup_len);
 SC_API int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t row_stride,
                 const void* out, int64_t out_row_stride, const void* dout, int64_t dout_row_stride,
-                float* dq, float* dk, float* dv, int64_t grad_row_stride,
+                void* dq, void* dk, void* dv, int64_t grad_row_stride, int32_t grad_dtype,
                 const int32_t* cu_seqlens, const int32_t* qgroup_len, int32_t nseq,
                 int32_t total_tokens, int32_t heads, int32_t head_dim,
                 const int32_t* links, int32_t padding, float scale, int32_t dtype,

@@ -59,7 +59,7 @@ SIGNATURES = {
     "sc_band_scores_backward": (C.c_int, [_p, _p, _p, _p, _p, _i64, _i32, _i32, _i32, _i32, _i32, _p]),
     "sc_band_apply_backward": (C.c_int, [_p, _p, _p, _p, _p, _i64, _i32, _i32, _i32, _i32, _i32, _p]),
     "sc_attn_bwd_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32]),
-    "sc_attn_bwd": (C.c_int, [_p, _p, _p, _i64, _p, _i64, _p, _i64, _p, _p, _p, _i64, _p, _p, _i32, _i32, _i32,
+    "sc_attn_bwd": (C.c_int, [_p, _p, _p, _i64, _p, _i64, _p, _i64, _p, _p, _p, _i64, _i32, _p, _p, _i32, _i32, _i32,
                               _i32, _p, _i32, _f32, _i32, _p, _p, _p, _p, _i32, _i32, _i32, _p, _sz, _p]),
     "sc_embed": (C.c_int, [_p, _p, _p, _p, _p, _p, _i32, _i32, _p]),
     "sc_residual_layernorm": (C.c_int, [_p, _p, _i32, _p, _p, _p, _p, _p, _i32, _i32, _p]),

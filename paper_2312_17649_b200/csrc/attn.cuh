@@ -39,7 +39,8 @@ bool load_links(const int32_t* links, Links* L);
 struct BandBwdArgs {
   const __nv_bfloat16 *q, *k, *v, *out, *dout;
   int64_t ld, ld_out, ld_dout;
-  float *dq, *dk, *dv;
+  void *dq, *dk, *dv;             // fp32, or bf16 when grad_bf16
+  int grad_bf16;
   int64_t ld_grad;
   float2* stats;                  // [T*H] (lse, D), shared with the generic kernels
   const int32_t *cu, *qlen, *tile_base;
@@ -52,6 +53,23 @@ struct BandBwdArgs {
   float* head_split;              // [nseq][H][head_ks][NH][2 + 64]
   int head_ks, head_phase;
 };
+// Gradient stores in fp32 or bf16 (element index idx of the buffer).
+__device__ __forceinline__ void store_grad(void* base, int64_t idx, float v, int bf16) {
+  if (bf16) reinterpret_cast<__nv_bfloat16*>(base)[idx] = __float2bfloat16_rn(v);
+  else reinterpret_cast<float*>(base)[idx] = v;
+}
+__device__ __forceinline__ void store_grad2(void* base, int64_t idx, float a, float b, int bf16) {  // idx even
+  if (bf16) *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(base) + idx) = __floats2bfloat162_rn(a, b);
+  else *reinterpret_cast<float2*>(reinterpret_cast<float*>(base) + idx) = make_float2(a, b);
+}
+__device__ __forceinline__ void add_grad(void* base, int64_t idx, float v, int bf16) {
+  if (bf16) {
+    __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(base) + idx;
+    *p = __float2bfloat16_rn(__bfloat162float(*p) + v);
+  } else {
+    reinterpret_cast<float*>(base)[idx] += v;
+  }
+}
 // phase 0: doc-row statistics + dQ (+ head-key partials); 1: doc-key dK / dV; 2: head-key partial
 // reduction; 3: head-row statistics + dQ.  max_head = 1 + max qgroup_len (<= 32); NH = 16 when max_head <= 16, else 32.
 int launch_attn_bwd_band(const BandBwdArgs& a, int ntiles, int max_head, int phase, cudaStream_t st);

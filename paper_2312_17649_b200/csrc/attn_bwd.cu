@@ -57,9 +57,10 @@ struct BwdArgs {
   AttnArgs a;
   const void* dout;
   int64_t ld_dout;
-  float* dq;
-  float* dk;
-  float* dv;
+  void* dq;
+  void* dk;
+  void* dv;
+  int grad_bf16;
   int64_t ld_grad;
   float2* stats;  // [T*H]: (lse, D); lse = +inf for rows without keys
   int mode;       // 0: every row; 1: only the head rows (cls + query group) of every sequence
@@ -380,11 +381,11 @@ __global__ void __launch_bounds__(ItemSlot<NS>::kWarpsPerCta * 32) attn_bwd_dq_k
       dq[e] = acc;
     }
   }
-  float* dqr = b.dq + (int64_t)row * b.ld_grad + hoff;
+  const int64_t dqo = (int64_t)row * b.ld_grad + hoff;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int c = lane + 32 * e;
-    if (c < d) dqr[c] = dq[e];
+    if (c < d) store_grad(b.dq, dqo + c, dq[e], b.grad_bf16);
   }
 }
 
@@ -497,12 +498,14 @@ __global__ void __launch_bounds__(ItemSlot<NS>::kWarpsPerCta * 32) attn_bwd_dkv_
       dv[e] = av;
     }
   }
-  float* dkr = b.dk + (int64_t)krow * b.ld_grad + hoff;
-  float* dvr = b.dv + (int64_t)krow * b.ld_grad + hoff;
+  const int64_t ko = (int64_t)krow * b.ld_grad + hoff;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int c = lane + 32 * e;
-    if (c < d) { dkr[c] = dk[e]; dvr[c] = dv[e]; }
+    if (c < d) {
+      store_grad(b.dk, ko + c, dk[e], b.grad_bf16);
+      store_grad(b.dv, ko + c, dv[e], b.grad_bf16);
+    }
   }
 }
 
@@ -579,8 +582,9 @@ extern "C" size_t sc_attn_bwd_workspace_bytes(int32_t total_tokens, int32_t head
 }
 
 extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t row_stride, const void* out,
-                           int64_t out_row_stride, const void* dout, int64_t dout_row_stride, float* dq, float* dk,
-                           float* dv, int64_t grad_row_stride, const int32_t* cu_seqlens, const int32_t* qgroup_len,
+                           int64_t out_row_stride, const void* dout, int64_t dout_row_stride, void* dq, void* dk,
+                           void* dv, int64_t grad_row_stride, int32_t grad_dtype, const int32_t* cu_seqlens,
+                           const int32_t* qgroup_len,
                            int32_t nseq, int32_t total_tokens, int32_t heads, int32_t head_dim, const int32_t* links,
                            int32_t padding, float scale, int32_t dtype, const uint8_t* tok_flags,
                            const int32_t* glob_cu, const int32_t* glob_pos, const int32_t* seq_tile_base,
@@ -599,12 +603,15 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
   SC_CHECK_ARG((glob_cu == nullptr) == (glob_pos == nullptr) && (glob_cu == nullptr || tok_flags != nullptr),
                "sc_attn_bwd: QDS globals need tok_flags, glob_cu and glob_pos");
   SC_CHECK_ARG(max_qgroup_len >= 1, "sc_attn_bwd: max_qgroup_len must be >= 1");
+  SC_CHECK_ARG(grad_dtype == SC_DTYPE_F32 || grad_dtype == SC_DTYPE_BF16, "sc_attn_bwd: bad grad_dtype %d",
+               grad_dtype);
   SC_CHECK_ARG(workspace && workspace_bytes >= stats_bytes(total_tokens, heads),
                "sc_attn_bwd: workspace must hold sc_attn_bwd_workspace_bytes(T, H, nseq, max_qgroup_len) bytes");
   a.q = q; a.k = k; a.v = v; a.ld = row_stride; a.out = const_cast<void*>(out); a.ld_out = out_row_stride;
   a.cu = cu_seqlens; a.qlen = qgroup_len; a.nseq = nseq; a.T = total_tokens; a.H = heads; a.d = head_dim;
   a.padding = padding; a.scale = scale; a.flags = tok_flags; a.glob_cu = glob_cu; a.glob_pos = glob_pos;
   b.dout = dout; b.ld_dout = dout_row_stride; b.dq = dq; b.dk = dk; b.dv = dv; b.ld_grad = grad_row_stride;
+  b.grad_bf16 = grad_dtype == SC_DTYPE_BF16;
   b.stats = static_cast<float2*>(workspace);
   b.maxh = 1 + max_qgroup_len;
   cudaStream_t st = (cudaStream_t)stream;
@@ -615,6 +622,7 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
   const bool aligned = ((row_stride | out_row_stride | dout_row_stride) % 8) == 0 &&
                        (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out | (uintptr_t)dout) % 16) == 0 &&
                        grad_row_stride % 2 == 0 && ((uintptr_t)dq | (uintptr_t)dk | (uintptr_t)dv) % 8 == 0;
+  // (bf16 gradients: 4-byte aligned pairs suffice, implied by the above)
   const bool fast = dtype == SC_DTYPE_BF16 && head_dim == 64 && glob_cu == nullptr && seq_tile_base &&
                     tile_rows == 64 && wdd >= 0 && wdd <= 24 && b.maxh <= 32 && aligned &&
                     !force_generic();
@@ -627,7 +635,7 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
   p.q = (const __nv_bfloat16*)q; p.k = (const __nv_bfloat16*)k; p.v = (const __nv_bfloat16*)v;
   p.out = (const __nv_bfloat16*)out; p.dout = (const __nv_bfloat16*)dout;
   p.ld = row_stride; p.ld_out = out_row_stride; p.ld_dout = dout_row_stride;
-  p.dq = dq; p.dk = dk; p.dv = dv; p.ld_grad = grad_row_stride; p.stats = b.stats;
+  p.dq = dq; p.dk = dk; p.dv = dv; p.ld_grad = grad_row_stride; p.stats = b.stats; p.grad_bf16 = b.grad_bf16;
   p.cu = cu_seqlens; p.qlen = qgroup_len; p.tile_base = seq_tile_base; p.nseq = nseq; p.H = heads; p.w = wdd;
   p.links = a.links; p.padding = padding; p.inv_scale = 1.f / scale;
   // head-key partials when the workspace has room (else the generic head-key pass sums doc sources)

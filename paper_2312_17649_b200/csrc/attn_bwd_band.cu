@@ -247,9 +247,9 @@ __global__ void __launch_bounds__(128) band_dq_kernel(Args p) {
   for (int i = 0; i < 8; ++i) {
     const int c = 8 * i + 2 * tq;
     if (rsA < dlen)
-      *reinterpret_cast<float2*>(p.dq + (int64_t)(dstart + rsA) * p.ld_grad + hoff + c) = make_float2(o[i][0], o[i][1]);
+      store_grad2(p.dq, (int64_t)(dstart + rsA) * p.ld_grad + hoff + c, o[i][0], o[i][1], p.grad_bf16);
     if (rsB < dlen)
-      *reinterpret_cast<float2*>(p.dq + (int64_t)(dstart + rsB) * p.ld_grad + hoff + c) = make_float2(o[i][2], o[i][3]);
+      store_grad2(p.dq, (int64_t)(dstart + rsB) * p.ld_grad + hoff + c, o[i][2], o[i][3], p.grad_bf16);
   }
   if (!part) return;
 
@@ -301,8 +301,7 @@ __global__ void __launch_bounds__(256) head_part_reduce_kernel(Args p) {
   float acc = 0.f;
   for (int t = p.tile_base[j]; t < p.tile_base[j + 1]; ++t)
     acc += p.head_part[(((int64_t)t * p.H + h) * 2 + which) * NH * 64 + sl * 64 + dim];
-  float* dst = (which ? p.dk : p.dv) + (int64_t)(g.start + sl) * p.ld_grad + h * 64 + dim;
-  *dst += acc;
+  add_grad(which ? p.dk : p.dv, (int64_t)(g.start + sl) * p.ld_grad + h * 64 + dim, acc, p.grad_bf16);
 }
 
 // Kernel B: doc keys [k0, k0+64) of one sequence, one head.  Sources: the band doc rows
@@ -443,13 +442,13 @@ __global__ void __launch_bounds__(128) band_dkv_kernel(Args p) {
     const int c = 8 * i + 2 * tq;
     if (kA < dlen) {
       const int64_t off = (int64_t)(dstart + kA) * p.ld_grad + hoff + c;
-      *reinterpret_cast<float2*>(p.dk + off) = make_float2(dk[i][0], dk[i][1]);
-      *reinterpret_cast<float2*>(p.dv + off) = make_float2(dv[i][0], dv[i][1]);
+      store_grad2(p.dk, off, dk[i][0], dk[i][1], p.grad_bf16);
+      store_grad2(p.dv, off, dv[i][0], dv[i][1], p.grad_bf16);
     }
     if (kB < dlen) {
       const int64_t off = (int64_t)(dstart + kB) * p.ld_grad + hoff + c;
-      *reinterpret_cast<float2*>(p.dk + off) = make_float2(dk[i][2], dk[i][3]);
-      *reinterpret_cast<float2*>(p.dv + off) = make_float2(dv[i][2], dv[i][3]);
+      store_grad2(p.dk, off, dk[i][2], dk[i][3], p.grad_bf16);
+      store_grad2(p.dv, off, dv[i][2], dv[i][3], p.grad_bf16);
     }
   }
 }
@@ -690,7 +689,7 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
     float acc = 0.f;
     for (int w = 0; w < kHeadWarps; ++w) acc += red_o[(w * NH + i) * 64 + c];
     if (split) part[((int64_t)ks * NH + i) * 66 + 2 + c] = acc;
-    else p.dq[(int64_t)(g.start + i) * p.ld_grad + hoff + c] = acc;
+    else store_grad(p.dq, (int64_t)(g.start + i) * p.ld_grad + hoff + c, acc, p.grad_bf16);
   }
 }
 
@@ -709,7 +708,7 @@ __global__ void __launch_bounds__(256) head_split_reduce_kernel(Args p) {
   const float* part = p.head_split + (((int64_t)j * p.H + h) * p.head_ks) * NH * 66;
   float acc = 0.f;
   for (int u = 0; u < p.head_ks; ++u) acc += part[((int64_t)u * NH + i) * 66 + 2 + c];
-  p.dq[(int64_t)(g.start + i) * p.ld_grad + h * 64 + c] = acc;
+  store_grad(p.dq, (int64_t)(g.start + i) * p.ld_grad + h * 64 + c, acc, p.grad_bf16);
 }
 
 template <int NH>

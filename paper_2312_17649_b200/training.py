@@ -91,27 +91,28 @@ class PatternAttention(torch.autograd.Function):
         layout, pattern, heads, scale, padding = ctx.meta
         dout = dout.to(qkv.dtype).contiguous()
         T, hd3 = qkv.shape
-        hd = hd3 // 3
-        g = torch.empty((T, hd3), dtype=torch.float32, device=qkv.device)
+        g = torch.empty((T, hd3), dtype=qkv.dtype, device=qkv.device)  # written in the input dtype
         attention_backward(qkv, out, dout, g, layout, pattern, heads, scale, padding)
-        return g.to(qkv.dtype), None, None, None, None, None, None
+        return g, None, None, None, None, None, None
 
 
 def attention_backward(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor, grad: torch.Tensor,
                        layout: PackedLayout, pattern, heads: int, scale: float, padding: str) -> None:
-    """Writes grad[:, :hd] = dQ, grad[:, hd:2hd] = dK, grad[:, 2hd:] = dV (fp32 [T, 3*H*d])."""
+    """Writes grad[:, :hd] = dQ, grad[:, hd:2hd] = dK, grad[:, 2hd:] = dV ([T, 3*H*d], fp32 or bf16)."""
     T, hd3 = qkv.shape
     hd = hd3 // 3
     d = hd // heads
     es = qkv.element_size()
     qds = pattern.name == "qds" and layout.tok_flags is not None
     base, gbase = qkv.data_ptr(), grad.data_ptr()
+    ges = grad.element_size()
     ws_bytes = _lib.load().sc_attn_bwd_workspace_bytes(T, heads, layout.nseq, layout.max_qgroup_len)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=qkv.device)
     _lib.call(
         "sc_attn_bwd",
         base, base + hd * es, base + 2 * hd * es, qkv.stride(0), out.data_ptr(), out.stride(0),
-        dout.data_ptr(), dout.stride(0), gbase, gbase + hd * 4, gbase + 2 * hd * 4, grad.stride(0),
+        dout.data_ptr(), dout.stride(0), gbase, gbase + hd * ges, gbase + 2 * hd * ges, grad.stride(0),
+        _dcode(grad),
         layout.cu_seqlens.data_ptr(), layout.qgroup_len.data_ptr(), layout.nseq, T, heads, d,
         pattern.links().ctypes.data, _lib.PAD_EXCLUDE if padding == "exclude" else _lib.PAD_ZERO_LOGIT,
         float(scale), _lib.DTYPE_BF16 if qkv.dtype == torch.bfloat16 else _lib.DTYPE_F32,
