@@ -74,6 +74,26 @@ extern "C" int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t 
   }
   const int w = a.links.w[2][2];
   const bool narrow = w >= 0 && w <= kBandMaxWindow;
+  if (dtype == SC_DTYPE_F32 && (algo == SC_ATTN_AUTO || algo == SC_ATTN_BAND_MMA) && seq_head_base) {
+    // fp32 parity path: doc rows on the tiled fp32 band kernel, head rows on the generic kernel
+    // full rows (cls, longformer query rows) merge per-tile records instead of rescanning the doc
+    const int fneed = full_rows_needed(a.links, max_qgroup_len);
+    const size_t rec_bytes = (size_t)((total_tokens + 63) / 64 + nseq) * heads * fneed * (head_dim + 2) * 4;
+    const bool recs = fneed > 0 && workspace && workspace_bytes >= rec_bytes;
+    int rc = launch_attn_band_f32(a, dtype, seq_tile_base, tile_rows, max_qgroup_len,
+                                  recs ? static_cast<float*>(workspace) : nullptr, recs ? fneed : 0, st);
+    if (rc == SC_OK) {
+      AttnArgs hrow = a;
+      hrow.head_base = seq_head_base;
+      hrow.n_head_rows = nseq * (1 + max_qgroup_len);
+      hrow.partials = recs ? static_cast<const float*>(workspace) : nullptr;
+      hrow.tile_base = seq_tile_base;
+      hrow.fmax = fneed;
+      hrow.rec_per_tile = 1;
+      return launch_attn_generic(hrow, dtype, st);
+    }
+    if (algo == SC_ATTN_BAND_MMA) return rc;
+  }
   if (algo == SC_ATTN_BAND_MMA || (algo == SC_ATTN_AUTO && narrow)) {
     int rc = launch_attn_band(a, dtype, seq_tile_base, seq_head_base, tile_rows, max_qgroup_len,
                               workspace, workspace_bytes, st);

@@ -226,9 +226,11 @@ def test_band_kernel_repeatable_and_forced(P, name):
     assert torch.equal(a, b) and torch.equal(a, c)
     gen = run("generic").float()
     assert (a.float() - gen).abs().max().item() < 2e-2
-    with pytest.raises(NotImplementedError):
-        xf = x.float()
-        P.attend_packed(xf[:, :H * d], xf[:, H * d:2 * H * d], xf[:, 2 * H * d:], lay, pat, H, algo="band")
+    # fp32 input: the fp32 band kernel (parity path) + generic head rows, vs the generic kernel
+    xf = x.float()
+    f_band = P.attend_packed(xf[:, :H * d], xf[:, H * d:2 * H * d], xf[:, 2 * H * d:], lay, pat, H, algo="band")
+    f_gen = P.attend_packed(xf[:, :H * d], xf[:, H * d:2 * H * d], xf[:, 2 * H * d:], lay, pat, H, algo="generic")
+    assert (f_band - f_gen).abs().max().item() < 1e-5
 
 
 @pytest.mark.parametrize("name,w,pad", [("sparse", 0, "exclude"), ("sparse", 4, "exclude"), ("sparse", 64, "exclude"),
