@@ -52,6 +52,7 @@ struct BandBwdArgs {
   // head-row pass split over key ranges (head_ks > 1): per (seq, head, split) (m, l) and dQ partials
   float* head_split;              // [nseq][H][head_ks][NH][2 + 64]
   int head_ks, head_phase;
+  int head_warps;                 // warps per head-row CTA (8, or 2 for short sequences)
 };
 // Gradient stores in fp32 or bf16 (element index idx of the buffer).
 __device__ __forceinline__ void store_grad(void* base, int64_t idx, float v, int bf16) {

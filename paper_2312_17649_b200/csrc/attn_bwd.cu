@@ -643,7 +643,9 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
   const size_t pbytes = (part_bytes(total_tokens, heads, nseq, max_qgroup_len) + 255) & ~(size_t)255;
   if (workspace_bytes >= soff + pbytes)
     p.head_part = reinterpret_cast<float*>(static_cast<char*>(workspace) + soff);
-  // head-row pass: split each (sequence, head)'s keys over CTAs when there are too few of them
+  // head-row pass: 2 warps per (sequence, head) for short sequences (<= 4 key chunks of 64),
+  // else 8, split over CTAs when there are too few (sequence, head) pairs
+  p.head_warps = (int64_t)total_tokens <= (int64_t)256 * nseq ? 2 : 8;
   p.head_ks = 1;
   if (workspace_bytes >= soff + pbytes + split_bytes(heads, nseq)) {
     p.head_split = reinterpret_cast<float*>(static_cast<char*>(workspace) + soff + pbytes);

@@ -456,12 +456,11 @@ __global__ void __launch_bounds__(128) band_dkv_kernel(Args p) {
 
 // Head rows (cls + query group, <= NH) of one sequence x one head against every key of the
 // sequence: S = Qh K^T on mma.sync with M = the head rows, keys in 64-row chunks dealt to the
-// 8 warps round-robin (each warp stages its chunk with cp.async into its own buffer).  Pass 1:
+// kHeadWarps warps round-robin (each warp stages its chunk with cp.async into its own buffer).  Pass 1:
 // per-row max / sum, combined across warps in order -> lse; pass 2: P, dP = dOh V^T, dS and
 // dQ_h = dS K, reduced across warps in order.  Writes the head rows' (lse, D) and dQ.
-constexpr int kHeadWarps = 8;
 
-template <int NH>
+template <int NH, int kHeadWarps>
 __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int MT = NH / 16;
@@ -711,24 +710,24 @@ __global__ void __launch_bounds__(256) head_split_reduce_kernel(Args p) {
   store_grad(p.dq, (int64_t)(g.start + i) * p.ld_grad + h * 64 + c, acc, p.grad_bf16);
 }
 
-template <int NH>
+template <int NH, int kHeadWarps>
 size_t head_smem_bytes() {
   return (size_t)(2 * NH + 2 * kHeadWarps * TILE) * ROWB +
          (size_t)(kHeadWarps * NH * 2 + 2 * NH + kHeadWarps * NH * 64) * sizeof(float);
 }
 
-template <int NH>
-int launch_head(const Args& a, cudaStream_t st) {
-  const size_t sm = head_smem_bytes<NH>();
+template <int NH, int HW>
+int launch_head_w(const Args& a, cudaStream_t st) {
+  const size_t sm = head_smem_bytes<NH, HW>();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(head_dq_kernel<NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(head_dq_kernel<NH, HW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
   if (a.head_ks <= 1 || !a.head_split) {
     Args b = a;
     b.head_ks = 1;
-    head_dq_kernel<NH><<<dim3(a.nseq, a.H, 1), kHeadWarps * 32, sm, st>>>(b);
+    head_dq_kernel<NH, HW><<<dim3(a.nseq, a.H, 1), HW * 32, sm, st>>>(b);
     SC_CHECK_LAUNCH("head_dq_kernel");
     return SC_OK;
   }
@@ -736,15 +735,22 @@ int launch_head(const Args& a, cudaStream_t st) {
   // with the combined lse, then the ordered sum
   Args b = a;
   b.head_phase = 1;
-  head_dq_kernel<NH><<<dim3(a.nseq, a.H, a.head_ks), kHeadWarps * 32, sm, st>>>(b);
+  head_dq_kernel<NH, HW><<<dim3(a.nseq, a.H, a.head_ks), HW * 32, sm, st>>>(b);
   SC_CHECK_LAUNCH("head_dq_kernel");
   b.head_phase = 2;
-  head_dq_kernel<NH><<<dim3(a.nseq, a.H, a.head_ks), kHeadWarps * 32, sm, st>>>(b);
+  head_dq_kernel<NH, HW><<<dim3(a.nseq, a.H, a.head_ks), HW * 32, sm, st>>>(b);
   SC_CHECK_LAUNCH("head_dq_kernel");
   const int64_t n = (int64_t)a.nseq * a.H * NH * 64;
   head_split_reduce_kernel<NH><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(b);
   SC_CHECK_LAUNCH("head_split_reduce_kernel");
   return SC_OK;
+}
+
+// Long sequences: 8 warps per (sequence, head) share the keys; short ones (passages, a few
+// 64-key chunks each): 2 warps, so several CTAs fit an SM.
+template <int NH>
+int launch_head(const Args& a, cudaStream_t st) {
+  return a.head_warps == 2 ? launch_head_w<NH, 2>(a, st) : launch_head_w<NH, 8>(a, st);
 }
 
 template <int NB, int NH>
