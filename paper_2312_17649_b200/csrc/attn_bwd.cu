@@ -667,8 +667,12 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
   int rc = launch_attn_bwd_band(p, ntiles, b.maxh, 3, st);   // head rows: stats + dQ (tensor cores)
   if (!rc && ntiles) rc = launch_attn_bwd_band(p, ntiles, b.maxh, 0, st);  // doc rows: stats + dQ
   if (!rc && ntiles) rc = launch_attn_bwd_band(p, ntiles, b.maxh, 1, st);  // doc keys: dK, dV
-  b.skip_doc_sources = p.head_part != nullptr && ntiles > 0;
-  if (!rc) rc = launch_generic_any(b, dtype, 1, st);          // head keys: dK, dV (non-doc sources)
-  if (!rc && b.skip_doc_sources) rc = launch_attn_bwd_band(p, ntiles, b.maxh, 2, st);  // + doc sources
+  // head keys: the head-row pass wrote their dK/dV from the head sources (chunk 0) when the
+  // doc-source partials exist; add those.  Otherwise the generic pass sums every source.
+  if (p.head_part != nullptr && ntiles > 0) {
+    if (!rc) rc = launch_attn_bwd_band(p, ntiles, b.maxh, 2, st);
+  } else if (!rc) {
+    rc = launch_generic_any(b, dtype, 1, st);
+  }
   return rc;
 }

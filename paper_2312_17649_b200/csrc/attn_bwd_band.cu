@@ -476,6 +476,8 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
   float* sD = red + kHeadWarps * NH * 2;                                                  // [NH]
   float* sL = sD + NH;                                                                     // [NH] lse (log2)
   float* red_o = sL + NH;                                                                  // [warps][NH][64]
+  float* sPS = red_o + kHeadWarps * NH * 64;  // [2][NH][64]: P and dS of key chunk 0 (the head keys)
+  const bool head_keys = p.head_part != nullptr;  // also write the head keys' dK/dV from head sources
 
   stage_rows(sQ, NH, p.q, [&](int r) { return r < nhead ? p.q + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
   stage_rows(sdO, NH, p.q, [&](int r) {
@@ -664,10 +666,35 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
             const int t = k0 + 8 * nt + 2 * tq + e;
             const float pr = ok(i, t) ? ex2(sv[nt][2 * hr + e] * c2 - lse2) : 0.f;
             sv[nt][2 * hr + e] = pr * (dp[nt][2 * hr + e] - Di) * p.inv_scale;
+            if (head_keys && ch == 0) {  // chunk 0 holds the cls / query keys
+              const int kc = 8 * nt + 2 * tq + e;
+              sPS[i * 64 + kc] = pr;
+              sPS[NH * 64 + i * 64 + kc] = sv[nt][2 * hr + e];
+            }
           }
       }
 #pragma unroll
       for (int kp = 0; kp < 4; ++kp) mm_nn16(sKw, 16 * kp, lane, sv[2 * kp], sv[2 * kp + 1], o[mt]);
+    }
+    if (head_keys && ch == 0) {
+      // head keys t < nhead, sources = the head rows: dK_t = sum_i dS_it Q_i, dV_t = sum_i P_it dO_i
+      __syncwarp();
+      for (int idx = lane; idx < nhead * 64; idx += 32) {
+        const int t = idx >> 6, c = idx & 63;
+        float dk = 0.f, dv = 0.f;
+        for (int i = 0; i < nhead; ++i) {
+          uint16_t qb, gb;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(qb) : "r"(swz(sQ, i, c >> 3) + (c & 7) * 2));
+          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(gb) : "r"(swz(sdO, i, c >> 3) + (c & 7) * 2));
+          const float qv = __bfloat162float(*reinterpret_cast<__nv_bfloat16*>(&qb));
+          const float gv = __bfloat162float(*reinterpret_cast<__nv_bfloat16*>(&gb));
+          dk = fmaf(sPS[NH * 64 + i * 64 + t], qv, dk);
+          dv = fmaf(sPS[i * 64 + t], gv, dv);
+        }
+        const int64_t off = (int64_t)(g.start + t) * p.ld_grad + hoff + c;
+        store_grad(p.dk, off, dk, p.grad_bf16);
+        store_grad(p.dv, off, dv, p.grad_bf16);
+      }
     }
   }
   // reduce dQ over the warps in order
@@ -713,7 +740,7 @@ __global__ void __launch_bounds__(256) head_split_reduce_kernel(Args p) {
 template <int NH, int kHeadWarps>
 size_t head_smem_bytes() {
   return (size_t)(2 * NH + 2 * kHeadWarps * TILE) * ROWB +
-         (size_t)(kHeadWarps * NH * 2 + 2 * NH + kHeadWarps * NH * 64) * sizeof(float);
+         (size_t)(kHeadWarps * NH * 2 + 2 * NH + kHeadWarps * NH * 64 + 2 * NH * 64) * sizeof(float);
 }
 
 template <int NH, int HW>
