@@ -287,7 +287,7 @@ SC_API int sc_layernorm_fwd(const void* a, int32_t a_dtype, const void* b, int32
  * 2 * sc_ln_partials(rows) * cols floats of scratch.  Deterministic. */
 SC_API int sc_layernorm_bwd(const float* dy, const void* dy_bf16, const void* a, int32_t a_dtype, const void* b,
                      int32_t b_dtype,
-                     const float* gamma, const float* mean, const float* rstd, float* dx, float* dgamma,
+                     const float* gamma, const float* mean, const float* rstd, float* dx, void* dx_bf16, float* dgamma,
                      float* dbeta, float* partials, int32_t rows, int32_t cols, void* stream);
 
 /* out[c] = sum_r x[r, c] (fp32 out; x fp32 or bf16 with row stride ld): the

@@ -72,7 +72,7 @@ SIGNATURES = {
     "sc_adamw_step": (C.c_int, [_p, _p, _p, _p, _p, _i64, C.c_double, C.c_double, C.c_double, C.c_double,
                                 C.c_double, _i64, _p]),
     "sc_layernorm_fwd": (C.c_int, [_p, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _i32, _i32, _f32, _p]),
-    "sc_layernorm_bwd": (C.c_int, [_p, _p, _p, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _i32, _i32, _p]),
+    "sc_layernorm_bwd": (C.c_int, [_p, _p, _p, _i32, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _i32, _p]),
     "sc_colsum": (C.c_int, [_p, _i32, _i64, _i32, _i32, _p, _p, _p]),
     "sc_ln_partials": (C.c_int, [_i32]),
     "sc_gelu_fwd": (C.c_int, [_p, _p, _i32, _i64, _p]),

@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(kLnWarps * 32, 2) ln_bwd_kernel(const float* _
                                                                   const float* __restrict__ rstd,
                                                                   float* __restrict__ dx, float* __restrict__ part_g,
                                                                   float* __restrict__ part_b, int rows, int cols,
-                                                                  const __nv_bfloat16* __restrict__ dy16) {
+                                                                  const __nv_bfloat16* __restrict__ dy16,
+                                                                  __nv_bfloat16* __restrict__ dx16) {
   extern __shared__ float4 lnsm[];  // [2][kLnWarps][ng] float4
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ng = cols >> 2;
@@ -133,10 +134,18 @@ __global__ void __launch_bounds__(kLnWarps * 32, 2) ln_bwd_kernel(const float* _
 #pragma unroll
     for (int k = 0; k < KV; ++k) {
       const int q = lane + 32 * k;
-      if (q < ng)
-        *reinterpret_cast<float4*>(dx + base + 4 * q) =
-            make_float4(rs * (gd[k].x - m1 - xh[k].x * m2), rs * (gd[k].y - m1 - xh[k].y * m2),
-                        rs * (gd[k].z - m1 - xh[k].z * m2), rs * (gd[k].w - m1 - xh[k].w * m2));
+      if (q < ng) {
+        const float4 o = make_float4(rs * (gd[k].x - m1 - xh[k].x * m2), rs * (gd[k].y - m1 - xh[k].y * m2),
+                                     rs * (gd[k].z - m1 - xh[k].z * m2), rs * (gd[k].w - m1 - xh[k].w * m2));
+        if (dx) *reinterpret_cast<float4*>(dx + base + 4 * q) = o;
+        if (dx16) {  // bf16 copy: the gradient of a bf16 input
+          __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
+          uint2 u;
+          u.x = *reinterpret_cast<uint32_t*>(&lo);
+          u.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(dx16 + base + 4 * q) = u;
+        }
+      }
     }
   }
   __syncthreads();
@@ -223,7 +232,7 @@ int num_sms() {
 template <typename TA, typename TB, int KV>
 void ln_launch(bool fwd, const void* a, const void* b, const float* gamma, const float* beta, const float* dy,
                float* y, float* mean, float* rstd, float* dx, float* pg, float* pb, int rows, int cols, float eps,
-               unsigned blocks, cudaStream_t st, void* aux) {
+               unsigned blocks, cudaStream_t st, void* aux, void* aux2) {
   if (fwd) {
     ln_fwd_kernel<TA, TB, KV><<<blocks, kLnWarps * 32, 0, st>>>((const TA*)a, (const TB*)b, gamma, beta, y, mean,
                                                                  rstd, rows, cols, eps, (__nv_bfloat16*)aux);
@@ -236,28 +245,30 @@ void ln_launch(bool fwd, const void* a, const void* b, const float* gamma, const
       attr = true;
     }
     ln_bwd_kernel<TA, TB, KV><<<blocks, kLnWarps * 32, sm, st>>>(dy, (const TA*)a, (const TB*)b, gamma, mean, rstd,
-                                                                  dx, pg, pb, rows, cols, (const __nv_bfloat16*)aux);
+                                                                  dx, pg, pb, rows, cols, (const __nv_bfloat16*)aux,
+                                                                  (__nv_bfloat16*)aux2);
   }
 }
 
 template <int KV>
 void ln_dispatch_types(bool af, bool bf, bool fwd, const void* a, const void* b, const float* gamma,
                        const float* beta, const float* dy, float* y, float* mean, float* rstd, float* dx, float* pg,
-                       float* pb, int rows, int cols, float eps, unsigned blocks, cudaStream_t st, void* aux) {
+                       float* pb, int rows, int cols, float eps, unsigned blocks, cudaStream_t st, void* aux,
+                       void* aux2) {
   using B16 = __nv_bfloat16;
-  if (af && bf) ln_launch<float, float, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux);
-  else if (af) ln_launch<float, B16, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux);
-  else if (bf) ln_launch<B16, float, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux);
-  else ln_launch<B16, B16, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux);
+  if (af && bf) ln_launch<float, float, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux, aux2);
+  else if (af) ln_launch<float, B16, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux, aux2);
+  else if (bf) ln_launch<B16, float, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux, aux2);
+  else ln_launch<B16, B16, KV>(fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux, aux2);
 }
 
 // Column groups (of 4) per lane rounded up to an instantiated width.
 void ln_dispatch(bool af, bool bf, bool fwd, const void* a, const void* b, const float* gamma, const float* beta,
                  const float* dy, float* y, float* mean, float* rstd, float* dx, float* pg, float* pb, int rows,
-                 int cols, float eps, unsigned blocks, cudaStream_t st, void* aux) {
+                 int cols, float eps, unsigned blocks, cudaStream_t st, void* aux, void* aux2) {
   const int kv = (cols / 4 + 31) / 32;
 #define SC_LN_CASE(W) \
-  if (kv <= W) return ln_dispatch_types<W>(af, bf, fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux);
+  if (kv <= W) return ln_dispatch_types<W>(af, bf, fwd, a, b, gamma, beta, dy, y, mean, rstd, dx, pg, pb, rows, cols, eps, blocks, st, aux, aux2);
   SC_LN_CASE(1) SC_LN_CASE(2) SC_LN_CASE(4) SC_LN_CASE(6) SC_LN_CASE(8)
 #undef SC_LN_CASE
 }
@@ -286,19 +297,21 @@ extern "C" int sc_layernorm_fwd(const void* a, int32_t a_dtype, const void* b, i
   if (rows == 0) return SC_OK;
   const unsigned blocks = (unsigned)((rows + kLnWarps - 1) / kLnWarps);
   ln_dispatch(a_dtype == SC_DTYPE_F32, !b || b_dtype == SC_DTYPE_F32, true, a, b, gamma, beta, nullptr, y, mean, rstd,
-              nullptr, nullptr, nullptr, rows, cols, eps, blocks, (cudaStream_t)stream, y_bf16);
+              nullptr, nullptr, nullptr, rows, cols, eps, blocks, (cudaStream_t)stream, y_bf16, nullptr);
   SC_CHECK_LAUNCH("ln_fwd_kernel");
   return SC_OK;
 }
 
 extern "C" int sc_layernorm_bwd(const float* dy, const void* dy_bf16, const void* a, int32_t a_dtype, const void* b,
                                 int32_t b_dtype,
-                                const float* gamma, const float* mean, const float* rstd, float* dx, float* dgamma,
+                                const float* gamma, const float* mean, const float* rstd, float* dx, void* dx_bf16, float* dgamma,
                                 float* dbeta, float* partials, int32_t rows, int32_t cols, void* stream) {
-  SC_CHECK_ARG(dy && a && gamma && mean && rstd && dx && dgamma && dbeta && partials, "sc_layernorm_bwd: null pointer");
+  SC_CHECK_ARG(dy && a && gamma && mean && rstd && (dx || dx_bf16) && dgamma && dbeta && partials,
+               "sc_layernorm_bwd: null pointer");
   SC_CHECK_ARG(rows >= 0 && cols >= 1, "sc_layernorm_bwd: bad shape");
   if (cols > kLnMaxV * 32 || cols % 4 ||
-      ((uintptr_t)a | (uintptr_t)b | (uintptr_t)dy | (uintptr_t)dy_bf16 | (uintptr_t)dx | (uintptr_t)gamma) % 8) {
+      ((uintptr_t)a | (uintptr_t)b | (uintptr_t)dy | (uintptr_t)dy_bf16 | (uintptr_t)dx | (uintptr_t)dx_bf16 |
+       (uintptr_t)gamma) % 8) {
     set_error("sc_layernorm_bwd: needs cols %% 4 == 0, cols <= %d and 8-byte aligned rows", kLnMaxV * 32);
     return SC_ERR_UNSUPPORTED;
   }
@@ -310,7 +323,8 @@ extern "C" int sc_layernorm_bwd(const float* dy, const void* dy_bf16, const void
   float* pb = partials + (int64_t)nparts * cols;
   if (rows > 0)
     ln_dispatch(a_dtype == SC_DTYPE_F32, !b || b_dtype == SC_DTYPE_F32, false, a, b, gamma, nullptr, dy, nullptr,
-                (float*)mean, (float*)rstd, dx, pg, pb, rows, cols, 0.f, (unsigned)nparts, st, (void*)dy_bf16);
+                (float*)mean, (float*)rstd, dx, pg, pb, rows, cols, 0.f, (unsigned)nparts, st, (void*)dy_bf16,
+                dx_bf16);
   SC_CHECK_LAUNCH("ln_bwd_kernel");
   colsum_reduce_kernel<<<(cols + 31) / 32, 256, 0, st>>>(pg, nparts, cols, dgamma);
   SC_CHECK_LAUNCH("colsum_reduce_kernel");

@@ -161,14 +161,19 @@ class ResidualLayerNorm(torch.autograd.Function):
         rows, cols = a.shape
         dy = torch.zeros(rows, cols, dtype=torch.float32, device=a.device) if dy is None else dy.float().contiguous()
         dy16 = None if dy16 is None else dy16.to(torch.bfloat16).contiguous()
-        dx = torch.empty(rows, cols, dtype=torch.float32, device=a.device)
+        # the kernel writes the input gradient in fp32 and/or bf16, as the inputs' dtypes need
+        dtypes = {a.dtype} | ({b.dtype} if b is not None else set())
+        dx = torch.empty(rows, cols, dtype=torch.float32, device=a.device) if torch.float32 in dtypes else None
+        dx16 = torch.empty(rows, cols, dtype=torch.bfloat16, device=a.device) if torch.bfloat16 in dtypes else None
         dg = torch.empty(cols, dtype=torch.float32, device=a.device)
         db = torch.empty_like(dg)
         parts = torch.empty(2 * _lib.load().sc_ln_partials(rows) * cols, dtype=torch.float32, device=a.device)
         _lib.call("sc_layernorm_bwd", dy.data_ptr(), _lib.ptr(dy16), a.data_ptr(), _dcode(a), _lib.ptr(b),
-                  0 if b is None else _dcode(b), gamma.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
-                  dg.data_ptr(), db.data_ptr(), parts.data_ptr(), rows, cols, _lib.stream_handle(), exc=EncoderError)
-        return dx.to(a.dtype), (None if b is None else dx.to(b.dtype)), dg, db, None
+                  0 if b is None else _dcode(b), gamma.data_ptr(), mean.data_ptr(), rstd.data_ptr(), _lib.ptr(dx),
+                  _lib.ptr(dx16), dg.data_ptr(), db.data_ptr(), parts.data_ptr(), rows, cols, _lib.stream_handle(),
+                  exc=EncoderError)
+        pick = lambda t: dx if t.dtype == torch.float32 else dx16  # noqa: E731
+        return pick(a), (None if b is None else pick(b)), dg, db, None
 
 
 def residual_layer_norm(a, b, gamma, beta, want16=False):
