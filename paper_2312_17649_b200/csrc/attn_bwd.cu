@@ -65,7 +65,6 @@ struct BwdArgs {
   float2* stats;  // [T*H]: (lse, D); lse = +inf for rows without keys
   int mode;       // 0: every row; 1: only the head rows (cls + query group) of every sequence
   int maxh;       // mode 1: 1 + max qgroup_len (items per sequence)
-  int skip_doc_sources;  // dK/dV kernel: doc-row sources are summed elsewhere (tiled path partials)
 };
 
 // Item -> (row, head).  Mode 1 enumerates nseq x maxh slots, skipping slots past a sequence's head rows.
@@ -116,10 +115,10 @@ __device__ __forceinline__ int key_ranges(const AttnArgs& a, const SeqGroups& g,
 
 // Source ranges whose slots address key (tg, r) of sequence j (the transposed pattern).
 __device__ __forceinline__ int source_ranges(const AttnArgs& a, const SeqGroups& g, int j, int tg, int r,
-                                             bool key_global, bool skip_doc, Range (&out)[5]) {
+                                             bool key_global, Range (&out)[5]) {
   const bool qds = a.glob_cu != nullptr;
   int n = 0;
-  for (int gs = 0; gs < (skip_doc ? 2 : 3); ++gs) {
+  for (int gs = 0; gs < 3; ++gs) {
     const int w = a.links.w[gs][tg];
     const bool qds_doc = qds && gs == 2;
     if (w == SC_LINK_NONE || (qds_doc && tg == 2 && w >= 0 && key_global)) continue;
@@ -427,7 +426,7 @@ __global__ void __launch_bounds__(ItemSlot<NS>::kWarpsPerCta * 32) attn_bwd_dkv_
   for (int e = 0; e < E; ++e) { dk[e] = 0.f; dv[e] = 0.f; }
 
   Range R[5];
-  const int nr = source_ranges(a, g, j, tg, r, key_global, b.skip_doc_sources != 0, R);
+  const int nr = source_ranges(a, g, j, tg, r, key_global, R);
   int unit = 0;
   for (int ri = 0; ri < nr; ++ri) {
     visit(a, R[ri], lane, split, NS, unit,
@@ -516,9 +515,7 @@ constexpr int kSplitMinAvgLen = 768;
 
 template <typename T, int E>
 int launch_generic(const BwdArgs& b, int which, cudaStream_t st) {
-  // (the head keys' dK/dV pass without doc sources only sees the short cls / query ranges)
-  const bool split = b.mode == 1 && (int64_t)b.a.T >= (int64_t)kSplitMinAvgLen * b.a.nseq &&
-                     !(which == 1 && b.skip_doc_sources);
+  const bool split = b.mode == 1 && (int64_t)b.a.T >= (int64_t)kSplitMinAvgLen * b.a.nseq;
   if (!split) {
     const int64_t items = b.mode == 0 ? (int64_t)b.a.T * b.a.H : (int64_t)b.a.nseq * b.maxh * b.a.H;
     const unsigned blocks = (unsigned)((items + kBwdWarps - 1) / kBwdWarps);
