@@ -512,3 +512,37 @@ def test_attention_backward_long_sequences_split_head_pass(P, pattern, window, p
     g16b = torch.empty_like(g16)
     attention_backward(qkv, out16, dout, g16b, lay, pat, H, 8.0, padding)
     assert torch.equal(g16, g16b)
+
+
+def test_attention_backward_minimal_workspace_fallback(P):
+    """sc_attn_bwd with only the T*H*8-byte statistics workspace: no head-key partials, no split
+    head pass -> the generic head-key pass; same gradients as with the full workspace."""
+    from paper_2312_17649_b200 import _lib
+
+    rng = np.random.default_rng(9)
+    m = rng.integers(1, 12, size=5)
+    n = rng.integers(50, 400, size=5)
+    seq = m + n + 3
+    H, d = 2, 64
+    lay = P.PackedLayout.from_lengths(seq, m + 1, device="cuda")
+    pat = P.make_pattern("sparse", 4)
+    T = int(seq.sum())
+    qkv = torch.randn(T, 3 * H * d, device="cuda").bfloat16()
+    dout = torch.randn(T, H * d, device="cuda").bfloat16()
+    out = P.attend_packed(qkv[:, :H * d], qkv[:, H * d:2 * H * d], qkv[:, 2 * H * d:], lay, pat, H)
+
+    def run(ws_bytes):
+        g = torch.empty(T, 3 * H * d, device="cuda")
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+        base, gb = qkv.data_ptr(), g.data_ptr()
+        _lib.call("sc_attn_bwd", base, base + H * d * 2, base + 2 * H * d * 2, qkv.stride(0), out.data_ptr(),
+                  out.stride(0), dout.data_ptr(), dout.stride(0), gb, gb + H * d * 4, gb + 2 * H * d * 4,
+                  g.stride(0), _lib.DTYPE_F32, lay.cu_seqlens.data_ptr(), lay.qgroup_len.data_ptr(), lay.nseq, T,
+                  H, d, pat.links().ctypes.data, _lib.PAD_EXCLUDE, 8.0, _lib.DTYPE_BF16, None, None, None,
+                  lay.seq_tile_base.data_ptr(), lay.tile_rows, lay.max_qgroup_len, lay.n_tiles, ws.data_ptr(),
+                  ws_bytes, _lib.stream_handle())
+        return g
+
+    full = run(_lib.load().sc_attn_bwd_workspace_bytes(T, H, lay.nseq, lay.max_qgroup_len))
+    small = run(T * H * 8)
+    close(small.cpu().numpy(), full.cpu().numpy(), 2e-2)  # bf16 P / dS in the mma paths
