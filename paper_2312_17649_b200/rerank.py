@@ -12,6 +12,7 @@ position); a candidate that cannot be scored gets -inf (R/evaluation.py:194-201)
 from __future__ import annotations
 
 import math
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -56,7 +57,8 @@ def parse_run(lines) -> list:
     return out
 
 
-def write_run(path, entries) -> None:
+def write_run(entries, path) -> None:
+    """R/evaluation.py:63-65 (same argument order)."""
     with open(path, "w", encoding="utf-8") as fh:
         fh.write(format_run(entries))
 
@@ -64,6 +66,57 @@ def write_run(path, entries) -> None:
 def read_run(path) -> list:
     with open(path, encoding="utf-8") as fh:
         return parse_run(fh)
+
+
+def parse_qrels(lines) -> dict:
+    """TREC qrels ``qid iter docid rel`` -> {qid: {docid: rel}} (R/evaluation.py:68-82)."""
+    qrels: dict = {}
+    for n, line in enumerate(lines, 1):
+        line = line.strip()
+        if not line:
+            continue
+        parts = line.split()
+        if len(parts) != 4:
+            raise EvaluationError(f"qrels line {n}: expected 4 fields, got {len(parts)}")
+        qid, _iter, did, rel = parts
+        rel = int(rel)
+        if rel < 0:
+            raise EvaluationError(f"qrels line {n}: negative relevance")
+        qrels.setdefault(qid, {})[did] = rel
+    return qrels
+
+
+def read_qrels(path) -> dict:
+    with open(path, encoding="utf-8") as fh:
+        return parse_qrels(fh)
+
+
+def _dcg(gains) -> float:
+    """sum (2^g - 1) / log2(rank + 1) (R/evaluation.py:94-95)."""
+    return sum((2.0 ** g - 1.0) / math.log2(r + 1) for r, g in enumerate(gains, 1))
+
+
+def ndcg_at_k(run, qrels, k: int = 10):
+    """(per-query nDCG@k, mean over the run's queries) (R/evaluation.py:98-123): documents in rank
+    order, the ideal from all judged documents; queries missing from qrels score 0 (with a warning)."""
+    if k < 1:
+        raise EvaluationError("k must be >= 1")
+    by_query: dict = {}
+    for e in run:
+        by_query.setdefault(e.query_id, []).append(e)
+    per_query = {}
+    for qid, entries in by_query.items():
+        entries = sorted(entries, key=lambda e: e.rank)
+        judged = qrels.get(qid)
+        if judged is None:
+            warnings.warn(f"query {qid} missing from qrels; scoring 0", stacklevel=2)
+            per_query[qid] = 0.0
+            continue
+        gains = [judged.get(e.doc_id, 0) for e in entries[:k]]
+        idcg = _dcg(sorted(judged.values(), reverse=True)[:k])
+        per_query[qid] = _dcg(gains) / idcg if idcg > 0 else 0.0
+    mean = sum(per_query.values()) / len(per_query) if per_query else 0.0
+    return per_query, mean
 
 
 def rank_entries(query_id: str, doc_ids, scores, top_k: int = 100, tag: str = "sparsecross") -> list:

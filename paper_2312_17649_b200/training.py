@@ -676,23 +676,19 @@ class SyntheticTask:
         return pools
 
 
-def _dcg(gains) -> float:
-    """sum (2^g - 1) / log2(rank + 1) (R/evaluation.py:94-95)."""
-    return sum((2.0 ** g - 1.0) / math.log2(r + 1) for r, g in enumerate(gains, 1))
-
-
 def validation_ndcg(model, val_set, k: int = 10):
     """(per-query nDCG@k, mean); pools ranked by (-score, position) (R/training.py:230-255)."""
-    per_query = {}
+    from .rerank import RunEntry, ndcg_at_k
+
+    run, qrels = [], {}
     for vq in val_set:
         seqs = [assemble_input(vq.query, doc, model.config.max_positions) for _, doc in vq.candidates]
         scores = model.score(np.stack([s.ids for s in seqs]), seqs[0].partition)
         order = sorted(range(len(seqs)), key=lambda j: (-float(scores[j]), j))
-        gains = [vq.relevance.get(vq.candidates[j][0], 0) for j in order[:k]]
-        idcg = _dcg(sorted(vq.relevance.values(), reverse=True)[:k])
-        per_query[vq.query_id] = _dcg(gains) / idcg if idcg > 0 else 0.0
-    mean = sum(per_query.values()) / len(per_query) if per_query else 0.0
-    return per_query, mean
+        for rank, j in enumerate(order, 1):
+            run.append(RunEntry(vq.query_id, vq.candidates[j][0], rank, float(scores[j])))
+        qrels[vq.query_id] = dict(vq.relevance)
+    return ndcg_at_k(run, qrels, k)
 
 
 # ---------------------------------------------------------------------------

@@ -68,7 +68,7 @@ def main():
     secs = float(t.item())
     if rank == 0:
         if args.run_file:
-            write_run(args.run_file, entries)
+            write_run(entries, args.run_file)
         pairs = args.queries * args.docs
         print(json.dumps({
             "metric": "re-ranked query-doc pairs/sec (whole job, wall clock)", "value": pairs / secs,

@@ -41,7 +41,7 @@ def _worker(rank, world, port, queries, out_path):
     if rank == 0:
         from paper_2312_17649_b200.rerank import write_run
 
-        write_run(out_path, entries)
+        write_run(entries, out_path)
     else:
         assert entries is None
     dist.barrier()

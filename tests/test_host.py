@@ -130,3 +130,48 @@ def test_pack_pairs_matches_assemble_input():
         np.testing.assert_array_equal(a.qgroup_lens, b.qgroup_lens)
     with pytest.raises(ValueError):
         pack_pairs(rng.integers(3, 9, size=30), docs, 20)
+
+
+class TestTrecEvaluation:
+    """TREC qrels IO and nDCG@k (R/evaluation.py:68-123; hand values from T/test_evaluation.py:29-62)."""
+
+    @staticmethod
+    def run_for(qid, docs_scores):
+        from paper_2312_17649_b200.rerank import RunEntry
+
+        return [RunEntry(qid, did, rank, score) for rank, (did, score) in enumerate(docs_scores, 1)]
+
+    def test_ideal_and_worked_example(self):
+        from paper_2312_17649_b200.rerank import ndcg_at_k
+
+        qrels = {"q1": {"a": 3, "b": 2, "c": 1, "d": 0}}
+        per_query, mean = ndcg_at_k(self.run_for("q1", [("a", 4.0), ("b", 3.0), ("c", 2.0), ("d", 1.0)]), qrels, 4)
+        assert per_query["q1"] == pytest.approx(1.0) and mean == pytest.approx(1.0)
+        qrels = {"q": {"d1": 0, "d2": 2, "d3": 1}}
+        per_query, _ = ndcg_at_k(self.run_for("q", [("d1", 3.0), ("d2", 2.0), ("d3", 1.0)]), qrels, 3)
+        assert per_query["q"] == pytest.approx(0.6590018048024133, abs=1e-10)
+        per_query, _ = ndcg_at_k(self.run_for("q1", [("a", 2.0), ("b", 1.0)]), {"q1": {"x": 2}}, 2)
+        assert per_query["q1"] == 0.0
+
+    def test_missing_query_and_bad_k(self):
+        from paper_2312_17649_b200.rerank import EvaluationError, ndcg_at_k
+
+        with pytest.warns(UserWarning):
+            per_query, mean = ndcg_at_k(self.run_for("ghost", [("a", 1.0)]), {}, 10)
+        assert per_query["ghost"] == 0.0 and mean == 0.0
+        with pytest.raises(EvaluationError):
+            ndcg_at_k([], {}, 0)
+
+    def test_qrels_and_run_round_trip(self, tmp_path):
+        from paper_2312_17649_b200.rerank import (EvaluationError, parse_qrels, read_qrels, read_run, write_run)
+
+        p = tmp_path / "qrels.txt"
+        p.write_text("q1 0 d1 2\n\nq1 0 d2 0\nq2 0 d9 1\n")
+        assert read_qrels(p) == {"q1": {"d1": 2, "d2": 0}, "q2": {"d9": 1}}
+        with pytest.raises(EvaluationError):
+            parse_qrels(["q1 0 d1"])
+        with pytest.raises(EvaluationError):
+            parse_qrels(["q1 0 d1 -1"])
+        entries = self.run_for("q1", [("d1", 0.5), ("d2", 0.25)])
+        write_run(entries, tmp_path / "run.txt")  # the reference's argument order
+        assert read_run(tmp_path / "run.txt") == entries
