@@ -16,12 +16,16 @@ from .attention import (
     apply_pattern,
     attend_packed,
     attend_segments,
+    attend_segments_backward,
     full_pattern,
     full_attention,
     group_attention,
+    group_attention_backward,
     longformer_pattern,
     make_pattern,
     masked_segment_softmax,
+    masked_segment_softmax_backward,
+    qds_band_exclusions,
     qds_pattern,
     sparse_pattern,
     windowed_cross_attention,
@@ -48,11 +52,18 @@ from .encoder import (
     TokenSequence,
     assemble_input,
     encoder_forward,
+    gelu,
+    gelu_grad,
     init_weights,
     interpolate_positions,
+    layer_backward,
+    layer_forward,
+    layer_norm,
+    layer_norm_backward,
     qds_global_positions,
     relevance_score,
     resolve_pattern,
+    weight_nbytes,
 )
 from .layout import PackedLayout
 from .serialize import SerializationError, load_model, save_model

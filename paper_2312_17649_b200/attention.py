@@ -223,7 +223,7 @@ def _compute_dtype(t: torch.Tensor):
     return t if t.dtype in (torch.float32, torch.bfloat16) else t.float()
 
 
-def _run_groups(qkv: dict, pattern: AttentionPattern, scale: float, padding: str):
+def _run_groups(qkv: dict, pattern: AttentionPattern, scale: float, padding: str, store=None):
     """Pack the three groups of (Q, K, V) views, run the kernel, return per-group outputs."""
     for g in GROUPS:
         if g not in qkv:
@@ -262,6 +262,9 @@ def _run_groups(qkv: dict, pattern: AttentionPattern, scale: float, padding: str
     if pattern.global_positions and max(pattern.global_positions) >= lens[2]:
         raise AttentionError("global positions outside the document group")
     out = attend_packed(cat[0], cat[1], cat[2], layout, pattern, H, scale, padding)
+    if store is not None:  # what group_attention_backward needs
+        store.update(layout=layout, qkv=torch.cat(cat, dim=1).contiguous(), out=out, H=H, d=d, lens=lens, lead=lead,
+                     was_np=was_np, np_dtype=np.dtype(str(orig_dtype).replace("torch.", "")))
     out = out.reshape(s, H, d).permute(1, 0, 2).reshape(*lead, s, d) if len(lead) else out.reshape(s, d)
     outs, lo = [], 0
     for n in lens:
@@ -274,12 +277,49 @@ def _run_groups(qkv: dict, pattern: AttentionPattern, scale: float, padding: str
 
 
 def group_attention(qkv: dict, source: str, pattern: AttentionPattern, scale: float,
-                    padding: str = "exclude"):
-    """Output of one source group under a pattern (R/attention.py:416-473)."""
+                    padding: str = "exclude", want_cache: bool = False):
+    """Output of one source group under a pattern (R/attention.py:416-473).  ``want_cache``
+    also returns what ``group_attention_backward`` needs (the packed q/k/v and output)."""
     if source not in GROUPS:
         raise AttentionError(f"unknown source group {source!r}")
     pattern.targets_of(source)
-    return _run_groups(qkv, pattern, scale, padding)[GROUPS.index(source)]
+    if not want_cache:
+        return _run_groups(qkv, pattern, scale, padding)[GROUPS.index(source)]
+    store = {}
+    outs = _run_groups(qkv, pattern, scale, padding, store=store)
+    store.update(pattern=pattern, scale=scale, padding=padding)
+    return outs[GROUPS.index(source)], store
+
+
+def group_attention_backward(cache, grad_out, source: str, pattern: AttentionPattern):
+    """Adjoint of group_attention (R/attention.py:476-507) on the fused device kernel
+    (sc_attn_bwd): (grad_q, [(target_group, None, grad_k, grad_v) for every group]).  The
+    reference lists one entry per segment (plus the QDS globals by index); the per-target
+    sums, which is what layer_backward accumulates, are identical."""
+    from .training import attention_backward
+
+    lay, qkv, out = cache["layout"], cache["qkv"], cache["out"]
+    H, d, lens, lead = cache["H"], cache["d"], cache["lens"], cache["lead"]
+    s = sum(lens)
+    lo = sum(lens[:GROUPS.index(source)])
+    go = _to_device(grad_out)[0].float().reshape(H, lens[GROUPS.index(source)], d)
+    dout = torch.zeros(s, H, d, dtype=qkv.dtype, device=qkv.device)
+    dout[lo:lo + go.shape[1]] = go.permute(1, 0, 2).to(qkv.dtype)
+    g = torch.empty(s, 3 * H * d, dtype=torch.float32, device=qkv.device)
+    attention_backward(qkv, out, dout.reshape(s, H * d), g, lay, cache["pattern"], H, cache["scale"],
+                       cache["padding"])
+    parts = g.reshape(s, 3, H, d).permute(1, 2, 0, 3)  # (3, H, s, d)
+
+    def cut(t, a, n):
+        t = t[:, a:a + n, :].reshape(*lead, n, d) if len(lead) else t[0, a:a + n, :]
+        return t.cpu().numpy().astype(cache["np_dtype"], copy=False) if cache["was_np"] else t
+
+    gq = cut(parts[0], lo, lens[GROUPS.index(source)])
+    contrib, a = [], 0
+    for gname, n in zip(GROUPS, lens):
+        contrib.append((gname, None, cut(parts[1], a, n), cut(parts[2], a, n)))
+        a += n
+    return gq, contrib
 
 
 def apply_pattern(partition, qkv: dict, pattern: AttentionPattern, scale: float | None = None,
@@ -327,24 +367,44 @@ def masked_segment_softmax(values, valids, scale: float, padding: str = "exclude
     return [e / denom for e in exps]
 
 
-def attend_segments(q, segments, scale: float, padding: str = "exclude"):
+def masked_segment_softmax_backward(probs, grad_probs):
+    """Adjoint of the joint softmax w.r.t. the scaled logits (R/attention.py:260-269):
+    p * (g - sum over all segments of p * g); invalid slots (p = 0) get 0."""
+    ts = [(_to_device(p)[0].float(), _to_device(g)[0].float()) for p, g in zip(probs, grad_probs)]
+    dot = sum((p * g).sum(dim=-1, keepdim=True) for p, g in ts)
+    out = [p * (g - dot) for p, g in ts]
+    if probs and not isinstance(probs[0], torch.Tensor):
+        return [o.cpu().numpy().astype(np.asarray(p).dtype, copy=False) for o, p in zip(out, probs)]
+    return out
+
+
+def attend_segments(q, segments, scale: float, padding: str = "exclude", want_cache: bool = False):
     """Windowed cross-attention core (R/attention.py:290-345).
 
     segments: nonempty list of (k, v, window, extra_invalid); extra_invalid is an
     optional bool (rows, 2w+1) mask of additionally excluded band slots (hard
     exclusions in both padding modes) and must be None for unwindowed segments.
-    numpy in -> numpy out (float64 results are computed in fp32 on the device)."""
-    from .band import band_apply, band_scores, band_validity
+    numpy in -> numpy out (float64 results are computed in fp32 on the device).
+    ``want_cache`` also returns the cache ``attend_segments_backward`` consumes
+    (the computation then carries autograd through the device band adjoints)."""
+    from .band import band_apply, band_apply_ad, band_scores, band_scores_ad, band_validity
 
     if not segments:
         raise AttentionError("segment tuple must be nonempty")
+    if want_cache:
+        band_scores, band_apply = band_scores_ad, band_apply_ad  # noqa: F811
     qt, was_np = _to_device(q)
     qf = qt.float()
+    if want_cache:
+        qf = qf.detach().requires_grad_(True)
     s = qf.shape[-2]
-    values, valids, metas = [], [], []
+    values, valids, metas, leaves = [], [], [], []
     for k, v, window, extra in segments:
         kt = _to_device(k)[0].float()
         vt = _to_device(v)[0].float()
+        if want_cache:
+            kt, vt = kt.detach().requires_grad_(True), vt.detach().requires_grad_(True)
+            leaves.append((kt, vt))
         if qf.shape[-1] != kt.shape[-1]:
             raise AttentionError("query/key feature dims differ")
         if kt.shape[-2] != vt.shape[-2]:
@@ -367,14 +427,42 @@ def attend_segments(q, segments, scale: float, padding: str = "exclude"):
         values.append(sc)
         valids.append(ok)
         metas.append((vt, window))
-    probs = masked_segment_softmax(values, valids, scale, padding)
-    out = None
-    for p, (vt, window) in zip(probs, metas):
-        part = torch.matmul(p, vt) if is_full(window) else band_apply(p.contiguous(), vt, int(window))
-        out = part if out is None else out + part
-    if was_np:
-        return out.cpu().numpy().astype(np.asarray(q).dtype, copy=False)
-    return out
+    with torch.set_grad_enabled(want_cache):
+        probs = masked_segment_softmax(values, valids, scale, padding)
+        out = None
+        for p, (vt, window) in zip(probs, metas):
+            part = torch.matmul(p, vt) if is_full(window) else band_apply(p.contiguous(), vt, int(window))
+            out = part if out is None else out + part
+    res = out.detach().cpu().numpy().astype(np.asarray(q).dtype, copy=False) if was_np else out.detach()
+    if not want_cache:
+        return res
+    return res, {"q": qf, "leaves": leaves, "out": out, "was_np": was_np,
+                 "dtype": np.asarray(q).dtype if was_np else None}
+
+
+def attend_segments_backward(cache, grad_out):
+    """Adjoint of attend_segments (R/attention.py:348-378): (grad_q, [(grad_k, grad_v), ...]) in
+    segment order, through autograd over the device band adjoints and cuBLAS."""
+    g = _to_device(grad_out)[0].float()
+    inputs = [cache["q"]] + [t for kv in cache["leaves"] for t in kv]
+    grads = torch.autograd.grad(cache["out"], inputs, grad_outputs=g, allow_unused=True)
+    grads = [torch.zeros_like(t) if gr is None else gr for t, gr in zip(inputs, grads)]
+    conv = (lambda t: t.cpu().numpy().astype(cache["dtype"], copy=False)) if cache["was_np"] else (lambda t: t)
+    gq = conv(grads[0])
+    kv = [(conv(grads[1 + 2 * i]), conv(grads[2 + 2 * i])) for i in range(len(cache["leaves"]))]
+    return gq, kv
+
+
+def qds_band_exclusions(doc_len: int, window: int, global_positions):
+    """Band slots of the doc-doc segment that hit global tokens (R/attention.py:403-413)."""
+    if not len(global_positions):
+        return None
+    w = int(window)
+    targets = np.arange(doc_len)[:, None] + np.arange(2 * w + 1)[None, :] - w
+    is_global = np.zeros(doc_len + 1, dtype=bool)
+    is_global[list(global_positions)] = True
+    valid = (targets >= 0) & (targets < doc_len)
+    return is_global[np.clip(targets, 0, doc_len)] & valid
 
 
 def windowed_cross_attention(q, kv, padding: str = "exclude"):

@@ -146,3 +146,45 @@ def band_pv_backward(grad_out: torch.Tensor, p: torch.Tensor, v: torch.Tensor, w
     if grad_out.dim() != 2 or p.dim() != 2 or v.dim() != 2:
         raise BandShapeError("grad_out, P and V must be 2-D")
     return band_apply_backward(grad_out, p, v, window)
+
+
+class _BandScoresFn(torch.autograd.Function):
+    """band_scores with its adjoint on the device (sc_band_scores_backward)."""
+
+    @staticmethod
+    def forward(ctx, q, k, window):
+        ctx.save_for_backward(q, k)
+        ctx.window = window
+        return band_scores(q, k, window)
+
+    @staticmethod
+    def backward(ctx, g):
+        q, k = ctx.saved_tensors
+        gq, gk = band_scores_backward(g.contiguous().to(q.dtype), q, k, ctx.window)
+        return gq, gk, None
+
+
+class _BandApplyFn(torch.autograd.Function):
+    """band_apply with its adjoint on the device (sc_band_apply_backward)."""
+
+    @staticmethod
+    def forward(ctx, p, v, window):
+        ctx.save_for_backward(p, v)
+        ctx.window = window
+        return band_apply(p, v, window)
+
+    @staticmethod
+    def backward(ctx, g):
+        p, v = ctx.saved_tensors
+        gp, gv = band_apply_backward(g.contiguous().to(p.dtype), p, v, ctx.window)
+        return gp, gv, None
+
+
+def band_scores_ad(q: torch.Tensor, k: torch.Tensor, window: int) -> torch.Tensor:
+    """Differentiable band_scores (autograd through the device adjoint kernels)."""
+    return _BandScoresFn.apply(q, k, window)
+
+
+def band_apply_ad(p: torch.Tensor, v: torch.Tensor, window: int) -> torch.Tensor:
+    """Differentiable band_apply (autograd through the device adjoint kernels)."""
+    return _BandApplyFn.apply(p, v, window)

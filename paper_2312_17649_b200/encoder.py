@@ -609,3 +609,40 @@ def relevance_score(last_layer, head_w, head_b=0.0) -> float:
     if last.ndim != 2 or last.shape[0] < 1:
         raise EncoderError("last layer matrix must be 2-D with a [CLS] row")
     return float(last[0] @ np.asarray(head_w) + head_b)
+
+
+# Reference-shaped layer primitives and adjoints (R/encoder.py:250-443) -- implemented on the device
+# in training.py (imported lazily: training builds on this module).
+def weight_nbytes(weights: dict) -> int:
+    from .training import weight_nbytes as f
+    return f(weights)
+
+
+def gelu(x):
+    from .training import gelu as f
+    return f(x)
+
+
+def gelu_grad(x):
+    from .training import gelu_grad as f
+    return f(x)
+
+
+def layer_norm(x, gain, bias):
+    from .training import layer_norm as f
+    return f(x, gain, bias)
+
+
+def layer_norm_backward(grad_y, cache, gain):
+    from .training import layer_norm_backward as f
+    return f(grad_y, cache, gain)
+
+
+def layer_forward(x, partition, pattern, weights, layer_index, config, want_cache=False):
+    from .training import layer_forward as f
+    return f(x, partition, pattern, weights, layer_index, config, want_cache)
+
+
+def layer_backward(grad_out, cache, partition, pattern, weights, layer_index, config, grads):
+    from .training import layer_backward as f
+    return f(grad_out, cache, partition, pattern, weights, layer_index, config, grads)

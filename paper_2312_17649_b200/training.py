@@ -306,6 +306,37 @@ class ParamDict(dict):
         return self.shadow_views
 
 
+def _layer_block(x, xh, W, S, p, layout, pattern, H, scale, cfg, check_keys):
+    """One post-LN layer (R/encoder.py:306-371) on the device, differentiable: returns (x, the GEMM
+    input copy of x).  W: fp32 parameters by reference name; S: their bf16 shadows or None."""
+    bf16 = cfg.precision == "bf16"
+    cd = torch.bfloat16 if bf16 else torch.float32
+
+    def lin(xin, wname, bname):
+        return Linear.apply(xin, W[wname], None if S is None else S[wname], W[bname],
+                            None if S is None else S[bname], cd)
+
+    wqkv = torch.cat([W[p + "wq"], W[p + "wk"], W[p + "wv"]], dim=1)
+    bqkv = torch.cat([W[p + "bq"], W[p + "bk"], W[p + "bv"]])
+    w16 = None if S is None else torch.cat([S[p + "wq"], S[p + "wk"], S[p + "wv"]], dim=1)
+    b16 = None if S is None else torch.cat([S[p + "bq"], S[p + "bk"], S[p + "bv"]])
+    qkv = Linear.apply(xh, wqkv, w16, bqkv, b16, cd)
+    o = PatternAttention.apply(qkv, layout, pattern, H, scale, cfg.padding, check_keys)
+    if bf16:
+        ln1, ln1h = residual_layer_norm(x, lin(o, p + "wo", p + "bo"), W[p + "ln1_g"], W[p + "ln1_b"], want16=True)
+    else:
+        ln1 = ln1h = residual_layer_norm(x, lin(o, p + "wo", p + "bo"), W[p + "ln1_g"], W[p + "ln1_b"])
+    if _gelu_ok(cfg.ff_dim):
+        g1 = LinearGelu.apply(ln1h, W[p + "w1"], None if S is None else S[p + "w1"], W[p + "b1"],
+                              None if S is None else S[p + "b1"], cd)
+    else:
+        g1 = F.gelu(lin(ln1h, p + "w1", p + "b1"))
+    if bf16:
+        return residual_layer_norm(ln1, lin(g1, p + "w2", p + "b2"), W[p + "ln2_g"], W[p + "ln2_b"], want16=True)
+    x = residual_layer_norm(ln1, lin(g1, p + "w2", p + "b2"), W[p + "ln2_g"], W[p + "ln2_b"])
+    return x, x
+
+
 class GradDict(dict):
     """Gradients that are views of one flat fp32 buffer in ParamDict order (``flat``)."""
 
@@ -372,39 +403,13 @@ class TrainableCrossEncoder:
         bf16 = cfg.precision == "bf16"
         scale = math.sqrt(cfg.head_dim)
         x = W["tok_emb"][ids_dev.long()] + W["pos_emb"][layout.tok_pos.long()]
-        cd = torch.bfloat16 if bf16 else torch.float32
         S = W.bf16_views() if (bf16 and isinstance(W, ParamDict)) else None
-
-        def lin(xin, wname, bname):
-            return Linear.apply(xin, W[wname], None if S is None else S[wname], W[bname],
-                                None if S is None else S[bname], cd)
 
         flags = []
         xh = x  # GEMM input of the layer (bf16 copy of the previous LayerNorm in the bf16 path)
         with self.gemm_mode():
             for i in range(cfg.layers):
-                p = f"L{i}."
-                wqkv = torch.cat([W[p + "wq"], W[p + "wk"], W[p + "wv"]], dim=1)
-                bqkv = torch.cat([W[p + "bq"], W[p + "bk"], W[p + "bv"]])
-                w16 = None if S is None else torch.cat([S[p + "wq"], S[p + "wk"], S[p + "wv"]], dim=1)
-                b16 = None if S is None else torch.cat([S[p + "bq"], S[p + "bk"], S[p + "bv"]])
-                qkv = Linear.apply(xh, wqkv, w16, bqkv, b16, cd)
-                o = PatternAttention.apply(qkv, layout, self.pattern, H, scale, cfg.padding, i == 0)
-                if bf16:
-                    ln1, ln1h = residual_layer_norm(x, lin(o, p + "wo", p + "bo"), W[p + "ln1_g"], W[p + "ln1_b"],
-                                                    want16=True)
-                else:
-                    ln1 = ln1h = residual_layer_norm(x, lin(o, p + "wo", p + "bo"), W[p + "ln1_g"], W[p + "ln1_b"])
-                if _gelu_ok(cfg.ff_dim):
-                    g1 = LinearGelu.apply(ln1h, W[p + "w1"], None if S is None else S[p + "w1"], W[p + "b1"],
-                                          None if S is None else S[p + "b1"], cd)
-                else:
-                    g1 = F.gelu(lin(ln1h, p + "w1", p + "b1"))
-                if bf16:
-                    x, xh = residual_layer_norm(ln1, lin(g1, p + "w2", p + "b2"), W[p + "ln2_g"], W[p + "ln2_b"],
-                                                want16=True)
-                else:
-                    x = xh = residual_layer_norm(ln1, lin(g1, p + "w2", p + "b2"), W[p + "ln2_g"], W[p + "ln2_b"])
+                x, xh = _layer_block(x, xh, W, S, f"L{i}.", layout, self.pattern, H, scale, cfg, i == 0)
                 if check_finite:
                     flags.append(torch.isfinite(x.detach()).all())
         if flags:
@@ -960,3 +965,147 @@ def grad_check(model: TrainableCrossEncoder, triples, eps: float = 1e-3, samples
         err = abs(analytic - fd) if denom < 1e-6 else abs(analytic - fd) / denom
         worst = max(worst, err)
     return worst
+
+
+# ---------------------------------------------------------------------------
+# Reference-shaped layer primitives (R/encoder.py:250-443) on the device; numpy in -> numpy out.
+# ---------------------------------------------------------------------------
+
+def _dev(a):
+    if torch.is_tensor(a):
+        return a, False, None
+    arr = np.asarray(a)
+    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).cuda(), True, arr.dtype
+
+
+def _back(t, was_np, dt):
+    return t.detach().cpu().numpy().astype(dt, copy=False) if was_np else t
+
+
+def _padded_flat(t, mult):
+    n = t.numel()
+    buf = torch.zeros(((n + mult - 1) // mult) * mult, dtype=torch.float32, device=t.device)
+    buf[:n] = t.reshape(-1).float()
+    return buf, n
+
+
+def gelu(x):
+    """Exact-erf GELU (R/encoder.py:258-259) by sc_gelu_fwd."""
+    t, was_np, dt = _dev(x)
+    buf, n = _padded_flat(t, 1024)
+    out = torch.empty_like(buf)
+    _lib.call("sc_gelu_fwd", buf.data_ptr(), out.data_ptr(), _lib.DTYPE_F32, buf.numel(), _lib.stream_handle(),
+              exc=EncoderError)
+    return _back(out[:n].reshape(t.shape), was_np, dt)
+
+
+def gelu_grad(x):
+    """d gelu / dx = Phi(x) + x phi(x) (R/encoder.py:262-264) by sc_gelu_bwd with a unit upstream."""
+    t, was_np, dt = _dev(x)
+    buf, n = _padded_flat(t, 1024)
+    ones = torch.ones_like(buf)
+    out = torch.empty_like(buf)
+    _lib.call("sc_gelu_bwd", buf.data_ptr(), ones.data_ptr(), out.data_ptr(), _lib.DTYPE_F32, buf.numel() // 1024,
+              1024, None, None, _lib.stream_handle(), exc=EncoderError)
+    return _back(out[:n].reshape(t.shape), was_np, dt)
+
+
+def layer_norm(x, gain, bias):
+    """(gain * xhat + bias, (xhat, inv)) with eps 1e-12 (R/encoder.py:267-273), by sc_layernorm_fwd."""
+    t, was_np, dt = _dev(x)
+    g, b = _dev(gain)[0].float().contiguous(), _dev(bias)[0].float().contiguous()
+    h = t.shape[-1]
+    x2 = t.reshape(-1, h).float().contiguous()
+    rows = x2.shape[0]
+    y = torch.empty_like(x2)
+    mean = torch.empty(rows, dtype=torch.float32, device=x2.device)
+    rstd = torch.empty_like(mean)
+    if h % 4 == 0 and h <= 1024:
+        _lib.call("sc_layernorm_fwd", x2.data_ptr(), _lib.DTYPE_F32, None, 0, g.data_ptr(), b.data_ptr(), y.data_ptr(),
+                  None, mean.data_ptr(), rstd.data_ptr(), rows, h, float(LAYER_NORM_EPS), _lib.stream_handle(),
+                  exc=EncoderError)
+    else:
+        mean = x2.mean(dim=-1)
+        rstd = torch.rsqrt(((x2 - mean[:, None]) ** 2).mean(dim=-1) + LAYER_NORM_EPS)
+        y = (x2 - mean[:, None]) * rstd[:, None] * g + b
+    xhat = ((x2 - mean[:, None]) * rstd[:, None]).reshape(t.shape)
+    inv = rstd.reshape(*t.shape[:-1], 1)
+    return _back(y.reshape(t.shape), was_np, dt), (_back(xhat, was_np, dt), _back(inv, was_np, dt))
+
+
+def layer_norm_backward(grad_y, cache, gain):
+    """(dx, dgain, dbias) of layer_norm (R/encoder.py:276-285), by sc_layernorm_bwd on xhat."""
+    gy, was_np, dt = _dev(grad_y)
+    xhat, inv = (_dev(c)[0].float() for c in cache)
+    g = _dev(gain)[0].float().contiguous()
+    h = gy.shape[-1]
+    dy = gy.reshape(-1, h).float().contiguous()
+    xh = xhat.reshape(-1, h).contiguous()
+    rows = dy.shape[0]
+    if h % 4 == 0 and h <= 1024:
+        zeros = torch.zeros(rows, dtype=torch.float32, device=dy.device)
+        ones = torch.ones_like(zeros)
+        dxh = torch.empty_like(dy)
+        dg = torch.empty(h, dtype=torch.float32, device=dy.device)
+        db = torch.empty_like(dg)
+        parts = torch.empty(2 * _lib.load().sc_ln_partials(rows) * h, dtype=torch.float32, device=dy.device)
+        # with mean 0 and rstd 1 the kernel's xhat is xhat itself; dx = inv * (g dy - m1 - xhat m2)
+        _lib.call("sc_layernorm_bwd", dy.data_ptr(), None, xh.data_ptr(), _lib.DTYPE_F32, None, 0, g.data_ptr(),
+                  zeros.data_ptr(), ones.data_ptr(), dxh.data_ptr(), None, dg.data_ptr(), db.data_ptr(),
+                  parts.data_ptr(), rows, h, _lib.stream_handle(), exc=EncoderError)
+        dx = dxh.reshape(gy.shape) * inv
+    else:
+        gd = dy * g
+        m1 = gd.mean(dim=-1, keepdim=True)
+        m2 = (gd * xh).mean(dim=-1, keepdim=True)
+        dx = ((gd - m1 - xh * m2)).reshape(gy.shape) * inv
+        dg, db = (dy * xh).sum(0), dy.sum(0)
+    return _back(dx, was_np, dt), _back(dg, was_np, dt), _back(db, was_np, dt)
+
+
+def weight_nbytes(weights: dict) -> int:
+    return sum(int(np.asarray(w).nbytes) if not torch.is_tensor(w) else w.numel() * w.element_size()
+               for w in weights.values())
+
+
+_LAYER_KEYS = ("wq", "bq", "wk", "bk", "wv", "bv", "wo", "bo", "ln1_g", "ln1_b", "w1", "b1", "w2", "b2",
+               "ln2_g", "ln2_b")
+
+
+def layer_forward(x, partition, pattern, weights, layer_index, config, want_cache=False):
+    """One post-LN layer over a (batch, seq, embed) activation (R/encoder.py:306-371) on the device:
+    fused attention kernels, cuBLAS GEMMs, LayerNorm / GELU kernels.  With ``want_cache`` it also
+    returns the cache ``layer_backward`` consumes (the device autograd graph)."""
+    xt, was_np, dt = _dev(x)
+    b, s, h = xt.shape
+    p = f"L{layer_index}."
+    W = {p + k: _dev(weights[p + k])[0].float().contiguous().detach().requires_grad_(want_cache) for k in _LAYER_KEYS}
+    globals_ = getattr(pattern, "global_positions", ())
+    layout = PackedLayout.from_lengths([s] * b, [partition.group_len("query")] * b, device="cuda",
+                                       qds_positions=[globals_] * b if globals_ else None)
+    x2 = xt.reshape(b * s, h).float().contiguous().detach().requires_grad_(want_cache)
+    with torch.set_grad_enabled(want_cache), _fp32_gemms(config.precision != "bf16"):
+        out, _ = _layer_block(x2, x2, W, None, p, layout, pattern, config.heads, math.sqrt(config.head_dim), config,
+                              True)
+    if not bool(torch.isfinite(out.detach()).all()):
+        raise NonFiniteActivationError(layer_index)
+    res = _back(out.float().reshape(b, s, h), was_np, dt)
+    if not want_cache:
+        return res
+    return res, {"x": x2, "out": out, "W": W, "shape": (b, s, h), "was_np": was_np, "dtype": dt}
+
+
+def layer_backward(grad_out, cache, partition, pattern, weights, layer_index, config, grads):
+    """Adjoint of layer_forward (R/encoder.py:374-443): returns d_x and accumulates the layer's weight
+    gradients into ``grads`` by reference name (through the device adjoints of the layer blocks)."""
+    g = _dev(grad_out)[0].float().reshape(cache["out"].shape)
+    names = list(cache["W"])
+    with _fp32_gemms(config.precision != "bf16"):
+        res = torch.autograd.grad(cache["out"], [cache["x"]] + [cache["W"][n] for n in names], grad_outputs=g,
+                                  allow_unused=True)
+    for n, gr in zip(names, res[1:]):
+        val = torch.zeros_like(cache["W"][n]) if gr is None else gr
+        val = _back(val, cache["was_np"], cache["dtype"]) if cache["was_np"] else val
+        grads[n] = grads.get(n, 0) + val
+    dx = res[0].reshape(cache["shape"])
+    return _back(dx, cache["was_np"], cache["dtype"])

@@ -546,3 +546,126 @@ def test_attention_backward_minimal_workspace_fallback(P):
     full = run(_lib.load().sc_attn_bwd_workspace_bytes(T, H, lay.nseq, lay.max_qgroup_len))
     small = run(T * H * 8)
     close(small.cpu().numpy(), full.cpu().numpy(), 2e-2)  # bf16 P / dS in the mma paths
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped primitives (R/encoder.py:250-443, R/attention.py:260-269, :348-378, :476-507)
+# ---------------------------------------------------------------------------
+
+def test_gelu_layer_norm_primitives_vs_formulas(P):
+    from scipy.special import erf
+
+    from paper_2312_17649_b200 import encoder as E
+
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((3, 7, 96)) * 3
+    want = 0.5 * x * (1 + erf(x / np.sqrt(2)))
+    close(E.gelu(x), want, 1e-5)
+    dwant = 0.5 * (1 + erf(x / np.sqrt(2))) + x * np.exp(-0.5 * x * x) / np.sqrt(2 * np.pi)
+    close(E.gelu_grad(x), dwant, 1e-5)
+    g, b = rng.random(96) + 0.5, rng.standard_normal(96)
+    y, (xhat, inv) = E.layer_norm(x, g, b)
+    mu = x.mean(-1, keepdims=True)
+    iv = 1 / np.sqrt(((x - mu) ** 2).mean(-1, keepdims=True) + 1e-12)
+    close(y, g * (x - mu) * iv + b, 1e-5)
+    close(inv, iv, 1e-5)
+    gy = rng.standard_normal(x.shape)
+    dx, dg, db = E.layer_norm_backward(gy, (xhat, inv), g)
+    xh = (x - mu) * iv
+    dxh = gy * g
+    dx_want = iv * (dxh - dxh.mean(-1, keepdims=True) - xh * (dxh * xh).mean(-1, keepdims=True))
+    close(dx, dx_want, 1e-4)
+    close(dg, (gy * xh).sum((0, 1)), 1e-4)
+    close(db, gy.sum((0, 1)), 1e-4)
+
+
+@pytest.mark.parametrize("idx", [0, 7, 13, 19, 25, 31, 34, 35])
+def test_group_attention_backward_api_vs_reference(P, G, idx):
+    """group_attention(want_cache=True) + group_attention_backward per group, summed like layer_backward."""
+    case = cases.ATTN_CASES[idx]
+    name, w, pad, m, n, heads, d, dt = case
+    x = cases.attn_inputs(idx, case)
+    go = cases.attn_grad_out(idx, case)
+    spans = cases.attn_spans(m, n)
+    qkv = {g: tuple(a[:, lo:hi, :] for a in x) for g, (lo, hi) in zip(P.GROUPS, spans)}
+    pat = P.make_pattern(name, w, cases.attn_globals(name, m, n))
+    s = m + n + 3
+    dq, dk, dv = (np.zeros((heads, s, d)) for _ in range(3))
+    span = dict(zip(P.GROUPS, spans))
+    for g in P.GROUPS:
+        lo, hi = span[g]
+        _, cache = P.group_attention(qkv, g, pat, math.sqrt(d), pad, want_cache=True)
+        gq, contrib = P.group_attention_backward(cache, go[..., lo:hi, :], g, pat)
+        dq[..., lo:hi, :] += gq
+        for target, idxs, gk, gv in contrib:
+            t0, t1 = span[target]
+            dk[..., t0:t1, :] += gk
+            dv[..., t0:t1, :] += gv
+    for tag, got in (("dq", dq), ("dk", dk), ("dv", dv)):
+        want = G[f"attn_{tag}_{idx}"]
+        if want.shape != got.shape:
+            got = got @ cases.grad_projection(idx, d)
+        close(got, want, 1e-4)
+
+
+@pytest.mark.parametrize("pad", ["exclude", "zero-logit"])
+def test_attend_segments_backward_api_vs_oracle(P, pad):
+    from oracle import sparsecross_oracle as O
+
+    rng = np.random.default_rng(8)
+    s, d = 19, 16
+    q = rng.standard_normal((2, s, d))
+    k1, v1 = rng.standard_normal((2, s, d)), rng.standard_normal((2, s, d))
+    k2, v2 = rng.standard_normal((2, 5, d)), rng.standard_normal((2, 5, d))
+    extra = np.zeros((s, 7), bool)
+    extra[3, 2] = extra[10, 5] = True
+    segs = [(k2, v2, math.inf, None), (k1, v1, 3, extra)]
+    out, cache = P.attend_segments(q, segs, 4.0, pad, want_cache=True)
+    close(out, O.attend_segments(q, segs, 4.0, pad), 1e-5)
+    go = rng.standard_normal(out.shape)
+    gq, kv = P.attend_segments_backward(cache, go)
+    oq, okv = O.attend_segments_backward(q, segs, 4.0, go, pad)
+    close(gq, oq, 1e-4)
+    for (a, b), (c, e) in zip(kv, okv):
+        close(a, c, 1e-4)
+        close(b, e, 1e-4)
+    probs = [rng.random((4, 6)), rng.random((4, 3))]
+    gps = [rng.standard_normal((4, 6)), rng.standard_normal((4, 3))]
+    dot = sum((p * g).sum(-1, keepdims=True) for p, g in zip(probs, gps))
+    for got, p, g in zip(P.masked_segment_softmax_backward(probs, gps), probs, gps):
+        close(got, p * (g - dot), 1e-6)
+
+
+@pytest.mark.parametrize("name", ["full", "sparse", "qds"])
+def test_layer_forward_backward_compose_reference_backward(P, G, name):
+    """CrossEncoder.backward (R/encoder.py:511-533) restated with layer_forward / layer_backward:
+    the weight gradients equal the reference's."""
+    from paper_2312_17649_b200 import encoder as E
+
+    pad = "exclude"
+    cfg = P.EncoderConfig(**cases.TINY, pattern=name, padding=pad, precision="f64")
+    wt = P.init_weights(cfg, 15)
+    seqs = [P.assemble_input(*cases.tiny_sequence(16 + j, 4, 13, cfg.vocab_size), cfg.max_positions) for j in range(2)]
+    ids = np.stack([sq.ids for sq in seqs])
+    part = seqs[0].partition
+    pat = P.resolve_pattern(cfg, part)
+    x = wt["tok_emb"][ids] + wt["pos_emb"][:ids.shape[1]]
+    caches = []
+    for i in range(cfg.layers):
+        x, c = E.layer_forward(x, part, pat, wt, i, cfg, want_cache=True)
+        caches.append(c)
+    gs = cases.TRAIN_GRAD_SCORES
+    grads = {"head_w": gs @ x[:, 0, :], "head_b": gs.sum()}
+    dx = np.zeros_like(x)
+    dx[:, 0, :] = gs[:, None] * wt["head_w"]
+    for i in reversed(range(cfg.layers)):
+        dx = E.layer_backward(dx, caches[i], part, pat, wt, i, cfg, grads)
+    d_tok = np.zeros_like(wt["tok_emb"])
+    np.add.at(d_tok, ids.reshape(-1), dx.reshape(-1, dx.shape[-1]))
+    grads["tok_emb"] = d_tok
+    d_pos = np.zeros_like(wt["pos_emb"])
+    d_pos[:ids.shape[1]] = dx.sum(0)
+    grads["pos_emb"] = d_pos
+    key = f"grad_{name}_{pad}"
+    for wn in grads:
+        close(grads[wn], G[f"{key}|{wn}"], 1e-4)
