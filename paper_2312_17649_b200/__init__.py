@@ -31,6 +31,7 @@ from .attention import (
     windowed_cross_attention,
 )
 from .band import (
+    BandMatrix,
     BandShapeError,
     band_apply,
     band_apply_backward,
@@ -40,6 +41,7 @@ from .band import (
     band_qk_backward,
     band_scores,
     band_scores_backward,
+    band_to_dense,
     band_validity,
 )
 from .encoder import (

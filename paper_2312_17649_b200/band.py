@@ -80,15 +80,86 @@ def band_apply(p: torch.Tensor, v: torch.Tensor, window: int) -> torch.Tensor:
     return out.reshape(*lead, s, d)
 
 
-def band_qk(q: torch.Tensor, k: torch.Tensor, window: int) -> torch.Tensor:
-    """2-D windowed query-key product (R/band.py:290-303); returns the (s, 2w+1) band data."""
+def _as_tensor(x) -> torch.Tensor:
+    return x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+class BandMatrix:
+    """Band storage on the device (R/band.py:55-114): ``data`` (seq_len, 2w+1), invalid slots exactly 0,
+    ``target_len`` = rows of the attended-to matrix."""
+
+    def __init__(self, data, window: int, target_len: int):
+        self.window = _check_window(window)
+        self.data = _as_tensor(data)
+        if self.data.dim() != 2 or self.data.shape[1] != 2 * self.window + 1:
+            raise BandShapeError(f"band data must be (s, {2 * self.window + 1}), got {tuple(self.data.shape)}")
+        self.target_len = int(target_len)
+        if self.target_len < 1:
+            raise BandShapeError("target_len must be >= 1")
+        if not bool(torch.isfinite(self.data).all()):
+            raise BandShapeError("band data contains non-finite entries")
+        if bool((self.data[~self.valid] != 0).any()):
+            raise BandShapeError("entries at invalid band positions must be exactly 0")
+
+    @property
+    def seq_len(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def width(self) -> int:
+        return self.data.shape[1]
+
+    @property
+    def valid(self) -> torch.Tensor:
+        return band_validity(self.seq_len, self.window, self.target_len, device=self.data.device)
+
+    def to_dense(self, fill=0.0) -> torch.Tensor:
+        return band_to_dense(self, fill=fill)
+
+    @classmethod
+    def from_dense(cls, dense, window: int) -> "BandMatrix":
+        """The in-band entries of a dense (s, s') matrix (R/band.py:100-114)."""
+        d = _as_tensor(dense)
+        if d.dim() != 2:
+            raise BandShapeError("dense input must be 2-D")
+        w = _check_window(window)
+        s, t = d.shape
+        cols = torch.arange(s, device=d.device)[:, None] + torch.arange(2 * w + 1, device=d.device)[None, :] - w
+        ok = (cols >= 0) & (cols < t)
+        data = torch.where(ok, d.gather(1, cols.clamp(0, t - 1)), torch.zeros((), dtype=d.dtype, device=d.device))
+        return cls(data, w, t)
+
+
+def band_to_dense(band: BandMatrix, target_cols: int | None = None, fill=0.0) -> torch.Tensor:
+    """Re-expand a band to a dense (s, target_cols) matrix, other entries ``fill`` (R/band.py:344-366)."""
+    t = band.target_len if target_cols is None else int(target_cols)
+    if t < 1:
+        raise BandShapeError("target_cols must be >= 1")
+    s, w = band.seq_len, band.window
+    cols = torch.arange(s, device=band.data.device)[:, None] + torch.arange(2 * w + 1, device=band.data.device)[None, :] - w
+    ok = (cols >= 0) & (cols < t)
+    dense = torch.full((s, t + 1), float(fill), dtype=band.data.dtype, device=band.data.device)
+    dense.scatter_(1, torch.where(ok, cols, torch.full_like(cols, t)), band.data)  # invalid slots -> spare column
+    return dense[:, :t]
+
+
+def band_qk(q, k, window: int) -> BandMatrix:
+    """Windowed query-key product of (s, h) and (s', h) matrices as a BandMatrix (R/band.py:290-303)."""
+    q, k = _as_tensor(q), _as_tensor(k)
     if q.dim() != 2 or k.dim() != 2:
         raise BandShapeError("Q and K must be 2-D")
-    return band_scores(q, k, window)
+    return BandMatrix(band_scores(q, k, window), window, k.shape[0])
 
 
-def band_pv(p: torch.Tensor, v: torch.Tensor, window: int) -> torch.Tensor:
-    """2-D band-probability-value product (R/band.py:306-313)."""
+def band_pv(p, v, window: int | None = None) -> torch.Tensor:
+    """Band probabilities (BandMatrix, or raw band data with ``window``) times a dense (s', h) value
+    matrix (R/band.py:306-313)."""
+    v = _as_tensor(v)
+    if isinstance(p, BandMatrix):
+        if v.dim() != 2 or v.shape[0] != p.target_len:
+            raise BandShapeError(f"V has {v.shape[0]} rows but band was built against {p.target_len}")
+        return band_apply(p.data, v, p.window)
+    p = _as_tensor(p)
     if p.dim() != 2 or v.dim() != 2:
         raise BandShapeError("P and V must be 2-D")
     return band_apply(p, v, window)
@@ -134,15 +205,32 @@ def band_apply_backward(grad_out: torch.Tensor, p: torch.Tensor, v: torch.Tensor
     return gp.reshape(*lead, s, 2 * w + 1), gv.reshape(*lead, t, d)
 
 
-def band_qk_backward(grad_band: torch.Tensor, q: torch.Tensor, k: torch.Tensor, window: int):
-    """2-D adjoint of band_qk (R/band.py:316-328)."""
+def band_qk_backward(grad_band, q, k, window: int):
+    """2-D adjoint of band_qk (R/band.py:316-328); grad_band a BandMatrix or raw band data."""
+    q, k = _as_tensor(q), _as_tensor(k)
+    if isinstance(grad_band, BandMatrix):
+        if grad_band.window != _check_window(window) or grad_band.seq_len != q.shape[0]:
+            raise BandShapeError("gradient band inconsistent with forward shapes")
+        if grad_band.target_len != k.shape[0]:
+            raise BandShapeError("gradient band target length inconsistent with K")
+        grad_band = grad_band.data
+    grad_band = _as_tensor(grad_band)
     if q.dim() != 2 or k.dim() != 2 or grad_band.dim() != 2:
         raise BandShapeError("gradient band, Q and K must be 2-D")
     return band_scores_backward(grad_band, q, k, window)
 
 
-def band_pv_backward(grad_out: torch.Tensor, p: torch.Tensor, v: torch.Tensor, window: int):
-    """2-D adjoint of band_pv (R/band.py:331-341)."""
+def band_pv_backward(grad_out, p, v, window: int | None = None):
+    """2-D adjoint of band_pv (R/band.py:331-341): (grad_p, grad_v); grad_p a BandMatrix when p is."""
+    grad_out, v = _as_tensor(grad_out), _as_tensor(v)
+    if isinstance(p, BandMatrix):
+        if v.shape[0] != p.target_len:
+            raise BandShapeError("V rows inconsistent with band target length")
+        if grad_out.dim() != 2 or tuple(grad_out.shape) != (p.seq_len, v.shape[1]):
+            raise BandShapeError("grad_out shape inconsistent with forward output")
+        gp, gv = band_apply_backward(grad_out, p.data, v, p.window)
+        return BandMatrix(gp, p.window, p.target_len), gv
+    p = _as_tensor(p)
     if grad_out.dim() != 2 or p.dim() != 2 or v.dim() != 2:
         raise BandShapeError("grad_out, P and V must be 2-D")
     return band_apply_backward(grad_out, p, v, window)

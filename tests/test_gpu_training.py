@@ -669,3 +669,31 @@ def test_layer_forward_backward_compose_reference_backward(P, G, name):
     key = f"grad_{name}_{pad}"
     for wn in grads:
         close(grads[wn], G[f"{key}|{wn}"], 1e-4)
+
+
+def test_band_matrix_api(P):
+    """BandMatrix / band_qk / band_pv / their adjoints / band_to_dense (R/band.py:55-366)."""
+    rng = np.random.default_rng(12)
+    s, t, h, w = 7, 9, 4, 2
+    q = torch.tensor(rng.standard_normal((s, h)), dtype=torch.float32, device="cuda")
+    k = torch.tensor(rng.standard_normal((t, h)), dtype=torch.float32, device="cuda")
+    v = torch.tensor(rng.standard_normal((t, h)), dtype=torch.float32, device="cuda")
+    band = P.band_qk(q, k, w)
+    assert isinstance(band, P.BandMatrix) and band.target_len == t and band.seq_len == s
+    dense = P.band_to_dense(band)
+    off = np.arange(t)[None, :] - np.arange(s)[:, None]
+    want = np.where(np.abs(off) <= w, (q @ k.T).cpu().numpy(), 0.0)
+    close(dense.cpu().numpy(), want, 1e-5)
+    back = P.BandMatrix.from_dense(dense, w)
+    assert torch.equal(back.data, band.data)
+    out = P.band_pv(band, v)
+    close(out.cpu().numpy(), (dense @ v).cpu().numpy(), 1e-5)
+    gp, gv = P.band_pv_backward(out, band, v)
+    assert isinstance(gp, P.BandMatrix)
+    gq, gk = P.band_qk_backward(band, q, k, w)
+    close(gq.cpu().numpy(), (dense @ k).cpu().numpy(), 1e-5)
+    close(gk.cpu().numpy(), (dense.T @ q).cpu().numpy(), 1e-5)
+    with pytest.raises(P.BandShapeError):
+        P.BandMatrix(torch.ones(s, 2 * w + 1, device="cuda"), w, t)  # nonzero invalid slots
+    with pytest.raises(P.BandShapeError):
+        P.band_pv(band, torch.zeros(t + 1, h, device="cuda"))
