@@ -23,7 +23,9 @@ from .attention import (
     group_attention_backward,
     longformer_pattern,
     make_pattern,
+    SegmentScores,
     masked_segment_softmax,
+    segment_softmax,
     masked_segment_softmax_backward,
     qds_band_exclusions,
     qds_pattern,
@@ -31,6 +33,7 @@ from .attention import (
     windowed_cross_attention,
 )
 from .band import (
+    MASKED,
     BandMatrix,
     BandShapeError,
     band_apply,
@@ -43,6 +46,19 @@ from .band import (
     band_scores_backward,
     band_to_dense,
     band_validity,
+    dense_band_oracle,
+)
+from .benchmark import (
+    BenchConfigError,
+    BenchRecord,
+    BenchSpec,
+    FlopBreakdown,
+    default_model_config,
+    emit_report,
+    flop_count,
+    gen_random_batch,
+    measure,
+    run_bench,
 )
 from .encoder import (
     CrossEncoder,
@@ -87,3 +103,4 @@ from .training import (
 )
 
 __version__ = "0.1.0"
+from .rerank import EvaluationError, RunEntry, ndcg_at_k, rerank  # noqa: E402  (R/evaluation.py; shadows the submodule attribute as the reference's top-level name does)

@@ -345,6 +345,66 @@ def apply_pattern(partition, qkv: dict, pattern: AttentionPattern, scale: float 
 # (that is attend_packed's fused kernels), but the same numerics.
 # ---------------------------------------------------------------------------
 
+class SegmentScores:
+    """Ordered score blocks of one source group (R/attention.py:164-187): dense (rows, target_len)
+    blocks (numpy or device tensors) for unwindowed targets, BandMatrix for windowed ones."""
+
+    def __init__(self, segments):
+        self.segments = list(segments)
+        if not self.segments:
+            raise AttentionError("segment tuple must be nonempty")
+        rows = {self._rows(seg) for seg in self.segments}
+        if len(rows) != 1:
+            raise AttentionError(f"segments disagree on row count: {sorted(rows)}")
+
+    @staticmethod
+    def _rows(seg) -> int:
+        from .band import BandMatrix
+        return seg.seq_len if isinstance(seg, BandMatrix) else int(seg.shape[0])
+
+    @property
+    def rows(self) -> int:
+        return self._rows(self.segments[0])
+
+
+def segment_softmax(scores, scale: float, padding: str = "exclude") -> SegmentScores:
+    """Joint softmax of a source group's score segments on the device (R/attention.py:190-225).
+
+    Band segments stay BandMatrix (invalid slots exactly 0; in zero-logit mode the
+    padded mass is computed but not stored); dense numpy blocks come back as numpy.
+    float64 inputs are normalised in float64."""
+    from .band import BandMatrix
+
+    if scale <= 0:
+        raise AttentionError(f"scale must be positive, got {scale}")
+    if padding not in PADDING_MODES:
+        raise AttentionError(f"unknown padding mode {padding!r}")
+    if not isinstance(scores, SegmentScores):
+        scores = SegmentScores(scores)
+    values, valids, was_np = [], [], []
+    for seg in scores.segments:
+        if isinstance(seg, BandMatrix):
+            values.append(seg.data)
+            valids.append(seg.valid)
+            was_np.append(False)
+        else:
+            t, np_in = _to_device(seg)
+            values.append(t)
+            valids.append(None)
+            was_np.append(np_in)
+    probs = masked_segment_softmax(values, valids, scale, padding)
+    out = []
+    for seg, p, ok, np_in in zip(scores.segments, probs, valids, was_np):
+        if isinstance(seg, BandMatrix):
+            p = torch.where(ok, p, torch.zeros((), dtype=p.dtype, device=p.device))
+            out.append(BandMatrix(p.to(seg.data.dtype), seg.window, seg.target_len))
+        elif np_in:
+            out.append(p.cpu().numpy().astype(np.asarray(seg).dtype, copy=False))
+        else:
+            out.append(p.to(seg.dtype))
+    return SegmentScores(out)
+
+
 def masked_segment_softmax(values, valids, scale: float, padding: str = "exclude"):
     """Joint softmax over score blocks with optional validity masks (R/attention.py:228-257).
 
@@ -354,7 +414,7 @@ def masked_segment_softmax(values, valids, scale: float, padding: str = "exclude
         raise AttentionError(f"unknown padding mode {padding!r}")
     scaled = []
     for val, ok in zip(values, valids):
-        y = val.float() / scale
+        y = (val if val.dtype == torch.float64 else val.float()) / scale
         if ok is not None:
             fill = 0.0 if padding == "zero-logit" else -math.inf
             y = torch.where(ok, y, torch.full_like(y, fill))

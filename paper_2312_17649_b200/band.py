@@ -84,6 +84,12 @@ def _as_tensor(x) -> torch.Tensor:
     return x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
+def _kernel_operand(x) -> torch.Tensor:
+    """Device operand for the band kernels: float64 (the reference's numpy default) computes in fp32."""
+    t = _as_tensor(x)
+    return t.float() if t.dtype == torch.float64 else t
+
+
 class BandMatrix:
     """Band storage on the device (R/band.py:55-114): ``data`` (seq_len, 2w+1), invalid slots exactly 0,
     ``target_len`` = rows of the attended-to matrix."""
@@ -130,22 +136,44 @@ class BandMatrix:
         return cls(data, w, t)
 
 
-def band_to_dense(band: BandMatrix, target_cols: int | None = None, fill=0.0) -> torch.Tensor:
-    """Re-expand a band to a dense (s, target_cols) matrix, other entries ``fill`` (R/band.py:344-366)."""
+MASKED = np.ma.masked   # band_to_dense fill marker (R/band.py:36)
+
+
+def band_to_dense(band: BandMatrix, target_cols: int | None = None, fill=0.0):
+    """Re-expand a band to a dense (s, target_cols) device matrix, other entries ``fill``
+    (R/band.py:344-366); ``fill=MASKED`` returns a host numpy masked array instead."""
     t = band.target_len if target_cols is None else int(target_cols)
     if t < 1:
         raise BandShapeError("target_cols must be >= 1")
     s, w = band.seq_len, band.window
-    cols = torch.arange(s, device=band.data.device)[:, None] + torch.arange(2 * w + 1, device=band.data.device)[None, :] - w
+    dev = band.data.device
+    cols = torch.arange(s, device=dev)[:, None] + torch.arange(2 * w + 1, device=dev)[None, :] - w
     ok = (cols >= 0) & (cols < t)
-    dense = torch.full((s, t + 1), float(fill), dtype=band.data.dtype, device=band.data.device)
+    masked = fill is MASKED
+    dense = torch.full((s, t + 1), 0.0 if masked else float(fill), dtype=band.data.dtype, device=dev)
     dense.scatter_(1, torch.where(ok, cols, torch.full_like(cols, t)), band.data)  # invalid slots -> spare column
-    return dense[:, :t]
+    if not masked:
+        return dense[:, :t]
+    off = torch.arange(t, device=dev)[None, :] - torch.arange(s, device=dev)[:, None]
+    return np.ma.MaskedArray(dense[:, :t].cpu().numpy(), mask=(off.abs() > w).cpu().numpy())
+
+
+def dense_band_oracle(q, k, window: int) -> np.ma.MaskedArray:
+    """Full Q K^T (cuBLAS) with out-of-band entries masked (R/band.py:369-386): the
+    independent dense check of band_qk, returned as a host masked array."""
+    q, k = _as_tensor(q), _as_tensor(k)
+    if q.dim() != 2 or k.dim() != 2:
+        raise BandShapeError("Q and K must be 2-D")
+    if q.shape[1] != k.shape[1]:
+        raise BandShapeError(f"embedding dims differ: Q has {q.shape[1]}, K has {k.shape[1]}")
+    w = _check_window(window)
+    off = np.arange(k.shape[0])[None, :] - np.arange(q.shape[0])[:, None]
+    return np.ma.MaskedArray((q @ k.T).cpu().numpy(), mask=np.abs(off) > w)
 
 
 def band_qk(q, k, window: int) -> BandMatrix:
     """Windowed query-key product of (s, h) and (s', h) matrices as a BandMatrix (R/band.py:290-303)."""
-    q, k = _as_tensor(q), _as_tensor(k)
+    q, k = _kernel_operand(q), _kernel_operand(k)
     if q.dim() != 2 or k.dim() != 2:
         raise BandShapeError("Q and K must be 2-D")
     return BandMatrix(band_scores(q, k, window), window, k.shape[0])
@@ -154,12 +182,12 @@ def band_qk(q, k, window: int) -> BandMatrix:
 def band_pv(p, v, window: int | None = None) -> torch.Tensor:
     """Band probabilities (BandMatrix, or raw band data with ``window``) times a dense (s', h) value
     matrix (R/band.py:306-313)."""
-    v = _as_tensor(v)
+    v = _kernel_operand(v)
     if isinstance(p, BandMatrix):
         if v.dim() != 2 or v.shape[0] != p.target_len:
             raise BandShapeError(f"V has {v.shape[0]} rows but band was built against {p.target_len}")
-        return band_apply(p.data, v, p.window)
-    p = _as_tensor(p)
+        return band_apply(_kernel_operand(p.data), v, p.window)
+    p = _kernel_operand(p)
     if p.dim() != 2 or v.dim() != 2:
         raise BandShapeError("P and V must be 2-D")
     return band_apply(p, v, window)
@@ -207,14 +235,14 @@ def band_apply_backward(grad_out: torch.Tensor, p: torch.Tensor, v: torch.Tensor
 
 def band_qk_backward(grad_band, q, k, window: int):
     """2-D adjoint of band_qk (R/band.py:316-328); grad_band a BandMatrix or raw band data."""
-    q, k = _as_tensor(q), _as_tensor(k)
+    q, k = _kernel_operand(q), _kernel_operand(k)
     if isinstance(grad_band, BandMatrix):
         if grad_band.window != _check_window(window) or grad_band.seq_len != q.shape[0]:
             raise BandShapeError("gradient band inconsistent with forward shapes")
         if grad_band.target_len != k.shape[0]:
             raise BandShapeError("gradient band target length inconsistent with K")
         grad_band = grad_band.data
-    grad_band = _as_tensor(grad_band)
+    grad_band = _kernel_operand(grad_band)
     if q.dim() != 2 or k.dim() != 2 or grad_band.dim() != 2:
         raise BandShapeError("gradient band, Q and K must be 2-D")
     return band_scores_backward(grad_band, q, k, window)
@@ -222,15 +250,15 @@ def band_qk_backward(grad_band, q, k, window: int):
 
 def band_pv_backward(grad_out, p, v, window: int | None = None):
     """2-D adjoint of band_pv (R/band.py:331-341): (grad_p, grad_v); grad_p a BandMatrix when p is."""
-    grad_out, v = _as_tensor(grad_out), _as_tensor(v)
+    grad_out, v = _kernel_operand(grad_out), _kernel_operand(v)
     if isinstance(p, BandMatrix):
         if v.shape[0] != p.target_len:
             raise BandShapeError("V rows inconsistent with band target length")
         if grad_out.dim() != 2 or tuple(grad_out.shape) != (p.seq_len, v.shape[1]):
             raise BandShapeError("grad_out shape inconsistent with forward output")
-        gp, gv = band_apply_backward(grad_out, p.data, v, p.window)
+        gp, gv = band_apply_backward(grad_out, _kernel_operand(p.data), v, p.window)
         return BandMatrix(gp, p.window, p.target_len), gv
-    p = _as_tensor(p)
+    p = _kernel_operand(p)
     if grad_out.dim() != 2 or p.dim() != 2 or v.dim() != 2:
         raise BandShapeError("grad_out, P and V must be 2-D")
     return band_apply_backward(grad_out, p, v, window)

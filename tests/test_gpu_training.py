@@ -697,3 +697,104 @@ def test_band_matrix_api(P):
         P.BandMatrix(torch.ones(s, 2 * w + 1, device="cuda"), w, t)  # nonzero invalid slots
     with pytest.raises(P.BandShapeError):
         P.band_pv(band, torch.zeros(t + 1, h, device="cuda"))
+
+
+def _concat_softmax(blocks, valids, scale):
+    """numpy joint softmax over concatenated segments (the reference tests' concatenation oracle)."""
+    ys = [np.where(ok, b / scale, -np.inf) if ok is not None else b / scale for b, ok in zip(blocks, valids)]
+    cat = np.concatenate(ys, axis=1)
+    e = np.exp(cat - cat.max(axis=1, keepdims=True))
+    e /= e.sum(axis=1, keepdims=True)
+    return np.split(e, np.cumsum([y.shape[1] for y in ys])[:-1], axis=1)
+
+
+def _random_band(P, rng, s, w, t):
+    ok = P.band_validity(s, w, t).cpu().numpy()
+    data = np.where(ok, rng.standard_normal((s, 2 * w + 1)), 0.0)
+    return P.BandMatrix(torch.tensor(data, device="cuda"), w, t), data, ok
+
+
+class TestSegmentSoftmax:
+    """segment_softmax / SegmentScores (R/attention.py:164-225), float64 on the device."""
+
+    def test_uniform(self, P):
+        probs = P.segment_softmax([np.zeros((4, 2)), np.zeros((4, 3))], scale=2.0)
+        for seg in probs.segments:
+            np.testing.assert_allclose(seg, np.full(seg.shape, 0.2))
+
+    def test_matches_concatenation(self, P):
+        rng = np.random.default_rng(0)
+        band, data, ok = _random_band(P, rng, 6, 1, 6)
+        dense = rng.standard_normal((6, 4))
+        res = P.segment_softmax([dense, band], 2.0)
+        want_d, want_b = _concat_softmax([dense, data], [None, ok], 2.0)
+        np.testing.assert_allclose(res.segments[0], want_d, atol=1e-14)
+        got = res.segments[1]
+        assert isinstance(got, P.BandMatrix)
+        gd = got.data.cpu().numpy()
+        np.testing.assert_allclose(gd[ok], want_b[ok], atol=1e-14)
+        assert not gd[~ok].any()
+
+    def test_rows_sum_to_one_and_zero_logit(self, P):
+        rng = np.random.default_rng(1)
+        band, data, ok = _random_band(P, rng, 8, 2, 8)
+        dense = rng.standard_normal((8, 3))
+        res = P.segment_softmax([band, dense], scale=1.7)
+        total = res.segments[0].data.cpu().numpy().sum(axis=1) + res.segments[1].sum(axis=1)
+        np.testing.assert_allclose(total, 1.0, atol=1e-12)
+        zl = P.segment_softmax([band, dense], scale=1.7, padding="zero-logit")
+        ys = [np.where(ok, data / 1.7, 0.0), dense / 1.7]
+        want = _concat_softmax(ys, [None, None], 1.0)
+        np.testing.assert_allclose(zl.segments[0].data.cpu().numpy(), np.where(ok, want[0], 0.0), atol=1e-14)
+        np.testing.assert_allclose(zl.segments[1], want[1], atol=1e-14)
+
+    def test_rejects_zero_valid_row(self, P):
+        band = P.BandMatrix(torch.zeros(6, 1, dtype=torch.float64, device="cuda"), 0, 3)
+        with pytest.raises(P.AttentionError):
+            P.segment_softmax([band], scale=1.0)
+
+
+class TestBenchHarnessGpu:
+    """benchmark.measure / run_bench on the device (R/bench.py:234-310)."""
+
+    @staticmethod
+    def spec(P, **kw):
+        d = dict(pattern="sparse", window=4, query_len=10, doc_lens=(16,), batch_size=2, repetitions=3,
+                 warmup=1, precision="f32", seed=0)
+        d.update(kw)
+        return P.BenchSpec(**d)
+
+    def test_record_fields_and_determinism(self, P):
+        s = self.spec(P)
+        cfg = P.default_model_config(s)
+        model = P.CrossEncoder(cfg, seed=0)
+        batch = P.gen_random_batch(s, 16, cfg)
+        r1, r2 = P.measure(model, batch, s), P.measure(model, batch, s)
+        assert r1.flops == r2.flops and r1.peak_bytes == r2.peak_bytes
+        assert r1.time_per_doc > 0 and r1.peak_bytes >= model.weight_nbytes and not r1.oom
+        assert r1.attn_score_bytes == 0
+
+    def test_oom_recorded_not_raised(self, P):
+        s = self.spec(P)
+        cfg = P.default_model_config(s)
+        model = P.CrossEncoder(cfg, seed=0)
+        r = P.measure(model, P.gen_random_batch(s, 16, cfg), s, mem_limit_bytes=model.weight_nbytes + 1)
+        assert r.oom and r.time_per_doc is None and r.peak_bytes is None and r.flops > 0
+
+    def test_run_bench_and_report(self, P):
+        recs = P.run_bench(self.spec(P, doc_lens=(16, 164), precision="bf16"))
+        assert [r.doc_len for r in recs] == [16, 164]
+        assert len(P.emit_report(recs, "csv").strip().split("\n")) == 3
+
+
+def test_dense_band_oracle_and_masked(P):
+    """dense_band_oracle (cuBLAS) vs band_to_dense(band_qk, MASKED) (R/band.py:344-386)."""
+    rng = np.random.default_rng(3)
+    q, k = rng.standard_normal((11, 5)), rng.standard_normal((9, 5))
+    want = P.dense_band_oracle(q, k, 3)
+    got = P.band_to_dense(P.band_qk(q, k, 3), fill=P.MASKED)
+    assert isinstance(got, np.ma.MaskedArray)
+    np.testing.assert_array_equal(got.mask, want.mask)
+    np.testing.assert_allclose(got.compressed(), want.compressed(), atol=1e-5)  # f64 in -> fp32 band kernel
+    with pytest.raises(P.BandShapeError):
+        P.dense_band_oracle(q, rng.standard_normal((9, 4)), 3)

@@ -175,3 +175,89 @@ class TestTrecEvaluation:
         entries = self.run_for("q1", [("d1", 0.5), ("d2", 0.25)])
         write_run(entries, tmp_path / "run.txt")  # the reference's argument order
         assert read_run(tmp_path / "run.txt") == entries
+
+
+class TestSegmentScoresHost:
+    """SegmentScores / segment_softmax argument checks (R/attention.py:164-210), no device needed."""
+
+    def test_rejects_empty_and_mismatched(self):
+        from paper_2312_17649_b200 import AttentionError, SegmentScores
+        with pytest.raises(AttentionError):
+            SegmentScores([])
+        with pytest.raises(AttentionError):
+            SegmentScores([np.zeros((2, 2)), np.zeros((3, 2))])
+        assert SegmentScores([np.zeros((3, 2)), np.zeros((3, 5))]).rows == 3
+
+    def test_rejects_bad_scale_and_padding(self):
+        from paper_2312_17649_b200 import AttentionError, segment_softmax
+        with pytest.raises(AttentionError):
+            segment_softmax([np.zeros((2, 2))], scale=0.0)
+        with pytest.raises(AttentionError):
+            segment_softmax([np.zeros((2, 2))], scale=1.0, padding="bogus")
+
+
+class TestBenchHarness:
+    """benchmark.py (R/bench.py:43-408): spec checks, bit-identical inputs, FLOP model, reports."""
+
+    @staticmethod
+    def spec(**kw):
+        from paper_2312_17649_b200 import BenchSpec
+        d = dict(pattern="sparse", window=4, query_len=10, doc_lens=(16,), batch_size=2, repetitions=3,
+                 warmup=1, precision="f32", seed=0)
+        d.update(kw)
+        return BenchSpec(**d)
+
+    def test_spec_rejections(self):
+        from paper_2312_17649_b200 import BenchConfigError
+        for bad in (dict(batch_size=101), dict(repetitions=2), dict(pattern="strided"), dict(doc_lens=()),
+                    dict(window=1.5), dict(warmup=-1)):
+            with pytest.raises(BenchConfigError):
+                self.spec(**bad)
+
+    def test_ids_match_reference_golden(self):
+        from paper_2312_17649_b200 import default_model_config, gen_random_batch
+        g = np.load(os.path.join(os.path.dirname(__file__), "golden", "encoder.npz"))
+        s = self.spec(doc_lens=(164,), batch_size=8)
+        cfg = default_model_config(s, vocab_size=cases.C1["vocab_size"])
+        b = gen_random_batch(s, 164, cfg)
+        np.testing.assert_array_equal(b.ids, g["c1_ids"])
+        assert b.partition.seq_len == 177
+        q = self.spec(pattern="qds", doc_lens=(120,))
+        assert len(gen_random_batch(q, 120, default_model_config(q)).pattern.global_positions) == 4
+
+    def test_flop_model_matches_reference_golden(self):
+        from paper_2312_17649_b200 import flop_count, make_pattern
+        g = np.load(os.path.join(os.path.dirname(__file__), "golden", "encoder.npz"))
+        c1 = flop_count(make_pattern("sparse", 4), (1, 11, 165), 32, 2, 2, 64)
+        assert c1.total == g["c1_flops"][3]
+        c3 = flop_count(make_pattern("sparse", 4), (1, 11, 4087), 768, 12, 12, 3072)
+        assert [c3.attention, c3.projections, c3.feed_forward] == list(g["c3_flops"][:3])
+        for name, w, gl in (("full", math.inf, ()), ("longformer", 8, ()), ("qds", 4, (29, 59, 89, 119)),
+                            ("sparse", 2, ())):
+            mine = flop_count(make_pattern(name, w, gl), (1, 11, 120), 8, 2, ff_dim=16)
+            ref = O.flop_count(O.make_pattern(name, w, gl), (1, 11, 120), 8, 2, 16)
+            assert (mine.attention, mine.projections, mine.feed_forward) == \
+                (ref["attention"], ref["projections"], ref["feed_forward"])
+        s = sum((1, 11, 20))
+        assert flop_count(make_pattern("full", math.inf), (1, 11, 20), 8, 1, ff_dim=16).attention_qk == s * s * 8
+        assert flop_count(make_pattern("sparse", 9), (1, 5, 10), 4, 1, ff_dim=8).window_exceeds_dense
+        assert not flop_count(make_pattern("sparse", 2), (1, 5, 10), 4, 1, ff_dim=8).window_exceeds_dense
+
+    def test_emit_report(self):
+        from paper_2312_17649_b200 import BenchConfigError, BenchRecord, emit_report
+
+        def rec(pattern="sparse", window=4, t=1e-3, peak=1000, oom=False):
+            return BenchRecord(pattern, window, 10, 16, 2, None if oom else t, None if oom else 0.0,
+                               None if oom else peak, None if oom else 0, 1234, 1, oom)
+        lines = emit_report([rec()], "csv").strip().split("\n")
+        assert lines[0] == "pattern,w,query_len,doc_len,batch,time_per_doc_s,peak_bytes,flops"
+        assert lines[1].startswith("sparse,4,10,16,2,")
+        assert "OOM" in emit_report([rec(oom=True)], "csv")
+        md = emit_report([rec(), rec("full", math.inf, 2e-3, 2000)], "md", baseline=("sparse", 4))
+        assert "(+100%)" in md and "| full " in md and "inf" in md
+        with pytest.raises(BenchConfigError):
+            emit_report([], "csv")
+        with pytest.raises(BenchConfigError):
+            emit_report([rec()], "md", baseline=("full", 3))
+        with pytest.raises(BenchConfigError):
+            emit_report([rec()], "html")
