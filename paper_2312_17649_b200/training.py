@@ -224,6 +224,31 @@ class Linear(torch.autograd.Function):
         return dx.to(xdt), dw, None, column_sum(go), None, None
 
 
+class LinearQKV(torch.autograd.Function):
+    """Linear over the column-concatenated [wq | wk | wv] (R/encoder.py:325-327) from the compute-dtype
+    concatenation ``w16`` / ``b16`` only: the fp32 masters are never concatenated (a strided copy per
+    layer per step); their gradients come back as column views of one dW GEMM."""
+
+    @staticmethod
+    def forward(ctx, x, wq, wk, wv, bq, bk, bv, w16, b16, cdt):
+        xc = x.to(cdt).contiguous()
+        out = torch.addmm(b16, xc, w16)
+        ctx.save_for_backward(xc, w16)
+        ctx.meta = (cdt, x.dtype, wq.shape[1], wk.shape[1])
+        return out
+
+    @staticmethod
+    def backward(ctx, go):
+        xc, wc = ctx.saved_tensors
+        cdt, xdt, nq, nk = ctx.meta
+        go = go.to(cdt).contiguous()
+        dx = torch.mm(go, wc.t(), out_dtype=torch.float32) if xdt == torch.float32 else torch.mm(go, wc.t())
+        dw = torch.mm(xc.t(), go, out_dtype=torch.float32)
+        db = column_sum(go)
+        a, b = nq, nq + nk
+        return (dx.to(xdt), dw[:, :a], dw[:, a:b], dw[:, b:], db[:a], db[a:b], db[b:], None, None, None)
+
+
 class LinearGelu(torch.autograd.Function):
     """gelu(x @ w + bias) (R/encoder.py:350-351) with sc_gelu_fwd / sc_gelu_bwd; the backward's
     GELU kernel also reduces the bias gradient (no second pass over dF)."""
@@ -316,11 +341,17 @@ def _layer_block(x, xh, W, S, p, layout, pattern, H, scale, cfg, check_keys):
         return Linear.apply(xin, W[wname], None if S is None else S[wname], W[bname],
                             None if S is None else S[bname], cd)
 
-    wqkv = torch.cat([W[p + "wq"], W[p + "wk"], W[p + "wv"]], dim=1)
-    bqkv = torch.cat([W[p + "bq"], W[p + "bk"], W[p + "bv"]])
-    w16 = None if S is None else torch.cat([S[p + "wq"], S[p + "wk"], S[p + "wv"]], dim=1)
-    b16 = None if S is None else torch.cat([S[p + "bq"], S[p + "bk"], S[p + "bv"]])
-    qkv = Linear.apply(xh, wqkv, w16, bqkv, b16, cd)
+    if S is not None and cd == torch.bfloat16:
+        w16 = torch.cat([S[p + "wq"], S[p + "wk"], S[p + "wv"]], dim=1)
+        b16 = torch.cat([S[p + "bq"], S[p + "bk"], S[p + "bv"]])
+        qkv = LinearQKV.apply(xh, W[p + "wq"], W[p + "wk"], W[p + "wv"], W[p + "bq"], W[p + "bk"], W[p + "bv"],
+                              w16, b16, cd)
+    else:
+        wqkv = torch.cat([W[p + "wq"], W[p + "wk"], W[p + "wv"]], dim=1)
+        bqkv = torch.cat([W[p + "bq"], W[p + "bk"], W[p + "bv"]])
+        w16 = None if S is None else torch.cat([S[p + "wq"], S[p + "wk"], S[p + "wv"]], dim=1)
+        b16 = None if S is None else torch.cat([S[p + "bq"], S[p + "bk"], S[p + "bv"]])
+        qkv = Linear.apply(xh, wqkv, w16, bqkv, b16, cd)
     o = PatternAttention.apply(qkv, layout, pattern, H, scale, cfg.padding, check_keys)
     if bf16:
         ln1, ln1h = residual_layer_norm(x, lin(o, p + "wo", p + "bo"), W[p + "ln1_g"], W[p + "ln1_b"], want16=True)
