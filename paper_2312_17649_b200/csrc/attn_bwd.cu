@@ -642,7 +642,9 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
     p.head_part = reinterpret_cast<float*>(static_cast<char*>(workspace) + soff);
   // head-row pass: 2 warps per (sequence, head) for short sequences (<= 4 key chunks of 64),
   // else 8, split over CTAs when there are too few (sequence, head) pairs
-  p.head_warps = (int64_t)total_tokens <= (int64_t)256 * nseq ? 2 : 8;
+  p.head_warps = (int64_t)total_tokens <= (int64_t)256 * nseq ? 1 : 8;
+  static const int hw_env = [] { const char* e = getenv("SC_BWD_HEAD_WARPS"); return e ? atoi(e) : 0; }();
+  if (hw_env == 1 || hw_env == 2 || hw_env == 8) p.head_warps = hw_env;  // measurement override
   p.head_ks = 1;
   if (workspace_bytes >= soff + pbytes + split_bytes(heads, nseq)) {
     p.head_split = reinterpret_cast<float*>(static_cast<char*>(workspace) + soff + pbytes);

@@ -285,23 +285,37 @@ __global__ void __launch_bounds__(128) band_dq_kernel(Args p) {
 }
 
 // dK / dV of the head keys (cls / query rows) += the sum over the sequence's doc tiles of the
-// kernel-A partials, in tile order (deterministic).  One thread per (seq, head, which, slot, dim).
-template <int NH>
+// kernel-A partials, in tile order (deterministic).  One thread per (seq, head, which, slot, V dims):
+// V = 4 (float4 loads) for short sequences, V = 1 when many tiles per sequence need more threads.
+template <int NH, int V>
 __global__ void __launch_bounds__(256) head_part_reduce_kernel(Args p) {
+  constexpr int G = 64 / V;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int dim = (int)(idx & 63);
-  int64_t r = idx >> 6;
+  const int dim = (int)(idx % G) * V;
+  int64_t r = idx / G;
   const int sl = (int)(r % NH); r /= NH;
   const int which = (int)(r & 1); r >>= 1;
   const int h = (int)(r % p.H);
   const int j = (int)(r / p.H);
   if (j >= p.nseq) return;
-  const SeqGroups g = seq_groups(p.cu, p.qlen, j);
-  if (sl >= 1 + g.len[1]) return;
-  float acc = 0.f;
-  for (int t = p.tile_base[j]; t < p.tile_base[j + 1]; ++t)
-    acc += p.head_part[(((int64_t)t * p.H + h) * 2 + which) * NH * 64 + sl * 64 + dim];
-  add_grad(which ? p.dk : p.dv, (int64_t)(g.start + sl) * p.ld_grad + h * 64 + dim, acc, p.grad_bf16);
+  if (sl >= 1 + __ldg(p.qlen + j)) return;
+  const int64_t off = (int64_t)(__ldg(p.cu + j) + sl) * p.ld_grad + h * 64 + dim;
+  const int64_t stride = (int64_t)p.H * 2 * NH * 64;
+  const float* src = p.head_part + ((int64_t)h * 2 + which) * NH * 64 + sl * 64 + dim;
+  float acc[V] = {};
+  const int t0 = __ldg(p.tile_base + j), t1 = __ldg(p.tile_base + j + 1);
+#pragma unroll 8
+  for (int t = t0; t < t1; ++t) {
+    if constexpr (V == 4) {
+      const float4 v = *reinterpret_cast<const float4*>(src + t * stride);
+      acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+    } else {
+      acc[0] += src[t * stride];
+    }
+  }
+  void* base = which ? p.dk : p.dv;
+#pragma unroll
+  for (int e = 0; e < V; ++e) add_grad(base, off + e, acc[e], p.grad_bf16);
 }
 
 // Kernel B: doc keys [k0, k0+64) of one sequence, one head.  Sources: the band doc rows
@@ -777,6 +791,7 @@ int launch_head_w(const Args& a, cudaStream_t st) {
 // 64-key chunks each): 2 warps, so several CTAs fit an SM.
 template <int NH>
 int launch_head(const Args& a, cudaStream_t st) {
+  if (a.head_warps == 1) return launch_head_w<NH, 1>(a, st);
   return a.head_warps == 2 ? launch_head_w<NH, 2>(a, st) : launch_head_w<NH, 8>(a, st);
 }
 
@@ -799,8 +814,13 @@ int launch_pair(const Args& a, int ntiles, int phase, cudaStream_t st) {
     band_dq_kernel<NB, NH><<<grid, 128, sm, st>>>(a);
     SC_CHECK_LAUNCH("band_dq_kernel");
   } else if (phase == 2) {
-    const int64_t n = (int64_t)a.nseq * a.H * 2 * NH * 64;
-    head_part_reduce_kernel<NH><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a);
+    if (ntiles <= 8 * a.nseq) {  // few tiles per sequence: 4 dims per thread
+      const int64_t n = (int64_t)a.nseq * a.H * 2 * NH * 16;
+      head_part_reduce_kernel<NH, 4><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a);
+    } else {
+      const int64_t n = (int64_t)a.nseq * a.H * 2 * NH * 64;
+      head_part_reduce_kernel<NH, 1><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a);
+    }
     SC_CHECK_LAUNCH("head_part_reduce_kernel");
   } else {
     band_dkv_kernel<NB, NH><<<grid, 128, sm, st>>>(a);

@@ -200,21 +200,25 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, in
   }
 }
 
-// out[c] = sum over partial rows k of part[k][c], in k order: block = 32 columns x 8 warps, warp w
-// sums rows k = w (mod 8), the 8 warp sums are added in warp order.
-__global__ void __launch_bounds__(256) colsum_reduce_kernel(const float* __restrict__ part, int nparts, int cols,
-                                                            float* __restrict__ out) {
-  __shared__ float red[8][33];
+// out[c] = sum over partial rows k of part[k][c]: block = 32 columns x 8 warps, warp w sums rows
+// k = w (mod 8) (four loads in flight), the 8 warp sums are added in warp order (deterministic).
+constexpr int kRedWarps = 8;
+__global__ void __launch_bounds__(kRedWarps * 32) colsum_reduce_kernel(const float* __restrict__ part, int nparts,
+                                                                       int cols, float* __restrict__ out) {
+  __shared__ float red[kRedWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   float acc = 0.f;
-  if (c < cols)
-    for (int k = warp; k < nparts; k += 8) acc += part[(int64_t)k * cols + c];
+  if (c < cols) {
+#pragma unroll 4
+    for (int k = warp; k < nparts; k += kRedWarps) acc += __ldg(part + (int64_t)k * cols + c);
+  }
   red[warp][lane] = acc;
   __syncthreads();
   if (warp == 0 && c < cols) {
     float t = 0.f;
-    for (int w = 0; w < 8; ++w) t += red[w][lane];
+#pragma unroll
+    for (int w = 0; w < kRedWarps; ++w) t += red[w][lane];
     out[c] = t;
   }
 }
@@ -326,9 +330,9 @@ extern "C" int sc_layernorm_bwd(const float* dy, const void* dy_bf16, const void
                 (float*)mean, (float*)rstd, dx, pg, pb, rows, cols, 0.f, (unsigned)nparts, st, (void*)dy_bf16,
                 dx_bf16);
   SC_CHECK_LAUNCH("ln_bwd_kernel");
-  colsum_reduce_kernel<<<(cols + 31) / 32, 256, 0, st>>>(pg, nparts, cols, dgamma);
+  colsum_reduce_kernel<<<(cols + 31) / 32, kRedWarps * 32, 0, st>>>(pg, nparts, cols, dgamma);
   SC_CHECK_LAUNCH("colsum_reduce_kernel");
-  colsum_reduce_kernel<<<(cols + 31) / 32, 256, 0, st>>>(pb, nparts, cols, dbeta);
+  colsum_reduce_kernel<<<(cols + 31) / 32, kRedWarps * 32, 0, st>>>(pb, nparts, cols, dbeta);
   SC_CHECK_LAUNCH("colsum_reduce_kernel");
   return SC_OK;
 }
@@ -347,7 +351,7 @@ extern "C" int sc_colsum(const void* x, int32_t dtype, int64_t ld, int32_t rows,
   else
     colsum_kernel<__nv_bfloat16><<<nparts, threads, 0, st>>>((const __nv_bfloat16*)x, ld, rows, cols, rpc, partials);
   SC_CHECK_LAUNCH("colsum_kernel");
-  colsum_reduce_kernel<<<(cols + 31) / 32, 256, 0, st>>>(partials, nparts, cols, out);
+  colsum_reduce_kernel<<<(cols + 31) / 32, kRedWarps * 32, 0, st>>>(partials, nparts, cols, out);
   SC_CHECK_LAUNCH("colsum_reduce_kernel");
   return SC_OK;
 }
@@ -540,7 +544,7 @@ extern "C" int sc_gelu_bwd(const void* x, const void* dy, void* dx, int32_t dtyp
                                                                (__nv_bfloat16*)dx, rows, cols, rpc, part);
   SC_CHECK_LAUNCH("gelu_bwd_kernel");
   if (dbias) {
-    colsum_reduce_kernel<<<(cols + 31) / 32, 256, 0, st>>>(partials, nparts, cols, dbias);
+    colsum_reduce_kernel<<<(cols + 31) / 32, kRedWarps * 32, 0, st>>>(partials, nparts, cols, dbias);
     SC_CHECK_LAUNCH("colsum_reduce_kernel");
   }
   return SC_OK;
