@@ -654,6 +654,8 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
     const int want = (2 * sms + items - 1) / items;
     const int by_len = (int)((int64_t)total_tokens / nseq / 64 / 8);  // >= one 64-key chunk per warp
     p.head_ks = std::max(1, std::min({kMaxHeadSplit, want, by_len}));
+    static const int ks_env = [] { const char* e = getenv("SC_BWD_HEAD_KS"); return e ? atoi(e) : 0; }();
+    if (ks_env >= 1 && ks_env <= kMaxHeadSplit) p.head_ks = ks_env;  // measurement override
   }
   int ntiles = n_tiles;
   if (ntiles < 0 && (cudaMemcpyAsync(&ntiles, seq_tile_base + nseq, sizeof(int), cudaMemcpyDeviceToHost, st) !=

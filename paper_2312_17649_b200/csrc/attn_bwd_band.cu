@@ -474,6 +474,30 @@ __global__ void __launch_bounds__(128) band_dkv_kernel(Args p) {
 // per-row max / sum, combined across warps in order -> lse; pass 2: P, dP = dOh V^T, dS and
 // dQ_h = dS K, reduced across warps in order.  Writes the head rows' (lse, D) and dQ.
 
+// Keys (sequence-relative) a head row attends: one interval per target group, from the link
+// table -- a few integer ops per chunk instead of a group lookup per (row, key).
+struct Span3 {
+  int lo[3], n[3];  // keys t with (unsigned)(t - lo) < n
+};
+__device__ __forceinline__ Span3 head_row_span(const Args& p, const SeqGroups& g, int i, int nhead) {
+  Span3 s;
+  const int rs = i == 0 ? 0 : i - 1;
+#pragma unroll
+  for (int tg = 0; tg < 3; ++tg) {
+    const int w = i == 0 ? p.links.w[0][tg] : p.links.w[1][tg];
+    int a = 0, b = 0;
+    if (w == SC_LINK_FULL) b = g.len[tg];
+    else if (w >= 0) a = max(0, rs - w), b = min(g.len[tg], rs + w + 1);
+    s.lo[tg] = g.off[tg] + a;
+    s.n[tg] = i < nhead ? max(0, b - a) : 0;
+  }
+  return s;
+}
+__device__ __forceinline__ bool in_span(const Span3& s, int t) {
+  return (unsigned)(t - s.lo[0]) < (unsigned)s.n[0] || (unsigned)(t - s.lo[1]) < (unsigned)s.n[1] ||
+         (unsigned)(t - s.lo[2]) < (unsigned)s.n[2];
+}
+
 template <int NH, int kHeadWarps>
 __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -526,13 +550,6 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
   uint32_t qa[MT][4][4];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) load_a(sQ, 16 * mt, lane, qa[mt]);
-  // row i (head slot) attends key t (sequence-relative)?
-  auto ok = [&](int i, int t) {
-    if (i >= nhead || t >= slen) return false;
-    const int gs = i == 0 ? 0 : 1, rs = i == 0 ? 0 : i - 1;
-    const int tg = t == 0 ? 0 : (t < 1 + g.len[1] ? 1 : 2), rt = t - g.off[tg];
-    return linked(p.links.w[gs][tg], rs, rt);
-  };
   auto stage_chunk = [&](uint32_t buf, const __nv_bfloat16* base, int k0) {
     for (int idx = lane; idx < TILE * 8; idx += 32) {
       const int r = idx >> 3, c = idx & 7;
@@ -565,13 +582,14 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
 #pragma unroll
       for (int hr = 0; hr < 2; ++hr) {
         const int i = 16 * mt + gq + 8 * hr;
+        const Span3 sp = head_row_span(p, g, i, nhead);
         float cm = -INFINITY;
 #pragma unroll
         for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int t = k0 + 8 * nt + 2 * tq + e;
-            sv[nt][2 * hr + e] = ok(i, t) ? sv[nt][2 * hr + e] * c2 : -INFINITY;
+            sv[nt][2 * hr + e] = in_span(sp, t) ? sv[nt][2 * hr + e] * c2 : -INFINITY;
             cm = fmaxf(cm, sv[nt][2 * hr + e]);
           }
         cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
@@ -673,12 +691,13 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
       for (int hr = 0; hr < 2; ++hr) {
         const int i = 16 * mt + gq + 8 * hr;
         const float lse2 = sL[i], Di = sD[i];
+        const Span3 sp = head_row_span(p, g, i, nhead);
 #pragma unroll
         for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int t = k0 + 8 * nt + 2 * tq + e;
-            const float pr = ok(i, t) ? ex2(sv[nt][2 * hr + e] * c2 - lse2) : 0.f;
+            const float pr = in_span(sp, t) ? ex2(sv[nt][2 * hr + e] * c2 - lse2) : 0.f;
             sv[nt][2 * hr + e] = pr * (dp[nt][2 * hr + e] - Di) * p.inv_scale;
             if (head_keys && ch == 0) {  // chunk 0 holds the cls / query keys
               const int kc = 8 * nt + 2 * tq + e;
