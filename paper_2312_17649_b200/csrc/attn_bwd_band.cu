@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(256) head_part_reduce_kernel(Args p) {
 // Kernel B: doc keys [k0, k0+64) of one sequence, one head.  Sources: the band doc rows
 // [k0 - w, k0 + 64 + w) and the head rows (cls / query) attending the doc.
 template <int NB, int NH>
-__global__ void __launch_bounds__(128) band_dkv_kernel(Args p) {
+__global__ void __launch_bounds__(128, 4) band_dkv_kernel(Args p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int KR = 48 + NB;
   const int tile = blockIdx.x, h = blockIdx.y;
@@ -826,6 +826,8 @@ int launch_pair(const Args& a, int ntiles, int phase, cudaStream_t st) {
   if (!attr) {
     cudaFuncSetAttribute(band_dq_kernel<NB, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(band_dkv_kernel<NB, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(band_dq_kernel<NB, NH>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(band_dkv_kernel<NB, NH>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr = true;
   }
   dim3 grid(ntiles, a.H);
