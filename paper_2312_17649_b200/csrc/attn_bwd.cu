@@ -640,9 +640,10 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
   const size_t pbytes = (part_bytes(total_tokens, heads, nseq, max_qgroup_len) + 255) & ~(size_t)255;
   if (workspace_bytes >= soff + pbytes)
     p.head_part = reinterpret_cast<float*>(static_cast<char*>(workspace) + soff);
-  // head-row pass: 2 warps per (sequence, head) for short sequences (<= 4 key chunks of 64),
-  // else 8, split over CTAs when there are too few (sequence, head) pairs
-  p.head_warps = (int64_t)total_tokens <= (int64_t)256 * nseq ? 1 : 8;
+  // head-row pass: 1 warp per (sequence, head) CTA for short sequences (<= 4 key chunks of 64: every
+  // CTA resident in one wave), else 2 (measured best of 1 / 2 / 8 at 8 x 4099), keys split over CTAs
+  // when there are too few (sequence, head) pairs
+  p.head_warps = (int64_t)total_tokens <= (int64_t)256 * nseq ? 1 : 2;
   static const int hw_env = [] { const char* e = getenv("SC_BWD_HEAD_WARPS"); return e ? atoi(e) : 0; }();
   if (hw_env == 1 || hw_env == 2 || hw_env == 8) p.head_warps = hw_env;  // measurement override
   p.head_ks = 1;
@@ -652,7 +653,7 @@ extern "C" int sc_attn_bwd(const void* q, const void* k, const void* v, int64_t 
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int items = nseq * heads;
     const int want = (2 * sms + items - 1) / items;
-    const int by_len = (int)((int64_t)total_tokens / nseq / 64 / 8);  // >= one 64-key chunk per warp
+    const int by_len = (int)((int64_t)total_tokens / nseq / 64 / p.head_warps);  // >= one 64-key chunk per warp
     p.head_ks = std::max(1, std::min({kMaxHeadSplit, want, by_len}));
     static const int ks_env = [] { const char* e = getenv("SC_BWD_HEAD_KS"); return e ? atoi(e) : 0; }();
     if (ks_env >= 1 && ks_env <= kMaxHeadSplit) p.head_ks = ks_env;  // measurement override
