@@ -551,6 +551,7 @@ __global__ void __launch_bounds__(kHeadWarps * 32) head_dq_kernel(Args p) {
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) load_a(sQ, 16 * mt, lane, qa[mt]);
   auto stage_chunk = [&](uint32_t buf, const __nv_bfloat16* base, int k0) {
+    __syncwarp();  // the previous chunk's ldmatrix reads of this buffer precede the refill
     for (int idx = lane; idx < TILE * 8; idx += 32) {
       const int r = idx >> 3, c = idx & 7;
       const bool in = k0 + r < slen;

@@ -17,6 +17,8 @@ for pattern, w, pad, dt, d, qds in [("sparse", 4, "exclude", torch.bfloat16, 64,
                                     ("qds", 4, "exclude", torch.float32, 32, 7)]:
     m = rng.integers(1, 12, size=3)
     n = rng.integers(1, 150, size=3)
+    if qds == 0 and pad == "exclude":
+        n = np.array([1200, 900, 40])  # long rows: 2-warp head-row CTAs with the key split, scalar partial reduce
     lay = P.PackedLayout.from_lengths(m + n + 3, m + 1, device="cuda", qds_every=qds)
     pat = P.make_pattern(pattern, w)
     H = 2
