@@ -203,8 +203,12 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, in
 // out[c] = sum over partial rows k of part[k][c]: block = 32 columns x 8 warps, warp w sums rows
 // k = w (mod 8) (four loads in flight), the 8 warp sums are added in warp order (deterministic).
 constexpr int kRedWarps = 8;
+// blockIdx.y = 1 reduces a second (part, out) pair in the same launch (LayerNorm dgamma + dbeta).
 __global__ void __launch_bounds__(kRedWarps * 32) colsum_reduce_kernel(const float* __restrict__ part, int nparts,
-                                                                       int cols, float* __restrict__ out) {
+                                                                       int cols, float* __restrict__ out,
+                                                                       const float* __restrict__ part1 = nullptr,
+                                                                       float* __restrict__ out1 = nullptr) {
+  if (blockIdx.y == 1) part = part1, out = out1;
   __shared__ float red[kRedWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
@@ -330,9 +334,7 @@ extern "C" int sc_layernorm_bwd(const float* dy, const void* dy_bf16, const void
                 (float*)mean, (float*)rstd, dx, pg, pb, rows, cols, 0.f, (unsigned)nparts, st, (void*)dy_bf16,
                 dx_bf16);
   SC_CHECK_LAUNCH("ln_bwd_kernel");
-  colsum_reduce_kernel<<<(cols + 31) / 32, kRedWarps * 32, 0, st>>>(pg, nparts, cols, dgamma);
-  SC_CHECK_LAUNCH("colsum_reduce_kernel");
-  colsum_reduce_kernel<<<(cols + 31) / 32, kRedWarps * 32, 0, st>>>(pb, nparts, cols, dbeta);
+  colsum_reduce_kernel<<<dim3((cols + 31) / 32, 2), kRedWarps * 32, 0, st>>>(pg, nparts, cols, dgamma, pb, dbeta);
   SC_CHECK_LAUNCH("colsum_reduce_kernel");
   return SC_OK;
 }
