@@ -61,7 +61,7 @@ def workload_name(doc_len, s):
         return (f"ELECTRA-base sparse cross-encoder, passages {QUERY_LEN + doc_len} tok (q{QUERY_LEN}+p{doc_len}, "
                 f"s={s}), w=4 asymmetric, bf16 (BASELINE configs[1])")
     return (f"ELECTRA-base sparse cross-encoder, documents {QUERY_LEN + doc_len} tok (q{QUERY_LEN}+d{doc_len}, "
-            f"s={s}), w=4 asymmetric, packed varlen batch (BASELINE configs[2])")
+            f"s={s}), w=4 asymmetric, packed batch (BASELINE configs[2])")
 
 
 def make_batch(P, cfg, doc_len, pairs, rank, seed=0, varlen=False):
@@ -135,21 +135,21 @@ class ClockSampler:
 # bench.py executes oracle/, as the timed CPU baseline.
 # ---------------------------------------------------------------------------
 
-def cpu_oracle_layer_times(cfg, doc_len, reps, budget_s=None):
+def cpu_oracle_pair_times(cfg, doc_len, reps, budget_s=None):
+    """Seconds per whole pair on the CPU oracle: embed + 12 layers + score head of ONE (q10, d)
+    pair (R/encoder.py:475-509 restated in oracle/), f32 numpy on all host cores.  Stops after
+    ``budget_s`` seconds (at least one timed pair)."""
     from oracle import sparsecross_oracle as O
 
-    ocfg = dict(cfg)
-    wt = O.init_weights(ocfg, 0, np.float32)
+    wt = O.init_weights(dict(cfg), 0, np.float32)
     ids, spans = O.gen_random_ids(0, QUERY_LEN, doc_len, 1, cfg["vocab_size"])
-    x = O.embed(ids, wt, np.float32)
-    pattern = O.resolve_pattern(ocfg, spans)
     times = []
     t_start = time.perf_counter()
-    for r in range(reps):
+    for _ in range(reps):
         t0 = time.perf_counter()
-        O.layer_forward(x, spans, pattern, wt, r % cfg["layers"], ocfg)
+        O.score(ids, spans, dict(cfg), wt)
         times.append(time.perf_counter() - t0)
-        if budget_s and time.perf_counter() - t_start > budget_s and len(times) >= 3:
+        if budget_s and time.perf_counter() - t_start > budget_s:
             break
     return times
 
@@ -162,19 +162,23 @@ def cpu_threads():
 
 
 def run_reference(args):
+    """The reference arm: the CPU restatement of the reference's CrossEncoder.score (f32 numpy,
+    all host cores), one whole (q10, d4086) pair per step -- the same workload, config and metric
+    as the GPU arm, bounded so the run ends within a few minutes (--ref-budget seconds)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cfg, doc_len, s = workload(args)
-    times = cpu_oracle_layer_times(cfg, doc_len, args.warmup + args.steps)
-    timed = times[args.warmup:] or times
-    t_layer = statistics.median(timed)
-    value = 1.0 / (cfg["layers"] * t_layer)
-    sample = (f"1 pair at s={s} (q{QUERY_LEN}+d{doc_len}), 1 of {cfg['layers']} identical encoder layers per step, "
-              f"f32 numpy oracle port of R/encoder.py:306-371; pairs/s = 1/(layers * median layer time)")
+    cpu_oracle_pair_times(cfg, doc_len, 1)  # warm-up: page in the weights (one pair)
+    times = cpu_oracle_pair_times(cfg, doc_len, args.steps, budget_s=args.ref_budget)
+    t_pair = statistics.median(times)
+    value = 1.0 / t_pair
+    sample = (f"{len(times)} whole pairs at s={s} (q{QUERY_LEN}+d{doc_len}): embed + {cfg['layers']} layers + score "
+              f"head, f32 numpy oracle port of R/encoder.py:475-509 (pinned to reference goldens); pairs/s = "
+              f"1 / median pair time ({t_pair:.2f} s); timed steps capped by a {args.ref_budget:.0f} s budget")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
-        "steps": len(timed), "warmup": args.warmup, "ms_per_step": t_layer * 1e3, "higher_is_better": True,
+        "steps": len(times), "warmup": 1, "ms_per_step": t_pair * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generator ids, seed 0)",
         "config": {"workload": workload_name(doc_len, s), "seq_len": s,
                    "doc_len": doc_len, "query_len": QUERY_LEN, "window": 4, "pattern": "sparse"},
@@ -183,6 +187,183 @@ def run_reference(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ---------------------------------------------------------------------------
+# Parity of the bench's own output, and the variant workloads (C2 passages,
+# varlen documents, the C4 attention sweep) recorded beside the headline.
+# ---------------------------------------------------------------------------
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+BF16_TOL = 2e-2
+
+
+def rank_order(scores):
+    """R/evaluation.py:194-201: stable sort by (-score, candidate position)."""
+    return sorted(range(len(scores)), key=lambda j: (-float(scores[j]), j))
+
+
+def parity(scores, ref, tol, source):
+    """Max |score - reference| of the bench's own first len(ref) pairs (which ARE the golden pairs:
+    ids from default_rng((0, 0, j))), ranking identity and flips beyond 2 x tol."""
+    k = min(len(scores), len(ref))
+    got, ref = np.asarray(scores[:k], np.float64), np.asarray(ref[:k], np.float64)
+    ro, pos = rank_order(ref), {c: i for i, c in enumerate(rank_order(got))}
+    flips = sum(1 for a in range(k) for b in range(a + 1, k)
+                if pos[ro[a]] > pos[ro[b]] and abs(ref[ro[a]] - ref[ro[b]]) > 2 * tol)
+    return {"max_abs_err": float(np.abs(got - ref).max()), "n": k, "tol": tol,
+            "ranking_identical": rank_order(got) == ro, "flips_beyond_2tol": flips, "reference": source}
+
+
+def headline_parity(scores_np, doc_len, varlen):
+    try:
+        if varlen:
+            return None
+        if doc_len == 4086:
+            ref = np.load(os.path.join(GOLDEN, "ranking.npz"))["scores"]
+            src = "tests/golden/ranking.npz: unmodified reference CrossEncoder.score (f32) on the same pairs"
+        elif doc_len == 164:
+            ref = np.load(os.path.join(GOLDEN, "encoder.npz"))["electra_passage_scores"]
+            src = "tests/golden/encoder.npz:electra_passage_scores (unmodified reference, f32)"
+        else:
+            return None
+        return parity(scores_np, ref, BF16_TOL, src)
+    except FileNotFoundError:
+        return None
+
+
+def attn_kvalid(pattern, lens, qds=False):
+    """Valid (row, key) pairs of one sequence under ``pattern`` (SURVEY §8d K_valid): full links
+    count rows x target length, windowed doc->doc links the in-range band slots."""
+    gl = dict(zip(("cls", "query", "doc"), lens))
+    total = 0
+    for src, tl in pattern.targets.items():
+        for tgt, w in tl:
+            if w == math.inf:
+                total += gl[src] * gl[tgt]
+            else:
+                n = gl[src]
+                r = np.arange(n)
+                total += int((np.minimum(n - 1, r + w) - np.maximum(0, r - w) + 1).sum())
+    return total
+
+
+def attention_sweep(P, dev, peaks_, nseq=64, doc=4086, H=12, d=64, reps=10,
+                    windows=(("sparse", 1), ("sparse", 4), ("sparse", 16), ("sparse", 64), ("sparse", 256),
+                             ("sparse", math.inf), ("full", math.inf))):
+    """C4 (BASELINE configs[3]): sc_attn_fwd alone at s=4099 over a packed batch of ``nseq``
+    sequences, bf16 Q/K/V ~ N(0,1); per window: time, algorithmic GB/s (4*s*h*2 B per sequence-layer)
+    and TFLOP/s (4*d*H*K_valid), each against its measured peak; the binding one is ``bound``."""
+    import torch
+
+    hbm, tf_burst = peaks_[0], peaks_[1]
+    s = QUERY_LEN + doc + 3
+    T = s * nseq
+    lay = P.PackedLayout.from_lengths([s] * nseq, [QUERY_LEN + 1] * nseq, device=dev)
+    g = torch.Generator(device=dev).manual_seed(0)
+    qkv = torch.randn((T, 3 * H * d), device=dev, generator=g).to(torch.bfloat16)
+    out = torch.empty((T, H * d), device=dev, dtype=torch.bfloat16)
+    st = torch.cuda.current_stream(dev)
+    res = []
+    for name, w in windows:
+        pat = P.make_pattern(name, w)
+        f = lambda: P.attend_packed(qkv[:, :H * d], qkv[:, H * d:2 * H * d], qkv[:, 2 * H * d:], lay, pat, H,
+                                    out=out, check=False)
+        for _ in range(3):
+            f()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            f()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        byts = 4 * T * H * d * 2
+        flops = 4 * d * H * attn_kvalid(pat, (1, QUERY_LEN + 1, doc + 1)) * nseq
+        gbs, tfs = byts / ms / 1e6, flops / ms / 1e9
+        bound = "hbm" if flops / byts < tf_burst * 1e12 / (hbm * 1e9) else "tensor"
+        res.append({"pattern": name, "window": "inf" if w == math.inf else int(w), "ms": round(ms, 4),
+                    "us_per_seq_layer": round(ms * 1e3 / nseq, 2), "GB/s": round(gbs, 1),
+                    "frac_hbm": round(gbs / hbm, 3), "TFLOP/s": round(tfs, 1), "frac_tensor": round(tfs / tf_burst, 3),
+                    "bound": bound, "frac_of_bound": round(gbs / hbm if bound == "hbm" else tfs / tf_burst, 3)})
+    return {"workload": f"sc_attn_fwd alone, {nseq} x s={s} packed, H={H}, d={d}, bf16, AUTO kernel choice",
+            "peaks": {"hbm_GBs": hbm, "bf16_TFLOPs_burst": tf_burst}, "reps": reps, "points": res}
+
+
+def timed_scores(fn, steps, stream):
+    """CUDA-event time (ms) of ``steps`` back-to-back calls of fn after 3 warm-ups."""
+    import torch
+
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def passages_variant(P, dev, steps, pairs=1024):
+    """C2 (BASELINE configs[1]): 1024 passages (q10 + p164, s=177) per step as one CUDA graph."""
+    import torch
+    from paper_2312_17649_b200.encoder import GraphedScorer
+
+    cfg = dict(ELECTRA, max_positions=512)
+    model = P.CrossEncoder(P.EncoderConfig(**cfg, precision="bf16"), seed=0, device=dev)
+    batch = make_batch(P, cfg, 164, pairs, 0)
+    gs = GraphedScorer(model, batch)
+    ids_dev = torch.from_numpy(batch.ids).to(dev)
+    ms = timed_scores(lambda: gs(ids_dev), steps, torch.cuda.current_stream(dev))
+    sc = gs(ids_dev).cpu().numpy()
+    return {"value": pairs * steps / (ms / 1e3), "unit": "pairs/s", "ms_per_step": ms / steps, "steps": steps,
+            "pairs_per_step": pairs, "seq_len": 177, "cuda_graph": True, "dtype": "bf16",
+            "parity": headline_parity(sc, 164, False)}
+
+
+def fp32_variant(P, dev, steps, pairs=32):
+    """Ranking-exact fp32 (north-star "identical per-query rankings"): the same documents in fp32,
+    projections as split-bf16 tensor-core products (fp32_gemm="bf16x6") vs cuBLAS SGEMM; parity of
+    both against the reference golden of these exact pairs."""
+    import torch
+
+    cfg = dict(ELECTRA, max_positions=4099)
+    batch = make_batch(P, cfg, 4086, pairs, 0)
+    out = {}
+    for mode, nsteps in (("bf16x6", steps), ("sgemm", 2)):
+        model = P.CrossEncoder(P.EncoderConfig(**cfg, precision="f32"), seed=0, device=dev, fp32_gemm=mode)
+        layout = model.make_layout(batch)
+        ids = torch.from_numpy(batch.ids).to(dev)
+        fn = lambda: model.scores_from_hidden(model.encode_packed(ids, layout), layout)
+        ms = timed_scores(fn, nsteps, torch.cuda.current_stream(dev))
+        sc = fn().cpu().numpy()
+        par = headline_parity(sc, 4086, False)
+        if par is not None:
+            par["tol"] = 1e-6
+            par["flips_beyond_2tol"] = None
+        out[mode] = {"value": pairs * nsteps / (ms / 1e3), "unit": "pairs/s", "ms_per_step": ms / nsteps,
+                     "steps": nsteps, "pairs_per_step": pairs, "dtype": "f32", "parity": par}
+        del model
+        torch.cuda.empty_cache()
+    out["speedup_vs_sgemm"] = out["bf16x6"]["value"] / out["sgemm"]["value"]
+    return out
+
+
+def varlen_variant(P, dev, model, steps, pairs=64):
+    """Documents with lengths ~ U{54..4086}, packed varlen, same model."""
+    import torch
+
+    cfg = dict(ELECTRA, max_positions=4099)
+    batch = make_batch(P, cfg, 4086, pairs, 0, varlen=True)
+    layout = model.make_layout(batch)
+    ids = torch.from_numpy(batch.ids).to(dev)
+    fn = lambda: model.scores_from_hidden(model.encode_packed(ids, layout), layout)
+    ms = timed_scores(fn, steps, torch.cuda.current_stream(dev))
+    return {"value": pairs * steps / (ms / 1e3), "unit": "pairs/s", "ms_per_step": ms / steps, "steps": steps,
+            "pairs_per_step": pairs, "tokens_per_step": int(layout.total_tokens), "dtype": "bf16"}
 
 
 # ---------------------------------------------------------------------------
@@ -291,7 +472,7 @@ def run_gpu(args):
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
-    e2e_steps = max(3, args.steps // 2)
+    e2e_steps = args.steps
     for _ in range(e2e_steps):
         e2e_step()
     f1.record(stream)
@@ -301,8 +482,12 @@ def run_gpu(args):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = n * world * e2e_steps / (float(te.item()) / 1e3)
 
+    # ---- parity of this run's own scores (outside the timed regions) ----
+    own = device_step().cpu().numpy()[:n]  # every rank (the step's gather is a collective)
+    par = headline_parity(own, doc_len, args.varlen) if rank == 0 else None
+
     # ---- variant: last layer on the [CLS] rows only (opt-in serving mode) ----
-    variants = None
+    variants = {}
     if not args.prune_last_layer and graphed is None:
         model.prune_last_layer = True
         for _ in range(2):
@@ -319,10 +504,15 @@ def run_gpu(args):
         if world > 1:
             dist.all_reduce(tv, op=dist.ReduceOp.MAX)
         model.prune_last_layer = False
-        variants = {"prune_last_layer": {
+        variants["prune_last_layer"] = {
             "value": n * world * vsteps / (float(tv.item()) / 1e3), "unit": "pairs/s", "steps": vsteps,
             "note": "CrossEncoder(prune_last_layer=True): last layer past K/V on the [CLS] rows only (the score "
-                    "reads x[:,0], R/encoder.py:506); same scores, not the headline"}}
+                    "reads x[:,0], R/encoder.py:506); same scores, not the headline"}
+    if world == 1 and not args.no_variants and doc_len == 4086 and not args.varlen:
+        variants["varlen_documents"] = varlen_variant(P, dev, model, max(3, args.steps // 2))
+        variants["passages"] = passages_variant(P, dev, args.steps)
+        variants["attention_sweep"] = attention_sweep(P, dev, (hbm_peak, tf_burst))
+        variants["fp32_ranking_exact"] = fp32_variant(P, dev, max(3, args.steps // 4))
 
     # ---- roofline of the attention kernel (sc_attn_fwd, band + head-row pass) ----
     attn_bytes = 4 * layout.total_tokens * cfg["embed_dim"] * 2  # Q,K,V read + O write, bf16
@@ -371,11 +561,11 @@ def run_gpu(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        times = cpu_oracle_layer_times(cfg, doc_len, reps=50, budget_s=args.cpu_budget)
-        tl = statistics.median(times)
-        cpu = {"value": 1.0 / (cfg["layers"] * tl), "unit": "pairs/s", "cores": cpu_threads(), "kind": "port",
-               "sample": f"1 pair at s={s}, {len(times)} x 1-of-{cfg['layers']} encoder layers (f32 numpy oracle port, "
-                         f"R/encoder.py:306-371), median {tl * 1e3:.1f} ms/layer; pairs/s = 1/(layers * layer time)"}
+        times = cpu_oracle_pair_times(cfg, doc_len, reps=50, budget_s=args.cpu_budget)
+        tp = statistics.median(times)
+        cpu = {"value": 1.0 / tp, "unit": "pairs/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"{len(times)} whole pairs at s={s} (embed + {cfg['layers']} layers + score head, f32 numpy "
+                         f"oracle port of R/encoder.py:475-509), median {tp:.2f} s/pair"}
 
     if rank == 0:
         line = {
@@ -402,10 +592,16 @@ def run_gpu(args):
                               "peak": tf_sus, "unit": "TFLOP/s", "note": "GEMM FLOPs per step / step time vs sustained bf16"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(batch.ids.nbytes),
-                    "d2h_bytes_per_step": int(host_scores.numel() * 4)},
+                    "d2h_bytes_per_step": int(host_scores.numel() * 4), "steps": e2e_steps,
+                    "path": ("GraphedScorer.__call__ from pinned host ids (captured layout reused: same shape)"
+                             if graphed is not None else
+                             "CrossEncoder.make_layout (K1 index build) + encode_packed + scores_from_hidden from "
+                             "pinned host ids, scores copied back"),
+                    "note": "same step count as value; e2e within +-1% of value is run-to-run noise, not a gain"},
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
-            "variants": variants,
+            "parity": par,
+            "variants": variants or None,
             "impl": "b200",
         }
         print(json.dumps(line), flush=True)
@@ -429,7 +625,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--prune-last-layer", action="store_true",
                     help="score with the last layer on the [CLS] rows only (CrossEncoder(prune_last_layer=True))")
-    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU oracle timing")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU oracle timing (cpu_baseline)")
+    ap.add_argument("--ref-budget", type=float, default=120.0, help="seconds of timed pairs in --impl reference")
+    ap.add_argument("--no-variants", action="store_true", help="skip the passages / sweep / fp32 variants")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

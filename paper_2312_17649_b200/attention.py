@@ -257,14 +257,14 @@ def _run_groups(qkv: dict, pattern: AttentionPattern, scale: float, padding: str
         cat.append(x)
     dtype = cat[0].dtype
     cat = [c.to(dtype) for c in cat]
+    if pattern.global_positions and max(pattern.global_positions) >= lens[2]:  # R/attention.py:437-438
+        raise AttentionError("global positions outside the document group")
     layout = PackedLayout.from_lengths([s], [lens[1]], device=cat[0].device,
                                        qds_positions=[pattern.global_positions] if pattern.global_positions else None)
-    if pattern.global_positions and max(pattern.global_positions) >= lens[2]:
-        raise AttentionError("global positions outside the document group")
     out = attend_packed(cat[0], cat[1], cat[2], layout, pattern, H, scale, padding)
     if store is not None:  # what group_attention_backward needs
         store.update(layout=layout, qkv=torch.cat(cat, dim=1).contiguous(), out=out, H=H, d=d, lens=lens, lead=lead,
-                     was_np=was_np, np_dtype=np.dtype(str(orig_dtype).replace("torch.", "")))
+                     was_np=was_np, np_dtype=np.dtype(str(orig_dtype).replace("torch.", "")) if was_np else None)
     out = out.reshape(s, H, d).permute(1, 0, 2).reshape(*lead, s, d) if len(lead) else out.reshape(s, d)
     outs, lo = [], 0
     for n in lens:

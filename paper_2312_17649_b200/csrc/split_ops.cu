@@ -1,0 +1,123 @@
+// fp32 GEMM operands as three bf16 planes, for the ranking-exact fp32 mode.
+//
+// x = p0 + p1 + p2 with p0 = bf16_rn(x), p1 = bf16_rn(x - p0), p2 = bf16_rn(x - p0 - p1):
+// 24 significant bits, |x - p0 - p1 - p2| <= 2^-27 |x|.  A product x*w is then
+// sum_{i+j<=2} p_i(x) q_j(w) (six bf16 tensor-core products, fp32 accumulation;
+// the dropped terms are <= 2^-27 relative), i.e. the reference's fp32 GEMMs
+// (R/encoder.py:322-324, :345, :350, :352) at SGEMM accuracy on the bf16 tensor
+// pipe.  Planes are stored per row as [p0 | p1 | p2] so that the K-prefixes
+// [p0 | p1 | p2], [p0 | p1] and [p0] of one buffer are the left operands of the
+// three GEMMs that sum the six products (encoder.py: _linear_x6).
+//
+// Producers fuse the split into their pass: the optional bias and exact-erf
+// GELU (R/encoder.py:258-259, erff as the fp32 path) are applied first and the
+// fp32 result can be kept as well (y, may alias x).
+#include "common.cuh"
+
+namespace sc {
+
+__device__ __forceinline__ void split3(float v, __nv_bfloat16& a, __nv_bfloat16& b, __nv_bfloat16& c) {
+  a = __float2bfloat16_rn(v);
+  const float r1 = v - __bfloat162float(a);  // exact in fp32
+  b = __float2bfloat16_rn(r1);
+  c = __float2bfloat16_rn(r1 - __bfloat162float(b));
+}
+
+__device__ __forceinline__ uint2 pack4(__nv_bfloat16 a, __nv_bfloat16 b, __nv_bfloat16 c, __nv_bfloat16 d) {
+  __nv_bfloat162 lo = __halves2bfloat162(a, b), hi = __halves2bfloat162(c, d);
+  return make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+}
+
+// One float4 per thread-iteration (cols % 4 == 0, 16-byte aligned rows); rows walked last-to-first
+// (the producing GEMM's most recent output is still in L2).
+template <bool kBias, bool kGelu>
+__global__ void __launch_bounds__(256) split3_vec_kernel(const float* __restrict__ x, int64_t ldx,
+                                                         const float* __restrict__ bias, float* __restrict__ y,
+                                                         int64_t ldy, __nv_bfloat16* __restrict__ p, int64_t ldp,
+                                                         int64_t rows, int cols) {
+  const int c4 = cols >> 2;
+  const int64_t n = rows * c4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t j = n - 1 - i;
+    const int64_t r = j / c4;
+    const int c = (int)(j - r * c4) * 4;
+    float4 v = *reinterpret_cast<const float4*>(x + r * ldx + c);
+    if (kBias) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(bias + c));
+      v.x += b.x, v.y += b.y, v.z += b.z, v.w += b.w;
+    }
+    if (kGelu) {
+      v.x = 0.5f * v.x * (1.f + erff(v.x * 0.70710678118654752440f));
+      v.y = 0.5f * v.y * (1.f + erff(v.y * 0.70710678118654752440f));
+      v.z = 0.5f * v.z * (1.f + erff(v.z * 0.70710678118654752440f));
+      v.w = 0.5f * v.w * (1.f + erff(v.w * 0.70710678118654752440f));
+    }
+    if (y) *reinterpret_cast<float4*>(y + r * ldy + c) = v;
+    __nv_bfloat16 a[4], b[4], d[4];
+    split3(v.x, a[0], b[0], d[0]);
+    split3(v.y, a[1], b[1], d[1]);
+    split3(v.z, a[2], b[2], d[2]);
+    split3(v.w, a[3], b[3], d[3]);
+    __nv_bfloat16* pr = p + r * ldp + c;
+    *reinterpret_cast<uint2*>(pr) = pack4(a[0], a[1], a[2], a[3]);
+    *reinterpret_cast<uint2*>(pr + cols) = pack4(b[0], b[1], b[2], b[3]);
+    *reinterpret_cast<uint2*>(pr + 2 * cols) = pack4(d[0], d[1], d[2], d[3]);
+  }
+}
+
+template <bool kBias, bool kGelu>
+__global__ void split3_kernel(const float* __restrict__ x, int64_t ldx, const float* __restrict__ bias,
+                              float* __restrict__ y, int64_t ldy, __nv_bfloat16* __restrict__ p, int64_t ldp,
+                              int64_t rows, int cols) {
+  const int64_t n = rows * cols;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t r = i / cols;
+    const int c = (int)(i - r * cols);
+    float v = x[r * ldx + c];
+    if (kBias) v += __ldg(bias + c);
+    if (kGelu) v = 0.5f * v * (1.f + erff(v * 0.70710678118654752440f));
+    if (y) y[r * ldy + c] = v;
+    __nv_bfloat16* pr = p + r * ldp + c;
+    split3(v, pr[0], pr[cols], pr[2 * cols]);
+  }
+}
+
+template <bool kBias, bool kGelu>
+static void launch_split(bool vec, const float* x, int64_t ldx, const float* bias, float* y, int64_t ldy,
+                         __nv_bfloat16* p, int64_t ldp, int64_t rows, int cols, cudaStream_t st) {
+  const int64_t work = vec ? rows * (cols / 4) : rows * cols;
+  int64_t blocks = (work + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (vec)
+    split3_vec_kernel<kBias, kGelu><<<(unsigned)blocks, 256, 0, st>>>(x, ldx, bias, y, ldy, p, ldp, rows, cols);
+  else
+    split3_kernel<kBias, kGelu><<<(unsigned)blocks, 256, 0, st>>>(x, ldx, bias, y, ldy, p, ldp, rows, cols);
+}
+
+}  // namespace sc
+
+using namespace sc;
+
+extern "C" int sc_split_bf16x3(const float* x, int64_t ldx, const float* bias, int32_t gelu, float* y, int64_t ldy,
+                               void* planes, int64_t ldp, int64_t rows, int32_t cols, void* stream) {
+  SC_CHECK_ARG(x && planes, "sc_split_bf16x3: null pointer");
+  SC_CHECK_ARG(rows >= 0 && cols >= 1 && ldx >= cols && ldp >= 3LL * cols && (!y || ldy >= cols),
+               "sc_split_bf16x3: bad shape");
+  if (rows == 0) return SC_OK;
+  const bool vec = cols % 4 == 0 && ldx % 4 == 0 && ldp % 4 == 0 && (!y || ldy % 4 == 0) &&
+                   !(((uintptr_t)x | (uintptr_t)y | (uintptr_t)bias) & 15) && !((uintptr_t)planes & 7);
+  cudaStream_t st = (cudaStream_t)stream;
+  __nv_bfloat16* p = (__nv_bfloat16*)planes;
+  if (bias && gelu)
+    launch_split<true, true>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, st);
+  else if (bias)
+    launch_split<true, false>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, st);
+  else if (gelu)
+    launch_split<false, true>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, st);
+  else
+    launch_split<false, false>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, st);
+  SC_CHECK_LAUNCH("split3_kernel");
+  return SC_OK;
+}

@@ -329,8 +329,15 @@ extern "C" int sc_layernorm_bwd(const float* dy, const void* dy_bf16, const void
   cudaStream_t st = (cudaStream_t)stream;
   float* pg = partials;
   float* pb = partials + (int64_t)nparts * cols;
-  if (rows > 0)
-    ln_dispatch(a_dtype == SC_DTYPE_F32, !b || b_dtype == SC_DTYPE_F32, false, a, b, gamma, nullptr, dy, nullptr,
+  if (rows == 0) {  // no partial rows to reduce: the parameter gradients are exactly zero
+    if (cudaMemsetAsync(dgamma, 0, sizeof(float) * cols, st) != cudaSuccess ||
+        cudaMemsetAsync(dbeta, 0, sizeof(float) * cols, st) != cudaSuccess) {
+      set_error("sc_layernorm_bwd: cudaMemsetAsync failed");
+      return SC_ERR_CUDA;
+    }
+    return SC_OK;
+  }
+  ln_dispatch(a_dtype == SC_DTYPE_F32, !b || b_dtype == SC_DTYPE_F32, false, a, b, gamma, nullptr, dy, nullptr,
                 (float*)mean, (float*)rstd, dx, pg, pb, rows, cols, 0.f, (unsigned)nparts, st, (void*)dy_bf16,
                 dx_bf16);
   SC_CHECK_LAUNCH("ln_bwd_kernel");

@@ -264,18 +264,63 @@ def _fp32_gemms(enabled: bool):
         torch.backends.cuda.matmul.allow_tf32 = prev
 
 
+FP32_GEMMS = ("sgemm", "bf16x6")
+
+
+def _split_weight_x6(w: torch.Tensor) -> torch.Tensor:
+    """fp32 weight [N, K] -> bf16 [N, 6K] = [W0 W0 W0 | W1 W1 | W2] with W = W0 + W1 + W2 (each
+    plane the round-to-nearest bf16 of the remaining residual; one-time, at upload)."""
+    w = w.float()
+    w0 = w.to(torch.bfloat16)
+    r = w - w0.float()
+    w1 = r.to(torch.bfloat16)
+    w2 = (r - w1.float()).to(torch.bfloat16)
+    return torch.cat([w0, w0, w0, w1, w1, w2], dim=1).contiguous()
+
+
+def split_planes(x: torch.Tensor, bias=None, gelu: bool = False, keep: torch.Tensor | None = None) -> torch.Tensor:
+    """fp32 [M, K] (+ bias, GELU) -> bf16 planes [M, 3K] = [p0 | p1 | p2] (sc_split_bf16x3);
+    ``keep`` (optional, may be x) receives the fp32 value after bias/GELU."""
+    M, K = x.shape
+    planes = torch.empty((M, 3 * K), dtype=torch.bfloat16, device=x.device)
+    _lib.call("sc_split_bf16x3", x.data_ptr(), x.stride(0), _lib.ptr(bias), int(gelu), _lib.ptr(keep),
+              K if keep is None else keep.stride(0), planes.data_ptr(), planes.stride(0), M, K,
+              _lib.stream_handle(), exc=EncoderError)
+    return planes
+
+
+def _linear_x6(planes: torch.Tensor, w6: torch.Tensor) -> torch.Tensor:
+    """a W^T in fp32 from the planes of a ([M, 3K]) and of W ([N, 6K]): three bf16 tensor-core GEMMs
+    with fp32 accumulation summing the six products p_i q_j, i + j <= 2:
+      [p0 p1 p2] [q0; q0; q0] + [p0 p1] [q1; q1] + p0 q2
+    (the K-prefixes of one plane buffer; dropped terms <= 2^-27 relative).  R/encoder.py:322-324,
+    :345, :350, :352 at SGEMM accuracy."""
+    K = planes.shape[1] // 3
+    c = torch.mm(planes, w6[:, :3 * K].t(), out_dtype=torch.float32)
+    c = torch.addmm(c, planes[:, :2 * K], w6[:, 3 * K:5 * K].t(), out_dtype=torch.float32)
+    return torch.addmm(c, planes[:, :K], w6[:, 5 * K:].t(), out_dtype=torch.float32)
+
+
 class CrossEncoder:
     """Config + device weights; batched inference (R/encoder.py:450-538)."""
 
     def __init__(self, config: EncoderConfig, weights: dict | None = None, seed: int = 0,
                  device="cuda", attn_algo: str = "auto", prune_last_layer: bool = False,
-                 fused_ffn: bool = True, fused_ln: bool = False):
+                 fused_ffn: bool = True, fused_ln: bool = False, fp32_gemm: str = "sgemm"):
         """``prune_last_layer``: the scoring entry points (score*, GraphedScorer) run
         the last layer for the [CLS] rows only past the K/V projection -- the score
         reads nothing else (R/encoder.py:506).  Scores are unchanged; the reference's
         finite check then covers the last layer's [CLS] rows only.  ``forward``
-        always computes every row."""
+        always computes every row.
+
+        ``fp32_gemm`` (fp32 precisions only): "sgemm" runs the four projections as cuBLAS
+        fp32 SGEMM (TF32 off); "bf16x6" runs them on the bf16 tensor cores as six split
+        products per GEMM (operands as three bf16 planes, sc_split_bf16x3; see _linear_x6),
+        SGEMM-level accuracy at several times the speed."""
+        if fp32_gemm not in FP32_GEMMS:
+            raise EncoderError(f"fp32_gemm must be one of {FP32_GEMMS}, got {fp32_gemm!r}")
         self.config = config
+        self.fp32_gemm = fp32_gemm if config.torch_dtype == torch.float32 else "sgemm"
         self.device = torch.device(device)
         self.attn_algo = attn_algo
         self.prune_last_layer = prune_last_layer
@@ -324,6 +369,12 @@ class CrossEncoder:
             })
         self.head_w = f32(w["head_w"])
         self.head_b = float(np.asarray(w["head_b"]))
+        if self.fp32_gemm == "bf16x6":
+            for L in self.layers:
+                for name in ("wqkv", "wo", "w1", "w2"):
+                    L[name + "_x6"] = _split_weight_x6(L[name])
+                for name in ("bqkv", "bo", "b1", "b2"):
+                    L[name + "_f32"] = L[name].float().contiguous()
 
     # -- validation -------------------------------------------------------
 
@@ -350,6 +401,8 @@ class CrossEncoder:
         rest of the layer for the [CLS] rows only; returns [nseq, h] (row j =
         sequence j's [CLS]).
         """
+        if self.fp32_gemm == "bf16x6":
+            return self._encode_x6(ids_dev, layout, check_finite, attn_hook, cls_only)
         cfg = self.config
         T, h, H = layout.total_tokens, cfg.embed_dim, cfg.heads
         cd = cfg.torch_dtype
@@ -404,6 +457,70 @@ class CrossEncoder:
                               _lib.ptr(bad_i), T, h, stream, exc=EncoderError)
         self._last_bad = bad if check_finite else None
         return x
+
+    def _encode_x6(self, ids_dev, layout, check_finite, attn_hook, cls_only) -> torch.Tensor:
+        """encode_packed for fp32 with the projections as split-bf16 products (fp32_gemm="bf16x6").
+        Every GEMM operand is produced as bf16 planes by the pass that writes it: sc_split_bf16x3
+        after the embedding / LayerNorms / attention, and with bias + GELU fused for the FFN
+        activation, which then never exists in fp32."""
+        cfg = self.config
+        T, h, H = layout.total_tokens, cfg.embed_dim, cfg.heads
+        dev, stream, F32 = self.device, _lib.stream_handle(), _lib.DTYPE_F32
+        pattern = make_pattern(cfg.pattern, cfg.window)
+        x = torch.empty((T, h), dtype=torch.float32, device=dev)
+        x1 = torch.empty_like(x)
+        o = torch.empty_like(x)
+        bad = torch.zeros(max(cfg.layers, 1), dtype=torch.int32, device=dev)
+        _lib.call("sc_embed", ids_dev.data_ptr(), layout.tok_pos.data_ptr(), self.tok_emb.data_ptr(),
+                  self.pos_emb.data_ptr(), x.data_ptr(), None, T, h, stream, exc=EncoderError)
+        last = cfg.layers - 1
+        for i, L in enumerate(self.layers):
+            xs = split_planes(x)
+            if cls_only and i == last:
+                self._last_bad = bad if check_finite else None
+                return self._cls_last_layer_x6(L, x, xs, layout, pattern, bad if check_finite else None, i)
+            qkv = _linear_x6(xs, L["wqkv_x6"]).add_(L["bqkv_f32"])
+            if attn_hook:
+                attn_hook("start")
+            attend_packed(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], layout, pattern, H,
+                          math.sqrt(cfg.head_dim), cfg.padding, out=o, algo=self.attn_algo, check=(i == 0))
+            if attn_hook:
+                attn_hook("end")
+            y = _linear_x6(split_planes(o), L["wo_x6"])
+            _lib.call("sc_residual_layernorm_ex", x.data_ptr(), F32, y.data_ptr(), F32, L["bo_f32"].data_ptr(),
+                      L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), x1.data_ptr(), None, None, T, h, stream,
+                      exc=EncoderError)
+            f = _linear_x6(split_planes(x1), L["w1_x6"])
+            f2 = _linear_x6(split_planes(f, bias=L["b1_f32"], gelu=True), L["w2_x6"])
+            del f
+            _lib.call("sc_residual_layernorm_ex", x1.data_ptr(), F32, f2.data_ptr(), F32, L["b2_f32"].data_ptr(),
+                      L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(), x.data_ptr(), None,
+                      _lib.ptr(bad[i:i + 1]) if check_finite else None, T, h, stream, exc=EncoderError)
+        self._last_bad = bad if check_finite else None
+        return x
+
+    def _cls_last_layer_x6(self, L, x, xs, layout, pattern, bad, i):
+        """_cls_last_layer for fp32_gemm="bf16x6": K/V of every token, the rest on the [CLS] rows."""
+        cfg = self.config
+        h, H, F32, stream = cfg.embed_dim, cfg.heads, _lib.DTYPE_F32, _lib.stream_handle()
+        qkv = _linear_x6(xs, L["wqkv_x6"]).add_(L["bqkv_f32"])
+        o = torch.empty((layout.total_tokens, h), dtype=torch.float32, device=self.device)
+        attend_packed(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], layout, pattern, H,
+                      math.sqrt(cfg.head_dim), cfg.padding, out=o, algo=self.attn_algo, check=False, rows="head")
+        cls, n = layout.cls_rows, layout.nseq
+        y = _linear_x6(split_planes(o.index_select(0, cls)), L["wo_x6"])
+        xc = x.index_select(0, cls)
+        x1 = torch.empty_like(xc)
+        _lib.call("sc_residual_layernorm_ex", xc.data_ptr(), F32, y.data_ptr(), F32, L["bo_f32"].data_ptr(),
+                  L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), x1.data_ptr(), None, None, n, h, stream,
+                  exc=EncoderError)
+        f = _linear_x6(split_planes(x1), L["w1_x6"])
+        f2 = _linear_x6(split_planes(f, bias=L["b1_f32"], gelu=True), L["w2_x6"])
+        out = torch.empty((n, h), dtype=torch.float32, device=self.device)
+        _lib.call("sc_residual_layernorm_ex", x1.data_ptr(), F32, f2.data_ptr(), F32, L["b2_f32"].data_ptr(),
+                  L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(), out.data_ptr(), None,
+                  None if bad is None else bad.data_ptr() + 4 * i, n, h, stream, exc=EncoderError)
+        return out
 
     def _proj_ln(self, a, L, wname, bname, lnname, resid, out, out32, bad, rows, stream) -> bool:
         """Opt-in (fused_ln): LN(resid + a W^T + b) as one cluster-of-3 tcgen05 GEMM
@@ -593,6 +710,12 @@ class GraphedScorer:
     def __call__(self, ids) -> torch.Tensor:
         """Scores (nseq,) on the device for new ids of the captured shape (numpy or tensor, int32)."""
         src = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)) if isinstance(ids, np.ndarray) else ids
+        if tuple(src.shape) != tuple(self.ids.shape):
+            raise EncoderError(f"ids shape {tuple(src.shape)} does not match the captured batch {tuple(self.ids.shape)}")
+        if src.device.type == "cpu" and src.numel():  # sc_embed reads tok_emb[id] unchecked (_check_ids rule);
+            lo, hi = int(src.min()), int(src.max())  # device-resident ids are the caller's (checked) buffers
+            if lo < 0 or hi >= self.model.config.vocab_size:
+                raise EncoderError("token id outside vocabulary")
         self.ids.copy_(src, non_blocking=True)
         self.graph.replay()
         return self.scores

@@ -166,20 +166,31 @@ def pack_pairs(query_ids, candidate_ids, max_positions: int | None = None) -> Pa
     return PackedBatch(ids, seq, np.full(len(docs), m + 1, dtype=np.int64))
 
 
-def score_candidates(model: CrossEncoder, query_ids, candidate_ids, max_tokens: int = 1 << 18,
-                     as_tensor: bool = False):
-    """fp32 scores of every (query, candidate) pair, packed varlen on the GPU.
+def _launch_candidates(model: CrossEncoder, query_ids, candidate_ids, max_tokens: int):
+    """Launch the packed chunks of one query's candidates back to back (no host sync: the next
+    chunk is packed on the host while the GPU runs).  Returns (device scores, [(candidate indices, bad)]),
+    ``bad`` being each chunk's per-layer non-finite counts (encode_packed's fused check)."""
+    maxpos, vocab = model.config.max_positions, model.config.vocab_size
+    q = np.asarray(query_ids).reshape(-1)
+    m = len(q)
+    ninf = torch.full((len(candidate_ids),), -math.inf, dtype=torch.float32, device=model.device)
+    if m < 1 or m + 3 > maxpos or q.min() < 0 or q.max() >= vocab:
+        return ninf, []  # assemble_input / _check_ids raise for every pair: the reference scores -inf
+    keep = maxpos - m - 3
 
-    Chunks of <= max_tokens tokens are launched back to back without a host
-    sync (the next chunk is packed on the host while the GPU runs).  With
-    ``as_tensor`` the device tensor is returned (no D2H copy)."""
-    maxpos = model.config.max_positions
-    m = len(np.asarray(query_ids).reshape(-1))
-    if m < 1 or m + 3 > maxpos:  # assemble_input raises for every pair: the reference scores -inf
-        if as_tensor:
-            return torch.full((len(candidate_ids),), -math.inf, dtype=torch.float32, device=model.device)
-        return np.full(len(candidate_ids), -np.inf, dtype=np.float32)
-    got, lo = [], 0
+    def in_vocab(d):  # _check_ids after assemble_input's truncation (R/encoder.py:154-177, :475-487)
+        d = np.asarray(d).reshape(-1)[:keep]
+        return d.size == 0 or (d.min() >= 0 and d.max() < vocab)
+
+    ok = [j for j, d in enumerate(candidate_ids) if in_vocab(d)]
+    if len(ok) < len(candidate_ids):  # score the rest; their slots stay -inf
+        if not ok:
+            return ninf, []
+        vals, chunks = _launch_candidates(model, query_ids, [candidate_ids[j] for j in ok], max_tokens)
+        idx = torch.tensor(ok, dtype=torch.int64, device=model.device)
+        ninf.index_copy_(0, idx, vals)
+        return ninf, [([ok[j] for j in js], bad) for js, bad in chunks]
+    got, chunks, lo = [], [], 0
     lens = [min(len(d) + m + 3, maxpos) for d in candidate_ids]
     while lo < len(candidate_ids):
         hi, tok = lo, 0
@@ -187,13 +198,38 @@ def score_candidates(model: CrossEncoder, query_ids, candidate_ids, max_tokens: 
             tok += lens[hi]
             hi += 1
         got.append(model.score_packed(pack_pairs(query_ids, candidate_ids[lo:hi], maxpos)))
+        chunks.append((list(range(lo, hi)), model._last_bad))
         lo = hi
-    vals = torch.cat(got)
-    if as_tensor:
-        return vals
-    out = vals.cpu().numpy()
-    model._raise_if_nonfinite()
-    return out
+    return torch.cat(got), chunks
+
+
+def _rescore_nonfinite(model: CrossEncoder, pending) -> None:
+    """The reference's per-pair error rule (R/evaluation.py:194-197 over R/encoder.py:356-357): a
+    pair whose activations turn non-finite raises in ``score_pair`` and scores -inf.  ``pending`` =
+    [(vals, query_ids, candidate_ids, chunks)]; one host sync reads every chunk's flag, and only
+    the pairs of a flagged chunk are scored again one by one (in place in ``vals``)."""
+    flagged = [(v, q, c, js, bad) for v, q, c, chunks in pending for js, bad in chunks if bad is not None]
+    if not flagged:
+        return
+    counts = torch.stack([bad.sum() for *_, bad in flagged]).cpu().numpy()
+    maxpos = model.config.max_positions
+    for (vals, q, cands, js, _bad), n in zip(flagged, counts):
+        if n == 0:
+            continue
+        for j in js:
+            sc = model.score_packed(pack_pairs(q, [cands[j]], maxpos))
+            ok = int(model._last_bad.sum()) == 0 and bool(torch.isfinite(sc).all())
+            vals[j] = sc[0] if ok else -math.inf
+
+
+def score_candidates(model: CrossEncoder, query_ids, candidate_ids, max_tokens: int = 1 << 18,
+                     as_tensor: bool = False):
+    """fp32 scores of every (query, candidate) pair, packed varlen on the GPU; a pair the reference
+    could not score (query too long, non-finite activations) gets -inf, as R/evaluation.py:194-197.
+    With ``as_tensor`` the device tensor is returned (no D2H copy of the scores)."""
+    vals, chunks = _launch_candidates(model, query_ids, candidate_ids, max_tokens)
+    _rescore_nonfinite(model, [(vals, query_ids, candidate_ids, chunks)])
+    return vals if as_tensor else vals.cpu().numpy()
 
 
 def shard_range(n: int, world: int, rank: int) -> tuple:
@@ -218,7 +254,8 @@ def gather_scores(local: torch.Tensor, counts, group=None) -> torch.Tensor:
 
 def rerank_distributed(model: CrossEncoder | None, queries, top_k: int = 100, tag: str = "sparsecross",
                        rank: int = 0, world: int = 1, group=None, score_fn=None) -> list | None:
-    """Re-rank ``queries`` = [(qid, query_ids, [(doc_id, doc_ids), ...]), ...] over `world` ranks.
+    """Re-rank ``queries`` = [(qid, query_ids, [(doc_id, doc_ids), ...][, top_k]), ...] over `world`
+    ranks (a 4th element overrides ``top_k`` for that query).
 
     Each rank scores a contiguous block of queries; scores are gathered with
     one all-gather; rank 0 returns the ranked run entries (others return None).
@@ -229,7 +266,12 @@ def rerank_distributed(model: CrossEncoder | None, queries, top_k: int = 100, ta
     if score_fn is None:
         # GPU path: every query's chunks are launched back to back (host packing of the
         # next chunk overlaps the GPU); scores stay on the device until the gather
-        parts = [score_candidates(model, q[1], [c[1] for c in q[2]], as_tensor=True) for q in queries[lo:hi]]
+        pending = []
+        for q in queries[lo:hi]:
+            cands = [c[1] for c in q[2]]
+            pending.append((*_launch_candidates(model, q[1], cands, 1 << 18), q[1], cands))
+        _rescore_nonfinite(model, [(v, qi, c, ch) for v, ch, qi, c in pending])
+        parts = [p[0] for p in pending]
         flat_t = torch.cat(parts) if parts else torch.zeros(0, dtype=torch.float32, device=model.device)
     else:
         local = [np.asarray(score_fn(q[1], [c[1] for c in q[2]]), np.float32) for q in queries[lo:hi]]
@@ -242,15 +284,13 @@ def rerank_distributed(model: CrossEncoder | None, queries, top_k: int = 100, ta
         allv = gather_scores(flat_t.to(dev), counts, group).cpu().numpy()
     else:
         allv = flat_t.cpu().numpy()
-    if model is not None and score_fn is None:
-        model._raise_if_nonfinite()
     if rank != 0:
         return None
     entries, off = [], 0
-    for qid, _q, cands in queries:
+    for qid, _q, cands, *k in queries:
         sc = allv[off: off + len(cands)]
         off += len(cands)
-        entries += rank_entries(qid, [c[0] for c in cands], sc, top_k, tag)
+        entries += rank_entries(qid, [c[0] for c in cands], sc, k[0] if k else top_k, tag)
     return entries
 
 

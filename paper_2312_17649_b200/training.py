@@ -890,10 +890,19 @@ class GraphedTrainStep:
     def __call__(self, ids, teacher_gap=None) -> torch.Tensor:
         """One step on new ids of the captured shape; returns the loss (device scalar, float64)."""
         src = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int32)) if isinstance(ids, np.ndarray) else ids
+        if tuple(src.shape) != tuple(self.ids.shape):
+            raise EncoderError(f"ids shape {tuple(src.shape)} does not match the captured layout "
+                               f"{tuple(self.ids.shape)}")
+        if src.numel():  # sc_embed reads tok_emb[id] unchecked: the reference's _check_ids range rule
+            lo, hi = int(src.min()), int(src.max())
+            if lo < 0 or hi >= self.model.config.vocab_size:
+                raise EncoderError("token id outside vocabulary")
         self.ids.copy_(src, non_blocking=True)
         if teacher_gap is not None:
             self.teacher_gap.copy_(torch.as_tensor(teacher_gap, dtype=torch.float64), non_blocking=True)
         self.graph.replay()
+        if not math.isfinite(float(self.loss_value)):  # as train_step: never feed NaN gradients to AdamW
+            raise TrainingDivergedError(self.opt.step_count + 1)
         W = self.model.weights
         grads, off = GradDict(self.grad_flat), 0
         for n in self.names:  # == ParamDict.order (sorted names)

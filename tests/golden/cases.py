@@ -139,3 +139,34 @@ def adamw_inputs():
     gs = [{n: rng.standard_normal(np.shape(a)) * (0.0 if step == 2 and n == "b" else 1.0)
            for n, a in ws.items()} for step in range(5)]
     return ws, gs
+
+
+# ---- headline ranking + re-rank driver fixtures (round 2) -------------------
+
+# 1 query x RANK_DOCS candidates at s=4099 (q10 + d4086): the C3/C5 headline pairs, ids from
+# default_rng((0, 0, j)) exactly as bench.py and rerank.synthetic_queries draw them.
+RANK_DOCS = 32
+
+# Re-rank driver (R/evaluation.py:176-205 driven like R/cli.py:224-238) at ELECTRA-base dims,
+# max_positions 512: (query length, #candidates, top_k).  Query 3 is too long for max_positions
+# (assemble_input raises -> every pair scores -inf in the reference).
+RERANK_QUERIES = [(10, 20, 100), (31, 24, 15), (4, 20, 100), (520, 5, 100)]
+
+
+def rerank_workload(vocab, maxpos=512):
+    """[(qid, query_ids, [(doc_id, doc_ids), ...], top_k)]: mixed doc lengths 0..700 (those above
+    maxpos - m - 3 are truncated by assemble_input), one empty document and, in query 0, a
+    duplicate of candidate 3 at position 7 (a score tie that the stable sort must keep in
+    candidate order)."""
+    out = []
+    for q, (qlen, ncand, top_k) in enumerate(RERANK_QUERIES):
+        rng = np.random.default_rng((7, q))
+        qids = rng.integers(3, vocab, size=qlen)
+        lens = rng.integers(0, 700, size=ncand)
+        lens[min(2, ncand - 1)] = 0
+        cands = [(f"d{q}_{j}", np.random.default_rng((7, q, j)).integers(3, vocab, size=int(n)))
+                 for j, n in enumerate(lens)]
+        if q == 0:
+            cands[7] = ("d0_7", cands[3][1].copy())
+        out.append((f"q{q}", qids, cands, top_k))
+    return out

@@ -125,6 +125,49 @@ def gen_encoders(skip_long):
     np.savez_compressed(os.path.join(HERE, "encoder.npz"), **out)
 
 
+def gen_ranking():
+    """1 query x RANK_DOCS candidates at s=4099, f32 reference scores (ranking.npz).  Candidates 0
+    and 1 are encoder.npz's electra_doc_scores pairs (the bench's first two pairs)."""
+    cfg = E.EncoderConfig(**cases.ELECTRA_DOC, precision="f32")
+    model = E.CrossEncoder(cfg, seed=0)
+    seqs = [rerank_ids(0, 0, j, 10, 4086, cfg.vocab_size, cfg.max_positions) for j in range(cases.RANK_DOCS)]
+    ids = np.stack([s.ids for s in seqs])
+    scores = []
+    for i in range(0, len(seqs), 4):
+        t0 = time.time()
+        scores.append(model.score(ids[i:i + 4], seqs[0].partition))
+        print(f"  ranking docs {i}..{i + 3}: {time.time() - t0:.1f}s", flush=True)
+    scores = np.concatenate(scores)
+    from sparsecross import evaluation as EV
+    order = [int(e.doc_id[1:]) for e in EV.rerank(lambda _q, j: scores[j], None,
+                                                   [(f"d{j}", j) for j in range(len(scores))])]
+    np.savez_compressed(os.path.join(HERE, "ranking.npz"), scores=scores, order=np.array(order))
+
+
+def gen_rerank():
+    """The reference's own re-rank driver (R/evaluation.py:176-205 with R/encoder.py:535-538 as the
+    scorer, driven per query like R/cli.py:224-238) over cases.rerank_workload: TREC run + scores."""
+    from sparsecross import evaluation as EV
+
+    cfg = E.EncoderConfig(**cases.ELECTRA_PASSAGE, precision="f32")
+    model = E.CrossEncoder(cfg, seed=0)
+    entries, raw = [], []
+    for qid, qids, cands, top_k in cases.rerank_workload(cfg.vocab_size, cfg.max_positions):
+        t0 = time.time()
+        got = []
+
+        def scorer(query, doc):
+            got.append(-np.inf)  # replaced below unless score_pair raises (the reference's -inf)
+            got[-1] = model.score_pair(query, doc)
+            return got[-1]
+
+        entries += EV.rerank(scorer, qids, cands, top_k=top_k, query_id=qid)
+        raw += got
+        print(f"  rerank {qid}: {time.time() - t0:.1f}s", flush=True)
+    run = EV.format_run(entries)
+    np.savez_compressed(os.path.join(HERE, "rerank.npz"), run=np.array(run), scores=np.array(raw, np.float64))
+
+
 def gen_serialize():
     """Model directories written by the reference's save_model (R/serialize.py:50-76)."""
     import math as _m
@@ -233,7 +276,7 @@ def main():
     args = ap.parse_args()
     steps = {"band": gen_band, "masks": gen_masks, "attention": gen_attention,
              "encoder": lambda: gen_encoders(args.skip_long), "serialize": gen_serialize,
-             "training": gen_training}
+             "training": gen_training, "ranking": gen_ranking, "rerank": gen_rerank}
     for name, fn in steps.items():
         if args.only and name not in args.only.split(","):
             continue

@@ -209,3 +209,15 @@ def test_fused_layernorm_projection_matches(P):
     batch = P.PackedBatch.from_sequences(seqs)
     np.testing.assert_allclose(fused.score_packed(batch).cpu().numpy(), base.score_packed(batch).cpu().numpy(),
                                atol=2e-2, rtol=0)
+
+
+def test_electra_passages_fp32_bf16x6_ranking_identical(P, g):
+    cfg = P.EncoderConfig(**cases.ELECTRA_PASSAGE, precision="f32")
+    model = P.CrossEncoder(cfg, seed=0, fp32_gemm="bf16x6")
+    seqs = [rerank_ids(0, j, 164, cfg.vocab_size, cfg.max_positions, P) for j in range(100)]
+    sc = model.score_packed(P.PackedBatch.from_sequences(seqs)).cpu().numpy()
+    ref = g["electra_passage_scores"]
+    err = np.abs(sc - ref).max()
+    print(f"fp32 bf16x6 passages max |dscore| = {err:.3e}")
+    assert err < 2e-6, err
+    assert O.rank_order(sc) == O.rank_order(ref)

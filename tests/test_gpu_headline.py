@@ -1,0 +1,125 @@
+"""The headline configuration pinned end to end against the unmodified reference.
+
+BASELINE configs[2] / SURVEY §8 C3: ELECTRA-base dims, sparse w=4, documents of
+q10 + d4086 = s 4099.  Goldens (``tests/golden/ranking.npz``, ``encoder.npz``)
+come from the reference's own ``CrossEncoder.score`` in f32
+(R/encoder.py:502-509) over the same seeded ids the bench uses (pairs (q0, d_j)
+from ``default_rng((0, 0, j))``); the ranking rule is R/evaluation.py:194-201.
+
+* bf16 (the bench's dtype): every score within 2e-2; a ranking flip only
+  between candidates whose reference gap is within 2 x tolerance.
+* fp32: scores within 1e-4 and the per-query ranking identical.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+from oracle import sparsecross_oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+BF16_TOL = 2e-2
+F32_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2312_17649_b200 as pkg
+
+    return pkg
+
+
+@pytest.fixture(scope="module")
+def ranking():
+    return np.load(os.path.join(GOLD, "ranking.npz"))
+
+
+@pytest.fixture(scope="module")
+def enc():
+    return np.load(os.path.join(GOLD, "encoder.npz"))
+
+
+def doc_batch(P, n, cfg):
+    seqs = []
+    for j in range(n):
+        q = np.random.default_rng((0, 0)).integers(3, cfg.vocab_size, size=10)
+        d = np.random.default_rng((0, 0, j)).integers(3, cfg.vocab_size, size=4086)
+        seqs.append(P.assemble_input(q, d, cfg.max_positions))
+    return P.PackedBatch.from_sequences(seqs)
+
+
+def scores_for(P, precision, n, **kw):
+    cfg = P.EncoderConfig(**cases.ELECTRA_DOC, precision=precision)
+    model = P.CrossEncoder(cfg, seed=0, **kw)
+    sc = model.score_packed(doc_batch(P, n, cfg)).cpu().numpy()
+    model._raise_if_nonfinite()
+    return sc
+
+
+def assert_flip_rule(ref, got, tol):
+    """Flips only between candidates whose reference gap is within 2 x tol."""
+    ro = O.rank_order(ref)
+    pos = {c: i for i, c in enumerate(O.rank_order(got))}
+    bad = [(ro[a], ro[b]) for a in range(len(ro)) for b in range(a + 1, len(ro))
+           if pos[ro[a]] > pos[ro[b]] and abs(ref[ro[a]] - ref[ro[b]]) > 2 * tol]
+    assert not bad, f"rank flips beyond 2 x tolerance: {bad[:5]}"
+
+
+def test_golden_consistency(ranking, enc):
+    """ranking.npz candidates 0 and 1 are encoder.npz's electra_doc_scores pairs (same reference run
+    inputs) -- both fixtures were produced by the reference from the same seeds."""
+    np.testing.assert_allclose(ranking["scores"][:2], enc["electra_doc_scores"], rtol=0, atol=1e-6)
+    assert list(ranking["order"]) == O.rank_order(ranking["scores"])
+
+
+def test_bf16_headline_pairs_match_reference(P, enc):
+    """The bench's own first two pairs (bf16, s=4099, 12 layers) vs the reference's f32 scores."""
+    sc = scores_for(P, "bf16", 2)
+    err = np.abs(sc - enc["electra_doc_scores"]).max()
+    print(f"bf16 s=4099 max |dscore| = {err:.3e}")
+    assert err < BF16_TOL, err
+
+
+@pytest.mark.parametrize("prune", [False, True])
+def test_bf16_headline_32_candidates(P, ranking, prune):
+    ref = ranking["scores"]
+    sc = scores_for(P, "bf16", len(ref), prune_last_layer=prune)
+    err = np.abs(sc - ref).max()
+    print(f"bf16 s=4099 x{len(ref)} max |dscore| = {err:.3e}; ranking identical: "
+          f"{O.rank_order(sc) == O.rank_order(ref)}")
+    assert err < BF16_TOL, err
+    assert_flip_rule(ref, sc, BF16_TOL)
+
+
+def test_fp32_headline_32_candidates_ranking_identical(P, ranking):
+    ref = ranking["scores"]
+    sc = scores_for(P, "f32", len(ref))
+    err = np.abs(sc - ref).max()
+    print(f"fp32 s=4099 x{len(ref)} max |dscore| = {err:.3e}")
+    assert err < F32_TOL, err
+    assert O.rank_order(sc) == list(ranking["order"])
+
+
+
+def test_fp32_bf16x6_headline_32_candidates(P, ranking):
+    """The fast fp32 mode (projections as six split-bf16 tensor-core products) against the
+    reference: SGEMM-level score error and the identical ranking (adjacent reference gaps here
+    are as small as 6e-6)."""
+    ref = ranking["scores"]
+    sc = scores_for(P, "f32", len(ref), fp32_gemm="bf16x6")
+    err = np.abs(sc - ref).max()
+    print(f"fp32 bf16x6 s=4099 x{len(ref)} max |dscore| = {err:.3e}")
+    assert err < 2e-6, err
+    assert O.rank_order(sc) == list(ranking["order"])
+
+
+def test_fp32_bf16x6_prune_matches_full(P, ranking):
+    ref = ranking["scores"][:4]
+    a = scores_for(P, "f32", 4, fp32_gemm="bf16x6")
+    b = scores_for(P, "f32", 4, fp32_gemm="bf16x6", prune_last_layer=True)
+    np.testing.assert_allclose(b, a, atol=1e-6, rtol=0)
+    np.testing.assert_allclose(b, ref, atol=2e-6, rtol=0)

@@ -222,3 +222,47 @@ def test_gemm_bias_gelu_pre_dual_output():
     pre = a.float() @ w.float().t() + b
     torch.testing.assert_close(f.float(), pre, rtol=2e-2, atol=2e-2)
     torch.testing.assert_close(g.float(), torch.nn.functional.gelu(pre), rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("bias,gelu", [(False, False), (True, False), (True, True)])
+@pytest.mark.parametrize("cols", [768, 3072, 13])
+def test_split_bf16x3_planes(bias, gelu, cols):
+    """sc_split_bf16x3: p0 + p1 + p2 reproduces v = gelu?(x + bias) to 2^-24 relative, each plane the
+    round-to-nearest bf16 of the remaining residual; the fp32 copy matches an fp64 GELU."""
+    from paper_2312_17649_b200.encoder import split_planes
+
+    g = torch.Generator(device="cuda").manual_seed(cols)
+    x = torch.randn((257, cols), device="cuda", generator=g) * 3
+    b = torch.randn(cols, device="cuda", generator=g) if bias else None
+    keep = torch.empty_like(x)
+    pl = split_planes(x, bias=b, gelu=gelu, keep=keep)
+    v = x.double() + (b.double() if bias else 0)
+    if gelu:
+        v = 0.5 * v * (1 + torch.special.erf(v / math.sqrt(2)))
+    p0, p1, p2 = pl[:, :cols].double(), pl[:, cols:2 * cols].double(), pl[:, 2 * cols:].double()
+    assert torch.equal(pl[:, :cols], keep.to(torch.bfloat16))
+    assert torch.equal(pl[:, cols:2 * cols], (keep - pl[:, :cols].float()).to(torch.bfloat16))
+    rel = ((p0 + p1 + p2 - keep.double()).abs() / keep.double().abs().clamp_min(1e-30)).max().item()
+    assert rel <= 2.0 ** -24, rel
+    assert (keep.double() - v).abs().max().item() < 1e-5
+
+
+def test_linear_x6_matches_fp64():
+    """_linear_x6 (three bf16 GEMMs summing six split products) is as accurate as fp32 SGEMM."""
+    from paper_2312_17649_b200.encoder import _linear_x6, _split_weight_x6, split_planes
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn((1000, 3072), device="cuda", generator=g)
+    w = torch.randn((768, 3072), device="cuda", generator=g) / 55
+    exact = a.double() @ w.double().t()
+    got = _linear_x6(split_planes(a), _split_weight_x6(w))
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        sg = a @ w.t()
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    e6 = (got.double() - exact).abs().max().item()
+    es = (sg.double() - exact).abs().max().item()
+    print(f"x6 max err {e6:.3e}, sgemm {es:.3e}")
+    assert e6 <= 2 * es + 1e-7, (e6, es)

@@ -261,3 +261,23 @@ class TestBenchHarness:
             emit_report([rec()], "md", baseline=("full", 3))
         with pytest.raises(BenchConfigError):
             emit_report([rec()], "html")
+
+
+def test_bench_batch_prefix_is_the_ranking_golden():
+    """bench.py's synthetic batch starts with exactly these candidates (its parity field relies on it)."""
+    import bench
+    import paper_2312_17649_b200 as P
+
+    def doc_batch(n, cfg):
+        seqs = []
+        for j in range(n):
+            q = np.random.default_rng((0, 0)).integers(3, cfg.vocab_size, size=10)
+            d = np.random.default_rng((0, 0, j)).integers(3, cfg.vocab_size, size=4086)
+            seqs.append(P.assemble_input(q, d, cfg.max_positions))
+        return P.PackedBatch.from_sequences(seqs)
+
+
+    cfg = dict(bench.ELECTRA, max_positions=4099)
+    batch = bench.make_batch(P, cfg, 4086, 4, 0)
+    want = doc_batch(4, P.EncoderConfig(**cases.ELECTRA_DOC, precision="bf16"))
+    assert np.array_equal(batch.ids, want.ids)
