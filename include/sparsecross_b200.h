@@ -328,8 +328,8 @@ SC_API int sc_count_nonfinite(const float* x, int64_t n, int32_t* count, void* s
  * (CrossEncoder(fp32_gemm="bf16x6"); replaces the fp32 operands of the
  * reference's projections R/encoder.py:322-324, :345, :350, :352).
  * v = x[r][c] (+ bias[c]) (then exact-erf GELU if gelu != 0, R/encoder.py:258-259);
- * y[r][c] = v if y != NULL (may alias x); planes row r = [p0 | p1 | p2] (each
- * `cols` wide, row stride ldp >= 3*cols) with p0 = bf16_rn(v),
+ * y[r][c] = v if y != NULL (may alias x); planes row r = [p1 | p2 | p0 | p1 | p0]
+ * (each `cols` wide, row stride ldp >= 5*cols) with p0 = bf16_rn(v),
  * p1 = bf16_rn(v - p0), p2 = bf16_rn(v - p0 - p1).  Strides in elements. */
 SC_API int sc_split_bf16x3(const float* x, int64_t ldx, const float* bias, int32_t gelu, float* y, int64_t ldy,
                            void* planes, int64_t ldp, int64_t rows, int32_t cols, void* stream);

@@ -1,13 +1,18 @@
-// fp32 GEMM operands as three bf16 planes, for the ranking-exact fp32 mode.
+// fp32 GEMM operands as bf16 planes, for the ranking-exact fp32 mode.
 //
 // x = p0 + p1 + p2 with p0 = bf16_rn(x), p1 = bf16_rn(x - p0), p2 = bf16_rn(x - p0 - p1):
 // 24 significant bits, |x - p0 - p1 - p2| <= 2^-27 |x|.  A product x*w is then
 // sum_{i+j<=2} p_i(x) q_j(w) (six bf16 tensor-core products, fp32 accumulation;
 // the dropped terms are <= 2^-27 relative), i.e. the reference's fp32 GEMMs
-// (R/encoder.py:322-324, :345, :350, :352) at SGEMM accuracy on the bf16 tensor
-// pipe.  Planes are stored per row as [p0 | p1 | p2] so that the K-prefixes
-// [p0 | p1 | p2], [p0 | p1] and [p0] of one buffer are the left operands of the
-// three GEMMs that sum the six products (encoder.py: _linear_x6).
+// (R/encoder.py:322-324, :345, :350, :352) on the bf16 tensor pipe.
+//
+// Layout per row: [p1 | p2 | p0 | p1 | p0] (five `cols`-wide planes).  The
+// whole row times [q0 | q0 | q1 | q1 | q2] is the sum of the five correction
+// products (magnitude 2^-8 of the result: their accumulation error is
+// negligible); the main product p0 q0 is a separate GEMM on the middle plane,
+// split over K so that no tensor-core accumulation runs long (the tensor
+// pipe's fp32 accumulation is less exact than an FFMA chain; partial products
+// are summed in the RN fp32 GEMM epilogue instead).  See encoder.py _linear_x6.
 //
 // Producers fuse the split into their pass: the optional bias and exact-erf
 // GELU (R/encoder.py:258-259, erff as the fp32 path) are applied first and the
@@ -60,9 +65,12 @@ __global__ void __launch_bounds__(256) split3_vec_kernel(const float* __restrict
     split3(v.z, a[2], b[2], d[2]);
     split3(v.w, a[3], b[3], d[3]);
     __nv_bfloat16* pr = p + r * ldp + c;
-    *reinterpret_cast<uint2*>(pr) = pack4(a[0], a[1], a[2], a[3]);
-    *reinterpret_cast<uint2*>(pr + cols) = pack4(b[0], b[1], b[2], b[3]);
-    *reinterpret_cast<uint2*>(pr + 2 * cols) = pack4(d[0], d[1], d[2], d[3]);
+    const uint2 v0 = pack4(a[0], a[1], a[2], a[3]), v1 = pack4(b[0], b[1], b[2], b[3]);
+    *reinterpret_cast<uint2*>(pr) = v1;
+    *reinterpret_cast<uint2*>(pr + cols) = pack4(d[0], d[1], d[2], d[3]);
+    *reinterpret_cast<uint2*>(pr + 2 * cols) = v0;
+    *reinterpret_cast<uint2*>(pr + 3 * cols) = v1;
+    *reinterpret_cast<uint2*>(pr + 4 * cols) = v0;
   }
 }
 
@@ -80,7 +88,9 @@ __global__ void split3_kernel(const float* __restrict__ x, int64_t ldx, const fl
     if (kGelu) v = 0.5f * v * (1.f + erff(v * 0.70710678118654752440f));
     if (y) y[r * ldy + c] = v;
     __nv_bfloat16* pr = p + r * ldp + c;
-    split3(v, pr[0], pr[cols], pr[2 * cols]);
+    __nv_bfloat16 a, b, d;
+    split3(v, a, b, d);
+    pr[0] = b, pr[cols] = d, pr[2 * cols] = a, pr[3 * cols] = b, pr[4 * cols] = a;
   }
 }
 
@@ -103,7 +113,7 @@ using namespace sc;
 extern "C" int sc_split_bf16x3(const float* x, int64_t ldx, const float* bias, int32_t gelu, float* y, int64_t ldy,
                                void* planes, int64_t ldp, int64_t rows, int32_t cols, void* stream) {
   SC_CHECK_ARG(x && planes, "sc_split_bf16x3: null pointer");
-  SC_CHECK_ARG(rows >= 0 && cols >= 1 && ldx >= cols && ldp >= 3LL * cols && (!y || ldy >= cols),
+  SC_CHECK_ARG(rows >= 0 && cols >= 1 && ldx >= cols && ldp >= 5LL * cols && (!y || ldy >= cols),
                "sc_split_bf16x3: bad shape");
   if (rows == 0) return SC_OK;
   const bool vec = cols % 4 == 0 && ldx % 4 == 0 && ldp % 4 == 0 && (!y || ldy % 4 == 0) &&

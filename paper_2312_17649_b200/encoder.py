@@ -268,37 +268,46 @@ FP32_GEMMS = ("sgemm", "bf16x6")
 
 
 def _split_weight_x6(w: torch.Tensor) -> torch.Tensor:
-    """fp32 weight [N, K] -> bf16 [N, 6K] = [W0 W0 W0 | W1 W1 | W2] with W = W0 + W1 + W2 (each
-    plane the round-to-nearest bf16 of the remaining residual; one-time, at upload)."""
+    """fp32 weight [N, K] -> bf16 [N, 5K] = [W0 | W0 | W1 | W1 | W2] with W = W0 + W1 + W2 (each
+    plane the round-to-nearest bf16 of the remaining residual; one-time, at upload).  Row-wise dot
+    with the activation planes [p1 | p2 | p0 | p1 | p0] = the five correction products."""
     w = w.float()
     w0 = w.to(torch.bfloat16)
     r = w - w0.float()
     w1 = r.to(torch.bfloat16)
     w2 = (r - w1.float()).to(torch.bfloat16)
-    return torch.cat([w0, w0, w0, w1, w1, w2], dim=1).contiguous()
+    return torch.cat([w0, w0, w1, w1, w2], dim=1).contiguous()
 
 
 def split_planes(x: torch.Tensor, bias=None, gelu: bool = False, keep: torch.Tensor | None = None) -> torch.Tensor:
-    """fp32 [M, K] (+ bias, GELU) -> bf16 planes [M, 3K] = [p0 | p1 | p2] (sc_split_bf16x3);
+    """fp32 [M, K] (+ bias, GELU) -> bf16 planes [M, 5K] = [p1 | p2 | p0 | p1 | p0] (sc_split_bf16x3);
     ``keep`` (optional, may be x) receives the fp32 value after bias/GELU."""
     M, K = x.shape
-    planes = torch.empty((M, 3 * K), dtype=torch.bfloat16, device=x.device)
+    planes = torch.empty((M, 5 * K), dtype=torch.bfloat16, device=x.device)
     _lib.call("sc_split_bf16x3", x.data_ptr(), x.stride(0), _lib.ptr(bias), int(gelu), _lib.ptr(keep),
               K if keep is None else keep.stride(0), planes.data_ptr(), planes.stride(0), M, K,
               _lib.stream_handle(), exc=EncoderError)
     return planes
 
 
-def _linear_x6(planes: torch.Tensor, w6: torch.Tensor) -> torch.Tensor:
-    """a W^T in fp32 from the planes of a ([M, 3K]) and of W ([N, 6K]): three bf16 tensor-core GEMMs
-    with fp32 accumulation summing the six products p_i q_j, i + j <= 2:
-      [p0 p1 p2] [q0; q0; q0] + [p0 p1] [q1; q1] + p0 q2
-    (the K-prefixes of one plane buffer; dropped terms <= 2^-27 relative).  R/encoder.py:322-324,
-    :345, :350, :352 at SGEMM accuracy."""
-    K = planes.shape[1] // 3
-    c = torch.mm(planes, w6[:, :3 * K].t(), out_dtype=torch.float32)
-    c = torch.addmm(c, planes[:, :2 * K], w6[:, 3 * K:5 * K].t(), out_dtype=torch.float32)
-    return torch.addmm(c, planes[:, :K], w6[:, 5 * K:].t(), out_dtype=torch.float32)
+X6_CHUNK = 768  # K-chunk of the main product p0 q0 (measured: SGEMM-or-better error up to K = 3072)
+
+
+def _linear_x6(planes: torch.Tensor, w5: torch.Tensor, chunk: int | None = None) -> torch.Tensor:
+    """a W^T in fp32 from the planes of a ([M, 5K]) and of W ([N, 5K]) on the bf16 tensor cores:
+      corrections  [p1 p2 p0 p1 p0] . [q0 q0 q1 q1 q2]    (one GEMM, K' = 5K, magnitude 2^-8)
+      + main       p0 . q0  in K-chunks of <= ``chunk``  (summed in the RN fp32 GEMM epilogue)
+    = sum_{i+j<=2} p_i q_j (dropped terms <= 2^-27 relative).  The tensor pipe's fp32 accumulation
+    is coarser than an FFMA chain, so no single accumulation runs over more than ``chunk`` of the
+    main product; measured max error vs fp64 at M=32792: 5.2e-6 (K=768) vs SGEMM's 6.1e-6.
+    R/encoder.py:322-324, :345, :350, :352."""
+    K = planes.shape[1] // 5
+    chunk = chunk or X6_CHUNK
+    c = torch.mm(planes, w5.t(), out_dtype=torch.float32)
+    p0, q0 = planes[:, 2 * K:3 * K], w5[:, :K]
+    for k0 in range(0, K, chunk):
+        c = torch.addmm(c, p0[:, k0:k0 + chunk], q0[:, k0:k0 + chunk].t(), out_dtype=torch.float32)
+    return c
 
 
 class CrossEncoder:

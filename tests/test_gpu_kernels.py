@@ -227,8 +227,9 @@ def test_gemm_bias_gelu_pre_dual_output():
 @pytest.mark.parametrize("bias,gelu", [(False, False), (True, False), (True, True)])
 @pytest.mark.parametrize("cols", [768, 3072, 13])
 def test_split_bf16x3_planes(bias, gelu, cols):
-    """sc_split_bf16x3: p0 + p1 + p2 reproduces v = gelu?(x + bias) to 2^-24 relative, each plane the
-    round-to-nearest bf16 of the remaining residual; the fp32 copy matches an fp64 GELU."""
+    """sc_split_bf16x3: planes [p1 | p2 | p0 | p1 | p0]; p0 + p1 + p2 reproduces v = gelu?(x + bias) to
+    2^-24 relative, each plane the round-to-nearest bf16 of the remaining residual; the fp32 copy
+    matches an fp64 GELU."""
     from paper_2312_17649_b200.encoder import split_planes
 
     g = torch.Generator(device="cuda").manual_seed(cols)
@@ -239,16 +240,18 @@ def test_split_bf16x3_planes(bias, gelu, cols):
     v = x.double() + (b.double() if bias else 0)
     if gelu:
         v = 0.5 * v * (1 + torch.special.erf(v / math.sqrt(2)))
-    p0, p1, p2 = pl[:, :cols].double(), pl[:, cols:2 * cols].double(), pl[:, 2 * cols:].double()
-    assert torch.equal(pl[:, :cols], keep.to(torch.bfloat16))
-    assert torch.equal(pl[:, cols:2 * cols], (keep - pl[:, :cols].float()).to(torch.bfloat16))
+    p1, p2, p0 = pl[:, :cols].double(), pl[:, cols:2 * cols].double(), pl[:, 2 * cols:3 * cols].double()
+    assert torch.equal(pl[:, 2 * cols:3 * cols], keep.to(torch.bfloat16))
+    assert torch.equal(pl[:, :cols], (keep - pl[:, 2 * cols:3 * cols].float()).to(torch.bfloat16))
+    assert torch.equal(pl[:, 3 * cols:4 * cols], pl[:, :cols]) and torch.equal(pl[:, 4 * cols:], pl[:, 2 * cols:3 * cols])
     rel = ((p0 + p1 + p2 - keep.double()).abs() / keep.double().abs().clamp_min(1e-30)).max().item()
     assert rel <= 2.0 ** -24, rel
     assert (keep.double() - v).abs().max().item() < 1e-5
 
 
 def test_linear_x6_matches_fp64():
-    """_linear_x6 (three bf16 GEMMs summing six split products) is as accurate as fp32 SGEMM."""
+    """_linear_x6 (six split products on the bf16 tensor cores) is at least as accurate as fp32 SGEMM
+    (K = 768: one main accumulation; K = 3072: four chunks)."""
     from paper_2312_17649_b200.encoder import _linear_x6, _split_weight_x6, split_planes
 
     g = torch.Generator(device="cuda").manual_seed(5)
@@ -265,4 +268,4 @@ def test_linear_x6_matches_fp64():
     e6 = (got.double() - exact).abs().max().item()
     es = (sg.double() - exact).abs().max().item()
     print(f"x6 max err {e6:.3e}, sgemm {es:.3e}")
-    assert e6 <= 2 * es + 1e-7, (e6, es)
+    assert e6 <= es * 1.25, (e6, es)
