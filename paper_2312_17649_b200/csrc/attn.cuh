@@ -94,6 +94,11 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
                      const int32_t* seq_head_base, int tile_rows, int max_qgroup_len, void* ws,
                      size_t ws_bytes, cudaStream_t st, bool doc_rows = true);
 
+// merge_full_rows_kernel alone: folds the per-tile split-softmax records (band-kernel layout,
+// 64-row tiles) into the head rows with a FULL doc link (used after the tcgen05 kernel).
+int launch_head_merge(const AttnArgs& a, const int32_t* seq_tile_base, int tile_rows, int max_qgroup_len, void* ws,
+                      cudaStream_t st);
+
 // fp32 doc-band kernel for the parity path (attn_band_f32.cu); head rows are the caller's.
 // records (fneed > 0): per-tile split-softmax records of the full rows, (m, l, acc[64]) x H x fneed
 // per tile, for the generic kernel's head-row merge.
@@ -101,7 +106,7 @@ int launch_attn_band_f32(const AttnArgs& a, int dtype, const int32_t* seq_tile_b
                          int max_qgroup_len, float* records, int fneed, cudaStream_t st);
 
 // tcgen05 / TMEM kernel for wide bands and dense doc rows (attn_tc.cu).
-size_t tc_workspace_bytes(int nseq, int H, int n_global);  // n_global: QDS global doc tokens
+size_t tc_workspace_bytes(int nseq, int T, int H, int n_global);  // n_global: QDS global doc tokens
 int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
                    const int32_t* seq_head_base, int tile_rows, int max_qgroup_len, void* ws,
                    size_t ws_bytes, cudaStream_t st);

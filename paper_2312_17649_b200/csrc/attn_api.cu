@@ -11,7 +11,7 @@ extern "C" size_t sc_attn_workspace_bytes_qds(int32_t nseq, int32_t total_tokens
   if (!load_links(links, &L) || n_global_tokens < 0) return 0;
   const size_t band = band_workspace_bytes(nseq, total_tokens, heads, head_dim, tile_rows, max_qgroup_len, L);
   // the tcgen05 path uses [band records | tile prefixes | QDS compact q/k/v rows]
-  return ((band + 255) & ~size_t(255)) + tc_workspace_bytes(nseq, heads, n_global_tokens);
+  return ((band + 255) & ~size_t(255)) + tc_workspace_bytes(nseq, total_tokens, heads, n_global_tokens);
 }
 
 extern "C" size_t sc_attn_workspace_bytes(int32_t nseq, int32_t total_tokens, int32_t heads,

@@ -941,4 +941,23 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   return SC_OK;
 }
 
+int launch_head_merge(const AttnArgs& a, const int32_t* seq_tile_base, int tile_rows, int max_qgroup_len, void* ws,
+                      cudaStream_t st) {
+  using namespace bandk;
+  const Links& L = a.links;
+  const int fneed = full_rows_needed(L, max_qgroup_len);
+  if (fneed == 0) return SC_OK;
+  Params p{};
+  p.nseq = a.nseq; p.H = a.H; p.fneed = fneed; p.fmax = fneed;
+  p.cu = a.cu; p.qlen = a.qlen; p.tile_base = seq_tile_base;
+  p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
+  p.partials = static_cast<float*>(ws);
+  p.ntiles_max = (int)((a.T + tile_rows - 1) / tile_rows + a.nseq);
+  for (int gsrc = 0; gsrc < 2; ++gsrc) p.hdoc[gsrc] = L.w[gsrc][2] == SC_LINK_FULL;
+  const int64_t items = (int64_t)a.nseq * a.H * fneed;
+  merge_full_rows_kernel<<<(unsigned)((items + MERGE_WARPS - 1) / MERGE_WARPS), MERGE_WARPS * 32, 0, st>>>(p);
+  SC_CHECK_LAUNCH("merge_full_rows_kernel");
+  return SC_OK;
+}
+
 }  // namespace sc

@@ -8,13 +8,26 @@
 //   0-3  softmax / epilogue: thread = row; tcgen05.ld of S, mask, online
 //        softmax (exp2 domain), P (bf16) written back over S in TMEM,
 //        O rescale in TMEM when the row max grows, final O / l -> bf16.
-//   4    TMA producer: Q tile, the sequence's global rows (cls + query group)
-//        and a 2-stage ring of 128-key K/V blocks (128B-swizzled boxes).
+//   4    TMA producer (lane 0): Q tile, the sequence's global rows (cls +
+//        query group) and a ring of BN-key K/V blocks (128B-swizzled boxes);
+//        all 32 lanes: the head rows (folded in, see below).
 //   5    MMA issuer (one thread): S = Q K^T (SS, K-major) into TMEM, then
 //        O += P V with P read from TMEM (TS) and V as an MN-major SMEM operand.
-// Key blocks: the global block (cls + query keys, N = 32) then doc keys
-// [max(0, r0-w), min(n, r0+128+w)) in blocks of 128.  Semantics as the band
-// kernel (R/band.py:48-52, R/attention.py:125-139, :228-257).
+// Key blocks: the global block (cls + query keys, N = GR) then doc keys from
+// r0 - ceil(w/BN)*BN (clamped at 0: BN-aligned with the tile, so the tile's own
+// 128 keys are whole ring blocks) to min(n, r0+128+w) in blocks of BN.
+// Semantics as the band kernel (R/band.py:48-52, R/attention.py:125-139, :228-257).
+//
+// Head rows (fold): the rows of the cls / query groups are computed by warp 4
+// on CUDA cores while the ring streams past -- no second pass over K/V.  Rows
+// with a FULL doc link (CLS; query rows under longformer / full / QDS) take a
+// split-softmax record (m, l, acc) over each 64-key half of the CTA's own doc
+// keys (the band kernel's record format, indexed by 64-row doc tile); the first
+// tile of each sequence also computes the head rows over the global keys (final
+// for rows without a doc link, else one more record), and
+// merge_full_rows_kernel folds the records (R/attention.py:416-473 for the
+// cls / query groups).
+#include "mma_tile.cuh"
 #include "tc_common.cuh"
 
 namespace sc {
@@ -42,6 +55,7 @@ struct Params {
   const int32_t* cu;
   const int32_t* qlen;
   const int32_t* tile_base;  // 128-row doc tiles per sequence (prefix)
+  const int32_t* tile_seq;   // 128-row tile -> sequence
   // QDS (R/attention.py:403-413, :434-470).  Doc-rows pass (qds = 1): a dense
   // key segment over the sequence's global doc tokens (gathered into a compact
   // [q|k|v] buffer) and band slots hitting a global excluded.  Global-rows pass
@@ -53,7 +67,13 @@ struct Params {
   const int32_t* glob_pos;   // doc-relative positions of the globals
   __nv_bfloat16* out;
   int64_t ld_out;
+  // head-row fold (fold = 1; 0 in the QDS global-rows pass)
+  int fold, fneed, fmax, ntiles_max;
+  int hl[2][2], hdoc[2];        // head group (cls, query) -> cls / query key links; FULL doc link
+  const int32_t* tile64;        // 64-row doc-tile prefix (record index of a 64-key half)
+  float* partials;              // records (m, l, pad, pad, acc[64]) x fmax x H per 64-row tile
 };
+constexpr int REC = D + 4;
 
 template <class C>
 struct Smem {
@@ -61,11 +81,150 @@ struct Smem {
   static constexpr int Q = 0;
   static constexpr int KG = Q + BM * ROWB;
   static constexpr int VG = KG + C::GR * ROWB;
-  static constexpr int KV = VG + C::GR * ROWB;  // NS x (K block, V block)
+  static constexpr int QF = VG + C::GR * ROWB;  // q rows of the head groups (TMA, 128B swizzle)
+  static constexpr int KV = QF + C::GR * ROWB;  // NS x (K block, V block)
   static constexpr int STAGE = 2 * C::BN * ROWB;
-  static constexpr int BAR = KV + C::NS * STAGE;
+  static constexpr int HST = KV + C::NS * STAGE;  // head-row softmax state: (GR/16) x 32 lanes x 36 fp32
+  static constexpr int BAR = HST + (C::GR / 16) * 32 * 36 * 4;
   // barriers: qbar, full[NS], empty[NS], s_full[2], p_full[2], pv_done[2], o_final; tmem holder
   static constexpr int TOTAL = BAR + 16 * 8 + 16;
+};
+
+// Head rows on the legacy tensor-core path (warp 4, all lanes; mma.sync m16n8k16 over the same
+// 128B-swizzled K / V blocks the ring holds): 16 head rows per fragment chunk, the online-softmax
+// state of a 64-key half kept in shared memory between the half's ring blocks.
+template <class C>
+struct HeadRows {
+  using SM = Smem<C>;
+  const Params& p;
+  uint32_t sm0;
+  float* hst;
+  int lane, h, j, n_doc, r0, G;
+  __device__ HeadRows(const Params& p_, uint8_t* smem, uint32_t sm0_, int lane_, int h_, int j_, const SeqGroups& g,
+                      int n_doc_, int r0_)
+      : p(p_), sm0(sm0_), hst(reinterpret_cast<float*>(smem + SM::HST)), lane(lane_), h(h_), j(j_), n_doc(n_doc_),
+        r0(r0_), G(1 + g.len[1]) {}
+
+  // split-softmax record of fragment rows (gq, gq + 8) of chunk fc (band-kernel format)
+  __device__ void write_recs(int64_t rec_idx, int fc, float m0, float m1, float l0, float l1, const float (&o)[8][4],
+                             bool only_doc_linked) const {
+    const int gq = lane >> 2, tq = lane & 3;
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    const float to_nat = p.c2 * 0.69314718055994530942f;  // raw logit -> natural units (1/scale)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int f = fc * 16 + gq + 8 * half;
+      if (f >= G || f >= (only_doc_linked ? p.fneed : C::GR)) continue;
+      const int grp = f == 0 ? 0 : 1;
+      const float mm = half ? m1 : m0, ll = half ? l1 : l0;
+      if (p.hdoc[grp]) {
+        float* rec = p.partials + ((rec_idx * p.H + h) * p.fmax + f) * REC;
+        if (tq == 0) {
+          rec[0] = ll > 0.f ? mm * to_nat : -INFINITY;
+          rec[1] = ll;
+        }
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb)
+          *reinterpret_cast<float2*>(rec + 4 + nb * 8 + 2 * tq) = make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
+      } else if (!only_doc_linked) {  // final row (no doc link): O / l
+        const float inv = ll > 0.f ? 1.f / ll : 0.f;
+        uint32_t* dst = reinterpret_cast<uint32_t*>(p.out + (int64_t)(__ldg(p.cu + j) + f) * p.ld_out + h * D + 2 * tq);
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][2 * half] * inv, o[nb][2 * half + 1] * inv);
+      }
+    }
+  }
+
+  // First tile of the sequence: head rows over the cls + query keys (links per source group).
+  __device__ void global_keys() const {
+    const int gq = lane >> 2, tq = lane & 3;
+    const int hl_bits = p.hl[0][0] | (p.hl[0][1] << 1) | (p.hl[1][0] << 2) | (p.hl[1][1] << 3);
+#pragma unroll
+    for (int fc = 0; fc < C::GR / 16; ++fc) {
+      if (fc * 16 >= G) break;
+      uint32_t qa[4][4];
+      mmat::load_a(sm0 + SM::QF, fc * 16, lane, qa);
+      float sc[C::GR / 8][4];
+#pragma unroll
+      for (int nb = 0; nb < C::GR / 8; ++nb) sc[nb][0] = sc[nb][1] = sc[nb][2] = sc[nb][3] = 0.f;
+#pragma unroll
+      for (int gc = 0; gc < C::GR / 16; ++gc) mmat::mm_nt16(sm0 + SM::KG, gc * 16, lane, qa, sc[2 * gc], sc[2 * gc + 1]);
+#pragma unroll
+      for (int nb = 0; nb < C::GR / 8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int f = fc * 16 + gq + ((e >> 1) << 3);
+          const int kg = nb * 8 + 2 * tq + (e & 1);
+          const int grp = f == 0 ? 0 : 1;
+          if (!(f < G && kg < G && ((hl_bits >> (grp * 2 + (kg == 0 ? 0 : 1))) & 1))) sc[nb][e] = -INFINITY;
+        }
+      float o[8][4];
+#pragma unroll
+      for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
+      float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+      mmat::softmax_update<C::GR / 8, true>(sc, p.c2, m0, m1, l0, l1, o);
+#pragma unroll
+      for (int gc = 0; gc < C::GR / 16; ++gc) mmat::mm_nn16(sm0 + SM::VG, gc * 16, lane, sc[2 * gc], sc[2 * gc + 1], o);
+      write_recs(p.ntiles_max + j, fc, m0, m1, l0, l1, o, false);
+    }
+  }
+
+  // One ring block of the CTA's own doc keys [r0 + off, r0 + off + BN) for the FULL-doc-link rows;
+  // a record closes each 64-key half (state carried in shared memory between the half's blocks).
+  __device__ void own_block(uint32_t kvbuf, int off) const {
+    constexpr int BN = C::BN;
+    const int tq = lane & 3;
+    const int k0 = r0 + off;
+    const int nk = min(BN, n_doc - k0);
+    const bool first = off % 64 == 0;
+    const bool close = ((off + BN) % 64 == 0) || (k0 + BN >= n_doc);
+    for (int fc = 0; fc < C::GR / 16; ++fc) {
+      if (fc * 16 >= p.fneed || fc * 16 >= G) break;
+      float* stt = hst + (fc * 32 + lane) * 36;
+      uint32_t qa[4][4];
+      mmat::load_a(sm0 + SM::QF, fc * 16, lane, qa);
+      float o[8][4];
+      float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+      if (first) {
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
+      } else {
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) {
+          const float4 t = *reinterpret_cast<const float4*>(stt + 4 * nb);
+          o[nb][0] = t.x, o[nb][1] = t.y, o[nb][2] = t.z, o[nb][3] = t.w;
+        }
+        m0 = stt[32], m1 = stt[33], l0 = stt[34], l1 = stt[35];
+      }
+#pragma unroll
+      for (int c = 0; c < BN; c += 32) {
+        float sc[4][4];
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) sc[nb][0] = sc[nb][1] = sc[nb][2] = sc[nb][3] = 0.f;
+        mmat::mm_nt16(kvbuf, c, lane, qa, sc[0], sc[1]);
+        mmat::mm_nt16(kvbuf, c + 16, lane, qa, sc[2], sc[3]);
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (c + nb * 8 + 2 * tq + (e & 1) >= nk) sc[nb][e] = -INFINITY;
+        mmat::softmax_update<4>(sc, p.c2, m0, m1, l0, l1, o);
+        mmat::mm_nn16(kvbuf + BN * ROWB, c, lane, sc[0], sc[1], o);
+        mmat::mm_nn16(kvbuf + BN * ROWB, c + 16, lane, sc[2], sc[3], o);
+      }
+      if (close) {
+        write_recs(__ldg(p.tile64 + j) + r0 / 64 + (off + BN - 1) / 64, fc, m0, m1, l0, l1, o, true);
+      } else {
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb)
+          *reinterpret_cast<float4*>(stt + 4 * nb) = make_float4(o[nb][0], o[nb][1], o[nb][2], o[nb][3]);
+        stt[32] = m0, stt[33] = m1, stt[34] = l0, stt[35] = l1;
+      }
+    }
+  }
 };
 
 template <class C>
@@ -73,7 +232,7 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKg,
     const __grid_constant__ CUtensorMap tmVg, const __grid_constant__ CUtensorMap tmK,
     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmKq,
-    const __grid_constant__ CUtensorMap tmVq, Params p) {
+    const __grid_constant__ CUtensorMap tmVq, const __grid_constant__ CUtensorMap tmQf, Params p) {
   using SM = Smem<C>;
   constexpr int NS = C::NS, O_COL = C::O_COL, TMEM_COLS = C::TMEM_COLS, NBUF = C::NBUF, BN = C::BN,
                 GR = C::GR;
@@ -81,7 +240,7 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tile = blockIdx.x, h = blockIdx.y;
   if (tile >= __ldg(p.tile_base + p.nseq)) return;
-  const int j = find_seq(p.tile_base, p.nseq, tile);
+  const int j = __ldg(p.tile_seq + tile);
   const SeqGroups g = seq_groups(p.cu, p.qlen, j);
   const int n_doc = g.len[2];
   const int r0 = (tile - __ldg(p.tile_base + j)) * BM;
@@ -92,7 +251,8 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
   const int G = 1 + g.len[1];
   const bool has_glob = (p.link_cls || p.link_query);
   const int w = p.global_rows ? -1 : p.w;
-  const int lo = w < 0 ? 0 : max(0, r0 - w);
+  // BN-aligned with r0 (r0 is a multiple of BM): the own keys [r0, r0 + BM) are whole ring blocks
+  const int lo = w < 0 ? 0 : max(0, r0 - (w + BN - 1) / BN * BN);
   const int hi = w < 0 ? n_doc : min(n_doc, r0 + rows_here + w);
   const int ngd = p.qds ? (n_gq + BN - 1) / BN : 0;  // key blocks over the compact QDS globals
   const int nkb = ngd + (hi - lo + BN - 1) / BN;       // K/V ring blocks: QDS globals, then band
@@ -112,7 +272,7 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
     mbar_init(qbar, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(full_bar + 8 * s, 1);
-      mbar_init(empty_bar + 8 * s, 1);
+      mbar_init(empty_bar + 8 * s, p.fold ? 2 : 1);  // MMA commit (+ the head-row lanes)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(s_full + 8 * b, 1);
@@ -135,25 +295,53 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 4) {
-    // ------------------------------------------------------------- TMA
+    // ------------------------------------------------------------- TMA (lane 0) + head rows
+    const int col = h * D;
+    auto issue = [&](int kb) {
+      const int s = kb % NS;
+      mbar_expect_tx(full_bar + 8 * s, SM::STAGE);
+      const uint32_t kbuf = sm0 + SM::KV + s * SM::STAGE;
+      if (kb < ngd) {
+        tma_load_2d(kbuf, &tmKq, col, gq0 + kb * BN, full_bar + 8 * s);
+        tma_load_2d(kbuf + BN * ROWB, &tmVq, col, gq0 + kb * BN, full_bar + 8 * s);
+      } else {
+        tma_load_2d(kbuf, &tmK, col, doc0 + lo + (kb - ngd) * BN, full_bar + 8 * s);
+        tma_load_2d(kbuf + BN * ROWB, &tmV, col, doc0 + lo + (kb - ngd) * BN, full_bar + 8 * s);
+      }
+    };
     if (lane == 0) {
-      const int col = h * D;
-      mbar_expect_tx(qbar, (BM + 2 * GR) * ROWB);
+      mbar_expect_tx(qbar, (BM + (p.fold ? 3 : 2) * GR) * ROWB);
       tma_load_2d(sm0 + SM::Q, &tmQ, col, p.global_rows ? gq0 + r0 : doc0 + r0, qbar);
       tma_load_2d(sm0 + SM::KG, &tmKg, col, g.start, qbar);
       tma_load_2d(sm0 + SM::VG, &tmVg, col, g.start, qbar);
+      if (p.fold) tma_load_2d(sm0 + SM::QF, &tmQf, col, g.start, qbar);
+      for (int kb = 0; kb < min(NS, nkb); ++kb) issue(kb);
+    }
+    if (!p.fold) {
+      if (lane == 0)
+        for (int kb = NS; kb < nkb; ++kb) {
+          mbar_wait(empty_bar + 8 * (kb % NS), ((kb / NS) & 1) ^ 1);
+          issue(kb);
+        }
+    } else {
+      const HeadRows<C> hr(p, smem, sm0, lane, h, j, g, n_doc, r0);
+      mbar_wait(qbar, 0);
+      if (r0 == 0) hr.global_keys();
+      const int own0 = ngd + (r0 - lo) / BN;          // first ring block of the own keys
+      const int nown = (min(BM, n_doc - r0) + BN - 1) / BN;
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % NS;
-        if (kb >= NS) mbar_wait(empty_bar + 8 * s, ((kb / NS) & 1) ^ 1);
-        mbar_expect_tx(full_bar + 8 * s, SM::STAGE);
-        const uint32_t kbuf = sm0 + SM::KV + s * SM::STAGE;
-        if (kb < ngd) {
-          tma_load_2d(kbuf, &tmKq, col, gq0 + kb * BN, full_bar + 8 * s);
-          tma_load_2d(kbuf + BN * ROWB, &tmVq, col, gq0 + kb * BN, full_bar + 8 * s);
-        } else {
-          tma_load_2d(kbuf, &tmK, col, doc0 + lo + (kb - ngd) * BN, full_bar + 8 * s);
-          tma_load_2d(kbuf + BN * ROWB, &tmV, col, doc0 + lo + (kb - ngd) * BN, full_bar + 8 * s);
+        mbar_wait(full_bar + 8 * s, (kb / NS) & 1);
+        if (kb >= own0 && kb < own0 + nown) hr.own_block(sm0 + SM::KV + s * SM::STAGE, (kb - own0) * BN);
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(empty_bar + 8 * s);
+          if (kb + NS < nkb) {
+            mbar_wait(empty_bar + 8 * s, (kb / NS) & 1);
+            issue(kb + NS);
+          }
         }
+        __syncwarp();
       }
     }
   } else if (warp == 5) {
@@ -229,6 +417,23 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
       const uint32_t sa = lane_addr + S_COL + buf * BN;
       mbar_wait(s_full + 8 * buf, (b / NBUF) & 1);
       tc_fence_after();
+      // A band block no row of this warp reaches (the tile is a rectangle of keys, the band a
+      // parallelogram): P = 0 for the warp's 32 lanes, no logits read, no exponentials.
+      if (!glob && w >= 0 && b - (has_glob ? 1 : 0) >= ngd) {
+        const int k0 = lo + (b - (has_glob ? 1 : 0) - ngd) * BN;
+        if (k0 + BN - 1 < r0 + warp * 32 - w || k0 > r0 + warp * 32 + 31 + w) {
+          uint32_t z[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) z[e] = 0u;
+#pragma unroll
+          for (int c = 0; c < BN / 2; c += 16) TC_ST16(sa + c, z);
+          tc_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(p_full + 8 * buf);
+          continue;
+        }
+      }
       uint32_t v[BN];
 #pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 32) TC_LD32(sa + c0, (&v[c0]));
@@ -343,7 +548,8 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
 // 128-row tile prefix per sequence (single CTA scan): over the doc rows, or
 // (glob_cu != nullptr) over the QDS global doc rows.
 __global__ void tile128_prefix_kernel(const int32_t* __restrict__ cu, const int32_t* __restrict__ qlen, int nseq,
-                                      const int32_t* __restrict__ glob_cu, int32_t* __restrict__ base) {
+                                      const int32_t* __restrict__ glob_cu, int32_t* __restrict__ base,
+                                      int32_t* __restrict__ tile_seq) {
   __shared__ int32_t s[1024];
   int carry = 0;
   for (int b = 0; b < nseq; b += blockDim.x) {
@@ -359,7 +565,10 @@ __global__ void tile128_prefix_kernel(const int32_t* __restrict__ cu, const int3
       s[threadIdx.x] += a;
       __syncthreads();
     }
-    if (j < nseq) base[j + 1] = carry + s[threadIdx.x];
+    if (j < nseq) {
+      base[j + 1] = carry + s[threadIdx.x];
+      for (int t = carry + s[threadIdx.x] - n; t < carry + s[threadIdx.x]; ++t) tile_seq[t] = j;  // tile -> sequence
+    }
     carry += s[blockDim.x - 1];
     __syncthreads();
   }
@@ -401,7 +610,8 @@ static int launch_kernel(dim3 grid, const CUtensorMap* maps, const Params& p, cu
     }
     attr = true;
   }
-  tc_attn_kernel<C><<<grid, NTHREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
+  tc_attn_kernel<C><<<grid, NTHREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6],
+                                                  maps[7], p);
   SC_CHECK_LAUNCH("tc_attn_kernel");
   return SC_OK;
 }
@@ -421,9 +631,13 @@ using VMID32 = Cfg<2, 32, 32, 4, 2>;
 }  // namespace tck
 
 // [doc-tile prefix | global-tile prefix] (+ the compact QDS [q|k|v] rows).
-static size_t tc_prefix_bytes(int nseq) { return ((size_t)2 * (nseq + 1) * sizeof(int32_t) + 255) & ~size_t(255); }
-size_t tc_workspace_bytes(int nseq, int H, int n_global) {
-  return tc_prefix_bytes(nseq) + (size_t)n_global * 3 * H * tck::D * sizeof(__nv_bfloat16);
+// [doc-tile prefix | global-tile prefix | doc-tile -> sequence map | global-tile -> sequence map]
+static int tc_max_tiles(int nseq, int T) { return (T + tck::BM - 1) / tck::BM + nseq; }
+static size_t tc_prefix_bytes(int nseq, int T) {
+  return ((size_t)(2 * (nseq + 1) + 2 * tc_max_tiles(nseq, T)) * sizeof(int32_t) + 255) & ~size_t(255);
+}
+size_t tc_workspace_bytes(int nseq, int T, int H, int n_global) {
+  return tc_prefix_bytes(nseq, T) + (size_t)n_global * 3 * H * tck::D * sizeof(__nv_bfloat16);
 }
 
 int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
@@ -453,9 +667,9 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   if ((a.ld * 2) % 16 || (a.ld_out * 2) % 16) return unsupported("row strides");
   // workspace = [band-kernel records (head rows) | tile prefixes | QDS compact rows]
   const size_t band_bytes = (band_workspace_bytes(a.nseq, a.T, a.H, a.d, tile_rows, max_qgroup_len, L) + 255) & ~size_t(255);
-  if (!ws || ws_bytes < band_bytes + tc_prefix_bytes(a.nseq)) return unsupported("workspace too small");
+  if (!ws || ws_bytes < band_bytes + tc_prefix_bytes(a.nseq, a.T)) return unsupported("workspace too small");
   const size_t row_bytes = (size_t)3 * a.H * D * sizeof(__nv_bfloat16);
-  const int cap = qds ? (int)((ws_bytes - band_bytes - tc_prefix_bytes(a.nseq)) / row_bytes) : 0;
+  const int cap = qds ? (int)((ws_bytes - band_bytes - tc_prefix_bytes(a.nseq, a.T)) / row_bytes) : 0;
 
   // Variant choice (env SC_TC_VARIANT = 0/1/2 forces VLONG/VMID/VMID32, for measurement sweeps).
   static int forced = -2;
@@ -471,7 +685,9 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   int32_t* tbase = reinterpret_cast<int32_t*>(wsb + band_bytes);
   int32_t* gtbase = tbase + a.nseq + 1;
-  __nv_bfloat16* compact = reinterpret_cast<__nv_bfloat16*>(wsb + band_bytes + tc_prefix_bytes(a.nseq));
+  int32_t* tseq = gtbase + a.nseq + 1;
+  int32_t* gtseq = tseq + tc_max_tiles(a.nseq, a.T);
+  __nv_bfloat16* compact = reinterpret_cast<__nv_bfloat16*>(wsb + band_bytes + tc_prefix_bytes(a.nseq, a.T));
   const int64_t cld = 3 * cols;  // compact row stride (elements)
   auto build_maps = [&](CUtensorMap* maps, int v, bool global_rows) {
     const int bn = v == 0 ? 64 : 32, gr = v == 1 ? 16 : 32;
@@ -479,6 +695,7 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
     bool ok = global_rows ? make_map(&maps[0], compact, cols, crow, cld, BM) : make_map(&maps[0], a.q, cols, a.T, a.ld, BM);
     ok = ok && make_map(&maps[1], a.k, cols, a.T, a.ld, gr) && make_map(&maps[2], a.v, cols, a.T, a.ld, gr) &&
          make_map(&maps[3], a.k, cols, a.T, a.ld, bn) && make_map(&maps[4], a.v, cols, a.T, a.ld, bn);
+    ok = ok && make_map(&maps[7], a.q, cols, a.T, a.ld, gr);
     if (qds) ok = ok && make_map(&maps[5], compact + cols, cols, crow, cld, bn) &&
                   make_map(&maps[6], compact + 2 * cols, cols, crow, cld, bn);
     else { maps[5] = maps[3]; maps[6] = maps[4]; }
@@ -491,7 +708,7 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   };
 
   if (qds) {
-    tile128_prefix_kernel<<<1, 1024, 0, st>>>(a.cu, a.qlen, a.nseq, a.glob_cu, gtbase);
+    tile128_prefix_kernel<<<1, 1024, 0, st>>>(a.cu, a.qlen, a.nseq, a.glob_cu, gtbase, gtseq);
     SC_CHECK_LAUNCH("tile128_prefix_kernel");
     if (cap > 0) {
       qds_gather_kernel<<<(cap + 7) / 8, 256, 0, st>>>(a.cu, a.qlen, a.nseq, a.glob_cu, a.glob_pos,
@@ -507,30 +724,39 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   p.nseq = a.nseq; p.H = a.H; p.w = w == SC_LINK_FULL ? -1 : w; p.padding = a.padding;
   p.link_cls = L.w[2][0] == SC_LINK_FULL; p.link_query = L.w[2][1] == SC_LINK_FULL;
   p.c2 = 1.4426950408889634f / a.scale;
-  p.cu = a.cu; p.qlen = a.qlen; p.tile_base = tbase;
+  p.cu = a.cu; p.qlen = a.qlen; p.tile_base = tbase; p.tile_seq = tseq;
   p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
   p.qds = qds ? 1 : 0; p.global_rows = 0;
   p.flags = a.flags; p.glob_cu = a.glob_cu; p.glob_pos = a.glob_pos;
-  tile128_prefix_kernel<<<1, 1024, 0, st>>>(a.cu, a.qlen, a.nseq, nullptr, tbase);
+  // head rows folded into the doc-rows pass (records in the band kernel's workspace layout)
+  const int fneed = full_rows_needed(L, max_qgroup_len);
+  p.fold = 1; p.fneed = fneed; p.fmax = fneed > 0 ? fneed : 1;
+  p.ntiles_max = (int)((a.T + tile_rows - 1) / tile_rows + a.nseq);
+  for (int gsrc = 0; gsrc < 2; ++gsrc) {
+    p.hl[gsrc][0] = L.w[gsrc][0] == SC_LINK_FULL;
+    p.hl[gsrc][1] = L.w[gsrc][1] == SC_LINK_FULL;
+    p.hdoc[gsrc] = L.w[gsrc][2] == SC_LINK_FULL;
+  }
+  p.tile64 = seq_tile_base; p.partials = static_cast<float*>(ws);
+  tile128_prefix_kernel<<<1, 1024, 0, st>>>(a.cu, a.qlen, a.nseq, nullptr, tbase, tseq);
   SC_CHECK_LAUNCH("tile128_prefix_kernel");
-  CUtensorMap maps[7];
+  CUtensorMap maps[8];
   if (!build_maps(maps, var, false)) return unsupported("cuTensorMapEncodeTiled failed");
   int rc = launch_var(var, dim3((unsigned)((a.T + BM - 1) / BM + a.nseq), (unsigned)a.H), maps, p);
   if (rc) return rc;
   if (qds && cap > 0) {
     // QDS global doc rows: every key of their sequence (R/attention.py:461-470)
     Params pg = p;
-    pg.qds = 0; pg.global_rows = 1; pg.tile_base = gtbase; pg.link_cls = pg.link_query = 1;
+    pg.qds = 0; pg.global_rows = 1; pg.tile_base = gtbase; pg.tile_seq = gtseq; pg.link_cls = pg.link_query = 1; pg.fold = 0;
     const int vg = forced >= 0 ? var : 0;
-    CUtensorMap gmaps[7];
+    CUtensorMap gmaps[8];
     if (!build_maps(gmaps, vg, true)) return unsupported("cuTensorMapEncodeTiled failed");
     rc = launch_var(vg, dim3((unsigned)((cap + BM - 1) / BM + a.nseq), (unsigned)a.H), gmaps, pg);
     if (rc) return rc;
   }
-  // Head rows (cls + query group): the band kernel in head-rows-only mode
-  // streams each doc key once for the CLS split-softmax records, then merges.
-  return launch_attn_band(a, dtype, seq_tile_base, seq_head_base, tile_rows, max_qgroup_len, ws,
-                          band_bytes, st, /*doc_rows=*/false);
+  // Head rows: the doc-rows pass left the split-softmax records; fold them into the
+  // rows with a FULL doc link.
+  return launch_head_merge(a, seq_tile_base, tile_rows, max_qgroup_len, ws, st);
 }
 
 }  // namespace sc

@@ -81,6 +81,50 @@ __device__ __forceinline__ void mm_nn16(uint32_t bbuf, int row0, int lane, const
   }
 }
 
+// Online-softmax update over NB n8 blocks of RAW logits (masked to -inf) for the two rows (g, g+8)
+// of an m16n8 C fragment; m in raw-logit units, c2 = log2(e)/scale.  Overwrites s with P.
+// kFresh: o is still zero (first update of a row block) -> no O rescale.
+template <int NB, bool kFresh = false>
+__device__ __forceinline__ void softmax_update(float (&s)[NB][4], float c2, float& m0, float& m1, float& l0,
+                                               float& l1, float (&o)[8][4]) {
+  float x0 = -INFINITY, x1 = -INFINITY;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    x0 = fmaxf(x0, fmaxf(s[b][0], s[b][1]));
+    x1 = fmaxf(x1, fmaxf(s[b][2], s[b][3]));
+  }
+  x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, 1));
+  x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, 2));
+  x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, 1));
+  x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, 2));
+  const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);
+  const float b0 = n0 == -INFINITY ? 0.f : n0 * c2, b1 = n1 == -INFINITY ? 0.f : n1 * c2;
+  const float a0 = ex2(fmaf(m0, c2, -b0)), a1 = ex2(fmaf(m1, c2, -b1));
+  float r0 = 0.f, r1 = 0.f;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    s[b][0] = ex2(fmaf(s[b][0], c2, -b0));
+    s[b][1] = ex2(fmaf(s[b][1], c2, -b0));
+    s[b][2] = ex2(fmaf(s[b][2], c2, -b1));
+    s[b][3] = ex2(fmaf(s[b][3], c2, -b1));
+    r0 += s[b][0] + s[b][1];
+    r1 += s[b][2] + s[b][3];
+  }
+  l0 = fmaf(l0, a0, r0);
+  l1 = fmaf(l1, a1, r1);
+  if constexpr (!kFresh) {
+#pragma unroll
+    for (int nb = 0; nb < 8; ++nb) {
+      o[nb][0] *= a0;
+      o[nb][1] *= a0;
+      o[nb][2] *= a1;
+      o[nb][3] *= a1;
+    }
+  }
+  m0 = n0;
+  m1 = n1;
+}
+
 // Stage `nrows` rows (64 bf16 each) into a swizzled smem buffer; rowptr(i) == nullptr zero-fills.
 template <typename F>
 __device__ __forceinline__ void stage_rows(uint32_t buf, int nrows, const __nv_bfloat16* any, F&& rowptr) {
