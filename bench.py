@@ -512,6 +512,8 @@ def run_gpu(args):
         variants["varlen_documents"] = varlen_variant(P, dev, model, max(3, args.steps // 2))
         variants["passages"] = passages_variant(P, dev, args.steps)
         variants["attention_sweep"] = attention_sweep(P, dev, (hbm_peak, tf_burst))
+        variants["attention_sweep_d32"] = attention_sweep(  # MiniLM-L6-H384 heads: 12 x d=32
+            P, dev, (hbm_peak, tf_burst), d=32, windows=(("sparse", 4), ("sparse", 64), ("sparse", 256)))
         variants["fp32_ranking_exact"] = fp32_variant(P, dev, max(3, args.steps // 4))
 
     # ---- roofline of the attention kernel (sc_attn_fwd, band + head-row pass) ----

@@ -49,6 +49,7 @@ struct Params {
   int reverse;  // visit tiles last-to-first: the producing GEMM's most recent output rows are still in L2
   int link_cls, link_query;
   int doc_rows;  // 0: head rows only (doc rows computed by the tcgen05 kernel)
+  int dout;      // head_dim (32 or 64; smem rows are always 64 dims, zero-padded)
   // head rows (cls = group 0, query = group 1): links to cls / query keys, doc FULL
   int hl[2][2], hdoc[2];
   int ntiles_max;      // record index of sequence j's global-key record = ntiles_max + j
@@ -84,24 +85,27 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
   }
 }
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
-                                            uint32_t bar) {
+// Tensor maps are 3-D [rows][heads][head_dim] with 64-element boxes along head_dim: a
+// 32-dim head lands zero-padded in a 64-dim (128 B) smem row (the out-of-bounds half of the
+// box is zero-filled; no extra HBM bytes), so one kernel serves head_dim 32 and 64.
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int head, int row, uint32_t bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(head), "r"(row), "r"(bar)
       : "memory");
 }
 // Pull a box into L2 only (no smem, no barrier): the producer runs one
 // pipeline round ahead so the next round's TMA loads are served from L2.
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
-               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int head, int row) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(head), "r"(row)
                : "memory");
 }
-// Shared -> global TMA store of a box (bulk-group completion).
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
-               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(src)
+// Shared -> global TMA store of a box (bulk-group completion); the padded half of a
+// 32-dim head is clipped.
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int head, int row) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(head), "r"(row), "r"(src)
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -380,19 +384,17 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
           if (it >= NS) mbar_wait(empty_bar + 8 * s, ((it / NS) & 1) ^ 1);
           const uint32_t fb = full_bar + 8 * s;
           if (h + NS < p.H) {  // L2 prefetch of the boxes this stage will hold next round
-            const int pc = (h + NS) * D;
-            if (p.doc_rows) tma_prefetch_2d(&tmQ, pc, doc_row0);
-            tma_prefetch_2d(&tmKb, pc, doc_row0 - w);
-            tma_prefetch_2d(&tmVb, pc, doc_row0 - w);
+            if (p.doc_rows) tma_prefetch_3d(&tmQ, h + NS, doc_row0);
+            tma_prefetch_3d(&tmKb, h + NS, doc_row0 - w);
+            tma_prefetch_3d(&tmVb, h + NS, doc_row0 - w);
           }
           mbar_expect_tx(fb, bytes);
-          const int col = h * D;
-          if (p.doc_rows) tma_load_2d(q_buf(s), &tmQ, col, doc_row0, fb);
-          tma_load_2d(kb_buf(s), &tmKb, col, doc_row0 - w, fb);
-          tma_load_2d(vb_buf(s), &tmVb, col, doc_row0 - w, fb);
-          tma_load_2d(kg_buf(s), &tmKg, col, g.start, fb);
-          tma_load_2d(vg_buf(s), &tmVg, col, g.start, fb);
-          tma_load_2d(qf_buf(s), &tmQf, col, g.start, fb);
+          if (p.doc_rows) tma_load_3d(q_buf(s), &tmQ, h, doc_row0, fb);
+          tma_load_3d(kb_buf(s), &tmKb, h, doc_row0 - w, fb);
+          tma_load_3d(vb_buf(s), &tmVb, h, doc_row0 - w, fb);
+          tma_load_3d(kg_buf(s), &tmKg, h, g.start, fb);
+          tma_load_3d(vg_buf(s), &tmVg, h, g.start, fb);
+          tma_load_3d(qf_buf(s), &tmQf, h, g.start, fb);
         }
       }
     }
@@ -574,18 +576,20 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
                     pack_bf16(o[2 * np + 1][2] * i1, o[2 * np + 1][3] * i1));
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0) tma_store_2d(&tmO, ob + wr0 * ROWB, h * D, doc_row0 + wr0);
+          if (lane == 0) tma_store_3d(&tmO, ob + wr0 * ROWB, h, doc_row0 + wr0);
         } else {
-        __nv_bfloat16* out_h = p.out + h * D + 2 * tq;
+        __nv_bfloat16* out_h = p.out + h * p.dout + 2 * tq;
         if (ra < n_doc) {
           uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq) * p.ld_out);
   #pragma unroll
-          for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][0] * i0, o[nb][1] * i0);
+          for (int nb = 0; nb < 8; ++nb)
+            if (nb * 8 < p.dout) dst[nb * 4] = pack_bf16(o[nb][0] * i0, o[nb][1] * i0);
         }
         if (rb < n_doc) {
           uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq + 8) * p.ld_out);
   #pragma unroll
-          for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][2] * i1, o[nb][3] * i1);
+          for (int nb = 0; nb < 8; ++nb)
+            if (nb * 8 < p.dout) dst[nb * 4] = pack_bf16(o[nb][2] * i1, o[nb][3] * i1);
         }
         }
       }
@@ -686,10 +690,10 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
                       make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
               } else {
                 const float inv = ll > 0.f ? 1.f / ll : 0.f;
-                uint32_t* dst = reinterpret_cast<uint32_t*>(p.out + (int64_t)(g.start + f) * p.ld_out + h * D + 2 * tq);
+                uint32_t* dst = reinterpret_cast<uint32_t*>(p.out + (int64_t)(g.start + f) * p.ld_out + h * p.dout + 2 * tq);
   #pragma unroll
                 for (int nb = 0; nb < 8; ++nb)
-                  dst[nb * 4] = pack_bf16(o[nb][2 * half] * inv, o[nb][2 * half + 1] * inv);
+                  if (nb * 8 < p.dout) dst[nb * 4] = pack_bf16(o[nb][2 * half] * inv, o[nb][2 * half + 1] * inv);
               }
             }
           }
@@ -768,9 +772,9 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32) merge_full_rows_kernel(Param
   }
   const float l = warp_sum(lsum);
   const float inv = l > 0.f ? 1.f / l : 0.f;
-  __nv_bfloat16* dst = p.out + (int64_t)(g.start + f) * p.ld_out + h * D;
+  __nv_bfloat16* dst = p.out + (int64_t)(g.start + f) * p.ld_out + h * p.dout;
   dst[lane] = __float2bfloat16_rn(acc0 * inv);
-  dst[lane + 32] = __float2bfloat16_rn(acc1 * inv);
+  if (p.dout > 32) dst[lane + 32] = __float2bfloat16_rn(acc1 * inv);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -789,15 +793,16 @@ static EncodeFn get_encode() {
   return fn;
 }
 
-static bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t ld_elems,
+// [rows][heads][d] bf16 (row stride ld elements) as a 3-D map with 64 x 1 x box_rows boxes
+static bool make_map(CUtensorMap* m, const void* base, int d, int heads, int64_t rows, int64_t ld_elems,
                      int box_rows) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld_elems * 2)};
-  cuuint32_t box[2] = {(cuuint32_t)D, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)heads, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {(cuuint64_t)(d * 2), (cuuint64_t)(ld_elems * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)D, 1u, (cuuint32_t)box_rows};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -866,7 +871,7 @@ size_t band_workspace_bytes(int nseq, int T, int H, int d, int tile_rows, int ma
   // records: one per doc tile (<= ceil(T/64) + nseq) + one global-key record per
   // sequence, each H x f x (m, l, pad, pad, acc[d]).
   int64_t recs = (T + tile_rows - 1) / tile_rows + 2 * (int64_t)nseq;
-  return (size_t)recs * H * f * (d + 4) * sizeof(float);
+  return (size_t)recs * H * f * ((d < 64 ? 64 : d) + 4) * sizeof(float);  // records keep 64 dims (d = 32 zero-padded)
 }
 
 int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
@@ -881,14 +886,14 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
     return SC_ERR_UNSUPPORTED;
   };
   if (dtype != SC_DTYPE_BF16) return unsupported("needs bf16");
-  if (a.d != D) return unsupported("needs head_dim 64");
+  if (a.d != D && a.d != 32) return unsupported("needs head_dim 32 or 64");
   // QDS head rows attend every key (like longformer), so head-rows-only mode
   // ignores the globals; QDS doc rows need the tcgen05 kernel's dense segment.
   if (a.glob_cu && doc_rows) return unsupported("QDS global tokens");
   if (w < 0 || w > MAX_W) return unsupported("doc->doc link must be a window <= 96");
   for (int x : {L.w[2][0], L.w[2][1], L.w[0][2], L.w[1][2], L.w[0][0], L.w[0][1], L.w[1][0], L.w[1][1]})
     if (x != SC_LINK_FULL && x != SC_LINK_NONE) return unsupported("windowed link outside doc->doc");
-  if (max_qgroup_len + 1 > 32) return unsupported("query group longer than 31 rows");
+  if (max_qgroup_len + 1 > 64) return unsupported("query group longer than 63 rows");
   if (tile_rows != BM || !seq_tile_base || !seq_head_base) return unsupported("layout tiles must be 64 rows");
   if (((uintptr_t)a.q | (uintptr_t)a.k | (uintptr_t)a.v | (uintptr_t)a.out) & 15)
     return unsupported("16-byte alignment");
@@ -896,19 +901,19 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   const int fneed = full_rows_needed(L, max_qgroup_len);
   const size_t need = band_workspace_bytes(a.nseq, a.T, a.H, a.d, tile_rows, max_qgroup_len, L);
   if (need > ws_bytes || (need && !ws)) return unsupported("workspace too small");
-  const int GR = (max_qgroup_len + 1 <= 16) ? 16 : 32;
+  const int GR = (max_qgroup_len + 1 <= 16) ? 16 : (max_qgroup_len + 1 <= 32 ? 32 : 64);
 
   CUtensorMap maps[7];
-  const int64_t cols = (int64_t)a.H * D;
-  if (!make_map(&maps[0], a.q, cols, a.T, a.ld, BM) || !make_map(&maps[1], a.q, cols, a.T, a.ld, GR) ||
-      !make_map(&maps[2], a.k, cols, a.T, a.ld, GR) || !make_map(&maps[3], a.v, cols, a.T, a.ld, GR) ||
-      !make_map(&maps[4], a.k, cols, a.T, a.ld, BM + 2 * w) ||
-      !make_map(&maps[5], a.v, cols, a.T, a.ld, BM + 2 * w) ||
-      !make_map(&maps[6], a.out, cols, a.T, a.ld_out, 16))
+  const int dd = a.d, H = a.H;
+  if (!make_map(&maps[0], a.q, dd, H, a.T, a.ld, BM) || !make_map(&maps[1], a.q, dd, H, a.T, a.ld, GR) ||
+      !make_map(&maps[2], a.k, dd, H, a.T, a.ld, GR) || !make_map(&maps[3], a.v, dd, H, a.T, a.ld, GR) ||
+      !make_map(&maps[4], a.k, dd, H, a.T, a.ld, BM + 2 * w) ||
+      !make_map(&maps[5], a.v, dd, H, a.T, a.ld, BM + 2 * w) ||
+      !make_map(&maps[6], a.out, dd, H, a.T, a.ld_out, 16))
     return unsupported("cuTensorMapEncodeTiled failed");
 
   Params p;
-  p.nseq = a.nseq; p.H = a.H; p.w = w; p.doc_rows = doc_rows ? 1 : 0;
+  p.nseq = a.nseq; p.H = a.H; p.w = w; p.doc_rows = doc_rows ? 1 : 0; p.dout = a.d;
   const int nbc = (16 + 2 * w + 31) / 32;
   p.kb_rows = 48 + 32 * nbc;
   p.fneed = fneed; p.fmax = fneed; p.padding = a.padding;
@@ -933,7 +938,9 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   // Doc rows + head rows over the global keys (first tile of each sequence).
   // (seq_head_base is unused: head rows are addressed through cu_seqlens.)
   (void)seq_head_base;
-  int rc = GR == 16 ? launch_gr<16>(nbc, maps, p, grid, st) : launch_gr<32>(nbc, maps, p, grid, st);
+  int rc = GR == 16 ? launch_gr<16>(nbc, maps, p, grid, st)
+         : GR == 32 ? launch_gr<32>(nbc, maps, p, grid, st)
+                    : launch_gr<64>(nbc, maps, p, grid, st);
   if (rc || fneed == 0) return rc;
   const int64_t items = (int64_t)a.nseq * a.H * fneed;
   merge_full_rows_kernel<<<(unsigned)((items + MERGE_WARPS - 1) / MERGE_WARPS), MERGE_WARPS * 32, 0, st>>>(p);
@@ -948,7 +955,7 @@ int launch_head_merge(const AttnArgs& a, const int32_t* seq_tile_base, int tile_
   const int fneed = full_rows_needed(L, max_qgroup_len);
   if (fneed == 0) return SC_OK;
   Params p{};
-  p.nseq = a.nseq; p.H = a.H; p.fneed = fneed; p.fmax = fneed;
+  p.nseq = a.nseq; p.H = a.H; p.fneed = fneed; p.fmax = fneed; p.dout = a.d;
   p.cu = a.cu; p.qlen = a.qlen; p.tile_base = seq_tile_base;
   p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
   p.partials = static_cast<float*>(ws);

@@ -67,6 +67,7 @@ struct Params {
   const int32_t* glob_pos;   // doc-relative positions of the globals
   __nv_bfloat16* out;
   int64_t ld_out;
+  int dout;  // head_dim (32 or 64; operands are staged as 64 zero-padded dims)
   // head-row fold (fold = 1; 0 in the QDS global-rows pass)
   int fold, fneed, fmax, ntiles_max;
   int hl[2][2], hdoc[2];        // head group (cls, query) -> cls / query key links; FULL doc link
@@ -131,9 +132,10 @@ struct HeadRows {
           *reinterpret_cast<float2*>(rec + 4 + nb * 8 + 2 * tq) = make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
       } else if (!only_doc_linked) {  // final row (no doc link): O / l
         const float inv = ll > 0.f ? 1.f / ll : 0.f;
-        uint32_t* dst = reinterpret_cast<uint32_t*>(p.out + (int64_t)(__ldg(p.cu + j) + f) * p.ld_out + h * D + 2 * tq);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(p.out + (int64_t)(__ldg(p.cu + j) + f) * p.ld_out + h * p.dout + 2 * tq);
 #pragma unroll
-        for (int nb = 0; nb < 8; ++nb) dst[nb * 4] = pack_bf16(o[nb][2 * half] * inv, o[nb][2 * half + 1] * inv);
+        for (int nb = 0; nb < 8; ++nb)
+          if (nb * 8 < p.dout) dst[nb * 4] = pack_bf16(o[nb][2 * half] * inv, o[nb][2 * half + 1] * inv);
       }
     }
   }
@@ -296,25 +298,24 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
 
   if (warp == 4) {
     // ------------------------------------------------------------- TMA (lane 0) + head rows
-    const int col = h * D;
     auto issue = [&](int kb) {
       const int s = kb % NS;
       mbar_expect_tx(full_bar + 8 * s, SM::STAGE);
       const uint32_t kbuf = sm0 + SM::KV + s * SM::STAGE;
       if (kb < ngd) {
-        tma_load_2d(kbuf, &tmKq, col, gq0 + kb * BN, full_bar + 8 * s);
-        tma_load_2d(kbuf + BN * ROWB, &tmVq, col, gq0 + kb * BN, full_bar + 8 * s);
+        tma_load_3d(kbuf, &tmKq, h, gq0 + kb * BN, full_bar + 8 * s);
+        tma_load_3d(kbuf + BN * ROWB, &tmVq, h, gq0 + kb * BN, full_bar + 8 * s);
       } else {
-        tma_load_2d(kbuf, &tmK, col, doc0 + lo + (kb - ngd) * BN, full_bar + 8 * s);
-        tma_load_2d(kbuf + BN * ROWB, &tmV, col, doc0 + lo + (kb - ngd) * BN, full_bar + 8 * s);
+        tma_load_3d(kbuf, &tmK, h, doc0 + lo + (kb - ngd) * BN, full_bar + 8 * s);
+        tma_load_3d(kbuf + BN * ROWB, &tmV, h, doc0 + lo + (kb - ngd) * BN, full_bar + 8 * s);
       }
     };
     if (lane == 0) {
       mbar_expect_tx(qbar, (BM + (p.fold ? 3 : 2) * GR) * ROWB);
-      tma_load_2d(sm0 + SM::Q, &tmQ, col, p.global_rows ? gq0 + r0 : doc0 + r0, qbar);
-      tma_load_2d(sm0 + SM::KG, &tmKg, col, g.start, qbar);
-      tma_load_2d(sm0 + SM::VG, &tmVg, col, g.start, qbar);
-      if (p.fold) tma_load_2d(sm0 + SM::QF, &tmQf, col, g.start, qbar);
+      tma_load_3d(sm0 + SM::Q, &tmQ, h, p.global_rows ? gq0 + r0 : doc0 + r0, qbar);
+      tma_load_3d(sm0 + SM::KG, &tmKg, h, g.start, qbar);
+      tma_load_3d(sm0 + SM::VG, &tmVg, h, g.start, qbar);
+      if (p.fold) tma_load_3d(sm0 + SM::QF, &tmQf, h, g.start, qbar);
       for (int kb = 0; kb < min(NS, nkb); ++kb) issue(kb);
     }
     if (!p.fold) {
@@ -517,9 +518,10 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     const int orow = p.global_rows ? (r < rows_here ? __ldg(p.glob_pos + gq0 + rr) : 0) : rr;
-    __nv_bfloat16* dst = p.out + (int64_t)(doc0 + orow) * p.ld_out + h * D;
+    __nv_bfloat16* dst = p.out + (int64_t)(doc0 + orow) * p.ld_out + h * p.dout;
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 32) {
+      if (c0 >= p.dout) break;  // head_dim 32: the zero-padded half of O stays in TMEM
       uint32_t o[32];
       TC_LD32(lane_addr + O_COL + c0, o);
       tc_wait_ld();
@@ -627,6 +629,7 @@ static int launch_kernel(dim3 grid, const CUtensorMap* maps, const Params& p, cu
 using VLONG = Cfg<2, 64, 32, 2, 4>;
 using VMID = Cfg<2, 32, 16, 4, 3>;
 using VMID32 = Cfg<2, 32, 32, 4, 2>;
+using VG64 = Cfg<2, 64, 64, 2, 3>;  // query groups of 32..63 rows (64 global key rows)
 
 }  // namespace tck
 
@@ -651,14 +654,14 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   };
   const bool qds = a.glob_cu != nullptr;
   if (dtype != SC_DTYPE_BF16) return unsupported("needs bf16");
-  if (a.d != D) return unsupported("needs head_dim 64");
+  if (a.d != D && a.d != 32) return unsupported("needs head_dim 32 or 64");
   if (qds && (!a.flags || !a.glob_pos)) return unsupported("QDS needs tok_flags and glob_pos");
   const int w = L.w[2][2];
   if (w == SC_LINK_NONE) return unsupported("doc rows must attend doc keys");
   if (qds && w == SC_LINK_FULL) return unsupported("QDS with a full doc->doc link");
   if (L.w[2][0] != SC_LINK_FULL && L.w[2][0] != SC_LINK_NONE) return unsupported("windowed doc->cls");
   if (L.w[2][1] != SC_LINK_FULL && L.w[2][1] != SC_LINK_NONE) return unsupported("windowed doc->query");
-  if (max_qgroup_len + 1 > 32) return unsupported("query group longer than 31 rows");
+  if (max_qgroup_len + 1 > 64) return unsupported("query group longer than 63 rows");
   // head rows go through the band kernel's head-rows-only mode: same link envelope
   for (int x : {L.w[0][0], L.w[0][1], L.w[0][2], L.w[1][0], L.w[1][1], L.w[1][2]})
     if (x != SC_LINK_FULL && x != SC_LINK_NONE) return unsupported("windowed head-row link");
@@ -668,7 +671,7 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   // workspace = [band-kernel records (head rows) | tile prefixes | QDS compact rows]
   const size_t band_bytes = (band_workspace_bytes(a.nseq, a.T, a.H, a.d, tile_rows, max_qgroup_len, L) + 255) & ~size_t(255);
   if (!ws || ws_bytes < band_bytes + tc_prefix_bytes(a.nseq, a.T)) return unsupported("workspace too small");
-  const size_t row_bytes = (size_t)3 * a.H * D * sizeof(__nv_bfloat16);
+  const size_t row_bytes = (size_t)3 * a.H * a.d * sizeof(__nv_bfloat16);
   const int cap = qds ? (int)((ws_bytes - band_bytes - tc_prefix_bytes(a.nseq, a.T)) / row_bytes) : 0;
 
   // Variant choice (env SC_TC_VARIANT = 0/1/2 forces VLONG/VMID/VMID32, for measurement sweeps).
@@ -679,9 +682,11 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   }
   const bool long_range = w == SC_LINK_FULL || w > 256;
   const bool small_gr = max_qgroup_len + 1 <= 16;
+  const bool big_gr = max_qgroup_len + 1 > 32;
   int var = forced >= 0 ? forced : (long_range ? 0 : (small_gr ? 1 : 2));
   if (var == 1 && !small_gr) var = 2;
-  const int64_t cols = (int64_t)a.H * D;
+  if (big_gr) var = 3;
+  const int64_t cols = (int64_t)a.H * a.d;
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   int32_t* tbase = reinterpret_cast<int32_t*>(wsb + band_bytes);
   int32_t* gtbase = tbase + a.nseq + 1;
@@ -690,21 +695,24 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   __nv_bfloat16* compact = reinterpret_cast<__nv_bfloat16*>(wsb + band_bytes + tc_prefix_bytes(a.nseq, a.T));
   const int64_t cld = 3 * cols;  // compact row stride (elements)
   auto build_maps = [&](CUtensorMap* maps, int v, bool global_rows) {
-    const int bn = v == 0 ? 64 : 32, gr = v == 1 ? 16 : 32;
+    const int bn = (v == 0 || v == 3) ? 64 : 32, gr = v == 1 ? 16 : (v == 3 ? 64 : 32);
     const int crow = cap > 0 ? cap : 1;
-    bool ok = global_rows ? make_map(&maps[0], compact, cols, crow, cld, BM) : make_map(&maps[0], a.q, cols, a.T, a.ld, BM);
-    ok = ok && make_map(&maps[1], a.k, cols, a.T, a.ld, gr) && make_map(&maps[2], a.v, cols, a.T, a.ld, gr) &&
-         make_map(&maps[3], a.k, cols, a.T, a.ld, bn) && make_map(&maps[4], a.v, cols, a.T, a.ld, bn);
-    ok = ok && make_map(&maps[7], a.q, cols, a.T, a.ld, gr);
-    if (qds) ok = ok && make_map(&maps[5], compact + cols, cols, crow, cld, bn) &&
-                  make_map(&maps[6], compact + 2 * cols, cols, crow, cld, bn);
+    const int dd = a.d, H = a.H;
+    bool ok = global_rows ? make_map_heads(&maps[0], compact, dd, H, crow, cld, BM)
+                          : make_map_heads(&maps[0], a.q, dd, H, a.T, a.ld, BM);
+    ok = ok && make_map_heads(&maps[1], a.k, dd, H, a.T, a.ld, gr) && make_map_heads(&maps[2], a.v, dd, H, a.T, a.ld, gr) &&
+         make_map_heads(&maps[3], a.k, dd, H, a.T, a.ld, bn) && make_map_heads(&maps[4], a.v, dd, H, a.T, a.ld, bn);
+    ok = ok && make_map_heads(&maps[7], a.q, dd, H, a.T, a.ld, gr);
+    if (qds) ok = ok && make_map_heads(&maps[5], compact + cols, dd, H, crow, cld, bn) &&
+                  make_map_heads(&maps[6], compact + 2 * cols, dd, H, crow, cld, bn);
     else { maps[5] = maps[3]; maps[6] = maps[4]; }
     return ok;
   };
   auto launch_var = [&](int v, dim3 grid, const CUtensorMap* maps, const Params& p) {
     return v == 0 ? launch_kernel<VLONG>(grid, maps, p, st)
          : v == 1 ? launch_kernel<VMID>(grid, maps, p, st)
-                  : launch_kernel<VMID32>(grid, maps, p, st);
+         : v == 2 ? launch_kernel<VMID32>(grid, maps, p, st)
+                  : launch_kernel<VG64>(grid, maps, p, st);
   };
 
   if (qds) {
@@ -725,7 +733,7 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   p.link_cls = L.w[2][0] == SC_LINK_FULL; p.link_query = L.w[2][1] == SC_LINK_FULL;
   p.c2 = 1.4426950408889634f / a.scale;
   p.cu = a.cu; p.qlen = a.qlen; p.tile_base = tbase; p.tile_seq = tseq;
-  p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
+  p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out; p.dout = a.d;
   p.qds = qds ? 1 : 0; p.global_rows = 0;
   p.flags = a.flags; p.glob_cu = a.glob_cu; p.glob_pos = a.glob_pos;
   // head rows folded into the doc-rows pass (records in the band kernel's workspace layout)
@@ -748,7 +756,7 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
     // QDS global doc rows: every key of their sequence (R/attention.py:461-470)
     Params pg = p;
     pg.qds = 0; pg.global_rows = 1; pg.tile_base = gtbase; pg.tile_seq = gtseq; pg.link_cls = pg.link_query = 1; pg.fold = 0;
-    const int vg = forced >= 0 ? var : 0;
+    const int vg = forced >= 0 ? var : (big_gr ? 3 : 0);
     CUtensorMap gmaps[8];
     if (!build_maps(gmaps, vg, true)) return unsupported("cuTensorMapEncodeTiled failed");
     rc = launch_var(vg, dim3((unsigned)((cap + BM - 1) / BM + a.nseq), (unsigned)a.H), gmaps, pg);

@@ -41,6 +41,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
+// 3-D [rows][heads][d] tensor maps with 64-dim boxes (make_map_heads): a 32-dim head arrives
+// zero-padded in a 64-dim smem row (the out-of-bounds half of the box is zero-filled).
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int head, int row, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(head), "r"(row), "r"(bar)
+      : "memory");
+}
 
 // ---- tcgen05 helpers -------------------------------------------------------
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -186,6 +194,27 @@ inline bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t row
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+
+// [rows][heads][d] bf16 (row stride ld elements) as a 3-D map, boxes of 64 dims x 1 head x box_rows
+// rows, 128B swizzle (d = 32: the upper half of every box row is zero-filled).
+inline bool make_map_heads(CUtensorMap* m, const void* base, int d, int heads, int64_t rows, int64_t ld, int box_rows) {
+  static EncodeFn enc = nullptr;
+  if (!enc) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    enc = reinterpret_cast<EncodeFn>(ptr);
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)heads, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {(cuuint64_t)(d * 2), (cuuint64_t)(ld * 2)};
+  cuuint32_t box[3] = {64u, 1u, (cuuint32_t)box_rows};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 }  // namespace tcx
 }  // namespace sc

