@@ -70,6 +70,7 @@ struct Params {
   int dout;  // head_dim (32 or 64; operands are staged as 64 zero-padded dims)
   // head-row fold (fold = 1; 0 in the QDS global-rows pass)
   int fold, fneed, fmax, ntiles_max;
+  int fold_skip;  // measurement only (SC_TC_FOLD_SKIP=1): the head-row lanes skip their math (wrong head rows)
   int hl[2][2], hdoc[2];        // head group (cls, query) -> cls / query key links; FULL doc link
   const int32_t* tile64;        // 64-row doc-tile prefix (record index of a 64-key half)
   float* partials;              // records (m, l, pad, pad, acc[64]) x fmax x H per 64-row tile
@@ -327,13 +328,13 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
     } else {
       const HeadRows<C> hr(p, smem, sm0, lane, h, j, g, n_doc, r0);
       mbar_wait(qbar, 0);
-      if (r0 == 0) hr.global_keys();
+      if (r0 == 0 && !p.fold_skip) hr.global_keys();
       const int own0 = ngd + (r0 - lo) / BN;          // first ring block of the own keys
       const int nown = (min(BM, n_doc - r0) + BN - 1) / BN;
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % NS;
         mbar_wait(full_bar + 8 * s, (kb / NS) & 1);
-        if (kb >= own0 && kb < own0 + nown) hr.own_block(sm0 + SM::KV + s * SM::STAGE, (kb - own0) * BN);
+        if (kb >= own0 && kb < own0 + nown && !p.fold_skip) hr.own_block(sm0 + SM::KV + s * SM::STAGE, (kb - own0) * BN);
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(empty_bar + 8 * s);
@@ -358,18 +359,20 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
       const uint64_t qd = sw128_desc(sm0 + SM::Q);
       auto issue_qk = [&](int b) {
         const uint32_t tS = tmem + S_COL + (b % NBUF) * BN;
-        if (has_glob && b == 0) {
-          const uint64_t kd = sw128_desc(sm0 + SM::KG);
-#pragma unroll
-          for (int ks = 0; ks < D / 16; ++ks) mma_ss(tS, qd + 2 * ks, kd + 2 * ks, id_qg, ks > 0);
-        } else {
+        // one issue site for both block kinds (operands chosen first): with two tcgen05.mma
+        // sites under divergent branches ptxas was seen to leave one copy's uniform operands
+        // unset when GR == BN (VMID32: wrong S, or an illegal-instruction trap)
+        uint32_t kaddr = sm0 + SM::KG, idq = id_qg;
+        if (!(has_glob && b == 0)) {
           const int kb = b - (has_glob ? 1 : 0), s = kb % NS;
           mbar_wait(full_bar + 8 * s, (kb / NS) & 1);
           tc_fence_after();
-          const uint64_t kd = sw128_desc(sm0 + SM::KV + s * SM::STAGE);
-#pragma unroll
-          for (int ks = 0; ks < D / 16; ++ks) mma_ss(tS, qd + 2 * ks, kd + 2 * ks, id_qk, ks > 0);
+          kaddr = sm0 + SM::KV + s * SM::STAGE;
+          idq = id_qk;
         }
+        const uint64_t kd = sw128_desc(kaddr);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) mma_ss(tS, qd + 2 * ks, kd + 2 * ks, idq, ks > 0);
         tc_commit(s_full + 8 * (b % NBUF));
       };
       issue_qk(0);
@@ -379,17 +382,14 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
         mbar_wait(p_full + 8 * buf, (b / NBUF) & 1);
         tc_fence_after();
         const uint32_t tS = tmem + S_COL + buf * BN;
-        if (has_glob && b == 0) {
-          const uint64_t vd = sw128_desc(sm0 + SM::VG);
+        const bool gblk = has_glob && b == 0;
+        const int kb = b - (has_glob ? 1 : 0), s = kb % NS;
+        const uint64_t vd = sw128_desc(gblk ? sm0 + SM::VG : sm0 + SM::KV + s * SM::STAGE + BN * ROWB);
+        const int nks = gblk ? GR / 16 : BN / 16;
 #pragma unroll
-          for (int ks = 0; ks < GR / 16; ++ks) mma_ts(tO, tS + 8 * ks, vd + 128 * ks, id_pv, ks > 0);
-        } else {
-          const int kb = b - (has_glob ? 1 : 0), s = kb % NS;
-          const uint64_t vd = sw128_desc(sm0 + SM::KV + s * SM::STAGE + BN * ROWB);
-#pragma unroll
-          for (int ks = 0; ks < BN / 16; ++ks) mma_ts(tO, tS + 8 * ks, vd + 128 * ks, id_pv, (b > 0 || ks > 0));
-          tc_commit(empty_bar + 8 * s);
-        }
+        for (int ks = 0; ks < (GR > BN ? GR : BN) / 16; ++ks)
+          if (ks < nks) mma_ts(tO, tS + 8 * ks, vd + 128 * ks, id_pv, (b > 0 || ks > 0));
+        if (!gblk) tc_commit(empty_bar + 8 * s);
         tc_commit(pv_done + 8 * buf);
         if (b + NBUF < nblocks) {
           mbar_wait(pv_done + 8 * buf, (b / NBUF) & 1);  // P(b) consumed: S buffer free
@@ -739,6 +739,7 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   // head rows folded into the doc-rows pass (records in the band kernel's workspace layout)
   const int fneed = full_rows_needed(L, max_qgroup_len);
   p.fold = 1; p.fneed = fneed; p.fmax = fneed > 0 ? fneed : 1;
+  p.fold_skip = getenv("SC_TC_FOLD_SKIP") ? atoi(getenv("SC_TC_FOLD_SKIP")) : 0;
   p.ntiles_max = (int)((a.T + tile_rows - 1) / tile_rows + a.nseq);
   for (int gsrc = 0; gsrc < 2; ++gsrc) {
     p.hl[gsrc][0] = L.w[gsrc][0] == SC_LINK_FULL;
