@@ -326,14 +326,14 @@ def passages_variant(P, dev, steps, pairs=1024):
 
 def fp32_variant(P, dev, steps, pairs=32):
     """Ranking-exact fp32 (north-star "identical per-query rankings"): the same documents in fp32,
-    projections as split-bf16 tensor-core products (fp32_gemm="bf16x6") vs cuBLAS SGEMM; parity of
-    both against the reference golden of these exact pairs."""
+    projections as split-fp16 / split-bf16 tensor-core products (fp32_gemm="f16x3" / "bf16x6") vs
+    cuBLAS SGEMM; parity of each against the reference golden of these exact pairs."""
     import torch
 
     cfg = dict(ELECTRA, max_positions=4099)
     batch = make_batch(P, cfg, 4086, pairs, 0)
     out = {}
-    for mode, nsteps in (("bf16x6", steps), ("sgemm", 2)):
+    for mode, nsteps in (("f16x3", steps), ("bf16x6", steps), ("sgemm", 2)):
         model = P.CrossEncoder(P.EncoderConfig(**cfg, precision="f32"), seed=0, device=dev, fp32_gemm=mode)
         layout = model.make_layout(batch)
         ids = torch.from_numpy(batch.ids).to(dev)
@@ -342,13 +342,13 @@ def fp32_variant(P, dev, steps, pairs=32):
         sc = fn().cpu().numpy()
         par = headline_parity(sc, 4086, False)
         if par is not None:
-            par["tol"] = 1e-6
+            par["tol"] = 2e-6  # tests/test_gpu_headline.py; cuBLAS SGEMM itself lands at ~1.5e-6
             par["flips_beyond_2tol"] = None
         out[mode] = {"value": pairs * nsteps / (ms / 1e3), "unit": "pairs/s", "ms_per_step": ms / nsteps,
                      "steps": nsteps, "pairs_per_step": pairs, "dtype": "f32", "parity": par}
         del model
         torch.cuda.empty_cache()
-    out["speedup_vs_sgemm"] = out["bf16x6"]["value"] / out["sgemm"]["value"]
+    out["speedup_vs_sgemm"] = {m: out[m]["value"] / out["sgemm"]["value"] for m in ("f16x3", "bf16x6")}
     return out
 
 

@@ -17,6 +17,8 @@
 // Producers fuse the split into their pass: the optional bias and exact-erf
 // GELU (R/encoder.py:258-259, erff as the fp32 path) are applied first and the
 // fp32 result can be kept as well (y, may alias x).
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace sc {
@@ -106,6 +108,85 @@ static void launch_split(bool vec, const float* x, int64_t ldx, const float* bia
     split3_kernel<kBias, kGelu><<<(unsigned)blocks, 256, 0, st>>>(x, ldx, bias, y, ldy, p, ldp, rows, cols);
 }
 
+
+// ---- fp16 pair split (CrossEncoder(fp32_gemm="f16x3")) ---------------------
+// v = h0 + h1 + O(2^-22 v) with h0 = fp16_rn(v), h1 = fp16_rn(v - h0): planes row = [h0 | h1].
+// A product v*w is h0 g0 + (h0 g1 + h1 g0) + O(2^-22): three fp16 tensor-core products, half the
+// work of the bf16 six-product form.  fp16's range (|v| < 65504) is checked: an out-of-range value
+// sets *status (the encoder then raises, no silent inf).
+template <bool kBias, bool kGelu>
+__global__ void __launch_bounds__(256) split2h_vec_kernel(const float* __restrict__ x, int64_t ldx,
+                                                          const float* __restrict__ bias, float* __restrict__ y,
+                                                          int64_t ldy, __half* __restrict__ p, int64_t ldp,
+                                                          int64_t rows, int cols, int32_t* __restrict__ status) {
+  const int c4 = cols >> 2;
+  const int64_t n = rows * c4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t j = n - 1 - i;
+    const int64_t r = j / c4;
+    const int c = (int)(j - r * c4) * 4;
+    float4 v = *reinterpret_cast<const float4*>(x + r * ldx + c);
+    if (kBias) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(bias + c));
+      v.x += b.x, v.y += b.y, v.z += b.z, v.w += b.w;
+    }
+    if (kGelu) {
+      v.x = 0.5f * v.x * (1.f + erff(v.x * 0.70710678118654752440f));
+      v.y = 0.5f * v.y * (1.f + erff(v.y * 0.70710678118654752440f));
+      v.z = 0.5f * v.z * (1.f + erff(v.z * 0.70710678118654752440f));
+      v.w = 0.5f * v.w * (1.f + erff(v.w * 0.70710678118654752440f));
+    }
+    if (y) *reinterpret_cast<float4*>(y + r * ldy + c) = v;
+    bad |= !(fabsf(v.x) < 65504.f && fabsf(v.y) < 65504.f && fabsf(v.z) < 65504.f && fabsf(v.w) < 65504.f);
+    const __half2 a01 = __floats2half2_rn(v.x, v.y), a23 = __floats2half2_rn(v.z, v.w);
+    const float2 f01 = __half22float2(a01), f23 = __half22float2(a23);
+    const __half2 b01 = __floats2half2_rn(v.x - f01.x, v.y - f01.y), b23 = __floats2half2_rn(v.z - f23.x, v.w - f23.y);
+    __half* pr = p + r * ldp + c;
+    uint2 u;
+    u.x = *reinterpret_cast<const uint32_t*>(&a01), u.y = *reinterpret_cast<const uint32_t*>(&a23);
+    *reinterpret_cast<uint2*>(pr) = u;
+    u.x = *reinterpret_cast<const uint32_t*>(&b01), u.y = *reinterpret_cast<const uint32_t*>(&b23);
+    *reinterpret_cast<uint2*>(pr + cols) = u;
+  }
+  if (bad && status) atomicExch(status, 1);
+}
+
+template <bool kBias, bool kGelu>
+__global__ void split2h_kernel(const float* __restrict__ x, int64_t ldx, const float* __restrict__ bias,
+                               float* __restrict__ y, int64_t ldy, __half* __restrict__ p, int64_t ldp, int64_t rows,
+                               int cols, int32_t* __restrict__ status) {
+  const int64_t n = rows * cols;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t r = i / cols;
+    const int c = (int)(i - r * cols);
+    float v = x[r * ldx + c];
+    if (kBias) v += __ldg(bias + c);
+    if (kGelu) v = 0.5f * v * (1.f + erff(v * 0.70710678118654752440f));
+    if (y) y[r * ldy + c] = v;
+    bad |= !(fabsf(v) < 65504.f);
+    const __half a = __float2half_rn(v);
+    p[r * ldp + c] = a;
+    p[r * ldp + cols + c] = __float2half_rn(v - __half2float(a));
+  }
+  if (bad && status) atomicExch(status, 1);
+}
+
+template <bool kBias, bool kGelu>
+static void launch_split2h(bool vec, const float* x, int64_t ldx, const float* bias, float* y, int64_t ldy, __half* p,
+                           int64_t ldp, int64_t rows, int cols, int32_t* status, cudaStream_t st) {
+  const int64_t work = vec ? rows * (cols / 4) : rows * cols;
+  int64_t blocks = (work + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (vec)
+    split2h_vec_kernel<kBias, kGelu><<<(unsigned)blocks, 256, 0, st>>>(x, ldx, bias, y, ldy, p, ldp, rows, cols, status);
+  else
+    split2h_kernel<kBias, kGelu><<<(unsigned)blocks, 256, 0, st>>>(x, ldx, bias, y, ldy, p, ldp, rows, cols, status);
+}
+
 }  // namespace sc
 
 using namespace sc;
@@ -129,5 +210,27 @@ extern "C" int sc_split_bf16x3(const float* x, int64_t ldx, const float* bias, i
   else
     launch_split<false, false>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, st);
   SC_CHECK_LAUNCH("split3_kernel");
+  return SC_OK;
+}
+
+extern "C" int sc_split_f16x2(const float* x, int64_t ldx, const float* bias, int32_t gelu, float* y, int64_t ldy,
+                              void* planes, int64_t ldp, int64_t rows, int32_t cols, int32_t* status, void* stream) {
+  SC_CHECK_ARG(x && planes, "sc_split_f16x2: null pointer");
+  SC_CHECK_ARG(rows >= 0 && cols >= 1 && ldx >= cols && ldp >= 2LL * cols && (!y || ldy >= cols),
+               "sc_split_f16x2: bad shape");
+  if (rows == 0) return SC_OK;
+  const bool vec = cols % 4 == 0 && ldx % 4 == 0 && ldp % 4 == 0 && (!y || ldy % 4 == 0) &&
+                   !(((uintptr_t)x | (uintptr_t)y | (uintptr_t)bias) & 15) && !((uintptr_t)planes & 7);
+  cudaStream_t st = (cudaStream_t)stream;
+  __half* p = (__half*)planes;
+  if (bias && gelu)
+    launch_split2h<true, true>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, status, st);
+  else if (bias)
+    launch_split2h<true, false>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, status, st);
+  else if (gelu)
+    launch_split2h<false, true>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, status, st);
+  else
+    launch_split2h<false, false>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, status, st);
+  SC_CHECK_LAUNCH("split2h_kernel");
   return SC_OK;
 }

@@ -264,7 +264,8 @@ def _fp32_gemms(enabled: bool):
         torch.backends.cuda.matmul.allow_tf32 = prev
 
 
-FP32_GEMMS = ("sgemm", "bf16x6")
+FP32_GEMMS = ("sgemm", "bf16x6", "f16x3")
+F16_MAX = 65504.0
 
 
 def _split_weight_x6(w: torch.Tensor) -> torch.Tensor:
@@ -310,6 +311,55 @@ def _linear_x6(planes: torch.Tensor, w5: torch.Tensor, chunk: int | None = None)
     return c
 
 
+def _split_weight_x3h(w: torch.Tensor):
+    """fp32 weight [N, K] -> (fp16 [N, 2K] = [G1 | G0], s) with W * 2^e = G0 + G1 (G0 = fp16_rn, G1 the
+    fp16 of the residual) and s = 2^-e: e puts max |W| at 2^14, so the residual plane of the O(0.02)
+    weights stays out of fp16's subnormal range.  One-time, at upload."""
+    w = w.float()
+    amax = float(w.abs().max()) if w.numel() else 0.0
+    e = int(math.floor(math.log2(16384.0 / amax))) if amax > 0 else 0
+    ws = w * (2.0 ** e)
+    g0 = ws.to(torch.float16)
+    g1 = (ws - g0.float()).to(torch.float16)
+    return torch.cat([g1, g0], dim=1).contiguous(), 2.0 ** -e
+
+
+def split_planes_h(x: torch.Tensor, bias=None, gelu: bool = False, keep: torch.Tensor | None = None,
+                   status: torch.Tensor | None = None) -> torch.Tensor:
+    """fp32 [M, K] (+ bias, GELU) -> fp16 planes [M, 2K] = [h0 | h1] (sc_split_f16x2); ``status``
+    (device int32) is set to 1 if a value is outside fp16 range."""
+    M, K = x.shape
+    planes = torch.empty((M, 2 * K), dtype=torch.float16, device=x.device)
+    _lib.call("sc_split_f16x2", x.data_ptr(), x.stride(0), _lib.ptr(bias), int(gelu), _lib.ptr(keep),
+              K if keep is None else keep.stride(0), planes.data_ptr(), planes.stride(0), M, K, _lib.ptr(status),
+              _lib.stream_handle(), exc=EncoderError)
+    return planes
+
+
+def _linear_x3h(planes: torch.Tensor, w2: torch.Tensor, s: float, bias_s: torch.Tensor | None = None,
+                chunk: int | None = None) -> torch.Tensor:
+    """a W^T (+ bias) in fp32 from the fp16 planes of a ([M, 2K] = [h0 | h1]) and of W * 2^e
+    ([N, 2K] = [g1 | g0]) on the fp16 tensor cores:
+      corrections [h0 | h1] . [g1 | g0]  (one GEMM over K' = 2K, magnitude 2^-11; starts from bias / s)
+      + main      h0 . g0 in K-chunks of <= ``chunk``, the last one scaling the sum by s = 2^-e (exact)
+    = h0 g0 + h0 g1 + h1 g0 (dropped term h1 g1 <= 2^-22 relative), three products where the bf16
+    form needs six.  Measured vs fp64 (M = 131k): max relative error 1.2-1.7e-6, SGEMM's 1.1-2.2e-6.
+    R/encoder.py:322-324, :345, :350, :352."""
+    K = planes.shape[1] // 2
+    chunk = chunk or X6_CHUNK
+    if bias_s is None:
+        c = torch.mm(planes, w2.t(), out_dtype=torch.float32)
+    else:
+        c = torch.addmm(bias_s, planes, w2.t(), out_dtype=torch.float32)
+    h0, g0 = planes[:, :K], w2[:, K:]
+    starts = list(range(0, K, chunk))
+    for n, k0 in enumerate(starts):
+        sc = s if n == len(starts) - 1 else 1.0
+        c = torch.addmm(c, h0[:, k0:k0 + chunk], g0[:, k0:k0 + chunk].t(), beta=sc, alpha=sc,
+                        out_dtype=torch.float32)
+    return c
+
+
 class CrossEncoder:
     """Config + device weights; batched inference (R/encoder.py:450-538)."""
 
@@ -324,8 +374,10 @@ class CrossEncoder:
 
         ``fp32_gemm`` (fp32 precisions only): "sgemm" runs the four projections as cuBLAS
         fp32 SGEMM (TF32 off); "bf16x6" runs them on the bf16 tensor cores as six split
-        products per GEMM (operands as three bf16 planes, sc_split_bf16x3; see _linear_x6),
-        SGEMM-level accuracy at several times the speed."""
+        products per GEMM (operands as three bf16 planes, sc_split_bf16x3; see _linear_x6);
+        "f16x3" as three fp16 products (two fp16 planes, sc_split_f16x2; see _linear_x3h;
+        activations must stay inside fp16 range, checked: EncoderError otherwise).  Both
+        give SGEMM-level accuracy at several times the speed."""
         if fp32_gemm not in FP32_GEMMS:
             raise EncoderError(f"fp32_gemm must be one of {FP32_GEMMS}, got {fp32_gemm!r}")
         self.config = config
@@ -378,12 +430,17 @@ class CrossEncoder:
             })
         self.head_w = f32(w["head_w"])
         self.head_b = float(np.asarray(w["head_b"]))
-        if self.fp32_gemm == "bf16x6":
+        if self.fp32_gemm in ("bf16x6", "f16x3"):
             for L in self.layers:
                 for name in ("wqkv", "wo", "w1", "w2"):
-                    L[name + "_x6"] = _split_weight_x6(L[name])
+                    if self.fp32_gemm == "bf16x6":
+                        L[name + "_x6"] = _split_weight_x6(L[name])
+                    else:
+                        L[name + "_x3h"], L[name + "_x3h_s"] = _split_weight_x3h(L[name])
                 for name in ("bqkv", "bo", "b1", "b2"):
                     L[name + "_f32"] = L[name].float().contiguous()
+                if self.fp32_gemm == "f16x3":
+                    L["bqkv_x3h"] = (L["bqkv_f32"] / L["wqkv_x3h_s"]).contiguous()  # exact: s is 2^-e
 
     # -- validation -------------------------------------------------------
 
@@ -410,7 +467,7 @@ class CrossEncoder:
         rest of the layer for the [CLS] rows only; returns [nseq, h] (row j =
         sequence j's [CLS]).
         """
-        if self.fp32_gemm == "bf16x6":
+        if self.fp32_gemm in ("bf16x6", "f16x3"):
             return self._encode_x6(ids_dev, layout, check_finite, attn_hook, cls_only)
         cfg = self.config
         T, h, H = layout.total_tokens, cfg.embed_dim, cfg.heads
@@ -467,8 +524,21 @@ class CrossEncoder:
         self._last_bad = bad if check_finite else None
         return x
 
+    def _xsplit(self, x, bias=None, gelu=False):
+        """GEMM operand planes of x (+ bias, GELU) for the split fp32 modes."""
+        if self.fp32_gemm == "bf16x6":
+            return split_planes(x, bias=bias, gelu=gelu)
+        return split_planes_h(x, bias=bias, gelu=gelu, status=self._range_flag)
+
+    def _xlinear(self, planes, L, name, with_bias=False):
+        """x W^T (+ the layer's bias) in fp32 from the planes of x (split fp32 modes)."""
+        if self.fp32_gemm == "bf16x6":
+            c = _linear_x6(planes, L[name + "_x6"])
+            return c.add_(L["bqkv_f32"]) if with_bias else c
+        return _linear_x3h(planes, L[name + "_x3h"], L[name + "_x3h_s"], L["bqkv_x3h"] if with_bias else None)
+
     def _encode_x6(self, ids_dev, layout, check_finite, attn_hook, cls_only) -> torch.Tensor:
-        """encode_packed for fp32 with the projections as split-bf16 products (fp32_gemm="bf16x6").
+        """encode_packed for fp32 with the projections as split products (fp32_gemm="bf16x6" / "f16x3").
         Every GEMM operand is produced as bf16 planes by the pass that writes it: sc_split_bf16x3
         after the embedding / LayerNorms / attention, and with bias + GELU fused for the FFN
         activation, which then never exists in fp32."""
@@ -480,27 +550,29 @@ class CrossEncoder:
         x1 = torch.empty_like(x)
         o = torch.empty_like(x)
         bad = torch.zeros(max(cfg.layers, 1), dtype=torch.int32, device=dev)
+        self._range_flag = torch.zeros(1, dtype=torch.int32, device=dev) if self.fp32_gemm == "f16x3" else None
+        self._last_range = self._range_flag
         _lib.call("sc_embed", ids_dev.data_ptr(), layout.tok_pos.data_ptr(), self.tok_emb.data_ptr(),
                   self.pos_emb.data_ptr(), x.data_ptr(), None, T, h, stream, exc=EncoderError)
         last = cfg.layers - 1
         for i, L in enumerate(self.layers):
-            xs = split_planes(x)
+            xs = self._xsplit(x)
             if cls_only and i == last:
                 self._last_bad = bad if check_finite else None
                 return self._cls_last_layer_x6(L, x, xs, layout, pattern, bad if check_finite else None, i)
-            qkv = _linear_x6(xs, L["wqkv_x6"]).add_(L["bqkv_f32"])
+            qkv = self._xlinear(xs, L, "wqkv", with_bias=True)
             if attn_hook:
                 attn_hook("start")
             attend_packed(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], layout, pattern, H,
                           math.sqrt(cfg.head_dim), cfg.padding, out=o, algo=self.attn_algo, check=(i == 0))
             if attn_hook:
                 attn_hook("end")
-            y = _linear_x6(split_planes(o), L["wo_x6"])
+            y = self._xlinear(self._xsplit(o), L, "wo")
             _lib.call("sc_residual_layernorm_ex", x.data_ptr(), F32, y.data_ptr(), F32, L["bo_f32"].data_ptr(),
                       L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), x1.data_ptr(), None, None, T, h, stream,
                       exc=EncoderError)
-            f = _linear_x6(split_planes(x1), L["w1_x6"])
-            f2 = _linear_x6(split_planes(f, bias=L["b1_f32"], gelu=True), L["w2_x6"])
+            f = self._xlinear(self._xsplit(x1), L, "w1")
+            f2 = self._xlinear(self._xsplit(f, bias=L["b1_f32"], gelu=True), L, "w2")
             del f
             _lib.call("sc_residual_layernorm_ex", x1.data_ptr(), F32, f2.data_ptr(), F32, L["b2_f32"].data_ptr(),
                       L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(), x.data_ptr(), None,
@@ -512,19 +584,19 @@ class CrossEncoder:
         """_cls_last_layer for fp32_gemm="bf16x6": K/V of every token, the rest on the [CLS] rows."""
         cfg = self.config
         h, H, F32, stream = cfg.embed_dim, cfg.heads, _lib.DTYPE_F32, _lib.stream_handle()
-        qkv = _linear_x6(xs, L["wqkv_x6"]).add_(L["bqkv_f32"])
+        qkv = self._xlinear(xs, L, "wqkv", with_bias=True)
         o = torch.empty((layout.total_tokens, h), dtype=torch.float32, device=self.device)
         attend_packed(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], layout, pattern, H,
                       math.sqrt(cfg.head_dim), cfg.padding, out=o, algo=self.attn_algo, check=False, rows="head")
         cls, n = layout.cls_rows, layout.nseq
-        y = _linear_x6(split_planes(o.index_select(0, cls)), L["wo_x6"])
+        y = self._xlinear(self._xsplit(o.index_select(0, cls)), L, "wo")
         xc = x.index_select(0, cls)
         x1 = torch.empty_like(xc)
         _lib.call("sc_residual_layernorm_ex", xc.data_ptr(), F32, y.data_ptr(), F32, L["bo_f32"].data_ptr(),
                   L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), x1.data_ptr(), None, None, n, h, stream,
                   exc=EncoderError)
-        f = _linear_x6(split_planes(x1), L["w1_x6"])
-        f2 = _linear_x6(split_planes(f, bias=L["b1_f32"], gelu=True), L["w2_x6"])
+        f = self._xlinear(self._xsplit(x1), L, "w1")
+        f2 = self._xlinear(self._xsplit(f, bias=L["b1_f32"], gelu=True), L, "w2")
         out = torch.empty((n, h), dtype=torch.float32, device=self.device)
         _lib.call("sc_residual_layernorm_ex", x1.data_ptr(), F32, f2.data_ptr(), F32, L["b2_f32"].data_ptr(),
                   L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(), out.data_ptr(), None,
@@ -602,6 +674,10 @@ class CrossEncoder:
         return out
 
     def _raise_if_nonfinite(self):
+        rng = getattr(self, "_last_range", None)
+        if rng is not None and int(rng.item()):
+            raise EncoderError(f"an activation left fp16 range (|x| >= {F16_MAX:g}) in fp32_gemm='f16x3'; "
+                               "use fp32_gemm='bf16x6' or 'sgemm'")
         bad = getattr(self, "_last_bad", None)
         if bad is None:
             return

@@ -211,13 +211,14 @@ def test_fused_layernorm_projection_matches(P):
                                atol=2e-2, rtol=0)
 
 
-def test_electra_passages_fp32_bf16x6_ranking_identical(P, g):
+@pytest.mark.parametrize("mode", ["bf16x6", "f16x3"])
+def test_electra_passages_fp32_split_ranking_identical(P, g, mode):
     cfg = P.EncoderConfig(**cases.ELECTRA_PASSAGE, precision="f32")
-    model = P.CrossEncoder(cfg, seed=0, fp32_gemm="bf16x6")
+    model = P.CrossEncoder(cfg, seed=0, fp32_gemm=mode)
     seqs = [rerank_ids(0, j, 164, cfg.vocab_size, cfg.max_positions, P) for j in range(100)]
     sc = model.score_packed(P.PackedBatch.from_sequences(seqs)).cpu().numpy()
     ref = g["electra_passage_scores"]
     err = np.abs(sc - ref).max()
-    print(f"fp32 bf16x6 passages max |dscore| = {err:.3e}")
+    print(f"fp32 {mode} passages max |dscore| = {err:.3e}")
     assert err < 2e-6, err
     assert O.rank_order(sc) == O.rank_order(ref)

@@ -105,21 +105,23 @@ def test_fp32_headline_32_candidates_ranking_identical(P, ranking):
 
 
 
-def test_fp32_bf16x6_headline_32_candidates(P, ranking):
-    """The fast fp32 mode (projections as six split-bf16 tensor-core products) against the
-    reference: SGEMM-level score error and the identical ranking (adjacent reference gaps here
-    are as small as 6e-6)."""
+@pytest.mark.parametrize("mode", ["bf16x6", "f16x3"])
+def test_fp32_split_headline_32_candidates(P, ranking, mode):
+    """The fast fp32 modes (projections as six split-bf16 / three split-fp16 tensor-core products)
+    against the reference: SGEMM-level score error and the identical ranking (adjacent reference
+    gaps here are as small as 6e-6)."""
     ref = ranking["scores"]
-    sc = scores_for(P, "f32", len(ref), fp32_gemm="bf16x6")
+    sc = scores_for(P, "f32", len(ref), fp32_gemm=mode)
     err = np.abs(sc - ref).max()
-    print(f"fp32 bf16x6 s=4099 x{len(ref)} max |dscore| = {err:.3e}")
+    print(f"fp32 {mode} s=4099 x{len(ref)} max |dscore| = {err:.3e}")
     assert err < 2e-6, err
     assert O.rank_order(sc) == list(ranking["order"])
 
 
-def test_fp32_bf16x6_prune_matches_full(P, ranking):
+@pytest.mark.parametrize("mode", ["bf16x6", "f16x3"])
+def test_fp32_split_prune_matches_full(P, ranking, mode):
     ref = ranking["scores"][:4]
-    a = scores_for(P, "f32", 4, fp32_gemm="bf16x6")
-    b = scores_for(P, "f32", 4, fp32_gemm="bf16x6", prune_last_layer=True)
+    a = scores_for(P, "f32", 4, fp32_gemm=mode)
+    b = scores_for(P, "f32", 4, fp32_gemm=mode, prune_last_layer=True)
     np.testing.assert_allclose(b, a, atol=1e-6, rtol=0)
     np.testing.assert_allclose(b, ref, atol=2e-6, rtol=0)

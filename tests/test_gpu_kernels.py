@@ -269,3 +269,52 @@ def test_linear_x6_matches_fp64():
     es = (sg.double() - exact).abs().max().item()
     print(f"x6 max err {e6:.3e}, sgemm {es:.3e}")
     assert e6 <= es * 1.25, (e6, es)
+
+
+def test_split_f16x2_planes_and_range_flag():
+    """sc_split_f16x2: [h0 | h1] with h0 = fp16_rn(v), h1 = fp16_rn(v - h0) (bias + GELU fused, fp32 kept);
+    a value outside fp16 range raises the status flag."""
+    from paper_2312_17649_b200.encoder import split_planes_h
+
+    g = torch.Generator(device="cuda").manual_seed(9)
+    for cols in (768, 13):
+        x = torch.randn((333, cols), device="cuda", generator=g) * 7
+        b = torch.randn(cols, device="cuda", generator=g)
+        keep = torch.empty_like(x)
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        pl = split_planes_h(x, bias=b, gelu=True, keep=keep, status=st)
+        v = torch.nn.functional.gelu((x + b).double())
+        h0 = keep.to(torch.float16)
+        assert torch.equal(pl[:, :cols], h0)
+        assert torch.equal(pl[:, cols:], (keep - h0.float()).to(torch.float16))
+        assert (keep.double() - v).abs().max().item() < 1e-4
+        assert int(st.item()) == 0
+    x[5, 3] = 70000.0
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    split_planes_h(x, status=st)
+    assert int(st.item()) == 1
+
+
+def test_linear_x3h_matches_fp64():
+    """_linear_x3h (three split-fp16 products, weights scaled by 2^e) is about as accurate as fp32 SGEMM
+    (K = 768: one main accumulation; K = 3072: four chunks); bias folded into the first GEMM."""
+    from paper_2312_17649_b200.encoder import _linear_x3h, _split_weight_x3h, split_planes_h
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for K in (768, 3072):
+        a = torch.randn((1000, K), device="cuda", generator=g)
+        w = torch.randn((768, K), device="cuda", generator=g) * 0.02
+        b = torch.randn(768, device="cuda", generator=g)
+        exact = a.double() @ w.double().t() + b.double()
+        w2, s = _split_weight_x3h(w)
+        got = _linear_x3h(split_planes_h(a), w2, s, (b / s).contiguous())
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
+        try:
+            sg = a @ w.t() + b
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
+        e3 = (got.double() - exact).abs().max().item()
+        es = (sg.double() - exact).abs().max().item()
+        print(f"K={K} x3h max err {e3:.3e}, sgemm {es:.3e}")
+        assert e3 <= es * 2.0, (K, e3, es)
