@@ -306,8 +306,8 @@ def _linear_x6(planes: torch.Tensor, w5: torch.Tensor, chunk: int | None = None)
     chunk = chunk or X6_CHUNK
     c = torch.mm(planes, w5.t(), out_dtype=torch.float32)
     p0, q0 = planes[:, 2 * K:3 * K], w5[:, :K]
-    for k0 in range(0, K, chunk):
-        c = torch.addmm(c, p0[:, k0:k0 + chunk], q0[:, k0:k0 + chunk].t(), out_dtype=torch.float32)
+    for k0 in range(0, K, chunk):  # in place (out=c): no copy of c per chunk
+        torch.addmm(c, p0[:, k0:k0 + chunk], q0[:, k0:k0 + chunk].t(), out_dtype=torch.float32, out=c)
     return c
 
 
@@ -353,10 +353,10 @@ def _linear_x3h(planes: torch.Tensor, w2: torch.Tensor, s: float, bias_s: torch.
         c = torch.addmm(bias_s, planes, w2.t(), out_dtype=torch.float32)
     h0, g0 = planes[:, :K], w2[:, K:]
     starts = list(range(0, K, chunk))
-    for n, k0 in enumerate(starts):
+    for n, k0 in enumerate(starts):  # in place (out=c): no copy of c per chunk
         sc = s if n == len(starts) - 1 else 1.0
-        c = torch.addmm(c, h0[:, k0:k0 + chunk], g0[:, k0:k0 + chunk].t(), beta=sc, alpha=sc,
-                        out_dtype=torch.float32)
+        torch.addmm(c, h0[:, k0:k0 + chunk], g0[:, k0:k0 + chunk].t(), beta=sc, alpha=sc,
+                    out_dtype=torch.float32, out=c)
     return c
 
 
