@@ -70,6 +70,7 @@ struct Params {
   int dout;  // head_dim (32 or 64; operands are staged as 64 zero-padded dims)
   // head-row fold (fold = 1; 0 in the QDS global-rows pass)
   int fold, fneed, fmax, ntiles_max;
+  int head_fast;  // grid (H, tiles) instead of (tiles, H)
   int fold_skip;  // measurement only (SC_TC_FOLD_SKIP=1): the head-row lanes skip their math (wrong head rows)
   int hl[2][2], hdoc[2];        // head group (cls, query) -> cls / query key links; FULL doc link
   const int32_t* tile64;        // 64-row doc-tile prefix (record index of a 64-key half)
@@ -241,7 +242,9 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
                 GR = C::GR;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int tile = blockIdx.x, h = blockIdx.y;
+  // grid (H, tiles): the 12 heads of a tile are dispatched together, so the CTAs in flight read
+  // whole 4.6 KB q|k|v rows of neighbouring tiles (L2 sectors of a row are shared, halos meet)
+  const int tile = p.head_fast ? blockIdx.y : blockIdx.x, h = p.head_fast ? blockIdx.x : blockIdx.y;
   if (tile >= __ldg(p.tile_base + p.nseq)) return;
   const int j = __ldg(p.tile_seq + tile);
   const SeqGroups g = seq_groups(p.cu, p.qlen, j);
@@ -327,14 +330,19 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
         }
     } else {
       const HeadRows<C> hr(p, smem, sm0, lane, h, j, g, n_doc, r0);
-      mbar_wait(qbar, 0);
-      if (r0 == 0 && !p.fold_skip) hr.global_keys();
       const int own0 = ngd + (r0 - lo) / BN;          // first ring block of the own keys
       const int nown = (min(BM, n_doc - r0) + BN - 1) / BN;
+      // Only the own-key blocks need the head-row lanes: the others are released (and their
+      // refills issued) as soon as the MMA has consumed them.  The global-key rows of the first
+      // tile come last, after the ring is done with this warp.
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % NS;
-        mbar_wait(full_bar + 8 * s, (kb / NS) & 1);
-        if (kb >= own0 && kb < own0 + nown && !p.fold_skip) hr.own_block(sm0 + SM::KV + s * SM::STAGE, (kb - own0) * BN);
+        const bool own = kb >= own0 && kb < own0 + nown;
+        if (own) {
+          mbar_wait(qbar, 0);  // QF (one-shot barrier: returns at once after the first time)
+          mbar_wait(full_bar + 8 * s, (kb / NS) & 1);
+          if (!p.fold_skip) hr.own_block(sm0 + SM::KV + s * SM::STAGE, (kb - own0) * BN);
+        }
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(empty_bar + 8 * s);
@@ -345,6 +353,8 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
         }
         __syncwarp();
       }
+      mbar_wait(qbar, 0);
+      if (r0 == 0 && !p.fold_skip) hr.global_keys();
     }
   } else if (warp == 5) {
     // ------------------------------------------------------------- MMA (one thread)
@@ -740,6 +750,7 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   const int fneed = full_rows_needed(L, max_qgroup_len);
   p.fold = 1; p.fneed = fneed; p.fmax = fneed > 0 ? fneed : 1;
   p.fold_skip = getenv("SC_TC_FOLD_SKIP") ? atoi(getenv("SC_TC_FOLD_SKIP")) : 0;
+  p.head_fast = getenv("SC_TC_HEAD_FAST") ? atoi(getenv("SC_TC_HEAD_FAST")) : 1;
   p.ntiles_max = (int)((a.T + tile_rows - 1) / tile_rows + a.nseq);
   for (int gsrc = 0; gsrc < 2; ++gsrc) {
     p.hl[gsrc][0] = L.w[gsrc][0] == SC_LINK_FULL;
@@ -751,7 +762,8 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   SC_CHECK_LAUNCH("tile128_prefix_kernel");
   CUtensorMap maps[8];
   if (!build_maps(maps, var, false)) return unsupported("cuTensorMapEncodeTiled failed");
-  int rc = launch_var(var, dim3((unsigned)((a.T + BM - 1) / BM + a.nseq), (unsigned)a.H), maps, p);
+  const unsigned ntile_grid = (unsigned)((a.T + BM - 1) / BM + a.nseq);
+  int rc = launch_var(var, p.head_fast ? dim3((unsigned)a.H, ntile_grid) : dim3(ntile_grid, (unsigned)a.H), maps, p);
   if (rc) return rc;
   if (qds && cap > 0) {
     // QDS global doc rows: every key of their sequence (R/attention.py:461-470)
@@ -760,7 +772,8 @@ int launch_attn_tc(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
     const int vg = forced >= 0 ? var : (big_gr ? 3 : 0);
     CUtensorMap gmaps[8];
     if (!build_maps(gmaps, vg, true)) return unsupported("cuTensorMapEncodeTiled failed");
-    rc = launch_var(vg, dim3((unsigned)((cap + BM - 1) / BM + a.nseq), (unsigned)a.H), gmaps, pg);
+    const unsigned gtile_grid = (unsigned)((cap + BM - 1) / BM + a.nseq);
+    rc = launch_var(vg, pg.head_fast ? dim3((unsigned)a.H, gtile_grid) : dim3(gtile_grid, (unsigned)a.H), gmaps, pg);
     if (rc) return rc;
   }
   // Head rows: the doc-rows pass left the split-softmax records; fold them into the

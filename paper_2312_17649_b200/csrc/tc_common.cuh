@@ -2,6 +2,7 @@
 // kernels (attn_tc.cu, attn_tc2.cu).
 #pragma once
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "attn.cuh"
 
@@ -197,6 +198,12 @@ inline bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t row
 
 // [rows][heads][d] bf16 (row stride ld elements) as a 3-D map, boxes of 64 dims x 1 head x box_rows
 // rows, 128B swizzle (d = 32: the upper half of every box row is zero-filled).
+// L2 promotion of the [rows][heads][d] maps (SC_TC_L2PROMO = 0 none / 1 128B / 2 256B; default 256B)
+inline CUtensorMapL2promotion heads_l2_promotion() {
+  static int v = -1;
+  if (v < 0) v = getenv("SC_TC_L2PROMO") ? atoi(getenv("SC_TC_L2PROMO")) : 2;
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
 inline bool make_map_heads(CUtensorMap* m, const void* base, int d, int heads, int64_t rows, int64_t ld, int box_rows) {
   static EncodeFn enc = nullptr;
   if (!enc) {
@@ -212,7 +219,7 @@ inline bool make_map_heads(CUtensorMap* m, const void* base, int d, int heads, i
   cuuint32_t box[3] = {64u, 1u, (cuuint32_t)box_rows};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, heads_l2_promotion(),
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
