@@ -335,12 +335,14 @@ SC_API int sc_split_bf16x3(const float* x, int64_t ldx, const float* bias, int32
                            void* planes, int64_t ldp, int64_t rows, int32_t cols, void* stream);
 
 /* fp32 GEMM operand -> two fp16 planes for the fast fp32 mode (CrossEncoder(fp32_gemm="f16x3"),
- * the same projections): v as above, y as above; planes row r = [h0 | h1] (row stride
- * ldp >= 2*cols) with h0 = fp16_rn(v), h1 = fp16_rn(v - h0), v = h0 + h1 + O(2^-22 |v|).
- * A value outside fp16 range (|v| >= 65504 or not finite) writes 1 to *status
- * (device int, may be NULL).  Strides in elements. */
+ * the same projections): v as above, y as above; planes row r = [h0 | h1] (onehot == 0) or
+ * [h0 | 1 0 0 0 0 0 0 0 | h1] (onehot != 0: a constant column that carries the projection's bias
+ * through the GEMM), row stride ldp >= 2*cols (+8), with h0 = fp16_rn(v), h1 = fp16_rn(v - h0),
+ * v = h0 + h1 + O(2^-22 |v|).  A value outside fp16 range (|v| >= 65504 or not finite) writes 1
+ * to *status (device int, may be NULL).  Strides in elements. */
 SC_API int sc_split_f16x2(const float* x, int64_t ldx, const float* bias, int32_t gelu, float* y, int64_t ldy,
-                          void* planes, int64_t ldp, int64_t rows, int32_t cols, int32_t* status, void* stream);
+                          void* planes, int64_t ldp, int64_t rows, int32_t cols, int32_t onehot, int32_t* status,
+                          void* stream);
 
 #ifdef __cplusplus
 }

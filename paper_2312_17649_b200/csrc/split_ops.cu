@@ -118,7 +118,8 @@ template <bool kBias, bool kGelu>
 __global__ void __launch_bounds__(256) split2h_vec_kernel(const float* __restrict__ x, int64_t ldx,
                                                           const float* __restrict__ bias, float* __restrict__ y,
                                                           int64_t ldy, __half* __restrict__ p, int64_t ldp,
-                                                          int64_t rows, int cols, int32_t* __restrict__ status) {
+                                                          int64_t rows, int cols, int h1_off, int onehot,
+                                                          int32_t* __restrict__ status) {
   const int c4 = cols >> 2;
   const int64_t n = rows * c4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -148,7 +149,8 @@ __global__ void __launch_bounds__(256) split2h_vec_kernel(const float* __restric
     u.x = *reinterpret_cast<const uint32_t*>(&a01), u.y = *reinterpret_cast<const uint32_t*>(&a23);
     *reinterpret_cast<uint2*>(pr) = u;
     u.x = *reinterpret_cast<const uint32_t*>(&b01), u.y = *reinterpret_cast<const uint32_t*>(&b23);
-    *reinterpret_cast<uint2*>(pr + cols) = u;
+    *reinterpret_cast<uint2*>(pr + h1_off) = u;
+    if (onehot && c == 0) *reinterpret_cast<uint4*>(p + r * ldp + cols) = make_uint4(0x3c00u, 0u, 0u, 0u);  // [1, 0 x 7]
   }
   if (bad && status) atomicExch(status, 1);
 }
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(256) split2h_vec_kernel(const float* __restric
 template <bool kBias, bool kGelu>
 __global__ void split2h_kernel(const float* __restrict__ x, int64_t ldx, const float* __restrict__ bias,
                                float* __restrict__ y, int64_t ldy, __half* __restrict__ p, int64_t ldp, int64_t rows,
-                               int cols, int32_t* __restrict__ status) {
+                               int cols, int h1_off, int onehot, int32_t* __restrict__ status) {
   const int64_t n = rows * cols;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   bool bad = false;
@@ -170,21 +172,25 @@ __global__ void split2h_kernel(const float* __restrict__ x, int64_t ldx, const f
     bad |= !(fabsf(v) < 65504.f);
     const __half a = __float2half_rn(v);
     p[r * ldp + c] = a;
-    p[r * ldp + cols + c] = __float2half_rn(v - __half2float(a));
+    p[r * ldp + h1_off + c] = __float2half_rn(v - __half2float(a));
+    if (onehot && c < 8) p[r * ldp + cols + c] = __float2half_rn(c == 0 ? 1.f : 0.f);
   }
   if (bad && status) atomicExch(status, 1);
 }
 
 template <bool kBias, bool kGelu>
 static void launch_split2h(bool vec, const float* x, int64_t ldx, const float* bias, float* y, int64_t ldy, __half* p,
-                           int64_t ldp, int64_t rows, int cols, int32_t* status, cudaStream_t st) {
+                           int64_t ldp, int64_t rows, int cols, int h1_off, int onehot, int32_t* status,
+                           cudaStream_t st) {
   const int64_t work = vec ? rows * (cols / 4) : rows * cols;
   int64_t blocks = (work + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (vec)
-    split2h_vec_kernel<kBias, kGelu><<<(unsigned)blocks, 256, 0, st>>>(x, ldx, bias, y, ldy, p, ldp, rows, cols, status);
+    split2h_vec_kernel<kBias, kGelu><<<(unsigned)blocks, 256, 0, st>>>(x, ldx, bias, y, ldy, p, ldp, rows, cols, h1_off,
+                                                                       onehot, status);
   else
-    split2h_kernel<kBias, kGelu><<<(unsigned)blocks, 256, 0, st>>>(x, ldx, bias, y, ldy, p, ldp, rows, cols, status);
+    split2h_kernel<kBias, kGelu><<<(unsigned)blocks, 256, 0, st>>>(x, ldx, bias, y, ldy, p, ldp, rows, cols, h1_off,
+                                                                   onehot, status);
 }
 
 }  // namespace sc
@@ -214,23 +220,26 @@ extern "C" int sc_split_bf16x3(const float* x, int64_t ldx, const float* bias, i
 }
 
 extern "C" int sc_split_f16x2(const float* x, int64_t ldx, const float* bias, int32_t gelu, float* y, int64_t ldy,
-                              void* planes, int64_t ldp, int64_t rows, int32_t cols, int32_t* status, void* stream) {
+                              void* planes, int64_t ldp, int64_t rows, int32_t cols, int32_t onehot, int32_t* status,
+                              void* stream) {
   SC_CHECK_ARG(x && planes, "sc_split_f16x2: null pointer");
-  SC_CHECK_ARG(rows >= 0 && cols >= 1 && ldx >= cols && ldp >= 2LL * cols && (!y || ldy >= cols),
+  const int h1_off = cols + (onehot ? 8 : 0);
+  SC_CHECK_ARG(rows >= 0 && cols >= 1 && ldx >= cols && ldp >= (int64_t)h1_off + cols && (!y || ldy >= cols),
                "sc_split_f16x2: bad shape");
   if (rows == 0) return SC_OK;
-  const bool vec = cols % 4 == 0 && ldx % 4 == 0 && ldp % 4 == 0 && (!y || ldy % 4 == 0) &&
-                   !(((uintptr_t)x | (uintptr_t)y | (uintptr_t)bias) & 15) && !((uintptr_t)planes & 7);
+  const bool vec = cols % 4 == 0 && ldx % 4 == 0 && ldp % 8 == 0 && (!y || ldy % 4 == 0) &&
+                   !(((uintptr_t)x | (uintptr_t)y | (uintptr_t)bias) & 15) && !((uintptr_t)planes & 15);
   cudaStream_t st = (cudaStream_t)stream;
   __half* p = (__half*)planes;
+  const int oh = onehot ? 1 : 0;
   if (bias && gelu)
-    launch_split2h<true, true>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, status, st);
+    launch_split2h<true, true>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, h1_off, oh, status, st);
   else if (bias)
-    launch_split2h<true, false>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, status, st);
+    launch_split2h<true, false>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, h1_off, oh, status, st);
   else if (gelu)
-    launch_split2h<false, true>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, status, st);
+    launch_split2h<false, true>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, h1_off, oh, status, st);
   else
-    launch_split2h<false, false>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, status, st);
+    launch_split2h<false, false>(vec, x, ldx, bias, y, ldy, p, ldp, rows, cols, h1_off, oh, status, st);
   SC_CHECK_LAUNCH("split2h_kernel");
   return SC_OK;
 }

@@ -311,52 +311,67 @@ def _linear_x6(planes: torch.Tensor, w5: torch.Tensor, chunk: int | None = None)
     return c
 
 
-def _split_weight_x3h(w: torch.Tensor):
-    """fp32 weight [N, K] -> (fp16 [N, 2K] = [G1 | G0], s) with W * 2^e = G0 + G1 (G0 = fp16_rn, G1 the
-    fp16 of the residual) and s = 2^-e: e puts max |W| at 2^14, so the residual plane of the O(0.02)
-    weights stays out of fp16's subnormal range.  One-time, at upload."""
+def _split_weight_x3h(w: torch.Tensor, bias: torch.Tensor | None = None):
+    """fp32 weight [N, K] (+ bias [N]) -> (fp16 [N, 2K (+16)], s): W * 2^e = G0 + G1 (G0 = fp16_rn,
+    G1 the fp16 of the residual) laid out [G1 | G0], or with a bias [G1 | B1 0 | G0 | B0 0] where
+    B0 + B1 = bias * 2^e the same way and "0" pads each bias column to 8; s = 2^-e, e putting
+    max(|W|, |bias|) at 2^14 so the residual planes stay out of fp16's subnormal range.  The bias
+    columns meet the constant column of split_planes_h(..., onehot=True): B0 rides in the main
+    product, B1 in the corrections.  One-time, at upload."""
     w = w.float()
     amax = float(w.abs().max()) if w.numel() else 0.0
+    if bias is not None and bias.numel():
+        amax = max(amax, float(bias.float().abs().max()))
     e = int(math.floor(math.log2(16384.0 / amax))) if amax > 0 else 0
-    ws = w * (2.0 ** e)
-    g0 = ws.to(torch.float16)
-    g1 = (ws - g0.float()).to(torch.float16)
-    return torch.cat([g1, g0], dim=1).contiguous(), 2.0 ** -e
+
+    def planes(a):
+        a = a.float() * (2.0 ** e)
+        hi = a.to(torch.float16)
+        return hi, (a - hi.float()).to(torch.float16)
+
+    g0, g1 = planes(w)
+    if bias is None:
+        return torch.cat([g1, g0], dim=1).contiguous(), 2.0 ** -e
+    b0, b1 = planes(bias.reshape(-1, 1))
+    pad = torch.zeros((w.shape[0], 7), dtype=torch.float16, device=w.device)
+    return torch.cat([g1, b1, pad, g0, b0, pad], dim=1).contiguous(), 2.0 ** -e
 
 
 def split_planes_h(x: torch.Tensor, bias=None, gelu: bool = False, keep: torch.Tensor | None = None,
-                   status: torch.Tensor | None = None) -> torch.Tensor:
-    """fp32 [M, K] (+ bias, GELU) -> fp16 planes [M, 2K] = [h0 | h1] (sc_split_f16x2); ``status``
-    (device int32) is set to 1 if a value is outside fp16 range."""
+                   status: torch.Tensor | None = None, onehot: bool = False) -> torch.Tensor:
+    """fp32 [M, K] (+ bias, GELU) -> fp16 planes [M, 2K] = [h0 | h1], or [M, 2K + 8] =
+    [h0 | 1 0 .. 0 | h1] with ``onehot`` (sc_split_f16x2); ``status`` (device int32) is set to 1 if a
+    value is outside fp16 range."""
     M, K = x.shape
-    planes = torch.empty((M, 2 * K), dtype=torch.float16, device=x.device)
+    planes = torch.empty((M, 2 * K + (8 if onehot else 0)), dtype=torch.float16, device=x.device)
     _lib.call("sc_split_f16x2", x.data_ptr(), x.stride(0), _lib.ptr(bias), int(gelu), _lib.ptr(keep),
-              K if keep is None else keep.stride(0), planes.data_ptr(), planes.stride(0), M, K, _lib.ptr(status),
-              _lib.stream_handle(), exc=EncoderError)
+              K if keep is None else keep.stride(0), planes.data_ptr(), planes.stride(0), M, K, int(onehot),
+              _lib.ptr(status), _lib.stream_handle(), exc=EncoderError)
     return planes
 
 
-def _linear_x3h(planes: torch.Tensor, w2: torch.Tensor, s: float, bias_s: torch.Tensor | None = None,
-                chunk: int | None = None) -> torch.Tensor:
-    """a W^T (+ bias) in fp32 from the fp16 planes of a ([M, 2K] = [h0 | h1]) and of W * 2^e
-    ([N, 2K] = [g1 | g0]) on the fp16 tensor cores:
-      corrections [h0 | h1] . [g1 | g0]  (one GEMM over K' = 2K, magnitude 2^-11; starts from bias / s)
-      + main      h0 . g0 in K-chunks of <= ``chunk``, the last one scaling the sum by s = 2^-e (exact)
-    = h0 g0 + h0 g1 + h1 g0 (dropped term h1 g1 <= 2^-22 relative), three products where the bf16
-    form needs six.  Measured vs fp64 (M = 131k): max relative error 1.2-1.7e-6, SGEMM's 1.1-2.2e-6.
-    R/encoder.py:322-324, :345, :350, :352."""
-    K = planes.shape[1] // 2
+def _linear_x3h(planes: torch.Tensor, w2: torch.Tensor, s: float, chunk: int | None = None) -> torch.Tensor:
+    """a W^T (+ bias) in fp32 from the fp16 planes of a ([M, 2K] = [h0 | h1], or [h0 | e | h1] with the
+    constant column e) and of W * 2^e ([N, 2K] = [g1 | g0], or [g1 | b1 | g0 | b0] with the bias):
+      corrections [h0 (e) h1] . [g1 (b1) g0]  (one GEMM; magnitude 2^-11)
+      + main      [h0 (e)] . [g0 (b0)]  in K-chunks of <= ``chunk``, accumulated in place, the last
+                  one scaling the sum by s = 2^-e (exact)
+    = h0 g0 + h0 g1 + h1 g0 (+ bias) (dropped term h1 g1 <= 2^-22 relative), three products where the
+    bf16 form needs six.  Measured vs fp64 (M = 131k): max relative error 1.2-1.7e-6, SGEMM's
+    1.1-2.2e-6.  R/encoder.py:322-324, :345, :350, :352."""
+    kb = 8 if w2.shape[1] == planes.shape[1] + 8 else 0  # constant / bias columns: [2K + 8] vs [2K + 16]
+    if w2.shape[1] != planes.shape[1] + kb:
+        raise EncoderError(f"split planes {tuple(planes.shape)} do not match the weight planes {tuple(w2.shape)}")
+    K = (planes.shape[1] - kb) // 2
     chunk = chunk or X6_CHUNK
-    if bias_s is None:
-        c = torch.mm(planes, w2.t(), out_dtype=torch.float32)
-    else:
-        c = torch.addmm(bias_s, planes, w2.t(), out_dtype=torch.float32)
-    h0, g0 = planes[:, :K], w2[:, K:]
+    c = torch.mm(planes[:, :2 * K + kb], w2[:, :2 * K + kb].t(), out_dtype=torch.float32)
+    h0, g0 = planes[:, :K + kb], w2[:, K + kb:]
     starts = list(range(0, K, chunk))
     for n, k0 in enumerate(starts):  # in place (out=c): no copy of c per chunk
-        sc = s if n == len(starts) - 1 else 1.0
-        torch.addmm(c, h0[:, k0:k0 + chunk], g0[:, k0:k0 + chunk].t(), beta=sc, alpha=sc,
-                    out_dtype=torch.float32, out=c)
+        last = n == len(starts) - 1
+        k1 = K + kb if last else k0 + chunk  # the bias column rides in the last chunk
+        sc = s if last else 1.0
+        torch.addmm(c, h0[:, k0:k1], g0[:, k0:k1].t(), beta=sc, alpha=sc, out_dtype=torch.float32, out=c)
     return c
 
 
@@ -436,11 +451,10 @@ class CrossEncoder:
                     if self.fp32_gemm == "bf16x6":
                         L[name + "_x6"] = _split_weight_x6(L[name])
                     else:
-                        L[name + "_x3h"], L[name + "_x3h_s"] = _split_weight_x3h(L[name])
+                        b = L["bqkv"] if name == "wqkv" else None  # the QKV bias rides in the GEMM
+                        L[name + "_x3h"], L[name + "_x3h_s"] = _split_weight_x3h(L[name], b)
                 for name in ("bqkv", "bo", "b1", "b2"):
                     L[name + "_f32"] = L[name].float().contiguous()
-                if self.fp32_gemm == "f16x3":
-                    L["bqkv_x3h"] = (L["bqkv_f32"] / L["wqkv_x3h_s"]).contiguous()  # exact: s is 2^-e
 
     # -- validation -------------------------------------------------------
 
@@ -524,18 +538,19 @@ class CrossEncoder:
         self._last_bad = bad if check_finite else None
         return x
 
-    def _xsplit(self, x, bias=None, gelu=False):
-        """GEMM operand planes of x (+ bias, GELU) for the split fp32 modes."""
+    def _xsplit(self, x, bias=None, gelu=False, qkv_input=False):
+        """GEMM operand planes of x (+ bias, GELU) for the split fp32 modes (``qkv_input``: the planes
+        feed the QKV projection, whose bias rides in the f16x3 GEMM through a constant column)."""
         if self.fp32_gemm == "bf16x6":
             return split_planes(x, bias=bias, gelu=gelu)
-        return split_planes_h(x, bias=bias, gelu=gelu, status=self._range_flag)
+        return split_planes_h(x, bias=bias, gelu=gelu, status=self._range_flag, onehot=qkv_input)
 
     def _xlinear(self, planes, L, name, with_bias=False):
-        """x W^T (+ the layer's bias) in fp32 from the planes of x (split fp32 modes)."""
+        """x W^T (+ the QKV bias) in fp32 from the planes of x (split fp32 modes)."""
         if self.fp32_gemm == "bf16x6":
             c = _linear_x6(planes, L[name + "_x6"])
             return c.add_(L["bqkv_f32"]) if with_bias else c
-        return _linear_x3h(planes, L[name + "_x3h"], L[name + "_x3h_s"], L["bqkv_x3h"] if with_bias else None)
+        return _linear_x3h(planes, L[name + "_x3h"], L[name + "_x3h_s"])  # f16x3: bias folded in (wqkv)
 
     def _encode_x6(self, ids_dev, layout, check_finite, attn_hook, cls_only) -> torch.Tensor:
         """encode_packed for fp32 with the projections as split products (fp32_gemm="bf16x6" / "f16x3").
@@ -556,7 +571,7 @@ class CrossEncoder:
                   self.pos_emb.data_ptr(), x.data_ptr(), None, T, h, stream, exc=EncoderError)
         last = cfg.layers - 1
         for i, L in enumerate(self.layers):
-            xs = self._xsplit(x)
+            xs = self._xsplit(x, qkv_input=True)
             if cls_only and i == last:
                 self._last_bad = bad if check_finite else None
                 return self._cls_last_layer_x6(L, x, xs, layout, pattern, bad if check_finite else None, i)

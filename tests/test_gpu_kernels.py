@@ -289,6 +289,9 @@ def test_split_f16x2_planes_and_range_flag():
         assert torch.equal(pl[:, cols:], (keep - h0.float()).to(torch.float16))
         assert (keep.double() - v).abs().max().item() < 1e-4
         assert int(st.item()) == 0
+    pl = split_planes_h(x, onehot=True)
+    assert torch.equal(pl[:, :cols], x.to(torch.float16)) and torch.equal(pl[:, cols + 8:], (x - x.half().float()).half())
+    assert (pl[:, cols] == 1).all() and (pl[:, cols + 1:cols + 8] == 0).all()
     x[5, 3] = 70000.0
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
     split_planes_h(x, status=st)
@@ -306,8 +309,8 @@ def test_linear_x3h_matches_fp64():
         w = torch.randn((768, K), device="cuda", generator=g) * 0.02
         b = torch.randn(768, device="cuda", generator=g)
         exact = a.double() @ w.double().t() + b.double()
-        w2, s = _split_weight_x3h(w)
-        got = _linear_x3h(split_planes_h(a), w2, s, (b / s).contiguous())
+        w2, s = _split_weight_x3h(w, b)
+        got = _linear_x3h(split_planes_h(a, onehot=True), w2, s)
         prev = torch.backends.cuda.matmul.allow_tf32
         torch.backends.cuda.matmul.allow_tf32 = False
         try:
