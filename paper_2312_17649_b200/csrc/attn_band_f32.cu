@@ -11,7 +11,11 @@
 // semantics (R/band.py:48-52, R/attention.py:228-257): band keys
 // |t - r| <= w inside the doc, the cls / query keys when linked, zero-logit
 // padding slots entering with logit 0.  Head rows go to the generic kernel.
+#include <cuda_fp16.h>
+#include <stdlib.h>
+
 #include "attn.cuh"
+#include "mma_tile.cuh"
 
 namespace sc {
 namespace bandf {
@@ -204,6 +208,329 @@ __global__ void __launch_bounds__(NT) band_f32_kernel(Params p) {
 
 }  // namespace bandf
 
+
+// ---------------------------------------------------------------------------
+// The same doc-band attention on the tensor cores: fp32 operands as fp16 pairs
+// (x = hi + lo, hi = fp16_rn(x), lo = fp16_rn(x - hi): 22 significant bits) and
+// three mma.sync m16n8k16 products per contraction, hi.hi + hi.lo + lo.hi
+// (dropped lo.lo <= 2^-22 relative), fp32 accumulation -- for S = Q K^T and for
+// O = P V alike.  CTA = 64 doc rows x 1 head, 4 warps x 16 rows; K / V of the
+// band (64 + 2w rows) and of the cls / query keys staged once per CTA as hi / lo
+// planes in 128B-swizzled shared memory (ldmatrix-able), Q straight from global
+// into A fragments.  One softmax over the row's whole key set (globals + band:
+// at most 32 + 80 keys).  The rotating warp (h % 4) also writes the full rows'
+// split-softmax records over the tile's own 64 keys (cls; query rows under
+// longformer / full) in the band_f32_kernel format.  The old SIMT kernel re-read
+// 2w + 1 K/V rows from shared memory per row and was bound by shared-memory
+// bandwidth (1.3 ms per layer at 32 x 4099); this one reads each staged row once
+// per 16-row block through ldmatrix.
+namespace bandx3 {
+
+constexpr int BM = 64, D = 64, MAXW = 32, GRM = 32, NT = 128;
+constexpr int MAXCH = (16 + 2 * MAXW + 15) / 16;  // band chunks of 16 keys per 16-row block
+constexpr int ROWB = 128;                          // one plane row: 64 fp16
+
+__device__ __forceinline__ void mma_h(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// (x, y) -> packed fp16 hi pair and the packed fp16 residual pair
+__device__ __forceinline__ void split_h2(float x, float y, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x, y);
+  const float2 f = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x - f.x, y - f.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+// C(16 x 16 keys, two n8 tiles) += A(16 x 64) . B[row0 .. row0+15]^T
+__device__ __forceinline__ void qk16h(uint32_t bbuf, int row0, int lane, const uint32_t (&a)[4][4], float (&c0)[4],
+                                      float (&c1)[4]) {
+  const int brow = row0 + (lane & 7) + ((lane >> 4) << 3);
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    uint32_t b[4];
+    mmat::ldsm_x4(mmat::swz(bbuf, brow, ks * 2 + ((lane >> 3) & 1)), b);
+    mma_h(c0, a[ks], b[0], b[1]);
+    mma_h(c1, a[ks], b[2], b[3]);
+  }
+}
+// O(16 x 64) += A(16 x 16 keys) . B[row0 .. row0+15]  (B rows = keys)
+__device__ __forceinline__ void pv16h(uint32_t bbuf, int row0, int lane, const uint32_t (&a)[4], float (&o)[8][4]) {
+  const int brow = row0 + (lane & 7) + (((lane >> 3) & 1) << 3);
+#pragma unroll
+  for (int np = 0; np < 4; ++np) {
+    uint32_t b[4];
+    mmat::ldsm_x4_t(mmat::swz(bbuf, brow, np * 2 + (lane >> 4)), b);
+    mma_h(o[2 * np], a, b[0], b[1]);
+    mma_h(o[2 * np + 1], a, b[2], b[3]);
+  }
+}
+// S += Q K^T over one 16-key block in three products (small terms first)
+__device__ __forceinline__ void qk16x3(uint32_t kh, uint32_t kl, int row0, int lane, const uint32_t (&qh)[4][4],
+                                       const uint32_t (&ql)[4][4], float (&c0)[4], float (&c1)[4]) {
+  qk16h(kl, row0, lane, qh, c0, c1);
+  qk16h(kh, row0, lane, ql, c0, c1);
+  qk16h(kh, row0, lane, qh, c0, c1);
+}
+// O += P V over one 16-key block (P as two C-layout n8 tiles of fp32 probabilities)
+__device__ __forceinline__ void pv16x3(uint32_t vh, uint32_t vl, int row0, int lane, const float (&p0)[4],
+                                       const float (&p1)[4], float (&o)[8][4]) {
+  uint32_t ah[4], al[4];
+  split_h2(p0[0], p0[1], ah[0], al[0]);
+  split_h2(p0[2], p0[3], ah[1], al[1]);
+  split_h2(p1[0], p1[1], ah[2], al[2]);
+  split_h2(p1[2], p1[3], ah[3], al[3]);
+  pv16h(vl, row0, lane, ah, o);
+  pv16h(vh, row0, lane, al, o);
+  pv16h(vh, row0, lane, ah, o);
+}
+// A fragments (hi, lo) of 16 fp32 rows x 64 dims straight from global; row(i) == nullptr -> zeros
+template <typename F>
+__device__ __forceinline__ void load_q_x3(int lane, F&& row, uint32_t (&qh)[4][4], uint32_t (&ql)[4][4]) {
+  const int gq = lane >> 2, tq = lane & 3;
+  const float* r0 = row(gq);
+  const float* r1 = row(gq + 8);
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int c = ks * 16 + half * 8 + 2 * tq;
+      const float2 a = r0 ? *reinterpret_cast<const float2*>(r0 + c) : make_float2(0.f, 0.f);
+      const float2 b = r1 ? *reinterpret_cast<const float2*>(r1 + c) : make_float2(0.f, 0.f);
+      split_h2(a.x, a.y, qh[ks][2 * half], ql[ks][2 * half]);
+      split_h2(b.x, b.y, qh[ks][2 * half + 1], ql[ks][2 * half + 1]);
+    }
+  }
+}
+// hi / lo planes of `nrows` fp32 rows (64 dims) into swizzled smem; row(i) == nullptr -> zeros
+template <typename F>
+__device__ __forceinline__ void stage_x3(uint32_t hbuf, uint32_t lbuf, int nrows, F&& row) {
+  for (int idx = threadIdx.x; idx < nrows * 16; idx += NT) {
+    const int r = idx >> 4, c4 = idx & 15;
+    const float* src = row(r);
+    const float4 v = src ? *reinterpret_cast<const float4*>(src + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t h0, l0, h1, l1;
+    split_h2(v.x, v.y, h0, l0);
+    split_h2(v.z, v.w, h1, l1);
+    const uint32_t off = (c4 & 1) * 8;
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(mmat::swz(hbuf, r, c4 >> 1) + off), "r"(h0), "r"(h1));
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(mmat::swz(lbuf, r, c4 >> 1) + off), "r"(l0), "r"(l1));
+  }
+}
+
+__global__ void __launch_bounds__(NT) band_f32x3_kernel(bandf::Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_x3[];
+  const int tile = blockIdx.x, h = blockIdx.y;
+  if (tile >= __ldg(p.tile_base + p.nseq)) return;  // grid is an upper bound
+  const int j = find_seq(p.tile_base, p.nseq, tile);
+  const SeqGroups g = seq_groups(p.cu, p.qlen, j);
+  const int dlen = g.len[2], dstart = g.start + g.off[2];
+  const int r0 = (tile - __ldg(p.tile_base + j)) * BM;
+  const int rows_here = min(BM, dlen - r0);
+  const int w = p.w, hoff = h * D;
+  const int nhead = 1 + g.len[1];
+  const int kb_rows = (BM + 2 * w + 15) & ~15;
+  const uint32_t sm = mmat::smem_u32(smem_x3);
+  const uint32_t KH = sm, KL = KH + kb_rows * ROWB, VH = KL + kb_rows * ROWB, VL = VH + kb_rows * ROWB;
+  const uint32_t GKH = VL + kb_rows * ROWB, GKL = GKH + GRM * ROWB, GVH = GKL + GRM * ROWB, GVL = GVH + GRM * ROWB;
+
+  // stage the band rows (doc positions r0 - w ..) and the cls / query keys as hi / lo planes
+  auto band_k = [&](int r) -> const float* {
+    const int pos = r0 - w + r;
+    return (pos >= 0 && pos < dlen) ? p.k + (int64_t)(dstart + pos) * p.ld + hoff : nullptr;
+  };
+  auto band_v = [&](int r) -> const float* {
+    const int pos = r0 - w + r;
+    return (pos >= 0 && pos < dlen) ? p.v + (int64_t)(dstart + pos) * p.ld + hoff : nullptr;
+  };
+  stage_x3(KH, KL, kb_rows, band_k);
+  stage_x3(VH, VL, kb_rows, band_v);
+  stage_x3(GKH, GKL, GRM, [&](int r) -> const float* { return r < nhead ? p.k + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
+  stage_x3(GVH, GVL, GRM, [&](int r) -> const float* { return r < nhead ? p.v + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const float c2 = 1.4426950408889634f / p.scale;
+  const int wr0 = warp * 16;
+  const bool glob = p.link_cls || p.link_query;
+  const int nch = (16 + 2 * w + 15) / 16;
+
+  if (wr0 < rows_here) {
+    uint32_t qh[4][4], ql[4][4];
+    load_q_x3(lane, [&](int i) -> const float* {
+      return wr0 + i < rows_here ? p.q + (int64_t)(dstart + r0 + wr0 + i) * p.ld + hoff : nullptr;
+    }, qh, ql);
+    float sg[4][4], sb[2 * MAXCH][4];
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) sg[nb][0] = sg[nb][1] = sg[nb][2] = sg[nb][3] = 0.f;
+#pragma unroll
+    for (int nb = 0; nb < 2 * MAXCH; ++nb) sb[nb][0] = sb[nb][1] = sb[nb][2] = sb[nb][3] = 0.f;
+    if (glob) {
+#pragma unroll
+      for (int gb = 0; gb < 2; ++gb)
+        if (gb * 16 < nhead) qk16x3(GKH, GKL, gb * 16, lane, qh, ql, sg[2 * gb], sg[2 * gb + 1]);
+    }
+#pragma unroll
+    for (int ch = 0; ch < MAXCH; ++ch)
+      if (ch < nch) qk16x3(KH, KL, wr0 + 16 * ch, lane, qh, ql, sb[2 * ch], sb[2 * ch + 1]);
+    // masks: global key kg valid when linked; band smem row kr = doc position r0 - w + kr
+    const int ra = r0 + wr0 + gq;  // doc-relative rows of this thread: ra, ra + 8
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int kg = nb * 8 + 2 * tq + (e & 1);
+        if (!(glob && kg < nhead && (kg == 0 ? p.link_cls : p.link_query))) sg[nb][e] = -INFINITY;
+      }
+#pragma unroll
+    for (int nb = 0; nb < 2 * MAXCH; ++nb)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int pos = r0 - w + wr0 + nb * 8 + 2 * tq + (e & 1);
+        const int rr = ra + ((e >> 1) << 3);
+        if (!(nb < 2 * nch && pos >= 0 && pos < dlen && pos - rr <= w && rr - pos <= w)) sb[nb][e] = -INFINITY;
+      }
+    // one softmax over the row's key set (zero-logit padding: the missing band slots enter with logit 0)
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    if (p.padding == SC_PAD_ZERO_LOGIT) {
+      const int rb = ra + 8;
+      const float na = (float)(2 * w + 1 - max(0, min(dlen, ra + w + 1) - max(0, ra - w)));
+      const float nbv = (float)(2 * w + 1 - max(0, min(dlen, rb + w + 1) - max(0, rb - w)));
+      if (na > 0.f) { m0 = 0.f; l0 = tq == 0 ? na : 0.f; }
+      if (nbv > 0.f) { m1 = 0.f; l1 = tq == 0 ? nbv : 0.f; }
+    }
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      m0 = fmaxf(m0, fmaxf(sg[nb][0], sg[nb][1]));
+      m1 = fmaxf(m1, fmaxf(sg[nb][2], sg[nb][3]));
+    }
+#pragma unroll
+    for (int nb = 0; nb < 2 * MAXCH; ++nb) {
+      m0 = fmaxf(m0, fmaxf(sb[nb][0], sb[nb][1]));
+      m1 = fmaxf(m1, fmaxf(sb[nb][2], sb[nb][3]));
+    }
+    m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+    m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
+    m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+    m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
+    if (p.padding == SC_PAD_ZERO_LOGIT) {  // the padding's exp(0 - m) share of l
+      l0 = l0 > 0.f && m0 != -INFINITY ? l0 * exp2f(-m0 * c2) : l0;
+      l1 = l1 > 0.f && m1 != -INFINITY ? l1 * exp2f(-m1 * c2) : l1;
+    }
+    const float b0 = m0 == -INFINITY ? 0.f : m0 * c2, b1 = m1 == -INFINITY ? 0.f : m1 * c2;
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) {
+      sg[nb][0] = exp2f(fmaf(sg[nb][0], c2, -b0)); sg[nb][1] = exp2f(fmaf(sg[nb][1], c2, -b0));
+      sg[nb][2] = exp2f(fmaf(sg[nb][2], c2, -b1)); sg[nb][3] = exp2f(fmaf(sg[nb][3], c2, -b1));
+      l0 += sg[nb][0] + sg[nb][1];
+      l1 += sg[nb][2] + sg[nb][3];
+    }
+#pragma unroll
+    for (int nb = 0; nb < 2 * MAXCH; ++nb) {
+      sb[nb][0] = exp2f(fmaf(sb[nb][0], c2, -b0)); sb[nb][1] = exp2f(fmaf(sb[nb][1], c2, -b0));
+      sb[nb][2] = exp2f(fmaf(sb[nb][2], c2, -b1)); sb[nb][3] = exp2f(fmaf(sb[nb][3], c2, -b1));
+      l0 += sb[nb][0] + sb[nb][1];
+      l1 += sb[nb][2] + sb[nb][3];
+    }
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    float o[8][4];
+#pragma unroll
+    for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
+    if (glob) {
+#pragma unroll
+      for (int gb = 0; gb < 2; ++gb)
+        if (gb * 16 < nhead) pv16x3(GVH, GVL, gb * 16, lane, sg[2 * gb], sg[2 * gb + 1], o);
+    }
+#pragma unroll
+    for (int ch = 0; ch < MAXCH; ++ch)
+      if (ch < nch) pv16x3(VH, VL, wr0 + 16 * ch, lane, sb[2 * ch], sb[2 * ch + 1], o);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int rr = ra + 8 * half;
+      if (rr >= dlen) continue;
+      const float l = half ? l1 : l0;
+      float* dst = p.out + (int64_t)(dstart + rr) * p.ld_out + hoff + 2 * tq;
+      if (!(l > 0.f)) {
+        if (tq == 0 && p.status) atomicOr(p.status, 1);
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) *reinterpret_cast<float2*>(dst + nb * 8) = make_float2(0.f, 0.f);
+        continue;
+      }
+      const float inv = 1.f / l;
+#pragma unroll
+      for (int nb = 0; nb < 8; ++nb)
+        *reinterpret_cast<float2*>(dst + nb * 8) = make_float2(o[nb][2 * half] * inv, o[nb][2 * half + 1] * inv);
+    }
+  }
+
+  // full-row records: head rows f < fneed against this tile's own doc keys (band rows w .. w + 63)
+  if (p.partials && warp == (h & 3)) {
+    for (int fc = 0; fc * 16 < p.fneed && fc * 16 < nhead; ++fc) {
+      uint32_t qh[4][4], ql[4][4];
+      load_q_x3(lane, [&](int i) -> const float* {
+        const int f = fc * 16 + i;
+        return f < p.fneed && f < nhead ? p.q + (int64_t)(g.start + f) * p.ld + hoff : nullptr;
+      }, qh, ql);
+      float sc[8][4];
+#pragma unroll
+      for (int nb = 0; nb < 8; ++nb) sc[nb][0] = sc[nb][1] = sc[nb][2] = sc[nb][3] = 0.f;
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) qk16x3(KH, KL, w + 16 * kc, lane, qh, ql, sc[2 * kc], sc[2 * kc + 1]);
+      float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+      for (int nb = 0; nb < 8; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (nb * 8 + 2 * tq + (e & 1) >= rows_here) sc[nb][e] = -INFINITY;
+          if (e < 2) m0 = fmaxf(m0, sc[nb][e]);
+          else m1 = fmaxf(m1, sc[nb][e]);
+        }
+      m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 1));
+      m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, 2));
+      m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 1));
+      m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, 2));
+      float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+      for (int nb = 0; nb < 8; ++nb) {
+        sc[nb][0] = exp2f((sc[nb][0] - m0) * c2); sc[nb][1] = exp2f((sc[nb][1] - m0) * c2);
+        sc[nb][2] = exp2f((sc[nb][2] - m1) * c2); sc[nb][3] = exp2f((sc[nb][3] - m1) * c2);
+        l0 += sc[nb][0] + sc[nb][1];
+        l1 += sc[nb][2] + sc[nb][3];
+      }
+      l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+      l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+      float o[8][4];
+#pragma unroll
+      for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) pv16x3(VH, VL, w + 16 * kc, lane, sc[2 * kc], sc[2 * kc + 1], o);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int f = fc * 16 + gq + 8 * half;
+        if (f >= p.fneed || f >= nhead) continue;
+        float* rec = p.partials + (((int64_t)tile * p.H + h) * p.fmax + f) * (D + 2);
+        if (tq == 0) {
+          rec[0] = (half ? m1 : m0) / p.scale;  // raw logit -> the record's natural units
+          rec[1] = half ? l1 : l0;
+        }
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb)
+          *reinterpret_cast<float2*>(rec + 2 + nb * 8 + 2 * tq) = make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
+      }
+    }
+  }
+}
+
+}  // namespace bandx3
+
 // fp32 doc rows by band_f32_kernel; the caller handles the head rows.  SC_ERR_UNSUPPORTED outside
 // the envelope (fp32, d = 64, window <= 32, doc -> cls / query links FULL or NONE, no QDS).
 int launch_attn_band_f32(const AttnArgs& a, int dtype, const int32_t* seq_tile_base, int tile_rows,
@@ -240,6 +567,21 @@ int launch_attn_band_f32(const AttnArgs& a, int dtype, const int32_t* seq_tile_b
     cudaFuncSetAttribute(band_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(((2 * KB + 2 * MAXH) * DP + kExtra) * sizeof(float)));
     attr = true;
+  }
+  static int simt = -1;  // SC_F32_SIMT=1: the CUDA-core kernel (measurement A/B)
+  if (simt < 0) simt = getenv("SC_F32_SIMT") ? atoi(getenv("SC_F32_SIMT")) : 0;
+  if (!simt) {
+    const int kb_rows = (bandx3::BM + 2 * w + 15) & ~15;
+    const size_t smem3 = (size_t)(4 * kb_rows + 4 * bandx3::GRM) * bandx3::ROWB;
+    static bool attr3 = false;
+    if (!attr3) {
+      cudaFuncSetAttribute(bandx3::band_f32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (4 * ((bandx3::BM + 2 * bandx3::MAXW + 15) & ~15) + 4 * bandx3::GRM) * bandx3::ROWB);
+      attr3 = true;
+    }
+    bandx3::band_f32x3_kernel<<<dim3(grid, (unsigned)a.H), bandx3::NT, smem3, st>>>(p);
+    SC_CHECK_LAUNCH("band_f32x3_kernel");
+    return SC_OK;
   }
   band_f32_kernel<<<dim3(grid, (unsigned)a.H), NT, smem, st>>>(p);
   SC_CHECK_LAUNCH("band_f32_kernel");
