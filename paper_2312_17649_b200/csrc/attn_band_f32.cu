@@ -304,23 +304,58 @@ __device__ __forceinline__ void load_q_x3(int lane, F&& row, uint32_t (&qh)[4][4
     }
   }
 }
-// hi / lo planes of `nrows` fp32 rows (64 dims) into swizzled smem; row(i) == nullptr -> zeros
+// The fp32 values behind load_q_x3's fragments (raw[ks][2 * half + row8]), and their split.
+template <typename F>
+__device__ __forceinline__ void load_q_raw(int lane, F&& row, float2 (&raw)[4][4]) {
+  const int gq = lane >> 2, tq = lane & 3;
+  const float* r0 = row(gq);
+  const float* r1 = row(gq + 8);
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int c = ks * 16 + half * 8 + 2 * tq;
+      raw[ks][2 * half] = r0 ? __ldg(reinterpret_cast<const float2*>(r0 + c)) : make_float2(0.f, 0.f);
+      raw[ks][2 * half + 1] = r1 ? __ldg(reinterpret_cast<const float2*>(r1 + c)) : make_float2(0.f, 0.f);
+    }
+}
+__device__ __forceinline__ void split_q(const float2 (&raw)[4][4], uint32_t (&qh)[4][4], uint32_t (&ql)[4][4]) {
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) split_h2(raw[ks][i].x, raw[ks][i].y, qh[ks][i], ql[ks][i]);
+}
+// hi / lo planes of `nrows` fp32 rows (64 dims) into swizzled smem; row(i) == nullptr -> zeros.
+// Loads are issued in batches of UNR float4 per thread before any is split and stored, so a
+// thread keeps UNR global loads in flight (one-at-a-time staging was load-latency bound).
+constexpr int UNR = 8;
 template <typename F>
 __device__ __forceinline__ void stage_x3(uint32_t hbuf, uint32_t lbuf, int nrows, F&& row) {
-  for (int idx = threadIdx.x; idx < nrows * 16; idx += NT) {
-    const int r = idx >> 4, c4 = idx & 15;
-    const float* src = row(r);
-    const float4 v = src ? *reinterpret_cast<const float4*>(src + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t h0, l0, h1, l1;
-    split_h2(v.x, v.y, h0, l0);
-    split_h2(v.z, v.w, h1, l1);
-    const uint32_t off = (c4 & 1) * 8;
-    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(mmat::swz(hbuf, r, c4 >> 1) + off), "r"(h0), "r"(h1));
-    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(mmat::swz(lbuf, r, c4 >> 1) + off), "r"(l0), "r"(l1));
+  const int n = nrows * 16;
+  for (int base = 0; base < n; base += NT * UNR) {
+    float4 v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int idx = base + u * NT + threadIdx.x;
+      const float* src = idx < n ? row(idx >> 4) : nullptr;
+      v[u] = src ? __ldg(reinterpret_cast<const float4*>(src + 4 * (idx & 15))) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int idx = base + u * NT + threadIdx.x;
+      if (idx >= n) break;
+      const int r = idx >> 4, c4 = idx & 15;
+      uint32_t h0, l0, h1, l1;
+      split_h2(v[u].x, v[u].y, h0, l0);
+      split_h2(v[u].z, v[u].w, h1, l1);
+      const uint32_t off = (c4 & 1) * 8;
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(mmat::swz(hbuf, r, c4 >> 1) + off), "r"(h0), "r"(h1));
+      asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(mmat::swz(lbuf, r, c4 >> 1) + off), "r"(l0), "r"(l1));
+    }
   }
 }
 
-__global__ void __launch_bounds__(NT) band_f32x3_kernel(bandf::Params p) {
+__global__ void __launch_bounds__(NT, 4) band_f32x3_kernel(bandf::Params p) {
   extern __shared__ __align__(1024) uint8_t smem_x3[];
   const int tile = blockIdx.x, h = blockIdx.y;
   if (tile >= __ldg(p.tile_base + p.nseq)) return;  // grid is an upper bound
@@ -345,10 +380,20 @@ __global__ void __launch_bounds__(NT) band_f32x3_kernel(bandf::Params p) {
     const int pos = r0 - w + r;
     return (pos >= 0 && pos < dlen) ? p.v + (int64_t)(dstart + pos) * p.ld + hoff : nullptr;
   };
+  // this thread's Q fragment values (rows gq, gq + 8 of its warp's block), loaded before the staging
+  // so their latency overlaps it
+  float2 qraw[4][4];
+  {
+    const int wq = (threadIdx.x >> 5) * 16, lq = threadIdx.x & 31;
+    load_q_raw(lq, [&](int i) -> const float* {
+      return wq + i < rows_here ? p.q + (int64_t)(dstart + r0 + wq + i) * p.ld + hoff : nullptr;
+    }, qraw);
+  }
   stage_x3(KH, KL, kb_rows, band_k);
   stage_x3(VH, VL, kb_rows, band_v);
-  stage_x3(GKH, GKL, GRM, [&](int r) -> const float* { return r < nhead ? p.k + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
-  stage_x3(GVH, GVL, GRM, [&](int r) -> const float* { return r < nhead ? p.v + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
+  const int g_rows = (p.link_cls || p.link_query || p.partials) ? (nhead + 15) & ~15 : 0;  // 16-key blocks used
+  stage_x3(GKH, GKL, g_rows, [&](int r) -> const float* { return r < nhead ? p.k + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
+  stage_x3(GVH, GVL, g_rows, [&](int r) -> const float* { return r < nhead ? p.v + (int64_t)(g.start + r) * p.ld + hoff : nullptr; });
   __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -360,9 +405,7 @@ __global__ void __launch_bounds__(NT) band_f32x3_kernel(bandf::Params p) {
 
   if (wr0 < rows_here) {
     uint32_t qh[4][4], ql[4][4];
-    load_q_x3(lane, [&](int i) -> const float* {
-      return wr0 + i < rows_here ? p.q + (int64_t)(dstart + r0 + wr0 + i) * p.ld + hoff : nullptr;
-    }, qh, ql);
+    split_q(qraw, qh, ql);
     float sg[4][4], sb[2 * MAXCH][4];
 #pragma unroll
     for (int nb = 0; nb < 4; ++nb) sg[nb][0] = sg[nb][1] = sg[nb][2] = sg[nb][3] = 0.f;
