@@ -13,7 +13,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libsparsecross_b200.so")
+# SC_LIB_PATH: an alternative build of the same library (measurement A/B only)
+LIB_PATH = os.environ.get("SC_LIB_PATH") or os.path.join(HERE, "_lib", "libsparsecross_b200.so")
 
 SC_OK = 0
 SC_ERR_INVALID = 1
