@@ -357,10 +357,11 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
       if (r0 == 0 && !p.fold_skip) hr.global_keys();
     }
   } else if (warp == 5) {
-    // ------------------------------------------------------------- MMA (one thread)
-    // S is double-buffered in TMEM: QK(b+2) is issued as soon as PV(b) has read
-    // P(b) out of the same buffer, so the tensor core runs ahead of softmax.
-    if (lane == 0) {
+    // ------------------------------------------------------------- MMA (one elected lane)
+    // The whole warp runs the loop and the barrier waits; one elected lane issues each group of
+    // tcgen05.mma + commit.  S is double-buffered in TMEM: QK(b+2) is issued as soon as PV(b)
+    // has read P(b) out of the same buffer, so the tensor core runs ahead of softmax.
+    {
       const uint32_t id_qk = idesc_bf16(BM, BN, 0), id_qg = idesc_bf16(BM, GR, 0),
                      id_pv = idesc_bf16(BM, D, 1);
       const uint32_t tO = tmem + O_COL;
@@ -381,9 +382,12 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
           idq = id_qk;
         }
         const uint64_t kd = sw128_desc(kaddr);
+        if (elect_one()) {
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) mma_ss(tS, qd + 2 * ks, kd + 2 * ks, idq, ks > 0);
-        tc_commit(s_full + 8 * (b % NBUF));
+          for (int ks = 0; ks < D / 16; ++ks) mma_ss(tS, qd + 2 * ks, kd + 2 * ks, idq, ks > 0);
+          tc_commit(s_full + 8 * (b % NBUF));
+        }
+        __syncwarp();
       };
       issue_qk(0);
       if (NBUF == 2 && nblocks > 1) issue_qk(1);
@@ -396,17 +400,21 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
         const int kb = b - (has_glob ? 1 : 0), s = kb % NS;
         const uint64_t vd = sw128_desc(gblk ? sm0 + SM::VG : sm0 + SM::KV + s * SM::STAGE + BN * ROWB);
         const int nks = gblk ? GR / 16 : BN / 16;
+        if (elect_one()) {
 #pragma unroll
-        for (int ks = 0; ks < (GR > BN ? GR : BN) / 16; ++ks)
-          if (ks < nks) mma_ts(tO, tS + 8 * ks, vd + 128 * ks, id_pv, (b > 0 || ks > 0));
-        if (!gblk) tc_commit(empty_bar + 8 * s);
-        tc_commit(pv_done + 8 * buf);
+          for (int ks = 0; ks < (GR > BN ? GR : BN) / 16; ++ks)
+            if (ks < nks) mma_ts(tO, tS + 8 * ks, vd + 128 * ks, id_pv, (b > 0 || ks > 0));
+          if (!gblk) tc_commit(empty_bar + 8 * s);
+          tc_commit(pv_done + 8 * buf);
+        }
+        __syncwarp();
         if (b + NBUF < nblocks) {
           mbar_wait(pv_done + 8 * buf, (b / NBUF) & 1);  // P(b) consumed: S buffer free
           issue_qk(b + NBUF);
         }
       }
-      tc_commit(o_final);
+      if (elect_one()) tc_commit(o_final);
+      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------- softmax (thread = row)
