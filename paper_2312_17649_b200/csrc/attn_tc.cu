@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 4) {
-    // ------------------------------------------------------------- TMA (lane 0) + head rows
+    // ------------------------------------------------------------- TMA (one lane) + head rows
     auto issue = [&](int kb) {
       const int s = kb % NS;
       mbar_expect_tx(full_bar + 8 * s, SM::STAGE);
@@ -314,7 +314,9 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
         tma_load_3d(kbuf + BN * ROWB, &tmV, h, doc0 + lo + (kb - ngd) * BN, full_bar + 8 * s);
       }
     };
-    if (lane == 0) {
+    // The warp runs converged; one elect.sync lane issues each group of TMA loads (their operands
+    // stay warp-uniform: no per-lane waterfall loop around UTMALDG).
+    if (elect_one()) {
       mbar_expect_tx(qbar, (BM + (p.fold ? 3 : 2) * GR) * ROWB);
       tma_load_3d(sm0 + SM::Q, &tmQ, h, p.global_rows ? gq0 + r0 : doc0 + r0, qbar);
       tma_load_3d(sm0 + SM::KG, &tmKg, h, g.start, qbar);
@@ -322,12 +324,13 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
       if (p.fold) tma_load_3d(sm0 + SM::QF, &tmQf, h, g.start, qbar);
       for (int kb = 0; kb < min(NS, nkb); ++kb) issue(kb);
     }
+    __syncwarp();
     if (!p.fold) {
-      if (lane == 0)
-        for (int kb = NS; kb < nkb; ++kb) {
-          mbar_wait(empty_bar + 8 * (kb % NS), ((kb / NS) & 1) ^ 1);
-          issue(kb);
-        }
+      for (int kb = NS; kb < nkb; ++kb) {
+        mbar_wait(empty_bar + 8 * (kb % NS), ((kb / NS) & 1) ^ 1);
+        if (elect_one()) issue(kb);
+        __syncwarp();
+      }
     } else {
       const HeadRows<C> hr(p, smem, sm0, lane, h, j, g, n_doc, r0);
       const int own0 = ngd + (r0 - lo) / BN;          // first ring block of the own keys
@@ -344,14 +347,13 @@ __global__ void __launch_bounds__(NTHREADS, C::CTAS) tc_attn_kernel(
           if (!p.fold_skip) hr.own_block(sm0 + SM::KV + s * SM::STAGE, (kb - own0) * BN);
         }
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(empty_bar + 8 * s);
-          if (kb + NS < nkb) {
-            mbar_wait(empty_bar + 8 * s, (kb / NS) & 1);
-            issue(kb + NS);
-          }
-        }
+        if (elect_one()) mbar_arrive(empty_bar + 8 * s);
         __syncwarp();
+        if (kb + NS < nkb) {
+          mbar_wait(empty_bar + 8 * s, (kb / NS) & 1);
+          if (elect_one()) issue(kb + NS);
+          __syncwarp();
+        }
       }
       mbar_wait(qbar, 0);
       if (r0 == 0 && !p.fold_skip) hr.global_keys();
