@@ -75,6 +75,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// One lane of a converged warp (elect.sync; the lowest active lane): TMA issue / bulk-store waits
+// under it keep their operands warp-uniform.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok = 0;
   while (!ok) {
@@ -369,9 +376,14 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
   __syncthreads();
 
   if (warp == PRODW) {
-    if (lane == 0) {
-      prefetch_map(&tmQ); prefetch_map(&tmKb); prefetch_map(&tmVb);
-      prefetch_map(&tmKg); prefetch_map(&tmVg); prefetch_map(&tmQf);
+    // The whole warp walks the items (converged); one elect.sync lane issues each item's loads, so
+    // the TMA operands stay warp-uniform (no per-lane waterfall loop around UTMALDG).
+    {
+      if (elect_one()) {
+        prefetch_map(&tmQ); prefetch_map(&tmKb); prefetch_map(&tmVb);
+        prefetch_map(&tmKg); prefetch_map(&tmVg); prefetch_map(&tmQf);
+      }
+      __syncwarp();
       const uint32_t bytes = (uint32_t)((p.doc_rows ? q_bytes : 0) + 3 * f_bytes + 2 * kb_box * ROWB);
       int it = 0;
       for (int tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
@@ -383,18 +395,21 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
           const int s = it % NS;
           if (it >= NS) mbar_wait(empty_bar + 8 * s, ((it / NS) & 1) ^ 1);
           const uint32_t fb = full_bar + 8 * s;
-          if (h + NS < p.H) {  // L2 prefetch of the boxes this stage will hold next round
-            if (p.doc_rows) tma_prefetch_3d(&tmQ, h + NS, doc_row0);
-            tma_prefetch_3d(&tmKb, h + NS, doc_row0 - w);
-            tma_prefetch_3d(&tmVb, h + NS, doc_row0 - w);
+          if (elect_one()) {
+            if (h + NS < p.H) {  // L2 prefetch of the boxes this stage will hold next round
+              if (p.doc_rows) tma_prefetch_3d(&tmQ, h + NS, doc_row0);
+              tma_prefetch_3d(&tmKb, h + NS, doc_row0 - w);
+              tma_prefetch_3d(&tmVb, h + NS, doc_row0 - w);
+            }
+            mbar_expect_tx(fb, bytes);
+            if (p.doc_rows) tma_load_3d(q_buf(s), &tmQ, h, doc_row0, fb);
+            tma_load_3d(kb_buf(s), &tmKb, h, doc_row0 - w, fb);
+            tma_load_3d(vb_buf(s), &tmVb, h, doc_row0 - w, fb);
+            tma_load_3d(kg_buf(s), &tmKg, h, g.start, fb);
+            tma_load_3d(vg_buf(s), &tmVg, h, g.start, fb);
+            tma_load_3d(qf_buf(s), &tmQf, h, g.start, fb);
           }
-          mbar_expect_tx(fb, bytes);
-          if (p.doc_rows) tma_load_3d(q_buf(s), &tmQ, h, doc_row0, fb);
-          tma_load_3d(kb_buf(s), &tmKb, h, doc_row0 - w, fb);
-          tma_load_3d(vb_buf(s), &tmVb, h, doc_row0 - w, fb);
-          tma_load_3d(kg_buf(s), &tmKg, h, g.start, fb);
-          tma_load_3d(vg_buf(s), &tmVg, h, g.start, fb);
-          tma_load_3d(qf_buf(s), &tmQf, h, g.start, fb);
+          __syncwarp();
         }
       }
     }
@@ -576,7 +591,8 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
                     pack_bf16(o[2 * np + 1][2] * i1, o[2 * np + 1][3] * i1));
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0) tma_store_3d(&tmO, ob + wr0 * ROWB, h, doc_row0 + wr0);
+          if (elect_one()) tma_store_3d(&tmO, ob + wr0 * ROWB, h, doc_row0 + wr0);
+          __syncwarp();
         } else {
         __nv_bfloat16* out_h = p.out + h * p.dout + 2 * tq;
         if (ra < n_doc) {
@@ -700,10 +716,11 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         }
       }
       __syncwarp();
-      if (lane == 0) {
+      if (elect_one()) {  // the same lane that issued this warp's O store
         if (active) tma_store_wait_read();  // the stage's Q rows are about to be refilled
         mbar_arrive(empty_bar + 8 * s);
       }
+      __syncwarp();
     }
 
   }
