@@ -42,7 +42,16 @@ constexpr int MAX_W = 96;  // Kb box rows 64 + 2w <= 256 (TMA box limit)
 constexpr int REC = D + 4; // split-softmax record: m, l, pad, pad, acc[D] (16B-aligned acc)
 // Resident CTAs per SM the register/smem budget targets (measured on B200,
 // s=4099 H=12: 3 CTAs / 2 stages is best for w <= 8, 2 CTAs / 3 stages above).
-__host__ __device__ constexpr int min_ctas(int nbc) { return nbc == 1 ? 3 : 2; }
+#ifndef SC_BAND_CTAS1
+#define SC_BAND_CTAS1 3  // resident CTAs per SM of the single-chunk (w <= 8) variant
+#endif
+#ifndef SC_BAND_PF
+// L2 prefetch (cp.async.bulk.prefetch.tensor) of the boxes SC_BAND_PF x NS items ahead; 0 = none.
+// Measured on B200: off 4.35 us vs on 4.83 us per sequence-layer at w=4 (88% vs 79% of HBM): the
+// stage loads are already in flight NS items ahead and the extra L2 fills only compete with them.
+#define SC_BAND_PF 0
+#endif
+__host__ __device__ constexpr int min_ctas(int nbc) { return nbc == 1 ? SC_BAND_CTAS1 : 2; }
 
 struct Params {
   int nseq, H, w, kb_rows, fneed, fmax, padding;
@@ -396,10 +405,10 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
           if (it >= NS) mbar_wait(empty_bar + 8 * s, ((it / NS) & 1) ^ 1);
           const uint32_t fb = full_bar + 8 * s;
           if (elect_one()) {
-            if (h + NS < p.H) {  // L2 prefetch of the boxes this stage will hold next round
-              if (p.doc_rows) tma_prefetch_3d(&tmQ, h + NS, doc_row0);
-              tma_prefetch_3d(&tmKb, h + NS, doc_row0 - w);
-              tma_prefetch_3d(&tmVb, h + NS, doc_row0 - w);
+            if (SC_BAND_PF > 0 && h + SC_BAND_PF * NS < p.H) {  // L2 prefetch of the boxes of a later item of this tile
+              if (p.doc_rows) tma_prefetch_3d(&tmQ, h + SC_BAND_PF * NS, doc_row0);
+              tma_prefetch_3d(&tmKb, h + SC_BAND_PF * NS, doc_row0 - w);
+              tma_prefetch_3d(&tmVb, h + SC_BAND_PF * NS, doc_row0 - w);
             }
             mbar_expect_tx(fb, bytes);
             if (p.doc_rows) tma_load_3d(q_buf(s), &tmQ, h, doc_row0, fb);

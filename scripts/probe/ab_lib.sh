@@ -2,7 +2,7 @@
 # A/B two builds of the library on one box: band/tc sweep + bench in-step roofline, alternating.
 cd $GRAFT_REPO_ROOT
 for rep in 1 2; do
-for L in old new; do
+for L in ${LIBS:-old new}; do
   echo "== $L (rep $rep)"
   SC_LIB_PATH=paper_2312_17649_b200/_lib_ab/$L.so timeout 300 python scripts/sweep_quick.py > gpurun_out/ab_$L.jsonl 2>&1
   python scripts/show_sweep.py gpurun_out/ab_$L.jsonl 2>/dev/null | sed -n 2,4p
