@@ -42,6 +42,9 @@ constexpr int MAX_W = 96;  // Kb box rows 64 + 2w <= 256 (TMA box limit)
 constexpr int REC = D + 4; // split-softmax record: m, l, pad, pad, acc[D] (16B-aligned acc)
 // Resident CTAs per SM the register/smem budget targets (measured on B200,
 // s=4099 H=12: 3 CTAs / 2 stages is best for w <= 8, 2 CTAs / 3 stages above).
+#ifndef SC_BAND_L2PROMO
+#define SC_BAND_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 #ifndef SC_BAND_CTAS1
 #define SC_BAND_CTAS1 3  // resident CTAs per SM of the single-chunk (w <= 8) variant
 #endif
@@ -830,7 +833,7 @@ static bool make_map(CUtensorMap* m, const void* base, int d, int heads, int64_t
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             SC_BAND_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, Params);
