@@ -22,11 +22,10 @@ extern "C" size_t sc_attn_workspace_bytes(int32_t nseq, int32_t total_tokens, in
 
 // AUTO kernel choice by doc window: the mma.sync band kernel while the band is
 // narrow (HBM-bound regime), the tcgen05 kernel once it is a dense contraction.
-// Crossover measured on B200 (s=4099, H=12, 64 sequences, us/seq-layer):
-// band 7.0 / 12.1 / 16.7 vs tcgen05 13.1 / ~13.5 / 13.7 at w = 40 / 48 / 64;
-// the band kernel's cost steps with ceil((16+2w)/32) key chunks, so it keeps
-// w <= 56 (four chunks).
-static constexpr int kBandMaxWindow = 56;
+// Crossover measured on B200 (s=4099, H=12, 64 sequences, us/seq-layer, round 2):
+// band 5.4 / 6.9 / 11.6 / 15.8 vs tcgen05 9.8 / 10.8 / 10.8 / 10.8 at w = 24 / 40 / 48 / 64;
+// the band kernel's cost steps with ceil((16+2w)/32) key chunks, so it keeps w <= 40 (three).
+static constexpr int kBandMaxWindow = 40;  // measured crossover (round 2): band 6.9 us at w=40, tcgen05 10.8 vs band 11.6 at w=48
 
 extern "C" int sc_attn_fwd(const void* q, const void* k, const void* v, int64_t row_stride,
                            void* out, int64_t out_row_stride, const int32_t* cu_seqlens,

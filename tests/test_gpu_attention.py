@@ -412,4 +412,4 @@ def test_fast_path_never_uses_generic_for_envelope_shapes(P):
     for d in (32, 64):
         for shapes in ([(62, 500), (3, 90)], [(10, 4086)]):
             for w in (4, 64):
-                _packed_vs_oracle(P, shapes, 2, d, "sparse", w, "exclude", "band" if w <= 56 else "tc")
+                _packed_vs_oracle(P, shapes, 2, d, "sparse", w, "exclude", "band" if w <= 40 else "tc")
