@@ -62,6 +62,7 @@ struct Params {
   int link_cls, link_query;
   int doc_rows;  // 0: head rows only (doc rows computed by the tcgen05 kernel)
   int dout;      // head_dim (32 or 64; smem rows are always 64 dims, zero-padded)
+  int Ht;        // heads of the layout (records / outputs); H counts items per tile (H / 2 in pair mode)
   // head rows (cls = group 0, query = group 1): links to cls / query keys, doc FULL
   int hl[2][2], hdoc[2];
   int ntiles_max;      // record index of sequence j's global-key record = ntiles_max + j
@@ -287,6 +288,81 @@ __device__ __forceinline__ void pv8(uint32_t vbuf, int key0, int lane, const flo
   }
 }
 
+// Head-pair mode (head_dim 32, two heads per 64-dim smem row): the same contractions restricted
+// to one head's 32 dims, hh = 0 (dims 0-31: k-steps / n-tiles of the first head) or 1.
+__device__ __forceinline__ void qk16_hh(uint32_t kbuf, int key0, const LaneOff& lo, const uint32_t (&qa)[4][4],
+                                        float (&s0)[4], float (&s1)[4], int hh) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s0[e] = s1[e] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int ks = 2 * hh + k;
+    uint32_t b[4];
+    ldsm_x4(kbuf + key0 * ROWB + lo.k[ks], b);
+    mma16816(s0, qa[ks], b[0], b[1]);
+    mma16816(s1, qa[ks], b[2], b[3]);
+  }
+}
+__device__ __forceinline__ void pv16_hh(uint32_t vbuf, int key0, const LaneOff& lo, const float (&p0)[4],
+                                        const float (&p1)[4], float (&o)[8][4], int hh) {
+  uint32_t a[4] = {pack_bf16(p0[0], p0[1]), pack_bf16(p0[2], p0[3]), pack_bf16(p1[0], p1[1]),
+                   pack_bf16(p1[2], p1[3])};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int np = 2 * hh + k;
+    uint32_t b[4];
+    ldsm_x4_t(vbuf + key0 * ROWB + lo.v[np], b);
+    mma16816(o[2 * np], a, b[0], b[1]);
+    mma16816(o[2 * np + 1], a, b[2], b[3]);
+  }
+}
+__device__ __forceinline__ void qk8_hh(uint32_t kbuf, int key0, int lane, const uint32_t (&qa)[4][4], float (&s0)[4],
+                                       int hh) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s0[e] = 0.f;
+  uint32_t b[4];
+  ldsm_x4(swz(kbuf, key0 + (lane & 7), 4 * hh + (lane >> 3)), b);
+  mma16816(s0, qa[2 * hh], b[0], b[1]);
+  mma16816(s0, qa[2 * hh + 1], b[2], b[3]);
+}
+__device__ __forceinline__ void pv8_hh(uint32_t vbuf, int key0, int lane, const float (&p0)[4], float (&o)[8][4],
+                                       int hh) {
+  const uint32_t a0 = pack_bf16(p0[0], p0[1]), a1 = pack_bf16(p0[2], p0[3]);
+  uint32_t b[4];
+  ldsm_x4_t(swz(vbuf, key0 + (lane & 7), 4 * hh + (lane >> 3)), b);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) mma1688(o[4 * hh + i], a0, a1, b[i]);
+}
+// unaligned-key (lane-addressed) variants for the full-row records (key0 = w + 16 np)
+__device__ __forceinline__ void qk16l_hh(uint32_t kbuf, int key0, int lane, const uint32_t (&qa)[4][4],
+                                         float (&s0)[4], float (&s1)[4], int hh) {
+  const int krow = key0 + (lane & 7) + ((lane >> 4) << 3);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s0[e] = s1[e] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int ks = 2 * hh + k;
+    uint32_t b[4];
+    ldsm_x4(swz(kbuf, krow, ks * 2 + ((lane >> 3) & 1)), b);
+    mma16816(s0, qa[ks], b[0], b[1]);
+    mma16816(s1, qa[ks], b[2], b[3]);
+  }
+}
+__device__ __forceinline__ void pv16l_hh(uint32_t vbuf, int key0, int lane, const float (&p0)[4],
+                                         const float (&p1)[4], float (&o)[8][4], int hh) {
+  uint32_t a[4] = {pack_bf16(p0[0], p0[1]), pack_bf16(p0[2], p0[3]), pack_bf16(p1[0], p1[1]),
+                   pack_bf16(p1[2], p1[3])};
+  const int vrow = key0 + (lane & 7) + (((lane >> 3) & 1) << 3);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int np = 2 * hh + k;
+    uint32_t b[4];
+    ldsm_x4_t(swz(vbuf, vrow, np * 2 + (lane >> 4)), b);
+    mma16816(o[2 * np], a, b[0], b[1]);
+    mma16816(o[2 * np + 1], a, b[2], b[3]);
+  }
+}
+
 // Online-softmax update over NB n8 blocks of RAW logits (masked to -inf) for
 // rows (g, g+8).  m is kept in raw-logit units; c2 = log2(e)/scale.  Overwrites s with P.
 // kFresh: o is still zero (first update of a row block) -> skip the O rescale.
@@ -338,7 +414,8 @@ __device__ __forceinline__ void zero_o(float (&o)[8][4]) {
 // NBC: band chunks of 32 keys per 16-row warp block (ceil((16+2w)/32)).
 // GR: global rows staged per head (16 or 32).  NS: pipeline stages.
 // NBB: band n8 blocks of the single-shot path (NBC = 1): 3 when 16 + 2w <= 24.
-template <int NBC, int GR, int NS, int NBB = 4>
+// PAIR (head_dim 32, NBC = 1): items are head pairs (2h, 2h + 1) sharing the 64-dim smem rows.
+template <int NBC, int GR, int NS, int NBB = 4, int PAIR = 0>
 __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQf,
     const __grid_constant__ CUtensorMap tmKg, const __grid_constant__ CUtensorMap tmVg,
@@ -526,7 +603,48 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
         if (ninv_a > 0.f) { m0 = 0.f; l0 = tq == 0 ? ninv_a : 0.f; }
         if (ninv_b > 0.f) { m1 = 0.f; l1 = tq == 0 ? ninv_b : 0.f; }
-        if constexpr (NBC == 1) {
+        float pinv0 = 0.f, pinv1 = 0.f;  // PAIR: 1 / l of head 2h + 1 (its half of O: n-tiles 4-7)
+        if constexpr (NBC == 1 && PAIR) {
+          // Head pair, single shot per head: heads 2h (dims 0-31) and 2h + 1 (dims 32-63) share the
+          // staged rows; two score sets and softmaxes, one O fragment (n-tiles 0-3 / 4-7).
+          constexpr int NG = GR / 8;
+          float ma0 = m0, ma1 = m1, la0 = l0, la1 = l1;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            float sc[NG + NBB][4];
+  #pragma unroll
+            for (int gc = 0; gc < GR / 16; ++gc) qk16_hh(kg_buf(s), gc * 16, LO, qa, sc[2 * gc], sc[2 * gc + 1], hh);
+            qk16_hh(kb_buf(s), wr0, LO, qa, sc[NG], sc[NG + 1], hh);
+            if constexpr (NBB == 4) qk16_hh(kb_buf(s), wr0 + 16, LO, qa, sc[NG + 2], sc[NG + 3], hh);
+            else qk8_hh(kb_buf(s), wr0 + 16, lane, qa, sc[NG + 2], hh);
+  #pragma unroll
+            for (int nb = 0; nb < NG; ++nb)
+  #pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (!((gmask[nb >> 1] >> ((nb & 1) * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+  #pragma unroll
+            for (int nb = 0; nb < NBB; ++nb)
+  #pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (!((bmask[0] >> (nb * 4 + e)) & 1)) sc[NG + nb][e] = -INFINITY;
+            float hm0 = ma0, hm1 = ma1, hl0 = la0, hl1 = la1;
+            softmax_update<NG + NBB, true>(sc, c2, hm0, hm1, hl0, hl1, o);
+  #pragma unroll
+            for (int gc = 0; gc < GR / 16; ++gc) pv16_hh(vg_buf(s), gc * 16, LO, sc[2 * gc], sc[2 * gc + 1], o, hh);
+            pv16_hh(vb_buf(s), wr0, LO, sc[NG], sc[NG + 1], o, hh);
+            if constexpr (NBB == 4) pv16_hh(vb_buf(s), wr0 + 16, LO, sc[NG + 2], sc[NG + 3], o, hh);
+            else pv8_hh(vb_buf(s), wr0 + 16, lane, sc[NG + 2], o, hh);
+            if (hh == 0) { m0 = hm0; m1 = hm1; l0 = hl0; l1 = hl1; }  // head 2h
+            else { ma0 = hm0; ma1 = hm1; la0 = hl0; la1 = hl1; }      // head 2h + 1
+          }
+          // head 2h + 1's row sums ride in (la0, la1); normalise its half of O here
+          la0 += __shfl_xor_sync(0xffffffffu, la0, 1);
+          la0 += __shfl_xor_sync(0xffffffffu, la0, 2);
+          la1 += __shfl_xor_sync(0xffffffffu, la1, 1);
+          la1 += __shfl_xor_sync(0xffffffffu, la1, 2);
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(pinv0) : "f"(la0));
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(pinv1) : "f"(la1));
+        } else if constexpr (NBC == 1) {
           // Single shot: all keys of the row block (globals + band) in one softmax.
           constexpr int NG = GR / 8;
           float sc[NG + NBB][4];
@@ -596,11 +714,13 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
           // 4-byte stores per row.
           const uint32_t ob = q_buf(s);
   #pragma unroll
-          for (int np = 0; np < 4; ++np)
+          for (int np = 0; np < 4; ++np) {
+            const float a0 = (PAIR && np >= 2) ? pinv0 : i0, a1 = (PAIR && np >= 2) ? pinv1 : i1;
             stsm_x4(ob + wr0 * ROWB + LO.v[np],
-                    pack_bf16(o[2 * np][0] * i0, o[2 * np][1] * i0), pack_bf16(o[2 * np][2] * i1, o[2 * np][3] * i1),
-                    pack_bf16(o[2 * np + 1][0] * i0, o[2 * np + 1][1] * i0),
-                    pack_bf16(o[2 * np + 1][2] * i1, o[2 * np + 1][3] * i1));
+                    pack_bf16(o[2 * np][0] * a0, o[2 * np][1] * a0), pack_bf16(o[2 * np][2] * a1, o[2 * np][3] * a1),
+                    pack_bf16(o[2 * np + 1][0] * a0, o[2 * np + 1][1] * a0),
+                    pack_bf16(o[2 * np + 1][2] * a1, o[2 * np + 1][3] * a1));
+          }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (elect_one()) tma_store_3d(&tmO, ob + wr0 * ROWB, h, doc_row0 + wr0);
@@ -610,21 +730,28 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         if (ra < n_doc) {
           uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq) * p.ld_out);
   #pragma unroll
-          for (int nb = 0; nb < 8; ++nb)
-            if (nb * 8 < p.dout) dst[nb * 4] = pack_bf16(o[nb][0] * i0, o[nb][1] * i0);
+          for (int nb = 0; nb < 8; ++nb) {
+            const float a0 = (PAIR && nb >= 4) ? pinv0 : i0;
+            if (nb * 8 < p.dout) dst[nb * 4] = pack_bf16(o[nb][0] * a0, o[nb][1] * a0);
+          }
         }
         if (rb < n_doc) {
           uint32_t* dst = reinterpret_cast<uint32_t*>(out_h + (int64_t)(doc_row0 + wr0 + gq + 8) * p.ld_out);
   #pragma unroll
-          for (int nb = 0; nb < 8; ++nb)
-            if (nb * 8 < p.dout) dst[nb * 4] = pack_bf16(o[nb][2] * i1, o[nb][3] * i1);
+          for (int nb = 0; nb < 8; ++nb) {
+            const float a1 = (PAIR && nb >= 4) ? pinv1 : i1;
+            if (nb * 8 < p.dout) dst[nb * 4] = pack_bf16(o[nb][2] * a1, o[nb][3] * a1);
+          }
         }
         }
       }
 
       // Full-row split-softmax partials over the tile's 64 own doc keys; the
       // designated warp rotates with the head so the extra work spreads evenly.
+      // (PAIR: both heads of the item, 32 dims each, records in the 64-dim layout's first half.)
       if (warp == (h & (NDOCW - 1))) {
+  #pragma unroll
+        for (int hh = 0; hh < (PAIR ? 2 : 1); ++hh) {
   #pragma unroll
         for (int fc = 0; fc < GR / 16; ++fc) {
           if (fc * 16 < p.fneed) {
@@ -632,7 +759,10 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
             load_q(qf_buf(s), fc * 16, LO, qa);
             float sc[8][4];
   #pragma unroll
-            for (int np = 0; np < 4; ++np) qk16(kb_buf(s), w + np * 16, lane, qa, sc[2 * np], sc[2 * np + 1]);
+            for (int np = 0; np < 4; ++np) {
+              if constexpr (PAIR) qk16l_hh(kb_buf(s), w + np * 16, lane, qa, sc[2 * np], sc[2 * np + 1], hh);
+              else qk16(kb_buf(s), w + np * 16, lane, qa, sc[2 * np], sc[2 * np + 1]);
+            }
   #pragma unroll
             for (int nb = 0; nb < 8; ++nb)
   #pragma unroll
@@ -643,27 +773,35 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
             float fm0 = -INFINITY, fm1 = -INFINITY, fl0 = 0.f, fl1 = 0.f;
             softmax_update<8, true>(sc, c2, fm0, fm1, fl0, fl1, o);
   #pragma unroll
-            for (int kp = 0; kp < 4; ++kp) pv16(vb_buf(s), w + kp * 16, lane, sc[2 * kp], sc[2 * kp + 1], o);
+            for (int kp = 0; kp < 4; ++kp) {
+              if constexpr (PAIR) pv16l_hh(vb_buf(s), w + kp * 16, lane, sc[2 * kp], sc[2 * kp + 1], o, hh);
+              else pv16(vb_buf(s), w + kp * 16, lane, sc[2 * kp], sc[2 * kp + 1], o);
+            }
             fl0 += __shfl_xor_sync(0xffffffffu, fl0, 1);
             fl0 += __shfl_xor_sync(0xffffffffu, fl0, 2);
             fl1 += __shfl_xor_sync(0xffffffffu, fl1, 1);
             fl1 += __shfl_xor_sync(0xffffffffu, fl1, 2);
             const float to_nat = c2 * 0.69314718055994530942f;  // raw logit -> natural units (1/scale)
+            const int ht = PAIR ? 2 * h + hh : h;                 // head of the layout
   #pragma unroll
             for (int half = 0; half < 2; ++half) {
               const int f = fc * 16 + gq + 8 * half;
               if (f >= p.fneed) continue;
-              float* rec = p.partials + (((int64_t)tile * p.H + h) * p.fmax + f) * REC;
+              float* rec = p.partials + (((int64_t)tile * p.Ht + ht) * p.fmax + f) * REC;
               if (tq == 0) {
                 rec[0] = (half ? fm1 : fm0) * to_nat;
                 rec[1] = half ? fl1 : fl0;
               }
   #pragma unroll
-              for (int nb = 0; nb < 8; ++nb)
+              for (int nb = 0; nb < 8; ++nb) {
+                const int src = PAIR ? (nb & 3) + 4 * hh : nb;  // PAIR: the head's 32 dims, then zeros
+                const bool live = !PAIR || nb < 4;
                 *reinterpret_cast<float2*>(rec + 4 + nb * 8 + 2 * tq) =
-                    make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
+                    live ? make_float2(o[src][2 * half], o[src][2 * half + 1]) : make_float2(0.f, 0.f);
+              }
             }
           }
+        }
         }
       }
       // Head rows over the global keys (first tile of the sequence only): rows
@@ -672,13 +810,18 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
       // others (sparse: query rows) are final and stored here.
       if (r0 == 0 && warp == ((h + 2) & (NDOCW - 1))) {
   #pragma unroll
+        for (int hh = 0; hh < (PAIR ? 2 : 1); ++hh) {
+  #pragma unroll
         for (int fc = 0; fc < GR / 16; ++fc) {
           if (fc * 16 < G) {
             uint32_t qa[4][4];
             load_q(qf_buf(s), fc * 16, LO, qa);
             float sc[GR / 8][4];
   #pragma unroll
-            for (int gc = 0; gc < GR / 16; ++gc) qk16(kg_buf(s), gc * 16, LO, qa, sc[2 * gc], sc[2 * gc + 1]);
+            for (int gc = 0; gc < GR / 16; ++gc) {
+              if constexpr (PAIR) qk16_hh(kg_buf(s), gc * 16, LO, qa, sc[2 * gc], sc[2 * gc + 1], hh);
+              else qk16(kg_buf(s), gc * 16, LO, qa, sc[2 * gc], sc[2 * gc + 1]);
+            }
   #pragma unroll
             for (int nb = 0; nb < GR / 8; ++nb)
   #pragma unroll
@@ -694,12 +837,16 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
             float hm0 = -INFINITY, hm1 = -INFINITY, hl0 = 0.f, hl1 = 0.f;
             softmax_update<GR / 8, true>(sc, c2, hm0, hm1, hl0, hl1, o);
   #pragma unroll
-            for (int gc = 0; gc < GR / 16; ++gc) pv16(vg_buf(s), gc * 16, LO, sc[2 * gc], sc[2 * gc + 1], o);
+            for (int gc = 0; gc < GR / 16; ++gc) {
+              if constexpr (PAIR) pv16_hh(vg_buf(s), gc * 16, LO, sc[2 * gc], sc[2 * gc + 1], o, hh);
+              else pv16(vg_buf(s), gc * 16, LO, sc[2 * gc], sc[2 * gc + 1], o);
+            }
             hl0 += __shfl_xor_sync(0xffffffffu, hl0, 1);
             hl0 += __shfl_xor_sync(0xffffffffu, hl0, 2);
             hl1 += __shfl_xor_sync(0xffffffffu, hl1, 1);
             hl1 += __shfl_xor_sync(0xffffffffu, hl1, 2);
             const float to_nat = c2 * 0.69314718055994530942f;
+            const int ht = PAIR ? 2 * h + hh : h;  // head of the layout
   #pragma unroll
             for (int half = 0; half < 2; ++half) {
               const int f = fc * 16 + gq + 8 * half;
@@ -707,24 +854,31 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
               const int grp = f == 0 ? 0 : 1;
               const float mm = half ? hm1 : hm0, ll = half ? hl1 : hl0;
               if ((hdoc_bits >> grp) & 1) {
-                float* rec = p.partials + (((int64_t)(p.ntiles_max + j) * p.H + h) * p.fmax + f) * REC;
+                float* rec = p.partials + (((int64_t)(p.ntiles_max + j) * p.Ht + ht) * p.fmax + f) * REC;
                 if (tq == 0) {
                   rec[0] = ll > 0.f ? mm * to_nat : -INFINITY;
                   rec[1] = ll;
                 }
   #pragma unroll
-                for (int nb = 0; nb < 8; ++nb)
+                for (int nb = 0; nb < 8; ++nb) {
+                  const int src = PAIR ? (nb & 3) + 4 * hh : nb;
+                  const bool live = !PAIR || nb < 4;
                   *reinterpret_cast<float2*>(rec + 4 + nb * 8 + 2 * tq) =
-                      make_float2(o[nb][2 * half], o[nb][2 * half + 1]);
+                      live ? make_float2(o[src][2 * half], o[src][2 * half + 1]) : make_float2(0.f, 0.f);
+                }
               } else {
                 const float inv = ll > 0.f ? 1.f / ll : 0.f;
-                uint32_t* dst = reinterpret_cast<uint32_t*>(p.out + (int64_t)(g.start + f) * p.ld_out + h * p.dout + 2 * tq);
+                const int hdim = PAIR ? 32 : p.dout;  // this head's dims
+                uint32_t* dst = reinterpret_cast<uint32_t*>(p.out + (int64_t)(g.start + f) * p.ld_out + ht * hdim + 2 * tq);
   #pragma unroll
-                for (int nb = 0; nb < 8; ++nb)
-                  if (nb * 8 < p.dout) dst[nb * 4] = pack_bf16(o[nb][2 * half] * inv, o[nb][2 * half + 1] * inv);
+                for (int nb = 0; nb < 8; ++nb) {
+                  const int src = PAIR ? nb + 4 * hh : nb;
+                  if (nb * 8 < hdim) dst[nb * 4] = pack_bf16(o[src & 7][2 * half] * inv, o[src & 7][2 * half + 1] * inv);
+                }
               }
             }
           }
+        }
         }
       }
       __syncwarp();
@@ -846,15 +1000,15 @@ constexpr int stages_for() {
   return (3 * stage_bytes <= budget) ? 3 : 2;
 }
 
-template <int NBC, int GR, int NBB = 4>
+template <int NBC, int GR, int NBB = 4, int PAIR = 0>
 static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, cudaStream_t st) {
   constexpr int NS = stages_for<NBC, GR>();
   constexpr int stage_bytes = (BM + 3 * GR + 2 * (48 + 32 * NBC)) * ROWB;
   constexpr size_t smem = (size_t)NS * stage_bytes + 2 * NS * 8 + 64 + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS, NBB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS, NBB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS, NBB, PAIR>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS, NBB, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess) {
       set_error("band kernel: shared memory request of %zu bytes failed", smem);
       return SC_ERR_UNSUPPORTED;
@@ -870,14 +1024,16 @@ static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, c
     if (num_sms <= 0) num_sms = 148;
   }
   const unsigned slots = (unsigned)(num_sms * min_ctas(NBC));
-  band_attn_kernel<NBC, GR, NS, NBB><<<grid < slots ? grid : slots, NTHREADS, smem, st>>>(
+  band_attn_kernel<NBC, GR, NS, NBB, PAIR><<<grid < slots ? grid : slots, NTHREADS, smem, st>>>(
       maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
   SC_CHECK_LAUNCH("band_attn_kernel");
   return SC_OK;
 }
 
 template <int GR>
-static int launch_gr(int nbc, const CUtensorMap* maps, const Params& p, unsigned grid, cudaStream_t st) {
+static int launch_gr(int nbc, bool pair, const CUtensorMap* maps, const Params& p, unsigned grid, cudaStream_t st) {
+  if (pair && nbc == 1)
+    return p.w <= 4 ? launch_one<1, GR, 3, 1>(maps, p, grid, st) : launch_one<1, GR, 4, 1>(maps, p, grid, st);
   switch (nbc) {
     case 1: return p.w <= 4 ? launch_one<1, GR, 3>(maps, p, grid, st) : launch_one<1, GR>(maps, p, grid, st);
     case 2: return launch_one<2, GR>(maps, p, grid, st);
@@ -932,8 +1088,14 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   if (need > ws_bytes || (need && !ws)) return unsupported("workspace too small");
   const int GR = (max_qgroup_len + 1 <= 16) ? 16 : (max_qgroup_len + 1 <= 32 ? 32 : 64);
 
+  // head_dim 32, single-chunk windows: items are head pairs (64-dim rows of two adjacent heads);
+  // SC_BAND_NOPAIR=1 keeps one zero-padded head per item (measurement A/B)
+  const int nbc0 = (16 + 2 * w + 31) / 32;
+  static int nopair = -1;
+  if (nopair < 0) nopair = getenv("SC_BAND_NOPAIR") ? atoi(getenv("SC_BAND_NOPAIR")) : 0;
+  const bool pair = doc_rows && a.d == 32 && a.H % 2 == 0 && nbc0 == 1 && !nopair;
   CUtensorMap maps[7];
-  const int dd = a.d, H = a.H;
+  const int dd = pair ? 64 : a.d, H = pair ? a.H / 2 : a.H;
   if (!make_map(&maps[0], a.q, dd, H, a.T, a.ld, BM) || !make_map(&maps[1], a.q, dd, H, a.T, a.ld, GR) ||
       !make_map(&maps[2], a.k, dd, H, a.T, a.ld, GR) || !make_map(&maps[3], a.v, dd, H, a.T, a.ld, GR) ||
       !make_map(&maps[4], a.k, dd, H, a.T, a.ld, BM + 2 * w) ||
@@ -942,7 +1104,7 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
     return unsupported("cuTensorMapEncodeTiled failed");
 
   Params p;
-  p.nseq = a.nseq; p.H = a.H; p.w = w; p.doc_rows = doc_rows ? 1 : 0; p.dout = a.d;
+  p.nseq = a.nseq; p.H = H; p.Ht = a.H; p.w = w; p.doc_rows = doc_rows ? 1 : 0; p.dout = pair ? 64 : a.d;
   const int nbc = (16 + 2 * w + 31) / 32;
   p.kb_rows = 48 + 32 * nbc;
   p.fneed = fneed; p.fmax = fneed; p.padding = a.padding;
@@ -967,12 +1129,15 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   // Doc rows + head rows over the global keys (first tile of each sequence).
   // (seq_head_base is unused: head rows are addressed through cu_seqlens.)
   (void)seq_head_base;
-  int rc = GR == 16 ? launch_gr<16>(nbc, maps, p, grid, st)
-         : GR == 32 ? launch_gr<32>(nbc, maps, p, grid, st)
-                    : launch_gr<64>(nbc, maps, p, grid, st);
+  int rc = GR == 16 ? launch_gr<16>(nbc, pair, maps, p, grid, st)
+         : GR == 32 ? launch_gr<32>(nbc, pair, maps, p, grid, st)
+                    : launch_gr<64>(nbc, pair, maps, p, grid, st);
   if (rc || fneed == 0) return rc;
+  Params pm = p;  // the merge walks the layout's heads
+  pm.H = a.H;
+  pm.dout = a.d;
   const int64_t items = (int64_t)a.nseq * a.H * fneed;
-  merge_full_rows_kernel<<<(unsigned)((items + MERGE_WARPS - 1) / MERGE_WARPS), MERGE_WARPS * 32, 0, st>>>(p);
+  merge_full_rows_kernel<<<(unsigned)((items + MERGE_WARPS - 1) / MERGE_WARPS), MERGE_WARPS * 32, 0, st>>>(pm);
   SC_CHECK_LAUNCH("merge_full_rows_kernel");
   return SC_OK;
 }
@@ -984,7 +1149,7 @@ int launch_head_merge(const AttnArgs& a, const int32_t* seq_tile_base, int tile_
   const int fneed = full_rows_needed(L, max_qgroup_len);
   if (fneed == 0) return SC_OK;
   Params p{};
-  p.nseq = a.nseq; p.H = a.H; p.fneed = fneed; p.fmax = fneed; p.dout = a.d;
+  p.nseq = a.nseq; p.H = a.H; p.Ht = a.H; p.fneed = fneed; p.fmax = fneed; p.dout = a.d;
   p.cu = a.cu; p.qlen = a.qlen; p.tile_base = seq_tile_base;
   p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
   p.partials = static_cast<float*>(ws);

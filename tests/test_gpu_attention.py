@@ -395,6 +395,16 @@ def test_head_dim_32_fast_kernels_vs_oracle(P, algo, name, w, pad):
     _packed_vs_oracle(P, shapes, 12, 32, name, w, pad, algo)
 
 
+@pytest.mark.parametrize("H,name,w,pad", [(12, "longformer", 4, "exclude"), (12, "longformer", 8, "zero-logit"),
+                                          (3, "sparse", 4, "exclude"), (2, "sparse", 8, "zero-logit")])
+def test_head_dim_32_band_head_pairs_vs_oracle(P, H, name, w, pad):
+    """head_dim 32 at w <= 8: the band kernel takes two adjacent heads per item (64-dim rows); head-row
+    records for every full row (longformer: query rows too), odd H falls back to one
+    zero-padded head per item."""
+    shapes = [(10, 300), (1, 1), (7, 130), (20, 127), (10, 700), (3, 64)]
+    _packed_vs_oracle(P, shapes, H, 32, name, w, pad, "band")
+
+
 @pytest.mark.parametrize("algo,name,w,pad", [("band", "sparse", 4, "exclude"), ("band", "longformer", 4, "zero-logit"),
                                              ("band", "sparse", 40, "exclude"), ("tc", "sparse", 64, "exclude"),
                                              ("tc", "longformer", 100, "exclude"), ("tc", "full", math.inf, "exclude"),
