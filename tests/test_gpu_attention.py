@@ -123,11 +123,12 @@ def test_attention_bf16_vs_oracle(P, idx):
     np.testing.assert_allclose(got, ref, atol=2e-2, rtol=0)
 
 
-@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-def test_sparse_query_rows_bitwise_independent_of_doc_and_cls(P, dtype):
-    """GPU analogue of T/test_attention.py:212-226."""
+@pytest.mark.parametrize("dtype,n", [(torch.float32, 300), (torch.bfloat16, 300), (torch.bfloat16, 4086),
+                                     (torch.float32, 4086)])
+def test_sparse_query_rows_bitwise_independent_of_doc_and_cls(P, dtype, n):
+    """GPU analogue of T/test_attention.py:212-226 (also at the headline s=4099)."""
     rng = np.random.default_rng(8)
-    m, n, H, d = 10, 300, 4, 64
+    m, H, d = 10, 4, 64
     s = m + n + 3
     x = rng.standard_normal((3, H, s, d))
     pat = P.sparse_pattern(4)
@@ -180,6 +181,22 @@ def test_full_size_document_vs_oracle(P, w):
     refb = np.concatenate(O.apply_pattern(spans, O.split_groups(spans, *xb), O.make_pattern("sparse", w), 8.0), axis=-2)
     gotb = run_attention(P, xb, m, n, P.sparse_pattern(w), "exclude", torch.bfloat16)
     np.testing.assert_allclose(gotb, refb, atol=2e-2, rtol=0)
+
+
+@pytest.mark.parametrize("name", ["full", "longformer"])
+def test_full_size_dense_patterns_vs_oracle(P, name):
+    """s = 4099 with whole-document rows: the full pattern (R/attention.py:528-537) and longformer with
+    w = inf, bf16 on the tcgen05 kernel and fp32 on the generic one, against the fp64 oracle."""
+    rng = np.random.default_rng(6)
+    m, n, d, H = 10, 4086, 64, 2
+    x = rng.standard_normal((3, H, m + n + 3, d)).astype(np.float32)
+    spans = cases.attn_spans(m, n)
+    pat_o, pat_p = O.make_pattern(name, math.inf), P.make_pattern(name, math.inf)
+    ref = np.concatenate(O.apply_pattern(spans, O.split_groups(spans, *x.astype(np.float64)), pat_o, 8.0), axis=-2)
+    np.testing.assert_allclose(run_attention(P, x, m, n, pat_p, "exclude", torch.float32), ref, atol=1e-4, rtol=0)
+    xb = torch.from_numpy(x).to(torch.bfloat16).double().numpy()
+    refb = np.concatenate(O.apply_pattern(spans, O.split_groups(spans, *xb), pat_o, 8.0), axis=-2)
+    np.testing.assert_allclose(run_attention(P, xb, m, n, pat_p, "exclude", torch.bfloat16), refb, atol=2e-2, rtol=0)
 
 
 def test_compat_group_attention_numpy_roundtrip(P):
