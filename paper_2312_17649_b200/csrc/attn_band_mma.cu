@@ -11,14 +11,15 @@
 //                        rows under longformer/full, that attend the whole doc)
 // Warps 0-3 each own 16 doc rows: S = Q K^T over {global keys} U {band keys}
 // with mma.sync m16n8k16 (bf16 -> fp32), static band mask, online softmax in
-// the exp2 domain, O += P V, bf16 stores.  One warp per head (rotating)
-// also emits the split-softmax record (m, l, acc) of the "full rows" over the
-// tile's 64 doc keys, so the CLS row never re-reads K/V from HBM.  The first
+// the exp2 domain, O += P V, bf16 stores.  The producer warp, one item behind
+// its loads, emits the split-softmax records (m, l, acc) of the "full rows"
+// over the tile's 64 doc keys (keys as the MMA's M dimension: 8 full rows per
+// n8 column block), so the CLS row never re-reads K/V from HBM.  The first
 // tile of a sequence also computes the head rows (cls, query group) over the
 // global keys -- final for rows without a doc link (sparse query rows), a
 // record for the others -- and merge_full_rows_kernel (one warp per sequence,
 // head and row) folds the records into the CLS (and longformer query) rows.
-// Warp 4 is the TMA producer.
+// Warp 4 is the TMA producer (and the full-row records).
 //
 // Semantics: doc row r attends cls (if linked), query group (if linked) and
 // doc keys t with |t - r| <= w, 0 <= t < n_doc (R/band.py:48-52,
@@ -66,6 +67,7 @@ struct Params {
   // head rows (cls = group 0, query = group 1): links to cls / query keys, doc FULL
   int hl[2][2], hdoc[2];
   int ntiles_max;      // record index of sequence j's global-key record = ntiles_max + j
+  int cls_skip;        // measurement only (SC_BAND_CLS_SKIP=1): no full-row records (wrong CLS rows)
   float c2;  // log2(e) / scale: raw logit -> exp2 domain
   const int32_t* cu;
   const int32_t* qlen;
@@ -411,6 +413,120 @@ __device__ __forceinline__ void zero_o(float (&o)[8][4]) {
 #pragma unroll
   for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
 }
+// movmatrix: 8x8 b16 transpose across the warp (C-fragment rows <-> B-fragment columns)
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+  uint32_t r;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
+
+// Full-row split-softmax records of one item (the producer warp, all 32 lanes): the "full rows"
+// (CLS; query rows under longformer) against the tile's own 64 doc keys, Kb/Vb rows w .. w + 63.
+// Keys are the M dimension (S^T = K Qf^T, O^T = V^T P^T), so 8 full rows cost one n8 column
+// block: 16 + 16 mma.sync for a tile instead of 64 with the rows as a 16-row M fragment of which
+// the sparse pattern uses one.  P^T moves from the C layout of S^T to the B layout of the PV
+// product by movmatrix.  Record f: (m, l, -, -, acc[64]) -- m in natural logit units, l the sum of
+// exp(s - m) over the tile's keys, acc = sum exp(s - m) v (R/attention.py:416-473 split form).
+template <int PAIR>
+__device__ __forceinline__ void full_row_records(const Params& p, uint32_t qf, uint32_t kb, uint32_t vb, int lane,
+                                                 int tile, int h, int rows_here) {
+  const int g8 = lane >> 2, t = lane & 3;
+  const float c2 = p.c2;
+  const float to_nat = c2 * 0.69314718055994530942f;  // raw logit -> natural units (1/scale)
+  const int w = p.w;
+#pragma unroll 1
+  for (int hh = 0; hh < (PAIR ? 2 : 1); ++hh) {
+    const int ks0 = PAIR ? 2 * hh : 0, nks = PAIR ? 2 : 4;  // this head's k-steps (dims) / m-tiles
+    const int ht = PAIR ? 2 * h + hh : h;
+#pragma unroll 1
+    for (int fb = 0; fb * 8 < p.fneed; ++fb) {
+      // B fragments of full rows fb*8 .. fb*8+7 (Qf rows = B columns): k-steps 2i, 2i+1 per x4
+      uint32_t qb[4][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        uint32_t r[4];
+        ldsm_x4(swz(qf, fb * 8 + (lane & 7), 4 * i + (lane >> 3)), r);
+        qb[2 * i][0] = r[0]; qb[2 * i][1] = r[1]; qb[2 * i + 1][0] = r[2]; qb[2 * i + 1][1] = r[3];
+      }
+      float s[4][4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        s[mt][0] = s[mt][1] = s[mt][2] = s[mt][3] = 0.f;
+#pragma unroll
+        for (int k = 0; k < nks; ++k) {
+          const int ks = ks0 + k;
+          uint32_t a[4];
+          ldsm_x4(swz(kb, w + mt * 16 + (lane & 15), ks * 2 + (lane >> 4)), a);
+          mma16816(s[mt], a, qb[ks][0], qb[ks][1]);
+        }
+      }
+      // keys past the document end: -inf; column (full row) max over the 64 keys
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (mt * 16 + g8 + ((e >> 1) << 3) >= rows_here) s[mt][e] = -INFINITY;
+          if (e & 1) mx1 = fmaxf(mx1, s[mt][e]);
+          else mx0 = fmaxf(mx0, s[mt][e]);
+        }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+      }
+      const float b0 = mx0 == -INFINITY ? 0.f : mx0 * c2, b1 = mx1 == -INFINITY ? 0.f : mx1 * c2;
+      float l0 = 0.f, l1 = 0.f;
+      uint32_t pb[4][2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        s[mt][0] = ex2(fmaf(s[mt][0], c2, -b0));
+        s[mt][1] = ex2(fmaf(s[mt][1], c2, -b1));
+        s[mt][2] = ex2(fmaf(s[mt][2], c2, -b0));
+        s[mt][3] = ex2(fmaf(s[mt][3], c2, -b1));
+        l0 += s[mt][0] + s[mt][2];
+        l1 += s[mt][1] + s[mt][3];
+        pb[mt][0] = movm_t(pack_bf16(s[mt][0], s[mt][1]));  // keys 2t, 2t+1 of column g8
+        pb[mt][1] = movm_t(pack_bf16(s[mt][2], s[mt][3]));  // keys 2t+8, 2t+9
+      }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+      }
+      // O^T (dims x full rows) = V^T P^T: A = V^T through ldmatrix.trans of the key-major V rows
+      float ot[4][4];
+#pragma unroll
+      for (int k = 0; k < nks; ++k) {
+        const int dm = ks0 + k;
+        ot[k][0] = ot[k][1] = ot[k][2] = ot[k][3] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          uint32_t a[4];
+          ldsm_x4_t(swz(vb, w + kk * 16 + (lane & 7) + ((lane >> 4) << 3), dm * 2 + ((lane >> 3) & 1)), a);
+          mma16816(ot[k], a, pb[kk][0], pb[kk][1]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int f = fb * 8 + 2 * t + c;
+        if (f >= p.fneed) continue;
+        float* rec = p.partials + (((int64_t)tile * p.Ht + ht) * p.fmax + f) * REC;
+        if (g8 == 0) {
+          rec[0] = (c ? mx1 : mx0) * to_nat;
+          rec[1] = c ? l1 : l0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool live = k < nks;  // PAIR: the head's 32 dims, then zeros
+          rec[4 + k * 16 + g8] = live ? ot[k][c] : 0.f;
+          rec[4 + k * 16 + g8 + 8] = live ? ot[k][2 + c] : 0.f;
+        }
+      }
+    }
+  }
+}
+
 // NBC: band chunks of 32 keys per 16-row warp block (ceil((16+2w)/32)).
 // GR: global rows staged per head (16 or 32).  NS: pipeline stages.
 // NBB: band n8 blocks of the single-shot path (NBC = 1): 3 when 16 + 2w <= 24.
@@ -457,7 +573,7 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(full_bar + 8 * s, 1);
-      mbar_init(empty_bar + 8 * s, NDOCW);
+      mbar_init(empty_bar + 8 * s, NDOCW + 1);  // doc warps + the producer's records
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -466,7 +582,9 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
 
   if (warp == PRODW) {
     // The whole warp walks the items (converged); one elect.sync lane issues each item's loads, so
-    // the TMA operands stay warp-uniform (no per-lane waterfall loop around UTMALDG).
+    // the TMA operands stay warp-uniform (no per-lane waterfall loop around UTMALDG).  One item
+    // behind the loads, the warp computes the item's full-row records (full_row_records) and
+    // releases the stage with the doc warps (empty barrier: NDOCW + 1 arrivals).
     {
       if (elect_one()) {
         prefetch_map(&tmQ); prefetch_map(&tmKb); prefetch_map(&tmVb);
@@ -474,12 +592,23 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
       }
       __syncwarp();
       const uint32_t bytes = (uint32_t)((p.doc_rows ? q_bytes : 0) + 3 * f_bytes + 2 * kb_box * ROWB);
-      int it = 0;
+      const bool recs = p.fneed > 0 && !p.cls_skip;
+      int it = 0, prev_tile = -1, prev_h = 0, prev_rows = 0;
+      auto records = [&](int pit) {  // full-row records of item pit, then release its stage
+        const int sp = pit % NS;
+        mbar_wait(full_bar + 8 * sp, (pit / NS) & 1);
+        if (recs) full_row_records<PAIR>(p, qf_buf(sp), kb_buf(sp), vb_buf(sp), lane, prev_tile, prev_h, prev_rows);
+        __syncwarp();
+        if (elect_one()) mbar_arrive(empty_bar + 8 * sp);
+        __syncwarp();
+      };
       for (int tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
         const int tile = p.reverse ? ntiles - 1 - tix : tix;
         const int j = find_seq(p.tile_base, p.nseq, tile);
         const SeqGroups g = seq_groups(p.cu, p.qlen, j);
-        const int doc_row0 = g.start + g.off[2] + (tile - __ldg(p.tile_base + j)) * BM;
+        const int r0 = (tile - __ldg(p.tile_base + j)) * BM;
+        const int doc_row0 = g.start + g.off[2] + r0;
+        const int rows_here = min(BM, g.len[2] - r0);
         for (int h = 0; h < p.H; ++h, ++it) {
           const int s = it % NS;
           if (it >= NS) mbar_wait(empty_bar + 8 * s, ((it / NS) & 1) ^ 1);
@@ -499,8 +628,11 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
             tma_load_3d(qf_buf(s), &tmQf, h, g.start, fb);
           }
           __syncwarp();
+          if (it > 0) records(it - 1);
+          prev_tile = tile; prev_h = h; prev_rows = rows_here;
         }
       }
+      if (it > 0) records(it - 1);
     }
     return;
   }
@@ -575,17 +707,6 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         gmask[gc] = m;
       }
     }
-    // Own-key mask of the tile's 64 doc keys for the full-row partials.
-    uint32_t fmask[2] = {0xffffu, 0xffffu};
-    if (rows_here < BM) {
-      fmask[0] = fmask[1] = 0u;
-  #pragma unroll
-      for (int nb = 0; nb < 8; ++nb)
-  #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          fmask[nb >> 2] |= ((nb * 8 + 2 * tq + (e & 1)) < rows_here ? 1u : 0u) << ((nb & 3) * 4 + e);
-    }
-
     float ninv_a = 0.f, ninv_b = 0.f;
     if (p.padding == SC_PAD_ZERO_LOGIT) {
       ninv_a = (float)(2 * w + 1 - max(0, min(n_doc, ra + w + 1) - max(0, ra - w)));
@@ -746,64 +867,6 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         }
       }
 
-      // Full-row split-softmax partials over the tile's 64 own doc keys; the
-      // designated warp rotates with the head so the extra work spreads evenly.
-      // (PAIR: both heads of the item, 32 dims each, records in the 64-dim layout's first half.)
-      if (warp == (h & (NDOCW - 1))) {
-  #pragma unroll
-        for (int hh = 0; hh < (PAIR ? 2 : 1); ++hh) {
-  #pragma unroll
-        for (int fc = 0; fc < GR / 16; ++fc) {
-          if (fc * 16 < p.fneed) {
-            uint32_t qa[4][4];
-            load_q(qf_buf(s), fc * 16, LO, qa);
-            float sc[8][4];
-  #pragma unroll
-            for (int np = 0; np < 4; ++np) {
-              if constexpr (PAIR) qk16l_hh(kb_buf(s), w + np * 16, lane, qa, sc[2 * np], sc[2 * np + 1], hh);
-              else qk16(kb_buf(s), w + np * 16, lane, qa, sc[2 * np], sc[2 * np + 1]);
-            }
-  #pragma unroll
-            for (int nb = 0; nb < 8; ++nb)
-  #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (!((fmask[nb >> 2] >> ((nb & 3) * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
-            float o[8][4];
-            zero_o(o);
-            float fm0 = -INFINITY, fm1 = -INFINITY, fl0 = 0.f, fl1 = 0.f;
-            softmax_update<8, true>(sc, c2, fm0, fm1, fl0, fl1, o);
-  #pragma unroll
-            for (int kp = 0; kp < 4; ++kp) {
-              if constexpr (PAIR) pv16l_hh(vb_buf(s), w + kp * 16, lane, sc[2 * kp], sc[2 * kp + 1], o, hh);
-              else pv16(vb_buf(s), w + kp * 16, lane, sc[2 * kp], sc[2 * kp + 1], o);
-            }
-            fl0 += __shfl_xor_sync(0xffffffffu, fl0, 1);
-            fl0 += __shfl_xor_sync(0xffffffffu, fl0, 2);
-            fl1 += __shfl_xor_sync(0xffffffffu, fl1, 1);
-            fl1 += __shfl_xor_sync(0xffffffffu, fl1, 2);
-            const float to_nat = c2 * 0.69314718055994530942f;  // raw logit -> natural units (1/scale)
-            const int ht = PAIR ? 2 * h + hh : h;                 // head of the layout
-  #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-              const int f = fc * 16 + gq + 8 * half;
-              if (f >= p.fneed) continue;
-              float* rec = p.partials + (((int64_t)tile * p.Ht + ht) * p.fmax + f) * REC;
-              if (tq == 0) {
-                rec[0] = (half ? fm1 : fm0) * to_nat;
-                rec[1] = half ? fl1 : fl0;
-              }
-  #pragma unroll
-              for (int nb = 0; nb < 8; ++nb) {
-                const int src = PAIR ? (nb & 3) + 4 * hh : nb;  // PAIR: the head's 32 dims, then zeros
-                const bool live = !PAIR || nb < 4;
-                *reinterpret_cast<float2*>(rec + 4 + nb * 8 + 2 * tq) =
-                    live ? make_float2(o[src][2 * half], o[src][2 * half + 1]) : make_float2(0.f, 0.f);
-              }
-            }
-          }
-        }
-        }
-      }
       // Head rows over the global keys (first tile of the sequence only): rows
       // f < G (cls, query group) attend cls / query keys per their links.  Rows
       // with a FULL doc link leave a split-softmax record (merged below); the
@@ -1023,7 +1086,9 @@ static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, c
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (num_sms <= 0) num_sms = 148;
   }
-  const unsigned slots = (unsigned)(num_sms * min_ctas(NBC));
+  static int grid_cap = -1;  // measurement only (SC_BAND_GRID=N): persistent grid of N CTAs
+  if (grid_cap < 0) grid_cap = getenv("SC_BAND_GRID") ? atoi(getenv("SC_BAND_GRID")) : 0;
+  const unsigned slots = grid_cap > 0 ? (unsigned)grid_cap : (unsigned)(num_sms * min_ctas(NBC));
   band_attn_kernel<NBC, GR, NS, NBB, PAIR><<<grid < slots ? grid : slots, NTHREADS, smem, st>>>(
       maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
   SC_CHECK_LAUNCH("band_attn_kernel");
@@ -1126,6 +1191,9 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
     rev = e ? (atoi(e) != 0) : 1;
   }
   p.reverse = rev;
+  static int cls_skip = -1;
+  if (cls_skip < 0) cls_skip = getenv("SC_BAND_CLS_SKIP") ? atoi(getenv("SC_BAND_CLS_SKIP")) : 0;
+  p.cls_skip = cls_skip;
   // Doc rows + head rows over the global keys (first tile of each sequence).
   // (seq_head_base is unused: head rows are addressed through cu_seqlens.)
   (void)seq_head_base;
