@@ -542,6 +542,8 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
 
   // Persistent: CTA b processes tiles b, b + gridDim.x, ...; the TMA ring runs
   // continuously across tile boundaries (global head iteration counter `it`).
+  // the record merge (a programmatic dependent) may be scheduled now; it waits for this grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int ntiles = __ldg(p.tile_base + p.nseq);
   if ((int)blockIdx.x >= ntiles) return;
   const int w = p.w;
@@ -956,16 +958,21 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
 }
 
 // Merge of the split-softmax records into the head rows with a FULL doc link
-// (CLS; query rows under longformer): one warp per (sequence, head, row).
-// Records: one per doc tile of the sequence + the first tile's global-key
-// record.  Each lane loads whole records (16B vectors, all loads independent),
-// scales them by exp(m_r - M), and the warp reduces them through shared memory.
-constexpr int MERGE_WARPS = 4;
+// (CLS; query rows under longformer): one CTA of MERGE_WARPS warps per (sequence,
+// head, row).  Records: one per doc tile of the sequence + the first tile's
+// global-key record.  Warp w folds records w, w + MERGE_WARPS, ... with a running
+// max (lane = 2 dims, loads of several records in flight), then warp 0 folds the
+// warps' (max, l, acc) through shared memory.  Launched as a programmatic dependent
+// of the band kernel (griddepcontrol): its CTAs are resident before the band
+// kernel's last CTAs finish, and wait for the grid's records here.
+constexpr int MERGE_WARPS = 8;
 
 __global__ void __launch_bounds__(MERGE_WARPS * 32) merge_full_rows_kernel(Params p) {
-  __shared__ float sacc[MERGE_WARPS][32][D + 1];
+  __shared__ float sacc[MERGE_WARPS][D];
+  __shared__ float sml[MERGE_WARPS][2];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t item = (int64_t)blockIdx.x * MERGE_WARPS + warp;
+  const int64_t item = blockIdx.x;
   const int f = (int)(item % p.fmax);
   const int h = (int)((item / p.fmax) % p.H);
   const int j = (int)(item / ((int64_t)p.fmax * p.H));
@@ -980,47 +987,75 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32) merge_full_rows_kernel(Param
   const float* grec = p.partials + (((int64_t)(p.ntiles_max + j) * p.H + h) * p.fmax + f) * REC;
   auto rec_of = [&](int r) { return r < nrec - 1 ? trec + r * rstride : grec; };
 
-  float mloc = -INFINITY;
-  for (int r = lane; r < nrec; r += 32) {
-    const float2 ml = *reinterpret_cast<const float2*>(rec_of(r));
-    if (ml.y > 0.f) mloc = fmaxf(mloc, ml.x);
-  }
-  const float M = warp_max(mloc);
-  float lsum = 0.f, acc0 = 0.f, acc1 = 0.f;
-  for (int base = 0; base < nrec; base += 32) {
-    const int r = base + lane;
-    float4 v[D / 4];
-    float b = 0.f;
-    if (r < nrec) {
-      const float* rc = rec_of(r);
-      const float2 ml = *reinterpret_cast<const float2*>(rc);
+  float M = -INFINITY, l = 0.f, a0 = 0.f, a1 = 0.f;
+  constexpr int U = 4;  // records in flight per warp
+  for (int base = warp; base < nrec; base += U * MERGE_WARPS) {
+    float2 ml[U], v[U];
 #pragma unroll
-      for (int q = 0; q < D / 4; ++q) v[q] = *reinterpret_cast<const float4*>(rc + 4 + 4 * q);
-      if (ml.y > 0.f) {
-        b = __expf(ml.x - M);
-        lsum = fmaf(b, ml.y, lsum);
+    for (int u = 0; u < U; ++u) {
+      const int r = base + u * MERGE_WARPS;
+      if (r < nrec) {
+        const float* rc = rec_of(r);
+        ml[u] = __ldg(reinterpret_cast<const float2*>(rc));
+        v[u] = __ldg(reinterpret_cast<const float2*>(rc + 4 + 2 * lane));
+      } else {
+        ml[u] = make_float2(-INFINITY, 0.f);
+        v[u] = make_float2(0.f, 0.f);
       }
     }
 #pragma unroll
-    for (int q = 0; q < D / 4; ++q) {
-      sacc[warp][lane][4 * q + 0] = b != 0.f ? b * v[q].x : 0.f;
-      sacc[warp][lane][4 * q + 1] = b != 0.f ? b * v[q].y : 0.f;
-      sacc[warp][lane][4 * q + 2] = b != 0.f ? b * v[q].z : 0.f;
-      sacc[warp][lane][4 * q + 3] = b != 0.f ? b * v[q].w : 0.f;
+    for (int u = 0; u < U; ++u) {
+      if (!(ml[u].y > 0.f)) continue;  // warp-uniform (every lane reads the same (m, l))
+      if (ml[u].x > M) {
+        const float sc = __expf(M - ml[u].x);  // M = -inf: 0
+        l *= sc; a0 *= sc; a1 *= sc;
+        M = ml[u].x;
+      }
+      const float b = __expf(ml[u].x - M);
+      l = fmaf(b, ml[u].y, l);
+      a0 = fmaf(b, v[u].x, a0);
+      a1 = fmaf(b, v[u].y, a1);
     }
-    __syncwarp();
-    const int cnt = min(32, nrec - base);
-    for (int k = 0; k < cnt; ++k) {
-      acc0 += sacc[warp][k][lane];
-      acc1 += sacc[warp][k][lane + 32];
-    }
-    __syncwarp();
   }
-  const float l = warp_sum(lsum);
-  const float inv = l > 0.f ? 1.f / l : 0.f;
-  __nv_bfloat16* dst = p.out + (int64_t)(g.start + f) * p.ld_out + h * p.dout;
-  dst[lane] = __float2bfloat16_rn(acc0 * inv);
-  if (p.dout > 32) dst[lane + 32] = __float2bfloat16_rn(acc1 * inv);
+  sacc[warp][2 * lane] = a0;
+  sacc[warp][2 * lane + 1] = a1;
+  if (lane == 0) { sml[warp][0] = M; sml[warp][1] = l; }
+  __syncthreads();
+  if (warp != 0) return;
+  float Mt = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < MERGE_WARPS; ++w) Mt = fmaxf(Mt, sml[w][0]);
+  float lt = 0.f, o0 = 0.f, o1 = 0.f;
+#pragma unroll
+  for (int w = 0; w < MERGE_WARPS; ++w) {
+    if (!(sml[w][1] > 0.f)) continue;
+    const float sc = __expf(sml[w][0] - Mt);
+    lt = fmaf(sc, sml[w][1], lt);
+    o0 = fmaf(sc, sacc[w][2 * lane], o0);
+    o1 = fmaf(sc, sacc[w][2 * lane + 1], o1);
+  }
+  const float inv = lt > 0.f ? 1.f / lt : 0.f;
+  if (2 * lane < p.dout) {
+    __nv_bfloat16* dst = p.out + (int64_t)(g.start + f) * p.ld_out + h * p.dout + 2 * lane;
+    *reinterpret_cast<uint32_t*>(dst) = pack_bf16(o0 * inv, o1 * inv);
+  }
+}
+
+// Programmatic-dependent launch of the merge (one CTA per (sequence, head, full row)).
+static int launch_merge(const Params& p, int64_t items, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)items);
+  cfg.blockDim = dim3(MERGE_WARPS * 32);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, merge_full_rows_kernel, p);
+  SC_CHECK_LAUNCH("merge_full_rows_kernel");
+  return SC_OK;
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1204,10 +1239,7 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   Params pm = p;  // the merge walks the layout's heads
   pm.H = a.H;
   pm.dout = a.d;
-  const int64_t items = (int64_t)a.nseq * a.H * fneed;
-  merge_full_rows_kernel<<<(unsigned)((items + MERGE_WARPS - 1) / MERGE_WARPS), MERGE_WARPS * 32, 0, st>>>(pm);
-  SC_CHECK_LAUNCH("merge_full_rows_kernel");
-  return SC_OK;
+  return launch_merge(pm, (int64_t)a.nseq * a.H * fneed, st);
 }
 
 int launch_head_merge(const AttnArgs& a, const int32_t* seq_tile_base, int tile_rows, int max_qgroup_len, void* ws,
@@ -1223,10 +1255,7 @@ int launch_head_merge(const AttnArgs& a, const int32_t* seq_tile_base, int tile_
   p.partials = static_cast<float*>(ws);
   p.ntiles_max = (int)((a.T + tile_rows - 1) / tile_rows + a.nseq);
   for (int gsrc = 0; gsrc < 2; ++gsrc) p.hdoc[gsrc] = L.w[gsrc][2] == SC_LINK_FULL;
-  const int64_t items = (int64_t)a.nseq * a.H * fneed;
-  merge_full_rows_kernel<<<(unsigned)((items + MERGE_WARPS - 1) / MERGE_WARPS), MERGE_WARPS * 32, 0, st>>>(p);
-  SC_CHECK_LAUNCH("merge_full_rows_kernel");
-  return SC_OK;
+  return launch_merge(p, (int64_t)a.nseq * a.H * fneed, st);
 }
 
 }  // namespace sc
