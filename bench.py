@@ -509,11 +509,16 @@ def run_gpu(args):
             "note": "CrossEncoder(prune_last_layer=True): last layer past K/V on the [CLS] rows only (the score "
                     "reads x[:,0], R/encoder.py:506); same scores, not the headline"}
     if world == 1 and not args.no_variants and doc_len == 4086 and not args.varlen:
+        # the kernel-alone sweeps first (before the GEMM-heavy variants), clocks sampled during each
+        with ClockSampler(local) as sclk:
+            variants["attention_sweep"] = attention_sweep(P, dev, (hbm_peak, tf_burst))
+        variants["attention_sweep"]["clocks"] = sclk.summary()
+        with ClockSampler(local) as sclk:
+            variants["attention_sweep_d32"] = attention_sweep(  # MiniLM-L6-H384 heads: 12 x d=32
+                P, dev, (hbm_peak, tf_burst), d=32, windows=(("sparse", 4), ("sparse", 64), ("sparse", 256)))
+        variants["attention_sweep_d32"]["clocks"] = sclk.summary()
         variants["varlen_documents"] = varlen_variant(P, dev, model, max(3, args.steps // 2))
         variants["passages"] = passages_variant(P, dev, args.steps)
-        variants["attention_sweep"] = attention_sweep(P, dev, (hbm_peak, tf_burst))
-        variants["attention_sweep_d32"] = attention_sweep(  # MiniLM-L6-H384 heads: 12 x d=32
-            P, dev, (hbm_peak, tf_burst), d=32, windows=(("sparse", 4), ("sparse", 64), ("sparse", 256)))
         variants["fp32_ranking_exact"] = fp32_variant(P, dev, max(3, args.steps // 4))
 
     # ---- roofline of the attention kernel (sc_attn_fwd, band + head-row pass) ----
