@@ -344,6 +344,16 @@ SC_API int sc_split_f16x2(const float* x, int64_t ldx, const float* bias, int32_
                           void* planes, int64_t ldp, int64_t rows, int32_t cols, int32_t onehot, int32_t* status,
                           void* stream);
 
+/* sc_residual_layernorm_ex for fp32 (resid, y, x_out fp32) that also writes the sc_split_f16x2
+ * planes of x_out ([h0 | h1], or [h0 | 1 0 .. 0 | h1] with onehot) -- the split pass of the fast
+ * fp32 mode fused into the LayerNorm that produces the next GEMM's operand (R/encoder.py:346-347,
+ * :353-354 feeding :322-324 / :350).  range_status as sc_split_f16x2's status.  SC_ERR_UNSUPPORTED
+ * unless hidden is one of 128, 256, 384, 512, 768, 1024 and pointers are 16-byte aligned. */
+SC_API int sc_residual_layernorm_f16x2(const float* resid, const float* y, const float* bias, const float* gamma,
+                                       const float* beta, float* x_out, void* planes, int64_t ldp, int32_t onehot,
+                                       int32_t* range_status, int32_t* nonfinite_count, int32_t rows,
+                                       int32_t hidden, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

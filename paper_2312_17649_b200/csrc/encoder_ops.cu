@@ -1,6 +1,8 @@
 // Encoder-loop kernels around the attention (R/encoder.py:306-371, :475-509):
 // embedding gather + per-sequence positions, residual + LayerNorm (eps 1e-12),
 // bias + exact-erf GELU, [CLS] relevance head, non-finite detection.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "gelu.cuh"
 
@@ -140,7 +142,8 @@ template <typename R, typename Y, int kVec, bool kRev = true>
 __global__ void __launch_bounds__(256, 3) residual_ln_vec_kernel(
     const R* __restrict__ resid, const Y* __restrict__ y, const float* __restrict__ bias,
     const float* __restrict__ gamma, const float* __restrict__ beta, float* __restrict__ out,
-    __nv_bfloat16* __restrict__ out_h, int32_t* __restrict__ bad, int rows, int h) {
+    __nv_bfloat16* __restrict__ out_h, int32_t* __restrict__ bad, int rows, int h,
+    __half* __restrict__ planes = nullptr, int64_t ldp = 0, int onehot = 0, int32_t* __restrict__ range = nullptr) {
   const int lane = threadIdx.x & 31;
   // rows last-to-first: the producing GEMM's most recent output rows are still in L2
   const int r = (kRev ? gridDim.x - 1 - blockIdx.x : blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -182,6 +185,18 @@ __global__ void __launch_bounds__(256, 3) residual_ln_vec_kernel(
       __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y), hi = __floats2bfloat162_rn(o.z, o.w);
       uint2 u = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
       *reinterpret_cast<uint2*>(out_h + (int64_t)r * h + c) = u;
+    }
+    if (planes) {  // f16x3 GEMM operand: [h0 | (1 0 .. 0) | h1], h0 = fp16_rn(o), h1 = fp16_rn(o - h0)
+      const __half2 a01 = __floats2half2_rn(o.x, o.y), a23 = __floats2half2_rn(o.z, o.w);
+      const float2 f01 = __half22float2(a01), f23 = __half22float2(a23);
+      const __half2 b01 = __floats2half2_rn(o.x - f01.x, o.y - f01.y), b23 = __floats2half2_rn(o.z - f23.x, o.w - f23.y);
+      __half* pr = planes + (int64_t)r * ldp + c;
+      *reinterpret_cast<uint2*>(pr) = make_uint2(*reinterpret_cast<const uint32_t*>(&a01), *reinterpret_cast<const uint32_t*>(&a23));
+      *reinterpret_cast<uint2*>(pr + h + (onehot ? 8 : 0)) =
+          make_uint2(*reinterpret_cast<const uint32_t*>(&b01), *reinterpret_cast<const uint32_t*>(&b23));
+      if (onehot && c == 0) *reinterpret_cast<uint4*>(planes + (int64_t)r * ldp + h) = make_uint4(0x3c00u, 0u, 0u, 0u);
+      if (range && !(fabsf(o.x) < 65504.f && fabsf(o.y) < 65504.f && fabsf(o.z) < 65504.f && fabsf(o.w) < 65504.f))
+        atomicExch(range, 1);
     }
   }
   flag_nonfinite(bad, nf);
@@ -386,6 +401,41 @@ extern "C" int sc_residual_layernorm(const float* resid, const void* y, int32_t 
   SC_CHECK_ARG(x_out, "sc_residual_layernorm: null pointer");
   return sc_residual_layernorm_ex(resid, SC_DTYPE_F32, y, y_dtype, bias, gamma, beta, x_out, out_h, nullptr,
                                   rows, hidden, stream);
+}
+
+// fp32 residual LayerNorm that also writes the f16x3 GEMM operand planes of its output (the split
+// pass of the ranking-exact fp32 mode fused into the producer; encoder.py split_planes_h).
+extern "C" int sc_residual_layernorm_f16x2(const float* resid, const float* y, const float* bias, const float* gamma,
+                                           const float* beta, float* x_out, void* planes, int64_t ldp, int32_t onehot,
+                                           int32_t* range_status, int32_t* nonfinite_count, int32_t rows,
+                                           int32_t hidden, void* stream) {
+  SC_CHECK_ARG(resid && y && gamma && beta && x_out && planes, "sc_residual_layernorm_f16x2: null pointer");
+  SC_CHECK_ARG(rows >= 0 && hidden >= 1 && ldp >= 2LL * hidden + (onehot ? 8 : 0),
+               "sc_residual_layernorm_f16x2: bad shape");
+  if (rows == 0) return SC_OK;
+  const bool vec = (hidden == 128 || hidden == 256 || hidden == 384 || hidden == 512 || hidden == 768 ||
+                    hidden == 1024) && ldp % 8 == 0 &&
+                   !(((uintptr_t)resid | (uintptr_t)y | (uintptr_t)x_out | (uintptr_t)gamma | (uintptr_t)beta |
+                      (uintptr_t)bias | (uintptr_t)planes) & 15);
+  if (!vec) {
+    set_error("sc_residual_layernorm_f16x2: needs hidden in {128,256,384,512,768,1024} and 16-byte alignment");
+    return SC_ERR_UNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned blocks = (unsigned)((rows + 7) / 8);
+  __half* pl = static_cast<__half*>(planes);
+#define SC_LNP_ARGS resid, y, bias, gamma, beta, x_out, nullptr, nonfinite_count, rows, hidden, pl, ldp, onehot ? 1 : 0, range_status
+  switch (hidden) {
+    case 128: residual_ln_vec_kernel<float, float, 1><<<blocks, 256, 0, st>>>(SC_LNP_ARGS); break;
+    case 256: residual_ln_vec_kernel<float, float, 2><<<blocks, 256, 0, st>>>(SC_LNP_ARGS); break;
+    case 384: residual_ln_vec_kernel<float, float, 3><<<blocks, 256, 0, st>>>(SC_LNP_ARGS); break;
+    case 512: residual_ln_vec_kernel<float, float, 4><<<blocks, 256, 0, st>>>(SC_LNP_ARGS); break;
+    case 768: residual_ln_vec_kernel<float, float, 6><<<blocks, 256, 0, st>>>(SC_LNP_ARGS); break;
+    default: residual_ln_vec_kernel<float, float, 8><<<blocks, 256, 0, st>>>(SC_LNP_ARGS); break;
+  }
+#undef SC_LNP_ARGS
+  SC_CHECK_LAUNCH("residual_ln_vec_kernel (planes)");
+  return SC_OK;
 }
 
 extern "C" int sc_bias_gelu(void* x, const float* bias, int32_t dtype, int64_t rows, int32_t cols,

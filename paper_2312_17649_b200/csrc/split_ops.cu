@@ -115,42 +115,65 @@ static void launch_split(bool vec, const float* x, int64_t ldx, const float* bia
 // work of the bf16 six-product form.  fp16's range (|v| < 65504) is checked: an out-of-range value
 // sets *status (the encoder then raises, no silent inf).
 template <bool kBias, bool kGelu>
-__global__ void __launch_bounds__(256) split2h_vec_kernel(const float* __restrict__ x, int64_t ldx,
+__device__ __forceinline__ bool split2h_one(float4 v, const float* __restrict__ bias, float* __restrict__ y, int64_t ldy,
+                                            __half* __restrict__ p, int64_t ldp, uint32_t r, int c, int cols, int h1_off,
+                                            int onehot) {
+  if (kBias) {
+    const float4 b = __ldg(reinterpret_cast<const float4*>(bias + c));
+    v.x += b.x, v.y += b.y, v.z += b.z, v.w += b.w;
+  }
+  if (kGelu) {
+    v.x = 0.5f * v.x * (1.f + erff(v.x * 0.70710678118654752440f));
+    v.y = 0.5f * v.y * (1.f + erff(v.y * 0.70710678118654752440f));
+    v.z = 0.5f * v.z * (1.f + erff(v.z * 0.70710678118654752440f));
+    v.w = 0.5f * v.w * (1.f + erff(v.w * 0.70710678118654752440f));
+  }
+  if (y) *reinterpret_cast<float4*>(y + (int64_t)r * ldy + c) = v;
+  const __half2 a01 = __floats2half2_rn(v.x, v.y), a23 = __floats2half2_rn(v.z, v.w);
+  const float2 f01 = __half22float2(a01), f23 = __half22float2(a23);
+  const __half2 b01 = __floats2half2_rn(v.x - f01.x, v.y - f01.y), b23 = __floats2half2_rn(v.z - f23.x, v.w - f23.y);
+  __half* pr = p + (int64_t)r * ldp + c;
+  uint2 u;
+  u.x = *reinterpret_cast<const uint32_t*>(&a01), u.y = *reinterpret_cast<const uint32_t*>(&a23);
+  *reinterpret_cast<uint2*>(pr) = u;
+  u.x = *reinterpret_cast<const uint32_t*>(&b01), u.y = *reinterpret_cast<const uint32_t*>(&b23);
+  *reinterpret_cast<uint2*>(pr + h1_off) = u;
+  if (onehot && c == 0) *reinterpret_cast<uint4*>(p + (int64_t)r * ldp + cols) = make_uint4(0x3c00u, 0u, 0u, 0u);  // [1, 0 x 7]
+  return !(fabsf(v.x) < 65504.f && fabsf(v.y) < 65504.f && fabsf(v.z) < 65504.f && fabsf(v.w) < 65504.f);
+}
+
+// float4 items walked last-to-first (the producing GEMM's most recent output is still in L2), U
+// loads in flight per thread before any math (one at a time left the pass at ~55-70% of HBM),
+// 32-bit index arithmetic (rows * cols / 4 < 2^32; the caller falls back otherwise).
+template <bool kBias, bool kGelu, int U>
+__global__ void __launch_bounds__(256, 4) split2h_vec_kernel(const float* __restrict__ x, int64_t ldx,
                                                           const float* __restrict__ bias, float* __restrict__ y,
                                                           int64_t ldy, __half* __restrict__ p, int64_t ldp,
                                                           int64_t rows, int cols, int h1_off, int onehot,
                                                           int32_t* __restrict__ status) {
-  const int c4 = cols >> 2;
-  const int64_t n = rows * c4;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint32_t c4 = (uint32_t)cols >> 2;
+  const uint32_t n = (uint32_t)(rows * c4);
+  const uint32_t stride = gridDim.x * blockDim.x;
   bool bad = false;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int64_t j = n - 1 - i;
-    const int64_t r = j / c4;
-    const int c = (int)(j - r * c4) * 4;
-    float4 v = *reinterpret_cast<const float4*>(x + r * ldx + c);
-    if (kBias) {
-      const float4 b = __ldg(reinterpret_cast<const float4*>(bias + c));
-      v.x += b.x, v.y += b.y, v.z += b.z, v.w += b.w;
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i < n; i += U * stride) {
+    float4 v[U];
+    uint32_t rr[U];
+    int cc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t k = i + u * stride;
+      if (k < n) {
+        const uint32_t j = n - 1 - k;
+        rr[u] = j / c4;
+        cc[u] = (int)(j - rr[u] * c4) * 4;
+        v[u] = __ldcs(reinterpret_cast<const float4*>(x + (int64_t)rr[u] * ldx + cc[u]));
+      }
     }
-    if (kGelu) {
-      v.x = 0.5f * v.x * (1.f + erff(v.x * 0.70710678118654752440f));
-      v.y = 0.5f * v.y * (1.f + erff(v.y * 0.70710678118654752440f));
-      v.z = 0.5f * v.z * (1.f + erff(v.z * 0.70710678118654752440f));
-      v.w = 0.5f * v.w * (1.f + erff(v.w * 0.70710678118654752440f));
-    }
-    if (y) *reinterpret_cast<float4*>(y + r * ldy + c) = v;
-    bad |= !(fabsf(v.x) < 65504.f && fabsf(v.y) < 65504.f && fabsf(v.z) < 65504.f && fabsf(v.w) < 65504.f);
-    const __half2 a01 = __floats2half2_rn(v.x, v.y), a23 = __floats2half2_rn(v.z, v.w);
-    const float2 f01 = __half22float2(a01), f23 = __half22float2(a23);
-    const __half2 b01 = __floats2half2_rn(v.x - f01.x, v.y - f01.y), b23 = __floats2half2_rn(v.z - f23.x, v.w - f23.y);
-    __half* pr = p + r * ldp + c;
-    uint2 u;
-    u.x = *reinterpret_cast<const uint32_t*>(&a01), u.y = *reinterpret_cast<const uint32_t*>(&a23);
-    *reinterpret_cast<uint2*>(pr) = u;
-    u.x = *reinterpret_cast<const uint32_t*>(&b01), u.y = *reinterpret_cast<const uint32_t*>(&b23);
-    *reinterpret_cast<uint2*>(pr + h1_off) = u;
-    if (onehot && c == 0) *reinterpret_cast<uint4*>(p + r * ldp + cols) = make_uint4(0x3c00u, 0u, 0u, 0u);  // [1, 0 x 7]
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i + u * stride < n)
+        bad |= split2h_one<kBias, kGelu>(v[u], bias, y, ldy, p, ldp, rr[u], cc[u], cols, h1_off, onehot);
   }
   if (bad && status) atomicExch(status, 1);
 }
@@ -182,15 +205,36 @@ template <bool kBias, bool kGelu>
 static void launch_split2h(bool vec, const float* x, int64_t ldx, const float* bias, float* y, int64_t ldy, __half* p,
                            int64_t ldp, int64_t rows, int cols, int h1_off, int onehot, int32_t* status,
                            cudaStream_t st) {
-  const int64_t work = vec ? rows * (cols / 4) : rows * cols;
-  int64_t blocks = (work + 255) / 256;
+  vec = vec && rows * (cols / 4) < (int64_t)UINT32_MAX;
+  if (vec) {
+    // U float4 loads in flight per thread; one resident wave of CTAs (occupancy API).  The GELU form
+    // is as much erff arithmetic as memory traffic: SC_SPLIT_GELU_U (measurement) picks its U.
+    static int ug = -1;
+    if (ug < 0) ug = getenv("SC_SPLIT_GELU_U") ? atoi(getenv("SC_SPLIT_GELU_U")) : 4;  // U = 1 / 2 / 4: 9.8 / 10.2 / 9.6 ms per 12 layers (erff-bound)
+    const int U = kGelu ? ug : 4;
+    auto kern = U == 1 ? split2h_vec_kernel<kBias, kGelu, 1>
+              : U == 2 ? split2h_vec_kernel<kBias, kGelu, 2> : split2h_vec_kernel<kBias, kGelu, 4>;
+    static int occ[3] = {0, 0, 0};
+    const int ui = U == 1 ? 0 : (U == 2 ? 1 : 2);
+    if (!occ[ui]) {
+      int dev = 0, sms = 148, per = 4;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, 0);
+      occ[ui] = sms * (per > 0 ? per : 1);
+    }
+    const int64_t work = (rows * (cols / 4) + U - 1) / U;
+    int64_t blocks = (work + 255) / 256;
+    if (blocks > occ[ui]) blocks = occ[ui];
+    kern<<<(unsigned)blocks, 256, 0, st>>>(x, ldx, bias, y, ldy, p, ldp, rows, cols, h1_off, onehot, status);
+    return;
+  }
+  int64_t blocks = (rows * cols + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  if (vec)
-    split2h_vec_kernel<kBias, kGelu><<<(unsigned)blocks, 256, 0, st>>>(x, ldx, bias, y, ldy, p, ldp, rows, cols, h1_off,
-                                                                       onehot, status);
-  else
+  {
     split2h_kernel<kBias, kGelu><<<(unsigned)blocks, 256, 0, st>>>(x, ldx, bias, y, ldy, p, ldp, rows, cols, h1_off,
                                                                    onehot, status);
+  }
 }
 
 }  // namespace sc

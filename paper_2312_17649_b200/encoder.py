@@ -570,8 +570,11 @@ class CrossEncoder:
         _lib.call("sc_embed", ids_dev.data_ptr(), layout.tok_pos.data_ptr(), self.tok_emb.data_ptr(),
                   self.pos_emb.data_ptr(), x.data_ptr(), None, T, h, stream, exc=EncoderError)
         last = cfg.layers - 1
+        f16 = self.fp32_gemm == "f16x3"
+        xs = None  # f16x3: the QKV planes of x, written by the previous layer's second LayerNorm
         for i, L in enumerate(self.layers):
-            xs = self._xsplit(x, qkv_input=True)
+            if xs is None:
+                xs = self._xsplit(x, qkv_input=True)
             if cls_only and i == last:
                 self._last_bad = bad if check_finite else None
                 return self._cls_last_layer_x6(L, x, xs, layout, pattern, bad if check_finite else None, i)
@@ -583,17 +586,40 @@ class CrossEncoder:
             if attn_hook:
                 attn_hook("end")
             y = self._xlinear(self._xsplit(o), L, "wo")
-            _lib.call("sc_residual_layernorm_ex", x.data_ptr(), F32, y.data_ptr(), F32, L["bo_f32"].data_ptr(),
-                      L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), x1.data_ptr(), None, None, T, h, stream,
-                      exc=EncoderError)
-            f = self._xlinear(self._xsplit(x1), L, "w1")
+            x1s = self._ln_planes(x, y, L["bo_f32"], L, "ln1", x1, None, False) if f16 else None
+            if x1s is None:
+                _lib.call("sc_residual_layernorm_ex", x.data_ptr(), F32, y.data_ptr(), F32, L["bo_f32"].data_ptr(),
+                          L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), x1.data_ptr(), None, None, T, h, stream,
+                          exc=EncoderError)
+                x1s = self._xsplit(x1)
+            f = self._xlinear(x1s, L, "w1")
+            del x1s
             f2 = self._xlinear(self._xsplit(f, bias=L["b1_f32"], gelu=True), L, "w2")
             del f
-            _lib.call("sc_residual_layernorm_ex", x1.data_ptr(), F32, f2.data_ptr(), F32, L["b2_f32"].data_ptr(),
-                      L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(), x.data_ptr(), None,
-                      _lib.ptr(bad[i:i + 1]) if check_finite else None, T, h, stream, exc=EncoderError)
+            bad_i = bad[i:i + 1] if check_finite else None
+            xs = self._ln_planes(x1, f2, L["b2_f32"], L, "ln2", x, bad_i, True) if f16 and i < last else None
+            if xs is None:
+                _lib.call("sc_residual_layernorm_ex", x1.data_ptr(), F32, f2.data_ptr(), F32, L["b2_f32"].data_ptr(),
+                          L["ln2_g"].data_ptr(), L["ln2_b"].data_ptr(), x.data_ptr(), None,
+                          _lib.ptr(bad_i), T, h, stream, exc=EncoderError)
         self._last_bad = bad if check_finite else None
         return x
+
+    def _ln_planes(self, resid, y, bias, L, ln, out, bad, qkv_input):
+        """f16x3: out = LN(resid + y + bias) (fp32) and its fp16 GEMM planes from one pass
+        (sc_residual_layernorm_f16x2, the split fused into the LayerNorm); None if unsupported."""
+        T, h = out.shape
+        planes = torch.empty((T, 2 * h + (8 if qkv_input else 0)), dtype=torch.float16, device=out.device)
+        rc = _lib.load().sc_residual_layernorm_f16x2(
+            resid.data_ptr(), y.data_ptr(), bias.data_ptr(), L[ln + "_g"].data_ptr(), L[ln + "_b"].data_ptr(),
+            out.data_ptr(), planes.data_ptr(), planes.stride(0), int(qkv_input), _lib.ptr(self._range_flag),
+            _lib.ptr(bad), T, h, _lib.stream_handle())
+        if rc == _lib.SC_OK:
+            _lib.launch_calls += 1
+            return planes
+        if rc != _lib.SC_ERR_UNSUPPORTED:
+            raise EncoderError(_lib.last_error())
+        return None
 
     def _cls_last_layer_x6(self, L, x, xs, layout, pattern, bad, i):
         """_cls_last_layer for fp32_gemm="bf16x6": K/V of every token, the rest on the [CLS] rows."""
