@@ -87,8 +87,8 @@ struct Smem {
   static constexpr int QF = VG + C::GR * ROWB;  // q rows of the head groups (TMA, 128B swizzle)
   static constexpr int KV = QF + C::GR * ROWB;  // NS x (K block, V block)
   static constexpr int STAGE = 2 * C::BN * ROWB;
-  static constexpr int HST = KV + C::NS * STAGE;  // head-row softmax state: (GR/16) x 32 lanes x 36 fp32
-  static constexpr int BAR = HST + (C::GR / 16) * 32 * 36 * 4;
+  static constexpr int HST = KV + C::NS * STAGE;  // head-row softmax state: (GR/8) x 32 lanes x 20 fp32
+  static constexpr int BAR = HST + (C::GR / 8) * 32 * 20 * 4;
   // barriers: qbar, full[NS], empty[NS], s_full[2], p_full[2], pv_done[2], o_final; tmem holder
   static constexpr int TOTAL = BAR + 16 * 8 + 16;
 };
@@ -178,54 +178,126 @@ struct HeadRows {
 
   // One ring block of the CTA's own doc keys [r0 + off, r0 + off + BN) for the FULL-doc-link rows;
   // a record closes each 64-key half (state carried in shared memory between the half's blocks).
+  // Keys are the MMA's M dimension (S^T = K Qf^T, O^T = V^T P^T; P^T to the B layout by movmatrix),
+  // so the full rows cost one n8 column block per 8 rows: for the sparse pattern's single CLS row
+  // 2 x BN/2 mma.sync per block instead of 2 x BN with the rows as a 16-row M fragment.
   __device__ void own_block(uint32_t kvbuf, int off) const {
-    constexpr int BN = C::BN;
-    const int tq = lane & 3;
+    constexpr int BN = C::BN, MT = BN / 16;
+    const int g8 = lane >> 2, t = lane & 3;
     const int k0 = r0 + off;
     const int nk = min(BN, n_doc - k0);
     const bool first = off % 64 == 0;
     const bool close = ((off + BN) % 64 == 0) || (k0 + BN >= n_doc);
-    for (int fc = 0; fc < C::GR / 16; ++fc) {
-      if (fc * 16 >= p.fneed || fc * 16 >= G) break;
-      float* stt = hst + (fc * 32 + lane) * 36;
-      uint32_t qa[4][4];
-      mmat::load_a(sm0 + SM::QF, fc * 16, lane, qa);
-      float o[8][4];
+    const float c2 = p.c2;
+    const uint32_t vbuf = kvbuf + BN * ROWB;
+    for (int fb = 0; fb < C::GR / 8; ++fb) {
+      if (fb * 8 >= p.fneed || fb * 8 >= G) break;
+      float* stt = hst + (fb * 32 + lane) * 20;
+      float ot[4][4];
       float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
       if (first) {
 #pragma unroll
-        for (int nb = 0; nb < 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
+        for (int k = 0; k < 4; ++k) ot[k][0] = ot[k][1] = ot[k][2] = ot[k][3] = 0.f;
       } else {
 #pragma unroll
-        for (int nb = 0; nb < 8; ++nb) {
-          const float4 t = *reinterpret_cast<const float4*>(stt + 4 * nb);
-          o[nb][0] = t.x, o[nb][1] = t.y, o[nb][2] = t.z, o[nb][3] = t.w;
+        for (int k = 0; k < 4; ++k) {
+          const float4 v = *reinterpret_cast<const float4*>(stt + 4 * k);
+          ot[k][0] = v.x, ot[k][1] = v.y, ot[k][2] = v.z, ot[k][3] = v.w;
         }
-        m0 = stt[32], m1 = stt[33], l0 = stt[34], l1 = stt[35];
+        m0 = stt[16], m1 = stt[17], l0 = stt[18], l1 = stt[19];
+      }
+      uint32_t qb[4][2];  // B fragments of full rows fb*8 .. fb*8+7: k-steps 2i, 2i+1 per x4
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        uint32_t r[4];
+        mmat::ldsm_x4(mmat::swz(sm0 + SM::QF, fb * 8 + (lane & 7), 4 * i + (lane >> 3)), r);
+        qb[2 * i][0] = r[0]; qb[2 * i][1] = r[1]; qb[2 * i + 1][0] = r[2]; qb[2 * i + 1][1] = r[3];
+      }
+      float s[MT][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        s[mt][0] = s[mt][1] = s[mt][2] = s[mt][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          uint32_t a[4];
+          mmat::ldsm_x4(mmat::swz(kvbuf, mt * 16 + (lane & 15), ks * 2 + (lane >> 4)), a);
+          mmat::mma16816(s[mt], a, qb[ks][0], qb[ks][1]);
+        }
+      }
+      float x0 = -INFINITY, x1 = -INFINITY;  // column (full-row) max over the block's keys
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (mt * 16 + g8 + ((e >> 1) << 3) >= nk) s[mt][e] = -INFINITY;
+          if (e & 1) x1 = fmaxf(x1, s[mt][e]);
+          else x0 = fmaxf(x0, s[mt][e]);
+        }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+        x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+      }
+      const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);
+      const float b0 = n0 == -INFINITY ? 0.f : n0 * c2, b1 = n1 == -INFINITY ? 0.f : n1 * c2;
+      const float a0 = mmat::ex2(fmaf(m0, c2, -b0)), a1 = mmat::ex2(fmaf(m1, c2, -b1));
+      float r0s = 0.f, r1s = 0.f;
+      uint32_t pb[MT][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        s[mt][0] = mmat::ex2(fmaf(s[mt][0], c2, -b0));
+        s[mt][1] = mmat::ex2(fmaf(s[mt][1], c2, -b1));
+        s[mt][2] = mmat::ex2(fmaf(s[mt][2], c2, -b0));
+        s[mt][3] = mmat::ex2(fmaf(s[mt][3], c2, -b1));
+        r0s += s[mt][0] + s[mt][2];
+        r1s += s[mt][1] + s[mt][3];
+        pb[mt][0] = mmat::movm_t(mmat::pack_bf16(s[mt][0], s[mt][1]));
+        pb[mt][1] = mmat::movm_t(mmat::pack_bf16(s[mt][2], s[mt][3]));
       }
 #pragma unroll
-      for (int c = 0; c < BN; c += 32) {
-        float sc[4][4];
+      for (int o = 4; o < 32; o <<= 1) {
+        r0s += __shfl_xor_sync(0xffffffffu, r0s, o);
+        r1s += __shfl_xor_sync(0xffffffffu, r1s, o);
+      }
+      l0 = fmaf(l0, a0, r0s);
+      l1 = fmaf(l1, a1, r1s);
+      m0 = n0;
+      m1 = n1;
 #pragma unroll
-        for (int nb = 0; nb < 4; ++nb) sc[nb][0] = sc[nb][1] = sc[nb][2] = sc[nb][3] = 0.f;
-        mmat::mm_nt16(kvbuf, c, lane, qa, sc[0], sc[1]);
-        mmat::mm_nt16(kvbuf, c + 16, lane, qa, sc[2], sc[3]);
+      for (int dm = 0; dm < 4; ++dm) {
+        ot[dm][0] *= a0; ot[dm][2] *= a0;
+        ot[dm][1] *= a1; ot[dm][3] *= a1;
 #pragma unroll
-        for (int nb = 0; nb < 4; ++nb)
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (c + nb * 8 + 2 * tq + (e & 1) >= nk) sc[nb][e] = -INFINITY;
-        mmat::softmax_update<4>(sc, p.c2, m0, m1, l0, l1, o);
-        mmat::mm_nn16(kvbuf + BN * ROWB, c, lane, sc[0], sc[1], o);
-        mmat::mm_nn16(kvbuf + BN * ROWB, c + 16, lane, sc[2], sc[3], o);
+        for (int kk = 0; kk < MT; ++kk) {
+          uint32_t a[4];
+          mmat::ldsm_x4_t(mmat::swz(vbuf, kk * 16 + (lane & 7) + ((lane >> 4) << 3), dm * 2 + ((lane >> 3) & 1)), a);
+          mmat::mma16816(ot[dm], a, pb[kk][0], pb[kk][1]);
+        }
       }
       if (close) {
-        write_recs(__ldg(p.tile64 + j) + r0 / 64 + (off + BN - 1) / 64, fc, m0, m1, l0, l1, o, true);
+        const int64_t rec_idx = __ldg(p.tile64 + j) + r0 / 64 + (off + BN - 1) / 64;
+        const float to_nat = c2 * 0.69314718055994530942f;  // raw logit -> natural units (1/scale)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int f = fb * 8 + 2 * t + c;
+          if (f >= G || f >= p.fneed || !p.hdoc[f == 0 ? 0 : 1]) continue;
+          float* rec = p.partials + ((rec_idx * p.H + h) * p.fmax + f) * REC;
+          const float ll = c ? l1 : l0;
+          if (g8 == 0) {
+            rec[0] = ll > 0.f ? (c ? m1 : m0) * to_nat : -INFINITY;
+            rec[1] = ll;
+          }
+#pragma unroll
+          for (int dm = 0; dm < 4; ++dm) {
+            rec[4 + dm * 16 + g8] = ot[dm][c];
+            rec[4 + dm * 16 + g8 + 8] = ot[dm][2 + c];
+          }
+        }
       } else {
 #pragma unroll
-        for (int nb = 0; nb < 8; ++nb)
-          *reinterpret_cast<float4*>(stt + 4 * nb) = make_float4(o[nb][0], o[nb][1], o[nb][2], o[nb][3]);
-        stt[32] = m0, stt[33] = m1, stt[34] = l0, stt[35] = l1;
+        for (int k = 0; k < 4; ++k)
+          *reinterpret_cast<float4*>(stt + 4 * k) = make_float4(ot[k][0], ot[k][1], ot[k][2], ot[k][3]);
+        stt[16] = m0, stt[17] = m1, stt[18] = l0, stt[19] = l1;
       }
     }
   }
