@@ -161,6 +161,15 @@ def cpu_threads():
     return os.cpu_count() or 1
 
 
+def bench_config(args, world, n, s, doc_len, use_graph, total_tokens):
+    """The line's ``config`` (both arms print the same dict for the same flags)."""
+    return {"workload": workload_name(doc_len, s), "cuda_graph": bool(use_graph),
+            "prune_last_layer": bool(args.prune_last_layer), "pairs_per_gpu": n, "global_batch": n * world,
+            "seq_len": s, "doc_len": doc_len, "query_len": QUERY_LEN, "varlen": bool(args.varlen), "pattern": "sparse",
+            "window": 4, "layers": 12, "hidden": 768, "heads": 12, "ff": 3072, "parallelism": f"dp{world}",
+            "l2": f"inputs larger than L2 (qkv activations {total_tokens * 2304 * 2 / 1e9:.2f} GB per layer)"}
+
+
 def run_reference(args):
     """The reference arm: the CPU restatement of the reference's CrossEncoder.score (f32 numpy,
     all host cores), one whole (q10, d4086) pair per step -- the same workload, config and metric
@@ -180,8 +189,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
         "steps": len(times), "warmup": 1, "ms_per_step": t_pair * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generator ids, seed 0)",
-        "config": {"workload": workload_name(doc_len, s), "seq_len": s,
-                   "doc_len": doc_len, "query_len": QUERY_LEN, "window": 4, "pattern": "sparse"},
+        "config": bench_config(args, int(os.environ.get("WORLD_SIZE", "1")), args.pairs_per_gpu, s, doc_len,
+                               args.graph == "on" or (args.graph == "auto" and doc_len <= 512),
+                               args.pairs_per_gpu * s),
         "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cpu_threads(), "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -580,11 +590,7 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic: reference-generator token ids (default_rng((seed,q,i))), random-init ELECTRA-base weights",
-            "config": {"workload": workload_name(doc_len, s), "cuda_graph": use_graph, "prune_last_layer": bool(args.prune_last_layer),
-                       "pairs_per_gpu": n, "global_batch": n * world, "seq_len": s, "doc_len": doc_len,
-                       "query_len": QUERY_LEN, "varlen": bool(args.varlen), "pattern": "sparse", "window": 4,
-                       "layers": 12, "hidden": 768, "heads": 12, "ff": 3072, "parallelism": f"dp{world}",
-                       "l2": f"inputs larger than L2 (qkv activations {layout.total_tokens * 2304 * 2 / 1e9:.2f} GB per layer)"},
+            "config": bench_config(args, world, n, s, doc_len, use_graph, layout.total_tokens),
             "roofline": {"bound": "hbm", "kernel": "sc_attn_fwd (band_attn_kernel + head-row combine)",
                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                          "peak_kind": peak_kind, "traffic": traffic,
