@@ -354,6 +354,17 @@ SC_API int sc_residual_layernorm_f16x2(const float* resid, const float* y, const
                                        int32_t* range_status, int32_t* nonfinite_count, int32_t rows,
                                        int32_t hidden, void* stream);
 
+/* Fused FFN up-projection of the fast fp32 mode (CrossEncoder(fp32_gemm="f16x3")): out_planes =
+ * sc_split_f16x2 planes of gelu_erf(x1 W1^T + b1) (R/encoder.py:350-351, :258-259) with x1 W1^T as
+ * three fp16 tensor-core products in one tcgen05 GEMM: a_planes [M, 2K] = [h0 | h1] of x1,
+ * w_planes [N, 2K] = [g1 | g0] of W1 * 2^e (w_scale = 2^-e), accumulating h0 g1 + h1 g0 + h0 g0 in
+ * fp32; the epilogue adds the bias, applies erff GELU and writes [M, 2N] = [hi | lo] fp16 planes
+ * (the fp32 activation is never stored).  range_status as sc_split_f16x2's status.
+ * SC_ERR_UNSUPPORTED unless N % 256 == 0, K % 64 == 0 and rows are 16-byte aligned. */
+SC_API int sc_gemm_x3h_gelu_planes(const void* a_planes, int64_t lda, const void* w_planes, int64_t ldw,
+                                   float w_scale, const float* bias, void* out_planes, int64_t ldo,
+                                   int32_t* range_status, int32_t M, int32_t N, int32_t K, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -592,10 +592,14 @@ class CrossEncoder:
                           L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), x1.data_ptr(), None, None, T, h, stream,
                           exc=EncoderError)
                 x1s = self._xsplit(x1)
-            f = self._xlinear(x1s, L, "w1")
+            fs = self._w1_gelu_planes(x1s, L) if f16 and self.fused_ffn else None
+            if fs is None:
+                f = self._xlinear(x1s, L, "w1")
+                fs = self._xsplit(f, bias=L["b1_f32"], gelu=True)
+                del f
             del x1s
-            f2 = self._xlinear(self._xsplit(f, bias=L["b1_f32"], gelu=True), L, "w2")
-            del f
+            f2 = self._xlinear(fs, L, "w2")
+            del fs
             bad_i = bad[i:i + 1] if check_finite else None
             xs = self._ln_planes(x1, f2, L["b2_f32"], L, "ln2", x, bad_i, True) if f16 and i < last else None
             if xs is None:
@@ -604,6 +608,23 @@ class CrossEncoder:
                           _lib.ptr(bad_i), T, h, stream, exc=EncoderError)
         self._last_bad = bad if check_finite else None
         return x
+
+    def _w1_gelu_planes(self, x1s, L):
+        """f16x3: the fp16 planes of gelu(x1 W1^T + b1) from one tcgen05 GEMM with the bias, erff GELU
+        and the split in its epilogue (sc_gemm_x3h_gelu_planes); None if the shape is unsupported."""
+        T, cfg = x1s.shape[0], self.config
+        planes = torch.empty((T, 2 * cfg.ff_dim), dtype=torch.float16, device=x1s.device)
+        w = L["w1_x3h"]
+        rc = _lib.load().sc_gemm_x3h_gelu_planes(
+            x1s.data_ptr(), x1s.stride(0), w.data_ptr(), w.stride(0), float(L["w1_x3h_s"]), L["b1_f32"].data_ptr(),
+            planes.data_ptr(), planes.stride(0), _lib.ptr(self._range_flag), T, cfg.ff_dim, cfg.embed_dim,
+            _lib.stream_handle())
+        if rc == _lib.SC_OK:
+            _lib.launch_calls += 1
+            return planes
+        if rc != _lib.SC_ERR_UNSUPPORTED:
+            raise EncoderError(_lib.last_error())
+        return None
 
     def _ln_planes(self, resid, y, bias, L, ln, out, bad, qkv_input):
         """f16x3: out = LN(resid + y + bias) (fp32) and its fp16 GEMM planes from one pass

@@ -336,6 +336,42 @@ def test_residual_layernorm_f16x2_equals_ln_then_split(lib, h, onehot):
                  lib.stream_handle())
 
 
+def test_gemm_x3h_gelu_planes_matches_unfused(lib):
+    """sc_gemm_x3h_gelu_planes (W1 as three fp16 products + bias + erff GELU + split, one tcgen05 GEMM)
+    against the unfused f16x3 path (_linear_x3h on cuBLAS, then sc_split_f16x2 with bias + GELU) and
+    fp64: the planes reconstruct gelu(x W^T + b) as accurately as the unfused path; ragged M; range flag."""
+    from paper_2312_17649_b200.encoder import _linear_x3h, _split_weight_x3h, split_planes_h
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    M, K, N = 1031, 768, 3072
+    x = torch.randn((M, K), device="cuda", generator=g)
+    w = torch.randn((N, K), device="cuda", generator=g) * 0.03
+    b = torch.randn(N, device="cuda", generator=g) * 0.5
+    xs = split_planes_h(x)
+    w2, sc = _split_weight_x3h(w)
+    ref_pl = split_planes_h(_linear_x3h(xs, w2, sc), bias=b, gelu=True)
+    out = torch.empty((M, 2 * N), dtype=torch.float16, device="cuda")
+    rng = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lib.call("sc_gemm_x3h_gelu_planes", xs.data_ptr(), xs.stride(0), w2.data_ptr(), w2.stride(0), float(sc),
+             b.data_ptr(), out.data_ptr(), out.stride(0), rng.data_ptr(), M, N, K, lib.stream_handle())
+    got = out[:, :N].double() + out[:, N:].double()
+    ref = ref_pl[:, :N].double() + ref_pl[:, N:].double()
+    pre = x.double() @ w.double().t() + b.double()
+    exact = 0.5 * pre * (1 + torch.special.erf(pre / math.sqrt(2)))
+    e_got = (got - exact).abs().max().item()
+    e_ref = (ref - exact).abs().max().item()
+    print(f"fused max err {e_got:.3e}, unfused {e_ref:.3e}, fused vs unfused {(got - ref).abs().max().item():.3e}")
+    assert e_got <= 2 * e_ref + 1e-7, (e_got, e_ref)
+    assert int(rng.item()) == 0
+    big = torch.full((N,), 1e5, device="cuda")
+    lib.call("sc_gemm_x3h_gelu_planes", xs.data_ptr(), xs.stride(0), w2.data_ptr(), w2.stride(0), float(sc),
+             big.data_ptr(), out.data_ptr(), out.stride(0), rng.data_ptr(), M, N, K, lib.stream_handle())
+    assert int(rng.item()) == 1
+    with pytest.raises(NotImplementedError):
+        lib.call("sc_gemm_x3h_gelu_planes", xs.data_ptr(), xs.stride(0), w2.data_ptr(), w2.stride(0), float(sc),
+                 b.data_ptr(), out.data_ptr(), out.stride(0), None, M, 300, K, lib.stream_handle())
+
+
 def test_linear_x3h_matches_fp64():
     """_linear_x3h (three split-fp16 products, weights scaled by 2^e) is about as accurate as fp32 SGEMM
     (K = 768: one main accumulation; K = 3072: four chunks); bias folded into the first GEMM."""
