@@ -390,10 +390,16 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    gloo = args.dist_backend == "gloo"
+    # gloo (test harness only): several ranks may share one GPU; collectives run on host copies
+    local = local % torch.cuda.device_count() if gloo else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     _lib.load()
     hbm_peak, tf_burst, tf_sus, peak_kind = peaks()
     cfg, doc_len, s = workload(args)
@@ -408,10 +414,23 @@ def run_gpu(args):
     stream = torch.cuda.current_stream()
 
     def gather(scores):
+        if world > 1 and gloo:
+            parts = [torch.empty_like(scores, device="cpu") for _ in range(world)]
+            dist.all_gather(parts, scores.cpu())
+            return torch.cat(parts).to(dev)
         if world > 1:
             dist.all_gather_into_tensor(gathered, scores)
             return gathered
         return scores
+
+    def reduce_max(t):  # device scalar -> max over ranks
+        if world > 1 and gloo:
+            c = t.cpu()
+            dist.all_reduce(c, op=dist.ReduceOp.MAX)
+            return c
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t
 
     attn_events = []
 
@@ -456,10 +475,7 @@ def run_gpu(args):
         launches += graphed.kernels_per_replay * args.steps
     ms = e0.elapsed_time(e1)
     attn_ms = [attn_events[i].elapsed_time(attn_events[i + 1]) for i in range(0, len(attn_events), 2)]
-    t = torch.tensor([ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = float(reduce_max(torch.tensor([ms], device=dev)).item())
     pairs_total = n * world * args.steps
     value = pairs_total / (ms_max / 1e3)
 
@@ -487,9 +503,7 @@ def run_gpu(args):
         e2e_step()
     f1.record(stream)
     barrier()
-    te = torch.tensor([f0.elapsed_time(f1)], device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    te = reduce_max(torch.tensor([f0.elapsed_time(f1)], device=dev))
     e2e_value = n * world * e2e_steps / (float(te.item()) / 1e3)
 
     # ---- parity of this run's own scores (outside the timed regions) ----
@@ -510,9 +524,7 @@ def run_gpu(args):
             device_step()
         v1.record(stream)
         barrier()
-        tv = torch.tensor([v0.elapsed_time(v1)], device=dev)
-        if world > 1:
-            dist.all_reduce(tv, op=dist.ReduceOp.MAX)
+        tv = reduce_max(torch.tensor([v0.elapsed_time(v1)], device=dev))
         model.prune_last_layer = False
         variants["prune_last_layer"] = {
             "value": n * world * vsteps / (float(tv.item()) / 1e3), "unit": "pairs/s", "steps": vsteps,
@@ -641,6 +653,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU oracle timing (cpu_baseline)")
     ap.add_argument("--ref-budget", type=float, default=120.0, help="seconds of timed pairs in --impl reference")
     ap.add_argument("--no-variants", action="store_true", help="skip the passages / sweep / fp32 variants")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N > 1: process group backend (gloo: test harness, ranks may share a GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
