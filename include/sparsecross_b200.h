@@ -365,6 +365,15 @@ SC_API int sc_gemm_x3h_gelu_planes(const void* a_planes, int64_t lda, const void
                                    float w_scale, const float* bias, void* out_planes, int64_t ldo,
                                    int32_t* range_status, int32_t M, int32_t N, int32_t K, void* stream);
 
+/* fp32 projection of the fast fp32 mode on the same tcgen05 GEMM: out[M][N] (fp32) =
+ * w_scale * ([h0 | e | h1] . [g1 | b1 | g0] + [h0 | e] . [g0 | b0]) -- x W^T (+ the bias carried by
+ * the constant column e when bias_cols == 8; bias_cols == 0: plain [h0 | h1] and [g1 | g0]) as the
+ * three fp16 products of encoder.py _linear_x3h (R/encoder.py:322-324, :345), accumulated in one
+ * fp32 TMEM accumulator.  a_planes as sc_split_f16x2 writes them, w_planes [N, 2K + 2*bias_cols].
+ * SC_ERR_UNSUPPORTED unless N % 256 == 0, K % 64 == 0 and rows are 16-byte aligned. */
+SC_API int sc_gemm_x3h(const void* a_planes, int64_t lda, const void* w_planes, int64_t ldw, float w_scale,
+                       float* out, int64_t ldo, int32_t M, int32_t N, int32_t K, int32_t bias_cols, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,6 +84,7 @@ SIGNATURES = {
     "sc_split_f16x2": (C.c_int, [_p, _i64, _p, _i32, _p, _i64, _p, _i64, _i64, _i32, _i32, _p, _p]),
     "sc_residual_layernorm_f16x2": (C.c_int, [_p, _p, _p, _p, _p, _p, _p, _i64, _i32, _p, _p, _i32, _i32, _p]),
     "sc_gemm_x3h_gelu_planes": (C.c_int, [_p, _i64, _p, _i64, _f32, _p, _p, _i64, _p, _i32, _i32, _i32, _p]),
+    "sc_gemm_x3h": (C.c_int, [_p, _i64, _p, _i64, _f32, _p, _i64, _i32, _i32, _i32, _i32, _p]),
 }
 
 # Entry points that launch device work (counted for the bench's gpu_launches).

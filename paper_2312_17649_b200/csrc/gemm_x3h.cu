@@ -43,10 +43,16 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
   return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1) gemm_x3h_gelu_planes_kernel(
+// kGelu: epilogue = bias + erff GELU + fp16 hi/lo planes (tmO: fp16 [M, 2N], 64-column boxes);
+// else fp32 out = acc * scale (+ bias) (tmO: fp32 [M, N], 32-column boxes).  kb = 0, or 8 when the
+// planes carry a constant column / bias columns (sc_split_f16x2 onehot, the QKV weight planes): the
+// correction k-blocks then span 2K + 8 columns and the main product's W block starts at K + 8; the
+// maps' widths make TMA zero-fill whatever a 64-column box reads past them.
+template <bool kGelu>
+__global__ void __launch_bounds__(NTHREADS, 1) gemm_x3h_kernel(
     const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
     const __grid_constant__ CUtensorMap tmO, const float* __restrict__ bias, float scale, int32_t* __restrict__ range,
-    int M, int N, int K) {
+    int M, int N, int K, int kb8) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sm0 = smem_u32(smem);
@@ -55,7 +61,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_x3h_gelu_planes_kernel(
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + SMEM_BAR + (2 * NS + 4) * 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_n = N / BN, tiles = ((M + BM - 1) / BM) * tiles_n;
-  const int nk_c = 2 * K / BK, nk = nk_c + K / BK;  // correction k-blocks, then the main product's
+  const int nk_c = (2 * K + kb8 + BK - 1) / BK, nk = nk_c + (K + kb8 + BK - 1) / BK;  // corrections, then main
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -92,7 +98,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_x3h_gelu_planes_kernel(
           if (it >= NS) mbar_wait(empty_bar + 8 * s, ((it / NS) & 1) ^ 1);
           // corrections: A[:, kb*64] x W[:, kb*64] over [h0 | h1] x [g1 | g0]; main: h0 x g0
           const int ca = kb < nk_c ? kb * BK : (kb - nk_c) * BK;
-          const int cb = kb < nk_c ? kb * BK : K + (kb - nk_c) * BK;
+          const int cb = kb < nk_c ? kb * BK : K + kb8 + (kb - nk_c) * BK;
           mbar_expect_tx(full_bar + 8 * s, STAGE);
           tma_load_2d(sm0 + s * STAGE, &tmA, ca, m0, full_bar + 8 * s);
           tma_load_2d(sm0 + s * STAGE + A_BYTES, &tmB, cb, n0, full_bar + 8 * s);
@@ -149,19 +155,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_x3h_gelu_planes_kernel(
           if (lane == 0) mbar_arrive(acc_empty + 8 * buf);
         }
         const float* bc = sb + c * 64;
-        uint32_t hi[32], lo[32];
+        uint32_t hi[32], lo[32];  // kGelu: fp16 hi / lo pairs; else the two 32-column fp32 halves
+        if constexpr (kGelu) {
 #pragma unroll
-        for (int e = 0; e < 64; e += 2) {
-          float x0 = fmaf(__uint_as_float(v[e]), scale, bc[e]);
-          float x1 = fmaf(__uint_as_float(v[e + 1]), scale, bc[e + 1]);
-          x0 = 0.5f * x0 * (1.f + erff(x0 * 0.70710678118654752440f));
-          x1 = 0.5f * x1 * (1.f + erff(x1 * 0.70710678118654752440f));
-          bad |= !(fabsf(x0) < 65504.f && fabsf(x1) < 65504.f);
-          const __half2 h = __floats2half2_rn(x0, x1);
-          const float2 hf = __half22float2(h);
-          const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
-          hi[e / 2] = *reinterpret_cast<const uint32_t*>(&h);
-          lo[e / 2] = *reinterpret_cast<const uint32_t*>(&l);
+          for (int e = 0; e < 64; e += 2) {
+            float x0 = fmaf(__uint_as_float(v[e]), scale, bc[e]);
+            float x1 = fmaf(__uint_as_float(v[e + 1]), scale, bc[e + 1]);
+            x0 = 0.5f * x0 * (1.f + erff(x0 * 0.70710678118654752440f));
+            x1 = 0.5f * x1 * (1.f + erff(x1 * 0.70710678118654752440f));
+            bad |= !(fabsf(x0) < 65504.f && fabsf(x1) < 65504.f);
+            const __half2 h = __floats2half2_rn(x0, x1);
+            const float2 hf = __half22float2(h);
+            const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+            hi[e / 2] = *reinterpret_cast<const uint32_t*>(&h);
+            lo[e / 2] = *reinterpret_cast<const uint32_t*>(&l);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            hi[e] = __float_as_uint(fmaf(__uint_as_float(v[e]), scale, bc[e]));
+            lo[e] = __float_as_uint(fmaf(__uint_as_float(v[32 + e]), scale, bc[32 + e]));
+          }
         }
         // staging pair (chunk & 1) is free once the stores issued two chunks ago (two groups per chunk)
         // have read it
@@ -181,8 +195,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_x3h_gelu_planes_kernel(
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         epi_sync();
         if (et == 0) {
-          tma_store_2d(&tmO, stg, n0 + c * 64, m0);                   // hi plane: columns [0, N)
-          tma_store_2d(&tmO, stg + STG_BYTES, N + n0 + c * 64, m0);   // lo plane: columns [N, 2N)
+          if constexpr (kGelu) {
+            tma_store_2d(&tmO, stg, n0 + c * 64, m0);                  // hi plane: columns [0, N)
+            tma_store_2d(&tmO, stg + STG_BYTES, N + n0 + c * 64, m0);  // lo plane: columns [N, 2N)
+          } else {
+            tma_store_2d(&tmO, stg, n0 + c * 64, m0);                  // fp32 columns c*64 .. +31
+            tma_store_2d(&tmO, stg + STG_BYTES, n0 + c * 64 + 32, m0); //              c*64+32 .. +63
+          }
         }
       }
     }
@@ -201,6 +220,57 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_x3h_gelu_planes_kernel(
 }  // namespace sc
 
 using namespace sc;
+
+namespace sc {
+namespace gx {
+// fp32 [rows][cols] as a 2-D map with 32-column (128 B) x box_rows boxes, 128B swizzle.
+static bool make_map_f32(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t ld, int box_rows) {
+  static tcx::EncodeFn enc = nullptr;
+  if (!enc) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    enc = reinterpret_cast<tcx::EncodeFn>(ptr);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool kGelu>
+static int launch_x3h(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mO, const float* bias,
+                      float scale, int32_t* range, int M, int N, int K, int kb8, cudaStream_t st, const char* name) {
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (num_sms <= 0) num_sms = 148;
+  }
+  static bool attr = false;
+  const size_t smem = SMEM_TOTAL + 1024;
+  if (!attr) {
+    if (cudaFuncSetAttribute(gemm_x3h_kernel<kGelu>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess) {
+      set_error("%s: shared memory request of %zu bytes failed", name, smem);
+      return SC_ERR_UNSUPPORTED;
+    }
+    attr = true;
+  }
+  const int tiles = ((M + BM - 1) / BM) * (N / BN);
+  gemm_x3h_kernel<kGelu><<<tiles < num_sms ? tiles : num_sms, NTHREADS, smem, st>>>(mA, mB, mO, bias, scale, range,
+                                                                                    M, N, K, kb8);
+  SC_CHECK_LAUNCH("gemm_x3h_kernel");
+  return SC_OK;
+}
+}  // namespace gx
+}  // namespace sc
 
 extern "C" int sc_gemm_x3h_gelu_planes(const void* a_planes, int64_t lda, const void* w_planes, int64_t ldw,
                                        float w_scale, const float* bias, void* out_planes, int64_t ldo,
@@ -222,26 +292,28 @@ extern "C" int sc_gemm_x3h_gelu_planes(const void* a_planes, int64_t lda, const 
     set_error("sc_gemm_x3h_gelu_planes: cuTensorMapEncodeTiled failed");
     return SC_ERR_UNSUPPORTED;
   }
-  static int num_sms = 0;
-  if (!num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (num_sms <= 0) num_sms = 148;
+  return launch_x3h<true>(mA, mB, mO, bias, w_scale, range_status, M, N, K, 0, (cudaStream_t)stream,
+                         "sc_gemm_x3h_gelu_planes");
+}
+
+extern "C" int sc_gemm_x3h(const void* a_planes, int64_t lda, const void* w_planes, int64_t ldw, float w_scale,
+                           float* out, int64_t ldo, int32_t M, int32_t N, int32_t K, int32_t bias_cols, void* stream) {
+  using namespace gx;
+  SC_CHECK_ARG(a_planes && w_planes && out && M >= 0 && N >= 1 && K >= 1 && (bias_cols == 0 || bias_cols == 8),
+               "sc_gemm_x3h: bad arguments");
+  if (M == 0) return SC_OK;
+  const int64_t acols = 2LL * K + bias_cols, wcols = 2LL * K + 2 * bias_cols;
+  if (N % BN || K % BK || lda < acols || ldw < wcols || ldo < N || (lda * 2) % 16 || (ldw * 2) % 16 ||
+      (ldo * 4) % 16 || (((uintptr_t)a_planes | (uintptr_t)w_planes | (uintptr_t)out) & 15)) {
+    set_error("sc_gemm_x3h: needs N %% 256 == 0, K %% 64 == 0 and 16-byte aligned rows");
+    return SC_ERR_UNSUPPORTED;
   }
-  static bool attr = false;
-  const size_t smem = SMEM_TOTAL + 1024;
-  if (!attr) {
-    if (cudaFuncSetAttribute(gemm_x3h_gelu_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess) {
-      set_error("sc_gemm_x3h_gelu_planes: shared memory request of %zu bytes failed", smem);
-      return SC_ERR_UNSUPPORTED;
-    }
-    attr = true;
+  CUtensorMap mA, mB, mO;
+  if (!make_map(&mA, a_planes, acols, M, lda, BM) || !make_map(&mB, w_planes, wcols, N, ldw, BN) ||
+      !make_map_f32(&mO, out, N, M, ldo, BM)) {
+    set_error("sc_gemm_x3h: cuTensorMapEncodeTiled failed");
+    return SC_ERR_UNSUPPORTED;
   }
-  const int tiles = ((M + BM - 1) / BM) * (N / BN);
-  gemm_x3h_gelu_planes_kernel<<<tiles < num_sms ? tiles : num_sms, NTHREADS, smem, (cudaStream_t)stream>>>(
-      mA, mB, mO, bias, w_scale, range_status, M, N, K);
-  SC_CHECK_LAUNCH("gemm_x3h_gelu_planes_kernel");
-  return SC_OK;
+  return launch_x3h<false>(mA, mB, mO, nullptr, w_scale, nullptr, M, N, K, bias_cols, (cudaStream_t)stream,
+                           "sc_gemm_x3h");
 }

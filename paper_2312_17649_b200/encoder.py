@@ -375,6 +375,25 @@ def _linear_x3h(planes: torch.Tensor, w2: torch.Tensor, s: float, chunk: int | N
     return c
 
 
+def _linear_x3h_tc(planes: torch.Tensor, w2: torch.Tensor, s: float) -> torch.Tensor | None:
+    """_linear_x3h as one tcgen05 GEMM (sc_gemm_x3h): the three fp16 products (and the bias columns)
+    accumulated in one fp32 TMEM accumulator, scaled by s in the epilogue -- no fp32 partial result
+    written and re-read between the products.  None when the shape is unsupported (cuBLAS path)."""
+    kb = 8 if w2.shape[1] == planes.shape[1] + 8 else 0
+    if w2.shape[1] != planes.shape[1] + kb:
+        raise EncoderError(f"split planes {tuple(planes.shape)} do not match the weight planes {tuple(w2.shape)}")
+    M, K, N = planes.shape[0], (planes.shape[1] - kb) // 2, w2.shape[0]
+    out = torch.empty((M, N), dtype=torch.float32, device=planes.device)
+    rc = _lib.load().sc_gemm_x3h(planes.data_ptr(), planes.stride(0), w2.data_ptr(), w2.stride(0), float(s),
+                                 out.data_ptr(), out.stride(0), M, N, K, kb, _lib.stream_handle())
+    if rc == _lib.SC_OK:
+        _lib.launch_calls += 1
+        return out
+    if rc != _lib.SC_ERR_UNSUPPORTED:
+        raise EncoderError(_lib.last_error())
+    return None
+
+
 class CrossEncoder:
     """Config + device weights; batched inference (R/encoder.py:450-538)."""
 
@@ -550,7 +569,12 @@ class CrossEncoder:
         if self.fp32_gemm == "bf16x6":
             c = _linear_x6(planes, L[name + "_x6"])
             return c.add_(L["bqkv_f32"]) if with_bias else c
-        return _linear_x3h(planes, L[name + "_x3h"], L[name + "_x3h_s"])  # f16x3: bias folded in (wqkv)
+        w2, sc = L[name + "_x3h"], L[name + "_x3h_s"]
+        if self.fused_ffn and name in ("wqkv", "wo"):  # K = 768: one accumulation on our tcgen05 GEMM
+            c = _linear_x3h_tc(planes, w2, sc)
+            if c is not None:
+                return c
+        return _linear_x3h(planes, w2, sc)  # f16x3: bias folded in (wqkv)
 
     def _encode_x6(self, ids_dev, layout, check_finite, attn_hook, cls_only) -> torch.Tensor:
         """encode_packed for fp32 with the projections as split products (fp32_gemm="bf16x6" / "f16x3").

@@ -372,6 +372,29 @@ def test_gemm_x3h_gelu_planes_matches_unfused(lib):
                  b.data_ptr(), out.data_ptr(), out.stride(0), None, M, 300, K, lib.stream_handle())
 
 
+@pytest.mark.parametrize("bias", [False, True])
+@pytest.mark.parametrize("N", [768, 2304])
+def test_gemm_x3h_matches_cublas_path_and_fp64(lib, bias, N):
+    """sc_gemm_x3h (the three fp16 products + the bias columns in one tcgen05 accumulation, fp32 out) vs
+    _linear_x3h on cuBLAS and fp64 at K = 768: as accurate as the cuBLAS form; ragged M."""
+    from paper_2312_17649_b200.encoder import _linear_x3h, _linear_x3h_tc, _split_weight_x3h, split_planes_h
+
+    g = torch.Generator(device="cuda").manual_seed(N + bias)
+    M, K = 1037, 768
+    x = torch.randn((M, K), device="cuda", generator=g)
+    w = torch.randn((N, K), device="cuda", generator=g) * 0.03
+    b = torch.randn(N, device="cuda", generator=g) if bias else None
+    xs = split_planes_h(x, onehot=bias)
+    w2, sc = _split_weight_x3h(w, b)
+    got = _linear_x3h_tc(xs, w2, sc)
+    ref = _linear_x3h(xs, w2, sc)
+    exact = x.double() @ w.double().t() + (b.double() if bias else 0)
+    e_got = (got.double() - exact).abs().max().item()
+    e_ref = (ref.double() - exact).abs().max().item()
+    print(f"x3h tc max err {e_got:.3e}, cuBLAS form {e_ref:.3e}")
+    assert e_got <= 1.5 * e_ref + 1e-7, (e_got, e_ref)
+
+
 def test_linear_x3h_matches_fp64():
     """_linear_x3h (three split-fp16 products, weights scaled by 2^e) is about as accurate as fp32 SGEMM
     (K = 768: one main accumulation; K = 3072: four chunks); bias folded into the first GEMM."""
