@@ -281,3 +281,28 @@ def test_bench_batch_prefix_is_the_ranking_golden():
     batch = bench.make_batch(P, cfg, 4086, 4, 0)
     want = doc_batch(4, P.EncoderConfig(**cases.ELECTRA_DOC, precision="bf16"))
     assert np.array_equal(batch.ids, want.ids)
+
+
+def test_bench_reference_arm_line_matches_gpu_arm_config():
+    """`bench.py --impl reference` (the CPU arm the driver times beside ours) prints one contract line
+    with the same metric and the same ``config`` dict the GPU arm prints for the same flags."""
+    import json
+    import subprocess
+    import sys
+    import types
+
+    import bench
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "3",
+                          "--ref-budget", "1", "--doc-len", "164"], cwd=root, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["metric"] == bench.METRIC and d["unit"] == "pairs/s"
+    assert d["higher_is_better"] is True and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"] == {"value": d["value"], "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    args = types.SimpleNamespace(prune_last_layer=False, varlen=False)
+    s = bench.QUERY_LEN + 164 + 3
+    assert d["config"] == bench.bench_config(args, 1, 64, s, 164, True, 64 * s)
