@@ -55,7 +55,7 @@ constexpr int REC = D + 4; // split-softmax record: m, l, pad, pad, acc[D] (16B-
 // stage loads are already in flight NS items ahead and the extra L2 fills only compete with them.
 #define SC_BAND_PF 0
 #endif
-__host__ __device__ constexpr int min_ctas(int nbc) { return nbc == 1 ? SC_BAND_CTAS1 : 2; }
+__host__ __device__ constexpr int min_ctas(int nbc, int qfg = 0) { return nbc == 1 || qfg ? SC_BAND_CTAS1 : 2; }
 
 struct Params {
   int nseq, H, w, kb_rows, fneed, fmax, padding;
@@ -72,6 +72,9 @@ struct Params {
   const int32_t* cu;
   const int32_t* qlen;
   const int32_t* tile_base;
+  const __nv_bfloat16* q;  // QFG variants: the cls + query rows' q read from global memory
+  int64_t ld_q;
+  int T;
   __nv_bfloat16* out;
   int64_t ld_out;
   float* partials;
@@ -427,9 +430,13 @@ __device__ __forceinline__ uint32_t movm_t(uint32_t x) {
 // the sparse pattern uses one.  P^T moves from the C layout of S^T to the B layout of the PV
 // product by movmatrix.  Record f: (m, l, -, -, acc[64]) -- m in natural logit units, l the sum of
 // exp(s - m) over the tile's keys, acc = sum exp(s - m) v (R/attention.py:416-473 split form).
-template <int PAIR>
+__device__ __forceinline__ uint32_t ldg_pair(const __nv_bfloat16* base, int64_t row, int T, int64_t ld, int col) {
+  return row < T ? __ldg(reinterpret_cast<const uint32_t*>(base + row * ld + col)) : 0u;
+}
+
+template <int PAIR, int QFG = 0>
 __device__ __forceinline__ void full_row_records(const Params& p, uint32_t qf, uint32_t kb, uint32_t vb, int lane,
-                                                 int tile, int h, int rows_here) {
+                                                 int tile, int h, int rows_here, int qrow0) {
   const int g8 = lane >> 2, t = lane & 3;
   const float c2 = p.c2;
   const float to_nat = c2 * 0.69314718055994530942f;  // raw logit -> natural units (1/scale)
@@ -442,11 +449,21 @@ __device__ __forceinline__ void full_row_records(const Params& p, uint32_t qf, u
     for (int fb = 0; fb * 8 < p.fneed; ++fb) {
       // B fragments of full rows fb*8 .. fb*8+7 (Qf rows = B columns): k-steps 2i, 2i+1 per x4
       uint32_t qb[4][2];
+      if constexpr (QFG) {  // B fragments straight from the rows' q (L2): rows qrow0 + fb*8 + g8
+        const __nv_bfloat16* qh = p.q + h * 64;
+        const int64_t row = qrow0 + fb * 8 + g8;
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        uint32_t r[4];
-        ldsm_x4(swz(qf, fb * 8 + (lane & 7), 4 * i + (lane >> 3)), r);
-        qb[2 * i][0] = r[0]; qb[2 * i][1] = r[1]; qb[2 * i + 1][0] = r[2]; qb[2 * i + 1][1] = r[3];
+        for (int ks = 0; ks < 4; ++ks) {
+          qb[ks][0] = ldg_pair(qh, row, p.T, p.ld_q, ks * 16 + 2 * t);
+          qb[ks][1] = ldg_pair(qh, row, p.T, p.ld_q, ks * 16 + 8 + 2 * t);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          uint32_t r[4];
+          ldsm_x4(swz(qf, fb * 8 + (lane & 7), 4 * i + (lane >> 3)), r);
+          qb[2 * i][0] = r[0]; qb[2 * i][1] = r[1]; qb[2 * i + 1][0] = r[2]; qb[2 * i + 1][1] = r[3];
+        }
       }
       float s[4][4];
 #pragma unroll
@@ -531,8 +548,11 @@ __device__ __forceinline__ void full_row_records(const Params& p, uint32_t qf, u
 // GR: global rows staged per head (16 or 32).  NS: pipeline stages.
 // NBB: band n8 blocks of the single-shot path (NBC = 1): 3 when 16 + 2w <= 24.
 // PAIR (head_dim 32, NBC = 1): items are head pairs (2h, 2h + 1) sharing the 64-dim smem rows.
-template <int NBC, int GR, int NS, int NBB = 4, int PAIR = 0>
-__global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
+// QFG (NBC = 2, 8 < w <= 16): no Qf box in the stage (the producer's records and the first tile's head
+// rows read those q rows from L2), the band's second chunk is 16 keys (16 + 2w <= 48), Kb/Vb rows = the
+// 96-row box: a 36 KB stage, so three CTAs per SM fit two stages each.
+template <int NBC, int GR, int NS, int NBB = 4, int PAIR = 0, int QFG = 0>
+__global__ void __launch_bounds__(NTHREADS, min_ctas(NBC, QFG)) band_attn_kernel(
     const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQf,
     const __grid_constant__ CUtensorMap tmKg, const __grid_constant__ CUtensorMap tmVg,
     const __grid_constant__ CUtensorMap tmKb, const __grid_constant__ CUtensorMap tmVb,
@@ -547,26 +567,28 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
   const int ntiles = __ldg(p.tile_base + p.nseq);
   if ((int)blockIdx.x >= ntiles) return;
   const int w = p.w;
-  constexpr int kb_rows = 48 + 32 * NBC;
+  constexpr int kb_rows = QFG ? 96 : 48 + 32 * NBC;
+  constexpr int NF = QFG ? 2 : 3;  // cls + query row boxes per stage: K, V (, Q)
   constexpr int q_bytes = BM * ROWB, f_bytes = GR * ROWB, kb_bytes = kb_rows * ROWB;
-  constexpr int stage_bytes = q_bytes + 3 * f_bytes + 2 * kb_bytes;
+  constexpr int stage_bytes = q_bytes + NF * f_bytes + 2 * kb_bytes;
+  constexpr int g_off = q_bytes + (QFG ? 0 : f_bytes);  // Kg, then Vg
   const int kb_box = BM + 2 * w;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * stage_bytes);
   const uint32_t sm0 = smem_u32(smem);
   auto q_buf = [&](int s) { return sm0 + s * stage_bytes; };
   auto qf_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes; };
-  auto kg_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + f_bytes; };
-  auto vg_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + 2 * f_bytes; };
-  auto kb_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + 3 * f_bytes; };
-  auto vb_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + 3 * f_bytes + kb_bytes; };
+  auto kg_buf = [&](int s) { return sm0 + s * stage_bytes + g_off; };
+  auto vg_buf = [&](int s) { return sm0 + s * stage_bytes + g_off + f_bytes; };
+  auto kb_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + NF * f_bytes; };
+  auto vb_buf = [&](int s) { return sm0 + s * stage_bytes + q_bytes + NF * f_bytes + kb_bytes; };
   const uint32_t full_bar = smem_u32(bars), empty_bar = smem_u32(bars + NS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // Zero the Kb/Vb rows the TMA box never writes (band chunks read up to kb_rows).
   for (int s = 0; s < NS; ++s) {
-    uint8_t* kb = smem + s * stage_bytes + q_bytes + 3 * f_bytes;
+    uint8_t* kb = smem + s * stage_bytes + q_bytes + NF * f_bytes;
     for (int o = kb_box * ROWB + threadIdx.x * 16; o < kb_bytes; o += NTHREADS * 16) {
       *reinterpret_cast<uint4*>(kb + o) = make_uint4(0, 0, 0, 0);
       *reinterpret_cast<uint4*>(kb + kb_bytes + o) = make_uint4(0, 0, 0, 0);
@@ -593,13 +615,15 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         prefetch_map(&tmKg); prefetch_map(&tmVg); prefetch_map(&tmQf);
       }
       __syncwarp();
-      const uint32_t bytes = (uint32_t)((p.doc_rows ? q_bytes : 0) + 3 * f_bytes + 2 * kb_box * ROWB);
+      const uint32_t bytes = (uint32_t)((p.doc_rows ? q_bytes : 0) + NF * f_bytes + 2 * kb_box * ROWB);
       const bool recs = p.fneed > 0 && !p.cls_skip;
-      int it = 0, prev_tile = -1, prev_h = 0, prev_rows = 0;
+      int it = 0, prev_tile = -1, prev_h = 0, prev_rows = 0, prev_start = 0;
       auto records = [&](int pit) {  // full-row records of item pit, then release its stage
         const int sp = pit % NS;
         mbar_wait(full_bar + 8 * sp, (pit / NS) & 1);
-        if (recs) full_row_records<PAIR>(p, qf_buf(sp), kb_buf(sp), vb_buf(sp), lane, prev_tile, prev_h, prev_rows);
+        if (recs)
+          full_row_records<PAIR, QFG>(p, qf_buf(sp), kb_buf(sp), vb_buf(sp), lane, prev_tile, prev_h, prev_rows,
+                                      prev_start);
         __syncwarp();
         if (elect_one()) mbar_arrive(empty_bar + 8 * sp);
         __syncwarp();
@@ -627,11 +651,11 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
             tma_load_3d(vb_buf(s), &tmVb, h, doc_row0 - w, fb);
             tma_load_3d(kg_buf(s), &tmKg, h, g.start, fb);
             tma_load_3d(vg_buf(s), &tmVg, h, g.start, fb);
-            tma_load_3d(qf_buf(s), &tmQf, h, g.start, fb);
+            if (!QFG) tma_load_3d(qf_buf(s), &tmQf, h, g.start, fb);
           }
           __syncwarp();
           if (it > 0) records(it - 1);
-          prev_tile = tile; prev_h = h; prev_rows = rows_here;
+          prev_tile = tile; prev_h = h; prev_rows = rows_here; prev_start = g.start;
         }
       }
       if (it > 0) records(it - 1);
@@ -810,6 +834,18 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
   #pragma unroll
           for (int bc = 0; bc < NBC; ++bc) {
             const int kb0 = wr0 + 32 * bc;
+            if (QFG && bc == NBC - 1) {  // the band's last 16 keys (16 + 2w <= 48)
+              float sc[2][4];
+              qk16(kb_buf(s), kb0, LO, qa, sc[0], sc[1]);
+  #pragma unroll
+              for (int nb = 0; nb < 2; ++nb)
+  #pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (!((bmask[bc] >> (nb * 4 + e)) & 1)) sc[nb][e] = -INFINITY;
+              softmax_update<2>(sc, c2, m0, m1, l0, l1, o);
+              pv16(vb_buf(s), kb0, LO, sc[0], sc[1], o);
+              continue;
+            }
             float sc[4][4];
             qk16(kb_buf(s), kb0, LO, qa, sc[0], sc[1]);
             qk16(kb_buf(s), kb0 + 16, LO, qa, sc[2], sc[3]);
@@ -880,7 +916,19 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC)) band_attn_kernel(
         for (int fc = 0; fc < GR / 16; ++fc) {
           if (fc * 16 < G) {
             uint32_t qa[4][4];
-            load_q(qf_buf(s), fc * 16, LO, qa);
+            if constexpr (QFG) {  // A fragments of rows fc*16 + (gq, gq + 8) straight from their q (L2)
+              const __nv_bfloat16* qh = p.q + h * 64;
+              const int64_t ra0 = g.start + fc * 16 + gq;
+  #pragma unroll
+              for (int ks = 0; ks < 4; ++ks) {
+                qa[ks][0] = ldg_pair(qh, ra0, p.T, p.ld_q, ks * 16 + 2 * tq);
+                qa[ks][1] = ldg_pair(qh, ra0 + 8, p.T, p.ld_q, ks * 16 + 2 * tq);
+                qa[ks][2] = ldg_pair(qh, ra0, p.T, p.ld_q, ks * 16 + 8 + 2 * tq);
+                qa[ks][3] = ldg_pair(qh, ra0 + 8, p.T, p.ld_q, ks * 16 + 8 + 2 * tq);
+              }
+            } else {
+              load_q(qf_buf(s), fc * 16, LO, qa);
+            }
             float sc[GR / 8][4];
   #pragma unroll
             for (int gc = 0; gc < GR / 16; ++gc) {
@@ -1091,22 +1139,25 @@ static bool make_map(CUtensorMap* m, const void* base, int d, int heads, int64_t
 using KernelFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, Params);
 
 // Stage count: as many as fit two CTAs per SM (<= ~113 KB each), at least 2.
-template <int NBC, int GR>
+template <int NBC, int GR, int QFG = 0>
+constexpr int stage_bytes_of() {
+  return (BM + (QFG ? 2 : 3) * GR + 2 * (QFG ? 96 : 48 + 32 * NBC)) * ROWB;
+}
+template <int NBC, int GR, int QFG = 0>
 constexpr int stages_for() {
-  constexpr int stage_bytes = (BM + 3 * GR + 2 * (48 + 32 * NBC)) * ROWB;
-  constexpr int budget = 227 * 1024 / min_ctas(NBC) - 2048;
-  return (3 * stage_bytes <= budget) ? 3 : 2;
+  constexpr int budget = 227 * 1024 / min_ctas(NBC, QFG) - 2048;
+  return (3 * stage_bytes_of<NBC, GR, QFG>() <= budget) ? 3 : 2;
 }
 
-template <int NBC, int GR, int NBB = 4, int PAIR = 0>
+template <int NBC, int GR, int NBB = 4, int PAIR = 0, int QFG = 0>
 static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, cudaStream_t st) {
-  constexpr int NS = stages_for<NBC, GR>();
-  constexpr int stage_bytes = (BM + 3 * GR + 2 * (48 + 32 * NBC)) * ROWB;
+  constexpr int NS = stages_for<NBC, GR, QFG>();
+  constexpr int stage_bytes = stage_bytes_of<NBC, GR, QFG>();
   constexpr size_t smem = (size_t)NS * stage_bytes + 2 * NS * 8 + 64 + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS, NBB, PAIR>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS, NBB, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS, NBB, PAIR, QFG>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (cudaFuncSetAttribute(band_attn_kernel<NBC, GR, NS, NBB, PAIR, QFG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess) {
       set_error("band kernel: shared memory request of %zu bytes failed", smem);
       return SC_ERR_UNSUPPORTED;
@@ -1123,11 +1174,18 @@ static int launch_one(const CUtensorMap* maps, const Params& p, unsigned grid, c
   }
   static int grid_cap = -1;  // measurement only (SC_BAND_GRID=N): persistent grid of N CTAs
   if (grid_cap < 0) grid_cap = getenv("SC_BAND_GRID") ? atoi(getenv("SC_BAND_GRID")) : 0;
-  const unsigned slots = grid_cap > 0 ? (unsigned)grid_cap : (unsigned)(num_sms * min_ctas(NBC));
-  band_attn_kernel<NBC, GR, NS, NBB, PAIR><<<grid < slots ? grid : slots, NTHREADS, smem, st>>>(
+  const unsigned slots = grid_cap > 0 ? (unsigned)grid_cap : (unsigned)(num_sms * min_ctas(NBC, QFG));
+  band_attn_kernel<NBC, GR, NS, NBB, PAIR, QFG><<<grid < slots ? grid : slots, NTHREADS, smem, st>>>(
       maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
   SC_CHECK_LAUNCH("band_attn_kernel");
   return SC_OK;
+}
+
+// SC_BAND_QFG=0 keeps the 2-CTA, Qf-staged form for 8 < w <= 16 (measurement A/B)
+static bool qfg_enabled() {
+  static int v = -1;
+  if (v < 0) v = getenv("SC_BAND_QFG") ? atoi(getenv("SC_BAND_QFG")) : 1;
+  return v != 0;
 }
 
 template <int GR>
@@ -1136,7 +1194,9 @@ static int launch_gr(int nbc, bool pair, const CUtensorMap* maps, const Params& 
     return p.w <= 4 ? launch_one<1, GR, 3, 1>(maps, p, grid, st) : launch_one<1, GR, 4, 1>(maps, p, grid, st);
   switch (nbc) {
     case 1: return p.w <= 4 ? launch_one<1, GR, 3>(maps, p, grid, st) : launch_one<1, GR>(maps, p, grid, st);
-    case 2: return launch_one<2, GR>(maps, p, grid, st);
+    case 2:
+      if (GR == 16 && p.w <= 16 && qfg_enabled()) return launch_one<2, 16, 4, 0, 1>(maps, p, grid, st);
+      return launch_one<2, GR>(maps, p, grid, st);
     case 3: return launch_one<3, GR>(maps, p, grid, st);
     case 4: return launch_one<4, GR>(maps, p, grid, st);
     case 5: return launch_one<5, GR>(maps, p, grid, st);
@@ -1211,6 +1271,7 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   p.link_cls = L.w[2][0] == SC_LINK_FULL; p.link_query = L.w[2][1] == SC_LINK_FULL;
   p.c2 = 1.4426950408889634f / a.scale;
   p.cu = a.cu; p.qlen = a.qlen; p.tile_base = seq_tile_base;
+  p.q = static_cast<const __nv_bfloat16*>(a.q); p.ld_q = a.ld; p.T = a.T;
   p.out = static_cast<__nv_bfloat16*>(a.out); p.ld_out = a.ld_out;
   p.partials = static_cast<float*>(ws);
   for (int gsrc = 0; gsrc < 2; ++gsrc) {
