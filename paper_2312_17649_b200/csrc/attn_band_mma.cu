@@ -430,8 +430,12 @@ __device__ __forceinline__ uint32_t movm_t(uint32_t x) {
 // the sparse pattern uses one.  P^T moves from the C layout of S^T to the B layout of the PV
 // product by movmatrix.  Record f: (m, l, -, -, acc[64]) -- m in natural logit units, l the sum of
 // exp(s - m) over the tile's keys, acc = sum exp(s - m) v (R/attention.py:416-473 split form).
-__device__ __forceinline__ uint32_t ldg_pair(const __nv_bfloat16* base, int64_t row, int T, int64_t ld, int col) {
-  return row < T ? __ldg(reinterpret_cast<const uint32_t*>(base + row * ld + col)) : 0u;
+// A bf16 pair (row, col..col+1) of one head's q for the QFG variants: zero past the token range and
+// past head_dim (32-dim heads ride in the zero-padded 64-dim layout of the staged rows).
+__device__ __forceinline__ uint32_t ldg_pair(const Params& p, int h, int64_t row, int col) {
+  return (row < p.T && col < p.dout)
+             ? __ldg(reinterpret_cast<const uint32_t*>(p.q + row * p.ld_q + (int64_t)h * p.dout + col))
+             : 0u;
 }
 
 template <int PAIR, int QFG = 0>
@@ -450,12 +454,11 @@ __device__ __forceinline__ void full_row_records(const Params& p, uint32_t qf, u
       // B fragments of full rows fb*8 .. fb*8+7 (Qf rows = B columns): k-steps 2i, 2i+1 per x4
       uint32_t qb[4][2];
       if constexpr (QFG) {  // B fragments straight from the rows' q (L2): rows qrow0 + fb*8 + g8
-        const __nv_bfloat16* qh = p.q + h * 64;
         const int64_t row = qrow0 + fb * 8 + g8;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          qb[ks][0] = ldg_pair(qh, row, p.T, p.ld_q, ks * 16 + 2 * t);
-          qb[ks][1] = ldg_pair(qh, row, p.T, p.ld_q, ks * 16 + 8 + 2 * t);
+          qb[ks][0] = ldg_pair(p, h, row, ks * 16 + 2 * t);
+          qb[ks][1] = ldg_pair(p, h, row, ks * 16 + 8 + 2 * t);
         }
       } else {
 #pragma unroll
@@ -917,14 +920,13 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC, QFG)) band_attn_kernel
           if (fc * 16 < G) {
             uint32_t qa[4][4];
             if constexpr (QFG) {  // A fragments of rows fc*16 + (gq, gq + 8) straight from their q (L2)
-              const __nv_bfloat16* qh = p.q + h * 64;
               const int64_t ra0 = g.start + fc * 16 + gq;
   #pragma unroll
               for (int ks = 0; ks < 4; ++ks) {
-                qa[ks][0] = ldg_pair(qh, ra0, p.T, p.ld_q, ks * 16 + 2 * tq);
-                qa[ks][1] = ldg_pair(qh, ra0 + 8, p.T, p.ld_q, ks * 16 + 2 * tq);
-                qa[ks][2] = ldg_pair(qh, ra0, p.T, p.ld_q, ks * 16 + 8 + 2 * tq);
-                qa[ks][3] = ldg_pair(qh, ra0 + 8, p.T, p.ld_q, ks * 16 + 8 + 2 * tq);
+                qa[ks][0] = ldg_pair(p, h, ra0, ks * 16 + 2 * tq);
+                qa[ks][1] = ldg_pair(p, h, ra0 + 8, ks * 16 + 2 * tq);
+                qa[ks][2] = ldg_pair(p, h, ra0, ks * 16 + 8 + 2 * tq);
+                qa[ks][3] = ldg_pair(p, h, ra0 + 8, ks * 16 + 8 + 2 * tq);
               }
             } else {
               load_q(qf_buf(s), fc * 16, LO, qa);

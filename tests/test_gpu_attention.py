@@ -440,3 +440,15 @@ def test_fast_path_never_uses_generic_for_envelope_shapes(P):
         for shapes in ([(62, 500), (3, 90)], [(10, 4086)]):
             for w in (4, 64):
                 _packed_vs_oracle(P, shapes, 2, d, "sparse", w, "exclude", "band" if w <= 40 else "tc")
+
+
+@pytest.mark.parametrize("d", [64, 32])
+@pytest.mark.parametrize("name,w,pad", [("sparse", 9, "exclude"), ("sparse", 16, "zero-logit"),
+                                        ("longformer", 12, "exclude"), ("longformer", 16, "zero-logit")])
+def test_band_three_cta_variant_vs_oracle(P, d, name, w, pad):
+    """8 < w <= 16 with query groups <= 15 rows: the band kernel variant that reads the cls / query rows'
+    q from L2 (no Qf box; full-row records and the first tile's head rows) and ends the band with a
+    16-key chunk; ragged sequences incl. a 1-token document and a short last sequence near the end of
+    the token range."""
+    shapes = [(10, 300), (1, 1), (7, 130), (14, 127), (10, 700), (3, 17), (2, 2)]
+    _packed_vs_oracle(P, shapes, 4, d, name, w, pad, "band")
