@@ -1017,33 +1017,41 @@ __global__ void __launch_bounds__(NTHREADS, min_ctas(NBC, QFG)) band_attn_kernel
 // kernel's last CTAs finish, and wait for the grid's records here.
 constexpr int MERGE_WARPS = 8;
 
+// WPI warps per (sequence, head, row) item, MERGE_WARPS / WPI items per CTA: 8 for long sequences
+// (65 records at 4k tokens), 1 for short ones (passages: 4 records -- one warp folds them all).
+template <int WPI>
 __global__ void __launch_bounds__(MERGE_WARPS * 32) merge_full_rows_kernel(Params p) {
+  constexpr int ITEMS = MERGE_WARPS / WPI;
   __shared__ float sacc[MERGE_WARPS][D];
   __shared__ float sml[MERGE_WARPS][2];
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t item = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = warp % WPI;
+  const int64_t item = (int64_t)blockIdx.x * ITEMS + warp / WPI;
   const int f = (int)(item % p.fmax);
   const int h = (int)((item / p.fmax) % p.H);
   const int j = (int)(item / ((int64_t)p.fmax * p.H));
-  if (j >= p.nseq) return;
-  const SeqGroups g = seq_groups(p.cu, p.qlen, j);
-  const int G = 1 + g.len[1];
-  if (f >= G || !p.hdoc[f == 0 ? 0 : 1]) return;
-  const int tb = __ldg(p.tile_base + j), te = __ldg(p.tile_base + j + 1);
-  const int nrec = te - tb + 1;
+  bool valid = j < p.nseq;
+  SeqGroups g{};
+  int nrec = 0;
+  const float *trec = nullptr, *grec = nullptr;
   const int64_t rstride = (int64_t)p.H * p.fmax * REC;
-  const float* trec = p.partials + (((int64_t)tb * p.H + h) * p.fmax + f) * REC;
-  const float* grec = p.partials + (((int64_t)(p.ntiles_max + j) * p.H + h) * p.fmax + f) * REC;
+  if (valid) {
+    g = seq_groups(p.cu, p.qlen, j);
+    valid = f < 1 + g.len[1] && p.hdoc[f == 0 ? 0 : 1];
+    const int tb = __ldg(p.tile_base + j), te = __ldg(p.tile_base + j + 1);
+    nrec = valid ? te - tb + 1 : 0;
+    trec = p.partials + (((int64_t)tb * p.H + h) * p.fmax + f) * REC;
+    grec = p.partials + (((int64_t)(p.ntiles_max + j) * p.H + h) * p.fmax + f) * REC;
+  }
   auto rec_of = [&](int r) { return r < nrec - 1 ? trec + r * rstride : grec; };
 
   float M = -INFINITY, l = 0.f, a0 = 0.f, a1 = 0.f;
   constexpr int U = 4;  // records in flight per warp
-  for (int base = warp; base < nrec; base += U * MERGE_WARPS) {
+  for (int base = sub; base < nrec; base += U * WPI) {
     float2 ml[U], v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int r = base + u * MERGE_WARPS;
+      const int r = base + u * WPI;
       if (r < nrec) {
         const float* rc = rec_of(r);
         ml[u] = __ldg(reinterpret_cast<const float2*>(rc));
@@ -1067,34 +1075,40 @@ __global__ void __launch_bounds__(MERGE_WARPS * 32) merge_full_rows_kernel(Param
       a1 = fmaf(b, v[u].y, a1);
     }
   }
-  sacc[warp][2 * lane] = a0;
-  sacc[warp][2 * lane + 1] = a1;
-  if (lane == 0) { sml[warp][0] = M; sml[warp][1] = l; }
-  __syncthreads();
-  if (warp != 0) return;
-  float Mt = -INFINITY;
+  if constexpr (WPI > 1) {  // fold the item's warps through shared memory (one item per CTA)
+    sacc[warp][2 * lane] = a0;
+    sacc[warp][2 * lane + 1] = a1;
+    if (lane == 0) { sml[warp][0] = M; sml[warp][1] = l; }
+    __syncthreads();
+    if (sub != 0) return;
+    float Mt = -INFINITY;
 #pragma unroll
-  for (int w = 0; w < MERGE_WARPS; ++w) Mt = fmaxf(Mt, sml[w][0]);
-  float lt = 0.f, o0 = 0.f, o1 = 0.f;
+    for (int w = 0; w < WPI; ++w) Mt = fmaxf(Mt, sml[warp + w][0]);
+    float lt = 0.f, o0 = 0.f, o1 = 0.f;
 #pragma unroll
-  for (int w = 0; w < MERGE_WARPS; ++w) {
-    if (!(sml[w][1] > 0.f)) continue;
-    const float sc = __expf(sml[w][0] - Mt);
-    lt = fmaf(sc, sml[w][1], lt);
-    o0 = fmaf(sc, sacc[w][2 * lane], o0);
-    o1 = fmaf(sc, sacc[w][2 * lane + 1], o1);
+    for (int w = 0; w < WPI; ++w) {
+      if (!(sml[warp + w][1] > 0.f)) continue;
+      const float sc = __expf(sml[warp + w][0] - Mt);
+      lt = fmaf(sc, sml[warp + w][1], lt);
+      o0 = fmaf(sc, sacc[warp + w][2 * lane], o0);
+      o1 = fmaf(sc, sacc[warp + w][2 * lane + 1], o1);
+    }
+    l = lt; a0 = o0; a1 = o1;
   }
-  const float inv = lt > 0.f ? 1.f / lt : 0.f;
+  if (!valid) return;
+  const float inv = l > 0.f ? 1.f / l : 0.f;
   if (2 * lane < p.dout) {
     __nv_bfloat16* dst = p.out + (int64_t)(g.start + f) * p.ld_out + h * p.dout + 2 * lane;
-    *reinterpret_cast<uint32_t*>(dst) = pack_bf16(o0 * inv, o1 * inv);
+    *reinterpret_cast<uint32_t*>(dst) = pack_bf16(a0 * inv, a1 * inv);
   }
 }
 
-// Programmatic-dependent launch of the merge (one CTA per (sequence, head, full row)).
-static int launch_merge(const Params& p, int64_t items, cudaStream_t st) {
+// Programmatic-dependent launch of the merge: 8 warps per item for long sequences, 1 for short ones
+// (average doc tiles per sequence <= 16: at most ~17 records).
+static int launch_merge(const Params& p, int64_t items, int64_t total_tokens, cudaStream_t st) {
+  const bool short_seqs = total_tokens <= (int64_t)p.nseq * 16 * BM;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)items);
+  cfg.gridDim = dim3((unsigned)(short_seqs ? (items + MERGE_WARPS - 1) / MERGE_WARPS : items));
   cfg.blockDim = dim3(MERGE_WARPS * 32);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
@@ -1103,7 +1117,8 @@ static int launch_merge(const Params& p, int64_t items, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, merge_full_rows_kernel, p);
+  if (short_seqs) cudaLaunchKernelEx(&cfg, merge_full_rows_kernel<1>, p);
+  else cudaLaunchKernelEx(&cfg, merge_full_rows_kernel<MERGE_WARPS>, p);
   SC_CHECK_LAUNCH("merge_full_rows_kernel");
   return SC_OK;
 }
@@ -1302,7 +1317,7 @@ int launch_attn_band(const AttnArgs& a, int dtype, const int32_t* seq_tile_base,
   Params pm = p;  // the merge walks the layout's heads
   pm.H = a.H;
   pm.dout = a.d;
-  return launch_merge(pm, (int64_t)a.nseq * a.H * fneed, st);
+  return launch_merge(pm, (int64_t)a.nseq * a.H * fneed, a.T, st);
 }
 
 int launch_head_merge(const AttnArgs& a, const int32_t* seq_tile_base, int tile_rows, int max_qgroup_len, void* ws,
@@ -1318,7 +1333,7 @@ int launch_head_merge(const AttnArgs& a, const int32_t* seq_tile_base, int tile_
   p.partials = static_cast<float*>(ws);
   p.ntiles_max = (int)((a.T + tile_rows - 1) / tile_rows + a.nseq);
   for (int gsrc = 0; gsrc < 2; ++gsrc) p.hdoc[gsrc] = L.w[gsrc][2] == SC_LINK_FULL;
-  return launch_merge(p, (int64_t)a.nseq * a.H * fneed, st);
+  return launch_merge(p, (int64_t)a.nseq * a.H * fneed, a.T, st);
 }
 
 }  // namespace sc
