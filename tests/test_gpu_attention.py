@@ -452,3 +452,27 @@ def test_band_three_cta_variant_vs_oracle(P, d, name, w, pad):
     the token range."""
     shapes = [(10, 300), (1, 1), (7, 130), (14, 127), (10, 700), (3, 17), (2, 2)]
     _packed_vs_oracle(P, shapes, 4, d, name, w, pad, "band")
+
+
+def _random_configs(n=64, seed=2312):
+    """Seeded random packed batches over the fast kernels' envelope (and past it): pattern, window,
+    padding, head_dim, heads, query / document lengths."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        name = ["sparse", "longformer", "full"][rng.integers(0, 3)]
+        w = math.inf if name == "full" else int(rng.choice([0, 1, 3, 4, 7, 8, 9, 13, 16, 17, 31, 40, 41, 64, 100, 300]))
+        pad = ["exclude", "zero-logit"][rng.integers(0, 2)]
+        d = int(rng.choice([32, 64]))
+        H = int(rng.integers(1, 5))
+        nseq = int(rng.integers(1, 6))
+        shapes = [(int(rng.integers(1, 31)), int(rng.integers(1, 400))) for _ in range(nseq)]
+        out.append(pytest.param(name, w, pad, d, H, shapes, id=f"r{i}-{name}-w{w}-{pad}-d{d}-H{H}"))
+    return out
+
+
+@pytest.mark.parametrize("name,w,pad,d,H,shapes", _random_configs())
+def test_random_packed_batches_auto_vs_oracle(P, name, w, pad, d, H, shapes):
+    """AUTO kernel choice (band / 3-CTA band / head pairs / tcgen05 / generic) on seeded random packed
+    batches vs the fp64 oracle, bf16 tolerance 2e-2."""
+    _packed_vs_oracle(P, shapes, H, d, name, w, pad, "auto", seed=len(shapes) * 131 + H)
