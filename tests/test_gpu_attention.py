@@ -379,12 +379,12 @@ def test_qds_full_size_bf16_tc_vs_fp32_generic(P):
     assert (got - ref).abs().max().item() < 2e-2
 
 
-def _packed_vs_oracle(P, shapes, H, d, name, w, pad, algo, tol=2e-2, seed=29):
+def _packed_vs_oracle(P, shapes, H, d, name, w, pad, algo, tol=2e-2, seed=29, dtype=torch.bfloat16):
     rng = np.random.default_rng(seed)
     seq = [m + n + 3 for m, n in shapes]
     lay = P.PackedLayout.from_lengths(seq, [m + 1 for m, _ in shapes], device="cuda")
     T = sum(seq)
-    x = torch.from_numpy(rng.standard_normal((T, 3 * H * d)).astype(np.float32)).cuda().to(torch.bfloat16)
+    x = torch.from_numpy(rng.standard_normal((T, 3 * H * d)).astype(np.float32)).cuda().to(dtype)
     pat = P.make_pattern(name, w)
     out = P.attend_packed(x[:, :H * d], x[:, H * d:2 * H * d], x[:, 2 * H * d:], lay, pat, H, padding=pad,
                           algo=algo).double().cpu().numpy()
@@ -476,3 +476,11 @@ def test_random_packed_batches_auto_vs_oracle(P, name, w, pad, d, H, shapes):
     """AUTO kernel choice (band / 3-CTA band / head pairs / tcgen05 / generic) on seeded random packed
     batches vs the fp64 oracle, bf16 tolerance 2e-2."""
     _packed_vs_oracle(P, shapes, H, d, name, w, pad, "auto", seed=len(shapes) * 131 + H)
+
+
+@pytest.mark.parametrize("name,w,pad,d,H,shapes", _random_configs(n=24, seed=1749))
+def test_random_packed_batches_fp32_vs_oracle(P, name, w, pad, d, H, shapes):
+    """The fp32 parity path (tiled fp32 band kernel on split-fp16 tensor cores where it applies, the
+    generic kernel elsewhere) on seeded random packed batches vs the fp64 oracle within 1e-4."""
+    _packed_vs_oracle(P, shapes, H, d, name, w, pad, "auto", tol=1e-4, seed=len(shapes) * 7 + H,
+                      dtype=torch.float32)
