@@ -222,3 +222,22 @@ def test_electra_passages_fp32_split_ranking_identical(P, g, mode):
     print(f"fp32 {mode} passages max |dscore| = {err:.3e}")
     assert err < 2e-6, err
     assert O.rank_order(sc) == O.rank_order(ref)
+
+
+@pytest.mark.parametrize("pattern,window", [("sparse", 4), ("longformer", 16), ("full", math.inf)])
+def test_fp32_f16x3_small_model_vs_oracle_and_sgemm(P, pattern, window):
+    """fp32_gemm="f16x3" at a non-ELECTRA shape whose projections all take the fused tcgen05 GEMMs
+    (h = 256, ff = 1024: QKV N = 768, Wo N = 256, W1 N = 1024, K = 256 -- sc_gemm_x3h /
+    sc_gemm_x3h_gelu_planes) against the fp64 oracle, and against the cuBLAS SGEMM path."""
+    cfg = dict(layers=2, embed_dim=256, heads=4, ff_dim=1024, max_positions=600, vocab_size=700,
+               pattern=pattern, window=window)
+    ids, spans = O.gen_random_ids(7, 12, 400, 5, cfg["vocab_size"])
+    ref = O.score(ids, spans, cfg, O.init_weights(cfg, 3), np.float64)
+    got = {}
+    for mode in ("f16x3", "sgemm"):
+        model = P.CrossEncoder(P.EncoderConfig(**cfg, precision="f32"), seed=3, fp32_gemm=mode)
+        got[mode] = model.score(ids, P.SubsequencePartition(*spans))
+    e_x3 = np.abs(got["f16x3"] - ref).max()
+    e_sg = np.abs(got["sgemm"] - ref).max()
+    print(f"{pattern}: f16x3 {e_x3:.3e}, sgemm {e_sg:.3e}")
+    assert e_x3 < 1e-5 and e_x3 <= 4 * e_sg + 1e-6
