@@ -306,3 +306,26 @@ def test_bench_reference_arm_line_matches_gpu_arm_config():
     args = types.SimpleNamespace(prune_last_layer=False, varlen=False)
     s = bench.QUERY_LEN + 164 + 3
     assert d["config"] == bench.bench_config(args, 1, 64, s, 164, True, 64 * s)
+
+
+def test_bench_reference_arm_under_torchrun_world2():
+    """The driver launches the reference arm like ours (torchrun, N ranks): rank 0 alone times and
+    prints one line with n_gpus N; the other ranks exit 0 without work."""
+    import json
+    import socket
+    import subprocess
+    import sys
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--impl",
+                          "reference", "--gpus", "2", "--steps", "1", "--warmup", "3", "--ref-budget", "1",
+                          "--doc-len", "164"], cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2"
